@@ -1,0 +1,135 @@
+"""Pin the CPU oracle (oracle/) against the reference's own outputs.
+
+Fixtures come from tests/golden/make_golden.py, which ran the reference
+(hetero-rt) in the dev container.  Bit-exact equality for trees, lists and
+float64 forces; these tests need no GPU.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import dm as odm
+from oracle import oracle as orc
+
+from conftest import GOLDEN
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode())
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, name + ".npz"))
+
+
+CASES = [("nbody2d_300", [0.0, 0.3, 0.7], 0.7), ("nbody3d_2048", [0.0, 0.7], 0.7),
+         ("plummer3d_4096", [0.7], 0.7)]
+
+
+def tag(th):
+    return f"theta{th:g}".replace(".", "p")
+
+
+@pytest.mark.parametrize("name,thetas,ftheta", CASES)
+def test_tree_lists_forces_bit_exact(name, thetas, ftheta):
+    g = load(name)
+    t = orc.build_bucket_tree(g["positions"], g["masses"], int(g["bucket_size"]), float(g["box"]))
+    for k in ("center", "half", "mass", "com", "first_child", "n_child", "buckets", "pidx"):
+        np.testing.assert_array_equal(getattr(t, k), g[f"tree_{k}"], err_msg=k)
+    pc = np.where(t.first_child < 0, t.pcount, 0)
+    np.testing.assert_array_equal(pc, g["tree_pcount"])
+    for th in thetas:
+        L = orc.build_interaction_lists(t, th)
+        for k in ("ptr", "ids", "kind", "item_count"):
+            np.testing.assert_array_equal(getattr(L, k), g[f"lists_{tag(th)}_{k}"], err_msg=f"{th} {k}")
+        if th == ftheta:
+            f = orc.eval_forces(t, L, g["positions"], g["masses"])
+            np.testing.assert_array_equal(f, g[f"forces_{tag(th)}"])
+
+
+def test_plummer16k_digests():
+    """Config 1 (Plummer 16K, theta 0.7): tree, lists, float64 forces equal the
+    reference's bit for bit (sha256 over the exact arrays)."""
+    from paper_2008_05712_b200 import generators as gen
+    d = json.load(open(os.path.join(GOLDEN, "digests.json")))["digests"]["plummer3d_16384"]
+    ps = gen.fp32_exact(gen.gen_plummer(16384, 42))
+    t = orc.build_bucket_tree(ps.positions, ps.masses, 8)
+    pc = np.where(t.first_child < 0, t.pcount, 0)
+    assert sha(t.center, t.half, t.mass, t.com, t.first_child, t.n_child, pc, t.buckets, t.pidx) == d["tree"]
+    L = orc.build_interaction_lists(t, 0.7)
+    assert sha(L.ptr, L.ids, L.kind, L.item_count) == d["lists_theta0p7"]
+    f = orc.eval_forces(t, L, ps.positions, ps.masses)
+    assert sha(f) == d["forces_theta0p7"]
+
+
+def test_kernels_golden():
+    g = load("kernels")
+    np.testing.assert_array_equal(orc.forces_from_points(g["ppos"], g["pmass"], g["spos"], g["smass"], 1.0, 1e-4),
+                                  g["ffp"])
+    np.testing.assert_array_equal(orc.forces_from_points(g["ppos"], g["pmass"], g["spos"], g["smass"], 1.0, 0.0),
+                                  g["ffp_eps0"])
+    fa, fb = orc.md_cross_forces(g["md_a"], g["md_b"], 1.0, 25.0)
+    np.testing.assert_array_equal(fa, g["md_fa"])
+    np.testing.assert_array_equal(fb, g["md_fb"])
+    np.testing.assert_array_equal(orc.md_self_forces(g["md_self_pos"], 1.0, 25.0), g["md_self_f"])
+    np.testing.assert_array_equal(orc.direct_forces(g["direct_pos"], g["direct_mass"], 1.0, 1e-4), g["direct_f"])
+    off = np.concatenate([[0], np.cumsum(g["runs_lens"])])
+    for i in range(len(g["runs_lens"])):
+        a = g["runs_in"][off[i]:off[i + 1]]
+        assert orc.count_address_runs(a) == g["runs_out"][i]
+        assert odm.count_runs(a.tolist()) == g["runs_out"][i]
+
+
+@pytest.mark.parametrize("tagname,periodic", [("wall", False), ("per", True)])
+def test_md2d_golden(tagname, periodic):
+    g = load("md2d")
+    f = orc.md2d_compute_forces(g[f"{tagname}_pos0"], g[f"{tagname}_patch0"], 10, 10, 1.0, 1.0, 25.0, periodic)
+    np.testing.assert_array_equal(f, g[f"{tagname}_f0"])
+    pos, vel, patch = g[f"{tagname}_pos0"], g[f"{tagname}_vel0"], g[f"{tagname}_patch0"]
+    for _ in range(3):
+        pos, vel, patch = orc.md2d_step(pos, vel, patch, 10, 10, 1.0, 1.0, 0.08, 25.0, periodic)
+    np.testing.assert_array_equal(pos, g[f"{tagname}_pos3"])
+    np.testing.assert_array_equal(vel, g[f"{tagname}_vel3"])
+    np.testing.assert_array_equal(patch, g[f"{tagname}_patch3"])
+
+
+def test_dm_plans_golden():
+    cases = json.load(open(os.path.join(GOLDEN, "dm_plans.json")))
+    for c in cases:
+        mem = odm.OracleDM(c["cap"], c["slot"], c["mode"])
+        for (members, now), want in zip(c["batches"], c["result"]):
+            try:
+                p = mem.plan(members, now)
+            except odm.OracleCapacityError:
+                assert not want["ok"], c["name"]
+                continue
+            assert want["ok"], c["name"]
+            assert p["to_transfer"] == want["to_transfer"], c["name"]
+            assert p["addresses"] == want["addresses"], c["name"]
+            assert p["bounds"] == want["bounds"]
+            assert p["total_bytes"] == want["total_bytes"]
+            assert p["indirection_bytes"] == want["indirection_bytes"]
+            assert odm.member_transactions(p) == want["transactions"]
+            if c["mode"] != "redundant":
+                assert sorted(mem.slot_of.items()) == [tuple(x) for x in want["table"]]
+            if c["release"]:
+                mem.release(members)
+
+
+def test_aggregator_golden():
+    g = json.load(open(os.path.join(GOLDEN, "aggregator.json")))
+    for e in g["emissions"]:
+        arr = [tuple(a) for a in e["arrivals"]]
+        got = odm.emissions(arr, e["max_size"], e["polls"])
+        assert [[t, list(ids)] for t, ids in got] == e["emissions"]
+    for p in g["partitions"]:
+        assert odm.partition(p["items"], p["share"], p["nearest"]) == p["cut"]
