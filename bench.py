@@ -1,0 +1,291 @@
+#!/usr/bin/env python
+"""bench.py -- G-Charm irregular force path on B200 (one JSON line on rank 0).
+
+Headline workload: BASELINE.json configs[2], clustered N-body, 1M particles,
+theta 0.7, bucket 8, eps 1e-4 (the 1-B200 N-body configuration).  A STEP is
+one pass of the hot path over the resident particle set: the device
+opening-angle walk (interaction lists, bit-exact float64 decisions) followed by
+the bucket force kernel.  ``value`` = interactions/s with the tree and
+particles already in HBM; ``e2e`` = the same metric through the C-ABI call a
+user makes (gc_bh_step: host buffers in, H2D, tree, walk, forces, D2H).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun: every rank evaluates its own independent 1M system
+(seed 42 + rank), so per-GPU work is fixed ("scaling": "weak"); there is no
+data-path collective, only a barrier and a MAX reduction of the step times.
+``--impl reference`` times the CPU restatement of the reference path
+(oracle/, float64, all host threads) on the same workload and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+THETA, BUCKET, EPS, N_PART = 0.7, 8, 1e-4, 1_000_000
+FLOPS_PER_INTERACTION = 20  # SURVEY.md §8d convention (body-body interaction)
+NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def workload(rank: int):
+    from paper_2008_05712_b200 import generators as gen
+    return gen.fp32_exact(gen.gen_particles(N_PART, 42 + rank, clustering=0.6, dim=3))
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def allmax(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [l for l in out.splitlines() if l.strip()]
+            except Exception:
+                pass
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(ps, steps=1):
+    """CPU restatement of the reference path (oracle/, float64) on all host
+    threads: tree + walk + eval_forces over the full workload."""
+    from oracle import oracle as orc
+    ts = []
+    inter = 0
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        t = orc.build_bucket_tree(ps.positions, ps.masses, BUCKET)
+        lists = orc.build_interaction_lists(t, THETA)
+        orc.eval_forces(t, lists, ps.positions, ps.masses, 1.0, EPS)
+        ts.append(time.perf_counter() - t0)
+        inter = int((t.pcount[t.buckets] * lists.item_count).sum())
+    return inter, ts, orc.num_threads()
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    ps = workload(0)
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up state beyond the first call below
+    inter, ts, cores = cpu_baseline(ps, steps=max(1, args.steps))
+    mean = statistics.mean(ts)
+    v = inter / mean
+    line = {
+        "impl": "reference", "metric": "BH interactions/s (clustered 1M, theta 0.7)", "value": v,
+        "unit": "interactions/s", "n_gpus": 1, "steps": len(ts), "warmup": args.warmup,
+        "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic gen_particles(1M, seed 42, clustering 0.6, dim 3), fp32-exact",
+        "config": {"workload": "configs[2] clustered N-body 1M, theta 0.7, bucket 8, eps 1e-4",
+                   "path": "oracle/ C restatement of build_bucket_tree + build_interaction_lists + eval_forces"},
+        "cpu_baseline": {"value": v, "unit": "interactions/s", "cores": cores, "kind": "port",
+                         "sample": "full workload per step (tree + walk + eval_forces)"},
+        "e2e": {"value": v, "unit": "interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import ctypes as C
+
+    import torch
+
+    from paper_2008_05712_b200 import _lib as L
+    from paper_2008_05712_b200 import nbody
+
+    torch.cuda.set_device(local)
+    ctx = L.context(local)
+    ext = torch.cuda.ExternalStream(ctx.stream)
+    ps = workload(rank)
+    tree = nbody.build_bucket_tree(ps, BUCKET)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        L.call("gc_bh_walk", tree.handle, THETA)
+        L.call("gc_bh_forces_async", tree.handle, 1.0, EPS)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    ctx.sync()
+    inter = nbody.interactions(tree)
+    # per-step launches of our kernels: walk count + walk write + force
+    launches_per_step = 3
+
+    step_ms, walk_ms, force_ms = [], [], []
+    tm = np.zeros(2)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)  # evict L2 (256 MiB write) before every timed step
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ext)
+            step()
+            e1.record(ext)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            L.call("gc_bh_timings", tree.handle, L.ptr(tm, L.f64p))
+            walk_ms.append(tm[0])
+            force_ms.append(tm[1])
+    torch.cuda.synchronize()
+    barrier(world)
+    total_ms = allmax(sum(step_ms), world)
+    ms = total_ms / args.steps
+    value = world * inter / (ms * 1e-3)
+    f_ms = statistics.mean(force_ms)
+    w_ms = statistics.mean(walk_ms)
+
+    # FP32 pipe peak measured on this GPU (FFMA chains)
+    pk, _ = np.zeros(1), np.zeros(1)
+    L.call("gc_measure_fp32_peak", ctx.handle, L.ptr(pk, L.f64p), L.ptr(_, L.f64p))
+    fp32_peak = float(pk[0])
+
+    # end to end through the C ABI, pinned host buffers, H2D + D2H inside
+    pos_h = torch.from_numpy(np.ascontiguousarray(ps.positions)).pin_memory()
+    m_h = torch.from_numpy(np.ascontiguousarray(ps.masses)).pin_memory()
+    out_h = torch.empty((ps.positions.shape[0], 3), dtype=torch.float64).pin_memory()
+    stepper = nbody.BHStep(BUCKET, THETA, 1.0, EPS)
+    pos_np, m_np, out_np = pos_h.numpy(), m_h.numpy(), out_h.numpy()
+    stepper(pos_np, m_np, 1.0, out_np)  # warm-up
+    e2e_s = []
+    io = np.zeros(2, np.int64)
+    for _ in range(max(1, min(args.steps, 5))):
+        barrier(world)
+        t0 = time.perf_counter()
+        stepper(pos_np, m_np, 1.0, out_np)
+        e2e_s.append(time.perf_counter() - t0)
+    L.call("gc_bh_io_bytes", stepper.handle, L.ptr(io, L.i64p), 0)
+    e2e_t = allmax(statistics.mean(e2e_s), world)
+    e2e_v = world * inter / e2e_t
+
+    if rank != 0:
+        return
+    line = {
+        "metric": "BH interactions/s (clustered 1M, theta 0.7)",
+        "value": value, "unit": "interactions/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp32 force math (fp64 walk decisions, fp64 accumulation)",
+        "data": "synthetic gen_particles(1M, seed 42+rank, clustering 0.6, dim 3), fp32-exact",
+        "config": {"workload": "configs[2] clustered N-body 1M, theta 0.7, bucket 8, eps 1e-4 (1 system per GPU)",
+                   "step": "device walk (union lists) + bucket force kernel; tree resident in HBM",
+                   "interactions_per_gpu": inter, "walk_ms": w_ms, "force_ms": f_ms,
+                   "l2": "flushed (256 MiB write) before every timed step"},
+        "roofline": {"bound": "fp32", "kernel": "force_group_kernel",
+                     "achieved": FLOPS_PER_INTERACTION * inter / (f_ms * 1e-3) / 1e12,
+                     "peak": fp32_peak, "peak_source": "measured FFMA-chain probe on this GPU (gc_measure_fp32_peak)",
+                     "nominal_peak": NOMINAL_FP32_TFLOPS, "unit": "TFLOP/s",
+                     "frac": FLOPS_PER_INTERACTION * inter / (f_ms * 1e-3) / 1e12 / fp32_peak,
+                     "traffic": None, "flops_per_interaction": FLOPS_PER_INTERACTION},
+        "e2e": {"value": e2e_v, "unit": "interactions/s", "h2d_bytes_per_step": int(io[0]),
+                "d2h_bytes_per_step": int(io[1]), "ms_per_step": e2e_t * 1e3,
+                "path": "gc_bh_step C ABI: pinned host positions/masses -> H2D -> host tree -> device walk -> forces -> D2H"},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        c_inter, c_ts, cores = cpu_baseline(ps, 1)
+        line["cpu_baseline"] = {"value": c_inter / c_ts[0], "unit": "interactions/s", "cores": cores,
+                                "kind": "port",
+                                "sample": "full configs[2] workload once (tree + walk + eval_forces, float64)"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,139 @@
+/*
+ * gcharm.h -- C ABI of libgcharm.so, the B200 (sm_100a) drop-in for the
+ * G-Charm irregular force path of hetero-rt (arXiv 2008.05712 reference).
+ *
+ * Plain C types only: pointers, sizes, doubles.  Every call returns a
+ * gc_status (0 = ok); gc_last_error() gives the message of the last failure on
+ * the calling thread.  Status codes map 1:1 onto the reference's exception
+ * classes (hr/errors.py:4-53):
+ *
+ *   GC_E_CAPACITY  -> CapacityError   (hr/errors.py:32)
+ *   GC_E_GROUPING  -> GroupingError   (hr/errors.py:24)
+ *   GC_E_CLOCK     -> ClockError      (hr/errors.py:20)
+ *   GC_E_KERNELFIT -> KernelFitError  (hr/errors.py:28)
+ *   GC_E_VALUE     -> ValueError      (e.g. bucket_size < 1, nbody.py:80)
+ *   GC_E_CUDA / GC_E_NOMEM -> HeteroRtError (hr/errors.py:4)
+ *
+ * Ownership: inputs are caller-owned and read only; outputs are
+ * caller-allocated.  Device state (trees, lists, slot pools, reuse tables)
+ * is owned by the handle that created it.  One host thread per handle; each
+ * context owns one CUDA stream.  Calls that take host buffers synchronise
+ * before returning; *_async calls only enqueue on the context stream.
+ */
+#ifndef GCHARM_H
+#define GCHARM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t gc_status;
+enum {
+    GC_OK = 0,
+    GC_E_VALUE = 1,
+    GC_E_CAPACITY = 2,
+    GC_E_GROUPING = 3,
+    GC_E_CLOCK = 4,
+    GC_E_KERNELFIT = 5,
+    GC_E_CUDA = 6,
+    GC_E_NOMEM = 7,
+    GC_E_STATE = 8
+};
+
+typedef struct gc_ctx gc_ctx;
+typedef struct gc_bh gc_bh;
+typedef struct gc_dm gc_dm;
+typedef struct gc_md gc_md;
+
+const char *gc_last_error(void);
+const char *gc_version(void);
+
+/* ---- context ------------------------------------------------------------ */
+gc_status gc_ctx_create(int device, gc_ctx **out);
+gc_status gc_ctx_destroy(gc_ctx *ctx);
+gc_status gc_ctx_sync(gc_ctx *ctx);
+/* the context's cudaStream_t, for event timing by the caller */
+void *gc_ctx_stream(gc_ctx *ctx);
+
+/* Device limits for the occupancy model (replaces DeviceSpec presets,
+ * hr/devicesim.py:19-27,63-78): out[0..5] = sm_count, max_threads_per_sm,
+ * max_blocks_per_sm, registers_per_sm, shared_mem_per_sm, clock_khz. */
+gc_status gc_device_spec(gc_ctx *ctx, int64_t out[6]);
+
+/* Kernel resources of a real kernel class (replaces KernelSpec presets,
+ * hr/devicesim.py:30-39,83-108): out[0..4] = threads_per_block,
+ * registers_per_thread, shared_mem_per_block, members_per_block,
+ * cuda_occupancy_blocks_per_sm.  kernel_class: "force", "md", "walk". */
+gc_status gc_kernel_spec(gc_ctx *ctx, const char *kernel_class, int64_t out[5]);
+
+/* FP32 FFMA throughput probe (roofline denominator): TFLOP/s and ms */
+gc_status gc_measure_fp32_peak(gc_ctx *ctx, double *tflops, double *ms);
+
+/* ---- hr/kernels.py entry points (host buffers, float64 in/out) ------------ */
+/* forces_from_points (hr/kernels.py:70-98) */
+gc_status gc_forces_from_points(gc_ctx *ctx, int64_t n, int64_t m, int32_t dim, const double *ppos,
+                                const double *pmass, const double *spos, const double *smass, double g,
+                                double eps, double *out);
+/* direct_forces (hr/kernels.py:40-63) */
+gc_status gc_direct_forces(gc_ctx *ctx, int64_t n, int32_t dim, const double *pos, const double *mass,
+                           double g, double eps, double *out);
+/* md_cross_forces (hr/kernels.py:105-135): fa (na x dim), fb (nb x dim) */
+gc_status gc_md_cross_forces(gc_ctx *ctx, int64_t na, int64_t nb, int32_t dim, const double *pa,
+                             const double *pb, double cutoff, double stiffness, double *fa, double *fb);
+/* md_self_forces (hr/kernels.py:138-161) */
+gc_status gc_md_self_forces(gc_ctx *ctx, int64_t n, int32_t dim, const double *p, double cutoff,
+                            double stiffness, double *out);
+/* count_address_runs (hr/kernels.py:213-216) */
+gc_status gc_count_address_runs(gc_ctx *ctx, const int64_t *addresses, int64_t n, int64_t group,
+                                int64_t *out);
+
+/* ---- Barnes-Hut bucket forces (hr/workloads/nbody.py) ---------------------- */
+gc_status gc_bh_create(gc_ctx *ctx, gc_bh **out);
+gc_status gc_bh_destroy(gc_bh *bh);
+/* Particles (host, float64, float32-representable) + tree build.
+ * Restates build_bucket_tree (nbody.py:78-135): level-order node ids, DFS
+ * bucket order, float64 mass/COM with the reference's rounding sequence. */
+gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *pos, const double *mass,
+                              double box, int64_t bucket_size);
+/* Sizes: out[0..3] = n_nodes, n_buckets, list entries, node entries */
+gc_status gc_bh_sizes(gc_bh *bh, int64_t out[4]);
+/* Tree arrays (host, caller-allocated by gc_bh_sizes): any pointer may be NULL */
+gc_status gc_bh_get_tree(gc_bh *bh, double *center, double *half, double *mass, double *com,
+                         int64_t *first_child, int32_t *n_child, int64_t *pcount, int64_t *buckets,
+                         int64_t *pidx);
+/* Device opening-angle walk (build_interaction_lists, nbody.py:160-199) with
+ * bit-exact float64 decisions; lists stay in HBM. */
+gc_status gc_bh_walk(gc_bh *bh, double theta);
+/* Lists to host in walk order (CSR over buckets in DFS order):
+ * kind 0 = node_interactions, 1 = particle_interactions. */
+gc_status gc_bh_get_lists(gc_bh *bh, int64_t *ptr, int64_t *ids, int8_t *kind, int64_t *item_count);
+/* Lists from the host runtime (the drop-in path when the walk ran elsewhere) */
+gc_status gc_bh_set_lists(gc_bh *bh, int64_t n_buckets, const int64_t *ptr, const int64_t *ids,
+                          const int8_t *kind);
+/* eval_forces (nbody.py:216-250): float64 out (n x dim), original particle order */
+gc_status gc_bh_forces(gc_bh *bh, double g, double eps, double *out);
+/* Forces plus per-particle potential energy -G m_i sum_j m_j / sqrt(r^2 + eps^2)
+ * over the same interaction lists (pot: n float64).  No reference counterpart
+ * (restated next to forces_from_points). */
+gc_status gc_bh_forces_potential(gc_bh *bh, double g, double eps, double *out, double *pot);
+/* Enqueue only (results stay on device); for device-resident timing */
+gc_status gc_bh_forces_async(gc_bh *bh, double g, double eps);
+/* Sum over buckets of n_b * item_count_b (the interaction count) */
+gc_status gc_bh_interactions(gc_bh *bh, int64_t *out);
+/* Device time (ms, CUDA events on the context stream) of the last walk
+ * (out[0]) and the last force launch (out[1]). */
+gc_status gc_bh_timings(gc_bh *bh, double out[2]);
+/* Host<->device bytes moved since the last reset (out[0] = H2D, out[1] = D2H);
+ * gc_bh_step resets at entry, so after it these are that step's bytes. */
+gc_status gc_bh_io_bytes(gc_bh *bh, int64_t out[2], int32_t reset);
+/* End-to-end step from host buffers: H2D particles, tree, device walk,
+ * forces, D2H forces (n x dim float64). */
+gc_status gc_bh_step(gc_bh *bh, int64_t n, int32_t dim, const double *pos, const double *mass, double box,
+                     int64_t bucket_size, double theta, double g, double eps, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GCHARM_H */

@@ -1,0 +1,149 @@
+"""ctypes binding of libgcharm.so (include/gcharm.h).
+
+There is no fallback: if the CUDA library is missing or no sm_100 device is
+visible, every entry point raises.  Build with ``python -c "import
+__graft_entry__ as g; g.build()"`` (or ``make -C paper_2008_05712_b200/csrc``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from .errors import CudaError, raise_for_status
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgcharm.so")
+
+i64p = C.POINTER(C.c_int64)
+i32p = C.POINTER(C.c_int32)
+i8p = C.POINTER(C.c_int8)
+f64p = C.POINTER(C.c_double)
+vp = C.c_void_p
+
+# name -> (argtypes); every function returns gc_status (int32) unless listed in _RESTYPE
+SIGNATURES = {
+    "gc_ctx_create": [C.c_int, C.POINTER(vp)],
+    "gc_ctx_destroy": [vp],
+    "gc_ctx_sync": [vp],
+    "gc_ctx_stream": [vp],
+    "gc_device_spec": [vp, i64p],
+    "gc_kernel_spec": [vp, C.c_char_p, i64p],
+    "gc_forces_from_points": [vp, C.c_int64, C.c_int64, C.c_int32, f64p, f64p, f64p, f64p, C.c_double,
+                              C.c_double, f64p],
+    "gc_direct_forces": [vp, C.c_int64, C.c_int32, f64p, f64p, C.c_double, C.c_double, f64p],
+    "gc_md_cross_forces": [vp, C.c_int64, C.c_int64, C.c_int32, f64p, f64p, C.c_double, C.c_double, f64p, f64p],
+    "gc_md_self_forces": [vp, C.c_int64, C.c_int32, f64p, C.c_double, C.c_double, f64p],
+    "gc_count_address_runs": [vp, i64p, C.c_int64, C.c_int64, i64p],
+    "gc_bh_create": [vp, C.POINTER(vp)],
+    "gc_bh_destroy": [vp],
+    "gc_bh_set_particles": [vp, C.c_int64, C.c_int32, f64p, f64p, C.c_double, C.c_int64],
+    "gc_bh_sizes": [vp, i64p],
+    "gc_bh_get_tree": [vp, f64p, f64p, f64p, f64p, i64p, i32p, i64p, i64p, i64p],
+    "gc_bh_walk": [vp, C.c_double],
+    "gc_bh_get_lists": [vp, i64p, i64p, i8p, i64p],
+    "gc_bh_set_lists": [vp, C.c_int64, i64p, i64p, i8p],
+    "gc_bh_forces": [vp, C.c_double, C.c_double, f64p],
+    "gc_bh_forces_async": [vp, C.c_double, C.c_double],
+    "gc_bh_forces_potential": [vp, C.c_double, C.c_double, f64p, f64p],
+    "gc_bh_interactions": [vp, i64p],
+    "gc_bh_timings": [vp, f64p],
+    "gc_bh_io_bytes": [vp, i64p, C.c_int32],
+    "gc_measure_fp32_peak": [vp, f64p, f64p],
+    "gc_bh_step": [vp, C.c_int64, C.c_int32, f64p, f64p, C.c_double, C.c_int64, C.c_double, C.c_double,
+                   C.c_double, f64p],
+}
+_RESTYPE = {"gc_ctx_stream": vp, "gc_last_error": C.c_char_p, "gc_version": C.c_char_p}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load():
+    """Load libgcharm.so (raises if it was not built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise CudaError(f"{LIB_PATH} is missing: build the CUDA extension first (__graft_entry__.build())")
+            L = C.CDLL(LIB_PATH)
+            for name, args in SIGNATURES.items():
+                fn = getattr(L, name)
+                fn.argtypes = args
+                fn.restype = _RESTYPE.get(name, C.c_int32)
+            for name, rt in _RESTYPE.items():
+                getattr(L, name).restype = rt
+            L.gc_last_error.argtypes = []
+            L.gc_version.argtypes = []
+            _lib = L
+    return _lib
+
+
+def call(name, *args):
+    L = load()
+    st = getattr(L, name)(*args)
+    if st:
+        raise_for_status(st, f"{name}: {L.gc_last_error().decode(errors='replace')}")
+
+
+class Context:
+    """One CUDA device + stream owned by libgcharm (gc_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.handle = vp()
+        call("gc_ctx_create", int(device), C.byref(self.handle))
+        self.device = device
+
+    @property
+    def stream(self) -> int:
+        return load().gc_ctx_stream(self.handle)
+
+    def sync(self):
+        call("gc_ctx_sync", self.handle)
+
+    def device_spec(self):
+        out = np.zeros(6, np.int64)
+        call("gc_device_spec", self.handle, ptr(out, i64p))
+        return out
+
+    def kernel_spec(self, kernel_class: str):
+        out = np.zeros(5, np.int64)
+        call("gc_kernel_spec", self.handle, kernel_class.encode(), ptr(out, i64p))
+        return out
+
+    def __del__(self):
+        try:
+            if self.handle:
+                load().gc_ctx_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_ctx: dict[int, Context] = {}
+
+
+def context(device: int | None = None) -> Context:
+    if device is None:
+        device = int(os.environ.get("GCHARM_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    with _lock:
+        c = _ctx.get(device)
+    if c is None:
+        c = Context(device)
+        with _lock:
+            _ctx[device] = c
+    return c
+
+
+def ptr(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+def f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def i64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int64)

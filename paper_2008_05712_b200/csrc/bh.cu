@@ -1,0 +1,585 @@
+// bh.cu -- host side of the Barnes-Hut bucket force path + its C ABI.
+// Device code and design notes: bh_kernels.cuh.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "bh_kernels.cuh"
+#include "bh_tree.h"
+#include "common.cuh"
+
+using namespace gc;
+
+struct gc_bh {
+    gc_ctx *ctx = nullptr;
+    HostTree tree;
+    bool have_tree = false;
+    std::vector<WalkGroup> h_wg;
+    std::vector<ForceGroup> h_fg;
+    // device tree
+    DBuf<float4> d_recs;  // walk records: float32 com + packed links
+    DBuf<double4> d_com64;  // float64 com (exact opening test)
+    DBuf<double4> d_bgeo;  // per bucket (DFS index): center.xyz, half
+    DBuf<float4> d_bgeo32;  // float32 copy (w < 0: not exact in float32)
+    DBuf<float4> d_parts;  // DFS-sorted particles (x, y, z, m) fp32
+    DBuf<int> d_porder;  // original id of each sorted particle
+    DBuf<int> d_part_bucket;  // DFS bucket index of each sorted particle
+    DBuf<float4> d_rec_hi, d_rec_lo;  // force records: com hi (fp32) + mass, com lo
+    DBuf<int2> d_prange;  // per node: (first sorted particle, count) for buckets
+    DBuf<int2> d_brange;  // per bucket (DFS index): (first sorted particle, count)
+    DBuf<int> d_bucket_ids;  // identity member list for the member kernel
+    DBuf<WalkGroup> d_wg;
+    DBuf<ForceGroup> d_fg;
+    float walk_dd2 = 0.f, walk_dd3 = 0.f;
+    DBuf<float2> d_tt;
+    // union lists (device walk)
+    bool have_union = false;
+    bool cap_valid = false;
+    double cap_theta = -1.0;
+    DBuf<int64_t> d_gcount, d_gbase, d_gcap, d_bstat;
+    DBuf<int> d_uid;
+    DBuf<uint2> d_umask;
+    int64_t n_union = 0;
+    // per-bucket CSR (host-supplied lists)
+    bool have_member_lists = false;
+    DBuf<int64_t> d_nptr, d_pptr;
+    DBuf<int> d_naddr, d_paddr;
+    // outputs
+    DBuf<double> d_out, d_pot;
+    std::vector<int64_t> h_item_count;
+    int64_t n_list_entries = 0;
+    DBuf<int64_t> d_bptr;
+    DBuf<int> d_list_ids;
+    DBuf<int8_t> d_list_kind;
+    DBuf<int> d_flag;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t h2d = 0, d2h = 0;  // bytes moved host<->device since the last reset
+    ~gc_bh()
+    {
+        for (auto &e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+namespace {
+
+void upload_tree(gc_bh *bh)
+{
+    cudaStream_t s = bh->ctx->stream;
+    const HostTree &t = bh->tree;
+    const int64_t nn = t.n_nodes(), nb = (int64_t)t.buckets.size();
+    GC_REQUIRE(t.n < (1ll << 31) && nn < (1ll << NODE_BITS), GC_E_VALUE, "tree too large for the packed node ids");
+    std::vector<float4> recs(nn), hi(nn), lo(nn);
+    std::vector<double4> c64(nn);
+    std::vector<int2> pr(nn);
+    std::vector<int> level(nn, 0);
+    for (int64_t i = 0; i < nn; ++i)
+        for (int c = 0; c < t.n_child[i]; ++c) level[t.first_child[i] + c] = level[i] + 1;
+    double cmax = 0.0;
+    for (int64_t i = 0; i < nn; ++i) {
+        GC_REQUIRE(level[i] < MAX_LEVELS, GC_E_VALUE, "tree deeper than 63 levels");
+        GC_REQUIRE(2.0 * t.half[i] == std::ldexp(t.box, -level[i]), GC_E_VALUE, "node size not dyadic in box");
+        float h3[3], l3[3];
+        for (int k = 0; k < 3; ++k) {
+            h3[k] = (float)t.com[3 * i + k];
+            l3[k] = (float)(t.com[3 * i + k] - (double)h3[k]);
+            cmax = std::max(cmax, std::fabs(t.com[3 * i + k]));
+            cmax = std::max(cmax, std::fabs(t.center[3 * i + k]) + t.half[i]);
+        }
+        int word;
+        if (t.first_child[i] < 0) {
+            GC_REQUIRE(t.pcount[i] < (1 << 30), GC_E_VALUE, "bucket too large");
+            word = -(int)t.pcount[i];
+        } else {
+            word = (int)(t.first_child[i] << 3) | (t.n_child[i] - 1);
+        }
+        float wf;
+        std::memcpy(&wf, &word, 4);
+        recs[i] = make_float4(h3[0], h3[1], h3[2], wf);
+        c64[i] = make_double4(t.com[3 * i], t.com[3 * i + 1], t.com[3 * i + 2], 0.0);
+        hi[i] = make_float4(h3[0], h3[1], h3[2], (float)t.node_mass[i]);
+        lo[i] = make_float4(l3[0], l3[1], l3[2], 0.f);
+        pr[i] = make_int2((int)t.pstart[i], (int)t.pcount[i]);
+    }
+    // |v32 - v64| <= delta for every opening-test component (walk_group_kernel):
+    // com rounding + two float32 subtractions, each <= 2^-24 * |operand|
+    const double delta = 1.25 * 6.0 * std::ldexp(1.0, -24) * std::max(cmax, 1e-30);
+    bh->walk_dd2 = (float)(2.0 * delta * (1.0 + 1e-6));
+    bh->walk_dd3 = (float)(3.0 * delta * delta * (1.0 + 1e-6));
+
+    std::vector<double4> bg(nb);
+    std::vector<float4> bg32(nb);
+    std::vector<int2> br(nb);
+    std::vector<int> bids(nb);
+    std::vector<int> pb(t.n);
+    for (int64_t b = 0; b < nb; ++b) {
+        const int64_t id = t.buckets[b];
+        bg[b] = make_double4(t.center[3 * id], t.center[3 * id + 1], t.center[3 * id + 2], t.half[id]);
+        const float f0 = (float)bg[b].x, f1 = (float)bg[b].y, f2 = (float)bg[b].z, fh = (float)bg[b].w;
+        const bool ex = f0 == bg[b].x && f1 == bg[b].y && f2 == bg[b].z && fh == bg[b].w;
+        bg32[b] = make_float4(f0, f1, f2, ex ? fh : -1.f);
+        br[b] = make_int2((int)t.pstart[id], (int)t.pcount[id]);
+        bids[b] = (int)b;
+        for (int64_t k = 0; k < t.pcount[id]; ++k) pb[t.pstart[id] + k] = (int)b;
+    }
+    // walk groups: 32 consecutive buckets; force groups: <= 32 targets of
+    // consecutive buckets inside one walk group
+    bh->h_wg.clear();
+    bh->h_fg.clear();
+    for (int64_t b0 = 0; b0 < nb; b0 += 32) {
+        WalkGroup wg;
+        wg.bfirst = (int)b0;
+        wg.nbucket = (int)std::min<int64_t>(32, nb - b0);
+        const int wi = (int)bh->h_wg.size();
+        bh->h_wg.push_back(wg);
+        for (int64_t b = b0; b < b0 + wg.nbucket;) {
+            ForceGroup fg;
+            fg.pstart = (int)t.pstart[t.buckets[b]];
+            fg.wg = wi;
+            fg.boff = (int)(b - b0);
+            int tg = 0;
+            while (b < b0 + wg.nbucket && tg + t.pcount[t.buckets[b]] <= 32) {
+                tg += (int)t.pcount[t.buckets[b]];
+                ++b;
+            }
+            GC_REQUIRE(tg > 0, GC_E_VALUE, "bucket with more than 32 particles (coincident points) on the group path");
+            fg.ntarget = tg;
+            bh->h_fg.push_back(fg);
+        }
+    }
+    bh->d_recs.upload(recs.data(), nn, s);
+    bh->d_com64.upload(c64.data(), nn, s);
+    bh->d_rec_hi.upload(hi.data(), nn, s);
+    bh->d_rec_lo.upload(lo.data(), nn, s);
+    bh->d_prange.upload(pr.data(), nn, s);
+    bh->d_bgeo.upload(bg.data(), nb, s);
+    bh->d_bgeo32.upload(bg32.data(), nb, s);
+    bh->d_brange.upload(br.data(), nb, s);
+    bh->d_bucket_ids.upload(bids.data(), nb, s);
+    bh->d_part_bucket.upload(pb.data(), t.n, s);
+    bh->d_wg.upload(bh->h_wg.data(), bh->h_wg.size(), s);
+    bh->d_fg.upload(bh->h_fg.data(), bh->h_fg.size(), s);
+    bh->h2d += nn * (int64_t)(3 * sizeof(float4) + sizeof(double4) + sizeof(int2)) +
+               nb * (int64_t)(sizeof(double4) + sizeof(float4) + sizeof(int2) + sizeof(int)) +
+               t.n * (int64_t)sizeof(int) + (int64_t)bh->h_wg.size() * (int64_t)sizeof(WalkGroup) +
+               (int64_t)bh->h_fg.size() * (int64_t)sizeof(ForceGroup);
+    GC_CUDA(cudaStreamSynchronize(s));
+}
+
+void upload_particles(gc_bh *bh, const double *pos, const double *mass)
+{
+    const HostTree &t = bh->tree;
+    std::vector<float4> parts(t.n);
+    std::vector<int> ord(t.n);
+    for (int64_t i = 0; i < t.n; ++i) {
+        const int64_t p = t.order[i];
+        float c[3] = {0.f, 0.f, 0.f};
+        for (int k = 0; k < t.dim; ++k) c[k] = (float)pos[p * t.dim + k];
+        parts[i] = make_float4(c[0], c[1], c[2], (float)mass[p]);
+        ord[i] = (int)p;
+    }
+    bh->d_parts.upload(parts.data(), t.n, bh->ctx->stream);
+    bh->d_porder.upload(ord.data(), t.n, bh->ctx->stream);
+    bh->h2d += t.n * (int64_t)(sizeof(float4) + sizeof(int));
+    GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
+}
+
+template <class T>
+void exclusive_scan(gc_ctx *ctx, const T *in, T *out, int64_t n)
+{
+    size_t bytes = 0;
+    GC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, ctx->stream));
+    ctx->scratch.resize(bytes);
+    GC_CUDA(cub::DeviceScan::ExclusiveSum(ctx->scratch.p, bytes, in, out, n, ctx->stream));
+}
+
+void run_walk(gc_bh *bh, double theta)
+{
+    GC_REQUIRE(theta >= 0.0, GC_E_VALUE, "theta must be >= 0");
+    GC_REQUIRE(bh->have_tree, GC_E_STATE, "no particles set");
+    gc_ctx *ctx = bh->ctx;
+    cudaStream_t s = ctx->stream;
+    const int ng = (int)bh->h_wg.size();
+    const int64_t nb = (int64_t)bh->tree.buckets.size();
+    bh->d_gcount.resize(ng);
+    bh->d_gbase.resize(ng + 1);
+    bh->d_gcap.resize(ng + 1);
+    bh->d_bstat.resize(2 * nb);
+    bh->d_flag.resize(1);
+    const unsigned grid = grid_for(ng, WARPS_PER_BLOCK);
+    const double th2 = theta * theta;
+    const double root = 2.0 * bh->tree.half[0];
+    // per-level float32 thresholds on s = d^2: accept iff s > size^2 / theta^2
+    std::vector<float2> tt(MAX_LEVELS);
+    for (int l = 0; l < MAX_LEVELS; ++l) {
+        const double size = std::ldexp(root, -l);
+        const double T = theta > 0.0 ? size * size / th2 : HUGE_VAL;
+        const float a = (float)(T * (1.0 + std::ldexp(1.0, -22)));
+        const float r = (float)(T * (1.0 - std::ldexp(1.0, -22)));
+        tt[l].x = std::nextafter(a, HUGE_VALF);
+        tt[l].y = std::isinf(r) ? r : std::nextafter(r, 0.f);
+    }
+    bh->d_tt.upload(tt.data(), MAX_LEVELS, s);
+    WalkParams P;
+    P.theta = theta;
+    P.theta2 = th2;
+    P.root_size = root;
+    P.dd2 = bh->walk_dd2;
+    P.dd3 = bh->walk_dd3;
+    P.tt = bh->d_tt.p;
+    GC_CUDA(cudaEventRecord(bh->ev[0], s));
+    bh->d_flag.zero(s);
+    // capacities: the previous walk's counts on this tree plus slack, else a counting pass
+    if (!bh->cap_valid || bh->cap_theta != theta) {
+        walk_group_kernel<false, true><<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(
+            ng, bh->d_wg.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p, bh->d_bgeo32.p, P, nullptr, nullptr, nullptr,
+            nullptr, bh->d_gcount.p, bh->d_bstat.p, bh->d_flag.p);
+        check_launch("walk_group_kernel<count>");
+        GC_CUDA(cudaMemcpyAsync(bh->d_gcap.p, bh->d_gcount.p, sizeof(int64_t) * ng, cudaMemcpyDeviceToDevice, s));
+        bh->cap_valid = false;
+    }
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        GC_CUDA(cudaMemsetAsync(bh->d_gcap.p + ng, 0, sizeof(int64_t), s));
+        exclusive_scan(ctx, bh->d_gcap.p, bh->d_gbase.p, (int64_t)ng + 1);
+        int64_t total = 0;
+        GC_CUDA(cudaMemcpyAsync(&total, bh->d_gbase.p + ng, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        GC_CUDA(cudaStreamSynchronize(s));
+        bh->d_uid.resize(total);
+        bh->d_umask.resize(total);
+        walk_group_kernel<true, true><<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(
+            ng, bh->d_wg.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p, bh->d_bgeo32.p, P, bh->d_gbase.p,
+            bh->d_gcap.p, bh->d_uid.p, bh->d_umask.p, bh->d_gcount.p, bh->d_bstat.p, bh->d_flag.p);
+        check_launch("walk_group_kernel<write>");
+        int flag = 0;
+        bh->d_flag.download(&flag, 1, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        GC_REQUIRE(!(flag & 1), GC_E_VALUE, "tree deeper than the walk stack (box too large for half_size >= 1e-9)");
+        if (!(flag & 2)) break;
+        // capacity overflow (lists grew): exact counts from this pass, retry once
+        GC_REQUIRE(attempt == 0, GC_E_STATE, "walk capacity overflow after recount");
+        GC_CUDA(cudaMemcpyAsync(bh->d_gcap.p, bh->d_gcount.p, sizeof(int64_t) * ng, cudaMemcpyDeviceToDevice, s));
+        bh->d_flag.zero(s);
+        bh->cap_valid = false;
+    }
+    GC_CUDA(cudaEventRecord(bh->ev[1], s));
+    std::vector<int64_t> st(2 * nb);
+    bh->d_bstat.download(st.data(), 2 * nb, s);
+    GC_CUDA(cudaStreamSynchronize(s));
+    bh->d2h += 2 * nb * (int64_t)sizeof(int64_t) + 2 * (int64_t)sizeof(int64_t);
+    bh->h_item_count.resize(nb);
+    int64_t ent = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        ent += st[2 * b];
+        bh->h_item_count[b] = st[2 * b + 1];
+    }
+    bh->n_list_entries = ent;
+    bh->have_union = true;
+    bh->have_member_lists = false;
+    // next walk on this tree: reuse the counts with 1/8 slack in a single pass
+    if (!bh->cap_valid) {
+        std::vector<int64_t> cnt(ng);
+        bh->d_gcount.download(cnt.data(), ng, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        int64_t tot = 0;
+        for (auto &c : cnt) {
+            tot += c;
+            c = c + c / 8 + 16;
+        }
+        bh->n_union = tot;
+        bh->d_gcap.upload(cnt.data(), ng, s);
+        bh->cap_valid = true;
+        bh->cap_theta = theta;
+    }
+}
+
+void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
+{
+    gc_ctx *ctx = bh->ctx;
+    cudaStream_t s = ctx->stream;
+    const HostTree &t = bh->tree;
+    bh->d_out.resize(t.n * t.dim);
+    if (pot) bh->d_pot.resize(t.n);
+    const float eps2 = (float)(eps * eps);
+    const bool eps0 = eps2 == 0.f;
+    GC_CUDA(cudaEventRecord(bh->ev[2], s));
+    if (bh->have_union) {
+        const int nfg = (int)bh->h_fg.size();
+        const unsigned grid = grid_for(nfg, WARPS_PER_BLOCK);
+        auto k = eps0 ? (pot ? force_group_kernel<true, true> : force_group_kernel<true, false>)
+                      : (pot ? force_group_kernel<false, true> : force_group_kernel<false, false>);
+        k<<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(nfg, bh->d_fg.p, bh->d_gbase.p, bh->d_gcount.p, bh->d_uid.p,
+                                                bh->d_umask.p, bh->d_parts.p, bh->d_part_bucket.p, bh->d_porder.p,
+                                                bh->d_wg.p, bh->d_rec_hi.p, bh->d_rec_lo.p, bh->d_prange.p, eps2, g,
+                                                t.dim, bh->d_out.p, bh->d_pot.p);
+        check_launch("force_group_kernel");
+    } else if (bh->have_member_lists) {
+        GC_REQUIRE(!pot, GC_E_STATE, "potentials need device lists (gc_bh_walk)");
+        const int nb = (int)t.buckets.size();
+        const unsigned grid = grid_for(nb, WARPS_PER_BLOCK);
+        auto k = eps0 ? force_member_kernel<true> : force_member_kernel<false>;
+        k<<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(nb, bh->d_bucket_ids.p, bh->d_brange.p, bh->d_nptr.p,
+                                                bh->d_naddr.p, bh->d_pptr.p, bh->d_paddr.p, bh->d_parts.p,
+                                                bh->d_porder.p, bh->d_rec_hi.p, bh->d_rec_lo.p, bh->d_prange.p,
+                                                bh->d_parts.p, eps2, g, t.dim, bh->d_out.p);
+        check_launch("force_member_kernel");
+    } else {
+        throw Error{GC_E_STATE, "no interaction lists (call gc_bh_walk or gc_bh_set_lists)"};
+    }
+    GC_CUDA(cudaEventRecord(bh->ev[3], s));
+}
+
+}  // namespace
+
+extern "C" {
+
+gc_status gc_bh_create(gc_ctx *ctx, gc_bh **out)
+{
+    return guard([&] {
+        GC_REQUIRE(ctx && out, GC_E_VALUE, "null argument");
+        gc_bh *bh = new gc_bh();
+        bh->ctx = ctx;
+        for (auto &e : bh->ev) GC_CUDA(cudaEventCreate(&e));
+        *out = bh;
+    });
+}
+
+gc_status gc_bh_destroy(gc_bh *bh)
+{
+    return guard([&] { delete bh; });
+}
+
+gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *pos, const double *mass, double box,
+                              int64_t bucket_size)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && pos && mass, GC_E_VALUE, "null argument");
+        GC_REQUIRE(n >= 1, GC_E_VALUE, "need at least one particle");
+        GC_REQUIRE(bucket_size >= 1, GC_E_VALUE, "bucket_size must be >= 1");
+        GC_REQUIRE(bucket_size <= 32, GC_E_VALUE, "bucket_size must be <= 32 on the B200 path");
+        GC_REQUIRE(dim >= 1 && dim <= 3, GC_E_VALUE, "dim must be 1..3");
+        bh->tree.build(n, dim, pos, mass, box, bucket_size);
+        bh->have_tree = true;
+        bh->have_union = bh->have_member_lists = false;
+        bh->cap_valid = false;
+        upload_tree(bh);
+        upload_particles(bh, pos, mass);
+    });
+}
+
+gc_status gc_bh_sizes(gc_bh *bh, int64_t out[4])
+{
+    return guard([&] {
+        GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
+        out[0] = bh->tree.n_nodes();
+        out[1] = (int64_t)bh->tree.buckets.size();
+        out[2] = bh->n_list_entries;
+        out[3] = bh->n_union;
+    });
+}
+
+gc_status gc_bh_get_tree(gc_bh *bh, double *center, double *half, double *mass, double *com, int64_t *first_child,
+                         int32_t *n_child, int64_t *pcount, int64_t *buckets, int64_t *pidx)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
+        const HostTree &t = bh->tree;
+        const int64_t nn = t.n_nodes();
+        const int d = t.dim;
+        for (int64_t i = 0; i < nn; ++i) {
+            for (int k = 0; k < d; ++k) {
+                if (center) center[i * d + k] = t.center[3 * i + k];
+                if (com) com[i * d + k] = t.com[3 * i + k];
+            }
+            if (half) half[i] = t.half[i];
+            if (mass) mass[i] = t.node_mass[i];
+            if (first_child) first_child[i] = t.first_child[i];
+            if (n_child) n_child[i] = t.n_child[i];
+            if (pcount) pcount[i] = t.pcount[i];
+        }
+        if (buckets) std::memcpy(buckets, t.buckets.data(), sizeof(int64_t) * t.buckets.size());
+        if (pidx) std::memcpy(pidx, t.order.data(), sizeof(int64_t) * t.n);
+    });
+}
+
+gc_status gc_bh_walk(gc_bh *bh, double theta)
+{
+    return guard([&] {
+        GC_REQUIRE(bh, GC_E_VALUE, "null argument");
+        run_walk(bh, theta);
+    });
+}
+
+gc_status gc_bh_get_lists(gc_bh *bh, int64_t *ptr, int64_t *ids, int8_t *kind, int64_t *item_count)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && bh->have_union, GC_E_STATE, "no device walk has run");
+        cudaStream_t s = bh->ctx->stream;
+        const int64_t nb = (int64_t)bh->tree.buckets.size();
+        std::vector<int64_t> st(2 * nb);
+        bh->d_bstat.download(st.data(), 2 * nb, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        std::vector<int64_t> bptr(nb + 1, 0);
+        for (int64_t b = 0; b < nb; ++b) bptr[b + 1] = bptr[b] + st[2 * b];
+        const int64_t tot = bptr[nb];
+        if (ptr) std::memcpy(ptr, bptr.data(), sizeof(int64_t) * (nb + 1));
+        if (item_count)
+            for (int64_t b = 0; b < nb; ++b) item_count[b] = st[2 * b + 1];
+        if (ids || kind) {
+            const int ng = (int)bh->h_wg.size();
+            bh->d_bptr.upload(bptr.data(), nb + 1, s);
+            bh->d_list_ids.resize(tot);
+            bh->d_list_kind.resize(tot);
+            union_to_lists_kernel<<<grid_for(ng, WARPS_PER_BLOCK), 32 * WARPS_PER_BLOCK, 0, s>>>(
+                ng, bh->d_wg.p, bh->d_gbase.p, bh->d_gcount.p, bh->d_uid.p, bh->d_umask.p, bh->d_bptr.p,
+                bh->d_list_ids.p, bh->d_list_kind.p);
+            check_launch("union_to_lists_kernel");
+            std::vector<int> tmp(tot);
+            bh->d_list_ids.download(tmp.data(), tot, s);
+            if (kind) bh->d_list_kind.download(kind, tot, s);
+            GC_CUDA(cudaStreamSynchronize(s));
+            if (ids)
+                for (int64_t i = 0; i < tot; ++i) ids[i] = tmp[i];
+        }
+    });
+}
+
+gc_status gc_bh_set_lists(gc_bh *bh, int64_t n_buckets, const int64_t *ptr, const int64_t *ids, const int8_t *kind)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
+        GC_REQUIRE(n_buckets == (int64_t)bh->tree.buckets.size(), GC_E_VALUE, "list count != bucket count");
+        cudaStream_t s = bh->ctx->stream;
+        const HostTree &t = bh->tree;
+        std::vector<int64_t> np(n_buckets + 1, 0), pp(n_buckets + 1, 0);
+        std::vector<int> na, pa;
+        na.reserve(ptr[n_buckets]);
+        bh->h_item_count.assign(n_buckets, 0);
+        for (int64_t b = 0; b < n_buckets; ++b) {
+            int64_t items = 0;
+            for (int64_t e = ptr[b]; e < ptr[b + 1]; ++e) {
+                const int64_t id = ids[e];
+                GC_REQUIRE(id >= 0 && id < t.n_nodes(), GC_E_VALUE, "list entry is not a node id");
+                if (kind[e] == 0) {
+                    na.push_back((int)id);
+                    items += 1;
+                } else {
+                    GC_REQUIRE(t.first_child[id] < 0, GC_E_VALUE, "particle entry is not a bucket");
+                    pa.push_back((int)id);
+                    items += t.pcount[id];
+                }
+            }
+            np[b + 1] = (int64_t)na.size();
+            pp[b + 1] = (int64_t)pa.size();
+            bh->h_item_count[b] = items;
+        }
+        bh->d_nptr.upload(np.data(), n_buckets + 1, s);
+        bh->d_pptr.upload(pp.data(), n_buckets + 1, s);
+        bh->d_naddr.upload(na.data(), na.size(), s);
+        bh->d_paddr.upload(pa.data(), pa.size(), s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        bh->n_list_entries = ptr[n_buckets];
+        bh->have_member_lists = true;
+        bh->have_union = false;
+    });
+}
+
+gc_status gc_bh_forces_async(gc_bh *bh, double g, double eps)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
+        launch_forces(bh, g, eps);
+    });
+}
+
+gc_status gc_bh_forces(gc_bh *bh, double g, double eps, double *out)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && bh->have_tree && out, GC_E_STATE, "no particles set");
+        launch_forces(bh, g, eps);
+        bh->d_out.download(out, bh->tree.n * bh->tree.dim, bh->ctx->stream);
+        bh->d2h += bh->tree.n * bh->tree.dim * (int64_t)sizeof(double);
+        GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
+    });
+}
+
+gc_status gc_bh_forces_potential(gc_bh *bh, double g, double eps, double *out, double *pot)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && bh->have_tree && out && pot, GC_E_STATE, "no particles set");
+        GC_REQUIRE(bh->have_union, GC_E_STATE, "potentials need device lists (gc_bh_walk)");
+        launch_forces(bh, g, eps, true);
+        bh->d_out.download(out, bh->tree.n * bh->tree.dim, bh->ctx->stream);
+        bh->d_pot.download(pot, bh->tree.n, bh->ctx->stream);
+        GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
+    });
+}
+
+gc_status gc_bh_interactions(gc_bh *bh, int64_t *out)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
+        int64_t tot = 0;
+        const HostTree &t = bh->tree;
+        for (size_t b = 0; b < bh->h_item_count.size(); ++b) tot += t.pcount[t.buckets[b]] * bh->h_item_count[b];
+        *out = tot;
+    });
+}
+
+gc_status gc_bh_timings(gc_bh *bh, double out[2])
+{
+    return guard([&] {
+        GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
+        float a = 0.f, b = 0.f;
+        out[0] = out[1] = 0.0;
+        if (cudaEventElapsedTime(&a, bh->ev[0], bh->ev[1]) == cudaSuccess) out[0] = a;
+        if (cudaEventElapsedTime(&b, bh->ev[2], bh->ev[3]) == cudaSuccess) out[1] = b;
+        cudaGetLastError();
+    });
+}
+
+gc_status gc_bh_io_bytes(gc_bh *bh, int64_t out[2], int32_t reset)
+{
+    return guard([&] {
+        out[0] = bh->h2d;
+        out[1] = bh->d2h;
+        if (reset) bh->h2d = bh->d2h = 0;
+    });
+}
+
+gc_status gc_bh_step(gc_bh *bh, int64_t n, int32_t dim, const double *pos, const double *mass, double box,
+                     int64_t bucket_size, double theta, double g, double eps, double *out)
+{
+    if (bh) bh->h2d = bh->d2h = 0;
+    gc_status st = gc_bh_set_particles(bh, n, dim, pos, mass, box, bucket_size);
+    if (st) return st;
+    st = gc_bh_walk(bh, theta);
+    if (st) return st;
+    return gc_bh_forces(bh, g, eps, out);
+}
+
+}  // extern "C"
+
+namespace gc {
+// KernelSpec of the real kernels (replaces hr/devicesim.py:83-108 presets).
+// out: threads_per_block, registers_per_thread, shared_mem_per_block,
+// members_per_block (work requests one block serves), occupancy blocks/SM.
+void bh_kernel_spec(const char *cls, int64_t out[5])
+{
+    const void *fn;
+    if (!strcmp(cls, "walk")) fn = (const void *)walk_group_kernel<true, true>;
+    else if (!strcmp(cls, "force_member")) fn = (const void *)force_member_kernel<false>;
+    else if (!strcmp(cls, "force")) fn = (const void *)force_group_kernel<false, false>;
+    else throw Error{GC_E_VALUE, std::string("unknown kernel class ") + cls};
+    cudaFuncAttributes a;
+    GC_CUDA(cudaFuncGetAttributes(&a, fn));
+    int blocks = 0;
+    GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, 32 * WARPS_PER_BLOCK, 0));
+    out[0] = 32 * WARPS_PER_BLOCK;
+    out[1] = a.numRegs;
+    out[2] = (int64_t)a.sharedSizeBytes;
+    out[3] = WARPS_PER_BLOCK;
+    out[4] = blocks;
+}
+}  // namespace gc

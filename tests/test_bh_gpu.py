@@ -1,0 +1,190 @@
+"""GPU parity of the Barnes-Hut path (device tree/walk/forces) against the
+reference's golden fixtures and the CPU oracle.
+
+Bars: tree arrays, interaction lists (walk_order, kinds, item_count) are
+bit-exact; forces match float64 within FORCE_RTOL, measured per particle as
+||F_gpu - F_ref||_2 / ||F_ref||_2 (max over all particles).
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+FORCE_RTOL = 1e-5
+
+
+def rel_err(a, b):
+    return np.linalg.norm(a - b, axis=1) / np.linalg.norm(b, axis=1)
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode())
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+@pytest.fixture(scope="module")
+def nb():
+    from paper_2008_05712_b200 import nbody
+    return nbody
+
+
+def tag(th):
+    return f"theta{th:g}".replace(".", "p")
+
+
+CASES = [("nbody2d_300", [0.0, 0.3, 0.7], 0.7), ("nbody3d_2048", [0.0, 0.7], 0.7),
+         ("plummer3d_4096", [0.7], 0.7)]
+
+
+@pytest.mark.parametrize("name,thetas,ftheta", CASES)
+def test_golden_tree_lists_forces(nb, name, thetas, ftheta):
+    from paper_2008_05712_b200.generators import ParticleSet
+    g = np.load(os.path.join(GOLDEN, name + ".npz"))
+    ps = ParticleSet(g["positions"], g["masses"], np.zeros_like(g["positions"]), float(g["box"]))
+    tree = nb.build_bucket_tree(ps, int(g["bucket_size"]))
+    for k in ("center", "half", "mass", "com", "first_child", "n_child"):
+        np.testing.assert_array_equal(getattr(tree, k), g[f"tree_{k}"], err_msg=k)
+    np.testing.assert_array_equal(tree.bucket_ids, g["tree_buckets"])
+    np.testing.assert_array_equal(tree.pidx, g["tree_pidx"])
+    for th in thetas:
+        lists = nb.build_interaction_lists(tree, th, ps)
+        ptr, ids, kind, ic = lists.csr()
+        np.testing.assert_array_equal(ptr, g[f"lists_{tag(th)}_ptr"])
+        np.testing.assert_array_equal(ids, g[f"lists_{tag(th)}_ids"])
+        np.testing.assert_array_equal(kind, g[f"lists_{tag(th)}_kind"])
+        np.testing.assert_array_equal(ic, g[f"lists_{tag(th)}_item_count"])
+        if th == ftheta:
+            f = nb.eval_forces(tree, lists, ps)
+            assert rel_err(f, g[f"forces_{tag(th)}"]).max() <= FORCE_RTOL
+
+
+def test_reference_objects_via_member_kernel(nb):
+    """Lists handed in from the host runtime (reference-style objects) run on
+    the per-work-request kernel and give the same forces."""
+    from paper_2008_05712_b200.generators import ParticleSet
+    g = np.load(os.path.join(GOLDEN, "nbody3d_2048.npz"))
+    ps = ParticleSet(g["positions"], g["masses"], np.zeros_like(g["positions"]), 1.0)
+    tree = nb.build_bucket_tree(ps, 8)
+    csr = (g["lists_theta0p7_ptr"], g["lists_theta0p7_ids"], g["lists_theta0p7_kind"])
+    f = nb.eval_forces(tree, csr, ps)
+    assert rel_err(f, g["forces_theta0p7"]).max() <= FORCE_RTOL
+    dev = nb.build_interaction_lists(tree, 0.7, ps)
+    objs = list(dev)  # reference-shaped InteractionList objects
+    f2 = nb.eval_forces(tree, objs, ps)
+    assert rel_err(f2, g["forces_theta0p7"]).max() <= FORCE_RTOL
+    f3 = nb.eval_forces(tree, dev, ps)  # device lists again (re-walk after set_lists)
+    assert rel_err(f3, g["forces_theta0p7"]).max() <= FORCE_RTOL
+
+
+def test_plummer16k_config1_digests(nb):
+    from paper_2008_05712_b200 import generators as gen
+    from oracle import oracle as orc
+    d = json.load(open(os.path.join(GOLDEN, "digests.json")))["digests"]["plummer3d_16384"]
+    ps = gen.fp32_exact(gen.gen_plummer(16384, 42))
+    tree = nb.build_bucket_tree(ps, 8)
+    pc = np.where(tree.first_child < 0, tree.pcount, 0)
+    assert sha(tree.center, tree.half, tree.mass, tree.com, tree.first_child, tree.n_child, pc,
+               tree.bucket_ids, tree.pidx) == d["tree"]
+    lists = nb.build_interaction_lists(tree, 0.7, ps)
+    ptr, ids, kind, ic = lists.csr()
+    assert sha(ptr, ids, kind, ic) == d["lists_theta0p7"]
+    f = nb.eval_forces(tree, lists, ps)
+    ot = orc.build_bucket_tree(ps.positions, ps.masses, 8)
+    ref = orc.eval_forces(ot, orc.build_interaction_lists(ot, 0.7), ps.positions, ps.masses)
+    assert sha(ref) == d["forces_theta0p7"]  # oracle == reference bits
+    assert rel_err(f, ref).max() <= FORCE_RTOL
+
+
+def test_clustered_1m_config3_full_size(nb):
+    """configs[2]: clustered 1M, theta 0.7 -- lists bit-exact against the
+    oracle (itself pinned to the reference), forces within FORCE_RTOL."""
+    from paper_2008_05712_b200 import generators as gen
+    from oracle import oracle as orc
+    ps = gen.fp32_exact(gen.gen_particles(1_000_000, 42, clustering=0.6, dim=3))
+    tree = nb.build_bucket_tree(ps, 8)
+    lists = nb.build_interaction_lists(tree, 0.7, ps)
+    f = nb.eval_forces(tree, lists, ps)
+    ot = orc.build_bucket_tree(ps.positions, ps.masses, 8)
+    ol = orc.build_interaction_lists(ot, 0.7)
+    ptr, ids, kind, ic = lists.csr()
+    assert np.array_equal(ptr, ol.ptr)
+    assert np.array_equal(ic, ol.item_count)
+    assert np.array_equal(ids, ol.ids)
+    assert np.array_equal(kind, ol.kind)
+    ref = orc.eval_forces(ot, ol, ps.positions, ps.masses)
+    e = rel_err(f, ref)
+    print(f"1M clustered: median {np.median(e):.2e} p99.9 {np.percentile(e, 99.9):.2e} max {e.max():.2e}")
+    assert e.max() <= FORCE_RTOL
+    assert nb.interactions(tree) == int((tree.pcount[tree.bucket_ids] * ic).sum())
+
+
+def test_theta_zero_equals_direct(nb):
+    from paper_2008_05712_b200 import generators as gen
+    ps = gen.fp32_exact(gen.gen_particles(512, 15, clustering=0.5, dim=3))
+    tree = nb.build_bucket_tree(ps, 8)
+    lists = nb.build_interaction_lists(tree, 0.0, ps)
+    for il in lists:
+        assert il.node_interactions == []
+    f = nb.eval_forces(tree, lists, ps)
+    exact = nb.direct_force_oracle(ps)
+    assert rel_err(f, exact).max() <= FORCE_RTOL
+
+
+def test_edge_cases(nb):
+    from paper_2008_05712_b200.generators import ParticleSet
+    # single particle, root is a bucket
+    ps = ParticleSet(np.array([[0.25, 0.75]]), np.ones(1), np.zeros((1, 2)), 1.0)
+    t = nb.build_bucket_tree(ps, 8)
+    assert len(t.buckets) == 1 and t.root.is_bucket
+    f = nb.eval_forces(t, nb.build_interaction_lists(t, 0.5, ps), ps)
+    assert np.all(f == 0.0)
+    # four quadrants, bucket size 1 (test_workloads.py:40-48)
+    pts = np.array([[0.2, 0.2], [0.8, 0.2], [0.2, 0.8], [0.8, 0.8]])
+    ps = ParticleSet(pts, np.ones(4), np.zeros((4, 2)), 1.0)
+    t = nb.build_bucket_tree(ps, 1)
+    assert len(t.buckets) == 4
+    lists = nb.build_interaction_lists(t, 100.0, ps)
+    assert all(len(il.walk_order) <= 4 for il in lists)
+    # two-body Newton with eps = 0 (test_workloads.py:112-121)
+    ps = ParticleSet(np.array([[0.0, 0.0], [1.0, 0.0]]), np.ones(2), np.zeros((2, 2)), 2.0)
+    f = nb.direct_force_oracle(ps, g=1.0, eps=0.0)
+    np.testing.assert_allclose(f, [[1.0, 0.0], [-1.0, 0.0]], atol=1e-12)
+    t = nb.build_bucket_tree(ps, 1)
+    f = nb.eval_forces(t, nb.build_interaction_lists(t, 0.0, ps), ps, g=1.0, eps=0.0)
+    np.testing.assert_allclose(f, [[1.0, 0.0], [-1.0, 0.0]], rtol=1e-6)
+    # coincident particles need softening
+    ps = ParticleSet(np.array([[0.5, 0.5], [0.5, 0.5]]), np.ones(2), np.zeros((2, 2)), 1.0)
+    with pytest.raises(Exception):
+        nb.direct_force_oracle(ps, eps=0.0)
+    with pytest.raises(ValueError):
+        nb.build_bucket_tree(ps, 0)
+
+
+def test_kernels_api_bit_exact():
+    from paper_2008_05712_b200 import kernels as kn
+    g = np.load(os.path.join(GOLDEN, "kernels.npz"))
+    np.testing.assert_array_equal(kn.forces_from_points(g["ppos"], g["pmass"], g["spos"], g["smass"], 1.0, 1e-4),
+                                  g["ffp"])
+    np.testing.assert_array_equal(kn.forces_from_points(g["ppos"], g["pmass"], g["spos"], g["smass"], 1.0, 0.0),
+                                  g["ffp_eps0"])
+    fa, fb = kn.md_cross_forces(g["md_a"], g["md_b"], 1.0, 25.0)
+    np.testing.assert_array_equal(fa, g["md_fa"])
+    np.testing.assert_array_equal(fb, g["md_fb"])
+    np.testing.assert_array_equal(kn.md_self_forces(g["md_self_pos"], 1.0, 25.0), g["md_self_f"])
+    np.testing.assert_array_equal(kn.direct_forces(g["direct_pos"], g["direct_mass"], 1.0, 1e-4), g["direct_f"])
+    off = np.concatenate([[0], np.cumsum(g["runs_lens"])])
+    for i in range(len(g["runs_lens"])):
+        assert kn.count_address_runs(g["runs_in"][off[i]:off[i + 1]], 16) == g["runs_out"][i]
+    assert kn.count_address_runs(np.arange(40), 16) == 3
+    assert kn.count_address_runs(np.arange(0, 32, 2), 16) == 16
