@@ -18,6 +18,8 @@ struct gc_bh {
     bool have_tree = false;
     std::vector<WalkGroup> h_wg;
     std::vector<ForceGroup> h_fg;
+    std::vector<unsigned> h_fgmask;
+    DBuf<unsigned> d_fgmask;
     // device tree
     DBuf<float4> d_recs;  // walk records: float32 com + packed links
     DBuf<double4> d_com64;  // float64 com (exact opening test)
@@ -54,6 +56,8 @@ struct gc_bh {
     DBuf<int> d_list_ids;
     DBuf<int8_t> d_list_kind;
     DBuf<int> d_flag;
+    WalkParams wp{};
+    bool stats_dirty = false;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     int64_t h2d = 0, d2h = 0;  // bytes moved host<->device since the last reset
     ~gc_bh()
@@ -128,26 +132,31 @@ void upload_tree(gc_bh *bh)
     // consecutive buckets inside one walk group
     bh->h_wg.clear();
     bh->h_fg.clear();
+    bh->h_fgmask.clear();
     for (int64_t b0 = 0; b0 < nb; b0 += 32) {
         WalkGroup wg;
         wg.bfirst = (int)b0;
         wg.nbucket = (int)std::min<int64_t>(32, nb - b0);
+        wg.fg_first = (int)bh->h_fg.size();
         const int wi = (int)bh->h_wg.size();
-        bh->h_wg.push_back(wg);
         for (int64_t b = b0; b < b0 + wg.nbucket;) {
             ForceGroup fg;
             fg.pstart = (int)t.pstart[t.buckets[b]];
             fg.wg = wi;
-            fg.boff = (int)(b - b0);
+            fg.bmask = 0u;
             int tg = 0;
             while (b < b0 + wg.nbucket && tg + t.pcount[t.buckets[b]] <= 32) {
                 tg += (int)t.pcount[t.buckets[b]];
+                fg.bmask |= 1u << (b - b0);
                 ++b;
             }
             GC_REQUIRE(tg > 0, GC_E_VALUE, "bucket with more than 32 particles (coincident points) on the group path");
             fg.ntarget = tg;
             bh->h_fg.push_back(fg);
+            bh->h_fgmask.push_back(fg.bmask);
         }
+        wg.nfg = (int)bh->h_fg.size() - wg.fg_first;
+        bh->h_wg.push_back(wg);
     }
     bh->d_recs.upload(recs.data(), nn, s);
     bh->d_com64.upload(c64.data(), nn, s);
@@ -161,10 +170,11 @@ void upload_tree(gc_bh *bh)
     bh->d_part_bucket.upload(pb.data(), t.n, s);
     bh->d_wg.upload(bh->h_wg.data(), bh->h_wg.size(), s);
     bh->d_fg.upload(bh->h_fg.data(), bh->h_fg.size(), s);
+    bh->d_fgmask.upload(bh->h_fgmask.data(), bh->h_fgmask.size(), s);
     bh->h2d += nn * (int64_t)(3 * sizeof(float4) + sizeof(double4) + sizeof(int2)) +
                nb * (int64_t)(sizeof(double4) + sizeof(float4) + sizeof(int2) + sizeof(int)) +
                t.n * (int64_t)sizeof(int) + (int64_t)bh->h_wg.size() * (int64_t)sizeof(WalkGroup) +
-               (int64_t)bh->h_fg.size() * (int64_t)sizeof(ForceGroup);
+               (int64_t)bh->h_fg.size() * (int64_t)(sizeof(ForceGroup) + sizeof(unsigned));
     GC_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -195,79 +205,20 @@ void exclusive_scan(gc_ctx *ctx, const T *in, T *out, int64_t n)
     GC_CUDA(cub::DeviceScan::ExclusiveSum(ctx->scratch.p, bytes, in, out, n, ctx->stream));
 }
 
-void run_walk(gc_bh *bh, double theta)
+// Per-walk host bookkeeping that needs the device stats (item counts,
+// entry totals) is done lazily, so a steady-state walk is fully asynchronous.
+void sync_walk_stats(gc_bh *bh)
 {
-    GC_REQUIRE(theta >= 0.0, GC_E_VALUE, "theta must be >= 0");
-    GC_REQUIRE(bh->have_tree, GC_E_STATE, "no particles set");
-    gc_ctx *ctx = bh->ctx;
-    cudaStream_t s = ctx->stream;
-    const int ng = (int)bh->h_wg.size();
+    if (!bh->stats_dirty) return;
+    cudaStream_t s = bh->ctx->stream;
     const int64_t nb = (int64_t)bh->tree.buckets.size();
-    bh->d_gcount.resize(ng);
-    bh->d_gbase.resize(ng + 1);
-    bh->d_gcap.resize(ng + 1);
-    bh->d_bstat.resize(2 * nb);
-    bh->d_flag.resize(1);
-    const unsigned grid = grid_for(ng, WARPS_PER_BLOCK);
-    const double th2 = theta * theta;
-    const double root = 2.0 * bh->tree.half[0];
-    // per-level float32 thresholds on s = d^2: accept iff s > size^2 / theta^2
-    std::vector<float2> tt(MAX_LEVELS);
-    for (int l = 0; l < MAX_LEVELS; ++l) {
-        const double size = std::ldexp(root, -l);
-        const double T = theta > 0.0 ? size * size / th2 : HUGE_VAL;
-        const float a = (float)(T * (1.0 + std::ldexp(1.0, -22)));
-        const float r = (float)(T * (1.0 - std::ldexp(1.0, -22)));
-        tt[l].x = std::nextafter(a, HUGE_VALF);
-        tt[l].y = std::isinf(r) ? r : std::nextafter(r, 0.f);
-    }
-    bh->d_tt.upload(tt.data(), MAX_LEVELS, s);
-    WalkParams P;
-    P.theta = theta;
-    P.theta2 = th2;
-    P.root_size = root;
-    P.dd2 = bh->walk_dd2;
-    P.dd3 = bh->walk_dd3;
-    P.tt = bh->d_tt.p;
-    GC_CUDA(cudaEventRecord(bh->ev[0], s));
-    bh->d_flag.zero(s);
-    // capacities: the previous walk's counts on this tree plus slack, else a counting pass
-    if (!bh->cap_valid || bh->cap_theta != theta) {
-        walk_group_kernel<false, true><<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(
-            ng, bh->d_wg.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p, bh->d_bgeo32.p, P, nullptr, nullptr, nullptr,
-            nullptr, bh->d_gcount.p, bh->d_bstat.p, bh->d_flag.p);
-        check_launch("walk_group_kernel<count>");
-        GC_CUDA(cudaMemcpyAsync(bh->d_gcap.p, bh->d_gcount.p, sizeof(int64_t) * ng, cudaMemcpyDeviceToDevice, s));
-        bh->cap_valid = false;
-    }
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        GC_CUDA(cudaMemsetAsync(bh->d_gcap.p + ng, 0, sizeof(int64_t), s));
-        exclusive_scan(ctx, bh->d_gcap.p, bh->d_gbase.p, (int64_t)ng + 1);
-        int64_t total = 0;
-        GC_CUDA(cudaMemcpyAsync(&total, bh->d_gbase.p + ng, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        GC_CUDA(cudaStreamSynchronize(s));
-        bh->d_uid.resize(total);
-        bh->d_umask.resize(total);
-        walk_group_kernel<true, true><<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(
-            ng, bh->d_wg.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p, bh->d_bgeo32.p, P, bh->d_gbase.p,
-            bh->d_gcap.p, bh->d_uid.p, bh->d_umask.p, bh->d_gcount.p, bh->d_bstat.p, bh->d_flag.p);
-        check_launch("walk_group_kernel<write>");
-        int flag = 0;
-        bh->d_flag.download(&flag, 1, s);
-        GC_CUDA(cudaStreamSynchronize(s));
-        GC_REQUIRE(!(flag & 1), GC_E_VALUE, "tree deeper than the walk stack (box too large for half_size >= 1e-9)");
-        if (!(flag & 2)) break;
-        // capacity overflow (lists grew): exact counts from this pass, retry once
-        GC_REQUIRE(attempt == 0, GC_E_STATE, "walk capacity overflow after recount");
-        GC_CUDA(cudaMemcpyAsync(bh->d_gcap.p, bh->d_gcount.p, sizeof(int64_t) * ng, cudaMemcpyDeviceToDevice, s));
-        bh->d_flag.zero(s);
-        bh->cap_valid = false;
-    }
-    GC_CUDA(cudaEventRecord(bh->ev[1], s));
     std::vector<int64_t> st(2 * nb);
+    int flag = 0;
     bh->d_bstat.download(st.data(), 2 * nb, s);
+    bh->d_flag.download(&flag, 1, s);
     GC_CUDA(cudaStreamSynchronize(s));
-    bh->d2h += 2 * nb * (int64_t)sizeof(int64_t) + 2 * (int64_t)sizeof(int64_t);
+    GC_REQUIRE(!(flag & 1), GC_E_VALUE, "tree deeper than the walk stack (box too large for half_size >= 1e-9)");
+    GC_REQUIRE(!(flag & 2), GC_E_STATE, "walk list capacity overflow (re-run gc_bh_walk)");
     bh->h_item_count.resize(nb);
     int64_t ent = 0;
     for (int64_t b = 0; b < nb; ++b) {
@@ -275,23 +226,82 @@ void run_walk(gc_bh *bh, double theta)
         bh->h_item_count[b] = st[2 * b + 1];
     }
     bh->n_list_entries = ent;
-    bh->have_union = true;
-    bh->have_member_lists = false;
-    // next walk on this tree: reuse the counts with 1/8 slack in a single pass
-    if (!bh->cap_valid) {
-        std::vector<int64_t> cnt(ng);
-        bh->d_gcount.download(cnt.data(), ng, s);
+    bh->stats_dirty = false;
+}
+
+void run_walk(gc_bh *bh, double theta)
+{
+    GC_REQUIRE(theta >= 0.0, GC_E_VALUE, "theta must be >= 0");
+    GC_REQUIRE(bh->have_tree, GC_E_STATE, "no particles set");
+    gc_ctx *ctx = bh->ctx;
+    cudaStream_t s = ctx->stream;
+    const int ng = (int)bh->h_wg.size();
+    const int nf = (int)bh->h_fg.size();  // lists are per force group
+    const int64_t nb = (int64_t)bh->tree.buckets.size();
+    const unsigned grid = grid_for(ng, WARPS_PER_BLOCK);
+    const bool fresh = !bh->cap_valid || bh->cap_theta != theta;
+    if (fresh) {
+        bh->d_gcount.resize(nf);
+        bh->d_gbase.resize(nf + 1);
+        bh->d_gcap.resize(nf + 1);
+        bh->d_bstat.resize(2 * nb);
+        bh->d_flag.resize(1);
+        const double th2 = theta * theta;
+        const double root = 2.0 * bh->tree.half[0];
+        // per-level float32 thresholds on s = d^2: accept iff s > size^2 / theta^2
+        std::vector<float2> tt(MAX_LEVELS);
+        for (int l = 0; l < MAX_LEVELS; ++l) {
+            const double size = std::ldexp(root, -l);
+            const double T = theta > 0.0 ? size * size / th2 : HUGE_VAL;
+            const float a = (float)(T * (1.0 + std::ldexp(1.0, -22)));
+            const float r = (float)(T * (1.0 - std::ldexp(1.0, -22)));
+            tt[l].x = std::nextafter(a, HUGE_VALF);
+            tt[l].y = std::isinf(r) ? r : std::nextafter(r, 0.f);
+        }
+        bh->d_tt.upload(tt.data(), MAX_LEVELS, s);
+        bh->wp.theta = theta;
+        bh->wp.theta2 = th2;
+        bh->wp.root_size = root;
+        bh->wp.dd2 = bh->walk_dd2;
+        bh->wp.dd3 = bh->walk_dd3;
+        bh->wp.tt = bh->d_tt.p;
+    }
+    GC_CUDA(cudaEventRecord(bh->ev[0], s));
+    bh->d_flag.zero(s);
+    if (fresh) {
+        // first walk on this tree: count, then size every force group's list
+        // with 1/8 slack so later walks (moved particles) run in one pass
+        walk_group_kernel<false, true><<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(
+            ng, bh->d_wg.p, bh->d_fgmask.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p, bh->d_bgeo32.p, bh->wp,
+            nullptr, nullptr, nullptr, nullptr, bh->d_gcount.p, bh->d_bstat.p, bh->d_flag.p);
+        check_launch("walk_group_kernel<count>");
+        std::vector<int64_t> cnt(nf + 1, 0);
+        bh->d_gcount.download(cnt.data(), nf, s);
         GC_CUDA(cudaStreamSynchronize(s));
+        std::vector<int64_t> cap(nf + 1, 0), basev(nf + 1, 0);
         int64_t tot = 0;
-        for (auto &c : cnt) {
-            tot += c;
-            c = c + c / 8 + 16;
+        for (int f = 0; f < nf; ++f) {
+            tot += cnt[f];
+            cap[f] = cnt[f] + cnt[f] / 8 + 16;
+            basev[f + 1] = basev[f] + cap[f];
         }
         bh->n_union = tot;
-        bh->d_gcap.upload(cnt.data(), ng, s);
+        bh->d_gcap.upload(cap.data(), nf + 1, s);
+        bh->d_gbase.upload(basev.data(), nf + 1, s);
+        bh->d_uid.resize(basev[nf]);
+        bh->d_umask.resize(basev[nf]);
         bh->cap_valid = true;
         bh->cap_theta = theta;
     }
+    walk_group_kernel<true, true><<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(
+        ng, bh->d_wg.p, bh->d_fgmask.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p, bh->d_bgeo32.p, bh->wp,
+        bh->d_gbase.p, bh->d_gcap.p, bh->d_uid.p, bh->d_umask.p, bh->d_gcount.p, bh->d_bstat.p, bh->d_flag.p);
+    check_launch("walk_group_kernel<write>");
+    GC_CUDA(cudaEventRecord(bh->ev[1], s));
+    bh->have_union = true;
+    bh->have_member_lists = false;
+    bh->stats_dirty = true;
+    if (fresh) sync_walk_stats(bh);
 }
 
 void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
@@ -363,6 +373,7 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
         bh->have_tree = true;
         bh->have_union = bh->have_member_lists = false;
         bh->cap_valid = false;
+        bh->stats_dirty = false;
         upload_tree(bh);
         upload_particles(bh, pos, mass);
     });
@@ -372,6 +383,7 @@ gc_status gc_bh_sizes(gc_bh *bh, int64_t out[4])
 {
     return guard([&] {
         GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
+        sync_walk_stats(bh);
         out[0] = bh->tree.n_nodes();
         out[1] = (int64_t)bh->tree.buckets.size();
         out[2] = bh->n_list_entries;
@@ -415,6 +427,7 @@ gc_status gc_bh_get_lists(gc_bh *bh, int64_t *ptr, int64_t *ids, int8_t *kind, i
 {
     return guard([&] {
         GC_REQUIRE(bh && bh->have_union, GC_E_STATE, "no device walk has run");
+        sync_walk_stats(bh);
         cudaStream_t s = bh->ctx->stream;
         const int64_t nb = (int64_t)bh->tree.buckets.size();
         std::vector<int64_t> st(2 * nb);
@@ -427,12 +440,12 @@ gc_status gc_bh_get_lists(gc_bh *bh, int64_t *ptr, int64_t *ids, int8_t *kind, i
         if (item_count)
             for (int64_t b = 0; b < nb; ++b) item_count[b] = st[2 * b + 1];
         if (ids || kind) {
-            const int ng = (int)bh->h_wg.size();
+            const int nf = (int)bh->h_fg.size();
             bh->d_bptr.upload(bptr.data(), nb + 1, s);
             bh->d_list_ids.resize(tot);
             bh->d_list_kind.resize(tot);
-            union_to_lists_kernel<<<grid_for(ng, WARPS_PER_BLOCK), 32 * WARPS_PER_BLOCK, 0, s>>>(
-                ng, bh->d_wg.p, bh->d_gbase.p, bh->d_gcount.p, bh->d_uid.p, bh->d_umask.p, bh->d_bptr.p,
+            union_to_lists_kernel<<<grid_for(nf, WARPS_PER_BLOCK), 32 * WARPS_PER_BLOCK, 0, s>>>(
+                nf, bh->d_fg.p, bh->d_wg.p, bh->d_gbase.p, bh->d_gcount.p, bh->d_uid.p, bh->d_umask.p, bh->d_bptr.p,
                 bh->d_list_ids.p, bh->d_list_kind.p);
             check_launch("union_to_lists_kernel");
             std::vector<int> tmp(tot);
@@ -501,6 +514,12 @@ gc_status gc_bh_forces(gc_bh *bh, double g, double eps, double *out)
         bh->d_out.download(out, bh->tree.n * bh->tree.dim, bh->ctx->stream);
         bh->d2h += bh->tree.n * bh->tree.dim * (int64_t)sizeof(double);
         GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
+        if (bh->have_union) {  // surface a deferred walk overflow
+            int flag = 0;
+            bh->d_flag.download(&flag, 1, bh->ctx->stream);
+            GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
+            GC_REQUIRE(!(flag & 2), GC_E_STATE, "walk list capacity overflow (re-run gc_bh_walk)");
+        }
     });
 }
 
@@ -520,6 +539,7 @@ gc_status gc_bh_interactions(gc_bh *bh, int64_t *out)
 {
     return guard([&] {
         GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
+        sync_walk_stats(bh);
         int64_t tot = 0;
         const HostTree &t = bh->tree;
         for (size_t b = 0; b < bh->h_item_count.size(); ++b) tot += t.pcount[t.buckets[b]] * bh->h_item_count[b];
@@ -531,6 +551,12 @@ gc_status gc_bh_timings(gc_bh *bh, double out[2])
 {
     return guard([&] {
         GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
+        if (bh->have_union) {
+            int flag = 0;
+            bh->d_flag.download(&flag, 1, bh->ctx->stream);
+            GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
+            GC_REQUIRE(!(flag & 2), GC_E_STATE, "walk list capacity overflow (re-run gc_bh_walk)");
+        }
         float a = 0.f, b = 0.f;
         out[0] = out[1] = 0.0;
         if (cudaEventElapsedTime(&a, bh->ev[0], bh->ev[1]) == cudaSuccess) out[0] = a;

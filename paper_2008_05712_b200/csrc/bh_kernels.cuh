@@ -38,13 +38,15 @@ constexpr int NODE_BITS = 26;  // stack entries pack node | level << NODE_BITS
 struct WalkGroup {
     int bfirst;  // first bucket (depth-first index)
     int nbucket;  // <= 32
+    int fg_first;  // its force groups: [fg_first, fg_first + nfg)
+    int nfg;
 };
 
 struct ForceGroup {
     int pstart;  // first target in the DFS-sorted particle array
     int ntarget;  // <= 32
-    int wg;  // walk group whose union list it reads
-    int boff;  // offset of its first bucket inside the walk group
+    int wg;  // walk group that emits its list
+    unsigned bmask;  // its buckets, as bits of the walk group (bit j = bucket bfirst + j)
 };
 
 struct WalkParams {
@@ -88,7 +90,8 @@ __device__ __forceinline__ bool mac_accept64(const double4 c, const double size,
 // ---------------------------------------------------------------------------
 template <bool WRITE, bool STATS>
 __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, 4)
-walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const float4 *__restrict__ recs,
+walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsigned *__restrict__ fg_mask,
+                  const float4 *__restrict__ recs,
                   const double4 *__restrict__ com64, const double4 *__restrict__ bgeo,
                   const float4 *__restrict__ bgeo32, const WalkParams P, const int64_t *__restrict__ gbase,
                   const int64_t *__restrict__ gcap, int *__restrict__ uid, uint2 *__restrict__ umask,
@@ -109,11 +112,15 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const float
     const unsigned full = gd.nbucket == 32 ? 0xffffffffu : ((1u << gd.nbucket) - 1u);
     const unsigned bit = 1u << lane;
     int2 *stack = stack_s[warp];
-    int sp = 0, w = 0;
-    const int64_t base = WRITE ? gbase[g] : 0;
-    const int cap = WRITE ? (int)gcap[g] : 0;
-    int my_entries = 0;
-    long long my_items = 0;
+    int sp = 0;
+    // lane f < nfg emits the list of force group fg_first + f
+    const bool emits = lane < gd.nfg;
+    const int my_fg = gd.fg_first + (emits ? lane : 0);
+    const unsigned fgm = emits ? fg_mask[my_fg] : 0u;
+    const int64_t base = WRITE && emits ? gbase[my_fg] : 0;
+    const int cap = WRITE && emits ? (int)gcap[my_fg] : 0;
+    int w = 0;
+    int my_entries = 0, my_items = 0;
     int node = 0, lvl = 0;
     unsigned act = full;
     float4 nd = recs[0];
@@ -122,7 +129,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const float
         const bool is_bucket = wr_bucket(wd);
         const int fc = wr_first(wd);
         // speculative loads of both possible successors
-        const int2 top = stack[sp > 0 ? sp - 1 : 0];
+        const int2 top = sp > 0 ? stack[sp - 1] : make_int2(0, 0);
         const float4 n_open = recs[is_bucket ? 0 : fc];
         const float4 n_pop = recs[top.x & ((1 << NODE_BITS) - 1)];
         // float32 opening test with error bound: certain accept / reject
@@ -141,19 +148,21 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const float
         const unsigned acc_m = __ballot_sync(0xffffffffu, acc);
         const unsigned part_m = is_bucket ? (act & ~acc_m) : 0u;
         if (acc_m | part_m) {
-            if (WRITE && lane == 0) {
-                if (w < cap) {
-                    uid[base + w] = node;
-                    umask[base + w] = make_uint2(acc_m, part_m);
-                } else {
-                    atomicOr(flag, 2);
+            if ((acc_m | part_m) & fgm) {
+                if (WRITE) {
+                    if (w < cap) {
+                        uid[base + w] = node;
+                        umask[base + w] = make_uint2(acc_m & fgm, part_m & fgm);
+                    } else {
+                        atomicOr(flag, 2);
+                    }
                 }
+                ++w;
             }
-            ++w;
             if (STATS) {
                 const bool a = acc_m & bit, p = part_m & bit;
                 my_entries += (a || p) ? 1 : 0;
-                my_items += a ? 1 : (p ? -wd : 0);
+                my_items += a ? 1 : (p ? -wd : 0);  // item_count (nbody.py:187-189)
             }
         }
         const unsigned open = is_bucket ? 0u : (act & ~acc_m);
@@ -182,7 +191,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const float
         }
     }
     if (STATS) {
-        if (lane == 0) gcount[g] = w;
+        if (emits) gcount[my_fg] = w;
         if (has) {
             bstat[2 * (int64_t)(gd.bfirst + lane)] = my_entries;
             bstat[2 * (int64_t)(gd.bfirst + lane) + 1] = my_items;
@@ -192,19 +201,21 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const float
 
 // Per-bucket walk_order / kind CSR from the union lists (parity + drop-in API).
 __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK)
-union_to_lists_kernel(int ngroups, const WalkGroup *__restrict__ groups, const int64_t *__restrict__ gbase,
-                      const int64_t *__restrict__ gcount, const int *__restrict__ uid, const uint2 *__restrict__ umask,
-                      const int64_t *__restrict__ bptr, int *__restrict__ ids, int8_t *__restrict__ kind)
+union_to_lists_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const WalkGroup *__restrict__ wgroups,
+                      const int64_t *__restrict__ gbase, const int64_t *__restrict__ gcount,
+                      const int *__restrict__ uid, const uint2 *__restrict__ umask, const int64_t *__restrict__ bptr,
+                      int *__restrict__ ids, int8_t *__restrict__ kind)
 {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = blockIdx.x * WARPS_PER_BLOCK + warp;
-    if (g >= ngroups) return;
-    const WalkGroup gd = groups[g];
-    int64_t cur = lane < gd.nbucket ? bptr[gd.bfirst + lane] : 0;
+    const int f = blockIdx.x * WARPS_PER_BLOCK + warp;
+    if (f >= nfg) return;
+    const ForceGroup fg = fgroups[f];
     const unsigned bit = 1u << lane;
-    for (int64_t e = gbase[g]; e < gbase[g] + gcount[g]; ++e) {
+    const bool mine = fg.bmask & bit;
+    int64_t cur = mine ? bptr[wgroups[fg.wg].bfirst + lane] : 0;
+    for (int64_t e = gbase[f]; e < gbase[f] + gcount[f]; ++e) {
         const uint2 m = umask[e];
-        if (lane < gd.nbucket && ((m.x | m.y) & bit)) {
+        if (mine && ((m.x | m.y) & bit)) {
             ids[cur] = uid[e];
             kind[cur] = (m.x & bit) ? 0 : 1;
             ++cur;
@@ -262,11 +273,10 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int64_
     const float4 xp = parts[p];
     const float3 xi = make_float3(xp.x, xp.y, xp.z);
     const unsigned mybit = tgt ? (1u << (part_bucket[p] - wfirst)) : 0u;
-    const unsigned fmask = __reduce_or_sync(0xffffffffu, mybit);  // buckets of this force group
     float4 *qh = q_hi[warp];
     float4 *ql = q_lo[warp];
     double ax = 0.0, ay = 0.0, az = 0.0, ap = 0.0;
-    const int64_t e0 = gbase[fg.wg], e1 = e0 + gcount[fg.wg];
+    const int64_t e0 = gbase[gi], e1 = e0 + min(gcount[gi], gbase[gi + 1] - gbase[gi]);
     for (int64_t c = e0; c < e1; c += 32) {
         const int64_t e = c + lane;
         int node = 0;
@@ -275,8 +285,6 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int64_
         if (e < e1) {
             node = uid[e];
             m = umask[e];
-            m.x &= fmask;
-            m.y &= fmask;
         }
         if (m.y) pr = prange[node];
         const int nrec = (m.x ? 1 : 0) + (m.y ? pr.y : 0);
