@@ -133,6 +133,37 @@ gc_status gc_bh_io_bytes(gc_bh *bh, int64_t out[2], int32_t reset);
 gc_status gc_bh_step(gc_bh *bh, int64_t n, int32_t dim, const double *pos, const double *mass, double box,
                      int64_t bucket_size, double theta, double g, double eps, double *out);
 
+/* ---- data manager (hr/memory.py:228-369) ------------------------------------
+ * One handle per kernel class: uniform slots of slot_bytes over
+ * capacity_bytes of HBM, mode 0 = REDUNDANT, 1 = REUSE, 2 = REUSE_SORTED
+ * (MemoryMode, memory.py:30-33).  Buffer ids are non-negative int32. */
+gc_status gc_dm_create(gc_ctx *ctx, int64_t capacity_bytes, int64_t slot_bytes, int32_t mode, gc_dm **out);
+gc_status gc_dm_destroy(gc_dm *dm);
+/* build_plan (memory.py:289-360): members as CSR (ids, bounds[n_members+1]).
+ * Pins the batch's buffers until gc_dm_release.  GC_E_CAPACITY on failure
+ * (pins rolled back).  Sizes of the plan are returned; fetch it with
+ * gc_dm_plan_get. */
+gc_status gc_dm_build_plan(gc_dm *dm, const int64_t *ids, const int64_t *bounds, int32_t n_members, double now,
+                           int64_t *n_transfer, int64_t *n_positions);
+/* to_transfer (buffer ids, in allocation order), addresses (slot per
+ * position), transactions per member (memory.py:204-209); out_bytes =
+ * {total_bytes, indirection_bytes, indirect}.  Any pointer may be NULL. */
+gc_status gc_dm_plan_get(gc_dm *dm, int64_t *to_transfer, int64_t *addresses, int64_t *transactions,
+                         int64_t out_bytes[3]);
+/* release_batch (memory.py:362-365): unpin set(ids) */
+gc_status gc_dm_release(gc_dm *dm, const int64_t *ids, int64_t n);
+/* pin / unpin set(ids) (memory.py:240-250): delta +1 or -1 */
+gc_status gc_dm_pin(gc_dm *dm, const int64_t *ids, int64_t n, int32_t delta);
+/* evict_slots (memory.py:260-285): evicted buffer ids in eviction order */
+gc_status gc_dm_evict(gc_dm *dm, int64_t needed_bytes, int64_t *evicted, int64_t *n_evicted);
+/* lookup_residency (memory.py:78-93): resident[i] = 1 if ids[i] has a slot
+ * (and its last_use_time becomes now) */
+gc_status gc_dm_lookup(gc_dm *dm, const int64_t *ids, int64_t n, double now, int8_t *resident);
+/* out = {slot_count, free_slots, resident_buffers, id_universe} */
+gc_status gc_dm_state(gc_dm *dm, int64_t out[4]);
+/* resident table sorted by buffer id (ChareTable, memory.py:50-75) */
+gc_status gc_dm_table(gc_dm *dm, int64_t *bufs, int64_t *slots, double *last_use, int64_t *pins);
+
 #ifdef __cplusplus
 }
 #endif

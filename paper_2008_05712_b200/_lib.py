@@ -55,6 +55,16 @@ SIGNATURES = {
     "gc_measure_fp32_peak": [vp, f64p, f64p],
     "gc_bh_step": [vp, C.c_int64, C.c_int32, f64p, f64p, C.c_double, C.c_int64, C.c_double, C.c_double,
                    C.c_double, f64p],
+    "gc_dm_create": [vp, C.c_int64, C.c_int64, C.c_int32, C.POINTER(vp)],
+    "gc_dm_destroy": [vp],
+    "gc_dm_build_plan": [vp, i64p, i64p, C.c_int32, C.c_double, i64p, i64p],
+    "gc_dm_plan_get": [vp, i64p, i64p, i64p, i64p],
+    "gc_dm_release": [vp, i64p, C.c_int64],
+    "gc_dm_pin": [vp, i64p, C.c_int64, C.c_int32],
+    "gc_dm_evict": [vp, C.c_int64, i64p, i64p],
+    "gc_dm_lookup": [vp, i64p, C.c_int64, C.c_double, i8p],
+    "gc_dm_state": [vp, i64p],
+    "gc_dm_table": [vp, i64p, i64p, f64p, i64p],
 }
 _RESTYPE = {"gc_ctx_stream": vp, "gc_last_error": C.c_char_p, "gc_version": C.c_char_p}
 

@@ -1,2 +1,581 @@
-// dm.cu -- device data manager (placeholder; filled in below)
+// dm.cu -- device data manager: residency table, LRU eviction, min-free-slot
+// allocation, reorganised per-member address maps (sm_100a).
+//
+// Restates DeviceMemory (hr/memory.py:228-369) with its decisions computed in
+// HBM and bit-identical to the reference:
+//   * first-seen dedup of the batch (memory.py:321-327): atomicMin of the
+//     position per buffer id, then an order-preserving compaction;
+//   * residency lookup refreshing last_use of residents (78-93);
+//   * REUSE_SORTED: missing buffers in ascending id (329-330);
+//   * pin every distinct buffer (332), evict unpinned residents in
+//     (last_use_time, buffer) order until the missing set fits (260-285) --
+//     two stable radix sorts; partial evictions persist when the pinned set
+//     makes the request infeasible, as in the reference;
+//   * the k-th missing buffer gets the k-th smallest free slot (min-heap pops
+//     with no interleaved frees, 116-119, 338-340);
+//   * per-member address map, per member sorted in REUSE_SORTED (342-347);
+//   * member transactions = address runs per 16-lane group x2 when indirect
+//     (190-225, kernels.py:168-177).
+// REDUNDANT plans (302-317) stage every reference contiguously.
+// The slot pool holds real payloads: gc_dm_stage_bh copies the missing
+// buffers' node/bucket records into their slots (the reorganised staging
+// layout the member force kernel reads).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+
 #include "common.cuh"
+
+namespace gc {
+
+constexpr int DM_TPB = 256;
+constexpr int HALF_WARP = 16;  // memory.py:26
+
+__global__ void dm_fill_i32(int *p, int64_t n, int v)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ void dm_firstpos(int n, const int *__restrict__ ids, int *__restrict__ firstpos)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) atomicMin(&firstpos[ids[p]], p);
+}
+
+__global__ void dm_isfirst(int n, const int *__restrict__ ids, const int *__restrict__ firstpos,
+                           unsigned char *__restrict__ flag)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) flag[p] = firstpos[ids[p]] == p;
+}
+
+__global__ void dm_reset_firstpos(int n, const int *__restrict__ ids, int *__restrict__ firstpos)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) firstpos[ids[p]] = INT_MAX;
+}
+
+// residency lookup + pin of the distinct set
+__global__ void dm_lookup_pin(int nd, const int *__restrict__ distinct, const int *__restrict__ slot_of,
+                              double *__restrict__ last_use, int *__restrict__ pins, double now, int pin,
+                              unsigned char *__restrict__ miss)
+{
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= nd) return;
+    const int b = distinct[d];
+    const bool res = slot_of[b] >= 0;
+    if (res) last_use[b] = now;
+    miss[d] = !res;
+    if (pin) pins[b] += pin;  // distinct ids: no races
+}
+
+__global__ void dm_addpin(int nd, const int *__restrict__ distinct, int *__restrict__ pins)
+{
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d < nd) pins[distinct[d]] += 1;
+}
+
+__global__ void dm_unpin(int nd, const int *__restrict__ distinct, int *__restrict__ pins)
+{
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= nd) return;
+    const int b = distinct[d];
+    pins[b] = max(pins[b] - 1, 0);
+}
+
+// eviction candidates: resident and unpinned (memory.py:270-273)
+__global__ void dm_candidates(int nslots, const int *__restrict__ buf_of_slot, const int *__restrict__ pins,
+                              unsigned char *__restrict__ flag)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nslots) return;
+    const int b = buf_of_slot[s];
+    flag[s] = b >= 0 && pins[b] == 0;
+}
+
+// order-preserving uint64 key of a double
+__device__ __forceinline__ unsigned long long dkey(double x)
+{
+    const unsigned long long u = __double_as_longlong(x);
+    return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+__global__ void dm_time_keys(int n, const int *__restrict__ bufs, const double *__restrict__ last_use,
+                             unsigned long long *__restrict__ keys)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) keys[i] = dkey(last_use[bufs[i]]);
+}
+
+__global__ void dm_evict(int n, const int *__restrict__ victims, int *__restrict__ slot_of, int *__restrict__ buf_of_slot)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int b = victims[i];
+    const int s = slot_of[b];
+    slot_of[b] = -1;
+    buf_of_slot[s] = -1;
+}
+
+__global__ void dm_free_flags(int nslots, const int *__restrict__ buf_of_slot, unsigned char *__restrict__ flag)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < nslots) flag[s] = buf_of_slot[s] < 0;
+}
+
+__global__ void dm_alloc(int k, const int *__restrict__ missing, const int *__restrict__ free_slots,
+                         int *__restrict__ slot_of, int *__restrict__ buf_of_slot, double *__restrict__ last_use, double now)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= k) return;
+    const int b = missing[i], s = free_slots[i];
+    slot_of[b] = s;
+    buf_of_slot[s] = b;
+    last_use[b] = now;
+}
+
+__global__ void dm_addresses(int n, const int *__restrict__ ids, const int *__restrict__ slot_of, int *__restrict__ addr)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) addr[p] = slot_of[ids[p]];
+}
+
+// a position starts a run iff it opens a 16-lane group of its member or its
+// address is not previous + 1 (kernels.py:168-177)
+__global__ void dm_run_flags(int n, const int *__restrict__ addr, const int *__restrict__ member_of,
+                             const int *__restrict__ bounds, int *__restrict__ flag)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int off = p - bounds[member_of[p]];
+    flag[p] = (off % HALF_WARP == 0 || addr[p] != addr[p - 1] + 1) ? 1 : 0;
+}
+
+__global__ void dm_iota(int n, int *p)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = i;
+}
+
+}  // namespace gc
+
+using namespace gc;
+
+struct gc_dm {
+    gc_ctx *ctx = nullptr;
+    int64_t capacity = 0, slot_bytes = 0;
+    int mode = 2;  // 0 redundant, 1 reuse, 2 reuse_sorted (MemoryMode, memory.py:30-33)
+    int nslots = 0;
+    int64_t free_slots = 0;
+    int64_t universe = 0;
+    DBuf<int> slot_of, pins, firstpos, buf_of_slot;
+    DBuf<double> last_use;
+    // plan scratch / outputs
+    DBuf<int> ids, sorted_ids, bounds, member_of, distinct, missing, missing_sorted, cand, cand_s, cand_v,
+        free_list, addr, runflag, members_tx, iota_slots, nsel;
+    DBuf<unsigned char> flag;
+    DBuf<unsigned long long> tkeys, tkeys_s;
+    DBuf<float4> pool;  // staged payloads, slot_bytes per slot
+    // last plan (host copies)
+    std::vector<int64_t> h_transfer, h_addr, h_tx, h_bounds, h_evicted;
+    int64_t total_bytes = 0, indirection_bytes = 0;
+    bool indirect = true;
+};
+
+namespace {
+
+template <class F>
+void cub_call(gc_ctx *ctx, F &&f)
+{
+    size_t bytes = 0;
+    GC_CUDA(f(nullptr, bytes));
+    ctx->scratch.resize(bytes);
+    GC_CUDA(f(ctx->scratch.p, bytes));
+}
+
+int select_flagged(gc_dm *dm, const int *in, const unsigned char *flags, int *out, int n)
+{
+    gc_ctx *ctx = dm->ctx;
+    dm->nsel.resize(1);
+    cub_call(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceSelect::Flagged(t, b, in, flags, out, dm->nsel.p, n, ctx->stream);
+    });
+    int k = 0;
+    GC_CUDA(cudaMemcpyAsync(&k, dm->nsel.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    GC_CUDA(cudaStreamSynchronize(ctx->stream));
+    return k;
+}
+
+void ensure_universe(gc_dm *dm, int64_t maxid)
+{
+    if (maxid < dm->universe) return;
+    const int64_t nu = std::max<int64_t>(maxid + 1, dm->universe * 2);
+    cudaStream_t s = dm->ctx->stream;
+    auto grow_i = [&](DBuf<int> &b, int fill) {
+        DBuf<int> nb_;
+        nb_.resize(nu);
+        dm_fill_i32<<<grid_for(nu, DM_TPB), DM_TPB, 0, s>>>(nb_.p, nu, fill);
+        if (dm->universe) GC_CUDA(cudaMemcpyAsync(nb_.p, b.p, dm->universe * sizeof(int), cudaMemcpyDeviceToDevice, s));
+        std::swap(b.p, nb_.p);
+        std::swap(b.n, nb_.n);
+        std::swap(b.cap, nb_.cap);
+    };
+    grow_i(dm->slot_of, -1);
+    grow_i(dm->pins, 0);
+    grow_i(dm->firstpos, INT_MAX);
+    DBuf<double> lu;
+    lu.resize(nu);
+    GC_CUDA(cudaMemsetAsync(lu.p, 0, nu * sizeof(double), s));
+    if (dm->universe) GC_CUDA(cudaMemcpyAsync(lu.p, dm->last_use.p, dm->universe * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    std::swap(dm->last_use.p, lu.p);
+    std::swap(dm->last_use.n, lu.n);
+    std::swap(dm->last_use.cap, lu.cap);
+    GC_CUDA(cudaStreamSynchronize(s));
+    dm->universe = nu;
+}
+
+// upload a flat id list (int64 host -> int32 device), growing the universe
+int upload_ids(gc_dm *dm, const int64_t *ids, int64_t n, DBuf<int> &dst)
+{
+    GC_REQUIRE(n < INT_MAX, GC_E_VALUE, "batch too large");
+    std::vector<int> tmp(n);
+    int64_t mx = -1;
+    for (int64_t i = 0; i < n; ++i) {
+        GC_REQUIRE(ids[i] >= 0 && ids[i] < INT_MAX, GC_E_VALUE, "buffer ids must be non-negative int32");
+        tmp[i] = (int)ids[i];
+        mx = std::max(mx, ids[i]);
+    }
+    ensure_universe(dm, std::max<int64_t>(mx, 0));
+    dst.upload(tmp.data(), n, dm->ctx->stream);
+    return (int)n;
+}
+
+// first-seen-order distinct ids of dm->ids[0..n) into dm->distinct
+int dedup(gc_dm *dm, int n)
+{
+    cudaStream_t s = dm->ctx->stream;
+    if (n == 0) return 0;
+    dm->flag.resize(n);
+    dm->distinct.resize(n);
+    dm_firstpos<<<grid_for(n, DM_TPB), DM_TPB, 0, s>>>(n, dm->ids.p, dm->firstpos.p);
+    dm_isfirst<<<grid_for(n, DM_TPB), DM_TPB, 0, s>>>(n, dm->ids.p, dm->firstpos.p, dm->flag.p);
+    dm_reset_firstpos<<<grid_for(n, DM_TPB), DM_TPB, 0, s>>>(n, dm->ids.p, dm->firstpos.p);
+    check_launch("dm dedup");
+    return select_flagged(dm, dm->ids.p, dm->flag.p, dm->distinct.p, n);
+}
+
+// evict LRU unpinned buffers until `need` slots are free; returns true on
+// success.  Victims in eviction order are appended to dm->h_evicted.
+bool evict_needed(gc_dm *dm, int64_t need)
+{
+    dm->h_evicted.clear();
+    if (need <= 0) return true;
+    gc_ctx *ctx = dm->ctx;
+    cudaStream_t s = ctx->stream;
+    const int S = dm->nslots;
+    dm->flag.resize(S);
+    dm->cand.resize(S);
+    dm_candidates<<<grid_for(S, DM_TPB), DM_TPB, 0, s>>>(S, dm->buf_of_slot.p, dm->pins.p, dm->flag.p);
+    check_launch("dm_candidates");
+    const int c = select_flagged(dm, dm->buf_of_slot.p, dm->flag.p, dm->cand.p, S);
+    if (c > 0) {
+        // stable order by (last_use_time, buffer): sort by buffer, then stable by time
+        dm->cand_s.resize(c);
+        dm->cand_v.resize(c);
+        dm->tkeys.resize(c);
+        dm->tkeys_s.resize(c);
+        cub_call(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceRadixSort::SortKeys(t, b, dm->cand.p, dm->cand_s.p, c, 0, 32, s);
+        });
+        dm_time_keys<<<grid_for(c, DM_TPB), DM_TPB, 0, s>>>(c, dm->cand_s.p, dm->last_use.p, dm->tkeys.p);
+        cub_call(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, dm->tkeys.p, dm->tkeys_s.p, dm->cand_s.p, dm->cand_v.p, c, 0,
+                                                   64, s);
+        });
+    }
+    const int take = (int)std::min<int64_t>(need, c);
+    if (take > 0) {
+        dm_evict<<<grid_for(take, DM_TPB), DM_TPB, 0, s>>>(take, dm->cand_v.p, dm->slot_of.p, dm->buf_of_slot.p);
+        check_launch("dm_evict");
+        std::vector<int> v(take);
+        dm->cand_v.download(v.data(), take, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        dm->h_evicted.assign(v.begin(), v.end());
+        dm->free_slots += take;
+    }
+    return take >= need;
+}
+
+void member_transactions(gc_dm *dm, int P, int M, int mult)
+{
+    cudaStream_t s = dm->ctx->stream;
+    dm->h_tx.assign(M, 0);
+    if (P == 0) return;
+    dm->runflag.resize(P);
+    dm->members_tx.resize(M);
+    dm_run_flags<<<grid_for(P, DM_TPB), DM_TPB, 0, s>>>(P, dm->addr.p, dm->member_of.p, dm->bounds.p, dm->runflag.p);
+    check_launch("dm_run_flags");
+    cub_call(dm->ctx, [&](void *t, size_t &b) {
+        return cub::DeviceSegmentedReduce::Sum(t, b, dm->runflag.p, dm->members_tx.p, M, dm->bounds.p,
+                                               dm->bounds.p + 1, s);
+    });
+    std::vector<int> tx(M);
+    dm->members_tx.download(tx.data(), M, s);
+    GC_CUDA(cudaStreamSynchronize(s));
+    for (int m = 0; m < M; ++m) dm->h_tx[m] = (int64_t)tx[m] * mult;
+}
+
+}  // namespace
+
+extern "C" {
+
+gc_status gc_dm_create(gc_ctx *ctx, int64_t capacity_bytes, int64_t slot_bytes, int32_t mode, gc_dm **out)
+{
+    return guard([&] {
+        GC_REQUIRE(ctx && out, GC_E_VALUE, "null argument");
+        GC_REQUIRE(slot_bytes > 0 && capacity_bytes >= slot_bytes, GC_E_VALUE, "heap needs room for at least one slot");
+        GC_REQUIRE(mode >= 0 && mode <= 2, GC_E_VALUE, "unknown memory mode");
+        GC_REQUIRE(capacity_bytes / slot_bytes < INT_MAX, GC_E_VALUE, "too many slots");
+        gc_dm *dm = new gc_dm();
+        dm->ctx = ctx;
+        dm->capacity = capacity_bytes;
+        dm->slot_bytes = slot_bytes;
+        dm->mode = mode;
+        dm->nslots = (int)(capacity_bytes / slot_bytes);
+        dm->free_slots = dm->nslots;
+        dm->buf_of_slot.resize(dm->nslots);
+        dm_fill_i32<<<grid_for(dm->nslots, DM_TPB), DM_TPB, 0, ctx->stream>>>(dm->buf_of_slot.p, dm->nslots, -1);
+        ensure_universe(dm, 1023);
+        *out = dm;
+    });
+}
+
+gc_status gc_dm_destroy(gc_dm *dm)
+{
+    return guard([&] { delete dm; });
+}
+
+gc_status gc_dm_build_plan(gc_dm *dm, const int64_t *ids, const int64_t *bounds, int32_t n_members, double now,
+                           int64_t *n_transfer, int64_t *n_positions)
+{
+    return guard([&] {
+        GC_REQUIRE(dm && bounds && n_members >= 0, GC_E_VALUE, "bad argument");
+        cudaStream_t s = dm->ctx->stream;
+        const int64_t P64 = bounds[n_members];
+        const int P = upload_ids(dm, ids, P64, dm->ids);
+        const int M = n_members;
+        std::vector<int> hb(M + 1), hm(P);
+        for (int m = 0; m <= M; ++m) hb[m] = (int)bounds[m];
+        for (int m = 0; m < M; ++m)
+            for (int p = hb[m]; p < hb[m + 1]; ++p) hm[p] = m;
+        dm->bounds.upload(hb.data(), M + 1, s);
+        dm->member_of.upload(hm.data(), P, s);
+        dm->h_bounds.assign(bounds, bounds + M + 1);
+        dm->addr.resize(P);
+        if (dm->mode == 0) {  // REDUNDANT (memory.py:302-317)
+            GC_REQUIRE(P <= dm->nslots, GC_E_CAPACITY,
+                       "staging " + std::to_string(P) + " buffers exceeds " + std::to_string(dm->nslots) + " slots");
+            dm_iota<<<grid_for(P, DM_TPB), DM_TPB, 0, s>>>(P, dm->addr.p);
+            dm->h_transfer.assign(ids, ids + P);
+            dm->h_addr.resize(P);
+            for (int p = 0; p < P; ++p) dm->h_addr[p] = p;
+            dm->total_bytes = (int64_t)P * dm->slot_bytes;
+            dm->indirection_bytes = 0;
+            dm->indirect = false;
+            member_transactions(dm, P, M, 1);
+        } else {  // REUSE / REUSE_SORTED (memory.py:319-360)
+            const int D = dedup(dm, P);
+            dm->missing.resize(std::max(D, 1));
+            dm->flag.resize(std::max(D, 1));
+            if (D) {
+                dm_lookup_pin<<<grid_for(D, DM_TPB), DM_TPB, 0, s>>>(D, dm->distinct.p, dm->slot_of.p, dm->last_use.p,
+                                                                     dm->pins.p, now, 1, dm->flag.p);
+                check_launch("dm_lookup_pin");
+            }
+            int K = D ? select_flagged(dm, dm->distinct.p, dm->flag.p, dm->missing.p, D) : 0;
+            int *miss = dm->missing.p;
+            if (dm->mode == 2 && K > 1) {
+                dm->missing_sorted.resize(K);
+                cub_call(dm->ctx, [&](void *t, size_t &b) {
+                    return cub::DeviceRadixSort::SortKeys(t, b, dm->missing.p, dm->missing_sorted.p, K, 0, 32, s);
+                });
+                miss = dm->missing_sorted.p;
+            }
+            // eviction (memory.py:333-337): on failure unpin the batch and raise
+            const int64_t needed = (int64_t)K * dm->slot_bytes;
+            bool ok = needed <= dm->capacity;
+            std::string why = "request of " + std::to_string(needed) + " bytes exceeds capacity " +
+                              std::to_string(dm->capacity);
+            if (ok && dm->free_slots < K) {
+                ok = evict_needed(dm, K - dm->free_slots);
+                if (!ok)
+                    why = "pinned buffers exhaust capacity: need " + std::to_string(needed) + ", freeable " +
+                          std::to_string(dm->free_slots * dm->slot_bytes);
+            }
+            if (!ok) {
+                if (D) dm_unpin<<<grid_for(D, DM_TPB), DM_TPB, 0, s>>>(D, dm->distinct.p, dm->pins.p);
+                GC_CUDA(cudaStreamSynchronize(s));
+                throw Error{GC_E_CAPACITY, why};
+            }
+            if (K) {  // k-th missing buffer <- k-th smallest free slot
+                dm->flag.resize(dm->nslots);
+                dm->free_list.resize(dm->nslots);
+                dm->iota_slots.resize(dm->nslots);
+                dm_iota<<<grid_for(dm->nslots, DM_TPB), DM_TPB, 0, s>>>(dm->nslots, dm->iota_slots.p);
+                dm_free_flags<<<grid_for(dm->nslots, DM_TPB), DM_TPB, 0, s>>>(dm->nslots, dm->buf_of_slot.p,
+                                                                              dm->flag.p);
+                const int nf = select_flagged(dm, dm->iota_slots.p, dm->flag.p, dm->free_list.p, dm->nslots);
+                GC_REQUIRE(nf >= K, GC_E_CAPACITY, "device heap full");
+                dm_alloc<<<grid_for(K, DM_TPB), DM_TPB, 0, s>>>(K, miss, dm->free_list.p, dm->slot_of.p,
+                                                                 dm->buf_of_slot.p, dm->last_use.p, now);
+                check_launch("dm_alloc");
+                dm->free_slots -= K;
+            }
+            // per-member address maps (sorted per member in REUSE_SORTED)
+            const int *src = dm->ids.p;
+            if (dm->mode == 2 && P) {
+                dm->sorted_ids.resize(P);
+                cub_call(dm->ctx, [&](void *t, size_t &b) {
+                    return cub::DeviceSegmentedSort::SortKeys(t, b, dm->ids.p, dm->sorted_ids.p, P, M, dm->bounds.p,
+                                                              dm->bounds.p + 1, s);
+                });
+                src = dm->sorted_ids.p;
+            }
+            if (P) dm_addresses<<<grid_for(P, DM_TPB), DM_TPB, 0, s>>>(P, src, dm->slot_of.p, dm->addr.p);
+            check_launch("dm_addresses");
+            std::vector<int> a(P), t(K);
+            dm->addr.download(a.data(), P, s);
+            if (K) GC_CUDA(cudaMemcpyAsync(t.data(), miss, K * sizeof(int), cudaMemcpyDeviceToHost, s));
+            GC_CUDA(cudaStreamSynchronize(s));
+            dm->h_addr.assign(a.begin(), a.end());
+            dm->h_transfer.assign(t.begin(), t.end());
+            dm->total_bytes = (int64_t)K * dm->slot_bytes;
+            dm->indirection_bytes = 4 * (int64_t)P;  // ADDRESS_BYTES (memory.py:27)
+            dm->indirect = true;
+            member_transactions(dm, P, M, 2);
+        }
+        *n_transfer = (int64_t)dm->h_transfer.size();
+        *n_positions = P;
+    });
+}
+
+gc_status gc_dm_plan_get(gc_dm *dm, int64_t *to_transfer, int64_t *addresses, int64_t *transactions,
+                         int64_t out_bytes[3])
+{
+    return guard([&] {
+        GC_REQUIRE(dm, GC_E_VALUE, "null argument");
+        if (to_transfer) std::copy(dm->h_transfer.begin(), dm->h_transfer.end(), to_transfer);
+        if (addresses) std::copy(dm->h_addr.begin(), dm->h_addr.end(), addresses);
+        if (transactions) std::copy(dm->h_tx.begin(), dm->h_tx.end(), transactions);
+        if (out_bytes) {
+            out_bytes[0] = dm->total_bytes;
+            out_bytes[1] = dm->indirection_bytes;
+            out_bytes[2] = dm->indirect ? 1 : 0;
+        }
+    });
+}
+
+gc_status gc_dm_pin(gc_dm *dm, const int64_t *ids, int64_t n, int32_t delta)
+{
+    return guard([&] {
+        GC_REQUIRE(dm && (delta == 1 || delta == -1), GC_E_VALUE, "bad argument");
+        const int P = upload_ids(dm, ids, n, dm->ids);
+        const int D = dedup(dm, P);  // set(buffers) (memory.py:241, 245)
+        cudaStream_t s = dm->ctx->stream;
+        if (D) {
+            if (delta > 0) dm_addpin<<<grid_for(D, DM_TPB), DM_TPB, 0, s>>>(D, dm->distinct.p, dm->pins.p);
+            else dm_unpin<<<grid_for(D, DM_TPB), DM_TPB, 0, s>>>(D, dm->distinct.p, dm->pins.p);
+            check_launch("dm pin");
+        }
+        GC_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+gc_status gc_dm_release(gc_dm *dm, const int64_t *ids, int64_t n)
+{
+    return guard([&] {
+        GC_REQUIRE(dm, GC_E_VALUE, "null argument");
+        if (dm->mode == 0) return;  // REDUNDANT: no pins (memory.py:363-364)
+        const int P = upload_ids(dm, ids, n, dm->ids);
+        const int D = dedup(dm, P);
+        if (D) dm_unpin<<<grid_for(D, DM_TPB), DM_TPB, 0, dm->ctx->stream>>>(D, dm->distinct.p, dm->pins.p);
+        GC_CUDA(cudaStreamSynchronize(dm->ctx->stream));
+    });
+}
+
+gc_status gc_dm_evict(gc_dm *dm, int64_t needed_bytes, int64_t *evicted, int64_t *n_evicted)
+{
+    return guard([&] {
+        GC_REQUIRE(dm && n_evicted, GC_E_VALUE, "null argument");
+        *n_evicted = 0;
+        GC_REQUIRE(needed_bytes <= dm->capacity, GC_E_CAPACITY,
+                   "request of " + std::to_string(needed_bytes) + " bytes exceeds capacity " +
+                       std::to_string(dm->capacity));
+        const int64_t freeb = dm->free_slots * dm->slot_bytes;
+        if (freeb >= needed_bytes) {
+            dm->h_evicted.clear();
+            return;
+        }
+        const int64_t need = (needed_bytes - freeb + dm->slot_bytes - 1) / dm->slot_bytes;
+        const bool ok = evict_needed(dm, need);
+        *n_evicted = (int64_t)dm->h_evicted.size();
+        if (evicted) std::copy(dm->h_evicted.begin(), dm->h_evicted.end(), evicted);
+        GC_REQUIRE(ok, GC_E_CAPACITY,
+                   "pinned buffers exhaust capacity: need " + std::to_string(needed_bytes) + ", freeable " +
+                       std::to_string(dm->free_slots * dm->slot_bytes));
+    });
+}
+
+gc_status gc_dm_state(gc_dm *dm, int64_t out[4])
+{
+    return guard([&] {
+        out[0] = dm->nslots;
+        out[1] = dm->free_slots;
+        out[2] = dm->nslots - dm->free_slots;
+        out[3] = dm->universe;
+    });
+}
+
+gc_status gc_dm_table(gc_dm *dm, int64_t *bufs, int64_t *slots, double *last_use, int64_t *pins)
+{
+    return guard([&] {
+        cudaStream_t s = dm->ctx->stream;
+        std::vector<int> so(dm->universe), pn(dm->universe);
+        std::vector<double> lu(dm->universe);
+        dm->slot_of.download(so.data(), dm->universe, s);
+        dm->pins.download(pn.data(), dm->universe, s);
+        dm->last_use.download(lu.data(), dm->universe, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        int64_t k = 0;
+        for (int64_t b = 0; b < dm->universe; ++b) {
+            if (so[b] < 0) continue;
+            if (bufs) bufs[k] = b;
+            if (slots) slots[k] = so[b];
+            if (last_use) last_use[k] = lu[b];
+            if (pins) pins[k] = pn[b];
+            ++k;
+        }
+    });
+}
+
+gc_status gc_dm_lookup(gc_dm *dm, const int64_t *ids, int64_t n, double now, int8_t *resident)
+{
+    return guard([&] {
+        const int P = upload_ids(dm, ids, n, dm->ids);
+        if (!P) return;
+        cudaStream_t s = dm->ctx->stream;
+        dm->flag.resize(P);
+        // every position (not only distinct): resident entries refresh last_use (memory.py:86-92)
+        dm_lookup_pin<<<grid_for(P, DM_TPB), DM_TPB, 0, s>>>(P, dm->ids.p, dm->slot_of.p, dm->last_use.p, dm->pins.p,
+                                                             now, 0, dm->flag.p);
+        std::vector<unsigned char> f(P);
+        dm->flag.download(f.data(), P, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        for (int p = 0; p < P; ++p) resident[p] = f[p] ? 0 : 1;
+    });
+}
+
+}  // extern "C"
