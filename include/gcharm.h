@@ -164,6 +164,26 @@ gc_status gc_dm_state(gc_dm *dm, int64_t out[4]);
 /* resident table sorted by buffer id (ChareTable, memory.py:50-75) */
 gc_status gc_dm_table(gc_dm *dm, int64_t *bufs, int64_t *slots, double *last_use, int64_t *pins);
 
+/* ---- cell-pair MD (hr/workloads/md.py; 3-D Lennard-Jones extension) --------
+ * law 0: soft repulsion, params = {cutoff, stiffness, -} (kernels.py:105-161);
+ * law 1: Lennard-Jones, params = {rc, epsilon, sigma} (no reference; oracle/).
+ * dims = cells per dimension (2-D: {rows, cols, 1}); cell_of (optional) is the
+ * caller's initial patch assignment (PatchGrid.patch_of, md.py:32).  Periodic
+ * grids need >= 3 cells per dimension. */
+gc_status gc_md_create(gc_ctx *ctx, gc_md **out);
+gc_status gc_md_destroy(gc_md *md);
+gc_status gc_md_set_system(gc_md *md, int64_t n, int32_t dim, const double *pos, const double *vel,
+                           const int64_t *cell_of, const int64_t dims[3], double cell_size, int32_t periodic,
+                           int32_t law, const double params[3]);
+/* compute_forces (md.py:121-163) on the current state: forces (n x dim) and,
+ * for LJ, per-atom energy (half of each pair energy); either may be NULL */
+gc_status gc_md_forces(gc_md *md, double *forces, double *energy);
+/* `steps` iterations of md_step (md.py:166-190) on the device (CUDA graph) */
+gc_status gc_md_run(gc_md *md, int32_t steps, double dt);
+gc_status gc_md_get_state(gc_md *md, double *pos, double *vel, int64_t *cell_of);
+/* device time (ms, CUDA events) of the last gc_md_forces or gc_md_run */
+gc_status gc_md_elapsed(gc_md *md, double *ms);
+
 #ifdef __cplusplus
 }
 #endif

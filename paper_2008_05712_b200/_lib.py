@@ -65,6 +65,14 @@ SIGNATURES = {
     "gc_dm_lookup": [vp, i64p, C.c_int64, C.c_double, i8p],
     "gc_dm_state": [vp, i64p],
     "gc_dm_table": [vp, i64p, i64p, f64p, i64p],
+    "gc_md_create": [vp, C.POINTER(vp)],
+    "gc_md_destroy": [vp],
+    "gc_md_set_system": [vp, C.c_int64, C.c_int32, f64p, f64p, i64p, i64p, C.c_double, C.c_int32, C.c_int32,
+                         f64p],
+    "gc_md_forces": [vp, f64p, f64p],
+    "gc_md_run": [vp, C.c_int32, C.c_double],
+    "gc_md_get_state": [vp, f64p, f64p, i64p],
+    "gc_md_elapsed": [vp, f64p],
 }
 _RESTYPE = {"gc_ctx_stream": vp, "gc_last_error": C.c_char_p, "gc_version": C.c_char_p}
 

@@ -1,12 +1,537 @@
-// md.cu -- molecular-dynamics cell-pair path (see below).
+// md.cu -- cell-pair molecular dynamics on sm_100a: the reference's 2-D
+// soft-repulsion patch MD (hr/workloads/md.py) and the 3-D cutoff
+// Lennard-Jones workload of the north star (no reference implementation;
+// restated in oracle/gcharm_oracle.c).
+//
+// Work decomposition.  The reference enumerates, per patch, the self pair and
+// the half-shell neighbours (md.py:21, 55-73, 138-162) and scatters Newton's
+// third law.  Here one thread owns one atom and visits the FULL shell (9
+// cells in 2-D, 27 in 3-D), so no atomics or scatter are needed.  Every pair
+// is evaluated in the reference's canonical orientation -- the atom of the
+// half-shell owner first, its partner shifted by the periodic image
+// (md.py:139-160) -- so the float64 separation and r^2 bits, and therefore
+// every cutoff decision, equal the reference's; the partner side takes the
+// negated force.  Self-cell pairs use ascending original index (i < j,
+// md_self_forces kernels.py:142-143).
+//
+// Per step (md_run, captured into one CUDA graph): cell assignment + counting
+// sort (atomics, then a per-cell sort by original id so the result is
+// deterministic), the force kernel, and the integrator of md_step
+// (md.py:166-190).
+#include <cub/cub.cuh>
+
+#include <cmath>
 #include <cstring>
 
 #include "common.cuh"
 
 namespace gc {
+
+constexpr int MD_TPB = 128;
+
+enum { LAW_SOFT = 0, LAW_LJ = 1 };
+
+struct MDParams {
+    int dim;
+    int nx, ny, nz;  // cells per dimension (reference: rows, cols, 1)
+    double cell;  // cell (patch) side
+    double bx, by, bz;  // box
+    int periodic;
+    double cutoff, c2;
+    double stiffness;  // soft law
+    double eps, sig2;  // LJ law
+};
+
+__device__ __forceinline__ bool md_forward(int dx, int dy, int dz)
+{
+    // half shell (md.py:21 in 2-D; its 3-D analogue in the oracle)
+    return dx > 0 || (dx == 0 && dy > 0) || (dx == 0 && dy == 0 && dz > 0);
+}
+
+// numpy floor_divide / remainder for floats (npy_divmod)
+__device__ __forceinline__ double np_floordiv(double a, double b)
+{
+    const double mod = fmod(a, b);
+    double div = __ddiv_rn(__dsub_rn(a, mod), b);
+    if (mod != 0.0 && ((b < 0) != (mod < 0))) div = __dsub_rn(div, 1.0);
+    double fd;
+    if (div != 0.0) {
+        fd = floor(div);
+        if (__dsub_rn(div, fd) > 0.5) fd = __dadd_rn(fd, 1.0);
+    } else {
+        fd = copysign(0.0, __ddiv_rn(a, b));
+    }
+    return fd;
+}
+
+__device__ __forceinline__ double np_remainder(double a, double b)
+{
+    double mod = fmod(a, b);
+    if (mod != 0.0) {
+        if ((b < 0) != (mod < 0)) mod = __dadd_rn(mod, b);
+    } else {
+        mod = copysign(0.0, b);
+    }
+    return mod;
+}
+
+template <int LAW, int DIM>
+__global__ void __launch_bounds__(MD_TPB)
+md_force_kernel(int n, const double4 *__restrict__ spos, const int *__restrict__ cell_start,
+                const int *__restrict__ scell, const MDParams P, double4 *__restrict__ out)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double4 a = spos[k];
+    const long long ia = __double_as_longlong(a.w);
+    const int c = scell[k];
+    const int cz = c % P.nz, cy = (c / P.nz) % P.ny, cx = c / (P.nz * P.ny);
+    double fx = 0.0, fy = 0.0, fz = 0.0, en = 0.0;
+    constexpr int RZ = DIM == 3 ? 1 : 0;
+    for (int ox = -1; ox <= 1; ++ox)
+        for (int oy = -1; oy <= 1; ++oy)
+            for (int oz = -RZ; oz <= RZ; ++oz) {
+                int qx = cx + ox, qy = cy + oy, qz = cz + oz;
+                double sx = 0.0, sy = 0.0, sz = 0.0;  // image shift of the neighbour cell
+                if (qx < 0 || qx >= P.nx) {
+                    if (!P.periodic) continue;
+                    sx = qx < 0 ? -P.bx : P.bx;
+                    qx = qx < 0 ? qx + P.nx : qx - P.nx;
+                }
+                if (qy < 0 || qy >= P.ny) {
+                    if (!P.periodic) continue;
+                    sy = qy < 0 ? -P.by : P.by;
+                    qy = qy < 0 ? qy + P.ny : qy - P.ny;
+                }
+                if (qz < 0 || qz >= P.nz) {
+                    if (!P.periodic) continue;
+                    sz = qz < 0 ? -P.bz : P.bz;
+                    qz = qz < 0 ? qz + P.nz : qz - P.nz;
+                }
+                const int q = (qx * P.ny + qy) * P.nz + qz;
+                const bool self = ox == 0 && oy == 0 && oz == 0;
+                const bool fwd_cell = md_forward(ox, oy, oz);
+                for (int j = cell_start[q]; j < cell_start[q + 1]; ++j) {
+                    if (j == k) continue;
+                    const double4 b = spos[j];
+                    bool fwd = fwd_cell;
+                    if (self) fwd = ia < __double_as_longlong(b.w);
+                    // canonical orientation: owner atom minus (partner + shift)
+                    double d0, d1, d2 = 0.0;
+                    if (fwd) {
+                        d0 = __dsub_rn(a.x, __dadd_rn(b.x, sx));
+                        d1 = __dsub_rn(a.y, __dadd_rn(b.y, sy));
+                        if (DIM == 3) d2 = __dsub_rn(a.z, __dadd_rn(b.z, sz));
+                    } else {
+                        d0 = __dsub_rn(b.x, __dadd_rn(a.x, -sx));
+                        d1 = __dsub_rn(b.y, __dadd_rn(a.y, -sy));
+                        if (DIM == 3) d2 = __dsub_rn(b.z, __dadd_rn(a.z, -sz));
+                    }
+                    double r2 = __dmul_rn(d0, d0);
+                    r2 = __dadd_rn(r2, __dmul_rn(d1, d1));
+                    if (DIM == 3) r2 = __dadd_rn(r2, __dmul_rn(d2, d2));
+                    if (r2 >= P.c2 || r2 < 1e-12) continue;
+                    double mag;
+                    if (LAW == LAW_SOFT) {
+                        const double r = __dsqrt_rn(r2);
+                        mag = __ddiv_rn(__dmul_rn(P.stiffness, __dsub_rn(P.cutoff, r)), r);
+                    } else {
+                        const double s2 = __ddiv_rn(P.sig2, r2);
+                        const double s6 = __dmul_rn(__dmul_rn(s2, s2), s2);
+                        const double s12 = __dmul_rn(s6, s6);
+                        mag = __ddiv_rn(__dmul_rn(__dmul_rn(24.0, P.eps), __dsub_rn(__dmul_rn(2.0, s12), s6)), r2);
+                        en = __dadd_rn(en, __dmul_rn(0.5, __dmul_rn(__dmul_rn(4.0, P.eps), __dsub_rn(s12, s6))));
+                    }
+                    const double g0 = __dmul_rn(d0, mag), g1 = __dmul_rn(d1, mag);
+                    const double g2 = DIM == 3 ? __dmul_rn(d2, mag) : 0.0;
+                    if (fwd) {
+                        fx += g0;
+                        fy += g1;
+                        fz += g2;
+                    } else {
+                        fx -= g0;
+                        fy -= g1;
+                        fz -= g2;
+                    }
+                }
+            }
+    out[ia] = make_double4(fx, fy, fz, en);
+}
+
+// cell of every atom: numpy floor_divide for the 2-D patches (md.py:187-189),
+// floor(x / cell) for the 3-D cells; clamped to the grid
+__global__ void md_assign_kernel(int n, const double4 *__restrict__ pos, const MDParams P, int use_npy,
+                                 int *__restrict__ cell_of, int *__restrict__ count)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double4 p = pos[i];
+    int c3[3];
+    const double xs[3] = {p.x, p.y, p.z};
+    const int dims[3] = {P.nx, P.ny, P.nz};
+    for (int k = 0; k < 3; ++k) {
+        if (k >= P.dim) {
+            c3[k] = 0;
+            continue;
+        }
+        const double f = use_npy ? np_floordiv(xs[k], P.cell) : floor(__ddiv_rn(xs[k], P.cell));
+        long long ck = (long long)f;
+        if (ck > dims[k] - 1) ck = dims[k] - 1;
+        if (ck < 0) ck = 0;
+        c3[k] = (int)ck;
+    }
+    const int c = (c3[0] * P.ny + c3[1]) * P.nz + c3[2];
+    cell_of[i] = c;
+    atomicAdd(&count[c], 1);
+}
+
+__global__ void md_count_kernel(int n, const int *__restrict__ cell_of, int *__restrict__ count)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) atomicAdd(&count[cell_of[i]], 1);
+}
+
+__global__ void md_scatter_kernel(int n, const double4 *__restrict__ pos, const int *__restrict__ cell_of,
+                                  int *__restrict__ cursor, int *__restrict__ perm)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    perm[atomicAdd(&cursor[cell_of[i]], 1)] = i;
+}
+
+// deterministic order inside each cell (ascending original id), then gather
+__global__ void md_cellsort_kernel(int ncell, const int *__restrict__ cell_start, int *__restrict__ perm)
+{
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncell) return;
+    const int s = cell_start[c], e = cell_start[c + 1];
+    for (int i = s + 1; i < e; ++i) {
+        const int v = perm[i];
+        int j = i - 1;
+        while (j >= s && perm[j] > v) {
+            perm[j + 1] = perm[j];
+            --j;
+        }
+        perm[j + 1] = v;
+    }
+}
+
+__global__ void md_gather_kernel(int n, const int *__restrict__ perm, const double4 *__restrict__ pos,
+                                 const int *__restrict__ cell_of, double4 *__restrict__ spos, int *__restrict__ scell)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int i = perm[k];
+    double4 p = pos[i];
+    p.w = __longlong_as_double((long long)i);
+    spos[k] = p;
+    scell[k] = cell_of[i];
+}
+
+// md_step integrator (md.py:171-189): v += F dt (unit mass); x += v dt; then
+// periodic wrap (np.remainder) or reflecting walls + clip to hi - 1e-12
+__global__ void md_integrate_kernel(int n, double4 *__restrict__ pos, double4 *__restrict__ vel,
+                                    const double4 *__restrict__ force, const MDParams P, double dt)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double x[3] = {pos[i].x, pos[i].y, pos[i].z};
+    double v[3] = {vel[i].x, vel[i].y, vel[i].z};
+    const double f[3] = {force[i].x, force[i].y, force[i].z};
+    const double hi[3] = {P.bx, P.by, P.bz};
+    for (int k = 0; k < P.dim; ++k) {
+        v[k] = __dadd_rn(v[k], __dmul_rn(f[k], dt));
+        x[k] = __dadd_rn(x[k], __dmul_rn(v[k], dt));
+    }
+    for (int k = 0; k < P.dim; ++k) {
+        if (P.periodic) {
+            x[k] = np_remainder(x[k], hi[k]);
+        } else {
+            if (x[k] < 0.0) {
+                x[k] = -x[k];
+                v[k] = -v[k];
+            }
+            if (x[k] > hi[k]) {
+                x[k] = __dsub_rn(__dmul_rn(2.0, hi[k]), x[k]);
+                v[k] = -v[k];
+            }
+            x[k] = fmin(fmax(x[k], 0.0), __dsub_rn(hi[k], 1e-12));
+        }
+    }
+    pos[i] = make_double4(x[0], x[1], x[2], 0.0);
+    vel[i] = make_double4(v[0], v[1], v[2], 0.0);
+}
+
+}  // namespace gc
+
+using namespace gc;
+
+struct gc_md {
+    gc_ctx *ctx = nullptr;
+    MDParams P{};
+    int law = LAW_SOFT;
+    int n = 0, ncell = 0;
+    int use_npy = 0;  // reference 2-D patches use numpy floor_divide
+    DBuf<double4> pos, vel, spos, force;
+    DBuf<int> cell_of, scell, count, cell_start, cursor, perm;
+    cudaGraphExec_t graph = nullptr;
+    int graph_steps = 0;
+    double graph_dt = 0.0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ~gc_md()
+    {
+        if (graph) cudaGraphExecDestroy(graph);
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+    }
+};
+
+namespace {
+
+void md_sort(gc_md *md, bool assign)
+{
+    cudaStream_t s = md->ctx->stream;
+    const int n = md->n, nc = md->ncell;
+    GC_CUDA(cudaMemsetAsync(md->count.p, 0, sizeof(int) * (nc + 1), s));
+    if (assign)
+        md_assign_kernel<<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->pos.p, md->P, md->use_npy, md->cell_of.p,
+                                                                md->count.p);
+    else
+        md_count_kernel<<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->cell_of.p, md->count.p);
+    size_t bytes = 0;
+    GC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, md->count.p, md->cell_start.p, nc + 1, s));
+    md->ctx->scratch.resize(bytes);
+    GC_CUDA(cub::DeviceScan::ExclusiveSum(md->ctx->scratch.p, bytes, md->count.p, md->cell_start.p, nc + 1, s));
+    GC_CUDA(cudaMemcpyAsync(md->cursor.p, md->cell_start.p, sizeof(int) * nc, cudaMemcpyDeviceToDevice, s));
+    md_scatter_kernel<<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->pos.p, md->cell_of.p, md->cursor.p, md->perm.p);
+    md_cellsort_kernel<<<grid_for(nc, MD_TPB), MD_TPB, 0, s>>>(nc, md->cell_start.p, md->perm.p);
+    md_gather_kernel<<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->perm.p, md->pos.p, md->cell_of.p, md->spos.p,
+                                                            md->scell.p);
+    check_launch("md sort");
+}
+
+void md_forces(gc_md *md)
+{
+    cudaStream_t s = md->ctx->stream;
+    const int n = md->n;
+    if (md->law == LAW_LJ) {
+        if (md->P.dim == 3)
+            md_force_kernel<LAW_LJ, 3><<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->spos.p, md->cell_start.p,
+                                                                              md->scell.p, md->P, md->force.p);
+        else
+            md_force_kernel<LAW_LJ, 2><<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->spos.p, md->cell_start.p,
+                                                                              md->scell.p, md->P, md->force.p);
+    } else {
+        if (md->P.dim == 3)
+            md_force_kernel<LAW_SOFT, 3><<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->spos.p, md->cell_start.p,
+                                                                                md->scell.p, md->P, md->force.p);
+        else
+            md_force_kernel<LAW_SOFT, 2><<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->spos.p, md->cell_start.p,
+                                                                                md->scell.p, md->P, md->force.p);
+    }
+    check_launch("md_force_kernel");
+}
+
+void md_step_once(gc_md *md, double dt)
+{
+    md_sort(md, true);
+    md_forces(md);
+    md_integrate_kernel<<<grid_for(md->n, MD_TPB), MD_TPB, 0, md->ctx->stream>>>(md->n, md->pos.p, md->vel.p,
+                                                                                  md->force.p, md->P, dt);
+    check_launch("md_integrate_kernel");
+}
+
+}  // namespace
+
+extern "C" {
+
+gc_status gc_md_create(gc_ctx *ctx, gc_md **out)
+{
+    return guard([&] {
+        GC_REQUIRE(ctx && out, GC_E_VALUE, "null argument");
+        gc_md *md = new gc_md();
+        md->ctx = ctx;
+        GC_CUDA(cudaEventCreate(&md->e0));
+        GC_CUDA(cudaEventCreate(&md->e1));
+        *out = md;
+    });
+}
+
+gc_status gc_md_destroy(gc_md *md)
+{
+    return guard([&] { delete md; });
+}
+
+gc_status gc_md_set_system(gc_md *md, int64_t n, int32_t dim, const double *pos, const double *vel,
+                           const int64_t *cell_of, const int64_t dims[3], double cell_size, int32_t periodic,
+                           int32_t law, const double params[3])
+{
+    return guard([&] {
+        GC_REQUIRE(md && pos && n >= 0 && n < (1ll << 31), GC_E_VALUE, "bad argument");
+        GC_REQUIRE(dim == 2 || dim == 3, GC_E_VALUE, "dim must be 2 or 3");
+        GC_REQUIRE(law == LAW_SOFT || law == LAW_LJ, GC_E_VALUE, "unknown force law");
+        GC_REQUIRE(dims[0] >= 1 && dims[1] >= 1 && dims[2] >= 1, GC_E_VALUE, "bad grid");
+        GC_REQUIRE(dim == 3 || dims[2] == 1, GC_E_VALUE, "2-D grids have one layer");
+        if (periodic)
+            for (int k = 0; k < dim; ++k)
+                GC_REQUIRE(dims[k] >= 3, GC_E_VALUE, "periodic cell grids need >= 3 cells per dimension");
+        GC_REQUIRE(cell_size >= params[0], GC_E_VALUE, "patch size must cover the cutoff distance");
+        MDParams &P = md->P;
+        P.dim = dim;
+        P.nx = (int)dims[0];
+        P.ny = (int)dims[1];
+        P.nz = (int)dims[2];
+        P.cell = cell_size;
+        P.bx = dims[0] * cell_size;
+        P.by = dims[1] * cell_size;
+        P.bz = dim == 3 ? dims[2] * cell_size : 0.0;
+        P.periodic = periodic;
+        P.cutoff = params[0];
+        P.c2 = params[0] * params[0];
+        P.stiffness = params[1];
+        P.eps = params[1];
+        P.sig2 = params[2] * params[2];
+        md->law = law;
+        md->use_npy = law == LAW_SOFT;
+        md->n = (int)n;
+        md->ncell = P.nx * P.ny * P.nz;
+        std::vector<double4> hp(n), hv(n);
+        for (int64_t i = 0; i < n; ++i) {
+            hp[i] = make_double4(pos[i * dim], pos[i * dim + 1], dim == 3 ? pos[i * dim + 2] : 0.0, 0.0);
+            hv[i] = vel ? make_double4(vel[i * dim], vel[i * dim + 1], dim == 3 ? vel[i * dim + 2] : 0.0, 0.0)
+                        : make_double4(0, 0, 0, 0);
+        }
+        cudaStream_t s = md->ctx->stream;
+        md->pos.upload(hp.data(), n, s);
+        md->vel.upload(hv.data(), n, s);
+        md->spos.resize(n);
+        md->force.resize(n);
+        md->cell_of.resize(n);
+        md->scell.resize(n);
+        md->perm.resize(n);
+        md->count.resize(md->ncell + 1);
+        md->cell_start.resize(md->ncell + 1);
+        md->cursor.resize(md->ncell + 1);
+        if (cell_of) {  // the caller's patch assignment (md.py PatchGrid.patch_of)
+            std::vector<int> c(n);
+            for (int64_t i = 0; i < n; ++i) {
+                GC_REQUIRE(cell_of[i] >= 0 && cell_of[i] < md->ncell, GC_E_VALUE, "cell id out of range");
+                c[i] = (int)cell_of[i];
+            }
+            md->cell_of.upload(c.data(), n, s);
+            md_sort(md, false);
+        } else {
+            md_sort(md, true);
+        }
+        if (md->graph) {
+            cudaGraphExecDestroy(md->graph);
+            md->graph = nullptr;
+        }
+        GC_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+gc_status gc_md_forces(gc_md *md, double *forces, double *energy)
+{
+    return guard([&] {
+        GC_REQUIRE(md && md->n > 0, GC_E_STATE, "no system set");
+        cudaStream_t s = md->ctx->stream;
+        GC_CUDA(cudaEventRecord(md->e0, s));
+        md_forces(md);
+        GC_CUDA(cudaEventRecord(md->e1, s));
+        std::vector<double4> f(md->n);
+        md->force.download(f.data(), md->n, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        const int d = md->P.dim;
+        for (int i = 0; i < md->n; ++i) {
+            if (forces) {
+                forces[i * d] = f[i].x;
+                forces[i * d + 1] = f[i].y;
+                if (d == 3) forces[i * d + 2] = f[i].z;
+            }
+            if (energy) energy[i] = f[i].w;
+        }
+    });
+}
+
+// `steps` md_step iterations on the device (one CUDA graph per step count)
+gc_status gc_md_run(gc_md *md, int32_t steps, double dt)
+{
+    return guard([&] {
+        GC_REQUIRE(md && md->n > 0 && steps >= 0, GC_E_STATE, "no system set");
+        cudaStream_t s = md->ctx->stream;
+        if (!md->graph || md->graph_steps != steps || md->graph_dt != dt) {
+            if (md->graph) cudaGraphExecDestroy(md->graph);
+            md->graph = nullptr;
+            // make sure cub's temp storage is allocated before capture
+            md_sort(md, true);
+            GC_CUDA(cudaStreamSynchronize(s));
+            cudaGraph_t g;
+            GC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            for (int k = 0; k < steps; ++k) md_step_once(md, dt);
+            GC_CUDA(cudaStreamEndCapture(s, &g));
+            GC_CUDA(cudaGraphInstantiate(&md->graph, g, 0));
+            cudaGraphDestroy(g);
+            md->graph_steps = steps;
+            md->graph_dt = dt;
+        }
+        GC_CUDA(cudaEventRecord(md->e0, s));
+        GC_CUDA(cudaGraphLaunch(md->graph, s));
+        GC_CUDA(cudaEventRecord(md->e1, s));
+        GC_CUDA(cudaStreamSynchronize(s));
+        // leave the cell ordering consistent with the final positions
+        md_sort(md, true);
+        GC_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+gc_status gc_md_get_state(gc_md *md, double *pos, double *vel, int64_t *cell_of)
+{
+    return guard([&] {
+        GC_REQUIRE(md, GC_E_VALUE, "null argument");
+        cudaStream_t s = md->ctx->stream;
+        const int n = md->n, d = md->P.dim;
+        std::vector<double4> p(n), v(n);
+        std::vector<int> c(n);
+        md->pos.download(p.data(), n, s);
+        md->vel.download(v.data(), n, s);
+        md->cell_of.download(c.data(), n, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        for (int i = 0; i < n; ++i) {
+            const double pp[3] = {p[i].x, p[i].y, p[i].z}, vv[3] = {v[i].x, v[i].y, v[i].z};
+            for (int k = 0; k < d; ++k) {
+                if (pos) pos[i * d + k] = pp[k];
+                if (vel) vel[i * d + k] = vv[k];
+            }
+            if (cell_of) cell_of[i] = c[i];
+        }
+    });
+}
+
+gc_status gc_md_elapsed(gc_md *md, double *ms)
+{
+    return guard([&] {
+        float t = 0.f;
+        GC_CUDA(cudaEventElapsedTime(&t, md->e0, md->e1));
+        *ms = t;
+    });
+}
+
+}  // extern "C"
+
+namespace gc {
 void md_kernel_spec(const char *cls, int64_t out[5])
 {
     (void)cls;
-    throw Error{GC_E_VALUE, "md kernel class not built yet"};
+    const void *fn = (const void *)md_force_kernel<LAW_LJ, 3>;
+    cudaFuncAttributes a;
+    GC_CUDA(cudaFuncGetAttributes(&a, fn));
+    int blocks = 0;
+    GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, MD_TPB, 0));
+    out[0] = MD_TPB;
+    out[1] = a.numRegs;
+    out[2] = (int64_t)a.sharedSizeBytes;
+    out[3] = MD_TPB;  // one atom (one cell-pair row) per thread
+    out[4] = blocks;
 }
 }  // namespace gc
