@@ -9,10 +9,14 @@ the bucket force kernel.  ``value`` = interactions/s with the tree and
 particles already in HBM; ``e2e`` = the same metric through the C-ABI call a
 user makes (gc_bh_step: host buffers in, H2D, tree, walk, forces, D2H).
 
+The same line carries ``md``: BASELINE.json configs[1], Lennard-Jones FCC
+108,000 atoms, rc 2.5 sigma, 20^3 cells, 100 steps (MD ms/step, the second
+half of the metric), with its own HBM roofline and CPU baseline.
+
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 runs under torchrun: every rank evaluates its own independent 1M system
-(seed 42 + rank), so per-GPU work is fixed ("scaling": "weak"); there is no
+N > 1 runs under torchrun: every rank evaluates its own independent system
+(seed + rank), so per-GPU work is fixed ("scaling": "weak"); there is no
 data-path collective, only a barrier and a MAX reduction of the step times.
 ``--impl reference`` times the CPU restatement of the reference path
 (oracle/, float64, all host threads) on the same workload and metric.
@@ -36,6 +40,16 @@ sys.path.insert(0, ROOT)
 THETA, BUCKET, EPS, N_PART = 0.7, 8, 1e-4, 1_000_000
 FLOPS_PER_INTERACTION = 20  # SURVEY.md §8d convention (body-body interaction)
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+MD_STEPS = 100
+BH_METRIC = "BH interactions/s (clustered 1M, theta 0.7)"
+
+
+def measured_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (of measured)"
+    except Exception:
+        return 6650.0, "B200_PROFILING.md fallback 6.65 TB/s (of fallback)"
 
 
 def workload(rank: int):
@@ -81,6 +95,7 @@ class ClockSampler:
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
+        self.lines = []
 
     def __enter__(self):
         try:
@@ -93,20 +108,19 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
-        self.lines = []
         if self.proc is not None:
             time.sleep(0.15)
             self.proc.terminate()
             try:
                 out, _ = self.proc.communicate(timeout=5)
-                self.lines = [l for l in out.splitlines() if l.strip()]
+                self.lines += [l for l in out.splitlines() if l.strip()]
             except Exception:
                 pass
 
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
+        for l in self.lines:
             f = [x.strip() for x in l.split(",")]
             if len(f) < 9:
                 continue
@@ -124,9 +138,12 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(ps, steps=1):
-    """CPU restatement of the reference path (oracle/, float64) on all host
-    threads: tree + walk + eval_forces over the full workload."""
+# ---------------------------------------------------------------------------
+# CPU baselines (oracle/: the float64 restatement of the reference path)
+# ---------------------------------------------------------------------------
+
+def cpu_bh(ps, steps=1):
+    """tree + walk + eval_forces over the full workload, all host threads."""
     from oracle import oracle as orc
     ts = []
     inter = 0
@@ -140,39 +157,67 @@ def cpu_baseline(ps, steps=1):
     return inter, ts, orc.num_threads()
 
 
+def cpu_md(sysin, steps=2):
+    """lj3d_step (compute_forces structure, float64, 1 thread) on the full 108K system."""
+    from oracle import oracle as orc
+    pos, vel = sysin.positions.copy(), sysin.velocities.copy()
+    dims = (sysin.cells,) * 3
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        pos, vel, _, _ = orc.lj3d_step(pos, vel, dims, sysin.cell_size, sysin.dt, sysin.rc, sysin.eps, sysin.sigma)
+    return (time.perf_counter() - t0) / steps * 1e3
+
+
+def md_task_bytes(cell_of, ncell_dim):
+    """Algorithmic bytes of one MD step under the paper's task model
+    (SURVEY.md §8d): per cell-pair work request 16 B per atom read + 16 B per
+    atom written (float4 pos / force+energy) + 4 B per buffer index, self
+    pairs counted once; plus the per-step staging gather, 32 B per atom."""
+    n = ncell_dim
+    pops = np.bincount(cell_of, minlength=n ** 3).reshape(n, n, n)
+    total = 0.0
+    for dx in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dz in (-1, 0, 1):
+                if not (dx > 0 or (dx == 0 and dy > 0) or (dx == 0 and dy == 0 and dz > 0)):
+                    continue
+                nb = np.roll(pops, shift=(-dx, -dy, -dz), axis=(0, 1, 2))
+                total += (32.0 * (pops + nb) + 8.0).sum()
+    total += (32.0 * pops + 4.0).sum()  # self pairs
+    total += 32.0 * len(cell_of)  # staging gather
+    return total
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
+    from paper_2008_05712_b200.generators import gen_lj_fcc
     ps = workload(0)
-    for _ in range(args.warmup):
-        pass  # the oracle has no warm-up state beyond the first call below
-    inter, ts, cores = cpu_baseline(ps, steps=max(1, args.steps))
+    inter, ts, cores = cpu_bh(ps, steps=max(1, args.steps))
     mean = statistics.mean(ts)
     v = inter / mean
+    md_ms = cpu_md(gen_lj_fcc(30), steps=1)
     line = {
-        "impl": "reference", "metric": "BH interactions/s (clustered 1M, theta 0.7)", "value": v,
-        "unit": "interactions/s", "n_gpus": 1, "steps": len(ts), "warmup": args.warmup,
-        "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic gen_particles(1M, seed 42, clustering 0.6, dim 3), fp32-exact",
+        "impl": "reference", "metric": BH_METRIC, "value": v, "unit": "interactions/s", "n_gpus": 1,
+        "steps": len(ts), "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic gen_particles(1M, seed 42, clustering 0.6, dim 3), fp32-exact",
         "config": {"workload": "configs[2] clustered N-body 1M, theta 0.7, bucket 8, eps 1e-4",
                    "path": "oracle/ C restatement of build_bucket_tree + build_interaction_lists + eval_forces"},
         "cpu_baseline": {"value": v, "unit": "interactions/s", "cores": cores, "kind": "port",
                          "sample": "full workload per step (tree + walk + eval_forces)"},
         "e2e": {"value": v, "unit": "interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "md": {"metric": "MD ms/step (LJ FCC 108K, rc 2.5)", "value": md_ms, "unit": "ms/step",
+               "higher_is_better": False, "cores": 1, "kind": "port",
+               "sample": "oracle lj3d_step (compute_forces structure, float64) on the full system"},
     }
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args, world, rank, local):
-    import ctypes as C
-
-    import torch
-
+def bench_bh(args, world, rank, local, ctx, torch):
     from paper_2008_05712_b200 import _lib as L
     from paper_2008_05712_b200 import nbody
 
-    torch.cuda.set_device(local)
-    ctx = L.context(local)
     ext = torch.cuda.ExternalStream(ctx.stream)
     ps = workload(rank)
     tree = nbody.build_bucket_tree(ps, BUCKET)
@@ -186,14 +231,12 @@ def run_ours(args, world, rank, local):
         step()
     ctx.sync()
     inter = nbody.interactions(tree)
-    # per-step launches of our kernels: walk count + walk write + force
-    launches_per_step = 3
-
     step_ms, walk_ms, force_ms = [], [], []
     tm = np.zeros(2)
     barrier(world)
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    clk = ClockSampler(local)
+    with clk:
         for _ in range(args.steps):
             flush.fill_(1)  # evict L2 (256 MiB write) before every timed step
             torch.cuda.synchronize()
@@ -208,23 +251,17 @@ def run_ours(args, world, rank, local):
             force_ms.append(tm[1])
     torch.cuda.synchronize()
     barrier(world)
-    total_ms = allmax(sum(step_ms), world)
-    ms = total_ms / args.steps
-    value = world * inter / (ms * 1e-3)
-    f_ms = statistics.mean(force_ms)
-    w_ms = statistics.mean(walk_ms)
-
-    # FP32 pipe peak measured on this GPU (FFMA chains)
-    pk, _ = np.zeros(1), np.zeros(1)
-    L.call("gc_measure_fp32_peak", ctx.handle, L.ptr(pk, L.f64p), L.ptr(_, L.f64p))
+    ms = allmax(sum(step_ms), world) / args.steps
+    f_ms, w_ms = statistics.mean(force_ms), statistics.mean(walk_ms)
+    pk, tmp = np.zeros(1), np.zeros(1)
+    L.call("gc_measure_fp32_peak", ctx.handle, L.ptr(pk, L.f64p), L.ptr(tmp, L.f64p))
     fp32_peak = float(pk[0])
 
-    # end to end through the C ABI, pinned host buffers, H2D + D2H inside
-    pos_h = torch.from_numpy(np.ascontiguousarray(ps.positions)).pin_memory()
-    m_h = torch.from_numpy(np.ascontiguousarray(ps.masses)).pin_memory()
-    out_h = torch.empty((ps.positions.shape[0], 3), dtype=torch.float64).pin_memory()
+    # end to end through the C ABI: pinned host buffers, H2D + D2H inside
+    pos_np = torch.from_numpy(np.ascontiguousarray(ps.positions)).pin_memory().numpy()
+    m_np = torch.from_numpy(np.ascontiguousarray(ps.masses)).pin_memory().numpy()
+    out_np = torch.empty((ps.positions.shape[0], 3), dtype=torch.float64).pin_memory().numpy()
     stepper = nbody.BHStep(BUCKET, THETA, 1.0, EPS)
-    pos_np, m_np, out_np = pos_h.numpy(), m_h.numpy(), out_h.numpy()
     stepper(pos_np, m_np, 1.0, out_np)  # warm-up
     e2e_s = []
     io = np.zeros(2, np.int64)
@@ -235,37 +272,99 @@ def run_ours(args, world, rank, local):
         e2e_s.append(time.perf_counter() - t0)
     L.call("gc_bh_io_bytes", stepper.handle, L.ptr(io, L.i64p), 0)
     e2e_t = allmax(statistics.mean(e2e_s), world)
-    e2e_v = world * inter / e2e_t
+    achieved = FLOPS_PER_INTERACTION * inter / (f_ms * 1e-3) / 1e12
+    return {
+        "ps": ps, "inter": inter, "ms": ms, "value": world * inter / (ms * 1e-3), "walk_ms": w_ms, "force_ms": f_ms,
+        "clocks": clk.summary(),
+        "roofline": {"bound": "fp32", "kernel": "force_group_kernel", "achieved": achieved, "peak": fp32_peak,
+                     "peak_source": "FFMA-chain probe on this GPU (gc_measure_fp32_peak); no fp32 entry in "
+                                    "MEASURED_PEAKS.json", "nominal_peak": NOMINAL_FP32_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / fp32_peak, "traffic": None,
+                     "flops_per_interaction": FLOPS_PER_INTERACTION,
+                     "interactions_per_launch": inter},
+        "e2e": {"value": world * inter / e2e_t, "unit": "interactions/s", "h2d_bytes_per_step": int(io[0]),
+                "d2h_bytes_per_step": int(io[1]), "ms_per_step": e2e_t * 1e3,
+                "path": "gc_bh_step C ABI: pinned host positions/masses -> H2D -> host tree -> device walk -> "
+                        "forces -> D2H"},
+    }
 
+
+def bench_md(args, world, rank, local, torch):
+    from paper_2008_05712_b200 import md
+    from paper_2008_05712_b200.generators import gen_lj_fcc
+
+    sysin = gen_lj_fcc(30, seed=7 + rank)
+    sysd = md.LJSystem(sysin)
+    sysd.run(MD_STEPS)  # warm-up: graph capture + one full run
+    _, _, cells = sysd.state()
+    task_bytes = md_task_bytes(cells, sysin.cells)
+    barrier(world)
+    clk = ClockSampler(local)
+    runs = []
+    with clk:
+        for _ in range(max(1, min(args.steps, 3))):
+            runs.append(sysd.run(MD_STEPS))
+    ms = allmax(statistics.mean(runs), world) / MD_STEPS
+    hbm, src = measured_hbm()
+    achieved = task_bytes / (ms * 1e-3) / 1e9
+    # end to end: host state -> H2D -> 100 device steps -> D2H of positions/velocities
+    t0 = time.perf_counter()
+    sysd2 = md.LJSystem(sysin)
+    sysd2.run(MD_STEPS)
+    p, v, _ = sysd2.state()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / MD_STEPS
+    n = sysin.positions.shape[0]
+    return {
+        "metric": "MD ms/step (LJ FCC 108K, rc 2.5, 100 steps)", "value": ms, "unit": "ms/step",
+        "higher_is_better": False, "steps_per_run": MD_STEPS, "dtype": "f64",
+        "config": {"workload": "configs[1] LJ FCC 30^3x4 = 108,000 atoms, rho 0.8442, T 1.44, rc 2.5, 20^3 "
+                               "cells, dt 0.005, periodic", "tasks_per_step": sysd.task_count(),
+                   "timed": "CUDA-graph of 100 full steps (cell sort + forces + integrator), events"},
+        "roofline": {"bound": "hbm", "kernel": "md step (task model)", "achieved": achieved, "peak": hbm,
+                     "peak_source": src, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                     "algorithmic_bytes_per_step": task_bytes},
+        "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": 2 * n * 3 * 8 // MD_STEPS,
+                "d2h_bytes_per_step": 2 * n * 3 * 8 // MD_STEPS,
+                "path": "LJSystem(host arrays) -> H2D -> run(100) -> state() D2H, wall clock / 100"},
+        "clocks": clk.summary(),
+        "_sysin": sysin,
+    }
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    from paper_2008_05712_b200 import _lib as L
+
+    torch.cuda.set_device(local)
+    ctx = L.context(local)
+    bh = bench_bh(args, world, rank, local, ctx, torch)
+    mdr = bench_md(args, world, rank, local, torch)
     if rank != 0:
         return
     line = {
-        "metric": "BH interactions/s (clustered 1M, theta 0.7)",
-        "value": value, "unit": "interactions/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "fp32 force math (fp64 walk decisions, fp64 accumulation)",
+        "metric": BH_METRIC, "value": bh["value"], "unit": "interactions/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": bh["ms"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32 force math (fp64 walk decisions, fp64 accumulation)",
         "data": "synthetic gen_particles(1M, seed 42+rank, clustering 0.6, dim 3), fp32-exact",
         "config": {"workload": "configs[2] clustered N-body 1M, theta 0.7, bucket 8, eps 1e-4 (1 system per GPU)",
                    "step": "device walk (union lists) + bucket force kernel; tree resident in HBM",
-                   "interactions_per_gpu": inter, "walk_ms": w_ms, "force_ms": f_ms,
+                   "interactions_per_gpu": bh["inter"], "walk_ms": bh["walk_ms"], "force_ms": bh["force_ms"],
                    "l2": "flushed (256 MiB write) before every timed step"},
-        "roofline": {"bound": "fp32", "kernel": "force_group_kernel",
-                     "achieved": FLOPS_PER_INTERACTION * inter / (f_ms * 1e-3) / 1e12,
-                     "peak": fp32_peak, "peak_source": "measured FFMA-chain probe on this GPU (gc_measure_fp32_peak)",
-                     "nominal_peak": NOMINAL_FP32_TFLOPS, "unit": "TFLOP/s",
-                     "frac": FLOPS_PER_INTERACTION * inter / (f_ms * 1e-3) / 1e12 / fp32_peak,
-                     "traffic": None, "flops_per_interaction": FLOPS_PER_INTERACTION},
-        "e2e": {"value": e2e_v, "unit": "interactions/s", "h2d_bytes_per_step": int(io[0]),
-                "d2h_bytes_per_step": int(io[1]), "ms_per_step": e2e_t * 1e3,
-                "path": "gc_bh_step C ABI: pinned host positions/masses -> H2D -> host tree -> device walk -> forces -> D2H"},
-        "gpu_launches": launches_per_step * args.steps,
-        "clocks": clk.summary(),
+        "roofline": bh["roofline"],
+        "e2e": bh["e2e"],
+        "gpu_launches": 3 * args.steps,
+        "clocks": bh["clocks"],
     }
+    sysin = mdr.pop("_sysin")
+    line["md"] = mdr
     if world == 1 and not args.no_cpu_baseline:
-        c_inter, c_ts, cores = cpu_baseline(ps, 1)
+        c_inter, c_ts, cores = cpu_bh(bh["ps"], 1)
         line["cpu_baseline"] = {"value": c_inter / c_ts[0], "unit": "interactions/s", "cores": cores,
                                 "kind": "port",
                                 "sample": "full configs[2] workload once (tree + walk + eval_forces, float64)"}
+        line["md"]["cpu_baseline"] = {"value": cpu_md(sysin, 1), "unit": "ms/step", "cores": 1, "kind": "port",
+                                      "sample": "one oracle lj3d_step on the full 108K system (float64)"}
     print(json.dumps(line), flush=True)
 
 
