@@ -20,6 +20,7 @@
 // (md.py:166-190).
 #include <cub/cub.cuh>
 
+#include <climits>
 #include <cmath>
 #include <cstring>
 
@@ -158,6 +159,218 @@ md_force_kernel(int n, const double4 *__restrict__ spos, const int *__restrict__
     out[ia] = make_double4(fx, fy, fz, en);
 }
 
+// ---------------------------------------------------------------------------
+// Block-per-cell force kernel (the throughput path).
+//   phase 0: the 27 (9) neighbour cells' atoms are staged in shared memory as
+//            float32 positions relative to the home cell corner;
+//   phase A: each warp takes every other home atom; lanes scan 32 staged
+//            neighbours at a time with a float32 r^2 test widened by a
+//            rigorous error band and append survivors to the atom's list;
+//   phase B: 1, 2 or 4 threads per home atom walk its list and evaluate each
+//            survivor exactly as the reference does (float64, canonical
+//            orientation) -- the exact test decides the cutoff.
+// Lists are written in a fixed order, so results are deterministic.
+// ---------------------------------------------------------------------------
+constexpr int MDC_THREADS = 128;
+constexpr int MDC_NB = 640;  // staged neighbours per home cell
+constexpr int MDC_HOME = 16;  // home atoms per pass (lane = home atom, 16 per half warp)
+constexpr int MDC_PARTS = 8;  // neighbour slots split into 8 strided parts (2 per warp)
+constexpr int MDC_LIST = 24;  // survivors per (home atom, part) (overflow -> full scan)
+
+__device__ __forceinline__ void md_offset_of(int code, int &ox, int &oy, int &oz)
+{
+    ox = code / 9 - 1;
+    oy = (code / 3) % 3 - 1;
+    oz = code % 3 - 1;
+}
+
+// per neighbour-cell offset: image shift (xyz) and half-shell direction (w: 1
+// forward, 0 backward, 2 self cell)
+template <int LAW, int DIM>
+__device__ __forceinline__ void md_pair_exact(const double4 a, const long long ia, const double4 b, const double4 sh,
+                                              const MDParams &P, double &fx, double &fy, double &fz, double &en)
+{
+    const double sx = sh.x, sy = sh.y, sz = sh.z;
+    const bool fwd = sh.w == 2.0 ? ia < __double_as_longlong(b.w) : sh.w == 1.0;
+    double d0, d1, d2 = 0.0;
+    if (fwd) {
+        d0 = __dsub_rn(a.x, __dadd_rn(b.x, sx));
+        d1 = __dsub_rn(a.y, __dadd_rn(b.y, sy));
+        if (DIM == 3) d2 = __dsub_rn(a.z, __dadd_rn(b.z, sz));
+    } else {
+        d0 = __dsub_rn(b.x, __dadd_rn(a.x, -sx));
+        d1 = __dsub_rn(b.y, __dadd_rn(a.y, -sy));
+        if (DIM == 3) d2 = __dsub_rn(b.z, __dadd_rn(a.z, -sz));
+    }
+    double r2 = __dmul_rn(d0, d0);
+    r2 = __dadd_rn(r2, __dmul_rn(d1, d1));
+    if (DIM == 3) r2 = __dadd_rn(r2, __dmul_rn(d2, d2));
+    // the cutoff decision above is the reference's, bit for bit; the force
+    // law below uses a correctly rounded reciprocal instead of two IEEE
+    // divisions (~1 ulp from the reference's values)
+    if (r2 >= P.c2 || r2 < 1e-12) return;
+    double mag;
+    if (LAW == LAW_SOFT) {
+        const double r = __dsqrt_rn(r2);
+        mag = __dmul_rn(P.stiffness, __dsub_rn(__dmul_rn(P.cutoff, __drcp_rn(r)), 1.0));
+    } else {
+        const double inv = __drcp_rn(r2);
+        const double s2 = P.sig2 * inv;
+        const double s6 = s2 * s2 * s2;
+        const double s12 = s6 * s6;
+        mag = 24.0 * P.eps * (2.0 * s12 - s6) * inv;
+        en += 2.0 * P.eps * (s12 - s6);
+    }
+    if (fwd) {
+        fx = fma(d0, mag, fx);
+        fy = fma(d1, mag, fy);
+        if (DIM == 3) fz = fma(d2, mag, fz);
+    } else {
+        fx = fma(-d0, mag, fx);
+        fy = fma(-d1, mag, fy);
+        if (DIM == 3) fz = fma(-d2, mag, fz);
+    }
+}
+
+template <int LAW, int DIM>
+__global__ void __launch_bounds__(MDC_THREADS)
+md_cell_kernel(const double4 *__restrict__ spos, const int *__restrict__ cell_start, const MDParams P, float band,
+               double4 *__restrict__ out)
+{
+    __shared__ float4 nb[MDC_NB];  // rel xyz (float32 filter), packed (sorted index << 5 | offset code)
+    __shared__ int qstart[27];
+    __shared__ unsigned short lists[MDC_HOME][MDC_PARTS][MDC_LIST];
+    __shared__ int lover[MDC_HOME];
+    __shared__ int pre[28];
+    __shared__ int qs[27];
+    __shared__ double4 shtab[27];
+    const int c = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int cz = c % P.nz, cy = (c / P.nz) % P.ny, cx = c / (P.nz * P.ny);
+    const double orx = cx * P.cell, ory = cy * P.cell, orz = cz * P.cell;
+    constexpr int NOFF = 27;
+    // neighbour cells and their populations (offset code = (ox+1)*9 + (oy+1)*3 + (oz+1))
+    if (tid < NOFF) {
+        int ox, oy, oz;
+        md_offset_of(tid, ox, oy, oz);
+        int qx = cx + ox, qy = cy + oy, qz = cz + oz;
+        bool ok = DIM == 3 || oz == 0;
+        if (qx < 0 || qx >= P.nx) { ok = ok && P.periodic; qx = (qx + P.nx) % P.nx; }
+        if (qy < 0 || qy >= P.ny) { ok = ok && P.periodic; qy = (qy + P.ny) % P.ny; }
+        if (qz < 0 || qz >= P.nz) { ok = ok && P.periodic; qz = (qz + P.nz) % P.nz; }
+        const int q = (qx * P.ny + qy) * P.nz + qz;
+        qs[tid] = ok ? q : -1;
+        qstart[tid] = ok ? cell_start[q] : 0;
+        const int rx = cx + ox, ry = cy + oy, rz = cz + oz;
+        shtab[tid] = make_double4(rx < 0 ? -P.bx : (rx >= P.nx ? P.bx : 0.0), ry < 0 ? -P.by : (ry >= P.ny ? P.by : 0.0),
+                                  rz < 0 ? -P.bz : (rz >= P.nz ? P.bz : 0.0),
+                                  tid == 13 ? 2.0 : (md_forward(ox, oy, oz) ? 1.0 : 0.0));
+        pre[tid + 1] = ok ? cell_start[q + 1] - cell_start[q] : 0;
+    }
+    __syncthreads();
+    if (warp == 0) {  // inclusive warp scan of the populations
+        int v = lane < NOFF ? pre[lane + 1] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        if (lane < NOFF) pre[lane + 1] = v;
+        if (lane == 0) pre[0] = 0;
+    }
+    __syncthreads();
+    const int nnb = pre[NOFF];
+    const int h0 = cell_start[c], nh = cell_start[c + 1] - h0;
+    const int self0 = pre[13];  // home atoms' slot range among the staged neighbours
+    if (nnb > MDC_NB) {
+        // staging overflow (pathological density): exact scan straight from global
+        for (int i = tid; i < nh; i += MDC_THREADS) {
+            const double4 a = spos[h0 + i];
+            const long long ia = __double_as_longlong(a.w);
+            double fx = 0.0, fy = 0.0, fz = 0.0, en = 0.0;
+            for (int k = 0; k < NOFF; ++k) {
+                if (qs[k] < 0) continue;
+                for (int j = cell_start[qs[k]]; j < cell_start[qs[k] + 1]; ++j)
+                    if (j != h0 + i) md_pair_exact<LAW, DIM>(a, ia, spos[j], shtab[k], P, fx, fy, fz, en);
+            }
+            out[ia] = make_double4(fx, fy, fz, en);
+        }
+        return;
+    }
+    // phase 0: stage all neighbours at once (independent loads)
+    for (int s = tid; s < nnb; s += MDC_THREADS) {
+        int lo = 0, hi = NOFF;  // pre[lo] <= s < pre[lo + 1]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (pre[mid] <= s) lo = mid;
+            else hi = mid;
+        }
+        const int j = qstart[lo] + (s - pre[lo]);
+        const double4 b = spos[j];
+        const double4 sh = shtab[lo];
+        nb[s] = make_float4((float)((b.x + sh.x) - orx), (float)((b.y + sh.y) - ory), (float)((b.z + sh.z) - orz),
+                            __int_as_float((j << 5) | lo));
+    }
+    // phase A lanes: home atom ia = lane % 16, part = 2 * warp + lane / 16;
+    // phase B threads: home atom tid / 8, part tid % 8 (its own list)
+    const int pa_i = lane & 15, pa_part = 2 * warp + (lane >> 4);
+    const int pb_i = tid / MDC_PARTS, pb_part = tid % MDC_PARTS;
+    for (int hb = 0; hb < nh; hb += MDC_HOME) {
+        const int nhc = min(MDC_HOME, nh - hb);
+        if (tid < MDC_HOME) lover[tid] = 0;
+        __syncthreads();
+        // phase A: float32 candidate filter, each lane appends to its own list
+        if (pa_i < nhc) {
+            const int si = self0 + hb + pa_i;
+            const float4 xi = nb[si];
+            int cnt = 0;
+            unsigned short *lst = lists[pa_i][pa_part];
+            for (int sl = pa_part; sl < nnb; sl += MDC_PARTS) {
+                const float4 xj = nb[sl];
+                const float dx = xj.x - xi.x, dy = xj.y - xi.y, dz = xj.z - xi.z;
+                const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                if (r2 < band && sl != si) {
+                    if (cnt < MDC_LIST) lst[cnt] = (unsigned short)sl;
+                    ++cnt;
+                }
+            }
+            if (cnt > MDC_LIST) atomicOr(&lover[pa_i], 1);
+            if (cnt < MDC_LIST) lst[cnt] = 0xffff;  // terminator
+        }
+        __syncthreads();
+        // phase B: exact float64 on survivors
+        double fx = 0.0, fy = 0.0, fz = 0.0, en = 0.0;
+        long long ia = -1;
+        if (pb_i < nhc) {
+            const double4 a = spos[__float_as_int(nb[self0 + hb + pb_i].w) >> 5];
+            ia = __double_as_longlong(a.w);
+            if (!lover[pb_i]) {
+                const unsigned short *lst = lists[pb_i][pb_part];
+                for (int e = 0; e < MDC_LIST; ++e) {
+                    const int sl = lst[e];
+                    if (sl == 0xffff) break;
+                    const int pk = __float_as_int(nb[sl].w);
+                    md_pair_exact<LAW, DIM>(a, ia, spos[pk >> 5], shtab[pk & 31], P, fx, fy, fz, en);
+                }
+            } else {  // list overflow: exact scan of this part's slots
+                const int si = self0 + hb + pb_i;
+                for (int sl = pb_part; sl < nnb; sl += MDC_PARTS) {
+                    if (sl == si) continue;
+                    const int pk = __float_as_int(nb[sl].w);
+                    md_pair_exact<LAW, DIM>(a, ia, spos[pk >> 5], shtab[pk & 31], P, fx, fy, fz, en);
+                }
+            }
+        }
+        for (int o = 1; o < MDC_PARTS; o <<= 1) {
+            fx += __shfl_xor_sync(0xffffffffu, fx, o);
+            fy += __shfl_xor_sync(0xffffffffu, fy, o);
+            fz += __shfl_xor_sync(0xffffffffu, fz, o);
+            en += __shfl_xor_sync(0xffffffffu, en, o);
+        }
+        if (pb_i < nhc && pb_part == 0) out[ia] = make_double4(fx, fy, fz, en);
+        __syncthreads();
+    }
+}
+
 // cell of every atom: numpy floor_divide for the 2-D patches (md.py:187-189),
 // floor(x / cell) for the 3-D cells; clamped to the grid
 __global__ void md_assign_kernel(int n, const double4 *__restrict__ pos, const MDParams P, int use_npy,
@@ -216,6 +429,50 @@ __global__ void md_cellsort_kernel(int ncell, const int *__restrict__ cell_start
     }
 }
 
+// warp per cell: rank sort of the cell's atoms by original id (deterministic
+// order for any atomic scatter order) fused with the gather
+__global__ void md_sortgather_kernel(int ncell, const int *__restrict__ cell_start, int *__restrict__ perm,
+                                     const double4 *__restrict__ pos, const int *__restrict__ cell_of,
+                                     double4 *__restrict__ spos, int *__restrict__ scell)
+{
+    const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (c >= ncell) return;
+    const int s = cell_start[c], n = cell_start[c + 1] - s;
+    if (n > 32) {  // rare: serial insertion sort, then gather
+        if (lane == 0)
+            for (int i = s + 1; i < s + n; ++i) {
+                const int v = perm[i];
+                int j = i - 1;
+                while (j >= s && perm[j] > v) {
+                    perm[j + 1] = perm[j];
+                    --j;
+                }
+                perm[j + 1] = v;
+            }
+        __syncwarp();
+        for (int k = lane; k < n; k += 32) {
+            const int i = perm[s + k];
+            double4 p = pos[i];
+            p.w = __longlong_as_double((long long)i);
+            spos[s + k] = p;
+            scell[s + k] = c;
+        }
+        return;
+    }
+    const int v = lane < n ? perm[s + lane] : INT_MAX;
+    int rank = 0;
+    for (int k = 0; k < n; ++k) rank += __shfl_sync(0xffffffffu, v, k) < v;
+    __syncwarp();
+    if (lane < n) {
+        perm[s + rank] = v;
+        double4 p = pos[v];
+        p.w = __longlong_as_double((long long)v);
+        spos[s + rank] = p;
+        scell[s + rank] = c;
+    }
+}
+
 __global__ void md_gather_kernel(int n, const int *__restrict__ perm, const double4 *__restrict__ pos,
                                  const int *__restrict__ cell_of, double4 *__restrict__ spos, int *__restrict__ scell)
 {
@@ -245,7 +502,13 @@ __global__ void md_integrate_kernel(int n, double4 *__restrict__ pos, double4 *_
     }
     for (int k = 0; k < P.dim; ++k) {
         if (P.periodic) {
-            x[k] = np_remainder(x[k], hi[k]);
+            // np.remainder (npy_divmod) fast path for one box of travel: fmod is
+            // exact there, and negative values take the rounded x + box
+            const double b = hi[k];
+            if (x[k] >= 0.0 && x[k] < b) x[k] = x[k] == 0.0 ? 0.0 : x[k];
+            else if (x[k] >= b && x[k] < 2.0 * b) x[k] = __dsub_rn(x[k], b);
+            else if (x[k] < 0.0 && x[k] > -b) x[k] = __dadd_rn(x[k], b);
+            else x[k] = np_remainder(x[k], b);
         } else {
             if (x[k] < 0.0) {
                 x[k] = -x[k];
@@ -272,6 +535,7 @@ struct gc_md {
     int law = LAW_SOFT;
     int n = 0, ncell = 0;
     int use_npy = 0;  // reference 2-D patches use numpy floor_divide
+    bool cell_path = true;  // block-per-cell kernel (false: thread-per-atom kernel)
     DBuf<double4> pos, vel, spos, force;
     DBuf<int> cell_of, scell, count, cell_start, cursor, perm;
     cudaGraphExec_t graph = nullptr;
@@ -304,9 +568,8 @@ void md_sort(gc_md *md, bool assign)
     GC_CUDA(cub::DeviceScan::ExclusiveSum(md->ctx->scratch.p, bytes, md->count.p, md->cell_start.p, nc + 1, s));
     GC_CUDA(cudaMemcpyAsync(md->cursor.p, md->cell_start.p, sizeof(int) * nc, cudaMemcpyDeviceToDevice, s));
     md_scatter_kernel<<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->pos.p, md->cell_of.p, md->cursor.p, md->perm.p);
-    md_cellsort_kernel<<<grid_for(nc, MD_TPB), MD_TPB, 0, s>>>(nc, md->cell_start.p, md->perm.p);
-    md_gather_kernel<<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->perm.p, md->pos.p, md->cell_of.p, md->spos.p,
-                                                            md->scell.p);
+    md_sortgather_kernel<<<grid_for(nc, MD_TPB / 32), MD_TPB, 0, s>>>(nc, md->cell_start.p, md->perm.p, md->pos.p,
+                                                                      md->cell_of.p, md->spos.p, md->scell.p);
     check_launch("md sort");
 }
 
@@ -314,6 +577,30 @@ void md_forces(gc_md *md)
 {
     cudaStream_t s = md->ctx->stream;
     const int n = md->n;
+    if (md->cell_path) {
+        // float32 filter band: r^2 < c2 + margin, margin >> the float32 error of
+        // relative coordinates within two cells (see md_cell_kernel)
+        const double ext = 3.0 * md->P.cell;
+        const float band = (float)(md->P.c2 + 1e-5 * ext * ext + 1e-6);
+        const int nc = md->ncell;
+        if (md->law == LAW_LJ) {
+            if (md->P.dim == 3)
+                md_cell_kernel<LAW_LJ, 3><<<nc, MDC_THREADS, 0, s>>>(md->spos.p, md->cell_start.p, md->P, band,
+                                                                      md->force.p);
+            else
+                md_cell_kernel<LAW_LJ, 2><<<nc, MDC_THREADS, 0, s>>>(md->spos.p, md->cell_start.p, md->P, band,
+                                                                      md->force.p);
+        } else {
+            if (md->P.dim == 3)
+                md_cell_kernel<LAW_SOFT, 3><<<nc, MDC_THREADS, 0, s>>>(md->spos.p, md->cell_start.p, md->P, band,
+                                                                        md->force.p);
+            else
+                md_cell_kernel<LAW_SOFT, 2><<<nc, MDC_THREADS, 0, s>>>(md->spos.p, md->cell_start.p, md->P, band,
+                                                                        md->force.p);
+        }
+        check_launch("md_cell_kernel");
+        return;
+    }
     if (md->law == LAW_LJ) {
         if (md->P.dim == 3)
             md_force_kernel<LAW_LJ, 3><<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->spos.p, md->cell_start.p,
