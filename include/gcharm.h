@@ -128,6 +128,13 @@ gc_status gc_bh_timings(gc_bh *bh, double out[2]);
 /* Host<->device bytes moved since the last reset (out[0] = H2D, out[1] = D2H);
  * gc_bh_step resets at entry, so after it these are that step's bytes. */
 gc_status gc_bh_io_bytes(gc_bh *bh, int64_t out[2], int32_t reset);
+/* Multi-GPU sharding: walk groups (32 consecutive DFS buckets each) and the
+ * per-bucket work n_b * item_count_b of the last walk; gc_bh_set_range
+ * restricts walk + forces to walk groups [wg_begin, wg_end) (a shard chosen
+ * by the K-way generalisation of partition_queue, hr/scheduler.py:73-107). */
+gc_status gc_bh_groups(gc_bh *bh, int64_t *n_walk_groups, int64_t *wg_first_bucket /* n+1, may be NULL */);
+gc_status gc_bh_bucket_work(gc_bh *bh, int64_t *work /* n_buckets */);
+gc_status gc_bh_set_range(gc_bh *bh, int64_t wg_begin, int64_t wg_end);
 /* End-to-end step from host buffers: H2D particles, tree, device walk,
  * forces, D2H forces (n x dim float64). */
 gc_status gc_bh_step(gc_bh *bh, int64_t n, int32_t dim, const double *pos, const double *mass, double box,

@@ -52,6 +52,9 @@ SIGNATURES = {
     "gc_bh_interactions": [vp, i64p],
     "gc_bh_timings": [vp, f64p],
     "gc_bh_io_bytes": [vp, i64p, C.c_int32],
+    "gc_bh_groups": [vp, i64p, i64p],
+    "gc_bh_bucket_work": [vp, i64p],
+    "gc_bh_set_range": [vp, C.c_int64, C.c_int64],
     "gc_measure_fp32_peak": [vp, f64p, f64p],
     "gc_bh_step": [vp, C.c_int64, C.c_int32, f64p, f64p, C.c_double, C.c_int64, C.c_double, C.c_double,
                    C.c_double, f64p],

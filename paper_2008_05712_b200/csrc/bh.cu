@@ -37,6 +37,7 @@ struct gc_bh {
     float walk_dd2 = 0.f, walk_dd3 = 0.f;
     DBuf<float2> d_tt;
     // union lists (device walk)
+    int rg0 = 0, rg1 = -1;  // walk-group range this handle evaluates (multi-GPU shard)
     bool have_union = false;
     bool cap_valid = false;
     double cap_theta = -1.0;
@@ -235,10 +236,12 @@ void run_walk(gc_bh *bh, double theta)
     GC_REQUIRE(bh->have_tree, GC_E_STATE, "no particles set");
     gc_ctx *ctx = bh->ctx;
     cudaStream_t s = ctx->stream;
-    const int ng = (int)bh->h_wg.size();
     const int nf = (int)bh->h_fg.size();  // lists are per force group
     const int64_t nb = (int64_t)bh->tree.buckets.size();
-    const unsigned grid = grid_for(ng, WARPS_PER_BLOCK);
+    const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? (int)bh->h_wg.size() : bh->rg1;
+    const int ng = g1 - g0;
+    const WalkGroup *wg = bh->d_wg.p + g0;
+    const unsigned grid = grid_for(std::max(ng, 1), WARPS_PER_BLOCK);
     const bool fresh = !bh->cap_valid || bh->cap_theta != theta;
     if (fresh) {
         bh->d_gcount.resize(nf);
@@ -271,8 +274,10 @@ void run_walk(gc_bh *bh, double theta)
     if (fresh) {
         // first walk on this tree: count, then size every force group's list
         // with 1/8 slack so later walks (moved particles) run in one pass
+        bh->d_gcount.zero(s);
+        bh->d_bstat.zero(s);
         walk_group_kernel<false, true><<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(
-            ng, bh->d_wg.p, bh->d_fgmask.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p, bh->d_bgeo32.p, bh->wp,
+            ng, wg, bh->d_fgmask.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p, bh->d_bgeo32.p, bh->wp,
             nullptr, nullptr, nullptr, nullptr, bh->d_gcount.p, bh->d_bstat.p, bh->d_flag.p);
         check_launch("walk_group_kernel<count>");
         std::vector<int64_t> cnt(nf + 1, 0);
@@ -294,7 +299,7 @@ void run_walk(gc_bh *bh, double theta)
         bh->cap_theta = theta;
     }
     walk_group_kernel<true, true><<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(
-        ng, bh->d_wg.p, bh->d_fgmask.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p, bh->d_bgeo32.p, bh->wp,
+        ng, wg, bh->d_fgmask.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p, bh->d_bgeo32.p, bh->wp,
         bh->d_gbase.p, bh->d_gcap.p, bh->d_uid.p, bh->d_umask.p, bh->d_gcount.p, bh->d_bstat.p, bh->d_flag.p);
     check_launch("walk_group_kernel<write>");
     GC_CUDA(cudaEventRecord(bh->ev[1], s));
@@ -315,11 +320,15 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
     const bool eps0 = eps2 == 0.f;
     GC_CUDA(cudaEventRecord(bh->ev[2], s));
     if (bh->have_union) {
-        const int nfg = (int)bh->h_fg.size();
-        const unsigned grid = grid_for(nfg, WARPS_PER_BLOCK);
+        const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? (int)bh->h_wg.size() : bh->rg1;
+        const int f0 = g0 < (int)bh->h_wg.size() ? bh->h_wg[g0].fg_first : (int)bh->h_fg.size();
+        const int f1 = g1 < (int)bh->h_wg.size() ? bh->h_wg[g1].fg_first : (int)bh->h_fg.size();
+        const int nfg = f1 - f0;
+        const unsigned grid = grid_for(std::max(nfg, 1), WARPS_PER_BLOCK);
         auto k = eps0 ? (pot ? force_group_kernel<true, true> : force_group_kernel<true, false>)
                       : (pot ? force_group_kernel<false, true> : force_group_kernel<false, false>);
-        k<<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(nfg, bh->d_fg.p, bh->d_gbase.p, bh->d_gcount.p, bh->d_uid.p,
+        if (nfg > 0)
+        k<<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(nfg, bh->d_fg.p + f0, bh->d_gbase.p + f0, bh->d_gcount.p + f0, bh->d_uid.p,
                                                 bh->d_umask.p, bh->d_parts.p, bh->d_part_bucket.p, bh->d_porder.p,
                                                 bh->d_wg.p, bh->d_rec_hi.p, bh->d_rec_lo.p, bh->d_prange.p, eps2, g,
                                                 t.dim, bh->d_out.p, bh->d_pot.p);
@@ -374,6 +383,8 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
         bh->have_union = bh->have_member_lists = false;
         bh->cap_valid = false;
         bh->stats_dirty = false;
+        bh->rg0 = 0;
+        bh->rg1 = -1;
         upload_tree(bh);
         upload_particles(bh, pos, mass);
     });
@@ -544,6 +555,42 @@ gc_status gc_bh_interactions(gc_bh *bh, int64_t *out)
         const HostTree &t = bh->tree;
         for (size_t b = 0; b < bh->h_item_count.size(); ++b) tot += t.pcount[t.buckets[b]] * bh->h_item_count[b];
         *out = tot;
+    });
+}
+
+gc_status gc_bh_set_range(gc_bh *bh, int64_t wg_begin, int64_t wg_end)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
+        const int64_t ng = (int64_t)bh->h_wg.size();
+        GC_REQUIRE(wg_begin >= 0 && wg_begin <= wg_end && wg_end <= ng, GC_E_VALUE, "bad walk-group range");
+        bh->rg0 = (int)wg_begin;
+        bh->rg1 = (int)wg_end;
+        bh->cap_valid = false;  // next walk recounts this range
+        bh->have_union = false;
+    });
+}
+
+gc_status gc_bh_groups(gc_bh *bh, int64_t *n_walk_groups, int64_t *wg_first_bucket)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
+        *n_walk_groups = (int64_t)bh->h_wg.size();
+        if (wg_first_bucket) {
+            for (size_t g = 0; g < bh->h_wg.size(); ++g) wg_first_bucket[g] = bh->h_wg[g].bfirst;
+            wg_first_bucket[bh->h_wg.size()] = (int64_t)bh->tree.buckets.size();
+        }
+    });
+}
+
+gc_status gc_bh_bucket_work(gc_bh *bh, int64_t *work)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
+        sync_walk_stats(bh);
+        const HostTree &t = bh->tree;
+        for (size_t b = 0; b < t.buckets.size(); ++b)
+            work[b] = b < bh->h_item_count.size() ? t.pcount[t.buckets[b]] * bh->h_item_count[b] : 0;
     });
 }
 
