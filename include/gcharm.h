@@ -97,6 +97,10 @@ gc_status gc_bh_destroy(gc_bh *bh);
  * bucket order, float64 mass/COM with the reference's rounding sequence. */
 gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *pos, const double *mass,
                               double box, int64_t bucket_size);
+/* Tree build on the GPU (device != 0, the default) or the host C++ build;
+ * both are bit-identical to build_bucket_tree.  Applies to the next
+ * gc_bh_set_particles / gc_bh_step. */
+gc_status gc_bh_set_build_mode(gc_bh *bh, int32_t device);
 /* Sizes: out[0..3] = n_nodes, n_buckets, list entries, node entries */
 gc_status gc_bh_sizes(gc_bh *bh, int64_t out[4]);
 /* Tree arrays (host, caller-allocated by gc_bh_sizes): any pointer may be NULL */

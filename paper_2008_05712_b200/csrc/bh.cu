@@ -6,67 +6,10 @@
 #include <cmath>
 #include <cstring>
 
-#include "bh_kernels.cuh"
-#include "bh_tree.h"
-#include "common.cuh"
+#include "bh_state.h"
 
 using namespace gc;
 
-struct gc_bh {
-    gc_ctx *ctx = nullptr;
-    HostTree tree;
-    bool have_tree = false;
-    std::vector<WalkGroup> h_wg;
-    std::vector<ForceGroup> h_fg;
-    std::vector<unsigned> h_fgmask;
-    DBuf<unsigned> d_fgmask;
-    // device tree
-    DBuf<float4> d_recs;  // walk records: float32 com + packed links
-    DBuf<double4> d_com64;  // float64 com (exact opening test)
-    DBuf<double4> d_bgeo;  // per bucket (DFS index): center.xyz, half
-    DBuf<float4> d_bgeo32;  // float32 copy (w < 0: not exact in float32)
-    DBuf<float4> d_parts;  // DFS-sorted particles (x, y, z, m) fp32
-    DBuf<int> d_porder;  // original id of each sorted particle
-    DBuf<int> d_part_bucket;  // DFS bucket index of each sorted particle
-    DBuf<float4> d_rec_hi, d_rec_lo;  // force records: com hi (fp32) + mass, com lo
-    DBuf<int2> d_prange;  // per node: (first sorted particle, count) for buckets
-    DBuf<int2> d_brange;  // per bucket (DFS index): (first sorted particle, count)
-    DBuf<int> d_bucket_ids;  // identity member list for the member kernel
-    DBuf<WalkGroup> d_wg;
-    DBuf<ForceGroup> d_fg;
-    float walk_dd2 = 0.f, walk_dd3 = 0.f;
-    DBuf<float2> d_tt;
-    // union lists (device walk)
-    int rg0 = 0, rg1 = -1;  // walk-group range this handle evaluates (multi-GPU shard)
-    bool have_union = false;
-    bool cap_valid = false;
-    double cap_theta = -1.0;
-    DBuf<int64_t> d_gcount, d_gbase, d_gcap, d_bstat;
-    DBuf<int> d_uid;
-    DBuf<uint2> d_umask;
-    int64_t n_union = 0;
-    // per-bucket CSR (host-supplied lists)
-    bool have_member_lists = false;
-    DBuf<int64_t> d_nptr, d_pptr;
-    DBuf<int> d_naddr, d_paddr;
-    // outputs
-    DBuf<double> d_out, d_pot;
-    std::vector<int64_t> h_item_count;
-    int64_t n_list_entries = 0;
-    DBuf<int64_t> d_bptr;
-    DBuf<int> d_list_ids;
-    DBuf<int8_t> d_list_kind;
-    DBuf<int> d_flag;
-    WalkParams wp{};
-    bool stats_dirty = false;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    int64_t h2d = 0, d2h = 0;  // bytes moved host<->device since the last reset
-    ~gc_bh()
-    {
-        for (auto &e : ev)
-            if (e) cudaEventDestroy(e);
-    }
-};
 
 namespace {
 
@@ -212,7 +155,7 @@ void sync_walk_stats(gc_bh *bh)
 {
     if (!bh->stats_dirty) return;
     cudaStream_t s = bh->ctx->stream;
-    const int64_t nb = (int64_t)bh->tree.buckets.size();
+    const int64_t nb = bh->n_buckets;
     std::vector<int64_t> st(2 * nb);
     int flag = 0;
     bh->d_bstat.download(st.data(), 2 * nb, s);
@@ -237,7 +180,7 @@ void run_walk(gc_bh *bh, double theta)
     gc_ctx *ctx = bh->ctx;
     cudaStream_t s = ctx->stream;
     const int nf = (int)bh->h_fg.size();  // lists are per force group
-    const int64_t nb = (int64_t)bh->tree.buckets.size();
+    const int64_t nb = bh->n_buckets;
     const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? (int)bh->h_wg.size() : bh->rg1;
     const int ng = g1 - g0;
     const WalkGroup *wg = bh->d_wg.p + g0;
@@ -250,7 +193,7 @@ void run_walk(gc_bh *bh, double theta)
         bh->d_bstat.resize(2 * nb);
         bh->d_flag.resize(1);
         const double th2 = theta * theta;
-        const double root = 2.0 * bh->tree.half[0];
+        const double root = bh->box;
         // per-level float32 thresholds on s = d^2: accept iff s > size^2 / theta^2
         std::vector<float2> tt(MAX_LEVELS);
         for (int l = 0; l < MAX_LEVELS; ++l) {
@@ -313,9 +256,8 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
 {
     gc_ctx *ctx = bh->ctx;
     cudaStream_t s = ctx->stream;
-    const HostTree &t = bh->tree;
-    bh->d_out.resize(t.n * t.dim);
-    if (pot) bh->d_pot.resize(t.n);
+    bh->d_out.resize(bh->n * bh->dim);
+    if (pot) bh->d_pot.resize(bh->n);
     const float eps2 = (float)(eps * eps);
     const bool eps0 = eps2 == 0.f;
     GC_CUDA(cudaEventRecord(bh->ev[2], s));
@@ -331,17 +273,17 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
         k<<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(nfg, bh->d_fg.p + f0, bh->d_gbase.p + f0, bh->d_gcount.p + f0, bh->d_uid.p,
                                                 bh->d_umask.p, bh->d_parts.p, bh->d_part_bucket.p, bh->d_porder.p,
                                                 bh->d_wg.p, bh->d_rec_hi.p, bh->d_rec_lo.p, bh->d_prange.p, eps2, g,
-                                                t.dim, bh->d_out.p, bh->d_pot.p);
+                                                bh->dim, bh->d_out.p, bh->d_pot.p);
         check_launch("force_group_kernel");
     } else if (bh->have_member_lists) {
         GC_REQUIRE(!pot, GC_E_STATE, "potentials need device lists (gc_bh_walk)");
-        const int nb = (int)t.buckets.size();
+        const int nb = (int)bh->n_buckets;
         const unsigned grid = grid_for(nb, WARPS_PER_BLOCK);
         auto k = eps0 ? force_member_kernel<true> : force_member_kernel<false>;
         k<<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(nb, bh->d_bucket_ids.p, bh->d_brange.p, bh->d_nptr.p,
                                                 bh->d_naddr.p, bh->d_pptr.p, bh->d_paddr.p, bh->d_parts.p,
                                                 bh->d_porder.p, bh->d_rec_hi.p, bh->d_rec_lo.p, bh->d_prange.p,
-                                                bh->d_parts.p, eps2, g, t.dim, bh->d_out.p);
+                                                bh->d_parts.p, eps2, g, bh->dim, bh->d_out.p);
         check_launch("force_member_kernel");
     } else {
         throw Error{GC_E_STATE, "no interaction lists (call gc_bh_walk or gc_bh_set_lists)"};
@@ -378,15 +320,36 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
         GC_REQUIRE(bucket_size >= 1, GC_E_VALUE, "bucket_size must be >= 1");
         GC_REQUIRE(bucket_size <= 32, GC_E_VALUE, "bucket_size must be <= 32 on the B200 path");
         GC_REQUIRE(dim >= 1 && dim <= 3, GC_E_VALUE, "dim must be 1..3");
-        bh->tree.build(n, dim, pos, mass, box, bucket_size);
+        if (bh->device_build) {
+            device_build_tree(bh, pos, mass, n, dim, box, bucket_size);
+        } else {
+            bh->tree.build(n, dim, pos, mass, box, bucket_size);
+            bh->host_tree_valid = true;
+            bh->n = n;
+            bh->dim = dim;
+            bh->box = box;
+            bh->bucket_size = bucket_size;
+            bh->n_nodes = bh->tree.n_nodes();
+            bh->n_buckets = (int64_t)bh->tree.buckets.size();
+        }
         bh->have_tree = true;
         bh->have_union = bh->have_member_lists = false;
         bh->cap_valid = false;
         bh->stats_dirty = false;
         bh->rg0 = 0;
         bh->rg1 = -1;
-        upload_tree(bh);
-        upload_particles(bh, pos, mass);
+        if (!bh->device_build) {
+            upload_tree(bh);
+            upload_particles(bh, pos, mass);
+        }
+    });
+}
+
+gc_status gc_bh_set_build_mode(gc_bh *bh, int32_t device)
+{
+    return guard([&] {
+        GC_REQUIRE(bh, GC_E_VALUE, "null argument");
+        bh->device_build = device != 0;
     });
 }
 
@@ -395,8 +358,8 @@ gc_status gc_bh_sizes(gc_bh *bh, int64_t out[4])
     return guard([&] {
         GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
         sync_walk_stats(bh);
-        out[0] = bh->tree.n_nodes();
-        out[1] = (int64_t)bh->tree.buckets.size();
+        out[0] = bh->n_nodes;
+        out[1] = bh->n_buckets;
         out[2] = bh->n_list_entries;
         out[3] = bh->n_union;
     });
@@ -407,6 +370,7 @@ gc_status gc_bh_get_tree(gc_bh *bh, double *center, double *half, double *mass, 
 {
     return guard([&] {
         GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
+        ensure_host_tree(bh);
         const HostTree &t = bh->tree;
         const int64_t nn = t.n_nodes();
         const int d = t.dim;
@@ -440,7 +404,7 @@ gc_status gc_bh_get_lists(gc_bh *bh, int64_t *ptr, int64_t *ids, int8_t *kind, i
         GC_REQUIRE(bh && bh->have_union, GC_E_STATE, "no device walk has run");
         sync_walk_stats(bh);
         cudaStream_t s = bh->ctx->stream;
-        const int64_t nb = (int64_t)bh->tree.buckets.size();
+        const int64_t nb = bh->n_buckets;
         std::vector<int64_t> st(2 * nb);
         bh->d_bstat.download(st.data(), 2 * nb, s);
         GC_CUDA(cudaStreamSynchronize(s));
@@ -473,7 +437,8 @@ gc_status gc_bh_set_lists(gc_bh *bh, int64_t n_buckets, const int64_t *ptr, cons
 {
     return guard([&] {
         GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
-        GC_REQUIRE(n_buckets == (int64_t)bh->tree.buckets.size(), GC_E_VALUE, "list count != bucket count");
+        GC_REQUIRE(n_buckets == bh->n_buckets, GC_E_VALUE, "list count != bucket count");
+        ensure_host_tree(bh);
         cudaStream_t s = bh->ctx->stream;
         const HostTree &t = bh->tree;
         std::vector<int64_t> np(n_buckets + 1, 0), pp(n_buckets + 1, 0);
@@ -522,8 +487,8 @@ gc_status gc_bh_forces(gc_bh *bh, double g, double eps, double *out)
     return guard([&] {
         GC_REQUIRE(bh && bh->have_tree && out, GC_E_STATE, "no particles set");
         launch_forces(bh, g, eps);
-        bh->d_out.download(out, bh->tree.n * bh->tree.dim, bh->ctx->stream);
-        bh->d2h += bh->tree.n * bh->tree.dim * (int64_t)sizeof(double);
+        bh->d_out.download(out, bh->n * bh->dim, bh->ctx->stream);
+        bh->d2h += bh->n * bh->dim * (int64_t)sizeof(double);
         GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
         if (bh->have_union) {  // surface a deferred walk overflow
             int flag = 0;
@@ -540,8 +505,8 @@ gc_status gc_bh_forces_potential(gc_bh *bh, double g, double eps, double *out, d
         GC_REQUIRE(bh && bh->have_tree && out && pot, GC_E_STATE, "no particles set");
         GC_REQUIRE(bh->have_union, GC_E_STATE, "potentials need device lists (gc_bh_walk)");
         launch_forces(bh, g, eps, true);
-        bh->d_out.download(out, bh->tree.n * bh->tree.dim, bh->ctx->stream);
-        bh->d_pot.download(pot, bh->tree.n, bh->ctx->stream);
+        bh->d_out.download(out, bh->n * bh->dim, bh->ctx->stream);
+        bh->d_pot.download(pot, bh->n, bh->ctx->stream);
         GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
     });
 }
@@ -551,6 +516,7 @@ gc_status gc_bh_interactions(gc_bh *bh, int64_t *out)
     return guard([&] {
         GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
         sync_walk_stats(bh);
+        ensure_host_tree(bh);
         int64_t tot = 0;
         const HostTree &t = bh->tree;
         for (size_t b = 0; b < bh->h_item_count.size(); ++b) tot += t.pcount[t.buckets[b]] * bh->h_item_count[b];
@@ -578,7 +544,7 @@ gc_status gc_bh_groups(gc_bh *bh, int64_t *n_walk_groups, int64_t *wg_first_buck
         *n_walk_groups = (int64_t)bh->h_wg.size();
         if (wg_first_bucket) {
             for (size_t g = 0; g < bh->h_wg.size(); ++g) wg_first_bucket[g] = bh->h_wg[g].bfirst;
-            wg_first_bucket[bh->h_wg.size()] = (int64_t)bh->tree.buckets.size();
+            wg_first_bucket[bh->h_wg.size()] = bh->n_buckets;
         }
     });
 }
@@ -588,6 +554,7 @@ gc_status gc_bh_bucket_work(gc_bh *bh, int64_t *work)
     return guard([&] {
         GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
         sync_walk_stats(bh);
+        ensure_host_tree(bh);
         const HostTree &t = bh->tree;
         for (size_t b = 0; b < t.buckets.size(); ++b)
             work[b] = b < bh->h_item_count.size() ? t.pcount[t.buckets[b]] * bh->h_item_count[b] : 0;

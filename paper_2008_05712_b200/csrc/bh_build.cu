@@ -1,0 +1,627 @@
+// bh_build.cu -- bucket-tree build on the GPU, bit-identical to the reference
+// build_bucket_tree + _fill_mass + _collect_buckets (hr/workloads/nbody.py:78-143).
+//
+//  1. Octant keys.  Every particle descends the reference's cells in float64:
+//     digit q_L = sum_k (x_k >= c_k) << k, child centre c + (+-1)*half/2
+//     (nbody.py:97-108), for every level at which a node may still split
+//     (half >= 1e-9, nbody.py:94).  3 bits per level, two 64-bit words.
+//  2. One stable radix sort by (key, original id): every node of the
+//     reference is a contiguous range of this order, its children are the
+//     sub-ranges of equal next digit in ascending digit (= octant) order.
+//  3. Level-synchronous expansion: at each level the splitting nodes
+//     (count > bucket_size and half >= 1e-9) are cut where the level digit
+//     changes; children are numbered in position order, which is the
+//     reference's breadth-first id order.  Non-splitting nodes are buckets.
+//  4. Buckets sorted by position = depth-first order; each bucket's particles
+//     re-sorted by original id (the reference keeps ascending particle_idx).
+//  5. Masses/centres of mass with the reference's float64 rounding sequence:
+//     bucket mass = numpy pairwise sum, COM = sequential column sum / mass;
+//     internal nodes add children in order, deepest level first.
+//  6. Force/walk records, bucket geometry and walk/force groups in HBM.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "bh_state.h"
+
+namespace gc {
+
+constexpr int BB_TPB = 256;
+constexpr int MAX_KEY_LEVELS = 42;  // 2 x 21 levels x 3 bits
+
+__device__ __forceinline__ int key_digit(unsigned long long k1, unsigned long long k2, int L)
+{
+    return L < 21 ? (int)((k1 >> (3 * (20 - L))) & 7ull) : (int)((k2 >> (3 * (41 - L))) & 7ull);
+}
+
+__global__ void bb_keys(int n, int dim, const double *__restrict__ pos, double box, int nlev,
+                        unsigned long long *__restrict__ k1, unsigned long long *__restrict__ k2, int *__restrict__ idx)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double c[3], x[3];
+    for (int k = 0; k < 3; ++k) {
+        c[k] = __ddiv_rn(box, 2.0);
+        x[k] = k < dim ? pos[(int64_t)i * dim + k] : 0.0;
+    }
+    double h = __ddiv_rn(box, 2.0);
+    unsigned long long a = 0, b = 0;
+    for (int L = 0; L < nlev; ++L) {
+        int q = 0;
+        for (int k = 0; k < dim; ++k) q |= (x[k] >= c[k] ? 1 : 0) << k;
+        if (L < 21) a |= (unsigned long long)q << (3 * (20 - L));
+        else b |= (unsigned long long)q << (3 * (41 - L));
+        const double ch = __ddiv_rn(h, 2.0);
+        for (int k = 0; k < dim; ++k) c[k] = __dadd_rn(c[k], ((q >> k) & 1) ? ch : -ch);
+        h = ch;
+    }
+    k1[i] = a;
+    k2[i] = b;
+    idx[i] = i;
+}
+
+__global__ void bb_fill(int n, int *p, int v)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ void bb_iota(int n, int v0, int *p)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v0 + i;
+}
+
+__global__ void bb_gather_u64(int n, const int *__restrict__ perm, const unsigned long long *__restrict__ src,
+                              unsigned long long *__restrict__ dst)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[perm[i]];
+}
+
+// positions that start a child of a splitting node at level L
+__global__ void bb_child_flags(int n, int L, const int *__restrict__ posnode, const unsigned char *__restrict__ split,
+                               const int *__restrict__ lstart, const unsigned long long *__restrict__ k1,
+                               const unsigned long long *__restrict__ k2, unsigned char *__restrict__ flag)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int p = posnode[i];
+    unsigned char f = 0;
+    if (p >= 0 && split[p]) {
+        f = i == lstart[p] || key_digit(k1[i], k2[i], L) != key_digit(k1[i - 1], k2[i - 1], L);
+    }
+    flag[i] = f;
+}
+
+__global__ void bb_level_split(int m, const int *__restrict__ lcount, double half, long long bucket,
+                               unsigned char *__restrict__ split)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < m) split[p] = lcount[p] > bucket && half >= 1e-9;
+}
+
+// children of level L: counts, centres, global ids and parent links
+__global__ void bb_children(int mc, int L, int next_id, const int *__restrict__ cstart, const int *__restrict__ posnode,
+                            const int *__restrict__ lstart, const int *__restrict__ lcount, const int *__restrict__ lid,
+                            const double4 *__restrict__ lcenter, int dim, const unsigned long long *__restrict__ k1,
+                            const unsigned long long *__restrict__ k2, int *__restrict__ ccount,
+                            double4 *__restrict__ ccenter, int *__restrict__ first_child, int *__restrict__ nchild)
+{
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= mc) return;
+    const int i = cstart[c];
+    const int p = posnode[i];
+    const int pend = lstart[p] + lcount[p];
+    const int nxt = c + 1 < mc ? cstart[c + 1] : pend;
+    const int end = nxt < pend ? nxt : pend;
+    ccount[c] = end - i;
+    const int q = key_digit(k1[i], k2[i], L);
+    const double4 pc = lcenter[p];
+    const double ch = __ddiv_rn(pc.w, 2.0);
+    double4 cc;
+    cc.x = dim > 0 ? __dadd_rn(pc.x, (q & 1) ? ch : -ch) : pc.x;
+    cc.y = dim > 1 ? __dadd_rn(pc.y, (q & 2) ? ch : -ch) : pc.y;
+    cc.z = dim > 2 ? __dadd_rn(pc.z, (q & 4) ? ch : -ch) : pc.z;
+    cc.w = ch;
+    ccenter[c] = cc;
+    if (i == lstart[p]) first_child[lid[p]] = next_id + c;
+    atomicAdd(&nchild[lid[p]], 1);
+}
+
+// level-local node of every position after the split (-1: finished in a bucket)
+__global__ void bb_posnode(int n, int *__restrict__ posnode, const unsigned char *__restrict__ split, int mc,
+                           const int *__restrict__ cstart)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int p = posnode[i];
+    if (p < 0) return;
+    if (!split[p]) {
+        posnode[i] = -1;
+        return;
+    }
+    int lo = 0, hi = mc;  // last child start <= i
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (cstart[mid] <= i) lo = mid;
+        else hi = mid;
+    }
+    posnode[i] = lo;
+}
+
+// record the level's nodes in the global arrays; non-splitting ones are buckets
+__global__ void bb_store_level(int m, int id0, const int *__restrict__ lstart, const int *__restrict__ lcount,
+                               const double4 *__restrict__ lcenter, const unsigned char *__restrict__ split,
+                               double4 *__restrict__ ncenter, int *__restrict__ pstart, int *__restrict__ pcount,
+                               int *__restrict__ leaf_key, int *__restrict__ leaf_id, int *__restrict__ nleaf)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= m) return;
+    const int id = id0 + p;
+    ncenter[id] = lcenter[p];
+    pstart[id] = lstart[p];
+    pcount[id] = split[p] ? 0 : lcount[p];
+    if (!split[p]) {
+        const int k = atomicAdd(nleaf, 1);
+        leaf_key[k] = lstart[p];
+        leaf_id[k] = id;
+    }
+}
+
+// numpy pairwise summation (np.sum of a 1-D float64 array)
+__device__ double np_pairwise(const double *a, int n)
+{
+    if (n < 8) {
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s = __dadd_rn(s, a[i]);
+        return s;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        int i = 8;
+        const int lim = n - (n % 8);
+        for (; i < lim; i += 8)
+            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+        double s = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                             __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < n; ++i) s = __dadd_rn(s, a[i]);
+        return s;
+    }
+    int h = n / 2;
+    h -= h % 8;
+    return __dadd_rn(np_pairwise(a, h), np_pairwise(a + h, n - h));
+}
+
+constexpr int BB_SMALL = 32;  // buckets up to this size sum from registers
+
+// bucket mass (pairwise) and COM (sequential column sums), nbody.py:124-128
+__global__ void bb_bucket_mass(int nb, int dim, const int *__restrict__ buckets, const int *__restrict__ pstart,
+                               const int *__restrict__ pcount, const int *__restrict__ pidx,
+                               const double *__restrict__ pos, const double *__restrict__ mass,
+                               double *__restrict__ nmass, double4 *__restrict__ com, double *__restrict__ scratch)
+{
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    const int id = buckets[b];
+    const int s = pstart[id], c = pcount[id];
+    double mloc[BB_SMALL];
+    const double *mb;
+    if (c <= BB_SMALL) {
+        for (int i = 0; i < c; ++i) mloc[i] = mass[pidx[s + i]];
+        mb = mloc;
+    } else {
+        for (int i = 0; i < c; ++i) scratch[s + i] = mass[pidx[s + i]];
+        mb = scratch + s;
+    }
+    const double m = np_pairwise(mb, c);
+    nmass[id] = m;
+    double cm[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < dim; ++k) {
+        double acc = __dmul_rn(pos[(int64_t)pidx[s] * dim + k], mb[0]);
+        for (int i = 1; i < c; ++i) acc = __dadd_rn(acc, __dmul_rn(pos[(int64_t)pidx[s + i] * dim + k], mb[i]));
+        cm[k] = __ddiv_rn(acc, m);
+    }
+    com[id] = make_double4(cm[0], cm[1], cm[2], 0.0);
+}
+
+// internal nodes of one level: children in order (nbody.py:129-135)
+__global__ void bb_internal_mass(int id0, int m, int dim, const int *__restrict__ first_child,
+                                 const int *__restrict__ nchild, double *__restrict__ nmass, double4 *__restrict__ com)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= m) return;
+    const int id = id0 + p;
+    const int fc = first_child[id];
+    if (fc < 0) return;
+    double ms = 0.0, c3[3] = {0.0, 0.0, 0.0};
+    for (int ch = fc; ch < fc + nchild[id]; ++ch) {
+        const double cmass = nmass[ch];
+        const double4 cc = com[ch];
+        ms = __dadd_rn(ms, cmass);
+        c3[0] = __dadd_rn(c3[0], __dmul_rn(cc.x, cmass));
+        if (dim > 1) c3[1] = __dadd_rn(c3[1], __dmul_rn(cc.y, cmass));
+        if (dim > 2) c3[2] = __dadd_rn(c3[2], __dmul_rn(cc.z, cmass));
+    }
+    nmass[id] = ms;
+    com[id] = make_double4(__ddiv_rn(c3[0], ms), dim > 1 ? __ddiv_rn(c3[1], ms) : 0.0,
+                           dim > 2 ? __ddiv_rn(c3[2], ms) : 0.0, 0.0);
+}
+
+// walk/force records of every node (same encoding as the host upload path)
+__global__ void bb_records(int nn, const double4 *__restrict__ com, const double *__restrict__ nmass,
+                           const int *__restrict__ first_child, const int *__restrict__ nchild,
+                           const int *__restrict__ pstart, const int *__restrict__ pcount,
+                           const double4 *__restrict__ ncenter, float4 *__restrict__ recs, double4 *__restrict__ com64,
+                           float4 *__restrict__ rec_hi, float4 *__restrict__ rec_lo, int2 *__restrict__ prange,
+                           double *__restrict__ cmax)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nn) return;
+    const double4 c = com[i];
+    const float hx = (float)c.x, hy = (float)c.y, hz = (float)c.z;
+    const int fc = first_child[i];
+    const int word = fc < 0 ? -pcount[i] : ((fc << 3) | (nchild[i] - 1));
+    recs[i] = make_float4(hx, hy, hz, __int_as_float(word));
+    com64[i] = c;
+    rec_hi[i] = make_float4(hx, hy, hz, (float)nmass[i]);
+    rec_lo[i] = make_float4((float)(c.x - (double)hx), (float)(c.y - (double)hy), (float)(c.z - (double)hz), 0.f);
+    prange[i] = make_int2(pstart[i], pcount[i]);
+    const double4 g = ncenter[i];
+    double mx = fmax(fmax(fabs(c.x), fabs(c.y)), fabs(c.z));
+    mx = fmax(mx, fmax(fmax(fabs(g.x), fabs(g.y)), fabs(g.z)) + g.w);
+    cmax[i] = mx;
+}
+
+__global__ void bb_buckets(int nb, int dim, const int *__restrict__ buckets, const double4 *__restrict__ ncenter,
+                           const int *__restrict__ pstart, const int *__restrict__ pcount, const int *__restrict__ pidx,
+                           const double *__restrict__ pos, const double *__restrict__ mass, double4 *__restrict__ bgeo,
+                           float4 *__restrict__ bgeo32, int2 *__restrict__ brange, int *__restrict__ bids,
+                           int *__restrict__ part_bucket, float4 *__restrict__ parts, int *__restrict__ porder)
+{
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    const int id = buckets[b];
+    const double4 g = ncenter[id];
+    bgeo[b] = g;
+    const float f0 = (float)g.x, f1 = (float)g.y, f2 = (float)g.z, fh = (float)g.w;
+    const bool ex = f0 == g.x && f1 == g.y && f2 == g.z && fh == g.w;
+    bgeo32[b] = make_float4(f0, f1, f2, ex ? fh : -1.f);
+    const int s = pstart[id], c = pcount[id];
+    brange[b] = make_int2(s, c);
+    bids[b] = b;
+    for (int k = 0; k < c; ++k) {
+        const int p = pidx[s + k];
+        part_bucket[s + k] = b;
+        porder[s + k] = p;
+        float x[3] = {0.f, 0.f, 0.f};
+        for (int d = 0; d < dim; ++d) x[d] = (float)pos[(int64_t)p * dim + d];
+        parts[s + k] = make_float4(x[0], x[1], x[2], (float)mass[p]);
+    }
+}
+
+// walk groups of 32 buckets; force groups greedily packed (<= 32 targets)
+// inside each walk group, as the host path: pass 0 counts, pass 1 writes
+template <int PASS>
+__global__ void bb_groups(int nwg, int nb, const int2 *__restrict__ brange, int *__restrict__ nfg_of,
+                          const int *__restrict__ fg_base, WalkGroup *__restrict__ wg, ForceGroup *__restrict__ fg,
+                          unsigned *__restrict__ fgmask, int *__restrict__ bad)
+{
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= nwg) return;
+    const int b0 = w * 32, b1 = min(nb, b0 + 32);
+    int k = 0;
+    for (int b = b0; b < b1;) {
+        ForceGroup g;
+        g.pstart = brange[b].x;
+        g.wg = w;
+        g.bmask = 0u;
+        int tg = 0;
+        while (b < b1 && tg + brange[b].y <= 32) {
+            tg += brange[b].y;
+            g.bmask |= 1u << (b - b0);
+            ++b;
+        }
+        if (tg == 0) {
+            atomicOr(bad, 1);
+            return;
+        }
+        g.ntarget = tg;
+        if (PASS == 1) {
+            fg[fg_base[w] + k] = g;
+            fgmask[fg_base[w] + k] = g.bmask;
+        }
+        ++k;
+    }
+    if (PASS == 0) nfg_of[w] = k;
+    else wg[w] = WalkGroup{b0, b1 - b0, fg_base[w], k};
+}
+
+template <class F>
+void cubc(gc_ctx *ctx, F &&f)
+{
+    size_t bytes = 0;
+    GC_CUDA(f(nullptr, bytes));
+    ctx->scratch.resize(bytes);
+    GC_CUDA(f(ctx->scratch.p, bytes));
+}
+
+void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int64_t n64, int dim, double box,
+                       int64_t bucket)
+{
+    gc_ctx *ctx = bh->ctx;
+    cudaStream_t s = ctx->stream;
+    GC_REQUIRE(n64 < (1 << 30), GC_E_VALUE, "too many particles for the device build");
+    const int n = (int)n64;
+    // levels at which a node may still split (half >= 1e-9, nbody.py:94)
+    int nlev = 0;
+    for (double h = box / 2.0; h >= 1e-9 && nlev <= MAX_KEY_LEVELS; h /= 2.0) ++nlev;
+    GC_REQUIRE(nlev <= MAX_KEY_LEVELS, GC_E_VALUE, "box too large for the device build keys");
+
+    DBuf<double> pos, mass, scratch;
+    pos.upload(pos_h, (size_t)n * dim, s);
+    mass.upload(mass_h, n, s);
+    bh->h2d += (int64_t)n * (dim + 1) * (int64_t)sizeof(double);
+    DBuf<unsigned long long> k1, k2, k1p, k1s, k2s;
+    DBuf<int> idx, perm1, perm;
+    k1.resize(n); k2.resize(n); k1p.resize(n); k1s.resize(n); k2s.resize(n);
+    idx.resize(n); perm1.resize(n); perm.resize(n);
+    bb_keys<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, dim, pos.p, box, nlev, k1.p, k2.p, idx.p);
+    check_launch("bb_keys");
+    // stable sort by (k1, k2), ties by original id: LSD on k2 then k1
+    cubc(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, k2.p, k2s.p, idx.p, perm1.p, n, 0, 64, s);
+    });
+    bb_gather_u64<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, perm1.p, k1.p, k1p.p);
+    cubc(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, k1p.p, k1s.p, perm1.p, perm.p, n, 0, 64, s);
+    });
+    bb_gather_u64<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, perm.p, k2.p, k2s.p);
+    check_launch("bb sort");
+
+    // level-synchronous expansion
+    std::vector<int> lvl_first{0};
+    DBuf<int> lstart, lcount, lid, cstart, ccount, posnode, nsel, leaf_key, leaf_id, nleaf;
+    DBuf<double4> lcenter, ccenter;
+    DBuf<unsigned char> split, flag;
+    const int cap_nodes = 3 * n + 1024;
+    bh->d_ncenter.resize(cap_nodes);
+    bh->d_pstart.resize(cap_nodes);
+    bh->d_pcount.resize(cap_nodes);
+    bh->d_first_child.resize(cap_nodes);
+    bh->d_nchild.resize(cap_nodes);
+    bb_fill<<<grid_for(cap_nodes, BB_TPB), BB_TPB, 0, s>>>(cap_nodes, bh->d_first_child.p, -1);
+    bh->d_nchild.zero(s);
+    leaf_key.resize(n + 1);
+    leaf_id.resize(n + 1);
+    nleaf.resize(1);
+    nleaf.zero(s);
+    posnode.resize(n);
+    GC_CUDA(cudaMemsetAsync(posnode.p, 0, sizeof(int) * n, s));
+    flag.resize(n);
+    cstart.resize(n);
+    nsel.resize(1);
+    // level 0: the root
+    {
+        int z = 0;
+        lstart.upload(&z, 1, s);
+        lcount.upload(&n, 1, s);
+        lid.upload(&z, 1, s);
+        const double4 root = make_double4(box / 2.0, dim > 1 ? box / 2.0 : 0.0, dim > 2 ? box / 2.0 : 0.0, box / 2.0);
+        lcenter.upload(&root, 1, s);
+    }
+    int m = 1, next_id = 1;
+    double half = box / 2.0;
+    for (int L = 0;; ++L) {
+        split.resize(m);
+        bb_level_split<<<grid_for(m, BB_TPB), BB_TPB, 0, s>>>(m, lcount.p, half, bucket, split.p);
+        bb_store_level<<<grid_for(m, BB_TPB), BB_TPB, 0, s>>>(m, lvl_first.back(), lstart.p, lcount.p, lcenter.p,
+                                                              split.p, bh->d_ncenter.p, bh->d_pstart.p,
+                                                              bh->d_pcount.p, leaf_key.p, leaf_id.p, nleaf.p);
+        if (L >= nlev) break;  // no node of this level can split (half < 1e-9)
+        bb_child_flags<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, L, posnode.p, split.p, lstart.p, k1s.p, k2s.p,
+                                                               flag.p);
+        check_launch("bb level");
+        {
+            auto it = cub::CountingInputIterator<int>(0);
+            cubc(ctx, [&](void *t, size_t &b) {
+                return cub::DeviceSelect::Flagged(t, b, it, flag.p, cstart.p, nsel.p, n, s);
+            });
+        }
+        int mc = 0;
+        GC_CUDA(cudaMemcpyAsync(&mc, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        GC_CUDA(cudaStreamSynchronize(s));
+        if (mc == 0) break;
+        GC_REQUIRE(next_id + mc <= cap_nodes, GC_E_VALUE, "node capacity exceeded");
+        ccount.resize(mc);
+        ccenter.resize(mc);
+        bb_children<<<grid_for(mc, BB_TPB), BB_TPB, 0, s>>>(mc, L, next_id, cstart.p, posnode.p, lstart.p, lcount.p,
+                                                            lid.p, lcenter.p, dim, k1s.p, k2s.p, ccount.p, ccenter.p,
+                                                            bh->d_first_child.p, bh->d_nchild.p);
+        bb_posnode<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, posnode.p, split.p, mc, cstart.p);
+        check_launch("bb children");
+        // the children become the next level
+        lvl_first.push_back(next_id);
+        std::swap(lstart.p, cstart.p);
+        std::swap(lstart.n, cstart.n);
+        std::swap(lstart.cap, cstart.cap);
+        cstart.resize(n);
+        std::swap(lcount.p, ccount.p);
+        std::swap(lcount.n, ccount.n);
+        std::swap(lcount.cap, ccount.cap);
+        std::swap(lcenter.p, ccenter.p);
+        std::swap(lcenter.n, ccenter.n);
+        std::swap(lcenter.cap, ccenter.cap);
+        lid.resize(mc);
+        bb_iota<<<grid_for(mc, BB_TPB), BB_TPB, 0, s>>>(mc, next_id, lid.p);
+        next_id += mc;
+        m = mc;
+        half = half / 2.0;
+    }
+    lvl_first.push_back(next_id);
+    const int nn = next_id;
+    int nb = 0;
+    GC_CUDA(cudaMemcpyAsync(&nb, nleaf.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    GC_CUDA(cudaStreamSynchronize(s));
+
+    // buckets in depth-first order = by start position
+    DBuf<int> lk_s;
+    bh->d_buckets.resize(nb);
+    lk_s.resize(nb);
+    cubc(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, leaf_key.p, lk_s.p, leaf_id.p, bh->d_buckets.p, nb, 0, 32, s);
+    });
+    // particles inside each bucket: ascending original id
+    DBuf<int> offs, pidx;
+    offs.resize(nb + 1);
+    {
+        // offsets = sorted bucket starts, plus n
+        GC_CUDA(cudaMemcpyAsync(offs.p, lk_s.p, sizeof(int) * nb, cudaMemcpyDeviceToDevice, s));
+        GC_CUDA(cudaMemcpyAsync(offs.p + nb, &n, sizeof(int), cudaMemcpyHostToDevice, s));
+    }
+    pidx.resize(n);
+    cubc(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceSegmentedSort::SortKeys(t, b, perm.p, pidx.p, n, nb, offs.p, offs.p + 1, s);
+    });
+    check_launch("bb buckets");
+
+    // masses and centres of mass
+    bh->d_nmass.resize(nn);
+    DBuf<double4> com;
+    com.resize(nn);
+    scratch.resize(n);
+    bb_bucket_mass<<<grid_for(nb, BB_TPB), BB_TPB, 0, s>>>(nb, dim, bh->d_buckets.p, bh->d_pstart.p, bh->d_pcount.p,
+                                                           pidx.p, pos.p, mass.p, bh->d_nmass.p, com.p, scratch.p);
+    for (int L = (int)lvl_first.size() - 2; L >= 0; --L) {
+        const int id0 = lvl_first[L], mL = lvl_first[L + 1] - id0;
+        bb_internal_mass<<<grid_for(mL, BB_TPB), BB_TPB, 0, s>>>(id0, mL, dim, bh->d_first_child.p, bh->d_nchild.p,
+                                                                bh->d_nmass.p, com.p);
+    }
+    check_launch("bb mass");
+
+    // records
+    DBuf<double> cmax, cmax_out;
+    cmax.resize(nn);
+    cmax_out.resize(1);
+    bh->d_recs.resize(nn);
+    bh->d_com64.resize(nn);
+    bh->d_rec_hi.resize(nn);
+    bh->d_rec_lo.resize(nn);
+    bh->d_prange.resize(nn);
+    bb_records<<<grid_for(nn, BB_TPB), BB_TPB, 0, s>>>(nn, com.p, bh->d_nmass.p, bh->d_first_child.p, bh->d_nchild.p,
+                                                       bh->d_pstart.p, bh->d_pcount.p, bh->d_ncenter.p, bh->d_recs.p,
+                                                       bh->d_com64.p, bh->d_rec_hi.p, bh->d_rec_lo.p, bh->d_prange.p,
+                                                       cmax.p);
+    cubc(ctx, [&](void *t, size_t &b) { return cub::DeviceReduce::Max(t, b, cmax.p, cmax_out.p, nn, s); });
+    bh->d_bgeo.resize(nb);
+    bh->d_bgeo32.resize(nb);
+    bh->d_brange.resize(nb);
+    bh->d_bucket_ids.resize(nb);
+    bh->d_part_bucket.resize(n);
+    bh->d_parts.resize(n);
+    bh->d_porder.resize(n);
+    bb_buckets<<<grid_for(nb, BB_TPB), BB_TPB, 0, s>>>(nb, dim, bh->d_buckets.p, bh->d_ncenter.p, bh->d_pstart.p,
+                                                       bh->d_pcount.p, pidx.p, pos.p, mass.p, bh->d_bgeo.p,
+                                                       bh->d_bgeo32.p, bh->d_brange.p, bh->d_bucket_ids.p,
+                                                       bh->d_part_bucket.p, bh->d_parts.p, bh->d_porder.p);
+    check_launch("bb records");
+    // groups
+    const int nwg = (nb + 31) / 32;
+    DBuf<int> nfg_of, fg_base, bad;
+    nfg_of.resize(nwg + 1);
+    fg_base.resize(nwg + 1);
+    bad.resize(1);
+    bad.zero(s);
+    bb_groups<0><<<grid_for(nwg, BB_TPB), BB_TPB, 0, s>>>(nwg, nb, bh->d_brange.p, nfg_of.p, nullptr, nullptr,
+                                                          nullptr, nullptr, bad.p);
+    GC_CUDA(cudaMemsetAsync(nfg_of.p + nwg, 0, sizeof(int), s));
+    cubc(ctx, [&](void *t, size_t &b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, nfg_of.p, fg_base.p, nwg + 1, s);
+    });
+    int nfg = 0, badh = 0;
+    GC_CUDA(cudaMemcpyAsync(&nfg, fg_base.p + nwg, sizeof(int), cudaMemcpyDeviceToHost, s));
+    GC_CUDA(cudaMemcpyAsync(&badh, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    double cm = 0.0;
+    GC_CUDA(cudaMemcpyAsync(&cm, cmax_out.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    GC_CUDA(cudaStreamSynchronize(s));
+    GC_REQUIRE(!badh, GC_E_VALUE, "bucket with more than 32 particles (coincident points) on the group path");
+    bh->d_wg.resize(nwg);
+    bh->d_fg.resize(nfg);
+    bh->d_fgmask.resize(nfg);
+    bb_groups<1><<<grid_for(nwg, BB_TPB), BB_TPB, 0, s>>>(nwg, nb, bh->d_brange.p, nullptr, fg_base.p, bh->d_wg.p,
+                                                          bh->d_fg.p, bh->d_fgmask.p, bad.p);
+    check_launch("bb groups");
+    bh->h_wg.resize(nwg);
+    bh->h_fg.resize(nfg);
+    bh->h_fgmask.resize(nfg);
+    bh->d_wg.download(bh->h_wg.data(), nwg, s);
+    bh->d_fg.download(bh->h_fg.data(), nfg, s);
+    bh->d_fgmask.download(bh->h_fgmask.data(), nfg, s);
+    GC_CUDA(cudaStreamSynchronize(s));
+    bh->d2h += (int64_t)nwg * sizeof(WalkGroup) + (int64_t)nfg * (sizeof(ForceGroup) + sizeof(unsigned));
+    const double delta = 1.25 * 6.0 * std::ldexp(1.0, -24) * std::max(cm, 1e-30);
+    bh->walk_dd2 = (float)(2.0 * delta * (1.0 + 1e-6));
+    bh->walk_dd3 = (float)(3.0 * delta * delta * (1.0 + 1e-6));
+    bh->n = n;
+    bh->dim = dim;
+    bh->box = box;
+    bh->bucket_size = bucket;
+    bh->n_nodes = nn;
+    bh->n_buckets = nb;
+    bh->host_tree_valid = false;
+}
+
+// host mirror of a device-built tree (parity checks, list validation)
+void ensure_host_tree(gc_bh *bh)
+{
+    if (bh->host_tree_valid) return;
+    cudaStream_t s = bh->ctx->stream;
+    HostTree &t = bh->tree;
+    const int64_t nn = bh->n_nodes, nb = bh->n_buckets;
+    std::vector<double4> c(nn), cm(nn);
+    std::vector<double> m(nn);
+    std::vector<int> fc(nn), nc(nn), ps(nn), pc(nn), bk(nb), po(bh->n);
+    bh->d_ncenter.download(c.data(), nn, s);
+    bh->d_com64.download(cm.data(), nn, s);
+    bh->d_nmass.download(m.data(), nn, s);
+    bh->d_first_child.download(fc.data(), nn, s);
+    bh->d_nchild.download(nc.data(), nn, s);
+    bh->d_pstart.download(ps.data(), nn, s);
+    bh->d_pcount.download(pc.data(), nn, s);
+    bh->d_buckets.download(bk.data(), nb, s);
+    bh->d_porder.download(po.data(), bh->n, s);
+    GC_CUDA(cudaStreamSynchronize(s));
+    t.n = bh->n;
+    t.dim = bh->dim;
+    t.box = bh->box;
+    t.bucket_size = bh->bucket_size;
+    t.center.resize(3 * nn);
+    t.com.resize(3 * nn);
+    t.half.resize(nn);
+    t.node_mass.assign(m.begin(), m.end());
+    t.first_child.resize(nn);
+    t.n_child.resize(nn);
+    t.pstart.resize(nn);
+    t.pcount.resize(nn);
+    for (int64_t i = 0; i < nn; ++i) {
+        t.center[3 * i] = c[i].x;
+        t.center[3 * i + 1] = c[i].y;
+        t.center[3 * i + 2] = c[i].z;
+        t.half[i] = c[i].w;
+        t.com[3 * i] = cm[i].x;
+        t.com[3 * i + 1] = cm[i].y;
+        t.com[3 * i + 2] = cm[i].z;
+        t.first_child[i] = fc[i];
+        t.n_child[i] = fc[i] < 0 ? 0 : nc[i];
+        t.pstart[i] = ps[i];
+        t.pcount[i] = pc[i];
+    }
+    t.buckets.assign(bk.begin(), bk.end());
+    t.order.assign(po.begin(), po.end());
+    bh->host_tree_valid = true;
+}
+
+}  // namespace gc

@@ -200,7 +200,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
 }
 
 // Per-bucket walk_order / kind CSR from the union lists (parity + drop-in API).
-__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK)
+static __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK)
 union_to_lists_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const WalkGroup *__restrict__ wgroups,
                       const int64_t *__restrict__ gbase, const int64_t *__restrict__ gcount,
                       const int *__restrict__ uid, const uint2 *__restrict__ umask, const int64_t *__restrict__ bptr,

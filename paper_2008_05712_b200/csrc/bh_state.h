@@ -1,0 +1,80 @@
+// bh_state.h -- the Barnes-Hut handle shared by bh.cu (walk, forces, C ABI)
+// and bh_build.cu (device tree build).
+#pragma once
+#include "bh_kernels.cuh"
+#include "bh_tree.h"
+#include "common.cuh"
+
+using namespace gc;
+
+struct gc_bh {
+    gc_ctx *ctx = nullptr;
+    HostTree tree;  // host mirror (valid when host_tree_valid)
+    bool have_tree = false;
+    bool host_tree_valid = false;
+    bool device_build = true;  // build the tree on the GPU (gc_bh_set_build_mode)
+    // tree metadata (always valid once particles are set)
+    int64_t n = 0, n_nodes = 0, n_buckets = 0, bucket_size = 8;
+    int dim = 3;
+    double box = 1.0;
+    // device tree topology (device build; downloaded on demand)
+    DBuf<double4> d_ncenter;  // per node: center.xyz, half
+    DBuf<double> d_nmass;
+    DBuf<int> d_first_child, d_nchild, d_pstart, d_pcount, d_buckets;
+    std::vector<WalkGroup> h_wg;
+    std::vector<ForceGroup> h_fg;
+    std::vector<unsigned> h_fgmask;
+    DBuf<unsigned> d_fgmask;
+    // device tree
+    DBuf<float4> d_recs;  // walk records: float32 com + packed links
+    DBuf<double4> d_com64;  // float64 com (exact opening test)
+    DBuf<double4> d_bgeo;  // per bucket (DFS index): center.xyz, half
+    DBuf<float4> d_bgeo32;  // float32 copy (w < 0: not exact in float32)
+    DBuf<float4> d_parts;  // DFS-sorted particles (x, y, z, m) fp32
+    DBuf<int> d_porder;  // original id of each sorted particle
+    DBuf<int> d_part_bucket;  // DFS bucket index of each sorted particle
+    DBuf<float4> d_rec_hi, d_rec_lo;  // force records: com hi (fp32) + mass, com lo
+    DBuf<int2> d_prange;  // per node: (first sorted particle, count) for buckets
+    DBuf<int2> d_brange;  // per bucket (DFS index): (first sorted particle, count)
+    DBuf<int> d_bucket_ids;  // identity member list for the member kernel
+    DBuf<WalkGroup> d_wg;
+    DBuf<ForceGroup> d_fg;
+    float walk_dd2 = 0.f, walk_dd3 = 0.f;
+    DBuf<float2> d_tt;
+    // union lists (device walk)
+    int rg0 = 0, rg1 = -1;  // walk-group range this handle evaluates (multi-GPU shard)
+    bool have_union = false;
+    bool cap_valid = false;
+    double cap_theta = -1.0;
+    DBuf<int64_t> d_gcount, d_gbase, d_gcap, d_bstat;
+    DBuf<int> d_uid;
+    DBuf<uint2> d_umask;
+    int64_t n_union = 0;
+    // per-bucket CSR (host-supplied lists)
+    bool have_member_lists = false;
+    DBuf<int64_t> d_nptr, d_pptr;
+    DBuf<int> d_naddr, d_paddr;
+    // outputs
+    DBuf<double> d_out, d_pot;
+    std::vector<int64_t> h_item_count;
+    int64_t n_list_entries = 0;
+    DBuf<int64_t> d_bptr;
+    DBuf<int> d_list_ids;
+    DBuf<int8_t> d_list_kind;
+    DBuf<int> d_flag;
+    WalkParams wp{};
+    bool stats_dirty = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t h2d = 0, d2h = 0;  // bytes moved host<->device since the last reset
+    ~gc_bh()
+    {
+        for (auto &e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+namespace gc {
+void device_build_tree(gc_bh *bh, const double *pos, const double *mass, int64_t n, int dim, double box,
+                       int64_t bucket_size);
+void ensure_host_tree(gc_bh *bh);
+}  // namespace gc

@@ -69,7 +69,7 @@ class TreeNode:
 class BucketTree:
     """Device-resident bucket tree (hr/workloads/nbody.py:71-75)."""
 
-    def __init__(self, ps: ParticleSet, bucket_size: int):
+    def __init__(self, ps: ParticleSet, bucket_size: int, device_build: bool = True):
         self.ps = ps
         self.bucket_size = int(bucket_size)
         self.dim = ps.positions.shape[1]
@@ -77,6 +77,7 @@ class BucketTree:
         self._ctx = L.context()
         self.handle = C.c_void_p()
         L.call("gc_bh_create", self._ctx.handle, C.byref(self.handle))
+        L.call("gc_bh_set_build_mode", self.handle, int(bool(device_build)))
         pos, m = L.f64(ps.positions), L.f64(ps.masses)
         L.call("gc_bh_set_particles", self.handle, self.n, self.dim, L.ptr(pos, L.f64p), L.ptr(m, L.f64p),
                float(ps.box), self.bucket_size)
@@ -145,12 +146,13 @@ class BucketTree:
         return [TreeNode(self, int(b)) for b in self.bucket_ids]
 
 
-def build_bucket_tree(ps: ParticleSet, bucket_size: int) -> BucketTree:
-    """hr/workloads/nbody.py:78-120 (host build of level-order ids + float64
-    mass/COM, uploaded to HBM)."""
+def build_bucket_tree(ps: ParticleSet, bucket_size: int, device_build: bool = True) -> BucketTree:
+    """hr/workloads/nbody.py:78-120: level-order ids, depth-first buckets,
+    float64 mass/COM with the reference's rounding -- built on the GPU
+    (csrc/bh_build.cu) or by the host C++ builder (device_build=False)."""
     if bucket_size < 1:
         raise ValueError("bucket_size must be >= 1")
-    return BucketTree(ps, bucket_size)
+    return BucketTree(ps, bucket_size, device_build)
 
 
 @dataclass
