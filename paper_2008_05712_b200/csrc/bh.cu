@@ -51,11 +51,7 @@ void upload_tree(gc_bh *bh)
         lo[i] = make_float4(l3[0], l3[1], l3[2], 0.f);
         pr[i] = make_int2((int)t.pstart[i], (int)t.pcount[i]);
     }
-    // |v32 - v64| <= delta for every opening-test component (walk_group_kernel):
-    // com rounding + two float32 subtractions, each <= 2^-24 * |operand|
-    const double delta = 1.25 * 6.0 * std::ldexp(1.0, -24) * std::max(cmax, 1e-30);
-    bh->walk_dd2 = (float)(2.0 * delta * (1.0 + 1e-6));
-    bh->walk_dd3 = (float)(3.0 * delta * delta * (1.0 + 1e-6));
+    set_tree_bounds(bh, cmax);
 
     std::vector<double4> bg(nb);
     std::vector<float4> bg32(nb);
@@ -149,20 +145,147 @@ void exclusive_scan(gc_ctx *ctx, const T *in, T *out, int64_t n)
     GC_CUDA(cub::DeviceScan::ExclusiveSum(ctx->scratch.p, bytes, in, out, n, ctx->stream));
 }
 
-// Per-walk host bookkeeping that needs the device stats (item counts,
-// entry totals) is done lazily, so a steady-state walk is fully asynchronous.
-void sync_walk_stats(gc_bh *bh)
+UnionPool pool_view(gc_bh *bh)
 {
-    if (!bh->stats_dirty) return;
+    UnionPool U;
+    U.uid = bh->d_uid.p;
+    U.umask = bh->d_umask.p;
+    U.cnext = bh->d_cnext.p;
+    U.gfirst = bh->d_gfirst.p;
+    U.gcount = bh->d_gcount.p;
+    U.top = bh->d_top.p;
+    U.nchunks = bh->pool_chunks;
+    return U;
+}
+
+void size_pool(gc_bh *bh, int64_t chunks)
+{
+    GC_REQUIRE(chunks * CHUNK < (1ll << 31), GC_E_VALUE, "union-list pool exceeds 2^31 entries");
+    bh->d_uid.resize(chunks * CHUNK);
+    bh->d_umask.resize(chunks * CHUNK);
+    bh->d_cnext.resize(chunks);
+    bh->pool_chunks = (int)chunks;
+}
+
+// Opening-test thresholds for (tree, theta).
+void walk_params(gc_bh *bh, double theta)
+{
+    if (bh->params_valid && bh->cap_theta == theta) return;
+    const double th2 = theta * theta;
+    const double root = bh->box;
+    // per-level float32 thresholds on s = d^2: accept iff s > size^2 / theta^2
+    std::vector<float2> tt(MAX_LEVELS);
+    for (int l = 0; l < MAX_LEVELS; ++l) {
+        const double size = std::ldexp(root, -l);
+        const double T = theta > 0.0 ? size * size / th2 : HUGE_VAL;
+        const float a = (float)(T * (1.0 + std::ldexp(1.0, -22)));
+        const float r = (float)(T * (1.0 - std::ldexp(1.0, -22)));
+        tt[l].x = std::nextafter(a, HUGE_VALF);
+        tt[l].y = std::isinf(r) ? r : std::nextafter(r, 0.f);
+    }
+    bh->d_tt.upload(tt.data(), MAX_LEVELS, bh->ctx->stream);
+    bh->wp.theta = theta;
+    bh->wp.theta2 = th2;
+    bh->wp.root_size = root;
+    bh->wp.dd2 = bh->walk_dd2;
+    bh->wp.dd3 = bh->walk_dd3;
+    bh->wp.tt = bh->d_tt.p;
+    bh->params_valid = true;
+    bh->cap_theta = theta;
+    bh->stats_valid = false;
+    bh->have_union = false;
+}
+
+// One walk launch over the handle's walk-group range (asynchronous).
+void launch_walk(gc_bh *bh, bool write, bool stats)
+{
     cudaStream_t s = bh->ctx->stream;
-    const int64_t nb = bh->n_buckets;
-    std::vector<int64_t> st(2 * nb);
-    int flag = 0;
-    bh->d_bstat.download(st.data(), 2 * nb, s);
+    const int nf = (int)bh->h_fg.size();
+    const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? (int)bh->h_wg.size() : bh->rg1;
+    const int ng = g1 - g0;
+    const WalkGroup *wg = bh->d_wg.p + g0;
+    const unsigned grid = grid_for(std::max(ng, 1), WARPS_PER_BLOCK);
+    bh->d_flag.resize(1);
+    bh->d_flag.zero(s);
+    if (stats) {
+        bh->d_bstat.resize(2 * bh->n_buckets);
+        bh->d_bstat.zero(s);
+    }
+    if (write) {
+        // first guess ~128 entries per bucket; an overflow grows it to the walk's demand
+        const int64_t guess = 2 * bh->n_buckets + 2 * (int64_t)nf + 64;
+        if (bh->pool_chunks < guess) size_pool(bh, guess);
+        bh->d_gfirst.resize(nf);
+        bh->d_gcount.resize(nf);
+        bh->d_gcount.zero(s);
+        bh->d_top.resize(1);
+        bh->d_top.zero(s);
+    }
+    if (ng <= 0) return;
+    const UnionPool U = pool_view(bh);
+    auto k = write ? (stats ? walk_group_kernel<true, true> : walk_group_kernel<true, false>)
+                   : walk_group_kernel<false, true>;
+    k<<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(ng, wg, bh->d_fgmask.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p,
+                                            bh->d_bgeo32.p, bh->wp, U, bh->d_bstat.p, bh->d_flag.p);
+    check_launch("walk_group_kernel");
+}
+
+// Synchronise and surface walk failures.  A pool overflow grows the pool to
+// the size the walk asked for and returns true (the caller re-walks).
+bool walk_overflowed(gc_bh *bh)
+{
+    cudaStream_t s = bh->ctx->stream;
+    int flag = 0, top = 0;
     bh->d_flag.download(&flag, 1, s);
+    if (bh->d_top.p) bh->d_top.download(&top, 1, s);
     GC_CUDA(cudaStreamSynchronize(s));
     GC_REQUIRE(!(flag & 1), GC_E_VALUE, "tree deeper than the walk stack (box too large for half_size >= 1e-9)");
-    GC_REQUIRE(!(flag & 2), GC_E_STATE, "walk list capacity overflow (re-run gc_bh_walk)");
+    if (flag & 2) {
+        size_pool(bh, (int64_t)top + top / 8 + 64);
+        return true;
+    }
+    return false;
+}
+
+// Device lists for theta: the walk writes the union pool (and the per-bucket
+// stats when requested).  Steady state (same tree and theta, stats known) is
+// fully asynchronous; a fresh walk with stats synchronises and retries on a
+// pool overflow.
+void run_walk(gc_bh *bh, double theta, bool want_stats)
+{
+    GC_REQUIRE(theta >= 0.0, GC_E_VALUE, "theta must be >= 0");
+    GC_REQUIRE(bh->have_tree, GC_E_STATE, "no particles set");
+    walk_params(bh, theta);
+    const bool stats = want_stats && !bh->stats_valid;
+    GC_CUDA(cudaEventRecord(bh->ev[0], bh->ctx->stream));
+    launch_walk(bh, true, stats);
+    GC_CUDA(cudaEventRecord(bh->ev[1], bh->ctx->stream));
+    bh->have_union = true;
+    bh->have_member_lists = false;
+    if (stats) {
+        while (walk_overflowed(bh)) launch_walk(bh, true, true);
+        bh->stats_valid = true;
+        bh->stats_dirty = true;
+    }
+}
+
+// Host copies of the per-bucket stats (item counts, entry totals); runs a
+// stats-only walk when the current tree/theta has none.
+void sync_walk_stats(gc_bh *bh)
+{
+    cudaStream_t s = bh->ctx->stream;
+    if (!bh->stats_valid) {
+        GC_REQUIRE(bh->params_valid, GC_E_STATE, "no walk has run (call gc_bh_walk)");
+        launch_walk(bh, false, true);
+        GC_REQUIRE(!walk_overflowed(bh), GC_E_STATE, "walk overflow in a stats-only walk");
+        bh->stats_valid = true;
+        bh->stats_dirty = true;
+    }
+    if (!bh->stats_dirty) return;
+    const int64_t nb = bh->n_buckets;
+    std::vector<int64_t> st(2 * nb);
+    bh->d_bstat.download(st.data(), 2 * nb, s);
+    GC_CUDA(cudaStreamSynchronize(s));
     bh->h_item_count.resize(nb);
     int64_t ent = 0;
     for (int64_t b = 0; b < nb; ++b) {
@@ -173,83 +296,11 @@ void sync_walk_stats(gc_bh *bh)
     bh->stats_dirty = false;
 }
 
-void run_walk(gc_bh *bh, double theta)
+// Make sure the union pool holds complete lists of the last walk.
+void ensure_union_complete(gc_bh *bh)
 {
-    GC_REQUIRE(theta >= 0.0, GC_E_VALUE, "theta must be >= 0");
-    GC_REQUIRE(bh->have_tree, GC_E_STATE, "no particles set");
-    gc_ctx *ctx = bh->ctx;
-    cudaStream_t s = ctx->stream;
-    const int nf = (int)bh->h_fg.size();  // lists are per force group
-    const int64_t nb = bh->n_buckets;
-    const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? (int)bh->h_wg.size() : bh->rg1;
-    const int ng = g1 - g0;
-    const WalkGroup *wg = bh->d_wg.p + g0;
-    const unsigned grid = grid_for(std::max(ng, 1), WARPS_PER_BLOCK);
-    const bool fresh = !bh->cap_valid || bh->cap_theta != theta;
-    if (fresh) {
-        bh->d_gcount.resize(nf);
-        bh->d_gbase.resize(nf + 1);
-        bh->d_gcap.resize(nf + 1);
-        bh->d_bstat.resize(2 * nb);
-        bh->d_flag.resize(1);
-        const double th2 = theta * theta;
-        const double root = bh->box;
-        // per-level float32 thresholds on s = d^2: accept iff s > size^2 / theta^2
-        std::vector<float2> tt(MAX_LEVELS);
-        for (int l = 0; l < MAX_LEVELS; ++l) {
-            const double size = std::ldexp(root, -l);
-            const double T = theta > 0.0 ? size * size / th2 : HUGE_VAL;
-            const float a = (float)(T * (1.0 + std::ldexp(1.0, -22)));
-            const float r = (float)(T * (1.0 - std::ldexp(1.0, -22)));
-            tt[l].x = std::nextafter(a, HUGE_VALF);
-            tt[l].y = std::isinf(r) ? r : std::nextafter(r, 0.f);
-        }
-        bh->d_tt.upload(tt.data(), MAX_LEVELS, s);
-        bh->wp.theta = theta;
-        bh->wp.theta2 = th2;
-        bh->wp.root_size = root;
-        bh->wp.dd2 = bh->walk_dd2;
-        bh->wp.dd3 = bh->walk_dd3;
-        bh->wp.tt = bh->d_tt.p;
-    }
-    GC_CUDA(cudaEventRecord(bh->ev[0], s));
-    bh->d_flag.zero(s);
-    if (fresh) {
-        // first walk on this tree: count, then size every force group's list
-        // with 1/8 slack so later walks (moved particles) run in one pass
-        bh->d_gcount.zero(s);
-        bh->d_bstat.zero(s);
-        walk_group_kernel<false, true><<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(
-            ng, wg, bh->d_fgmask.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p, bh->d_bgeo32.p, bh->wp,
-            nullptr, nullptr, nullptr, nullptr, bh->d_gcount.p, bh->d_bstat.p, bh->d_flag.p);
-        check_launch("walk_group_kernel<count>");
-        std::vector<int64_t> cnt(nf + 1, 0);
-        bh->d_gcount.download(cnt.data(), nf, s);
-        GC_CUDA(cudaStreamSynchronize(s));
-        std::vector<int64_t> cap(nf + 1, 0), basev(nf + 1, 0);
-        int64_t tot = 0;
-        for (int f = 0; f < nf; ++f) {
-            tot += cnt[f];
-            cap[f] = cnt[f] + cnt[f] / 8 + 16;
-            basev[f + 1] = basev[f] + cap[f];
-        }
-        bh->n_union = tot;
-        bh->d_gcap.upload(cap.data(), nf + 1, s);
-        bh->d_gbase.upload(basev.data(), nf + 1, s);
-        bh->d_uid.resize(basev[nf]);
-        bh->d_umask.resize(basev[nf]);
-        bh->cap_valid = true;
-        bh->cap_theta = theta;
-    }
-    walk_group_kernel<true, true><<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(
-        ng, wg, bh->d_fgmask.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p, bh->d_bgeo32.p, bh->wp,
-        bh->d_gbase.p, bh->d_gcap.p, bh->d_uid.p, bh->d_umask.p, bh->d_gcount.p, bh->d_bstat.p, bh->d_flag.p);
-    check_launch("walk_group_kernel<write>");
-    GC_CUDA(cudaEventRecord(bh->ev[1], s));
-    bh->have_union = true;
-    bh->have_member_lists = false;
-    bh->stats_dirty = true;
-    if (fresh) sync_walk_stats(bh);
+    GC_REQUIRE(bh->have_union, GC_E_STATE, "no device walk has run");
+    while (walk_overflowed(bh)) launch_walk(bh, true, false);
 }
 
 void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
@@ -269,11 +320,14 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
         const unsigned grid = grid_for(std::max(nfg, 1), WARPS_PER_BLOCK);
         auto k = eps0 ? (pot ? force_group_kernel<true, true> : force_group_kernel<true, false>)
                       : (pot ? force_group_kernel<false, true> : force_group_kernel<false, false>);
+        UnionPool U = pool_view(bh);
+        U.gfirst += f0;
+        U.gcount += f0;
         if (nfg > 0)
-        k<<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(nfg, bh->d_fg.p + f0, bh->d_gbase.p + f0, bh->d_gcount.p + f0, bh->d_uid.p,
-                                                bh->d_umask.p, bh->d_parts.p, bh->d_part_bucket.p, bh->d_porder.p,
-                                                bh->d_wg.p, bh->d_rec_hi.p, bh->d_rec_lo.p, bh->d_prange.p, eps2, g,
-                                                bh->dim, bh->d_out.p, bh->d_pot.p);
+        k<<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(nfg, bh->d_fg.p + f0, U, bh->d_parts.p, bh->d_part_bucket.p,
+                                                bh->d_porder.p, bh->d_wg.p, bh->d_rec_hi.p, bh->d_rec_lo.p,
+                                                bh->d_prange.p, bh->cgrid, eps2, g, bh->dim, bh->d_out.p,
+                                                bh->d_pot.p);
         check_launch("force_group_kernel");
     } else if (bh->have_member_lists) {
         GC_REQUIRE(!pot, GC_E_STATE, "potentials need device lists (gc_bh_walk)");
@@ -334,7 +388,8 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
         }
         bh->have_tree = true;
         bh->have_union = bh->have_member_lists = false;
-        bh->cap_valid = false;
+        bh->params_valid = false;
+        bh->stats_valid = false;
         bh->stats_dirty = false;
         bh->rg0 = 0;
         bh->rg1 = -1;
@@ -357,11 +412,22 @@ gc_status gc_bh_sizes(gc_bh *bh, int64_t out[4])
 {
     return guard([&] {
         GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
-        sync_walk_stats(bh);
         out[0] = bh->n_nodes;
         out[1] = bh->n_buckets;
-        out[2] = bh->n_list_entries;
-        out[3] = bh->n_union;
+        out[2] = out[3] = 0;
+        if (bh->params_valid) {
+            sync_walk_stats(bh);
+            out[2] = bh->n_list_entries;
+        }
+        if (bh->have_union) {
+            ensure_union_complete(bh);
+            std::vector<int> cnt(bh->d_gcount.n);
+            bh->d_gcount.download(cnt.data(), cnt.size(), bh->ctx->stream);
+            GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
+            int64_t tot = 0;
+            for (int c : cnt) tot += c;
+            out[3] = tot;
+        }
     });
 }
 
@@ -394,7 +460,7 @@ gc_status gc_bh_walk(gc_bh *bh, double theta)
 {
     return guard([&] {
         GC_REQUIRE(bh, GC_E_VALUE, "null argument");
-        run_walk(bh, theta);
+        run_walk(bh, theta, true);
     });
 }
 
@@ -402,6 +468,8 @@ gc_status gc_bh_get_lists(gc_bh *bh, int64_t *ptr, int64_t *ids, int8_t *kind, i
 {
     return guard([&] {
         GC_REQUIRE(bh && bh->have_union, GC_E_STATE, "no device walk has run");
+        GC_REQUIRE(bh->rg0 == 0 && bh->rg1 < 0, GC_E_STATE, "per-bucket lists need the full walk-group range");
+        ensure_union_complete(bh);
         sync_walk_stats(bh);
         cudaStream_t s = bh->ctx->stream;
         const int64_t nb = bh->n_buckets;
@@ -420,8 +488,7 @@ gc_status gc_bh_get_lists(gc_bh *bh, int64_t *ptr, int64_t *ids, int8_t *kind, i
             bh->d_list_ids.resize(tot);
             bh->d_list_kind.resize(tot);
             union_to_lists_kernel<<<grid_for(nf, WARPS_PER_BLOCK), 32 * WARPS_PER_BLOCK, 0, s>>>(
-                nf, bh->d_fg.p, bh->d_wg.p, bh->d_gbase.p, bh->d_gcount.p, bh->d_uid.p, bh->d_umask.p, bh->d_bptr.p,
-                bh->d_list_ids.p, bh->d_list_kind.p);
+                nf, bh->d_fg.p, bh->d_wg.p, pool_view(bh), bh->d_bptr.p, bh->d_list_ids.p, bh->d_list_kind.p);
             check_launch("union_to_lists_kernel");
             std::vector<int> tmp(tot);
             bh->d_list_ids.download(tmp.data(), tot, s);
@@ -487,15 +554,14 @@ gc_status gc_bh_forces(gc_bh *bh, double g, double eps, double *out)
     return guard([&] {
         GC_REQUIRE(bh && bh->have_tree && out, GC_E_STATE, "no particles set");
         launch_forces(bh, g, eps);
+        // a walk that overflowed the union pool is re-run (pool grown) before its forces count
+        while (bh->have_union && walk_overflowed(bh)) {
+            launch_walk(bh, true, false);
+            launch_forces(bh, g, eps);
+        }
         bh->d_out.download(out, bh->n * bh->dim, bh->ctx->stream);
         bh->d2h += bh->n * bh->dim * (int64_t)sizeof(double);
         GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
-        if (bh->have_union) {  // surface a deferred walk overflow
-            int flag = 0;
-            bh->d_flag.download(&flag, 1, bh->ctx->stream);
-            GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
-            GC_REQUIRE(!(flag & 2), GC_E_STATE, "walk list capacity overflow (re-run gc_bh_walk)");
-        }
     });
 }
 
@@ -504,6 +570,7 @@ gc_status gc_bh_forces_potential(gc_bh *bh, double g, double eps, double *out, d
     return guard([&] {
         GC_REQUIRE(bh && bh->have_tree && out && pot, GC_E_STATE, "no particles set");
         GC_REQUIRE(bh->have_union, GC_E_STATE, "potentials need device lists (gc_bh_walk)");
+        ensure_union_complete(bh);
         launch_forces(bh, g, eps, true);
         bh->d_out.download(out, bh->n * bh->dim, bh->ctx->stream);
         bh->d_pot.download(pot, bh->n, bh->ctx->stream);
@@ -532,8 +599,8 @@ gc_status gc_bh_set_range(gc_bh *bh, int64_t wg_begin, int64_t wg_end)
         GC_REQUIRE(wg_begin >= 0 && wg_begin <= wg_end && wg_end <= ng, GC_E_VALUE, "bad walk-group range");
         bh->rg0 = (int)wg_begin;
         bh->rg1 = (int)wg_end;
-        bh->cap_valid = false;  // next walk recounts this range
         bh->have_union = false;
+        bh->stats_valid = false;  // stats cover the walked range
     });
 }
 
@@ -565,12 +632,9 @@ gc_status gc_bh_timings(gc_bh *bh, double out[2])
 {
     return guard([&] {
         GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
-        if (bh->have_union) {
-            int flag = 0;
-            bh->d_flag.download(&flag, 1, bh->ctx->stream);
-            GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
-            GC_REQUIRE(!(flag & 2), GC_E_STATE, "walk list capacity overflow (re-run gc_bh_walk)");
-        }
+        // asynchronous walk + forces: an overflowed pool is grown, the step must be repeated
+        GC_REQUIRE(!(bh->have_union && walk_overflowed(bh)), GC_E_STATE,
+                   "union-list pool overflow (pool grown; re-run gc_bh_walk)");
         float a = 0.f, b = 0.f;
         out[0] = out[1] = 0.0;
         if (cudaEventElapsedTime(&a, bh->ev[0], bh->ev[1]) == cudaSuccess) out[0] = a;
@@ -594,7 +658,7 @@ gc_status gc_bh_step(gc_bh *bh, int64_t n, int32_t dim, const double *pos, const
     if (bh) bh->h2d = bh->d2h = 0;
     gc_status st = gc_bh_set_particles(bh, n, dim, pos, mass, box, bucket_size);
     if (st) return st;
-    st = gc_bh_walk(bh, theta);
+    st = guard([&] { run_walk(bh, theta, false); });  // no per-bucket stats on the step path
     if (st) return st;
     return gc_bh_forces(bh, g, eps, out);
 }

@@ -361,12 +361,20 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     for (double h = box / 2.0; h >= 1e-9 && nlev <= MAX_KEY_LEVELS; h /= 2.0) ++nlev;
     GC_REQUIRE(nlev <= MAX_KEY_LEVELS, GC_E_VALUE, "box too large for the device build keys");
 
-    DBuf<double> pos, mass, scratch;
+    auto &pos = bh->ws.pos;
+    auto &mass = bh->ws.mass;
+    auto &scratch = bh->ws.scratch;
     pos.upload(pos_h, (size_t)n * dim, s);
     mass.upload(mass_h, n, s);
     bh->h2d += (int64_t)n * (dim + 1) * (int64_t)sizeof(double);
-    DBuf<unsigned long long> k1, k2, k1p, k1s, k2s;
-    DBuf<int> idx, perm1, perm;
+    auto &k1 = bh->ws.k1;
+    auto &k2 = bh->ws.k2;
+    auto &k1p = bh->ws.k1p;
+    auto &k1s = bh->ws.k1s;
+    auto &k2s = bh->ws.k2s;
+    auto &idx = bh->ws.idx;
+    auto &perm1 = bh->ws.perm1;
+    auto &perm = bh->ws.perm;
     k1.resize(n); k2.resize(n); k1p.resize(n); k1s.resize(n); k2s.resize(n);
     idx.resize(n); perm1.resize(n); perm.resize(n);
     bb_keys<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, dim, pos.p, box, nlev, k1.p, k2.p, idx.p);
@@ -384,9 +392,20 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
 
     // level-synchronous expansion
     std::vector<int> lvl_first{0};
-    DBuf<int> lstart, lcount, lid, cstart, ccount, posnode, nsel, leaf_key, leaf_id, nleaf;
-    DBuf<double4> lcenter, ccenter;
-    DBuf<unsigned char> split, flag;
+    auto &lstart = bh->ws.lstart;
+    auto &lcount = bh->ws.lcount;
+    auto &lid = bh->ws.lid;
+    auto &cstart = bh->ws.cstart;
+    auto &ccount = bh->ws.ccount;
+    auto &posnode = bh->ws.posnode;
+    auto &nsel = bh->ws.nsel;
+    auto &leaf_key = bh->ws.leaf_key;
+    auto &leaf_id = bh->ws.leaf_id;
+    auto &nleaf = bh->ws.nleaf;
+    auto &lcenter = bh->ws.lcenter;
+    auto &ccenter = bh->ws.ccenter;
+    auto &split = bh->ws.split;
+    auto &flag = bh->ws.flag;
     const int cap_nodes = 3 * n + 1024;
     bh->d_ncenter.resize(cap_nodes);
     bh->d_pstart.resize(cap_nodes);
@@ -468,14 +487,15 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     GC_CUDA(cudaStreamSynchronize(s));
 
     // buckets in depth-first order = by start position
-    DBuf<int> lk_s;
+    auto &lk_s = bh->ws.lk_s;
     bh->d_buckets.resize(nb);
     lk_s.resize(nb);
     cubc(ctx, [&](void *t, size_t &b) {
         return cub::DeviceRadixSort::SortPairs(t, b, leaf_key.p, lk_s.p, leaf_id.p, bh->d_buckets.p, nb, 0, 32, s);
     });
     // particles inside each bucket: ascending original id
-    DBuf<int> offs, pidx;
+    auto &offs = bh->ws.offs;
+    auto &pidx = bh->ws.pidx;
     offs.resize(nb + 1);
     {
         // offsets = sorted bucket starts, plus n
@@ -490,7 +510,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
 
     // masses and centres of mass
     bh->d_nmass.resize(nn);
-    DBuf<double4> com;
+    auto &com = bh->ws.com;
     com.resize(nn);
     scratch.resize(n);
     bb_bucket_mass<<<grid_for(nb, BB_TPB), BB_TPB, 0, s>>>(nb, dim, bh->d_buckets.p, bh->d_pstart.p, bh->d_pcount.p,
@@ -503,7 +523,8 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     check_launch("bb mass");
 
     // records
-    DBuf<double> cmax, cmax_out;
+    auto &cmax = bh->ws.cmax;
+    auto &cmax_out = bh->ws.cmax_out;
     cmax.resize(nn);
     cmax_out.resize(1);
     bh->d_recs.resize(nn);
@@ -530,7 +551,9 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     check_launch("bb records");
     // groups
     const int nwg = (nb + 31) / 32;
-    DBuf<int> nfg_of, fg_base, bad;
+    auto &nfg_of = bh->ws.nfg_of;
+    auto &fg_base = bh->ws.fg_base;
+    auto &bad = bh->ws.bad;
     nfg_of.resize(nwg + 1);
     fg_base.resize(nwg + 1);
     bad.resize(1);
@@ -562,9 +585,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     bh->d_fgmask.download(bh->h_fgmask.data(), nfg, s);
     GC_CUDA(cudaStreamSynchronize(s));
     bh->d2h += (int64_t)nwg * sizeof(WalkGroup) + (int64_t)nfg * (sizeof(ForceGroup) + sizeof(unsigned));
-    const double delta = 1.25 * 6.0 * std::ldexp(1.0, -24) * std::max(cm, 1e-30);
-    bh->walk_dd2 = (float)(2.0 * delta * (1.0 + 1e-6));
-    bh->walk_dd3 = (float)(3.0 * delta * delta * (1.0 + 1e-6));
+    set_tree_bounds(bh, cm);
     bh->n = n;
     bh->dim = dim;
     bh->box = box;

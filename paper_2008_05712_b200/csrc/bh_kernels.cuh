@@ -32,7 +32,7 @@ constexpr int WARPS_PER_BLOCK = 8;
 constexpr int STACK_CAP = 384;  // >= 1 + 7*depth; depth <= log2(box/1e-9) (nbody.py:94)
 constexpr int MAX_LEVELS = 64;
 constexpr int QWIN = 128;  // window of expanded source records per warp
-constexpr int FLUSH = 8;  // fp32 partial sums are flushed to fp64 every FLUSH records
+constexpr int FLUSH = 8;  // fp32 partial sums are flushed to fp64 every FLUSH records (the mask loads assume 8)
 constexpr int NODE_BITS = 26;  // stack entries pack node | level << NODE_BITS
 
 struct WalkGroup {
@@ -85,17 +85,33 @@ __device__ __forceinline__ bool mac_accept64(const double4 c, const double size,
 }
 
 // ---------------------------------------------------------------------------
-// group walk.  WRITE: store union entries at gbase[g] (bounded by gcap[g]);
-// STATS: per-group entry counts and per-bucket [entries, items].
+// Union lists live in a chunked pool: every force group owns a chain of
+// CHUNK-entry chunks allocated on the fly (one atomicAdd per CHUNK entries),
+// so a walk over a new tree needs no counting pass.  Entry i of force group f
+// is in chunk chain position i / CHUNK, slot i % CHUNK.
+// ---------------------------------------------------------------------------
+constexpr int CHUNK = 64;  // multiple of 32: a warp's 32-entry read never straddles chunks
+
+struct UnionPool {
+    int *uid;  // node id per entry
+    uint2 *umask;  // (accept mask, particle mask) over the walk group's buckets
+    int *cnext;  // next chunk of the chain
+    int *gfirst;  // first chunk per force group
+    int *gcount;  // entries per force group
+    int *top;  // chunks handed out (may exceed nchunks: overflow, size to retry with)
+    int nchunks;
+};
+
+// ---------------------------------------------------------------------------
+// group walk.  WRITE: emit union entries into the pool; STATS: per-bucket
+// [entries, items] (item_count, nbody.py:187-189).
 // ---------------------------------------------------------------------------
 template <bool WRITE, bool STATS>
 __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, 4)
 walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsigned *__restrict__ fg_mask,
-                  const float4 *__restrict__ recs,
-                  const double4 *__restrict__ com64, const double4 *__restrict__ bgeo,
-                  const float4 *__restrict__ bgeo32, const WalkParams P, const int64_t *__restrict__ gbase,
-                  const int64_t *__restrict__ gcap, int *__restrict__ uid, uint2 *__restrict__ umask,
-                  int64_t *__restrict__ gcount, int64_t *__restrict__ bstat, int *__restrict__ flag)
+                  const float4 *__restrict__ recs, const double4 *__restrict__ com64,
+                  const double4 *__restrict__ bgeo, const float4 *__restrict__ bgeo32, const WalkParams P,
+                  UnionPool U, int64_t *__restrict__ bstat, int *__restrict__ flag)
 {
     __shared__ int2 stack_s[WARPS_PER_BLOCK][STACK_CAP];
     __shared__ float2 tt_s[MAX_LEVELS];
@@ -106,7 +122,6 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
     if (g >= ngroups) return;
     const WalkGroup gd = groups[g];
     const bool has = lane < gd.nbucket;
-    const double4 bg = has ? bgeo[gd.bfirst + lane] : make_double4(0, 0, 0, 0);
     const float4 bf = has ? bgeo32[gd.bfirst + lane] : make_float4(0.f, 0.f, 0.f, -1.f);
     const bool exact32 = bf.w >= 0.f;  // bucket geometry representable in float32
     const unsigned full = gd.nbucket == 32 ? 0xffffffffu : ((1u << gd.nbucket) - 1u);
@@ -117,9 +132,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
     const bool emits = lane < gd.nfg;
     const int my_fg = gd.fg_first + (emits ? lane : 0);
     const unsigned fgm = emits ? fg_mask[my_fg] : 0u;
-    const int64_t base = WRITE && emits ? gbase[my_fg] : 0;
-    const int cap = WRITE && emits ? (int)gcap[my_fg] : 0;
-    int w = 0;
+    int w = 0, chunk = 0;
     int my_entries = 0, my_items = 0;
     int node = 0, lvl = 0;
     unsigned act = full;
@@ -143,27 +156,33 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
         bool acc = mine && exact32 && (s - err > th.x);
         const bool unsure = mine && !acc && !(exact32 && (s + err < th.y));
         if (__any_sync(0xffffffffu, unsure)) {
-            if (unsure) acc = mac_accept64(com64[node], ldexp(P.root_size, -lvl), bg, P.theta, P.theta2);
+            if (unsure)
+                acc = mac_accept64(com64[node], ldexp(P.root_size, -lvl), bgeo[gd.bfirst + lane], P.theta, P.theta2);
         }
         const unsigned acc_m = __ballot_sync(0xffffffffu, acc);
         const unsigned part_m = is_bucket ? (act & ~acc_m) : 0u;
-        if (acc_m | part_m) {
-            if ((acc_m | part_m) & fgm) {
-                if (WRITE) {
-                    if (w < cap) {
-                        uid[base + w] = node;
-                        umask[base + w] = make_uint2(acc_m & fgm, part_m & fgm);
-                    } else {
-                        atomicOr(flag, 2);
-                    }
-                }
-                ++w;
+        const unsigned hit = (acc_m | part_m) & fgm;
+        if (WRITE && hit) {
+            const int slot = w & (CHUNK - 1);
+            if (slot == 0) {
+                const int c = atomicAdd(U.top, 1);
+                if (w == 0) U.gfirst[my_fg] = c;
+                else if (chunk < U.nchunks) U.cnext[chunk] = c;
+                chunk = c;
             }
-            if (STATS) {
-                const bool a = acc_m & bit, p = part_m & bit;
-                my_entries += (a || p) ? 1 : 0;
-                my_items += a ? 1 : (p ? -wd : 0);  // item_count (nbody.py:187-189)
+            if (chunk < U.nchunks) {
+                const int at = chunk * CHUNK + slot;
+                U.uid[at] = node;
+                U.umask[at] = make_uint2(acc_m & fgm, part_m & fgm);
+            } else if (slot == 0) {
+                atomicOr(flag, 2);
             }
+        }
+        w += hit ? 1 : 0;
+        if (STATS) {
+            const bool a = acc_m & bit, p = part_m & bit;
+            my_entries += (a || p) ? 1 : 0;
+            my_items += a ? 1 : (p ? -wd : 0);  // item_count (nbody.py:187-189)
         }
         const unsigned open = is_bucket ? 0u : (act & ~acc_m);
         if (open) {
@@ -190,21 +209,18 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
             nd = n_pop;
         }
     }
-    if (STATS) {
-        if (emits) gcount[my_fg] = w;
-        if (has) {
-            bstat[2 * (int64_t)(gd.bfirst + lane)] = my_entries;
-            bstat[2 * (int64_t)(gd.bfirst + lane) + 1] = my_items;
-        }
+    if (WRITE && emits) U.gcount[my_fg] = w;
+    if (STATS && has) {
+        bstat[2 * (int64_t)(gd.bfirst + lane)] = my_entries;
+        bstat[2 * (int64_t)(gd.bfirst + lane) + 1] = my_items;
     }
 }
 
 // Per-bucket walk_order / kind CSR from the union lists (parity + drop-in API).
 static __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK)
 union_to_lists_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const WalkGroup *__restrict__ wgroups,
-                      const int64_t *__restrict__ gbase, const int64_t *__restrict__ gcount,
-                      const int *__restrict__ uid, const uint2 *__restrict__ umask, const int64_t *__restrict__ bptr,
-                      int *__restrict__ ids, int8_t *__restrict__ kind)
+                      const UnionPool U, const int64_t *__restrict__ bptr, int *__restrict__ ids,
+                      int8_t *__restrict__ kind)
 {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int f = blockIdx.x * WARPS_PER_BLOCK + warp;
@@ -213,10 +229,14 @@ union_to_lists_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const Wal
     const unsigned bit = 1u << lane;
     const bool mine = fg.bmask & bit;
     int64_t cur = mine ? bptr[wgroups[fg.wg].bfirst + lane] : 0;
-    for (int64_t e = gbase[f]; e < gbase[f] + gcount[f]; ++e) {
-        const uint2 m = umask[e];
+    const int n = U.gcount[f];
+    int chunk = n > 0 ? U.gfirst[f] : 0;
+    for (int e = 0; e < n; ++e) {
+        if (e > 0 && (e & (CHUNK - 1)) == 0) chunk = U.cnext[chunk];
+        const int at = chunk * CHUNK + (e & (CHUNK - 1));
+        const uint2 m = U.umask[at];
         if (mine && ((m.x | m.y) & bit)) {
-            ids[cur] = uid[e];
+            ids[cur] = U.uid[at];
             kind[cur] = (m.x & bit) ? 0 : 1;
             ++cur;
         }
@@ -251,18 +271,63 @@ __device__ __forceinline__ void interact(const float4 h, const float3 l, const f
     if (POT) pot = fmaf(r2 != eps2 ? w : 0.f, r2, pot);  // m / sqrt(r^2 + eps^2); coincident skipped
 }
 
+// One group-relative source record (x, y, z, m) against one target.
+template <bool EPS0, bool POT>
+__device__ __forceinline__ void interact_rel(const float4 q, const float m_eff, const float3 xi, const float eps2,
+                                             float3 &a, float &pot)
+{
+    const float dx = q.x - xi.x, dy = q.y - xi.y, dz = q.z - xi.z;
+    const float r2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, eps2)));
+    const float r6 = r2 * r2 * r2;
+    float inv3 = rsqrt_approx(r6);
+    if (EPS0) inv3 = r2 > 0.f ? inv3 : 0.f;  // coincident source (kernels.py:83-84)
+    const float w = m_eff * inv3;
+    a.x = fmaf(dx, w, a.x);
+    a.y = fmaf(dy, w, a.y);
+    a.z = fmaf(dz, w, a.z);
+    if (POT) pot = fmaf(r2 != eps2 ? w : 0.f, r2, pot);  // m / sqrt(r^2 + eps^2); coincident skipped
+}
+
+__device__ __forceinline__ float warp_min(float v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Reference point of a force group, per dimension, from its targets' range
+// [lo, hi]: a multiple of cgrid (>= the float32 ulp of every coordinate of the
+// tree) between 0 and the targets, so target - c and nearby particle - c are
+// exact in float32 (both multiples of ulp(p), |p - c| <= |p|).
+__device__ __forceinline__ float group_origin(float lo, float hi, float cgrid, float inv_cgrid)
+{
+    if (lo >= 0.f) return floorf(lo * inv_cgrid) * cgrid;
+    if (hi <= 0.f) return -floorf(-hi * inv_cgrid) * cgrid;
+    return 0.f;
+}
+
+// Force-group kernel.  One warp per force group, lane = target.  Entries are
+// read 32 at a time; their records (one node record and/or the opened
+// bucket's particles) are expanded warp-cooperatively into a shared-memory
+// window in group-relative float32 coordinates (node COM hi + lo folded in
+// once per record, not once per pair), then broadcast to all lanes.
 template <bool EPS0, bool POT>
 __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, 4)
-force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int64_t *__restrict__ gbase,
-                   const int64_t *__restrict__ gcount, const int *__restrict__ uid, const uint2 *__restrict__ umask,
+force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U,
                    const float4 *__restrict__ parts, const int *__restrict__ part_bucket,
                    const int *__restrict__ porder, const WalkGroup *__restrict__ wgroups,
                    const float4 *__restrict__ rec_hi, const float4 *__restrict__ rec_lo,
-                   const int2 *__restrict__ prange, float eps2, double g, int dim, double *__restrict__ out,
-                   double *__restrict__ pot_out)
+                   const int2 *__restrict__ prange, float cgrid, float eps2, double g, int dim,
+                   double *__restrict__ out, double *__restrict__ pot_out)
 {
-    __shared__ float4 q_hi[WARPS_PER_BLOCK][QWIN + FLUSH];
-    __shared__ float4 q_lo[WARPS_PER_BLOCK][QWIN + FLUSH];  // lo.xyz, .w = bucket mask bits
+    __shared__ __align__(16) float4 q_rec[WARPS_PER_BLOCK][QWIN];
+    __shared__ __align__(16) unsigned q_msk[WARPS_PER_BLOCK][QWIN];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gi = blockIdx.x * WARPS_PER_BLOCK + warp;
     if (gi >= nfg) return;
@@ -271,24 +336,32 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int64_
     const bool tgt = lane < fg.ntarget;
     const int p = fg.pstart + (tgt ? lane : 0);
     const float4 xp = parts[p];
-    const float3 xi = make_float3(xp.x, xp.y, xp.z);
     const unsigned mybit = tgt ? (1u << (part_bucket[p] - wfirst)) : 0u;
-    float4 *qh = q_hi[warp];
-    float4 *ql = q_lo[warp];
+    const float inv_cgrid = 1.0f / cgrid;  // power of two: exact
+    const float cx = group_origin(warp_min(xp.x), warp_max(xp.x), cgrid, inv_cgrid);
+    const float cy = group_origin(warp_min(xp.y), warp_max(xp.y), cgrid, inv_cgrid);
+    const float cz = group_origin(warp_min(xp.z), warp_max(xp.z), cgrid, inv_cgrid);
+    const float3 xi = make_float3(xp.x - cx, xp.y - cy, xp.z - cz);  // exact
+    float4 *qr = q_rec[warp];
+    unsigned *qm = q_msk[warp];
     double ax = 0.0, ay = 0.0, az = 0.0, ap = 0.0;
-    const int64_t e0 = gbase[gi], e1 = e0 + min(gcount[gi], gbase[gi + 1] - gbase[gi]);
-    for (int64_t c = e0; c < e1; c += 32) {
-        const int64_t e = c + lane;
+    const int n = U.gcount[gi];
+    int chunk = n > 0 ? U.gfirst[gi] : 0;
+    for (int e0 = 0; e0 < n; e0 += 32) {
+        if (e0 > 0 && (e0 & (CHUNK - 1)) == 0) chunk = U.cnext[chunk];
+        const int e = e0 + lane;
         int node = 0;
         uint2 m = make_uint2(0u, 0u);
         int2 pr = make_int2(0, 0);
-        if (e < e1) {
-            node = uid[e];
-            m = umask[e];
+        if (e < n) {
+            const int at = chunk * CHUNK + (e & (CHUNK - 1));
+            node = U.uid[at];
+            m = U.umask[at];
         }
         if (m.y) pr = prange[node];
-        const int nrec = (m.x ? 1 : 0) + (m.y ? pr.y : 0);
-        // warp exclusive scan of record counts -> queue slots
+        const int hasnode = m.x ? 1 : 0;
+        const int nrec = hasnode + (m.y ? pr.y : 0);
+        // warp inclusive scan of record counts
         int incl = nrec;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -296,37 +369,61 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int64_
             if (lane >= o) incl += t;
         }
         const int total = __shfl_sync(0xffffffffu, incl, 31);
-        const int first = incl - nrec;  // this lane's first queue slot
-        // the expanded chunk is consumed in windows of QWIN records
+        const int first = incl - nrec;
+        const int psrc = pr.x - hasnode;  // particle record r >= hasnode is parts[psrc + r]
         for (int w0 = 0; w0 < total; w0 += QWIN) {
-            const int r0 = max(0, w0 - first), r1 = min(nrec, w0 + QWIN - first);
-            for (int r = r0; r < r1; ++r) {
-                const int slot = first + r - w0;
-                if (m.x && r == 0) {
-                    const float4 l = rec_lo[node];
-                    qh[slot] = rec_hi[node];
-                    ql[slot] = make_float4(l.x, l.y, l.z, __uint_as_float(m.x));
-                } else {
-                    qh[slot] = parts[pr.x + r - (m.x ? 1 : 0)];
-                    ql[slot] = make_float4(0.f, 0.f, 0.f, __uint_as_float(m.y));
-                }
-            }
             const int nin = min(QWIN, total - w0);
-            const int padded = (nin + FLUSH - 1) / FLUSH * FLUSH;  // massless padding records
-            if (lane < padded - nin) {
-                qh[nin + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-                ql[nin + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+            const int padded = (nin + FLUSH - 1) & ~(FLUSH - 1);
+            // cooperative expansion: slot s of the window belongs to the lane
+            // whose [first, incl) holds w0 + s (binary search over the scan)
+            for (int s0 = 0; s0 < padded; s0 += 32) {
+                const int s = s0 + lane;
+                const int gs = w0 + s;
+                int own = 0;
+#pragma unroll
+                for (int step = 16; step >= 1; step >>= 1) {
+                    const int v = __shfl_sync(0xffffffffu, incl, own + step - 1);
+                    if (v <= gs) own += step;
+                }
+                own = min(own, 31);
+                const int o_first = __shfl_sync(0xffffffffu, first, own);
+                const int o_node = __shfl_sync(0xffffffffu, node, own);
+                const unsigned o_mx = __shfl_sync(0xffffffffu, m.x, own);
+                const unsigned o_my = __shfl_sync(0xffffffffu, m.y, own);
+                const int o_psrc = __shfl_sync(0xffffffffu, psrc, own);
+                if (s < nin) {
+                    const int r = gs - o_first;
+                    float4 q;
+                    unsigned mk;
+                    if (o_mx && r == 0) {
+                        const float4 h = rec_hi[o_node];
+                        const float4 l = rec_lo[o_node];
+                        q = make_float4((h.x - cx) + l.x, (h.y - cy) + l.y, (h.z - cz) + l.z, h.w);
+                        mk = o_mx;
+                    } else {
+                        const float4 h = parts[o_psrc + r];
+                        q = make_float4(h.x - cx, h.y - cy, h.z - cz, h.w);
+                        mk = o_my;
+                    }
+                    qr[s] = q;
+                    qm[s] = mk;
+                } else if (s < padded) {  // massless padding up to a FLUSH multiple
+                    qr[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    qm[s] = 0u;
+                }
             }
             __syncwarp();
             for (int j0 = 0; j0 < padded; j0 += FLUSH) {
                 float3 a = make_float3(0.f, 0.f, 0.f);
                 float pt = 0.f;
+                const uint4 k0 = *reinterpret_cast<const uint4 *>(qm + j0);
+                const uint4 k1 = *reinterpret_cast<const uint4 *>(qm + j0 + 4);
+                const unsigned ks[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
 #pragma unroll
                 for (int jj = 0; jj < FLUSH; ++jj) {
-                    const float4 h = qh[j0 + jj];
-                    const float4 l = ql[j0 + jj];
-                    const float me = (__float_as_uint(l.w) & mybit) ? h.w : 0.f;
-                    interact<EPS0, POT>(h, make_float3(l.x, l.y, l.z), me, xi, eps2, a, pt);
+                    const float4 q = qr[j0 + jj];
+                    const float me = (ks[jj] & mybit) ? q.w : 0.f;
+                    interact_rel<EPS0, POT>(q, me, xi, eps2, a, pt);
                 }
                 ax += (double)a.x;
                 ay += (double)a.y;

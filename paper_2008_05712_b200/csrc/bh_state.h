@@ -5,7 +5,24 @@
 #include "bh_tree.h"
 #include "common.cuh"
 
+#include <algorithm>
+#include <cmath>
+
 using namespace gc;
+
+struct BuildWs {  // device-build scratch, kept across builds (no per-step cudaMalloc/cudaFree)
+    DBuf<double> pos, mass, scratch;
+    DBuf<unsigned long long> k1, k2, k1p, k1s, k2s;
+    DBuf<int> idx, perm1, perm;
+    DBuf<int> lstart, lcount, lid, cstart, ccount, posnode, nsel, leaf_key, leaf_id, nleaf;
+    DBuf<double4> lcenter, ccenter;
+    DBuf<unsigned char> split, flag;
+    DBuf<int> lk_s;
+    DBuf<int> offs, pidx;
+    DBuf<double4> com;
+    DBuf<double> cmax, cmax_out;
+    DBuf<int> nfg_of, fg_base, bad;
+};
 
 struct gc_bh {
     gc_ctx *ctx = nullptr;
@@ -44,12 +61,16 @@ struct gc_bh {
     // union lists (device walk)
     int rg0 = 0, rg1 = -1;  // walk-group range this handle evaluates (multi-GPU shard)
     bool have_union = false;
-    bool cap_valid = false;
+    bool params_valid = false;  // walk thresholds for (tree, theta) uploaded
     double cap_theta = -1.0;
-    DBuf<int64_t> d_gcount, d_gbase, d_gcap, d_bstat;
-    DBuf<int> d_uid;
+    bool stats_valid = false;  // d_bstat describes the current tree + theta
+    // chunked union-list pool (bh_kernels.cuh: UnionPool)
+    DBuf<int> d_uid, d_cnext, d_gfirst, d_gcount, d_top;
     DBuf<uint2> d_umask;
+    int pool_chunks = 0;
+    DBuf<int64_t> d_bstat;
     int64_t n_union = 0;
+    float cgrid = 0.f;  // float32 ulp bound of every tree coordinate (force-group origins)
     // per-bucket CSR (host-supplied lists)
     bool have_member_lists = false;
     DBuf<int64_t> d_nptr, d_pptr;
@@ -63,8 +84,9 @@ struct gc_bh {
     DBuf<int8_t> d_list_kind;
     DBuf<int> d_flag;
     WalkParams wp{};
-    bool stats_dirty = false;
+    bool stats_dirty = false;  // d_bstat newer than the host copies
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    BuildWs ws;
     int64_t h2d = 0, d2h = 0;  // bytes moved host<->device since the last reset
     ~gc_bh()
     {
@@ -74,6 +96,20 @@ struct gc_bh {
 };
 
 namespace gc {
+// Coordinate bounds of a tree (cmax >= |every com / particle coordinate|):
+// the walk's float32 error band and the force groups' origin grid.
+inline void set_tree_bounds(gc_bh *bh, double cmax)
+{
+    cmax = std::max(cmax, 1e-30);
+    // |v32 - v64| <= delta for every opening-test component (walk_group_kernel):
+    // com rounding + two float32 subtractions, each <= 2^-24 * |operand|
+    const double delta = 1.25 * 6.0 * std::ldexp(1.0, -24) * cmax;
+    bh->walk_dd2 = (float)(2.0 * delta * (1.0 + 1e-6));
+    bh->walk_dd3 = (float)(3.0 * delta * delta * (1.0 + 1e-6));
+    int e = 0;
+    std::frexp(cmax, &e);  // cmax < 2^e, so ulp32(x) <= 2^(e-24) for every |x| <= cmax
+    bh->cgrid = (float)std::ldexp(1.0, e - 24);
+}
 void device_build_tree(gc_bh *bh, const double *pos, const double *mass, int64_t n, int dim, double box,
                        int64_t bucket_size);
 void ensure_host_tree(gc_bh *bh);
