@@ -16,7 +16,7 @@ import numpy as np
 from .errors import CudaError, raise_for_status
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgcharm.so")
+LIB_PATH = os.environ.get("GCHARM_LIB") or os.path.join(_HERE, "libgcharm.so")  # override: kernel A/B experiments
 
 i64p = C.POINTER(C.c_int64)
 i32p = C.POINTER(C.c_int32)

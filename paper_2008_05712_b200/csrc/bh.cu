@@ -18,7 +18,8 @@ void upload_tree(gc_bh *bh)
     cudaStream_t s = bh->ctx->stream;
     const HostTree &t = bh->tree;
     const int64_t nn = t.n_nodes(), nb = (int64_t)t.buckets.size();
-    GC_REQUIRE(t.n < (1ll << 31) && nn < (1ll << NODE_BITS), GC_E_VALUE, "tree too large for the packed node ids");
+    GC_REQUIRE(t.n < (1ll << PSTART_BITS) && nn < (1ll << NODE_BITS), GC_E_VALUE,
+               "tree too large for the packed node ids / bucket words");
     std::vector<float4> recs(nn), hi(nn), lo(nn);
     std::vector<double4> c64(nn);
     std::vector<int2> pr(nn);
@@ -38,8 +39,9 @@ void upload_tree(gc_bh *bh)
         }
         int word;
         if (t.first_child[i] < 0) {
-            GC_REQUIRE(t.pcount[i] < (1 << 30), GC_E_VALUE, "bucket too large");
-            word = -(int)t.pcount[i];
+            GC_REQUIRE(t.pcount[i] <= 32, GC_E_VALUE,
+                       "bucket with more than 32 particles (coincident points) on the group path");
+            word = wr_bucket_word((int)t.pstart[i], (int)t.pcount[i]);
         } else {
             word = (int)(t.first_child[i] << 3) | (t.n_child[i] - 1);
         }
@@ -148,8 +150,7 @@ void exclusive_scan(gc_ctx *ctx, const T *in, T *out, int64_t n)
 UnionPool pool_view(gc_bh *bh)
 {
     UnionPool U;
-    U.uid = bh->d_uid.p;
-    U.umask = bh->d_umask.p;
+    U.ent = bh->d_ent.p;
     U.cnext = bh->d_cnext.p;
     U.gfirst = bh->d_gfirst.p;
     U.gcount = bh->d_gcount.p;
@@ -161,9 +162,8 @@ UnionPool pool_view(gc_bh *bh)
 void size_pool(gc_bh *bh, int64_t chunks)
 {
     GC_REQUIRE(chunks * CHUNK < (1ll << 31), GC_E_VALUE, "union-list pool exceeds 2^31 entries");
-    bh->d_uid.resize(chunks * CHUNK);
-    bh->d_umask.resize(chunks * CHUNK);
-    bh->d_cnext.resize(chunks);
+    bh->d_ent.resize((chunks + 1) * CHUNK);  // + the overflow sink chunk
+    bh->d_cnext.resize(chunks + 1);
     bh->pool_chunks = (int)chunks;
 }
 
@@ -326,8 +326,7 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
         if (nfg > 0)
         k<<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(nfg, bh->d_fg.p + f0, U, bh->d_parts.p, bh->d_part_bucket.p,
                                                 bh->d_porder.p, bh->d_wg.p, bh->d_rec_hi.p, bh->d_rec_lo.p,
-                                                bh->d_prange.p, bh->cgrid, eps2, g, bh->dim, bh->d_out.p,
-                                                bh->d_pot.p);
+                                                bh->cgrid, eps2, g, bh->dim, bh->d_out.p, bh->d_pot.p);
         check_launch("force_group_kernel");
     } else if (bh->have_member_lists) {
         GC_REQUIRE(!pot, GC_E_STATE, "potentials need device lists (gc_bh_walk)");
@@ -483,19 +482,40 @@ gc_status gc_bh_get_lists(gc_bh *bh, int64_t *ptr, int64_t *ids, int8_t *kind, i
         if (item_count)
             for (int64_t b = 0; b < nb; ++b) item_count[b] = st[2 * b + 1];
         if (ids || kind) {
+            GC_REQUIRE(tot < (1ll << 31), GC_E_VALUE, "more than 2^31 list entries");
             const int nf = (int)bh->h_fg.size();
+            // preorder (depth-first, children in octant order) index of every node
+            ensure_host_tree(bh);
+            const HostTree &t = bh->tree;
+            const int64_t nn = t.n_nodes();
+            std::vector<int> pre(nn), todo{0};
+            int counter = 0;
+            while (!todo.empty()) {
+                const int v = todo.back();
+                todo.pop_back();
+                pre[v] = counter++;
+                for (int c = t.n_child[v] - 1; c >= 0; --c) todo.push_back((int)(t.first_child[v] + c));
+            }
+            bh->d_pre.upload(pre.data(), nn, s);
             bh->d_bptr.upload(bptr.data(), nb + 1, s);
-            bh->d_list_ids.resize(tot);
-            bh->d_list_kind.resize(tot);
+            auto &k0 = bh->d_list_key, &k1 = bh->d_list_key2, &v0 = bh->d_list_val, &v1 = bh->d_list_val2;
+            k0.resize(tot); k1.resize(tot); v0.resize(tot); v1.resize(tot);
             union_to_lists_kernel<<<grid_for(nf, WARPS_PER_BLOCK), 32 * WARPS_PER_BLOCK, 0, s>>>(
-                nf, bh->d_fg.p, bh->d_wg.p, pool_view(bh), bh->d_bptr.p, bh->d_list_ids.p, bh->d_list_kind.p);
+                nf, bh->d_fg.p, bh->d_wg.p, pool_view(bh), bh->d_bptr.p, bh->d_pre.p, k0.p, v0.p);
             check_launch("union_to_lists_kernel");
+            size_t bytes = 0;
+            GC_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, k0.p, k1.p, v0.p, v1.p, (int)tot, (int)nb,
+                                                        bh->d_bptr.p, bh->d_bptr.p + 1, s));
+            bh->ctx->scratch.resize(bytes);
+            GC_CUDA(cub::DeviceSegmentedSort::SortPairs(bh->ctx->scratch.p, bytes, k0.p, k1.p, v0.p, v1.p, (int)tot,
+                                                        (int)nb, bh->d_bptr.p, bh->d_bptr.p + 1, s));
             std::vector<int> tmp(tot);
-            bh->d_list_ids.download(tmp.data(), tot, s);
-            if (kind) bh->d_list_kind.download(kind, tot, s);
+            v1.download(tmp.data(), tot, s);
             GC_CUDA(cudaStreamSynchronize(s));
-            if (ids)
-                for (int64_t i = 0; i < tot; ++i) ids[i] = tmp[i];
+            for (int64_t i = 0; i < tot; ++i) {
+                if (ids) ids[i] = tmp[i] >> 1;
+                if (kind) kind[i] = (int8_t)(tmp[i] & 1);
+            }
         }
     });
 }

@@ -264,7 +264,8 @@ __global__ void bb_records(int nn, const double4 *__restrict__ com, const double
     const double4 c = com[i];
     const float hx = (float)c.x, hy = (float)c.y, hz = (float)c.z;
     const int fc = first_child[i];
-    const int word = fc < 0 ? -pcount[i] : ((fc << 3) | (nchild[i] - 1));
+    // buckets of > 32 particles are rejected by bb_groups before any walk
+    const int word = fc < 0 ? wr_bucket_word(pstart[i], min(pcount[i], 32)) : ((fc << 3) | (nchild[i] - 1));
     recs[i] = make_float4(hx, hy, hz, __int_as_float(word));
     com64[i] = c;
     rec_hi[i] = make_float4(hx, hy, hz, (float)nmass[i]);
@@ -354,7 +355,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
 {
     gc_ctx *ctx = bh->ctx;
     cudaStream_t s = ctx->stream;
-    GC_REQUIRE(n64 < (1 << 30), GC_E_VALUE, "too many particles for the device build");
+    GC_REQUIRE(n64 < (1 << PSTART_BITS), GC_E_VALUE, "too many particles for one tree (packed bucket words)");
     const int n = (int)n64;
     // levels at which a node may still split (half >= 1e-9, nbody.py:94)
     int nlev = 0;

@@ -65,8 +65,8 @@ struct gc_bh {
     double cap_theta = -1.0;
     bool stats_valid = false;  // d_bstat describes the current tree + theta
     // chunked union-list pool (bh_kernels.cuh: UnionPool)
-    DBuf<int> d_uid, d_cnext, d_gfirst, d_gcount, d_top;
-    DBuf<uint2> d_umask;
+    DBuf<int> d_cnext, d_gfirst, d_gcount, d_top;
+    DBuf<int4> d_ent;
     int pool_chunks = 0;
     DBuf<int64_t> d_bstat;
     int64_t n_union = 0;
@@ -80,8 +80,7 @@ struct gc_bh {
     std::vector<int64_t> h_item_count;
     int64_t n_list_entries = 0;
     DBuf<int64_t> d_bptr;
-    DBuf<int> d_list_ids;
-    DBuf<int8_t> d_list_kind;
+    DBuf<int> d_pre, d_list_key, d_list_key2, d_list_val, d_list_val2;
     DBuf<int> d_flag;
     WalkParams wp{};
     bool stats_dirty = false;  // d_bstat newer than the host copies

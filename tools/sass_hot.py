@@ -24,3 +24,12 @@ for b in blocks[:1]:
         e, w = int(r[iE] or 0), int(r[iW] or 0)
         if e > tot * frac or w > totw * 2 * frac:
             print(f"{r[0][-5:]} {e:>11d} {w:>6d}  {r[iS].strip()[:90]}")
+
+if len(sys.argv) > 3:  # top-N by stall samples
+    b = blocks[0]
+    h = b["hdr"]
+    iS, iE, iW = h.index("Source"), h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
+    rows = sorted(b["rows"], key=lambda r: -int(r[iW] or 0))[: int(sys.argv[3])]
+    print("--- top by samples")
+    for r in sorted(rows, key=lambda r: r[0]):
+        print(f"{r[0][-5:]} {int(r[iE] or 0):>11d} {int(r[iW] or 0):>6d}  {r[iS].strip()[:90]}")
