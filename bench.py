@@ -232,7 +232,7 @@ def bench_bh(args, world, rank, local, ctx, torch):
     ctx.sync()
     inter = nbody.interactions(tree)
     step_ms, walk_ms, force_ms = [], [], []
-    tm = np.zeros(2)
+    tm = np.zeros(3)
     barrier(world)
     torch.cuda.synchronize()
     clk = ClockSampler(local)

@@ -127,8 +127,9 @@ gc_status gc_bh_forces_async(gc_bh *bh, double g, double eps);
 /* Sum over buckets of n_b * item_count_b (the interaction count) */
 gc_status gc_bh_interactions(gc_bh *bh, int64_t *out);
 /* Device time (ms, CUDA events on the context stream) of the last walk
- * (out[0]) and the last force launch (out[1]). */
-gc_status gc_bh_timings(gc_bh *bh, double out[2]);
+ * (out[0]), the last force kernel (out[1]) and the reorganisation (staging
+ * gather) that precedes it (out[2]). */
+gc_status gc_bh_timings(gc_bh *bh, double out[3]);
 /* Host<->device bytes moved since the last reset (out[0] = H2D, out[1] = D2H);
  * gc_bh_step resets at entry, so after it these are that step's bytes. */
 gc_status gc_bh_io_bytes(gc_bh *bh, int64_t out[2], int32_t reset);

@@ -154,10 +154,34 @@ UnionPool pool_view(gc_bh *bh)
     U.cnext = bh->d_cnext.p;
     U.gfirst = bh->d_gfirst.p;
     U.gcount = bh->d_gcount.p;
+    U.grec = bh->d_grec.p;
     U.top = bh->d_top.p;
     U.nchunks = bh->pool_chunks;
     return U;
 }
+
+void size_staging(gc_bh *bh, int64_t records)
+{
+    records = (records + TILE - 1) / TILE * TILE;
+    bh->d_srec.resize(records + TILE);  // + one tile: the last cp.async stage may read past a run
+    bh->d_smask.resize(records + TILE);
+    bh->staging_cap = records;
+}
+
+__global__ void bb_iota_kernel(int n, int *p)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = i;
+}
+
+struct RoundRun {  // records of a force group's staging run (multiple of PFLUSH); 0 past the end
+    const int *grec;
+    int n;
+    __host__ __device__ int64_t operator()(int i) const
+    {
+        return i < n ? (int64_t)((grec[i] + PFLUSH - 1) & ~(PFLUSH - 1)) : 0;
+    }
+};
 
 void size_pool(gc_bh *bh, int64_t chunks)
 {
@@ -218,6 +242,8 @@ void launch_walk(gc_bh *bh, bool write, bool stats)
         bh->d_gfirst.resize(nf);
         bh->d_gcount.resize(nf);
         bh->d_gcount.zero(s);
+        bh->d_grec.resize(nf);
+        bh->d_grec.zero(s);
         bh->d_top.resize(1);
         bh->d_top.zero(s);
     }
@@ -242,6 +268,13 @@ bool walk_overflowed(gc_bh *bh)
     GC_REQUIRE(!(flag & 1), GC_E_VALUE, "tree deeper than the walk stack (box too large for half_size >= 1e-9)");
     if (flag & 2) {
         size_pool(bh, (int64_t)top + top / 8 + 64);
+        return true;
+    }
+    if (flag & 4) {  // staging run overflow (expand_kernel): size it to the walk's demand
+        int64_t need = 0;
+        bh->d_rbase.download(&need, 1, s, bh->d_rbase.n - 1);
+        GC_CUDA(cudaStreamSynchronize(s));
+        size_staging(bh, need + need / 16);
         return true;
     }
     return false;
@@ -318,21 +351,68 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
         const int f1 = g1 < (int)bh->h_wg.size() ? bh->h_wg[g1].fg_first : (int)bh->h_fg.size();
         const int nfg = f1 - f0;
         const unsigned grid = grid_for(std::max(nfg, 1), WARPS_PER_BLOCK);
-        auto k = eps0 ? (pot ? force_group_kernel<true, true> : force_group_kernel<true, false>)
-                      : (pot ? force_group_kernel<false, true> : force_group_kernel<false, false>);
         UnionPool U = pool_view(bh);
         U.gfirst += f0;
         U.gcount += f0;
-        if (nfg > 0)
-        k<<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(nfg, bh->d_fg.p + f0, U, bh->d_parts.p, bh->d_part_bucket.p,
-                                                bh->d_porder.p, bh->d_wg.p, bh->d_rec_hi.p, bh->d_rec_lo.p,
-                                                bh->cgrid, eps2, g, bh->dim, bh->d_out.p, bh->d_pot.p);
-        check_launch("force_group_kernel");
+        U.grec += f0;
+        // staging runs: exclusive scan of the rounded record counts
+        bh->d_rbase.resize(nfg + 1);
+        {
+            auto it = cub::TransformInputIterator<int64_t, RoundRun, cub::CountingInputIterator<int>>(
+                cub::CountingInputIterator<int>(0), RoundRun{U.grec, nfg});
+            size_t bytes = 0;
+            GC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, bh->d_rbase.p, nfg + 1, s));
+            ctx->scratch.resize(bytes);
+            GC_CUDA(cub::DeviceScan::ExclusiveSum(ctx->scratch.p, bytes, it, bh->d_rbase.p, nfg + 1, s));
+        }
+        // first guess ~160 records per bucket; an overflow grows it to the walk's demand
+        if (bh->staging_cap == 0) size_staging(bh, 160 * bh->n_buckets + 1024);
+        // processing order of the persistent force kernel: longest run first
+        bh->d_fg_key.resize(nfg);
+        bh->d_fg_iota.resize(nfg);
+        bh->d_fg_order.resize(nfg);
+        bh->d_next.resize(1);
+        bh->d_next.zero(s);
+        if (nfg > 0) {
+            bb_iota_kernel<<<grid_for(nfg, 256), 256, 0, s>>>(nfg, bh->d_fg_iota.p);
+            size_t bytes = 0;
+            GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, U.grec, bh->d_fg_key.p,
+                                                              bh->d_fg_iota.p, bh->d_fg_order.p, nfg, 0, 32, s));
+            ctx->scratch.resize(bytes);
+            GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(ctx->scratch.p, bytes, U.grec, bh->d_fg_key.p,
+                                                              bh->d_fg_iota.p, bh->d_fg_order.p, nfg, 0, 32, s));
+        }
+        Staging S;
+        S.rec = bh->d_srec.p;
+        S.mask = bh->d_smask.p;
+        S.rbase = bh->d_rbase.p;
+        S.order = bh->d_fg_order.p;
+        S.next = bh->d_next.p;
+        S.cap = bh->staging_cap;
+        if (nfg > 0) {
+            expand_kernel<<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(nfg, bh->d_fg.p + f0, U, bh->d_parts.p, bh->d_rec_hi.p,
+                                                                bh->d_rec_lo.p, bh->cgrid, S, bh->d_flag.p);
+            check_launch("expand_kernel");
+        }
+        GC_CUDA(cudaEventRecord(bh->ev[4], s));
+        auto k = eps0 ? (pot ? force_group_kernel<true, true> : force_group_kernel<true, false>)
+                      : (pot ? force_group_kernel<false, true> : force_group_kernel<false, false>);
+        if (nfg > 0) {
+            int per_sm = 0;
+            GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * WARPS_PER_BLOCK, 0));
+            const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(
+                (int64_t)per_sm * ctx->prop.multiProcessorCount, grid_for(nfg, WARPS_PER_BLOCK)));
+            k<<<pgrid, 32 * WARPS_PER_BLOCK, 0, s>>>(nfg, bh->d_fg.p + f0, U.grec, S, bh->d_parts.p,
+                                                     bh->d_part_bucket.p, bh->d_porder.p, bh->d_wg.p, bh->cgrid, eps2,
+                                                     g, bh->dim, bh->d_out.p, bh->d_pot.p);
+            check_launch("force_group_kernel");
+        }
     } else if (bh->have_member_lists) {
         GC_REQUIRE(!pot, GC_E_STATE, "potentials need device lists (gc_bh_walk)");
         const int nb = (int)bh->n_buckets;
         const unsigned grid = grid_for(nb, WARPS_PER_BLOCK);
         auto k = eps0 ? force_member_kernel<true> : force_member_kernel<false>;
+        GC_CUDA(cudaEventRecord(bh->ev[4], s));
         k<<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(nb, bh->d_bucket_ids.p, bh->d_brange.p, bh->d_nptr.p,
                                                 bh->d_naddr.p, bh->d_pptr.p, bh->d_paddr.p, bh->d_parts.p,
                                                 bh->d_porder.p, bh->d_rec_hi.p, bh->d_rec_lo.p, bh->d_prange.p,
@@ -648,17 +728,18 @@ gc_status gc_bh_bucket_work(gc_bh *bh, int64_t *work)
     });
 }
 
-gc_status gc_bh_timings(gc_bh *bh, double out[2])
+gc_status gc_bh_timings(gc_bh *bh, double out[3])
 {
     return guard([&] {
         GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
         // asynchronous walk + forces: an overflowed pool is grown, the step must be repeated
         GC_REQUIRE(!(bh->have_union && walk_overflowed(bh)), GC_E_STATE,
                    "union-list pool overflow (pool grown; re-run gc_bh_walk)");
-        float a = 0.f, b = 0.f;
-        out[0] = out[1] = 0.0;
+        float a = 0.f, b = 0.f, c = 0.f;
+        out[0] = out[1] = out[2] = 0.0;
         if (cudaEventElapsedTime(&a, bh->ev[0], bh->ev[1]) == cudaSuccess) out[0] = a;
-        if (cudaEventElapsedTime(&b, bh->ev[2], bh->ev[3]) == cudaSuccess) out[1] = b;
+        if (cudaEventElapsedTime(&b, bh->ev[4], bh->ev[3]) == cudaSuccess) out[1] = b;
+        if (cudaEventElapsedTime(&c, bh->ev[2], bh->ev[4]) == cudaSuccess) out[2] = c;
         cudaGetLastError();
     });
 }

@@ -107,6 +107,7 @@ struct UnionPool {
     int *cnext;  // next chunk of the chain
     int *gfirst;  // first chunk per force group
     int *gcount;  // entries per force group
+    int *grec;  // source records per force group (node records + opened-bucket particles)
     int *top;  // chunks handed out (may exceed nchunks: overflow, size to retry with)
     int nchunks;  // chunk nchunks is a sink for writes after an overflow
 };
@@ -156,7 +157,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
     const bool emits = lane < gd.nfg;
     const int my_fg = gd.fg_first + (emits ? lane : 0);
     const unsigned fgm = emits ? fg_mask[my_fg] : 0u;
-    int w = 0, chunk = 0;
+    int w = 0, chunk = 0, nrec = 0;
     if (WRITE && emits) {
         chunk = atomicAdd(U.top, 1);
         if (chunk >= U.nchunks) {  // overflow: park in the sink chunk, the host re-walks
@@ -198,6 +199,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
                 if (emits) U.ent[chunk * CHUNK + (w & (CHUNK - 1))] =
                     make_int4(node, (int)(acc_m & fgm), (int)(part_m & fgm), wd);
                 w += hit ? 1 : 0;
+                nrec += ((acc_m & fgm) ? 1 : 0) + ((part_m & fgm) ? wr_pcount(wd) : 0);
                 if (hit && (w & (CHUNK - 1)) == 0) {  // chunk full: link the next one
                     int cn = atomicAdd(U.top, 1);
                     if (cn >= U.nchunks) {
@@ -238,7 +240,10 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
         lvl = slvl[sp];
         __syncwarp();
     }
-    if (WRITE && emits) U.gcount[my_fg] = w;
+    if (WRITE && emits) {
+        U.gcount[my_fg] = w;
+        U.grec[my_fg] = nrec;
+    }
     if (STATS && has) {
         bstat[2 * (int64_t)(gd.bfirst + lane)] = my_entries;
         bstat[2 * (int64_t)(gd.bfirst + lane) + 1] = my_items;
@@ -342,138 +347,225 @@ __device__ __forceinline__ float group_origin(float lo, float hi, float cgrid, f
     return 0.f;
 }
 
-// Force-group kernel.  One warp per force group, lane = target.  Entries are
-// read 32 at a time; their records (one node record and/or the opened
-// bucket's particles) are expanded warp-cooperatively into a shared-memory
-// window in group-relative float32 coordinates (node COM hi + lo folded in
-// once per record, not once per pair) and broadcast to all lanes.  Records
-// are stored in PAIRS, (x0 x1 y0 y1)(z0 z1 m0 m1), so every lane evaluates two
-// records per step with packed FADD2/FFMA2/FMUL2 (sm_100 f32x2): half the
-// issue slots of scalar FP32 for the same arithmetic.
-constexpr int PWIN = QWIN / 2;  // record pairs per window
-constexpr int PFLUSH = 16;  // records per fp64 flush (8 per packed half)
+// ---------------------------------------------------------------------------
+// Reorganisation + force kernels.
+//
+// EXPAND (the BH form of the paper's data reorganisation):
+// one warp per force group gathers every source record its union list names
+// -- the node's centre of mass (hi + lo) and mass, or an opened bucket's
+// particles -- from their scattered homes into ONE contiguous staging run of
+// float4 (x, y, z, m) records in the group's float32 frame (node COM hi + lo
+// folded in once per record instead of once per pair), plus a bucket mask
+// per record.  Runs start at multiples of PFLUSH records and are padded with
+// massless records.
+//
+// FORCE: one warp per force group, lane = target, streams its run through
+// shared memory (cp.async double buffer, TILE records per stage), transposes
+// each stage into PAIRS, A (x0 x1 y0 y1) / B (z0 z1 m0 m1), and evaluates two
+// records per step with FADD2/FFMA2/FMUL2 (sm_100 f32x2): half the issue
+// slots of scalar FP32 for the same arithmetic.
+// ---------------------------------------------------------------------------
+constexpr int PFLUSH = 16;  // records per fp64 flush (8 per packed half); run granularity
+constexpr int TILE = 64;  // records per cp.async stage
+
+struct Staging {
+    float4 *rec;  // per record: x, y, z (group frame), m
+    unsigned *mask;  // per record: buckets (bits of the walk group) that use it
+    const int64_t *rbase;  // first record of each force group's run (multiple of PFLUSH)
+    const int *order;  // force groups in processing order (longest run first)
+    int *next;  // dynamic work counter of the force kernel
+    int64_t cap;  // records
+};
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-#ifndef FORCE_MINB
-#define FORCE_MINB 3  // blocks per SM the force kernel is register-budgeted for
-#endif
-template <bool EPS0, bool POT>
-__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, FORCE_MINB)
-force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U,
-                   const float4 *__restrict__ parts, const int *__restrict__ part_bucket,
-                   const int *__restrict__ porder, const WalkGroup *__restrict__ wgroups,
-                   const float4 *__restrict__ rec_hi, const float4 *__restrict__ rec_lo, float cgrid, float eps2,
-                   double g, int dim, double *__restrict__ out, double *__restrict__ pot_out)
+// The force group's frame: origin from its targets (see group_origin).
+struct GroupFrame {
+    float cx, cy, cz;
+};
+__device__ __forceinline__ GroupFrame group_frame(float4 xp, float cgrid)
 {
-    __shared__ __align__(16) float4 q_xy[WARPS_PER_BLOCK][PWIN];  // (x0, x1, y0, y1)
-    __shared__ __align__(16) float4 q_zm[WARPS_PER_BLOCK][PWIN];  // (z0, z1, m0, m1)
-    __shared__ __align__(16) unsigned q_msk[WARPS_PER_BLOCK][QWIN];
+    const float inv_cgrid = 1.0f / cgrid;  // power of two: exact
+    GroupFrame f;
+    f.cx = group_origin(warp_min(xp.x), warp_max(xp.x), cgrid, inv_cgrid);
+    f.cy = group_origin(warp_min(xp.y), warp_max(xp.y), cgrid, inv_cgrid);
+    f.cz = group_origin(warp_min(xp.z), warp_max(xp.z), cgrid, inv_cgrid);
+    return f;
+}
+
+static __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK)
+expand_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U, const float4 *__restrict__ parts,
+              const float4 *__restrict__ rec_hi, const float4 *__restrict__ rec_lo, float cgrid, const Staging S,
+              int *__restrict__ flag)
+{
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gi = blockIdx.x * WARPS_PER_BLOCK + warp;
     if (gi >= nfg) return;
+    const int64_t rb = S.rbase[gi];
+    const int nrec = U.grec[gi];
+    const int padded = (nrec + PFLUSH - 1) & ~(PFLUSH - 1);
+    if (rb + padded > S.cap) {  // staging too small: the host resizes and re-runs
+        if (lane == 0) atomicOr(flag, 4);
+        return;
+    }
     const ForceGroup fg = fgroups[gi];
-    const int wfirst = wgroups[fg.wg].bfirst;
-    const bool tgt = lane < fg.ntarget;
-    const int p = fg.pstart + (tgt ? lane : 0);
-    const float4 xp = parts[p];
-    const unsigned mybit = tgt ? (1u << (part_bucket[p] - wfirst)) : 0u;
-    const float inv_cgrid = 1.0f / cgrid;  // power of two: exact
-    const float cx = group_origin(warp_min(xp.x), warp_max(xp.x), cgrid, inv_cgrid);
-    const float cy = group_origin(warp_min(xp.y), warp_max(xp.y), cgrid, inv_cgrid);
-    const float cz = group_origin(warp_min(xp.z), warp_max(xp.z), cgrid, inv_cgrid);
-    // target in group coordinates (exact), negated and duplicated for the packed subtract
-    const float2 nx = f2(cx - xp.x, cx - xp.x), ny = f2(cy - xp.y, cy - xp.y), nz = f2(cz - xp.z, cz - xp.z);
-    const float2 e2 = f2(eps2, eps2);
-    float *qa = reinterpret_cast<float *>(q_xy[warp]);
-    float *qb = reinterpret_cast<float *>(q_zm[warp]);
-    unsigned *qm = q_msk[warp];
-    double ax = 0.0, ay = 0.0, az = 0.0, ap = 0.0;
+    const float4 xp = parts[fg.pstart + min(lane, fg.ntarget - 1)];
+    const GroupFrame F = group_frame(xp, cgrid);
+    float4 *rec = S.rec + rb;
+    unsigned *msk = S.mask + rb;
     const int n = U.gcount[gi];
     int chunk = n > 0 ? U.gfirst[gi] : 0;
-    int next_chunk = n > CHUNK ? U.cnext[chunk] : 0;
-    // entries of batch e0 are loaded one batch ahead (latency overlaps the window compute)
-    int4 en = lane < n ? U.ent[chunk * CHUNK + lane] : make_int4(0, 0, 0, 0);
+    int out = 0;  // records written so far
     for (int e0 = 0; e0 < n; e0 += 32) {
-        const int node = en.x;
-        const uint2 m = make_uint2((unsigned)en.y, (unsigned)en.z);
-        const int word = en.w;
-        {
-            const int e1 = e0 + 32;
-            if (e1 < n && (e1 & (CHUNK - 1)) == 0) {
-                chunk = next_chunk;
-                if (e1 + CHUNK < n) next_chunk = U.cnext[chunk];
-            }
-            en = e1 + lane < n ? U.ent[chunk * CHUNK + (e1 & (CHUNK - 1)) + lane] : make_int4(0, 0, 0, 0);
+        if (e0 > 0 && (e0 & (CHUNK - 1)) == 0) chunk = U.cnext[chunk];
+        const int e = e0 + lane;
+        const int4 en = e < n ? U.ent[chunk * CHUNK + (e & (CHUNK - 1))] : make_int4(0, 0, 0, 0);
+        const unsigned mx = (unsigned)en.y, my = (unsigned)en.z;
+        float4 h = make_float4(0.f, 0.f, 0.f, 0.f), l = h;
+        if (mx) {
+            h = rec_hi[en.x];
+            l = rec_lo[en.x];
         }
-        const int hasnode = m.x ? 1 : 0;
-        const int nrec = hasnode + (m.y ? wr_pcount(word) : 0);
-        // warp inclusive scan of record counts
-        int incl = nrec;
+        const int hasnode = mx ? 1 : 0;
+        const int pc = my ? wr_pcount(en.w) : 0;
+        const int cnt = hasnode + pc;
+        int incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int t = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += t;
         }
         const int total = __shfl_sync(0xffffffffu, incl, 31);
-        const int first = incl - nrec;
-        const int psrc = wr_pstart(word) - hasnode;  // particle record r >= hasnode is parts[psrc + r]
-        for (int w0 = 0; w0 < total; w0 += QWIN) {
-            const int nin = min(QWIN, total - w0);
-            const int padded = (nin + PFLUSH - 1) & ~(PFLUSH - 1);
-            // cooperative expansion: slot s of the window belongs to the lane
-            // whose [first, incl) holds w0 + s (binary search over the scan)
-            for (int s0 = 0; s0 < padded; s0 += 32) {
-                const int s = s0 + lane;
-                const int gs = w0 + s;
-                int own = 0;
+        const int r = out + incl - cnt;  // this entry's first record
+        if (mx) {
+            rec[r] = make_float4((h.x - F.cx) + l.x, (h.y - F.cy) + l.y, (h.z - F.cz) + l.z, h.w);
+            msk[r] = mx;
+        }
+        // opened buckets: particle k of every entry in round k (loads grouped by 4)
+        const int maxpc = (int)__reduce_max_sync(0xffffffffu, (unsigned)pc);
+        const float4 *src = parts + wr_pstart(en.w);
+        float4 *dst = rec + r + hasnode;
+        for (int k0 = 0; k0 < maxpc; k0 += 4) {
+            float4 q[4];
 #pragma unroll
-                for (int step = 16; step >= 1; step >>= 1) {
-                    const int v = __shfl_sync(0xffffffffu, incl, own + step - 1);
-                    if (v <= gs) own += step;
+            for (int k = 0; k < 4; ++k)
+                if (k0 + k < pc) q[k] = src[k0 + k];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k0 + k < pc) {
+                    dst[k0 + k] = make_float4(q[k].x - F.cx, q[k].y - F.cy, q[k].z - F.cz, q[k].w);
+                    msk[r + hasnode + k0 + k] = my;
                 }
-                own = min(own, 31);
-                const int o_first = __shfl_sync(0xffffffffu, first, own);
-                const int o_node = __shfl_sync(0xffffffffu, node, own);
-                const unsigned o_mx = __shfl_sync(0xffffffffu, m.x, own);
-                const unsigned o_my = __shfl_sync(0xffffffffu, m.y, own);
-                const int o_psrc = __shfl_sync(0xffffffffu, psrc, own);
-                if (s < padded) {
-                    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);  // massless padding up to a PFLUSH multiple
-                    unsigned mk = 0u;
-                    if (s < nin) {
-                        const int r = gs - o_first;
-#if FORCE_EXP == 2
-                        if (true) {
-                            q = make_float4(r * 0.001f, o_node * 1e-7f, 0.5f, 1e-6f);
-                            mk = o_mx | o_my;
-                        } else
+        }
+        out += total;
+    }
+    if (out + lane < padded) {
+        rec[out + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+        msk[out + lane] = 0u;
+    }
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+#ifndef FORCE_SCALAR
+#define FORCE_SCALAR 0  // 1: scalar FP32 inner loop (A/B reference for the packed f32x2 loop)
 #endif
-                        if (o_mx && r == 0) {
-                            const float4 h = rec_hi[o_node];
-                            const float4 l = rec_lo[o_node];
-                            q = make_float4((h.x - cx) + l.x, (h.y - cy) + l.y, (h.z - cz) + l.z, h.w);
-                            mk = o_mx;
-                        } else {
-                            const float4 h = parts[o_psrc + r];
-                            q = make_float4(h.x - cx, h.y - cy, h.z - cz, h.w);
-                            mk = o_my;
-                        }
-                    }
-                    const int base = (s >> 1) * 4 + (s & 1);
-                    qa[base] = q.x;
-                    qa[base + 2] = q.y;
-                    qb[base] = q.z;
-                    qb[base + 2] = q.w;
-                    qm[s] = mk;
-                }
+#ifndef FORCE_MINB
+#define FORCE_MINB 4  // blocks per SM the force kernel is register-budgeted for
+#endif
+template <bool EPS0, bool POT>
+__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, FORCE_MINB)
+force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int *__restrict__ grec, const Staging S,
+                   const float4 *__restrict__ parts, const int *__restrict__ part_bucket,
+                   const int *__restrict__ porder, const WalkGroup *__restrict__ wgroups, float cgrid, float eps2,
+                   double g, int dim, double *__restrict__ out, double *__restrict__ pot_out)
+{
+    __shared__ __align__(16) float4 t_rec[WARPS_PER_BLOCK][2][TILE];  // cp.async stages (AoS)
+    __shared__ __align__(16) unsigned t_m[WARPS_PER_BLOCK][2][TILE];
+    __shared__ __align__(16) float4 t_a[WARPS_PER_BLOCK][TILE / 2];  // pairs: x0 x1 y0 y1
+    __shared__ __align__(16) float4 t_b[WARPS_PER_BLOCK][TILE / 2];  // pairs: z0 z1 m0 m1
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float4 *qa = t_a[warp];
+    float4 *qb = t_b[warp];
+    const float2 e2 = f2(eps2, eps2);
+    // persistent warps: force groups in longest-run-first order, handed out dynamically
+    for (int slot = lane == 0 ? atomicAdd(S.next, 1) : 0;;) {
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if (slot >= nfg) break;
+        const int gi = S.order[slot];
+        const ForceGroup fg = fgroups[gi];
+        const int64_t rb = S.rbase[gi];
+        const int padded = (grec[gi] + PFLUSH - 1) & ~(PFLUSH - 1);
+        const int ntile = (padded + TILE - 1) / TILE;
+        // stage tile t of the run into buffer t & 1 (2 records + 2 masks per lane)
+        auto issue = [&](int t) {
+            const int64_t r0 = rb + (int64_t)t * TILE;
+            const int buf = t & 1;
+            cp_async16(&t_rec[warp][buf][lane], S.rec + r0 + lane);
+            cp_async16(&t_rec[warp][buf][lane + 32], S.rec + r0 + lane + 32);
+            if (lane < TILE / 4) cp_async16(&t_m[warp][buf][4 * lane], S.mask + r0 + 4 * lane);
+            cp_async_commit();
+        };
+        if (ntile > 0) issue(0);
+        const bool tgt = lane < fg.ntarget;
+        const int p = fg.pstart + (tgt ? lane : 0);
+        const float4 xp = parts[p];
+        const unsigned mybit = tgt ? (1u << (part_bucket[p] - wgroups[fg.wg].bfirst)) : 0u;
+        const GroupFrame F = group_frame(xp, cgrid);
+        // target in group coordinates (exact), negated and duplicated for the packed subtract
+        const float2 nx = f2(F.cx - xp.x, F.cx - xp.x), ny = f2(F.cy - xp.y, F.cy - xp.y),
+                     nz = f2(F.cz - xp.z, F.cz - xp.z);
+        double ax = 0.0, ay = 0.0, az = 0.0, ap = 0.0;
+        for (int t = 0; t < ntile; ++t) {
+            if (t + 1 < ntile) {
+                issue(t + 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
             }
             __syncwarp();
-#if FORCE_EXP == 1
-            if (qm[lane] != 0xdeadbeefu) ax += 1.0;
-            else
-#endif
-            for (int j0 = 0; j0 < padded; j0 += PFLUSH) {
+            const int buf = t & 1;
+            if (!FORCE_SCALAR) {  // transpose the stage into pairs
+                const float4 r0 = t_rec[warp][buf][2 * lane], r1 = t_rec[warp][buf][2 * lane + 1];
+                qa[lane] = make_float4(r0.x, r1.x, r0.y, r1.y);
+                qb[lane] = make_float4(r0.z, r1.z, r0.w, r1.w);
+            }
+            __syncwarp();
+#if FORCE_SCALAR
+            const unsigned *qm = t_m[warp][buf];
+            const int nin = min(TILE, padded - t * TILE);
+            const float4 *qr = t_rec[warp][buf];
+            const float3 xr = make_float3(-nx.x, -ny.x, -nz.x);
+            for (int j0 = 0; j0 < nin; j0 += PFLUSH) {
+                float3 a = make_float3(0.f, 0.f, 0.f);
+                float pt = 0.f;
+#pragma unroll
+                for (int kk = 0; kk < PFLUSH; kk += 4) {
+                    const uint4 k4 = *reinterpret_cast<const uint4 *>(qm + j0 + kk);
+                    const unsigned ks[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const float4 q = qr[j0 + kk + h];
+                        const float me = (ks[h] & mybit) ? q.w : 0.f;
+                        interact_rel<EPS0, POT>(q, me, xr, eps2, a, pt);
+                    }
+                }
+                ax += (double)a.x;
+                ay += (double)a.y;
+                az += (double)a.z;
+                if (POT) ap += (double)pt;
+            }
+#else
+            const unsigned *qm = t_m[warp][buf];
+            const int nin = min(TILE, padded - t * TILE);
+            for (int j0 = 0; j0 < nin; j0 += PFLUSH) {
                 float2 sx = f2(0.f, 0.f), sy = f2(0.f, 0.f), sz = f2(0.f, 0.f), sp = f2(0.f, 0.f);
 #pragma unroll
                 for (int kk = 0; kk < PFLUSH; kk += 4) {
@@ -481,8 +573,8 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int pi = (j0 + kk) / 2 + h;
-                        const float4 A = q_xy[warp][pi];
-                        const float4 B = q_zm[warp][pi];
+                        const float4 A = qa[pi];
+                        const float4 B = qb[pi];
                         const unsigned k0 = h ? k4.z : k4.x, k1 = h ? k4.w : k4.y;
                         const float2 dx = __fadd2_rn(f2(A.x, A.y), nx);
                         const float2 dy = __fadd2_rn(f2(A.z, A.w), ny);
@@ -507,21 +599,24 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
                         }
                     }
                 }
-                ax += (double)sx.x + (double)sx.y;
-                ay += (double)sy.x + (double)sy.y;
-                az += (double)sz.x + (double)sz.y;
-                if (POT) ap += (double)sp.x + (double)sp.y;
+                // fold the packed halves in float32 (8 + 8 terms), accumulate in float64
+                ax += (double)(sx.x + sx.y);
+                ay += (double)(sy.x + sy.y);
+                az += (double)(sz.x + sz.y);
+                if (POT) ap += (double)(sp.x + sp.y);
             }
-            __syncwarp();
+#endif
+            __syncwarp();  // stage t & 1 and the pair buffer are rewritten next
         }
-    }
-    if (tgt) {
-        const int orig = porder[p];
-        const double gm = g * (double)xp.w;
-        out[(int64_t)orig * dim + 0] = gm * ax;
-        if (dim > 1) out[(int64_t)orig * dim + 1] = gm * ay;
-        if (dim > 2) out[(int64_t)orig * dim + 2] = gm * az;
-        if (POT) pot_out[orig] = -gm * ap;  // -G m_i sum_j m_j / sqrt(r^2 + eps^2)
+        if (tgt) {
+            const int orig = porder[p];
+            const double gm = g * (double)xp.w;
+            out[(int64_t)orig * dim + 0] = gm * ax;
+            if (dim > 1) out[(int64_t)orig * dim + 1] = gm * ay;
+            if (dim > 2) out[(int64_t)orig * dim + 2] = gm * az;
+            if (POT) pot_out[orig] = -gm * ap;  // -G m_i sum_j m_j / sqrt(r^2 + eps^2)
+        }
+        if (lane == 0) slot = atomicAdd(S.next, 1);
     }
 }
 

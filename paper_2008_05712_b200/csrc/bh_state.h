@@ -65,7 +65,13 @@ struct gc_bh {
     double cap_theta = -1.0;
     bool stats_valid = false;  // d_bstat describes the current tree + theta
     // chunked union-list pool (bh_kernels.cuh: UnionPool)
-    DBuf<int> d_cnext, d_gfirst, d_gcount, d_top;
+    DBuf<int> d_cnext, d_gfirst, d_gcount, d_grec, d_top;
+    // staging runs of source records per force group (expand_kernel -> force_group_kernel)
+    DBuf<int64_t> d_rbase;
+    DBuf<float4> d_srec;
+    DBuf<unsigned> d_smask;
+    DBuf<int> d_fg_key, d_fg_iota, d_fg_order, d_next;
+    int64_t staging_cap = 0;
     DBuf<int4> d_ent;
     int pool_chunks = 0;
     DBuf<int64_t> d_bstat;
@@ -84,7 +90,8 @@ struct gc_bh {
     DBuf<int> d_flag;
     WalkParams wp{};
     bool stats_dirty = false;  // d_bstat newer than the host copies
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // walk begin/end, forces begin/end, reorganisation end (= force kernel begin)
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     BuildWs ws;
     int64_t h2d = 0, d2h = 0;  // bytes moved host<->device since the last reset
     ~gc_bh()

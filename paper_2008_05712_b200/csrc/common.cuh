@@ -81,9 +81,9 @@ struct DBuf {
         resize(count);
         if (count) GC_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
     }
-    void download(T *h, size_t count, cudaStream_t s) const
+    void download(T *h, size_t count, cudaStream_t s, size_t offset = 0) const
     {
-        if (count) GC_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+        if (count) GC_CUDA(cudaMemcpyAsync(h, p + offset, count * sizeof(T), cudaMemcpyDeviceToHost, s));
     }
     void zero(cudaStream_t s)
     {

@@ -13,8 +13,8 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
 ps = gen.fp32_exact(gen.gen_particles(n, 42, clustering=0.6, dim=3))
 tree = nbody.build_bucket_tree(ps, 8)
 ctx = L.context()
-tm = np.zeros(2)
-w, f = [], []
+tm = np.zeros(3)
+w, f, r = [], [], []
 for i in range(12):
     L.call("gc_bh_walk", tree.handle, 0.7)
     L.call("gc_bh_forces_async", tree.handle, 1.0, 1e-4)
@@ -22,7 +22,8 @@ for i in range(12):
     if i >= 2:
         w.append(tm[0])
         f.append(tm[1])
+        r.append(tm[2])
 inter = nbody.interactions(tree)
 fm = statistics.median(f)
-print(f"{L.LIB_PATH.split('/')[-1]}: walk {statistics.median(w):.3f} ms  force {fm:.3f} ms  "
+print(f"{L.LIB_PATH.split('/')[-1]}: walk {statistics.median(w):.3f} ms  reorg {statistics.median(r):.3f} ms  force {fm:.3f} ms  "
       f"{20 * inter / fm / 1e9:.2f} TFLOP/s ({inter} interactions)")
