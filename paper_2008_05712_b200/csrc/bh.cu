@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "bh_state.h"
@@ -367,21 +368,12 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
         }
         // first guess ~160 records per bucket; an overflow grows it to the walk's demand
         if (bh->staging_cap == 0) size_staging(bh, 160 * bh->n_buckets + 1024);
-        // processing order of the persistent force kernel: longest run first
-        bh->d_fg_key.resize(nfg);
-        bh->d_fg_iota.resize(nfg);
+        // the persistent force kernel hands out force groups in depth-first order
+        // (a longest-run-first sort costs more than the tail it removes at 1M)
         bh->d_fg_order.resize(nfg);
         bh->d_next.resize(1);
         bh->d_next.zero(s);
-        if (nfg > 0) {
-            bb_iota_kernel<<<grid_for(nfg, 256), 256, 0, s>>>(nfg, bh->d_fg_iota.p);
-            size_t bytes = 0;
-            GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, U.grec, bh->d_fg_key.p,
-                                                              bh->d_fg_iota.p, bh->d_fg_order.p, nfg, 0, 32, s));
-            ctx->scratch.resize(bytes);
-            GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(ctx->scratch.p, bytes, U.grec, bh->d_fg_key.p,
-                                                              bh->d_fg_iota.p, bh->d_fg_order.p, nfg, 0, 32, s));
-        }
+        if (nfg > 0) bb_iota_kernel<<<grid_for(nfg, 256), 256, 0, s>>>(nfg, bh->d_fg_order.p);
         Staging S;
         S.rec = bh->d_srec.p;
         S.mask = bh->d_smask.p;

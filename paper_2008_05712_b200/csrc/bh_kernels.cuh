@@ -372,7 +372,7 @@ struct Staging {
     float4 *rec;  // per record: x, y, z (group frame), m
     unsigned *mask;  // per record: buckets (bits of the walk group) that use it
     const int64_t *rbase;  // first record of each force group's run (multiple of PFLUSH)
-    const int *order;  // force groups in processing order (longest run first)
+    const int *order;  // force groups in processing order
     int *next;  // dynamic work counter of the force kernel
     int64_t cap;  // records
 };
@@ -392,6 +392,15 @@ __device__ __forceinline__ GroupFrame group_frame(float4 xp, float cgrid)
     f.cz = group_origin(warp_min(xp.z), warp_max(xp.z), cgrid, inv_cgrid);
     return f;
 }
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 static __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK)
 expand_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U, const float4 *__restrict__ parts,
@@ -413,19 +422,21 @@ expand_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U
     const GroupFrame F = group_frame(xp, cgrid);
     float4 *rec = S.rec + rb;
     unsigned *msk = S.mask + rb;
+    // union chunks stream through shared memory, one chunk ahead (cp.async)
+    __shared__ __align__(16) int4 ebuf[WARPS_PER_BLOCK][2][CHUNK];
     const int n = U.gcount[gi];
+    const int nchunk = (n + CHUNK - 1) / CHUNK;
     int chunk = n > 0 ? U.gfirst[gi] : 0;
+    auto fetch = [&](int c, int buf) {
+#pragma unroll
+        for (int k = 0; k < CHUNK / 32; ++k) cp_async16(&ebuf[warp][buf][lane + 32 * k], U.ent + (int64_t)c * CHUNK + lane + 32 * k);
+        cp_async_commit();
+    };
+    if (nchunk > 0) fetch(chunk, 0);
     int out = 0;  // records written so far
-    for (int e0 = 0; e0 < n; e0 += 32) {
-        if (e0 > 0 && (e0 & (CHUNK - 1)) == 0) chunk = U.cnext[chunk];
-        const int e = e0 + lane;
-        const int4 en = e < n ? U.ent[chunk * CHUNK + (e & (CHUNK - 1))] : make_int4(0, 0, 0, 0);
+    // one union entry -> its node record and/or its opened bucket's particles
+    auto emit = [&](const int4 en, const float4 h, const float4 l) {
         const unsigned mx = (unsigned)en.y, my = (unsigned)en.z;
-        float4 h = make_float4(0.f, 0.f, 0.f, 0.f), l = h;
-        if (mx) {
-            h = rec_hi[en.x];
-            l = rec_lo[en.x];
-        }
         const int hasnode = mx ? 1 : 0;
         const int pc = my ? wr_pcount(en.w) : 0;
         const int cnt = hasnode + pc;
@@ -458,21 +469,34 @@ expand_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U
                 }
         }
         out += total;
+    };
+    for (int e0 = 0; e0 < n; e0 += 32) {
+        const int ci = e0 / CHUNK;
+        if ((e0 & (CHUNK - 1)) == 0) {
+            __syncwarp();  // the previous chunk's buffer is refilled below
+            if (ci + 1 < nchunk) {
+                chunk = U.cnext[chunk];
+                fetch(chunk, (ci + 1) & 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncwarp();
+        }
+        const int e = e0 + lane;
+        const int4 en = e < n ? ebuf[warp][ci & 1][e & (CHUNK - 1)] : make_int4(0, 0, 0, 0);
+        float4 h = make_float4(0.f, 0.f, 0.f, 0.f), l = h;
+        if (en.y) {
+            h = rec_hi[en.x];
+            l = rec_lo[en.x];
+        }
+        emit(en, h, l);
     }
     if (out + lane < padded) {
         rec[out + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
         msk[out + lane] = 0u;
     }
 }
-
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
-{
-    const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 #ifndef FORCE_SCALAR
 #define FORCE_SCALAR 0  // 1: scalar FP32 inner loop (A/B reference for the packed f32x2 loop)
@@ -495,7 +519,7 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int *_
     float4 *qa = t_a[warp];
     float4 *qb = t_b[warp];
     const float2 e2 = f2(eps2, eps2);
-    // persistent warps: force groups in longest-run-first order, handed out dynamically
+    // persistent warps: force groups handed out dynamically
     for (int slot = lane == 0 ? atomicAdd(S.next, 1) : 0;;) {
         slot = __shfl_sync(0xffffffffu, slot, 0);
         if (slot >= nfg) break;

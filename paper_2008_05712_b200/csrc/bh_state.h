@@ -70,7 +70,7 @@ struct gc_bh {
     DBuf<int64_t> d_rbase;
     DBuf<float4> d_srec;
     DBuf<unsigned> d_smask;
-    DBuf<int> d_fg_key, d_fg_iota, d_fg_order, d_next;
+    DBuf<int> d_fg_order, d_next;
     int64_t staging_cap = 0;
     DBuf<int4> d_ent;
     int pool_chunks = 0;
