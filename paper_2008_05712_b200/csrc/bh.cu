@@ -198,15 +198,36 @@ void walk_params(gc_bh *bh, double theta)
     if (bh->params_valid && bh->cap_theta == theta) return;
     const double th2 = theta * theta;
     const double root = bh->box;
-    // per-level float32 thresholds on s = d^2: accept iff s > size^2 / theta^2
+    // Per-level float32 thresholds on the float32 s ~ d^2 (walk_group_kernel).
+    // Exact rule: accept iff d^2 > T = size^2 / theta^2 (nbody.py:178), decided
+    // with a 2^-22 relative margin (ta, tr) for the float64 rounding.  The
+    // float32 s differs from the exact sum by at most
+    //   E(s) = dd2 * sum(v) + dd3 + 4.8e-7 s <= dd2 * sqrt(3.000001 s) + dd3 + 4.8e-7 s,
+    // so s > A certainly accepts when A - E(A) >= ta and s < R certainly rejects
+    // when R + E(R) <= tr (both sides monotone in s there); A and R solve the
+    // quadratics in sqrt(s), widened by 1e-6 and rounded outwards.
+    const double dd2 = bh->walk_dd2, dd3 = bh->walk_dd3, c = 4.8e-7, k = dd2 * std::sqrt(3.000001);
     std::vector<float2> tt(MAX_LEVELS);
     for (int l = 0; l < MAX_LEVELS; ++l) {
         const double size = std::ldexp(root, -l);
         const double T = theta > 0.0 ? size * size / th2 : HUGE_VAL;
-        const float a = (float)(T * (1.0 + std::ldexp(1.0, -22)));
-        const float r = (float)(T * (1.0 - std::ldexp(1.0, -22)));
-        tt[l].x = std::nextafter(a, HUGE_VALF);
-        tt[l].y = std::isinf(r) ? r : std::nextafter(r, 0.f);
+        const double ta = T * (1.0 + std::ldexp(1.0, -22)), tr = T * (1.0 - std::ldexp(1.0, -22));
+        float A = HUGE_VALF, R = -HUGE_VALF;
+        if (std::isfinite(ta)) {
+            const double u = (k + std::sqrt(k * k + 4.0 * (1.0 - c) * (dd3 + ta))) / (2.0 * (1.0 - c));
+            const double a = u * u * (1.0 + 1e-6);
+            if (a < 3e38) A = std::nextafter((float)a, HUGE_VALF);
+        }
+        if (tr > dd3) {
+            if (std::isfinite(tr)) {
+                const double u = (-k + std::sqrt(k * k + 4.0 * (1.0 + c) * (tr - dd3))) / (2.0 * (1.0 + c));
+                R = std::nextafter((float)(u * u * (1.0 - 1e-6)), 0.f);
+            } else {
+                R = HUGE_VALF;  // theta = 0: nothing is ever accepted, every node is certainly rejected
+            }
+        }
+        tt[l].x = A;
+        tt[l].y = R;
     }
     bh->d_tt.upload(tt.data(), MAX_LEVELS, bh->ctx->stream);
     bh->wp.theta = theta;

@@ -52,7 +52,7 @@ struct ForceGroup {
 struct WalkParams {
     double theta, theta2, root_size;
     float dd2, dd3;  // 2*delta and 3*delta^2: float32 coordinate error bound
-    const float2 *tt;  // per level: (certain-accept, certain-reject) thresholds on d^2
+    const float2 *tt;  // per level: s > x certainly accepts, s < y certainly rejects (error band folded in)
 };
 
 // Walk record per node: float32 centre of mass and a packed word
@@ -150,14 +150,15 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
     int2 *stack = stack_s[warp];
     unsigned char *slvl = lvl_s[warp];
     int sp = 0;
-    // lanes whose geometry is not float32-exact always take the float64 test
-    const float dd3l = exact32 ? P.dd3 : __int_as_float(0x7f800000);
+    // lanes whose geometry is not float32-exact always take the float64 test (s = NaN)
+    const float s0 = exact32 ? 0.f : __int_as_float(0x7fc00000);
     // lane f < nfg emits the list of force group fg_first + f; its current
     // chunk always has room for slot w % CHUNK (allocated one entry ahead)
     const bool emits = lane < gd.nfg;
     const int my_fg = gd.fg_first + (emits ? lane : 0);
     const unsigned fgm = emits ? fg_mask[my_fg] : 0u;
     int w = 0, chunk = 0, nrec = 0;
+    int4 *wp = U.ent;  // next entry slot of this lane's force group
     if (WRITE && emits) {
         chunk = atomicAdd(U.top, 1);
         if (chunk >= U.nchunks) {  // overflow: park in the sink chunk, the host re-walks
@@ -165,6 +166,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
             chunk = U.nchunks;
         }
         U.gfirst[my_fg] = chunk;
+        wp = U.ent + (int64_t)chunk * CHUNK;
     }
     int my_entries = 0, my_items = 0;
     // the root is a sibling group of one, tested by every bucket
@@ -174,6 +176,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
         const float2 th = tt_s[lvl];
         const int last = first + nc - 1;
         float4 nd = recs[first];
+#pragma unroll 2
         for (int node = first; node <= last; ++node) {
             const float4 nd_next = recs[min(node + 1, last)];  // prefetch the next sibling
             const int wd = __float_as_int(nd.w);
@@ -182,10 +185,9 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
             const float v0 = fmaxf(fabsf(nd.x - bf.x) - bf.w, 0.f);
             const float v1 = fmaxf(fabsf(nd.y - bf.y) - bf.w, 0.f);
             const float v2 = fmaxf(fabsf(nd.z - bf.z) - bf.w, 0.f);
-            const float s = fmaf(v2, v2, fmaf(v1, v1, v0 * v0));
-            const float err = fmaf(P.dd2, v0 + v1 + v2, fmaf(s, 4.8e-7f, dd3l));
-            unsigned acc_m = __ballot_sync(0xffffffffu, s - err > th.x) & act;
-            const unsigned unsure_m = ~__ballot_sync(0xffffffffu, s + err < th.y) & ~acc_m & act;
+            const float s = fmaf(v2, v2, fmaf(v1, v1, fmaf(v0, v0, s0)));
+            unsigned acc_m = __ballot_sync(0xffffffffu, s > th.x) & act;
+            const unsigned unsure_m = ~__ballot_sync(0xffffffffu, s < th.y) & ~acc_m & act;
             if (unsure_m) {  // rare: the reference's float64 test (warp-uniform branch)
                 bool a = false;
                 if (unsure_m & bit)
@@ -196,9 +198,9 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
             const unsigned part_m = is_bucket ? (act & ~acc_m) : 0u;
             const unsigned hit = (acc_m | part_m) & fgm;
             if (WRITE) {
-                if (emits) U.ent[chunk * CHUNK + (w & (CHUNK - 1))] =
-                    make_int4(node, (int)(acc_m & fgm), (int)(part_m & fgm), wd);
+                if (emits) *wp = make_int4(node, (int)(acc_m & fgm), (int)(part_m & fgm), wd);
                 w += hit ? 1 : 0;
+                wp += hit ? 1 : 0;
                 nrec += ((acc_m & fgm) ? 1 : 0) + ((part_m & fgm) ? wr_pcount(wd) : 0);
                 if (hit && (w & (CHUNK - 1)) == 0) {  // chunk full: link the next one
                     int cn = atomicAdd(U.top, 1);
@@ -208,6 +210,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
                     }
                     U.cnext[chunk] = cn;
                     chunk = cn;
+                    wp = U.ent + (int64_t)cn * CHUNK;
                 }
             }
             if (STATS) {
