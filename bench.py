@@ -214,6 +214,16 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the
+    committed ncu --set full summary (profiles/ncu_traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh).get(kernel)
+    except Exception:
+        return None
+
+
 def bench_bh(args, world, rank, local, ctx, torch):
     from paper_2008_05712_b200 import _lib as L
     from paper_2008_05712_b200 import nbody
@@ -231,7 +241,9 @@ def bench_bh(args, world, rank, local, ctx, torch):
         step()
     ctx.sync()
     inter = nbody.interactions(tree)
-    step_ms, walk_ms, force_ms = [], [], []
+    sizes = tree.sizes()
+    n_union, n_records = int(sizes[3]), int(sizes[4])
+    step_ms, walk_ms, reorg_ms, force_ms = [], [], [], []
     tm = np.zeros(3)
     barrier(world)
     torch.cuda.synchronize()
@@ -249,13 +261,15 @@ def bench_bh(args, world, rank, local, ctx, torch):
             L.call("gc_bh_timings", tree.handle, L.ptr(tm, L.f64p))
             walk_ms.append(tm[0])
             force_ms.append(tm[1])
+            reorg_ms.append(tm[2])
     torch.cuda.synchronize()
     barrier(world)
     ms = allmax(sum(step_ms), world) / args.steps
-    f_ms, w_ms = statistics.mean(force_ms), statistics.mean(walk_ms)
+    f_ms, w_ms, r_ms = statistics.mean(force_ms), statistics.mean(walk_ms), statistics.mean(reorg_ms)
     pk, tmp = np.zeros(1), np.zeros(1)
     L.call("gc_measure_fp32_peak", ctx.handle, L.ptr(pk, L.f64p), L.ptr(tmp, L.f64p))
     fp32_peak = float(pk[0])
+    hbm, hbm_src = measured_hbm()
 
     # end to end through the C ABI: pinned host buffers, H2D + D2H inside
     pos_np = torch.from_numpy(np.ascontiguousarray(ps.positions)).pin_memory().numpy()
@@ -265,27 +279,34 @@ def bench_bh(args, world, rank, local, ctx, torch):
     stepper(pos_np, m_np, 1.0, out_np)  # warm-up
     e2e_s = []
     io = np.zeros(2, np.int64)
-    for _ in range(max(1, min(args.steps, 5))):
+    for _ in range(max(3, min(args.steps, 10))):
         barrier(world)
         t0 = time.perf_counter()
         stepper(pos_np, m_np, 1.0, out_np)
         e2e_s.append(time.perf_counter() - t0)
     L.call("gc_bh_io_bytes", stepper.handle, L.ptr(io, L.i64p), 0)
-    e2e_t = allmax(statistics.mean(e2e_s), world)
+    e2e_t = allmax(statistics.median(e2e_s), world)
     achieved = FLOPS_PER_INTERACTION * inter / (f_ms * 1e-3) / 1e12
+    # reorganisation: union entries read (16 B) + staged records written (16 B record + 4 B mask)
+    reorg_bytes = 16 * n_union + 20 * n_records
     return {
         "ps": ps, "inter": inter, "ms": ms, "value": world * inter / (ms * 1e-3), "walk_ms": w_ms, "force_ms": f_ms,
+        "reorg_ms": r_ms, "n_union": n_union, "n_records": n_records,
         "clocks": clk.summary(),
         "roofline": {"bound": "fp32", "kernel": "force_group_kernel", "achieved": achieved, "peak": fp32_peak,
                      "peak_source": "FFMA-chain probe on this GPU (gc_measure_fp32_peak); no fp32 entry in "
                                     "MEASURED_PEAKS.json", "nominal_peak": NOMINAL_FP32_TFLOPS, "unit": "TFLOP/s",
-                     "frac": achieved / fp32_peak, "traffic": None,
+                     "frac": achieved / fp32_peak, "traffic": ncu_traffic("force_group_kernel"),
                      "flops_per_interaction": FLOPS_PER_INTERACTION,
-                     "interactions_per_launch": inter},
+                     "interactions_per_launch": inter, "kernel_ms": f_ms},
+        "reorg_roofline": {"bound": "hbm", "kernel": "expand_kernel (+ run scan)", "unit": "GB/s",
+                           "achieved": reorg_bytes / (r_ms * 1e-3) / 1e9, "peak": hbm, "peak_source": hbm_src,
+                           "frac": reorg_bytes / (r_ms * 1e-3) / 1e9 / hbm, "traffic": ncu_traffic("expand_kernel"),
+                           "algorithmic_bytes_per_launch": reorg_bytes, "kernel_ms": r_ms},
         "e2e": {"value": world * inter / e2e_t, "unit": "interactions/s", "h2d_bytes_per_step": int(io[0]),
                 "d2h_bytes_per_step": int(io[1]), "ms_per_step": e2e_t * 1e3,
-                "path": "gc_bh_step C ABI: pinned host positions/masses -> H2D -> host tree -> device walk -> "
-                        "forces -> D2H"},
+                "path": "gc_bh_step C ABI: pinned host positions/masses -> H2D -> device tree build -> device walk "
+                        "-> reorganisation -> forces -> D2H (median of the timed calls)"},
     }
 
 
@@ -348,12 +369,15 @@ def run_ours(args, world, rank, local):
         "vs_baseline": None, "dtype": "fp32 force math (fp64 walk decisions, fp64 accumulation)",
         "data": "synthetic gen_particles(1M, seed 42+rank, clustering 0.6, dim 3), fp32-exact",
         "config": {"workload": "configs[2] clustered N-body 1M, theta 0.7, bucket 8, eps 1e-4 (1 system per GPU)",
-                   "step": "device walk (union lists) + bucket force kernel; tree resident in HBM",
-                   "interactions_per_gpu": bh["inter"], "walk_ms": bh["walk_ms"], "force_ms": bh["force_ms"],
+                   "step": "device walk (union lists) + reorganisation (staging runs) + force kernel; tree resident",
+                   "interactions_per_gpu": bh["inter"], "walk_ms": bh["walk_ms"], "reorg_ms": bh["reorg_ms"],
+                   "force_ms": bh["force_ms"], "union_entries": bh["n_union"], "staged_records": bh["n_records"],
                    "l2": "flushed (256 MiB write) before every timed step"},
         "roofline": bh["roofline"],
+        "reorg_roofline": bh["reorg_roofline"],
         "e2e": bh["e2e"],
-        "gpu_launches": 3 * args.steps,
+        # per step: walk_group_kernel, 2 cub scan kernels (run offsets), iota, expand_kernel, force_group_kernel
+        "gpu_launches": 6 * args.steps,
         "clocks": bh["clocks"],
     }
     sysin = mdr.pop("_sysin")

@@ -101,8 +101,9 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
  * both are bit-identical to build_bucket_tree.  Applies to the next
  * gc_bh_set_particles / gc_bh_step. */
 gc_status gc_bh_set_build_mode(gc_bh *bh, int32_t device);
-/* Sizes: out[0..3] = n_nodes, n_buckets, list entries, node entries */
-gc_status gc_bh_sizes(gc_bh *bh, int64_t out[4]);
+/* Sizes: out[0..4] = n_nodes, n_buckets, per-bucket list entries, union
+ * entries of the last device walk, source records they expand to (staging) */
+gc_status gc_bh_sizes(gc_bh *bh, int64_t out[5]);
 /* Tree arrays (host, caller-allocated by gc_bh_sizes): any pointer may be NULL */
 gc_status gc_bh_get_tree(gc_bh *bh, double *center, double *half, double *mass, double *com,
                          int64_t *first_child, int32_t *n_child, int64_t *pcount, int64_t *buckets,

@@ -500,25 +500,28 @@ gc_status gc_bh_set_build_mode(gc_bh *bh, int32_t device)
     });
 }
 
-gc_status gc_bh_sizes(gc_bh *bh, int64_t out[4])
+gc_status gc_bh_sizes(gc_bh *bh, int64_t out[5])
 {
     return guard([&] {
         GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
         out[0] = bh->n_nodes;
         out[1] = bh->n_buckets;
-        out[2] = out[3] = 0;
+        out[2] = out[3] = out[4] = 0;
         if (bh->params_valid) {
             sync_walk_stats(bh);
             out[2] = bh->n_list_entries;
         }
         if (bh->have_union) {
             ensure_union_complete(bh);
-            std::vector<int> cnt(bh->d_gcount.n);
-            bh->d_gcount.download(cnt.data(), cnt.size(), bh->ctx->stream);
+            const size_t nf = bh->d_gcount.n;
+            std::vector<int> cnt(nf), rec(nf);
+            bh->d_gcount.download(cnt.data(), nf, bh->ctx->stream);
+            bh->d_grec.download(rec.data(), nf, bh->ctx->stream);
             GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
-            int64_t tot = 0;
-            for (int c : cnt) tot += c;
-            out[3] = tot;
+            for (size_t f = 0; f < nf; ++f) {
+                out[3] += cnt[f];
+                out[4] += rec[f];
+            }
         }
     });
 }

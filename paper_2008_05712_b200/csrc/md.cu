@@ -76,6 +76,63 @@ __device__ __forceinline__ double np_remainder(double a, double b)
     return mod;
 }
 
+// md_step integrator (md.py:171-189): v += F dt (unit mass); x += v dt; then
+// periodic wrap (np.remainder) or reflecting walls + clip to hi - 1e-12
+__device__ __forceinline__ void md_advance(double x[3], double v[3], const double f[3], const MDParams &P, double dt)
+{
+    const double hi[3] = {P.bx, P.by, P.bz};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (k >= P.dim) break;
+        v[k] = __dadd_rn(v[k], __dmul_rn(f[k], dt));
+        x[k] = __dadd_rn(x[k], __dmul_rn(v[k], dt));
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (k >= P.dim) break;
+        if (P.periodic) {
+            // np.remainder (npy_divmod) fast path for one box of travel: fmod is
+            // exact there, and negative values take the rounded x + box
+            const double b = hi[k];
+            if (x[k] >= 0.0 && x[k] < b) x[k] = x[k] == 0.0 ? 0.0 : x[k];
+            else if (x[k] >= b && x[k] < 2.0 * b) x[k] = __dsub_rn(x[k], b);
+            else if (x[k] < 0.0 && x[k] > -b) x[k] = __dadd_rn(x[k], b);
+            else x[k] = np_remainder(x[k], b);
+        } else {
+            if (x[k] < 0.0) {
+                x[k] = -x[k];
+                v[k] = -v[k];
+            }
+            if (x[k] > hi[k]) {
+                x[k] = __dsub_rn(__dmul_rn(2.0, hi[k]), x[k]);
+                v[k] = -v[k];
+            }
+            x[k] = fmin(fmax(x[k], 0.0), __dsub_rn(hi[k], 1e-12));
+        }
+    }
+}
+
+// cell of a position: numpy floor_divide for the 2-D patches (md.py:187-189),
+// floor(x / cell) for the 3-D cells; clamped to the grid
+__device__ __forceinline__ int md_cell_index(const double x[3], const MDParams &P, int use_npy)
+{
+    int c3[3];
+    const int dims[3] = {P.nx, P.ny, P.nz};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (k >= P.dim) {
+            c3[k] = 0;
+            continue;
+        }
+        const double f = use_npy ? np_floordiv(x[k], P.cell) : floor(__ddiv_rn(x[k], P.cell));
+        long long ck = (long long)f;
+        if (ck > dims[k] - 1) ck = dims[k] - 1;
+        if (ck < 0) ck = 0;
+        c3[k] = (int)ck;
+    }
+    return (c3[0] * P.ny + c3[1]) * P.nz + c3[2];
+}
+
 template <int LAW, int DIM>
 __global__ void __launch_bounds__(MD_TPB)
 md_force_kernel(int n, const double4 *__restrict__ spos, const int *__restrict__ cell_start,
@@ -232,10 +289,63 @@ __device__ __forceinline__ void md_pair_exact(const double4 a, const long long i
     }
 }
 
+// Pair whose cutoff decision is already certain (float32 r^2 well inside the
+// cutoff): the same float64 force law in one orientation (home atom minus
+// shifted partner), reciprocal by float seed + two Newton steps.
 template <int LAW, int DIM>
+__device__ __forceinline__ void md_pair_inside(const double4 a, const double4 b, const double4 sh, const MDParams &P,
+                                               double &fx, double &fy, double &fz, double &en)
+{
+    const double d0 = a.x - (b.x + sh.x), d1 = a.y - (b.y + sh.y), d2 = DIM == 3 ? a.z - (b.z + sh.z) : 0.0;
+    const double r2 = fma(d2, d2, fma(d1, d1, d0 * d0));
+    double inv = (double)__frcp_rn((float)r2);
+    inv = fma(inv, fma(-r2, inv, 1.0), inv);
+    inv = fma(inv, fma(-r2, inv, 1.0), inv);
+    double mag;
+    if (LAW == LAW_SOFT) {
+        const double rinv = rsqrt(r2);
+        mag = P.stiffness * (P.cutoff * rinv - 1.0);
+    } else {
+        const double s2 = P.sig2 * inv;
+        const double s6 = s2 * s2 * s2;
+        const double s12 = s6 * s6;
+        mag = 24.0 * P.eps * (2.0 * s12 - s6) * inv;
+        en += 2.0 * P.eps * (s12 - s6);
+    }
+    fx = fma(d0, mag, fx);
+    fy = fma(d1, mag, fy);
+    if (DIM == 3) fz = fma(d2, mag, fz);
+}
+
+// Optional fused integrator epilogue (md_step, md.py:171-189): the home atom's
+// velocity and position are advanced as soon as its force is known (other
+// blocks read the cell-sorted copy, not pos), its new cell is assigned and
+// counted for the next step's cell sort.
+struct MDInteg {
+    double4 *pos, *vel;
+    int *cell_of, *count;
+    double dt;
+    int use_npy;
+};
+
+template <int DIM>
+__device__ __forceinline__ void md_integrate_one(long long ia, double3 f3, const MDParams &P, const MDInteg &I)
+{
+    const double4 p = I.pos[ia], q = I.vel[ia];
+    double x[3] = {p.x, p.y, p.z}, v[3] = {q.x, q.y, q.z};
+    const double f[3] = {f3.x, f3.y, f3.z};
+    md_advance(x, v, f, P, I.dt);
+    I.pos[ia] = make_double4(x[0], x[1], x[2], 0.0);
+    I.vel[ia] = make_double4(v[0], v[1], v[2], 0.0);
+    const int c = md_cell_index(x, P, I.use_npy);
+    I.cell_of[ia] = c;
+    atomicAdd(&I.count[c], 1);
+}
+
+template <int LAW, int DIM, bool INTEG>
 __global__ void __launch_bounds__(MDC_THREADS)
 md_cell_kernel(const double4 *__restrict__ spos, const int *__restrict__ cell_start, const MDParams P, float band,
-               double4 *__restrict__ out)
+               float inner, double4 *__restrict__ out, const MDInteg I)
 {
     __shared__ float4 nb[MDC_NB];  // rel xyz (float32 filter), packed (sorted index << 5 | offset code)
     __shared__ int qstart[27];
@@ -293,6 +403,7 @@ md_cell_kernel(const double4 *__restrict__ spos, const int *__restrict__ cell_st
                     if (j != h0 + i) md_pair_exact<LAW, DIM>(a, ia, spos[j], shtab[k], P, fx, fy, fz, en);
             }
             out[ia] = make_double4(fx, fy, fz, en);
+            if (INTEG) md_integrate_one<DIM>(ia, make_double3(fx, fy, fz), P, I);
         }
         return;
     }
@@ -328,8 +439,8 @@ md_cell_kernel(const double4 *__restrict__ spos, const int *__restrict__ cell_st
                 const float4 xj = nb[sl];
                 const float dx = xj.x - xi.x, dy = xj.y - xi.y, dz = xj.z - xi.z;
                 const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                if (r2 < band && sl != si) {
-                    if (cnt < MDC_LIST) lst[cnt] = (unsigned short)sl;
+                if (r2 < band && sl != si) {  // bit 15: inside the error band, take the exact test
+                    if (cnt < MDC_LIST) lst[cnt] = (unsigned short)(sl | (r2 < inner && r2 > 1e-6f ? 0 : 0x8000));
                     ++cnt;
                 }
             }
@@ -348,8 +459,9 @@ md_cell_kernel(const double4 *__restrict__ spos, const int *__restrict__ cell_st
                 for (int e = 0; e < MDC_LIST; ++e) {
                     const int sl = lst[e];
                     if (sl == 0xffff) break;
-                    const int pk = __float_as_int(nb[sl].w);
-                    md_pair_exact<LAW, DIM>(a, ia, spos[pk >> 5], shtab[pk & 31], P, fx, fy, fz, en);
+                    const int pk = __float_as_int(nb[sl & 0x7fff].w);
+                    if (sl & 0x8000) md_pair_exact<LAW, DIM>(a, ia, spos[pk >> 5], shtab[pk & 31], P, fx, fy, fz, en);
+                    else md_pair_inside<LAW, DIM>(a, spos[pk >> 5], shtab[pk & 31], P, fx, fy, fz, en);
                 }
             } else {  // list overflow: exact scan of this part's slots
                 const int si = self0 + hb + pb_i;
@@ -366,34 +478,23 @@ md_cell_kernel(const double4 *__restrict__ spos, const int *__restrict__ cell_st
             fz += __shfl_xor_sync(0xffffffffu, fz, o);
             en += __shfl_xor_sync(0xffffffffu, en, o);
         }
-        if (pb_i < nhc && pb_part == 0) out[ia] = make_double4(fx, fy, fz, en);
+        if (pb_i < nhc && pb_part == 0) {
+            out[ia] = make_double4(fx, fy, fz, en);
+            if (INTEG) md_integrate_one<DIM>(ia, make_double3(fx, fy, fz), P, I);
+        }
         __syncthreads();
     }
 }
 
-// cell of every atom: numpy floor_divide for the 2-D patches (md.py:187-189),
-// floor(x / cell) for the 3-D cells; clamped to the grid
+// cell of every atom (unfused path)
 __global__ void md_assign_kernel(int n, const double4 *__restrict__ pos, const MDParams P, int use_npy,
                                  int *__restrict__ cell_of, int *__restrict__ count)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double4 p = pos[i];
-    int c3[3];
-    const double xs[3] = {p.x, p.y, p.z};
-    const int dims[3] = {P.nx, P.ny, P.nz};
-    for (int k = 0; k < 3; ++k) {
-        if (k >= P.dim) {
-            c3[k] = 0;
-            continue;
-        }
-        const double f = use_npy ? np_floordiv(xs[k], P.cell) : floor(__ddiv_rn(xs[k], P.cell));
-        long long ck = (long long)f;
-        if (ck > dims[k] - 1) ck = dims[k] - 1;
-        if (ck < 0) ck = 0;
-        c3[k] = (int)ck;
-    }
-    const int c = (c3[0] * P.ny + c3[1]) * P.nz + c3[2];
+    const double x[3] = {p.x, p.y, p.z};
+    const int c = md_cell_index(x, P, use_npy);
     cell_of[i] = c;
     atomicAdd(&count[c], 1);
 }
@@ -404,12 +505,13 @@ __global__ void md_count_kernel(int n, const int *__restrict__ cell_of, int *__r
     if (i < n) atomicAdd(&count[cell_of[i]], 1);
 }
 
-__global__ void md_scatter_kernel(int n, const double4 *__restrict__ pos, const int *__restrict__ cell_of,
-                                  int *__restrict__ cursor, int *__restrict__ perm)
+__global__ void md_scatter_kernel(int n, const int *__restrict__ cell_start, const int *__restrict__ cell_of,
+                                  int *__restrict__ count, int *__restrict__ perm)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    perm[atomicAdd(&cursor[cell_of[i]], 1)] = i;
+    const int c = cell_of[i];
+    perm[cell_start[c] + atomicSub(&count[c], 1) - 1] = i;  // counts end at zero
 }
 
 // deterministic order inside each cell (ascending original id), then gather
@@ -485,8 +587,7 @@ __global__ void md_gather_kernel(int n, const int *__restrict__ perm, const doub
     scell[k] = cell_of[i];
 }
 
-// md_step integrator (md.py:171-189): v += F dt (unit mass); x += v dt; then
-// periodic wrap (np.remainder) or reflecting walls + clip to hi - 1e-12
+// md_step integrator (md.py:171-189), one atom per thread (unfused path)
 __global__ void md_integrate_kernel(int n, double4 *__restrict__ pos, double4 *__restrict__ vel,
                                     const double4 *__restrict__ force, const MDParams P, double dt)
 {
@@ -495,32 +596,7 @@ __global__ void md_integrate_kernel(int n, double4 *__restrict__ pos, double4 *_
     double x[3] = {pos[i].x, pos[i].y, pos[i].z};
     double v[3] = {vel[i].x, vel[i].y, vel[i].z};
     const double f[3] = {force[i].x, force[i].y, force[i].z};
-    const double hi[3] = {P.bx, P.by, P.bz};
-    for (int k = 0; k < P.dim; ++k) {
-        v[k] = __dadd_rn(v[k], __dmul_rn(f[k], dt));
-        x[k] = __dadd_rn(x[k], __dmul_rn(v[k], dt));
-    }
-    for (int k = 0; k < P.dim; ++k) {
-        if (P.periodic) {
-            // np.remainder (npy_divmod) fast path for one box of travel: fmod is
-            // exact there, and negative values take the rounded x + box
-            const double b = hi[k];
-            if (x[k] >= 0.0 && x[k] < b) x[k] = x[k] == 0.0 ? 0.0 : x[k];
-            else if (x[k] >= b && x[k] < 2.0 * b) x[k] = __dsub_rn(x[k], b);
-            else if (x[k] < 0.0 && x[k] > -b) x[k] = __dadd_rn(x[k], b);
-            else x[k] = np_remainder(x[k], b);
-        } else {
-            if (x[k] < 0.0) {
-                x[k] = -x[k];
-                v[k] = -v[k];
-            }
-            if (x[k] > hi[k]) {
-                x[k] = __dsub_rn(__dmul_rn(2.0, hi[k]), x[k]);
-                v[k] = -v[k];
-            }
-            x[k] = fmin(fmax(x[k], 0.0), __dsub_rn(hi[k], 1e-12));
-        }
-    }
+    md_advance(x, v, f, P, dt);
     pos[i] = make_double4(x[0], x[1], x[2], 0.0);
     vel[i] = make_double4(v[0], v[1], v[2], 0.0);
 }
@@ -537,7 +613,7 @@ struct gc_md {
     int use_npy = 0;  // reference 2-D patches use numpy floor_divide
     bool cell_path = true;  // block-per-cell kernel (false: thread-per-atom kernel)
     DBuf<double4> pos, vel, spos, force;
-    DBuf<int> cell_of, scell, count, cell_start, cursor, perm;
+    DBuf<int> cell_of, scell, count, cell_start, perm;
     cudaGraphExec_t graph = nullptr;
     int graph_steps = 0;
     double graph_dt = 0.0;
@@ -552,6 +628,24 @@ struct gc_md {
 
 namespace {
 
+// Cell sort from the per-cell counts: exclusive scan -> cell_start, scatter
+// (count is consumed back to zero, ready for the next step's counting),
+// per-cell rank sort by original id fused with the gather into spos.
+void md_sort_counted(gc_md *md)
+{
+    cudaStream_t s = md->ctx->stream;
+    const int n = md->n, nc = md->ncell;
+    size_t bytes = 0;
+    GC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, md->count.p, md->cell_start.p, nc + 1, s));
+    md->ctx->scratch.resize(bytes);
+    GC_CUDA(cub::DeviceScan::ExclusiveSum(md->ctx->scratch.p, bytes, md->count.p, md->cell_start.p, nc + 1, s));
+    md_scatter_kernel<<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->cell_start.p, md->cell_of.p, md->count.p,
+                                                             md->perm.p);
+    md_sortgather_kernel<<<grid_for(nc, MD_TPB / 32), MD_TPB, 0, s>>>(nc, md->cell_start.p, md->perm.p, md->pos.p,
+                                                                      md->cell_of.p, md->spos.p, md->scell.p);
+    check_launch("md sort");
+}
+
 void md_sort(gc_md *md, bool assign)
 {
     cudaStream_t s = md->ctx->stream;
@@ -562,15 +656,40 @@ void md_sort(gc_md *md, bool assign)
                                                                 md->count.p);
     else
         md_count_kernel<<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->cell_of.p, md->count.p);
-    size_t bytes = 0;
-    GC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, md->count.p, md->cell_start.p, nc + 1, s));
-    md->ctx->scratch.resize(bytes);
-    GC_CUDA(cub::DeviceScan::ExclusiveSum(md->ctx->scratch.p, bytes, md->count.p, md->cell_start.p, nc + 1, s));
-    GC_CUDA(cudaMemcpyAsync(md->cursor.p, md->cell_start.p, sizeof(int) * nc, cudaMemcpyDeviceToDevice, s));
-    md_scatter_kernel<<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->pos.p, md->cell_of.p, md->cursor.p, md->perm.p);
-    md_sortgather_kernel<<<grid_for(nc, MD_TPB / 32), MD_TPB, 0, s>>>(nc, md->cell_start.p, md->perm.p, md->pos.p,
-                                                                      md->cell_of.p, md->spos.p, md->scell.p);
-    check_launch("md sort");
+    md_sort_counted(md);
+}
+
+template <int LAW, int DIM>
+void md_cell_launch(gc_md *md, bool integ, double dt)
+{
+    // float32 filter: r^2 < band keeps a candidate, r^2 < inner decides it is
+    // inside the cutoff; the margin >> the float32 error of relative
+    // coordinates within two cells (see md_cell_kernel)
+    const double ext = 3.0 * md->P.cell;
+    const double margin = 1e-5 * ext * ext + 1e-6;
+    const float band = (float)(md->P.c2 + margin);
+    const float inner = (float)(md->P.c2 - margin);
+    MDInteg I{md->pos.p, md->vel.p, md->cell_of.p, md->count.p, dt, md->use_npy};
+    cudaStream_t s = md->ctx->stream;
+    if (integ)
+        md_cell_kernel<LAW, DIM, true><<<md->ncell, MDC_THREADS, 0, s>>>(md->spos.p, md->cell_start.p, md->P, band,
+                                                                          inner, md->force.p, I);
+    else
+        md_cell_kernel<LAW, DIM, false><<<md->ncell, MDC_THREADS, 0, s>>>(md->spos.p, md->cell_start.p, md->P, band,
+                                                                           inner, md->force.p, I);
+    check_launch("md_cell_kernel");
+}
+
+// forces of the current (sorted) state; with integ, the fused step epilogue
+void md_cell_forces(gc_md *md, bool integ, double dt)
+{
+    if (md->law == LAW_LJ) {
+        if (md->P.dim == 3) md_cell_launch<LAW_LJ, 3>(md, integ, dt);
+        else md_cell_launch<LAW_LJ, 2>(md, integ, dt);
+    } else {
+        if (md->P.dim == 3) md_cell_launch<LAW_SOFT, 3>(md, integ, dt);
+        else md_cell_launch<LAW_SOFT, 2>(md, integ, dt);
+    }
 }
 
 void md_forces(gc_md *md)
@@ -578,27 +697,7 @@ void md_forces(gc_md *md)
     cudaStream_t s = md->ctx->stream;
     const int n = md->n;
     if (md->cell_path) {
-        // float32 filter band: r^2 < c2 + margin, margin >> the float32 error of
-        // relative coordinates within two cells (see md_cell_kernel)
-        const double ext = 3.0 * md->P.cell;
-        const float band = (float)(md->P.c2 + 1e-5 * ext * ext + 1e-6);
-        const int nc = md->ncell;
-        if (md->law == LAW_LJ) {
-            if (md->P.dim == 3)
-                md_cell_kernel<LAW_LJ, 3><<<nc, MDC_THREADS, 0, s>>>(md->spos.p, md->cell_start.p, md->P, band,
-                                                                      md->force.p);
-            else
-                md_cell_kernel<LAW_LJ, 2><<<nc, MDC_THREADS, 0, s>>>(md->spos.p, md->cell_start.p, md->P, band,
-                                                                      md->force.p);
-        } else {
-            if (md->P.dim == 3)
-                md_cell_kernel<LAW_SOFT, 3><<<nc, MDC_THREADS, 0, s>>>(md->spos.p, md->cell_start.p, md->P, band,
-                                                                        md->force.p);
-            else
-                md_cell_kernel<LAW_SOFT, 2><<<nc, MDC_THREADS, 0, s>>>(md->spos.p, md->cell_start.p, md->P, band,
-                                                                        md->force.p);
-        }
-        check_launch("md_cell_kernel");
+        md_cell_forces(md, false, 0.0);
         return;
     }
     if (md->law == LAW_LJ) {
@@ -619,13 +718,21 @@ void md_forces(gc_md *md)
     check_launch("md_force_kernel");
 }
 
+// One md_step (md.py:166-190) on a sorted state whose counts are zero:
+// forces + integrator + new cell + counting in the cell kernel, then the
+// cell sort of the new positions (4 launches).
 void md_step_once(gc_md *md, double dt)
 {
-    md_sort(md, true);
+    if (md->cell_path) {
+        md_cell_forces(md, true, dt);
+        md_sort_counted(md);
+        return;
+    }
     md_forces(md);
     md_integrate_kernel<<<grid_for(md->n, MD_TPB), MD_TPB, 0, md->ctx->stream>>>(md->n, md->pos.p, md->vel.p,
                                                                                   md->force.p, md->P, dt);
     check_launch("md_integrate_kernel");
+    md_sort(md, true);
 }
 
 }  // namespace
@@ -698,7 +805,6 @@ gc_status gc_md_set_system(gc_md *md, int64_t n, int32_t dim, const double *pos,
         md->perm.resize(n);
         md->count.resize(md->ncell + 1);
         md->cell_start.resize(md->ncell + 1);
-        md->cursor.resize(md->ncell + 1);
         if (cell_of) {  // the caller's patch assignment (md.py PatchGrid.patch_of)
             std::vector<int> c(n);
             for (int64_t i = 0; i < n; ++i) {
@@ -765,10 +871,7 @@ gc_status gc_md_run(gc_md *md, int32_t steps, double dt)
         GC_CUDA(cudaEventRecord(md->e0, s));
         GC_CUDA(cudaGraphLaunch(md->graph, s));
         GC_CUDA(cudaEventRecord(md->e1, s));
-        GC_CUDA(cudaStreamSynchronize(s));
-        // leave the cell ordering consistent with the final positions
-        md_sort(md, true);
-        GC_CUDA(cudaStreamSynchronize(s));
+        GC_CUDA(cudaStreamSynchronize(s));  // every step ends with the cell sort of its new positions
     });
 }
 

@@ -92,7 +92,7 @@ class BucketTree:
             pass
 
     def sizes(self):
-        s = np.zeros(4, np.int64)
+        s = np.zeros(5, np.int64)
         L.call("gc_bh_sizes", self.handle, L.ptr(s, L.i64p))
         return s
 
