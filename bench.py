@@ -15,9 +15,14 @@ half of the metric), with its own HBM roofline and CPU baseline.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 runs under torchrun: every rank evaluates its own independent system
-(seed + rank), so per-GPU work is fixed ("scaling": "weak"); there is no
-data-path collective, only a barrier and a MAX reduction of the step times.
+N > 1 runs under torchrun, one rank per GPU, weak scaling (per-GPU work
+fixed): BH shards ONE clustered system of N x 1M particles -- every rank
+builds the same tree, the depth-first walk groups are cut into N contiguous
+ranges weighted by measured work (K-way partition_queue, sharding.py) and each
+rank walks / reorganises / evaluates only its range (no data-path
+collective); MD decomposes ONE periodic LJ system of N x 108K atoms into x
+slabs with a per-step NCCL halo exchange and atom migration (md_dist.py).
+Step times are MAX-reduced over ranks.
 ``--impl reference`` times the CPU restatement of the reference path
 (oracle/, float64, all host threads) on the same workload and metric.
 """
@@ -36,6 +41,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+DIST_BACKEND = os.environ.get("GCHARM_DIST_BACKEND", "nccl")  # gloo: N > 1 dry run on one GPU
 
 THETA, BUCKET, EPS, N_PART = 0.7, 8, 1e-4, 1_000_000
 FLOPS_PER_INTERACTION = 20  # SURVEY.md §8d convention (body-body interaction)
@@ -52,9 +58,10 @@ def measured_hbm():
         return 6650.0, "B200_PROFILING.md fallback 6.65 TB/s (of fallback)"
 
 
-def workload(rank: int):
+def workload(world: int = 1):
+    """configs[2]: clustered 1M (one shared system of world x 1M under torchrun)."""
     from paper_2008_05712_b200 import generators as gen
-    return gen.fp32_exact(gen.gen_particles(N_PART, 42 + rank, clustering=0.6, dim=3))
+    return gen.fp32_exact(gen.gen_particles(N_PART * world, 42, clustering=0.6, dim=3))
 
 
 def dist_setup():
@@ -64,8 +71,14 @@ def dist_setup():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if DIST_BACKEND == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # gloo: dry runs of the N > 1 path with several ranks sharing one GPU
+            local = local % torch.cuda.device_count()
+            os.environ["GCHARM_DEVICE"] = str(local)
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
     return world, rank, local
 
 
@@ -74,8 +87,18 @@ def allmax(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if DIST_BACKEND == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allsum(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda" if DIST_BACKEND == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
 
@@ -192,7 +215,7 @@ def run_reference(args, world, rank):
     if rank != 0:
         return
     from paper_2008_05712_b200.generators import gen_lj_fcc
-    ps = workload(0)
+    ps = workload(1)
     inter, ts, cores = cpu_bh(ps, steps=max(1, args.steps))
     mean = statistics.mean(ts)
     v = inter / mean
@@ -228,8 +251,10 @@ def bench_bh(args, world, rank, local, ctx, torch):
     from paper_2008_05712_b200 import _lib as L
     from paper_2008_05712_b200 import nbody
 
+    from paper_2008_05712_b200 import sharding
+
     ext = torch.cuda.ExternalStream(ctx.stream)
-    ps = workload(rank)
+    ps = workload(world)
     tree = nbody.build_bucket_tree(ps, BUCKET)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -237,10 +262,14 @@ def bench_bh(args, world, rank, local, ctx, torch):
         L.call("gc_bh_walk", tree.handle, THETA)
         L.call("gc_bh_forces_async", tree.handle, 1.0, EPS)
 
+    shard = None
+    if world > 1:  # this rank's work-weighted range of the shared tree's walk groups
+        L.call("gc_bh_walk", tree.handle, THETA)
+        shard = sharding.shard_tree(tree, rank, world)
     for _ in range(max(3, args.warmup)):
         step()
     ctx.sync()
-    inter = nbody.interactions(tree)
+    inter = nbody.interactions(tree)  # this rank's range
     sizes = tree.sizes()
     n_union, n_records = int(sizes[3]), int(sizes[4])
     step_ms, walk_ms, reorg_ms, force_ms = [], [], [], []
@@ -265,6 +294,7 @@ def bench_bh(args, world, rank, local, ctx, torch):
     torch.cuda.synchronize()
     barrier(world)
     ms = allmax(sum(step_ms), world) / args.steps
+    total_inter = allsum(inter, world)
     f_ms, w_ms, r_ms = statistics.mean(force_ms), statistics.mean(walk_ms), statistics.mean(reorg_ms)
     pk, tmp = np.zeros(1), np.zeros(1)
     L.call("gc_measure_fp32_peak", ctx.handle, L.ptr(pk, L.f64p), L.ptr(tmp, L.f64p))
@@ -272,6 +302,8 @@ def bench_bh(args, world, rank, local, ctx, torch):
     hbm, hbm_src = measured_hbm()
 
     # end to end through the C ABI: pinned host buffers, H2D + D2H inside
+    # (one 1M system per rank: gc_bh_step evaluates a whole system)
+    ps = ps if world == 1 else workload(1)
     pos_np = torch.from_numpy(np.ascontiguousarray(ps.positions)).pin_memory().numpy()
     m_np = torch.from_numpy(np.ascontiguousarray(ps.masses)).pin_memory().numpy()
     out_np = torch.empty((ps.positions.shape[0], 3), dtype=torch.float64).pin_memory().numpy()
@@ -286,11 +318,18 @@ def bench_bh(args, world, rank, local, ctx, torch):
         e2e_s.append(time.perf_counter() - t0)
     L.call("gc_bh_io_bytes", stepper.handle, L.ptr(io, L.i64p), 0)
     e2e_t = allmax(statistics.median(e2e_s), world)
+    if world == 1:
+        e2e_inter = inter
+    else:  # the replica system's own interaction count (stats walk on the stepper's handle)
+        cnt = np.zeros(1, np.int64)
+        L.call("gc_bh_interactions", stepper.handle, L.ptr(cnt, L.i64p))
+        e2e_inter = int(cnt[0])
     achieved = FLOPS_PER_INTERACTION * inter / (f_ms * 1e-3) / 1e12
     # reorganisation: union entries read (16 B) + staged records written (16 B record + 4 B mask)
     reorg_bytes = 16 * n_union + 20 * n_records
     return {
-        "ps": ps, "inter": inter, "ms": ms, "value": world * inter / (ms * 1e-3), "walk_ms": w_ms, "force_ms": f_ms,
+        "ps": ps, "inter": inter, "ms": ms, "value": total_inter / (ms * 1e-3), "walk_ms": w_ms, "force_ms": f_ms,
+        "shard": shard, "total_inter": total_inter,
         "reorg_ms": r_ms, "n_union": n_union, "n_records": n_records,
         "clocks": clk.summary(),
         "roofline": {"bound": "fp32", "kernel": "force_group_kernel", "achieved": achieved, "peak": fp32_peak,
@@ -303,18 +342,59 @@ def bench_bh(args, world, rank, local, ctx, torch):
                            "achieved": reorg_bytes / (r_ms * 1e-3) / 1e9, "peak": hbm, "peak_source": hbm_src,
                            "frac": reorg_bytes / (r_ms * 1e-3) / 1e9 / hbm, "traffic": ncu_traffic("expand_kernel"),
                            "algorithmic_bytes_per_launch": reorg_bytes, "kernel_ms": r_ms},
-        "e2e": {"value": world * inter / e2e_t, "unit": "interactions/s", "h2d_bytes_per_step": int(io[0]),
+        "e2e": {"value": world * e2e_inter / e2e_t, "unit": "interactions/s", "h2d_bytes_per_step": int(io[0]),
                 "d2h_bytes_per_step": int(io[1]), "ms_per_step": e2e_t * 1e3,
                 "path": "gc_bh_step C ABI: pinned host positions/masses -> H2D -> device tree build -> device walk "
                         "-> reorganisation -> forces -> D2H (median of the timed calls)"},
     }
 
 
+def bench_md_slabs(args, world, rank, local, torch):
+    """N > 1: one periodic LJ system of N x 108K atoms in x slabs (20 cells each),
+    per-step NCCL halo exchange + migration (md_dist.py)."""
+    from paper_2008_05712_b200 import md_dist
+    from paper_2008_05712_b200.generators import gen_lj_fcc
+
+    sysin = gen_lj_fcc(30, seed=7, repeat_x=world)
+    b = md_dist.slab_bounds(sysin.cells_xyz[0], world)
+    slab = md_dist.LJSlab(sysin, b[rank], b[rank + 1])
+    tr = md_dist.DistTransport()
+    steps = MD_STEPS // 4
+    for _ in range(3):
+        slab.step(tr)
+    barrier(world)
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with clk:
+        e0.record()
+        for _ in range(steps):
+            slab.step(tr)
+        e1.record()
+        e1.synchronize()
+    ms = allmax(e0.elapsed_time(e1), world) / steps
+    n_own = slab.owned()[2].shape[0]
+    return {
+        "metric": "MD ms/step (LJ FCC 108K atoms per GPU, rc 2.5, x-slab decomposition)", "value": ms,
+        "unit": "ms/step", "higher_is_better": False, "steps_timed": steps, "dtype": "f64",
+        "config": {"workload": f"configs[4]-style: LJ FCC ({30 * world}x30x30)x4 = {sysin.positions.shape[0]} atoms, "
+                               f"{sysin.cells_xyz[0]}x20x20 cells, {world} x slabs of 20 cells, periodic",
+                   "atoms_this_rank": int(n_own),
+                   "timed": "events around whole steps: halo pack -> NCCL exchange -> fused force/integrate kernel "
+                            "-> migrant pack -> NCCL exchange -> migrate (host-orchestrated)"},
+        "roofline": None,
+        "clocks": clk.summary(),
+        "_sysin": None,
+    }
+
+
 def bench_md(args, world, rank, local, torch):
+    if world > 1:
+        return bench_md_slabs(args, world, rank, local, torch)
     from paper_2008_05712_b200 import md
     from paper_2008_05712_b200.generators import gen_lj_fcc
 
-    sysin = gen_lj_fcc(30, seed=7 + rank)
+    sysin = gen_lj_fcc(30, seed=7)
     sysd = md.LJSystem(sysin)
     sysd.run(MD_STEPS)  # warm-up: graph capture + one full run
     _, _, cells = sysd.state()
@@ -340,10 +420,13 @@ def bench_md(args, world, rank, local, torch):
         "higher_is_better": False, "steps_per_run": MD_STEPS, "dtype": "f64",
         "config": {"workload": "configs[1] LJ FCC 30^3x4 = 108,000 atoms, rho 0.8442, T 1.44, rc 2.5, 20^3 "
                                "cells, dt 0.005, periodic", "tasks_per_step": sysd.task_count(),
-                   "timed": "CUDA-graph of 100 full steps (cell sort + forces + integrator), events"},
+                   "timed": "CUDA-graph of 100 full steps (fused force+integrator+cell count kernel, cell sort), "
+                            "events"},
         "roofline": {"bound": "hbm", "kernel": "md step (task model)", "achieved": achieved, "peak": hbm,
                      "peak_source": src, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
-                     "algorithmic_bytes_per_step": task_bytes},
+                     "algorithmic_bytes_per_step": task_bytes,
+                     "note": "the 3.5 MB system is L2-resident: ncu measures ~3.5 MB DRAM per step, the task-model "
+                             "bytes are served from L2 (profiles/r01_md_ncu_summary.txt)"},
         "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": 2 * n * 3 * 8 // MD_STEPS,
                 "d2h_bytes_per_step": 2 * n * 3 * 8 // MD_STEPS,
                 "path": "LJSystem(host arrays) -> H2D -> run(100) -> state() D2H, wall clock / 100"},
@@ -367,8 +450,8 @@ def run_ours(args, world, rank, local):
         "metric": BH_METRIC, "value": bh["value"], "unit": "interactions/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": bh["ms"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp32 force math (fp64 walk decisions, fp64 accumulation)",
-        "data": "synthetic gen_particles(1M, seed 42+rank, clustering 0.6, dim 3), fp32-exact",
-        "config": {"workload": "configs[2] clustered N-body 1M, theta 0.7, bucket 8, eps 1e-4 (1 system per GPU)",
+        "data": "synthetic gen_particles(1M, seed 42, clustering 0.6, dim 3), fp32-exact",
+        "config": {"workload": "configs[2] clustered N-body 1M per GPU, theta 0.7, bucket 8, eps 1e-4",
                    "step": "device walk (union lists) + reorganisation (staging runs) + force kernel; tree resident",
                    "interactions_per_gpu": bh["inter"], "walk_ms": bh["walk_ms"], "reorg_ms": bh["reorg_ms"],
                    "force_ms": bh["force_ms"], "union_entries": bh["n_union"], "staged_records": bh["n_records"],
@@ -382,6 +465,11 @@ def run_ours(args, world, rank, local):
     }
     sysin = mdr.pop("_sysin")
     line["md"] = mdr
+    if world > 1:
+        line["config"]["shard"] = {"walk_groups": bh["shard"], "interactions_this_rank": bh["inter"],
+                                   "interactions_all_ranks": bh["total_inter"],
+                                   "system": f"one shared clustered system of {world} x 1M particles"}
+        line["data"] = f"synthetic gen_particles({world}M, seed 42, clustering 0.6, dim 3), fp32-exact"
     if world == 1 and not args.no_cpu_baseline:
         c_inter, c_ts, cores = cpu_bh(bh["ps"], 1)
         line["cpu_baseline"] = {"value": c_inter / c_ts[0], "unit": "interactions/s", "cores": cores,

@@ -194,8 +194,26 @@ gc_status gc_md_forces(gc_md *md, double *forces, double *energy);
 /* `steps` iterations of md_step (md.py:166-190) on the device (CUDA graph) */
 gc_status gc_md_run(gc_md *md, int32_t steps, double dt);
 gc_status gc_md_get_state(gc_md *md, double *pos, double *vel, int64_t *cell_of);
-/* device time (ms, CUDA events) of the last gc_md_forces or gc_md_run */
+/* device time (ms, CUDA events) of the last gc_md_forces, gc_md_run or gc_md_slab_step */
 gc_status gc_md_elapsed(gc_md *md, double *ms);
+
+/* ---- x-slab spatial decomposition (multi-GPU MD) -------------
+ * The reference has no multi-process MD: the patch loop of compute_forces /
+ * md_step (hr/workloads/md.py:121-190) runs in one process.  A slab handle
+ * owns global x cells [gx0, gx0 + nx - 2) of a periodic gnx x ny x nz grid;
+ * gc_md_set_system is called with the local dims (owned + 2 ghost planes)
+ * and the owned atoms (global coordinates).  Per step: pack ghost planes
+ * (what 0 = left, 1 = right) -> exchange -> gc_md_set_ghosts ->
+ * gc_md_slab_step -> pack migrants (what 2 = left, 3 = right) -> exchange ->
+ * gc_md_migrate.  Pointers to packed records are DEVICE pointers (ghost
+ * record = double4 (x, y, z, global id bits); migrant = 2 x double4, + (v, 0)).
+ * Forces, positions and decisions are bit-identical to the whole-domain run. */
+gc_status gc_md_set_slab(gc_md *md, int64_t gx0, int64_t gnx, const int64_t *gid /* host, owned; may be NULL */);
+gc_status gc_md_pack(gc_md *md, int32_t what, void *out /* device, may be NULL */, int64_t cap, int64_t *count);
+gc_status gc_md_set_ghosts(gc_md *md, const void *left, int64_t n_left, const void *right, int64_t n_right);
+gc_status gc_md_slab_step(gc_md *md, double dt);
+gc_status gc_md_migrate(gc_md *md, const void *in_left, int64_t n_left, const void *in_right, int64_t n_right);
+gc_status gc_md_owned(gc_md *md, int64_t *n_owned, double *pos, double *vel, int64_t *gid /* host; may be NULL */);
 
 #ifdef __cplusplus
 }

@@ -77,6 +77,12 @@ SIGNATURES = {
     "gc_md_run": [vp, C.c_int32, C.c_double],
     "gc_md_get_state": [vp, f64p, f64p, i64p],
     "gc_md_elapsed": [vp, f64p],
+    "gc_md_set_slab": [vp, C.c_int64, C.c_int64, i64p],
+    "gc_md_pack": [vp, C.c_int32, vp, C.c_int64, i64p],
+    "gc_md_set_ghosts": [vp, vp, C.c_int64, vp, C.c_int64],
+    "gc_md_slab_step": [vp, C.c_double],
+    "gc_md_migrate": [vp, vp, C.c_int64, vp, C.c_int64],
+    "gc_md_owned": [vp, i64p, f64p, f64p, i64p],
 }
 _RESTYPE = {"gc_ctx_stream": vp, "gc_last_error": C.c_char_p, "gc_version": C.c_char_p}
 

@@ -1,6 +1,8 @@
 // common.cuh -- shared helpers for libgcharm (sm_100a).
 #pragma once
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <stdint.h>
 #include <stdio.h>
 #include <string>
@@ -72,6 +74,21 @@ struct DBuf {
             release();
             size_t c = count ? count : 1;
             GC_CUDA(cudaMalloc(&p, c * sizeof(T)));
+            cap = c;
+        }
+        n = count;
+    }
+    // grow-only, keeping the first n elements (device-side copy on the stream)
+    void grow(size_t count, cudaStream_t s)
+    {
+        if (count > cap) {
+            T *q = nullptr;
+            const size_t c = std::max(count, cap + cap / 2);
+            GC_CUDA(cudaMalloc(&q, c * sizeof(T)));
+            if (p && n) GC_CUDA(cudaMemcpyAsync(q, p, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+            GC_CUDA(cudaStreamSynchronize(s));
+            if (p) cudaFree(p);
+            p = q;
             cap = c;
         }
         n = count;

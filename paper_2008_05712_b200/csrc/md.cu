@@ -41,7 +41,20 @@ struct MDParams {
     double cutoff, c2;
     double stiffness;  // soft law
     double eps, sig2;  // LJ law
+    // x slab of a global periodic grid (multi-GPU spatial decomposition):
+    // local cell x = 1 is global cell gx0; local x = 0 and nx - 1 are ghost
+    // planes; x image shifts follow the GLOBAL grid (gnx cells, box gbx).  A
+    // whole domain is slab = 0, gx0 = 1, gnx = nx, gbx = bx.
+    int slab, gx0, gnx;
+    double gbx;
 };
+
+// x image shift of a neighbour cell at local x index qx (global wrap)
+__device__ __forceinline__ double md_xshift(int qx, const MDParams &P)
+{
+    const int gx = P.gx0 - 1 + qx;
+    return gx < 0 ? -P.gbx : (gx >= P.gnx ? P.gbx : 0.0);
+}
 
 __device__ __forceinline__ bool md_forward(int dx, int dy, int dz)
 {
@@ -80,7 +93,7 @@ __device__ __forceinline__ double np_remainder(double a, double b)
 // periodic wrap (np.remainder) or reflecting walls + clip to hi - 1e-12
 __device__ __forceinline__ void md_advance(double x[3], double v[3], const double f[3], const MDParams &P, double dt)
 {
-    const double hi[3] = {P.bx, P.by, P.bz};
+    const double hi[3] = {P.slab ? P.gbx : P.bx, P.by, P.bz};  // slabs wrap x in the global box
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         if (k >= P.dim) break;
@@ -117,7 +130,7 @@ __device__ __forceinline__ void md_advance(double x[3], double v[3], const doubl
 __device__ __forceinline__ int md_cell_index(const double x[3], const MDParams &P, int use_npy)
 {
     int c3[3];
-    const int dims[3] = {P.nx, P.ny, P.nz};
+    const int dims[3] = {P.slab ? P.gnx : P.nx, P.ny, P.nz};
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         if (k >= P.dim) {
@@ -130,18 +143,25 @@ __device__ __forceinline__ int md_cell_index(const double x[3], const MDParams &
         if (ck < 0) ck = 0;
         c3[k] = (int)ck;
     }
+    if (P.slab) {  // global x cell -> local slab index (ghost planes wrap around the periodic box)
+        int lx = c3[0] - (P.gx0 - 1);
+        if (lx < 0) lx += P.gnx;
+        if (lx >= P.nx) lx -= P.gnx;
+        c3[0] = min(max(lx, 0), P.nx - 1);
+    }
     return (c3[0] * P.ny + c3[1]) * P.nz + c3[2];
 }
 
 template <int LAW, int DIM>
 __global__ void __launch_bounds__(MD_TPB)
-md_force_kernel(int n, const double4 *__restrict__ spos, const int *__restrict__ cell_start,
-                const int *__restrict__ scell, const MDParams P, double4 *__restrict__ out)
+md_force_kernel(int n, const double4 *__restrict__ spos, const int *__restrict__ sidx,
+                const int *__restrict__ cell_start, const int *__restrict__ scell, const MDParams P,
+                double4 *__restrict__ out)
 {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const double4 a = spos[k];
-    const long long ia = __double_as_longlong(a.w);
+    const long long ia = __double_as_longlong(a.w);  // global id (self-cell orientation)
     const int c = scell[k];
     const int cz = c % P.nz, cy = (c / P.nz) % P.ny, cx = c / (P.nz * P.ny);
     double fx = 0.0, fy = 0.0, fz = 0.0, en = 0.0;
@@ -150,10 +170,9 @@ md_force_kernel(int n, const double4 *__restrict__ spos, const int *__restrict__
         for (int oy = -1; oy <= 1; ++oy)
             for (int oz = -RZ; oz <= RZ; ++oz) {
                 int qx = cx + ox, qy = cy + oy, qz = cz + oz;
-                double sx = 0.0, sy = 0.0, sz = 0.0;  // image shift of the neighbour cell
+                double sx = md_xshift(qx, P), sy = 0.0, sz = 0.0;  // image shift of the neighbour cell
                 if (qx < 0 || qx >= P.nx) {
-                    if (!P.periodic) continue;
-                    sx = qx < 0 ? -P.bx : P.bx;
+                    if (!P.periodic || P.slab) continue;
                     qx = qx < 0 ? qx + P.nx : qx - P.nx;
                 }
                 if (qy < 0 || qy >= P.ny) {
@@ -213,7 +232,7 @@ md_force_kernel(int n, const double4 *__restrict__ spos, const int *__restrict__
                     }
                 }
             }
-    out[ia] = make_double4(fx, fy, fz, en);
+    out[sidx[k]] = make_double4(fx, fy, fz, en);
 }
 
 // ---------------------------------------------------------------------------
@@ -344,8 +363,8 @@ __device__ __forceinline__ void md_integrate_one(long long ia, double3 f3, const
 
 template <int LAW, int DIM, bool INTEG>
 __global__ void __launch_bounds__(MDC_THREADS)
-md_cell_kernel(const double4 *__restrict__ spos, const int *__restrict__ cell_start, const MDParams P, float band,
-               float inner, double4 *__restrict__ out, const MDInteg I)
+md_cell_kernel(const double4 *__restrict__ spos, const int *__restrict__ sidx, const int *__restrict__ cell_start,
+               const MDParams P, float band, float inner, double4 *__restrict__ out, const MDInteg I)
 {
     __shared__ float4 nb[MDC_NB];  // rel xyz (float32 filter), packed (sorted index << 5 | offset code)
     __shared__ int qstart[27];
@@ -354,7 +373,7 @@ md_cell_kernel(const double4 *__restrict__ spos, const int *__restrict__ cell_st
     __shared__ int pre[28];
     __shared__ int qs[27];
     __shared__ double4 shtab[27];
-    const int c = blockIdx.x;
+    const int c = blockIdx.x + (P.slab ? P.ny * P.nz : 0);  // slabs: owned cells only (skip ghost plane 0)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cz = c % P.nz, cy = (c / P.nz) % P.ny, cx = c / (P.nz * P.ny);
     const double orx = cx * P.cell, ory = cy * P.cell, orz = cz * P.cell;
@@ -365,14 +384,14 @@ md_cell_kernel(const double4 *__restrict__ spos, const int *__restrict__ cell_st
         md_offset_of(tid, ox, oy, oz);
         int qx = cx + ox, qy = cy + oy, qz = cz + oz;
         bool ok = DIM == 3 || oz == 0;
-        if (qx < 0 || qx >= P.nx) { ok = ok && P.periodic; qx = (qx + P.nx) % P.nx; }
+        if (qx < 0 || qx >= P.nx) { ok = ok && P.periodic && !P.slab; qx = (qx + P.nx) % P.nx; }
         if (qy < 0 || qy >= P.ny) { ok = ok && P.periodic; qy = (qy + P.ny) % P.ny; }
         if (qz < 0 || qz >= P.nz) { ok = ok && P.periodic; qz = (qz + P.nz) % P.nz; }
         const int q = (qx * P.ny + qy) * P.nz + qz;
         qs[tid] = ok ? q : -1;
         qstart[tid] = ok ? cell_start[q] : 0;
         const int rx = cx + ox, ry = cy + oy, rz = cz + oz;
-        shtab[tid] = make_double4(rx < 0 ? -P.bx : (rx >= P.nx ? P.bx : 0.0), ry < 0 ? -P.by : (ry >= P.ny ? P.by : 0.0),
+        shtab[tid] = make_double4(md_xshift(rx, P), ry < 0 ? -P.by : (ry >= P.ny ? P.by : 0.0),
                                   rz < 0 ? -P.bz : (rz >= P.nz ? P.bz : 0.0),
                                   tid == 13 ? 2.0 : (md_forward(ox, oy, oz) ? 1.0 : 0.0));
         pre[tid + 1] = ok ? cell_start[q + 1] - cell_start[q] : 0;
@@ -396,14 +415,15 @@ md_cell_kernel(const double4 *__restrict__ spos, const int *__restrict__ cell_st
         for (int i = tid; i < nh; i += MDC_THREADS) {
             const double4 a = spos[h0 + i];
             const long long ia = __double_as_longlong(a.w);
+            const int li = sidx[h0 + i];
             double fx = 0.0, fy = 0.0, fz = 0.0, en = 0.0;
             for (int k = 0; k < NOFF; ++k) {
                 if (qs[k] < 0) continue;
                 for (int j = cell_start[qs[k]]; j < cell_start[qs[k] + 1]; ++j)
                     if (j != h0 + i) md_pair_exact<LAW, DIM>(a, ia, spos[j], shtab[k], P, fx, fy, fz, en);
             }
-            out[ia] = make_double4(fx, fy, fz, en);
-            if (INTEG) md_integrate_one<DIM>(ia, make_double3(fx, fy, fz), P, I);
+            out[li] = make_double4(fx, fy, fz, en);
+            if (INTEG) md_integrate_one<DIM>(li, make_double3(fx, fy, fz), P, I);
         }
         return;
     }
@@ -451,9 +471,12 @@ md_cell_kernel(const double4 *__restrict__ spos, const int *__restrict__ cell_st
         // phase B: exact float64 on survivors
         double fx = 0.0, fy = 0.0, fz = 0.0, en = 0.0;
         long long ia = -1;
+        int li = -1;
         if (pb_i < nhc) {
-            const double4 a = spos[__float_as_int(nb[self0 + hb + pb_i].w) >> 5];
+            const int hj = __float_as_int(nb[self0 + hb + pb_i].w) >> 5;
+            const double4 a = spos[hj];
             ia = __double_as_longlong(a.w);
+            li = sidx[hj];
             if (!lover[pb_i]) {
                 const unsigned short *lst = lists[pb_i][pb_part];
                 for (int e = 0; e < MDC_LIST; ++e) {
@@ -479,8 +502,8 @@ md_cell_kernel(const double4 *__restrict__ spos, const int *__restrict__ cell_st
             en += __shfl_xor_sync(0xffffffffu, en, o);
         }
         if (pb_i < nhc && pb_part == 0) {
-            out[ia] = make_double4(fx, fy, fz, en);
-            if (INTEG) md_integrate_one<DIM>(ia, make_double3(fx, fy, fz), P, I);
+            out[li] = make_double4(fx, fy, fz, en);
+            if (INTEG) md_integrate_one<DIM>(li, make_double3(fx, fy, fz), P, I);
         }
         __syncthreads();
     }
@@ -514,39 +537,24 @@ __global__ void md_scatter_kernel(int n, const int *__restrict__ cell_start, con
     perm[cell_start[c] + atomicSub(&count[c], 1) - 1] = i;  // counts end at zero
 }
 
-// deterministic order inside each cell (ascending original id), then gather
-__global__ void md_cellsort_kernel(int ncell, const int *__restrict__ cell_start, int *__restrict__ perm)
-{
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= ncell) return;
-    const int s = cell_start[c], e = cell_start[c + 1];
-    for (int i = s + 1; i < e; ++i) {
-        const int v = perm[i];
-        int j = i - 1;
-        while (j >= s && perm[j] > v) {
-            perm[j + 1] = perm[j];
-            --j;
-        }
-        perm[j + 1] = v;
-    }
-}
-
-// warp per cell: rank sort of the cell's atoms by original id (deterministic
-// order for any atomic scatter order) fused with the gather
+// warp per cell: rank sort of the cell's atoms by global id (deterministic
+// order for any atomic scatter order, the same order on every slab) fused
+// with the gather: spos = (x, y, z, global id bits), sidx = local index
 __global__ void md_sortgather_kernel(int ncell, const int *__restrict__ cell_start, int *__restrict__ perm,
-                                     const double4 *__restrict__ pos, const int *__restrict__ cell_of,
-                                     double4 *__restrict__ spos, int *__restrict__ scell)
+                                     const double4 *__restrict__ pos, const long long *__restrict__ gid,
+                                     double4 *__restrict__ spos, int *__restrict__ sidx, int *__restrict__ scell)
 {
     const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (c >= ncell) return;
     const int s = cell_start[c], n = cell_start[c + 1] - s;
-    if (n > 32) {  // rare: serial insertion sort, then gather
+    if (n > 32) {  // rare: serial insertion sort by global id, then gather
         if (lane == 0)
             for (int i = s + 1; i < s + n; ++i) {
                 const int v = perm[i];
+                const long long gv = gid[v];
                 int j = i - 1;
-                while (j >= s && perm[j] > v) {
+                while (j >= s && gid[perm[j]] > gv) {
                     perm[j + 1] = perm[j];
                     --j;
                 }
@@ -556,35 +564,26 @@ __global__ void md_sortgather_kernel(int ncell, const int *__restrict__ cell_sta
         for (int k = lane; k < n; k += 32) {
             const int i = perm[s + k];
             double4 p = pos[i];
-            p.w = __longlong_as_double((long long)i);
+            p.w = __longlong_as_double(gid[i]);
             spos[s + k] = p;
+            sidx[s + k] = i;
             scell[s + k] = c;
         }
         return;
     }
-    const int v = lane < n ? perm[s + lane] : INT_MAX;
+    const int v = lane < n ? perm[s + lane] : -1;
+    const long long g = lane < n ? gid[v] : LLONG_MAX;
     int rank = 0;
-    for (int k = 0; k < n; ++k) rank += __shfl_sync(0xffffffffu, v, k) < v;
+    for (int k = 0; k < n; ++k) rank += __shfl_sync(0xffffffffu, g, k) < g;
     __syncwarp();
     if (lane < n) {
         perm[s + rank] = v;
         double4 p = pos[v];
-        p.w = __longlong_as_double((long long)v);
+        p.w = __longlong_as_double(g);
         spos[s + rank] = p;
+        sidx[s + rank] = v;
         scell[s + rank] = c;
     }
-}
-
-__global__ void md_gather_kernel(int n, const int *__restrict__ perm, const double4 *__restrict__ pos,
-                                 const int *__restrict__ cell_of, double4 *__restrict__ spos, int *__restrict__ scell)
-{
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    const int i = perm[k];
-    double4 p = pos[i];
-    p.w = __longlong_as_double((long long)i);
-    spos[k] = p;
-    scell[k] = cell_of[i];
 }
 
 // md_step integrator (md.py:171-189), one atom per thread (unfused path)
@@ -601,6 +600,73 @@ __global__ void md_integrate_kernel(int n, double4 *__restrict__ pos, double4 *_
     vel[i] = make_double4(v[0], v[1], v[2], 0.0);
 }
 
+// ghost atoms [base, base + n) of x plane `plane`: y / z cells from the
+// position, x plane from the side they arrived on (a one-slab ring would
+// otherwise map its own boundary atoms back onto owned planes)
+__global__ void md_ghost_assign_kernel(int n, int base, int plane, const double4 *__restrict__ pos, const MDParams P,
+                                       int *__restrict__ cell_of, int *__restrict__ count)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double4 p = pos[base + k];
+    const double x[3] = {p.x, p.y, p.z};
+    const int c = md_cell_index(x, P, 0);
+    const int cyz = c % (P.ny * P.nz);
+    const int cg = plane * (P.ny * P.nz) + cyz;
+    cell_of[base + k] = cg;
+    atomicAdd(&count[cg], 1);
+}
+
+// --- slab decomposition helpers (multi-GPU MD, md_dist.py) -------------------
+// owned atoms of local x plane `plane` -> packed records: ghosts (x, y, z, gid
+// bits); migrants (x, y, z, gid bits) + (vx, vy, vz, 0).  Order is irrelevant:
+// every cell is re-sorted by global id.
+__global__ void md_pack_kernel(int n_owned, const int *__restrict__ cell_of, int plane_cells, int plane,
+                               const double4 *__restrict__ pos, const double4 *__restrict__ vel,
+                               const long long *__restrict__ gid, int with_vel, double4 *__restrict__ out,
+                               long long cap, int *__restrict__ cnt)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_owned || cell_of[i] / plane_cells != plane) return;
+    const int k = atomicAdd(cnt, 1);
+    if (k >= cap) return;
+    const double4 p = pos[i];
+    if (with_vel) {
+        out[2 * k] = make_double4(p.x, p.y, p.z, __longlong_as_double(gid[i]));
+        out[2 * k + 1] = vel[i];
+    } else {
+        out[k] = make_double4(p.x, p.y, p.z, __longlong_as_double(gid[i]));
+    }
+}
+
+// records -> atoms [base, base + n): positions and ids (+ velocities)
+__global__ void md_unpack_kernel(int n, const double4 *__restrict__ rec, int with_vel, int base,
+                                 double4 *__restrict__ pos, double4 *__restrict__ vel, long long *__restrict__ gid)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double4 r = with_vel ? rec[2 * k] : rec[k];
+    pos[base + k] = make_double4(r.x, r.y, r.z, 0.0);
+    gid[base + k] = __double_as_longlong(r.w);
+    if (with_vel) vel[base + k] = rec[2 * k + 1];
+}
+
+// keep owned atoms still inside the slab (local x planes 1 .. nx - 2)
+__global__ void md_keep_kernel(int n_owned, const int *__restrict__ cell_of, int plane_cells, int nx,
+                               const double4 *__restrict__ pos, const double4 *__restrict__ vel,
+                               const long long *__restrict__ gid, double4 *__restrict__ tpos,
+                               double4 *__restrict__ tvel, long long *__restrict__ tgid, int *__restrict__ cnt)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_owned) return;
+    const int lx = cell_of[i] / plane_cells;
+    if (lx < 1 || lx > nx - 2) return;
+    const int k = atomicAdd(cnt, 1);
+    tpos[k] = pos[i];
+    tvel[k] = vel[i];
+    tgid[k] = gid[i];
+}
+
 }  // namespace gc
 
 using namespace gc;
@@ -612,8 +678,14 @@ struct gc_md {
     int n = 0, ncell = 0;
     int use_npy = 0;  // reference 2-D patches use numpy floor_divide
     bool cell_path = true;  // block-per-cell kernel (false: thread-per-atom kernel)
-    DBuf<double4> pos, vel, spos, force;
-    DBuf<int> cell_of, scell, count, cell_start, perm;
+    DBuf<double4> pos, vel, spos, force;  // pos/vel/gid/cell_of: owned atoms [0, n_owned), then ghosts
+    DBuf<int> cell_of, scell, sidx, count, cell_start, perm;
+    DBuf<long long> gid;  // global atom id (cell order, self-pair orientation)
+    int n_owned = 0;
+    // slab scratch (pack / migrate)
+    DBuf<int> flag, sel, nsel;
+    DBuf<double4> tmp4;
+    DBuf<long long> tmp8;
     cudaGraphExec_t graph = nullptr;
     int graph_steps = 0;
     double graph_dt = 0.0;
@@ -642,7 +714,7 @@ void md_sort_counted(gc_md *md)
     md_scatter_kernel<<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->cell_start.p, md->cell_of.p, md->count.p,
                                                              md->perm.p);
     md_sortgather_kernel<<<grid_for(nc, MD_TPB / 32), MD_TPB, 0, s>>>(nc, md->cell_start.p, md->perm.p, md->pos.p,
-                                                                      md->cell_of.p, md->spos.p, md->scell.p);
+                                                                      md->gid.p, md->spos.p, md->sidx.p, md->scell.p);
     check_launch("md sort");
 }
 
@@ -671,12 +743,14 @@ void md_cell_launch(gc_md *md, bool integ, double dt)
     const float inner = (float)(md->P.c2 - margin);
     MDInteg I{md->pos.p, md->vel.p, md->cell_of.p, md->count.p, dt, md->use_npy};
     cudaStream_t s = md->ctx->stream;
+    const int blocks = md->P.slab ? (md->P.nx - 2) * md->P.ny * md->P.nz : md->ncell;  // home = owned cells
+    if (blocks <= 0) return;
     if (integ)
-        md_cell_kernel<LAW, DIM, true><<<md->ncell, MDC_THREADS, 0, s>>>(md->spos.p, md->cell_start.p, md->P, band,
-                                                                          inner, md->force.p, I);
+        md_cell_kernel<LAW, DIM, true><<<blocks, MDC_THREADS, 0, s>>>(md->spos.p, md->sidx.p, md->cell_start.p, md->P,
+                                                                       band, inner, md->force.p, I);
     else
-        md_cell_kernel<LAW, DIM, false><<<md->ncell, MDC_THREADS, 0, s>>>(md->spos.p, md->cell_start.p, md->P, band,
-                                                                           inner, md->force.p, I);
+        md_cell_kernel<LAW, DIM, false><<<blocks, MDC_THREADS, 0, s>>>(md->spos.p, md->sidx.p, md->cell_start.p, md->P,
+                                                                        band, inner, md->force.p, I);
     check_launch("md_cell_kernel");
 }
 
@@ -702,18 +776,22 @@ void md_forces(gc_md *md)
     }
     if (md->law == LAW_LJ) {
         if (md->P.dim == 3)
-            md_force_kernel<LAW_LJ, 3><<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->spos.p, md->cell_start.p,
-                                                                              md->scell.p, md->P, md->force.p);
+            md_force_kernel<LAW_LJ, 3><<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->spos.p, md->sidx.p,
+                                                                              md->cell_start.p, md->scell.p, md->P,
+                                                                              md->force.p);
         else
-            md_force_kernel<LAW_LJ, 2><<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->spos.p, md->cell_start.p,
-                                                                              md->scell.p, md->P, md->force.p);
+            md_force_kernel<LAW_LJ, 2><<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->spos.p, md->sidx.p,
+                                                                              md->cell_start.p, md->scell.p, md->P,
+                                                                              md->force.p);
     } else {
         if (md->P.dim == 3)
-            md_force_kernel<LAW_SOFT, 3><<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->spos.p, md->cell_start.p,
-                                                                                md->scell.p, md->P, md->force.p);
+            md_force_kernel<LAW_SOFT, 3><<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->spos.p, md->sidx.p,
+                                                                                md->cell_start.p, md->scell.p, md->P,
+                                                                                md->force.p);
         else
-            md_force_kernel<LAW_SOFT, 2><<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->spos.p, md->cell_start.p,
-                                                                                md->scell.p, md->P, md->force.p);
+            md_force_kernel<LAW_SOFT, 2><<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->spos.p, md->sidx.p,
+                                                                                md->cell_start.p, md->scell.p, md->P,
+                                                                                md->force.p);
     }
     check_launch("md_force_kernel");
 }
@@ -785,9 +863,14 @@ gc_status gc_md_set_system(gc_md *md, int64_t n, int32_t dim, const double *pos,
         P.stiffness = params[1];
         P.eps = params[1];
         P.sig2 = params[2] * params[2];
+        P.slab = 0;
+        P.gx0 = 1;
+        P.gnx = P.nx;
+        P.gbx = P.bx;
         md->law = law;
         md->use_npy = law == LAW_SOFT;
         md->n = (int)n;
+        md->n_owned = (int)n;
         md->ncell = P.nx * P.ny * P.nz;
         std::vector<double4> hp(n), hv(n);
         for (int64_t i = 0; i < n; ++i) {
@@ -802,7 +885,13 @@ gc_status gc_md_set_system(gc_md *md, int64_t n, int32_t dim, const double *pos,
         md->force.resize(n);
         md->cell_of.resize(n);
         md->scell.resize(n);
+        md->sidx.resize(n);
         md->perm.resize(n);
+        {
+            std::vector<long long> g(n);
+            for (int64_t i = 0; i < n; ++i) g[i] = i;
+            md->gid.upload(g.data(), n, s);
+        }
         md->count.resize(md->ncell + 1);
         md->cell_start.resize(md->ncell + 1);
         if (cell_of) {  // the caller's patch assignment (md.py PatchGrid.patch_of)
@@ -907,7 +996,179 @@ gc_status gc_md_elapsed(gc_md *md, double *ms)
     });
 }
 
+// ---- slab decomposition (multi-GPU MD; orchestration in md_dist.py) ---------
+static void md_grow(gc_md *md, int n)
+{
+    cudaStream_t s = md->ctx->stream;
+    md->pos.grow(n, s);
+    md->vel.grow(n, s);
+    md->gid.grow(n, s);
+    md->cell_of.grow(n, s);
+    md->spos.resize(n);
+    md->force.resize(n);
+    md->scell.resize(n);
+    md->sidx.resize(n);
+    md->perm.resize(n);
+}
+
+gc_status gc_md_set_slab(gc_md *md, int64_t gx0, int64_t gnx, const int64_t *gid)
+{
+    return guard([&] {
+        GC_REQUIRE(md && md->n > 0 || (md && md->ncell > 0), GC_E_STATE, "no system set");
+        MDParams &P = md->P;
+        GC_REQUIRE(P.dim == 3 && P.periodic, GC_E_VALUE, "slabs decompose a periodic 3-D grid");
+        GC_REQUIRE(P.nx >= 3 && gnx >= P.nx - 2 && gx0 >= 0 && gx0 + P.nx - 2 <= gnx, GC_E_VALUE,
+                   "slab must be local x cells = owned + 2 ghost planes inside the global grid");
+        P.slab = 1;
+        P.gx0 = (int)gx0;
+        P.gnx = (int)gnx;
+        P.gbx = (double)gnx * P.cell;
+        cudaStream_t s = md->ctx->stream;
+        if (gid) {
+            std::vector<long long> g(md->n_owned);
+            for (int i = 0; i < md->n_owned; ++i) g[i] = gid[i];
+            md->gid.upload(g.data(), md->n_owned, s);
+        }
+        md->n = md->n_owned;
+        if (md->graph) {
+            cudaGraphExecDestroy(md->graph);
+            md->graph = nullptr;
+        }
+        md_sort(md, true);
+        GC_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+gc_status gc_md_pack(gc_md *md, int32_t what, void *out, int64_t cap, int64_t *count)
+{
+    return guard([&] {
+        GC_REQUIRE(md && md->P.slab && count, GC_E_STATE, "not a slab");
+        GC_REQUIRE(what >= 0 && what <= 3, GC_E_VALUE, "what: 0/1 ghost planes, 2/3 migrants");
+        cudaStream_t s = md->ctx->stream;
+        const int nx = md->P.nx, pc = md->P.ny * md->P.nz;
+        const int plane = what == 0 ? 1 : what == 1 ? nx - 2 : what == 2 ? 0 : nx - 1;
+        md->nsel.resize(1);
+        md->nsel.zero(s);
+        if (md->n_owned > 0)
+            md_pack_kernel<<<grid_for(md->n_owned, MD_TPB), MD_TPB, 0, s>>>(
+                md->n_owned, md->cell_of.p, pc, plane, md->pos.p, md->vel.p, md->gid.p, what >= 2,
+                (double4 *)out, out ? cap : 0, md->nsel.p);
+        check_launch("md_pack_kernel");
+        int c = 0;
+        md->nsel.download(&c, 1, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        *count = c;
+        GC_REQUIRE(!out || c <= cap, GC_E_CAPACITY, "pack buffer too small (count returned)");
+    });
+}
+
+gc_status gc_md_set_ghosts(gc_md *md, const void *left, int64_t nl, const void *right, int64_t nr)
+{
+    return guard([&] {
+        GC_REQUIRE(md && md->P.slab, GC_E_STATE, "not a slab");
+        cudaStream_t s = md->ctx->stream;
+        const int n = md->n_owned + (int)(nl + nr);
+        md_grow(md, n);
+        if (nl > 0)
+            md_unpack_kernel<<<grid_for(nl, MD_TPB), MD_TPB, 0, s>>>((int)nl, (const double4 *)left, 0, md->n_owned,
+                                                                     md->pos.p, md->vel.p, md->gid.p);
+        if (nr > 0)
+            md_unpack_kernel<<<grid_for(nr, MD_TPB), MD_TPB, 0, s>>>((int)nr, (const double4 *)right, 0,
+                                                                     md->n_owned + (int)nl, md->pos.p, md->vel.p,
+                                                                     md->gid.p);
+        check_launch("md_unpack_kernel");
+        md->n = n;
+        const int nc = md->ncell, no = md->n_owned;
+        GC_CUDA(cudaMemsetAsync(md->count.p, 0, sizeof(int) * (nc + 1), s));
+        if (no > 0)
+            md_assign_kernel<<<grid_for(no, MD_TPB), MD_TPB, 0, s>>>(no, md->pos.p, md->P, md->use_npy, md->cell_of.p,
+                                                                     md->count.p);
+        if (nl > 0)
+            md_ghost_assign_kernel<<<grid_for(nl, MD_TPB), MD_TPB, 0, s>>>((int)nl, no, 0, md->pos.p, md->P,
+                                                                           md->cell_of.p, md->count.p);
+        if (nr > 0)
+            md_ghost_assign_kernel<<<grid_for(nr, MD_TPB), MD_TPB, 0, s>>>((int)nr, no + (int)nl, md->P.nx - 1,
+                                                                           md->pos.p, md->P, md->cell_of.p,
+                                                                           md->count.p);
+        check_launch("md ghost cells");
+        md_sort_counted(md);
+    });
+}
+
+gc_status gc_md_migrate(gc_md *md, const void *in_left, int64_t nl, const void *in_right, int64_t nr)
+{
+    return guard([&] {
+        GC_REQUIRE(md && md->P.slab, GC_E_STATE, "not a slab");
+        cudaStream_t s = md->ctx->stream;
+        const int nown = md->n_owned;
+        md->tmp4.resize(2 * (size_t)std::max(nown, 1));
+        md->tmp8.resize(std::max(nown, 1));
+        md->nsel.resize(1);
+        md->nsel.zero(s);
+        if (nown > 0)
+            md_keep_kernel<<<grid_for(nown, MD_TPB), MD_TPB, 0, s>>>(
+                nown, md->cell_of.p, md->P.ny * md->P.nz, md->P.nx, md->pos.p, md->vel.p, md->gid.p, md->tmp4.p,
+                md->tmp4.p + nown, md->tmp8.p, md->nsel.p);
+        check_launch("md_keep_kernel");
+        int kept = 0;
+        md->nsel.download(&kept, 1, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        const int n = kept + (int)(nl + nr);
+        md_grow(md, std::max(n, nown));
+        GC_CUDA(cudaMemcpyAsync(md->pos.p, md->tmp4.p, sizeof(double4) * kept, cudaMemcpyDeviceToDevice, s));
+        GC_CUDA(cudaMemcpyAsync(md->vel.p, md->tmp4.p + nown, sizeof(double4) * kept, cudaMemcpyDeviceToDevice, s));
+        GC_CUDA(cudaMemcpyAsync(md->gid.p, md->tmp8.p, sizeof(long long) * kept, cudaMemcpyDeviceToDevice, s));
+        if (nl > 0)
+            md_unpack_kernel<<<grid_for(nl, MD_TPB), MD_TPB, 0, s>>>((int)nl, (const double4 *)in_left, 1, kept,
+                                                                     md->pos.p, md->vel.p, md->gid.p);
+        if (nr > 0)
+            md_unpack_kernel<<<grid_for(nr, MD_TPB), MD_TPB, 0, s>>>((int)nr, (const double4 *)in_right, 1,
+                                                                     kept + (int)nl, md->pos.p, md->vel.p, md->gid.p);
+        check_launch("md_unpack_kernel");
+        md->n_owned = md->n = n;
+        md_grow(md, n);
+        md_sort(md, true);  // cells of the owned atoms (ghosts are refreshed before the next step)
+        GC_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+gc_status gc_md_slab_step(gc_md *md, double dt)
+{
+    return guard([&] {
+        GC_REQUIRE(md && md->P.slab, GC_E_STATE, "not a slab");
+        GC_CUDA(cudaEventRecord(md->e0, md->ctx->stream));
+        md_cell_forces(md, true, dt);  // forces on owned cells, integrator, new cells of owned atoms
+        GC_CUDA(cudaEventRecord(md->e1, md->ctx->stream));
+    });
+}
+
+gc_status gc_md_owned(gc_md *md, int64_t *n_owned, double *pos, double *vel, int64_t *gid)
+{
+    return guard([&] {
+        GC_REQUIRE(md && n_owned, GC_E_VALUE, "null argument");
+        const int n = md->n_owned;
+        *n_owned = n;
+        if (!pos && !vel && !gid) return;
+        cudaStream_t s = md->ctx->stream;
+        std::vector<double4> p(n), v(n);
+        std::vector<long long> g(n);
+        md->pos.download(p.data(), n, s);
+        md->vel.download(v.data(), n, s);
+        md->gid.download(g.data(), n, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        for (int i = 0; i < n; ++i) {
+            const double pp[3] = {p[i].x, p[i].y, p[i].z}, vv[3] = {v[i].x, v[i].y, v[i].z};
+            for (int k = 0; k < 3; ++k) {
+                if (pos) pos[3 * i + k] = pp[k];
+                if (vel) vel[3 * i + k] = vv[k];
+            }
+            if (gid) gid[i] = g[i];
+        }
+    });
+}
+
 }  // extern "C"
+
 
 namespace gc {
 void md_kernel_spec(const char *cls, int64_t out[5])

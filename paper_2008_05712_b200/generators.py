@@ -99,28 +99,42 @@ def gen_md_system(grid_dim, particles_per_patch, cutoff, seed, patch_size=None):
 class LJSystem:
     positions: np.ndarray  # (n, 3) float64 (float32-exact)
     velocities: np.ndarray  # (n, 3)
-    box: float
-    cells: int  # cells per dimension
+    box: float  # y / z box (and x for repeat_x = 1)
+    cells: int  # cells per y / z dimension
     cell_size: float
     rc: float = 2.5
     eps: float = 1.0
     sigma: float = 1.0
     dt: float = 0.005
+    repeat_x: int = 1  # the lattice is repeated along x (slab decompositions)
+
+    @property
+    def cells_xyz(self):
+        return (self.cells * self.repeat_x, self.cells, self.cells)
+
+    @property
+    def box_xyz(self):
+        # the device's box: cells x cell size per dimension
+        return tuple(c * self.cell_size for c in self.cells_xyz)
 
 
 def gen_lj_fcc(lattice_cells: int = 30, rho: float = 0.8442, temperature: float = 1.44, seed: int = 7,
-               rc: float = 2.5, dt: float = 0.005) -> LJSystem:
-    """FCC lattice, 4 atoms per unit cell, lattice_cells^3 unit cells."""
+               rc: float = 2.5, dt: float = 0.005, repeat_x: int = 1) -> LJSystem:
+    """FCC lattice, 4 atoms per unit cell, lattice_cells^3 unit cells (x
+    lattice_cells * repeat_x along x)."""
     a = (4.0 / rho) ** (1.0 / 3.0)
     box = lattice_cells * a
     basis = np.array([[0.0, 0.0, 0.0], [0.5, 0.5, 0.0], [0.5, 0.0, 0.5], [0.0, 0.5, 0.5]])
     g = np.arange(lattice_cells)
-    cell = np.stack(np.meshgrid(g, g, g, indexing="ij"), axis=-1).reshape(-1, 3)
+    gx = np.arange(lattice_cells * repeat_x)
+    cell = np.stack(np.meshgrid(gx, g, g, indexing="ij"), axis=-1).reshape(-1, 3)
     pos = ((cell[:, None, :] + basis[None, :, :] + 0.25) * a).reshape(-1, 3)
-    pos = pos.astype(np.float32).astype(np.float64) % box
+    ncell = max(3, int(np.floor(box / rc)))
+    cs = box / ncell
+    bx = (ncell * repeat_x) * cs if repeat_x > 1 else box
+    pos = pos.astype(np.float32).astype(np.float64) % np.array([bx, box, box])
     rng = np.random.default_rng(seed)
     vel = rng.normal(0.0, np.sqrt(temperature), size=pos.shape)
     vel -= vel.mean(axis=0)
     vel = vel.astype(np.float32).astype(np.float64)
-    ncell = max(3, int(np.floor(box / rc)))
-    return LJSystem(pos, vel, box, ncell, box / ncell, rc=rc, dt=dt)
+    return LJSystem(pos, vel, box, ncell, cs, rc=rc, dt=dt, repeat_x=repeat_x)

@@ -165,7 +165,7 @@ class LJSystem:
     def __init__(self, inp: _LJInput):
         self.inp = inp
         self.dev = _Device()
-        self.dims = (inp.cells, inp.cells, inp.cells)
+        self.dims = inp.cells_xyz
         self.dev.set(inp.positions, inp.velocities, None, self.dims, inp.cell_size, True, LAW_LJ,
                      (inp.rc, inp.eps, inp.sigma))
         self.n = inp.positions.shape[0]

@@ -1,0 +1,222 @@
+"""x-slab spatial decomposition of the cell-pair LJ MD over the GPUs of one box
+(BASELINE.json configs[4]: LJ MD spatially decomposed across
+B200s with a halo exchange).
+
+The reference runs every patch pair of ``compute_forces`` / ``md_step``
+(hr/workloads/md.py:121-190) in one process.  Here rank r owns the global x
+cells [bounds[r], bounds[r+1]) of the periodic cell grid and keeps its atoms
+resident in HBM (a gc_md slab handle, csrc/md.cu).  One step:
+
+  1. halo: the owned atoms of the first / last owned cell plane go to the
+     left / right neighbour, whose ghost planes they become;
+  2. the fused cell-pair force + integrator kernel runs on the owned cells
+     (ghost cells are read, never integrated), image shifts follow the GLOBAL
+     periodic grid, cells are ordered by global atom id, so every force,
+     cutoff decision and position is bit-identical to the whole-domain run;
+  3. migration: owned atoms whose new cell left the slab move to the
+     neighbour (position, velocity, global id).
+
+The exchanges are neighbour send/recv of variable-size records (counts first),
+over NCCL between GPUs (``DistTransport``), over gloo on CPU tensors in the
+tests, or in-process between slabs sharing one device (``LocalTransport``).
+There is no collective on the force path; per-step device time is reduced by
+MAX over ranks only for reporting.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib as L
+from .md import LAW_LJ, _Device
+
+GHOST, MIGRANT = 4, 8  # float64 words per packed record (1 or 2 double4)
+
+
+def slab_bounds(gnx: int, k: int) -> list:
+    """K + 1 cell boundaries splitting gnx x cells as evenly as possible."""
+    if k < 1 or gnx < k:
+        raise ValueError("need 1 <= k <= gnx")
+    return [r * gnx // k for r in range(k + 1)]
+
+
+def neighbours(rank: int, k: int):
+    """(left, right) ranks on the periodic ring of slabs."""
+    return (rank - 1) % k, (rank + 1) % k
+
+
+def global_cell_x(x: np.ndarray, cell: float, gnx: int) -> np.ndarray:
+    """Global x cell of positions: floor(x / cell) clamped to the grid (the
+    device's md_cell_index for 3-D cells)."""
+    return np.clip(np.floor(x / cell).astype(np.int64), 0, gnx - 1)
+
+
+class DistTransport:
+    """Neighbour exchange over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.k = dist.get_world_size(group)
+
+    def _peer(self, r):
+        return self.dist.get_global_rank(self.group, r) if self.group is not None else r
+
+    def exchange(self, to_left, to_right):
+        """Send `to_left` to the left neighbour and `to_right` to the right one;
+        return (from_left, from_right).  Tensors are (n, w) float64 on the
+        transport's device; n may differ per message and may be 0."""
+        import torch
+        if self.k == 1:  # a single slab is its own left and right neighbour
+            return to_right, to_left
+        if self.dist.get_backend(self.group) == "gloo" and to_left.device.type == "cuda":
+            dev = to_left.device  # gloo moves host tensors
+            fl, fr = self.exchange(to_left.cpu(), to_right.cpu())
+            return fl.to(dev), fr.to(dev)
+        dist = self.dist
+        left, right = neighbours(self.rank, self.k)
+        dev, w = to_left.device, to_left.shape[1]
+        # counts first (tag 0: travelling left, tag 1: travelling right)
+        sl = torch.tensor([to_left.shape[0]], dtype=torch.int64, device=dev)
+        sr = torch.tensor([to_right.shape[0]], dtype=torch.int64, device=dev)
+        rl, rr = torch.zeros_like(sl), torch.zeros_like(sr)
+        ops = [dist.P2POp(dist.isend, sl, self._peer(left), self.group, 0),
+               dist.P2POp(dist.isend, sr, self._peer(right), self.group, 1),
+               dist.P2POp(dist.irecv, rl, self._peer(left), self.group, 1),
+               dist.P2POp(dist.irecv, rr, self._peer(right), self.group, 0)]
+        for q in dist.batch_isend_irecv(ops):
+            q.wait()
+        fl = torch.empty((int(rl.item()), w), dtype=torch.float64, device=dev)
+        fr = torch.empty((int(rr.item()), w), dtype=torch.float64, device=dev)
+        ops = []
+        if to_left.shape[0]:
+            ops.append(dist.P2POp(dist.isend, to_left.contiguous(), self._peer(left), self.group, 2))
+        if to_right.shape[0]:
+            ops.append(dist.P2POp(dist.isend, to_right.contiguous(), self._peer(right), self.group, 3))
+        if fl.shape[0]:
+            ops.append(dist.P2POp(dist.irecv, fl, self._peer(left), self.group, 3))
+        if fr.shape[0]:
+            ops.append(dist.P2POp(dist.irecv, fr, self._peer(right), self.group, 2))
+        if ops:
+            for q in dist.batch_isend_irecv(ops):
+                q.wait()
+        if dev.type == "cuda":
+            torch.cuda.synchronize(dev)  # the slab's own stream reads the received records next
+        return fl, fr
+
+
+class LocalTransport:
+    """All K slabs in one process (one GPU): messages are handed over directly.
+    ``exchange_all`` takes every slab's (to_left, to_right) at once."""
+
+    def __init__(self, k: int):
+        self.k = k
+
+    def exchange_all(self, outgoing):
+        out = []
+        for r in range(self.k):
+            left, right = neighbours(r, self.k)
+            out.append((outgoing[left][1], outgoing[right][0]))
+        return out
+
+
+class LJSlab:
+    """One rank's slab of a periodic LJ system (an ``md.LJSystem`` input)."""
+
+    def __init__(self, inp, gx0: int, gx1: int):
+        import torch
+        self.torch = torch
+        self.inp = inp
+        self.gnx, self.ny, self.nz = (int(c) for c in inp.cells_xyz)
+        self.gx0, self.gx1 = gx0, gx1
+        cx = global_cell_x(inp.positions[:, 0], inp.cell_size, self.gnx)
+        own = np.nonzero((cx >= gx0) & (cx < gx1))[0]
+        self.dev = _Device()
+        self.dev.set(inp.positions[own], inp.velocities[own], None, (gx1 - gx0 + 2, self.ny, self.nz),
+                     inp.cell_size, True, LAW_LJ, (inp.rc, inp.eps, inp.sigma))
+        gid = np.ascontiguousarray(own, dtype=np.int64)
+        L.call("gc_md_set_slab", self.dev.handle, gx0, self.gnx, L.ptr(gid, L.i64p))
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def _pack(self, what: int, width: int):
+        torch = self.torch
+        n = np.zeros(1, np.int64)
+        L.call("gc_md_pack", self.dev.handle, what, None, 0, L.ptr(n, L.i64p))
+        buf = torch.empty((int(n[0]), width), dtype=torch.float64, device=self.device)
+        if n[0]:
+            L.call("gc_md_pack", self.dev.handle, what, C.c_void_p(buf.data_ptr()), int(n[0]), L.ptr(n, L.i64p))
+        return buf
+
+    @staticmethod
+    def _ptr(t):
+        return C.c_void_p(t.data_ptr()) if t.shape[0] else None
+
+    def halo_out(self):
+        """(to_left, to_right): owned atoms of the first / last owned plane."""
+        return self._pack(0, GHOST), self._pack(1, GHOST)
+
+    def set_halo(self, from_left, from_right):
+        L.call("gc_md_set_ghosts", self.dev.handle, self._ptr(from_left), from_left.shape[0], self._ptr(from_right),
+               from_right.shape[0])
+
+    def advance(self, dt: float):
+        L.call("gc_md_slab_step", self.dev.handle, float(dt))
+
+    def migrants_out(self):
+        return self._pack(2, MIGRANT), self._pack(3, MIGRANT)
+
+    def take_migrants(self, from_left, from_right):
+        L.call("gc_md_migrate", self.dev.handle, self._ptr(from_left), from_left.shape[0], self._ptr(from_right),
+               from_right.shape[0])
+
+    def step(self, transport: DistTransport, dt: float | None = None):
+        dt = self.inp.dt if dt is None else dt
+        self.set_halo(*transport.exchange(*self.halo_out()))
+        self.advance(dt)
+        self.take_migrants(*transport.exchange(*self.migrants_out()))
+
+    def elapsed_ms(self) -> float:
+        return self.dev.elapsed_ms()
+
+    def owned(self):
+        """(positions, velocities, global ids) of the owned atoms (host)."""
+        n = np.zeros(1, np.int64)
+        L.call("gc_md_owned", self.dev.handle, L.ptr(n, L.i64p), None, None, None)
+        k = int(n[0])
+        p, v, g = np.zeros((k, 3)), np.zeros((k, 3)), np.zeros(k, np.int64)
+        L.call("gc_md_owned", self.dev.handle, L.ptr(n, L.i64p), L.ptr(p, L.f64p), L.ptr(v, L.f64p),
+               L.ptr(g, L.i64p))
+        return p, v, g
+
+
+def run_local(inp, k: int, steps: int, dt: float | None = None):
+    """K slabs on the current GPU, exchanged in-process; returns the assembled
+    global (positions, velocities) in original atom order."""
+    b = slab_bounds(inp.cells_xyz[0], k)
+    slabs = [LJSlab(inp, b[r], b[r + 1]) for r in range(k)]
+    tr = LocalTransport(k)
+    dt = inp.dt if dt is None else dt
+    for _ in range(steps):
+        for s, (fl, fr) in zip(slabs, tr.exchange_all([s.halo_out() for s in slabs])):
+            s.set_halo(fl, fr)
+        for s in slabs:
+            s.advance(dt)
+        for s, (fl, fr) in zip(slabs, tr.exchange_all([s.migrants_out() for s in slabs])):
+            s.take_migrants(fl, fr)
+    return assemble([s.owned() for s in slabs], inp.positions.shape[0])
+
+
+def assemble(parts, n: int):
+    """Global (positions, velocities) from every slab's owned atoms."""
+    pos, vel = np.full((n, 3), np.nan), np.full((n, 3), np.nan)
+    seen = np.zeros(n, np.int64)
+    for p, v, g in parts:
+        pos[g], vel[g] = p, v
+        np.add.at(seen, g, 1)
+    if not np.all(seen == 1):
+        raise RuntimeError("slab decomposition lost or duplicated atoms")
+    return pos, vel

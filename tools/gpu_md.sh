@@ -15,3 +15,8 @@ for _ in range(3):
 f, e = sysd.forces()
 print("force-only ms", sysd.dev.elapsed_ms())
 PY
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/md_launches.csv python -c "
+import sys; sys.path.insert(0, '.')
+from paper_2008_05712_b200 import md
+from paper_2008_05712_b200.generators import gen_lj_fcc
+s = md.LJSystem(gen_lj_fcc(30)); s.run(3)" > /dev/null 2>&1

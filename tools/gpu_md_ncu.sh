@@ -7,8 +7,6 @@ from paper_2008_05712_b200 import md
 from paper_2008_05712_b200.generators import gen_lj_fcc
 s = gen_lj_fcc(30)
 sysd = md.LJSystem(s)
-f, e = sysd.forces()
-sysd.run(2)
+sysd.forces(); sysd.forces()
 PY
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/md_launches.csv python /tmp/mdprof.py > gpurun_out/ncu_md_l.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"md_cell_kernel" -c 1 -o gpurun_out/prof_md python /tmp/mdprof.py > gpurun_out/ncu_md.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"md_cell_kernel" -s 1 -c 1 -o gpurun_out/prof_md python /tmp/mdprof.py > gpurun_out/ncu_md.log 2>&1
