@@ -42,24 +42,38 @@ __global__ void bb_keys(int n, int dim, const double *__restrict__ pos, double b
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double c[3], x[3];
+#pragma unroll
     for (int k = 0; k < 3; ++k) {
-        c[k] = __ddiv_rn(box, 2.0);
+        c[k] = box * 0.5;  // x * 0.5 == x / 2 exactly (nbody.py:83-108 halvings)
         x[k] = k < dim ? pos[(int64_t)i * dim + k] : 0.0;
     }
-    double h = __ddiv_rn(box, 2.0);
+    double h = box * 0.5;
     unsigned long long a = 0, b = 0;
     for (int L = 0; L < nlev; ++L) {
         int q = 0;
-        for (int k = 0; k < dim; ++k) q |= (x[k] >= c[k] ? 1 : 0) << k;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) q |= (k < dim && x[k] >= c[k] ? 1 : 0) << k;
         if (L < 21) a |= (unsigned long long)q << (3 * (20 - L));
         else b |= (unsigned long long)q << (3 * (41 - L));
-        const double ch = __ddiv_rn(h, 2.0);
-        for (int k = 0; k < dim; ++k) c[k] = __dadd_rn(c[k], ((q >> k) & 1) ? ch : -ch);
+        const double ch = h * 0.5;
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (k < dim) c[k] = __dadd_rn(c[k], ((q >> k) & 1) ? ch : -ch);
         h = ch;
     }
     k1[i] = a;
     k2[i] = b;
     idx[i] = i;
+}
+
+// a run of more than `bucket` equal sorted keys (above bit `shift`): some node
+// at the deepest sorted level still splits
+__global__ void bb_long_runs(int n, int bucket, const unsigned long long *__restrict__ ks, int shift,
+                             int *__restrict__ flag)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i + bucket >= n) return;
+    if ((ks[i] >> shift) == (ks[i + bucket] >> shift)) *flag = 1;
 }
 
 __global__ void bb_fill(int n, int *p, int v)
@@ -120,7 +134,7 @@ __global__ void bb_children(int mc, int L, int next_id, const int *__restrict__ 
     ccount[c] = end - i;
     const int q = key_digit(k1[i], k2[i], L);
     const double4 pc = lcenter[p];
-    const double ch = __ddiv_rn(pc.w, 2.0);
+    const double ch = pc.w * 0.5;  // == pc.w / 2 exactly
     double4 cc;
     cc.x = dim > 0 ? __dadd_rn(pc.x, (q & 1) ? ch : -ch) : pc.x;
     cc.y = dim > 1 ? __dadd_rn(pc.y, (q & 2) ? ch : -ch) : pc.y;
@@ -374,20 +388,41 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     auto &k1s = bh->ws.k1s;
     auto &k2s = bh->ws.k2s;
     auto &idx = bh->ws.idx;
+    auto &scratch_i = bh->ws.nsel2;
     auto &perm1 = bh->ws.perm1;
     auto &perm = bh->ws.perm;
     k1.resize(n); k2.resize(n); k1p.resize(n); k1s.resize(n); k2s.resize(n);
     idx.resize(n); perm1.resize(n); perm.resize(n);
     bb_keys<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, dim, pos.p, box, nlev, k1.p, k2.p, idx.p);
     check_launch("bb_keys");
-    // stable sort by (k1, k2), ties by original id: LSD on k2 then k1
+    // stable sort by (k1, k2), ties by original id.  Digits of a level no
+    // node splits at do not change the tree, so first sort by the top
+    // SORT_LEVELS levels only; if some run of equal top keys is longer than a
+    // bucket (a node of that level would split), redo it with all levels
+    // (LSD on k2, then k1).
+    constexpr int SORT_LEVELS = 14;
+    const int top_bits = 3 * std::min(nlev, SORT_LEVELS);
     cubc(ctx, [&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, k2.p, k2s.p, idx.p, perm1.p, n, 0, 64, s);
+        return cub::DeviceRadixSort::SortPairs(t, b, k1.p, k1s.p, idx.p, perm.p, n, 63 - top_bits, 63, s);
     });
-    bb_gather_u64<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, perm1.p, k1.p, k1p.p);
-    cubc(ctx, [&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, k1p.p, k1s.p, perm1.p, perm.p, n, 0, 64, s);
-    });
+    int deep = 0;
+    if (nlev > SORT_LEVELS) {
+        scratch_i.resize(1);
+        scratch_i.zero(s);
+        bb_long_runs<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, (int)bucket, k1s.p, 63 - top_bits, scratch_i.p);
+        GC_CUDA(cudaMemcpyAsync(&deep, scratch_i.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        GC_CUDA(cudaStreamSynchronize(s));
+    }
+    if (deep) {
+        cubc(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, k2.p, k2s.p, idx.p, perm1.p, n, 0, 64, s);
+        });
+        bb_gather_u64<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, perm1.p, k1.p, k1p.p);
+        cubc(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, k1p.p, k1s.p, perm1.p, perm.p, n, 0, 64, s);
+        });
+    }
+    bb_gather_u64<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, perm.p, k1.p, k1s.p);
     bb_gather_u64<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, perm.p, k2.p, k2s.p);
     check_launch("bb sort");
 

@@ -362,7 +362,7 @@ __device__ __forceinline__ void md_integrate_one(long long ia, double3 f3, const
 }
 
 template <int LAW, int DIM, bool INTEG>
-__global__ void __launch_bounds__(MDC_THREADS)
+__global__ void __launch_bounds__(MDC_THREADS, 8)
 md_cell_kernel(const double4 *__restrict__ spos, const int *__restrict__ sidx, const int *__restrict__ cell_start,
                const MDParams P, float band, float inner, double4 *__restrict__ out, const MDInteg I)
 {
@@ -586,6 +586,26 @@ __global__ void md_sortgather_kernel(int ncell, const int *__restrict__ cell_sta
     }
 }
 
+// md_step integrator (md.py:171-189) fused with the cell assignment of the
+// new positions and the per-cell counts of the next cell sort (one thread per
+// owned atom, coalesced)
+__global__ void md_integrate_assign_kernel(int n, double4 *__restrict__ pos, double4 *__restrict__ vel,
+                                           const double4 *__restrict__ force, const MDParams P, double dt,
+                                           int use_npy, int *__restrict__ cell_of, int *__restrict__ count)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double4 p = pos[i], q = vel[i], f4 = force[i];
+    double x[3] = {p.x, p.y, p.z}, v[3] = {q.x, q.y, q.z};
+    const double f[3] = {f4.x, f4.y, f4.z};
+    md_advance(x, v, f, P, dt);
+    pos[i] = make_double4(x[0], x[1], x[2], 0.0);
+    vel[i] = make_double4(v[0], v[1], v[2], 0.0);
+    const int c = md_cell_index(x, P, use_npy);
+    cell_of[i] = c;
+    atomicAdd(&count[c], 1);
+}
+
 // md_step integrator (md.py:171-189), one atom per thread (unfused path)
 __global__ void md_integrate_kernel(int n, double4 *__restrict__ pos, double4 *__restrict__ vel,
                                     const double4 *__restrict__ force, const MDParams P, double dt)
@@ -802,7 +822,10 @@ void md_forces(gc_md *md)
 void md_step_once(gc_md *md, double dt)
 {
     if (md->cell_path) {
-        md_cell_forces(md, true, dt);
+        md_cell_forces(md, false, dt);
+        md_integrate_assign_kernel<<<grid_for(md->n, MD_TPB), MD_TPB, 0, md->ctx->stream>>>(
+            md->n, md->pos.p, md->vel.p, md->force.p, md->P, dt, md->use_npy, md->cell_of.p, md->count.p);
+        check_launch("md_integrate_assign_kernel");
         md_sort_counted(md);
         return;
     }
@@ -1136,9 +1159,14 @@ gc_status gc_md_slab_step(gc_md *md, double dt)
 {
     return guard([&] {
         GC_REQUIRE(md && md->P.slab, GC_E_STATE, "not a slab");
-        GC_CUDA(cudaEventRecord(md->e0, md->ctx->stream));
-        md_cell_forces(md, true, dt);  // forces on owned cells, integrator, new cells of owned atoms
-        GC_CUDA(cudaEventRecord(md->e1, md->ctx->stream));
+        cudaStream_t s = md->ctx->stream;
+        GC_CUDA(cudaEventRecord(md->e0, s));
+        md_cell_forces(md, false, dt);  // forces on the owned cells
+        if (md->n_owned > 0)  // integrator + new cells of the owned atoms (ghosts are never advanced)
+            md_integrate_assign_kernel<<<grid_for(md->n_owned, MD_TPB), MD_TPB, 0, s>>>(
+                md->n_owned, md->pos.p, md->vel.p, md->force.p, md->P, dt, md->use_npy, md->cell_of.p, md->count.p);
+        check_launch("md_integrate_assign_kernel");
+        GC_CUDA(cudaEventRecord(md->e1, s));
     });
 }
 

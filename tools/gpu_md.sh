@@ -20,3 +20,5 @@ import sys; sys.path.insert(0, '.')
 from paper_2008_05712_b200 import md
 from paper_2008_05712_b200.generators import gen_lj_fcc
 s = md.LJSystem(gen_lj_fcc(30)); s.run(3)" > /dev/null 2>&1
+timeout 900 python -m pytest tests/test_md_dist_gpu.py tests/test_md_gpu.py -q -p no:cacheprovider -x > gpurun_out/pytest_md.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_md.log
