@@ -71,34 +71,33 @@ void upload_tree(gc_bh *bh)
         bids[b] = (int)b;
         for (int64_t k = 0; k < t.pcount[id]; ++k) pb[t.pstart[id] + k] = (int)b;
     }
-    // walk groups: 32 consecutive buckets; force groups: <= 32 targets of
-    // consecutive buckets inside one walk group
+    // walk groups: WG_BUCKETS consecutive buckets; force groups: <= 32 targets
+    // of consecutive buckets inside one walk group
     bh->h_wg.clear();
     bh->h_fg.clear();
-    bh->h_fgmask.clear();
-    for (int64_t b0 = 0; b0 < nb; b0 += 32) {
+    for (int64_t b0 = 0; b0 < nb; b0 += WG_BUCKETS) {
         WalkGroup wg;
         wg.bfirst = (int)b0;
-        wg.nbucket = (int)std::min<int64_t>(32, nb - b0);
+        wg.nbucket = (int)std::min<int64_t>(WG_BUCKETS, nb - b0);
         wg.fg_first = (int)bh->h_fg.size();
         const int wi = (int)bh->h_wg.size();
         for (int64_t b = b0; b < b0 + wg.nbucket;) {
             ForceGroup fg;
             fg.pstart = (int)t.pstart[t.buckets[b]];
             fg.wg = wi;
-            fg.bmask = 0u;
+            fg.boff = (int)(b - b0);
             int tg = 0;
             while (b < b0 + wg.nbucket && tg + t.pcount[t.buckets[b]] <= 32) {
                 tg += (int)t.pcount[t.buckets[b]];
-                fg.bmask |= 1u << (b - b0);
                 ++b;
             }
             GC_REQUIRE(tg > 0, GC_E_VALUE, "bucket with more than 32 particles (coincident points) on the group path");
             fg.ntarget = tg;
+            fg.nb = (int)(b - b0) - fg.boff;
             bh->h_fg.push_back(fg);
-            bh->h_fgmask.push_back(fg.bmask);
         }
         wg.nfg = (int)bh->h_fg.size() - wg.fg_first;
+        GC_REQUIRE(wg.nfg <= 32, GC_E_VALUE, "walk group with more than 32 force groups");
         bh->h_wg.push_back(wg);
     }
     bh->d_recs.upload(recs.data(), nn, s);
@@ -113,11 +112,10 @@ void upload_tree(gc_bh *bh)
     bh->d_part_bucket.upload(pb.data(), t.n, s);
     bh->d_wg.upload(bh->h_wg.data(), bh->h_wg.size(), s);
     bh->d_fg.upload(bh->h_fg.data(), bh->h_fg.size(), s);
-    bh->d_fgmask.upload(bh->h_fgmask.data(), bh->h_fgmask.size(), s);
     bh->h2d += nn * (int64_t)(3 * sizeof(float4) + sizeof(double4) + sizeof(int2)) +
                nb * (int64_t)(sizeof(double4) + sizeof(float4) + sizeof(int2) + sizeof(int)) +
                t.n * (int64_t)sizeof(int) + (int64_t)bh->h_wg.size() * (int64_t)sizeof(WalkGroup) +
-               (int64_t)bh->h_fg.size() * (int64_t)(sizeof(ForceGroup) + sizeof(unsigned));
+               (int64_t)bh->h_fg.size() * (int64_t)sizeof(ForceGroup);
     GC_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -239,6 +237,7 @@ void walk_params(gc_bh *bh, double theta)
     bh->params_valid = true;
     bh->cap_theta = theta;
     bh->stats_valid = false;
+    bh->wg_order_valid = false;
     bh->have_union = false;
 }
 
@@ -273,9 +272,53 @@ void launch_walk(gc_bh *bh, bool write, bool stats)
     const UnionPool U = pool_view(bh);
     auto k = write ? (stats ? walk_group_kernel<true, true> : walk_group_kernel<true, false>)
                    : walk_group_kernel<false, true>;
-    k<<<grid, 32 * WARPS_PER_BLOCK, 0, s>>>(ng, wg, bh->d_fgmask.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p,
-                                            bh->d_bgeo32.p, bh->wp, U, bh->d_bstat.p, bh->d_flag.p);
+    int per_sm = 0;
+    GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * WARPS_PER_BLOCK, 0));
+    const unsigned pgrid = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)per_sm * bh->ctx->prop.multiProcessorCount, grid));
+    bh->d_wnext.resize(1);
+    bh->d_wnext.zero(s);
+    k<<<pgrid, 32 * WARPS_PER_BLOCK, 0, s>>>(ng, wg, bh->d_fg.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p,
+                                             bh->d_bgeo32.p, bh->wp, U, bh->d_bstat.p, bh->d_flag.p,
+                                             bh->wg_order_valid ? bh->d_wg_order.p : nullptr, bh->d_wnext.p);
     check_launch("walk_group_kernel");
+}
+
+// Heaviest-first walk-group order from a completed walk's union lists (entries
+// per force group ~ nodes visited); reused by later walks of the same tree.
+void make_walk_order(gc_bh *bh)
+{
+    cudaStream_t s = bh->ctx->stream;
+    const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? (int)bh->h_wg.size() : bh->rg1;
+    const int ng = g1 - g0, nf = (int)bh->h_fg.size();
+    if (ng <= 0) return;
+    std::vector<int> cnt(nf);
+    bh->d_gcount.download(cnt.data(), nf, s);
+    GC_CUDA(cudaStreamSynchronize(s));
+    std::vector<std::pair<int64_t, int>> w(ng);
+    for (int g = 0; g < ng; ++g) {
+        const WalkGroup &wg = bh->h_wg[g0 + g];
+        int64_t e = 0;
+        for (int f = wg.fg_first; f < wg.fg_first + wg.nfg; ++f) e += cnt[f];
+        w[g] = {-e, g};
+    }
+    std::stable_sort(w.begin(), w.end());
+    std::vector<int> order(ng);
+    for (int g = 0; g < ng; ++g) order[g] = w[g].second;
+    bh->d_wg_order.upload(order.data(), ng, s);
+    // force groups of the range, longest staging run first (force_group_kernel)
+    const int f0 = bh->h_wg[g0].fg_first;
+    const int f1 = g1 < (int)bh->h_wg.size() ? bh->h_wg[g1].fg_first : nf;
+    std::vector<int> rec(nf);
+    bh->d_grec.download(rec.data(), nf, s);
+    GC_CUDA(cudaStreamSynchronize(s));
+    std::vector<std::pair<int, int>> r(f1 - f0);
+    for (int f = f0; f < f1; ++f) r[f - f0] = {-rec[f], f - f0};
+    std::stable_sort(r.begin(), r.end());
+    std::vector<int> forder(f1 - f0);
+    for (size_t i = 0; i < r.size(); ++i) forder[i] = r[i].second;
+    bh->d_fg_lpt.upload(forder.data(), forder.size(), s);
+    bh->wg_order_valid = true;
 }
 
 // Synchronise and surface walk failures.  A pool overflow grows the pool to
@@ -321,6 +364,7 @@ void run_walk(gc_bh *bh, double theta, bool want_stats)
         while (walk_overflowed(bh)) launch_walk(bh, true, true);
         bh->stats_valid = true;
         bh->stats_dirty = true;
+        make_walk_order(bh);
     }
 }
 
@@ -389,17 +433,21 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
         }
         // first guess ~160 records per bucket; an overflow grows it to the walk's demand
         if (bh->staging_cap == 0) size_staging(bh, 160 * bh->n_buckets + 1024);
-        // the persistent force kernel hands out force groups in depth-first order
-        // (a longest-run-first sort costs more than the tail it removes at 1M)
-        bh->d_fg_order.resize(nfg);
+        // the persistent force kernel hands out force groups longest run first
+        // when a previous walk of this tree/range fixed that order, else in
+        // depth-first order (sorting every step costs more than its tail saves)
         bh->d_next.resize(1);
         bh->d_next.zero(s);
-        if (nfg > 0) bb_iota_kernel<<<grid_for(nfg, 256), 256, 0, s>>>(nfg, bh->d_fg_order.p);
+        const bool lpt = bh->wg_order_valid && (int64_t)bh->d_fg_lpt.n == nfg;
+        if (!lpt) {
+            bh->d_fg_order.resize(nfg);
+            if (nfg > 0) bb_iota_kernel<<<grid_for(nfg, 256), 256, 0, s>>>(nfg, bh->d_fg_order.p);
+        }
         Staging S;
         S.rec = bh->d_srec.p;
         S.mask = bh->d_smask.p;
         S.rbase = bh->d_rbase.p;
-        S.order = bh->d_fg_order.p;
+        S.order = lpt ? bh->d_fg_lpt.p : bh->d_fg_order.p;
         S.next = bh->d_next.p;
         S.cap = bh->staging_cap;
         if (nfg > 0) {
@@ -483,6 +531,7 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
         bh->params_valid = false;
         bh->stats_valid = false;
         bh->stats_dirty = false;
+        bh->wg_order_valid = false;
         bh->rg0 = 0;
         bh->rg1 = -1;
         if (!bh->device_build) {
@@ -717,6 +766,7 @@ gc_status gc_bh_set_range(gc_bh *bh, int64_t wg_begin, int64_t wg_end)
         bh->rg1 = (int)wg_end;
         bh->have_union = false;
         bh->stats_valid = false;  // stats cover the walked range
+        bh->wg_order_valid = false;
     });
 }
 

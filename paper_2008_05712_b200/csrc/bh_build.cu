@@ -323,21 +323,20 @@ __global__ void bb_buckets(int nb, int dim, const int *__restrict__ buckets, con
 template <int PASS>
 __global__ void bb_groups(int nwg, int nb, const int2 *__restrict__ brange, int *__restrict__ nfg_of,
                           const int *__restrict__ fg_base, WalkGroup *__restrict__ wg, ForceGroup *__restrict__ fg,
-                          unsigned *__restrict__ fgmask, int *__restrict__ bad)
+                          int *__restrict__ bad)
 {
     const int w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= nwg) return;
-    const int b0 = w * 32, b1 = min(nb, b0 + 32);
+    const int b0 = w * WG_BUCKETS, b1 = min(nb, b0 + WG_BUCKETS);
     int k = 0;
     for (int b = b0; b < b1;) {
         ForceGroup g;
         g.pstart = brange[b].x;
         g.wg = w;
-        g.bmask = 0u;
+        g.boff = b - b0;
         int tg = 0;
         while (b < b1 && tg + brange[b].y <= 32) {
             tg += brange[b].y;
-            g.bmask |= 1u << (b - b0);
             ++b;
         }
         if (tg == 0) {
@@ -345,12 +344,11 @@ __global__ void bb_groups(int nwg, int nb, const int2 *__restrict__ brange, int 
             return;
         }
         g.ntarget = tg;
-        if (PASS == 1) {
-            fg[fg_base[w] + k] = g;
-            fgmask[fg_base[w] + k] = g.bmask;
-        }
+        g.nb = b - b0 - g.boff;
+        if (PASS == 1) fg[fg_base[w] + k] = g;
         ++k;
     }
+    if (k > 32) atomicOr(bad, 2);
     if (PASS == 0) nfg_of[w] = k;
     else wg[w] = WalkGroup{b0, b1 - b0, fg_base[w], k};
 }
@@ -586,7 +584,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
                                                        bh->d_part_bucket.p, bh->d_parts.p, bh->d_porder.p);
     check_launch("bb records");
     // groups
-    const int nwg = (nb + 31) / 32;
+    const int nwg = (nb + WG_BUCKETS - 1) / WG_BUCKETS;
     auto &nfg_of = bh->ws.nfg_of;
     auto &fg_base = bh->ws.fg_base;
     auto &bad = bh->ws.bad;
@@ -595,7 +593,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     bad.resize(1);
     bad.zero(s);
     bb_groups<0><<<grid_for(nwg, BB_TPB), BB_TPB, 0, s>>>(nwg, nb, bh->d_brange.p, nfg_of.p, nullptr, nullptr,
-                                                          nullptr, nullptr, bad.p);
+                                                          nullptr, bad.p);
     GC_CUDA(cudaMemsetAsync(nfg_of.p + nwg, 0, sizeof(int), s));
     cubc(ctx, [&](void *t, size_t &b) {
         return cub::DeviceScan::ExclusiveSum(t, b, nfg_of.p, fg_base.p, nwg + 1, s);
@@ -606,21 +604,19 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     double cm = 0.0;
     GC_CUDA(cudaMemcpyAsync(&cm, cmax_out.p, sizeof(double), cudaMemcpyDeviceToHost, s));
     GC_CUDA(cudaStreamSynchronize(s));
-    GC_REQUIRE(!badh, GC_E_VALUE, "bucket with more than 32 particles (coincident points) on the group path");
+    GC_REQUIRE(!(badh & 1), GC_E_VALUE, "bucket with more than 32 particles (coincident points) on the group path");
+    GC_REQUIRE(!(badh & 2), GC_E_VALUE, "walk group with more than 32 force groups");
     bh->d_wg.resize(nwg);
     bh->d_fg.resize(nfg);
-    bh->d_fgmask.resize(nfg);
     bb_groups<1><<<grid_for(nwg, BB_TPB), BB_TPB, 0, s>>>(nwg, nb, bh->d_brange.p, nullptr, fg_base.p, bh->d_wg.p,
-                                                          bh->d_fg.p, bh->d_fgmask.p, bad.p);
+                                                          bh->d_fg.p, bad.p);
     check_launch("bb groups");
     bh->h_wg.resize(nwg);
     bh->h_fg.resize(nfg);
-    bh->h_fgmask.resize(nfg);
     bh->d_wg.download(bh->h_wg.data(), nwg, s);
     bh->d_fg.download(bh->h_fg.data(), nfg, s);
-    bh->d_fgmask.download(bh->h_fgmask.data(), nfg, s);
     GC_CUDA(cudaStreamSynchronize(s));
-    bh->d2h += (int64_t)nwg * sizeof(WalkGroup) + (int64_t)nfg * (sizeof(ForceGroup) + sizeof(unsigned));
+    bh->d2h += (int64_t)nwg * sizeof(WalkGroup) + (int64_t)nfg * sizeof(ForceGroup);
     set_tree_bounds(bh, cm);
     bh->n = n;
     bh->dim = dim;

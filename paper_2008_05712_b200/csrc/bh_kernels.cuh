@@ -35,18 +35,22 @@ constexpr int QWIN = 128;  // window of expanded source records per warp
 constexpr int FLUSH = 8;  // fp32 partial sums are flushed to fp64 every FLUSH records (the mask loads assume 8)
 constexpr int NODE_BITS = 26;  // stack entries pack node | level << NODE_BITS
 
+constexpr int BPL = 2;  // buckets per lane in the walk
+constexpr int WG_BUCKETS = 32 * BPL;  // buckets per walk group (lane l holds buckets l, l + 32, ...)
+
 struct WalkGroup {
     int bfirst;  // first bucket (depth-first index)
-    int nbucket;  // <= 32
+    int nbucket;  // <= WG_BUCKETS
     int fg_first;  // its force groups: [fg_first, fg_first + nfg)
-    int nfg;
+    int nfg;  // <= 32
 };
 
 struct ForceGroup {
     int pstart;  // first target in the DFS-sorted particle array
     int ntarget;  // <= 32
     int wg;  // walk group that emits its list
-    unsigned bmask;  // its buckets, as bits of the walk group (bit j = bucket bfirst + j)
+    int boff;  // its buckets: walk-group buckets [boff, boff + nb); list masks use bit j = bucket boff + j
+    int nb;  // <= 32
 };
 
 struct WalkParams {
@@ -128,35 +132,54 @@ struct UnionPool {
 // ---------------------------------------------------------------------------
 template <bool WRITE, bool STATS>
 __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, 4)
-walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsigned *__restrict__ fg_mask,
+walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const ForceGroup *__restrict__ fgroups,
                   const float4 *__restrict__ recs, const double4 *__restrict__ com64,
                   const double4 *__restrict__ bgeo, const float4 *__restrict__ bgeo32, const WalkParams P,
-                  UnionPool U, int64_t *__restrict__ bstat, int *__restrict__ flag)
+                  UnionPool U, int64_t *__restrict__ bstat, int *__restrict__ flag, const int *__restrict__ order,
+                  int *__restrict__ next)
 {
-    __shared__ int2 stack_s[WARPS_PER_BLOCK][STACK_CAP];  // (first | (nc - 1) << NODE_BITS, active buckets)
+    using u64 = unsigned long long;
+    __shared__ int2 stack_s[WARPS_PER_BLOCK][STACK_CAP];  // (first | (nc - 1) << NODE_BITS, active buckets 0-31)
+    __shared__ unsigned act_hi_s[WARPS_PER_BLOCK][STACK_CAP];  // active buckets 32-63
     __shared__ unsigned char lvl_s[WARPS_PER_BLOCK][STACK_CAP];
     __shared__ float2 tt_s[MAX_LEVELS];
     for (int i = threadIdx.x; i < MAX_LEVELS; i += blockDim.x) tt_s[i] = P.tt[i];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = blockIdx.x * WARPS_PER_BLOCK + warp;
-    if (g >= ngroups) return;
+    // persistent warps: walk groups handed out dynamically, in `order` (heaviest
+    // first, from the previous walk of this tree) when known
+    for (;;) {
+    int gi = 0;
+    if (lane == 0) gi = atomicAdd(next, 1);
+    gi = __shfl_sync(0xffffffffu, gi, 0);
+    if (gi >= ngroups) break;
+    const int g = order ? order[gi] : gi;
     const WalkGroup gd = groups[g];
-    const bool has = lane < gd.nbucket;
-    const float4 bf = has ? bgeo32[gd.bfirst + lane] : make_float4(0.f, 0.f, 0.f, -1.f);
-    const bool exact32 = bf.w >= 0.f;  // bucket geometry representable in float32
-    const unsigned full = gd.nbucket == 32 ? 0xffffffffu : ((1u << gd.nbucket) - 1u);
-    const unsigned bit = 1u << lane;
+    // lane holds buckets lane and lane + 32 of the group
+    float4 bf[BPL];
+    float s0[BPL];  // NaN: geometry not float32-exact, always take the float64 test
+#pragma unroll
+    for (int k = 0; k < BPL; ++k) {
+        const int j = lane + 32 * k;
+        bf[k] = j < gd.nbucket ? bgeo32[gd.bfirst + j] : make_float4(0.f, 0.f, 0.f, -1.f);
+        s0[k] = bf[k].w >= 0.f ? 0.f : __int_as_float(0x7fc00000);
+    }
+    const u64 full = gd.nbucket >= 64 ? ~0ull : ((1ull << gd.nbucket) - 1ull);
     int2 *stack = stack_s[warp];
+    unsigned *sact = act_hi_s[warp];
     unsigned char *slvl = lvl_s[warp];
     int sp = 0;
-    // lanes whose geometry is not float32-exact always take the float64 test (s = NaN)
-    const float s0 = exact32 ? 0.f : __int_as_float(0x7fc00000);
-    // lane f < nfg emits the list of force group fg_first + f; its current
-    // chunk always has room for slot w % CHUNK (allocated one entry ahead)
+    // lane f < nfg emits the list of force group fg_first + f (masks shifted to
+    // its own buckets); its current chunk always has room for slot w % CHUNK
     const bool emits = lane < gd.nfg;
     const int my_fg = gd.fg_first + (emits ? lane : 0);
-    const unsigned fgm = emits ? fg_mask[my_fg] : 0u;
+    int boff = 0;
+    u64 fgm = 0ull;
+    if (emits) {
+        const ForceGroup fg = fgroups[my_fg];
+        boff = fg.boff;
+        fgm = ((1ull << fg.nb) - 1ull) << boff;
+    }
     int w = 0, chunk = 0, nrec = 0;
     int4 *wp = U.ent;  // next entry slot of this lane's force group
     if (WRITE && emits) {
@@ -168,10 +191,10 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
         U.gfirst[my_fg] = chunk;
         wp = U.ent + (int64_t)chunk * CHUNK;
     }
-    int my_entries = 0, my_items = 0;
+    int my_entries[BPL] = {}, my_items[BPL] = {};
     // the root is a sibling group of one, tested by every bucket
     int first = 0, nc = 1, lvl = 0;
-    unsigned act = full;
+    u64 act = full;
     while (true) {
         const float2 th = tt_s[lvl];
         const int last = first + nc - 1;
@@ -182,26 +205,36 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
             const int wd = __float_as_int(nd.w);
             const bool is_bucket = wr_bucket(wd);
             // float32 opening test with error bound: certain accept / certain reject
-            const float v0 = fmaxf(fabsf(nd.x - bf.x) - bf.w, 0.f);
-            const float v1 = fmaxf(fabsf(nd.y - bf.y) - bf.w, 0.f);
-            const float v2 = fmaxf(fabsf(nd.z - bf.z) - bf.w, 0.f);
-            const float s = fmaf(v2, v2, fmaf(v1, v1, fmaf(v0, v0, s0)));
-            unsigned acc_m = __ballot_sync(0xffffffffu, s > th.x) & act;
-            const unsigned unsure_m = ~__ballot_sync(0xffffffffu, s < th.y) & ~acc_m & act;
-            if (unsure_m) {  // rare: the reference's float64 test (warp-uniform branch)
-                bool a = false;
-                if (unsure_m & bit)
-                    a = mac_accept64(com64[node], ldexp(P.root_size, -lvl), bgeo[gd.bfirst + lane], P.theta,
-                                     P.theta2);
-                acc_m |= __ballot_sync(0xffffffffu, a);
+            u64 acc = 0ull, rej = 0ull;
+#pragma unroll
+            for (int k = 0; k < BPL; ++k) {
+                const float v0 = fmaxf(fabsf(nd.x - bf[k].x) - bf[k].w, 0.f);
+                const float v1 = fmaxf(fabsf(nd.y - bf[k].y) - bf[k].w, 0.f);
+                const float v2 = fmaxf(fabsf(nd.z - bf[k].z) - bf[k].w, 0.f);
+                const float sv = fmaf(v2, v2, fmaf(v1, v1, fmaf(v0, v0, s0[k])));
+                acc |= (u64)__ballot_sync(0xffffffffu, sv > th.x) << (32 * k);
+                rej |= (u64)__ballot_sync(0xffffffffu, sv < th.y) << (32 * k);
             }
-            const unsigned part_m = is_bucket ? (act & ~acc_m) : 0u;
-            const unsigned hit = (acc_m | part_m) & fgm;
+            acc &= act;
+            const u64 unsure = ~rej & ~acc & act;
+            if (unsure) {  // rare: the reference's float64 test (warp-uniform branch)
+#pragma unroll
+                for (int k = 0; k < BPL; ++k) {
+                    bool a = false;
+                    if ((unsure >> (lane + 32 * k)) & 1ull)
+                        a = mac_accept64(com64[node], ldexp(P.root_size, -lvl), bgeo[gd.bfirst + lane + 32 * k],
+                                         P.theta, P.theta2);
+                    acc |= (u64)__ballot_sync(0xffffffffu, a) << (32 * k);
+                }
+            }
+            const u64 part = is_bucket ? (act & ~acc) : 0ull;
             if (WRITE) {
-                if (emits) *wp = make_int4(node, (int)(acc_m & fgm), (int)(part_m & fgm), wd);
+                const unsigned ma = (unsigned)((acc & fgm) >> boff), mp = (unsigned)((part & fgm) >> boff);
+                const bool hit = (ma | mp) != 0u;
+                if (emits) *wp = make_int4(node, (int)ma, (int)mp, wd);
                 w += hit ? 1 : 0;
                 wp += hit ? 1 : 0;
-                nrec += ((acc_m & fgm) ? 1 : 0) + ((part_m & fgm) ? wr_pcount(wd) : 0);
+                nrec += (ma ? 1 : 0) + (mp ? wr_pcount(wd) : 0);
                 if (hit && (w & (CHUNK - 1)) == 0) {  // chunk full: link the next one
                     int cn = atomicAdd(U.top, 1);
                     if (cn >= U.nchunks) {
@@ -214,11 +247,14 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
                 }
             }
             if (STATS) {
-                const bool a = acc_m & bit, p = part_m & bit;
-                my_entries += (a || p) ? 1 : 0;
-                my_items += a ? 1 : (p ? wr_pcount(wd) : 0);  // item_count (nbody.py:187-189)
+#pragma unroll
+                for (int k = 0; k < BPL; ++k) {
+                    const bool a = (acc >> (lane + 32 * k)) & 1ull, p = (part >> (lane + 32 * k)) & 1ull;
+                    my_entries[k] += (a || p) ? 1 : 0;
+                    my_items[k] += a ? 1 : (p ? wr_pcount(wd) : 0);  // item_count (nbody.py:187-189)
+                }
             }
-            const unsigned open = is_bucket ? 0u : (act & ~acc_m);
+            const u64 open = is_bucket ? 0ull : (act & ~acc);
             if (open) {  // the children wait as one sibling group (nbody.py:184-186)
                 if (sp >= STACK_CAP) {
                     if (lane == 0) atomicOr(flag, 1);
@@ -226,7 +262,8 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
                     break;
                 }
                 if (lane == 0) {
-                    stack[sp] = make_int2(wr_first(wd) | ((wd & 7) << NODE_BITS), (int)open);
+                    stack[sp] = make_int2(wr_first(wd) | ((wd & 7) << NODE_BITS), (int)(unsigned)open);
+                    sact[sp] = (unsigned)(open >> 32);
                     slvl[sp] = (unsigned char)(lvl + 1);
                 }
                 ++sp;
@@ -239,7 +276,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
         const int2 top = stack[sp];
         first = top.x & ((1 << NODE_BITS) - 1);
         nc = (top.x >> NODE_BITS) + 1;
-        act = (unsigned)top.y;
+        act = (u64)(unsigned)top.y | ((u64)sact[sp] << 32);
         lvl = slvl[sp];
         __syncwarp();
     }
@@ -247,10 +284,17 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const unsig
         U.gcount[my_fg] = w;
         U.grec[my_fg] = nrec;
     }
-    if (STATS && has) {
-        bstat[2 * (int64_t)(gd.bfirst + lane)] = my_entries;
-        bstat[2 * (int64_t)(gd.bfirst + lane) + 1] = my_items;
+    if (STATS) {
+#pragma unroll
+        for (int k = 0; k < BPL; ++k) {
+            const int j = lane + 32 * k;
+            if (j < gd.nbucket) {
+                bstat[2 * (int64_t)(gd.bfirst + j)] = my_entries[k];
+                bstat[2 * (int64_t)(gd.bfirst + j) + 1] = my_items[k];
+            }
+        }
     }
+    }  // persistent loop
 }
 
 // Per-bucket walk_order / kind CSR from the union lists (parity + drop-in API):
@@ -266,8 +310,8 @@ union_to_lists_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const Wal
     if (f >= nfg) return;
     const ForceGroup fg = fgroups[f];
     const unsigned bit = 1u << lane;
-    const bool mine = fg.bmask & bit;
-    int64_t cur = mine ? bptr[wgroups[fg.wg].bfirst + lane] : 0;
+    const bool mine = lane < fg.nb;  // lane = the force group's bucket boff + lane
+    int64_t cur = mine ? bptr[wgroups[fg.wg].bfirst + fg.boff + lane] : 0;
     const int n = U.gcount[f];
     int chunk = n > 0 ? U.gfirst[f] : 0;
     for (int e = 0; e < n; ++e) {
@@ -544,7 +588,7 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int *_
         const bool tgt = lane < fg.ntarget;
         const int p = fg.pstart + (tgt ? lane : 0);
         const float4 xp = parts[p];
-        const unsigned mybit = tgt ? (1u << (part_bucket[p] - wgroups[fg.wg].bfirst)) : 0u;
+        const unsigned mybit = tgt ? (1u << (part_bucket[p] - wgroups[fg.wg].bfirst - fg.boff)) : 0u;
         const GroupFrame F = group_frame(xp, cgrid);
         // target in group coordinates (exact), negated and duplicated for the packed subtract
         const float2 nx = f2(F.cx - xp.x, F.cx - xp.x), ny = f2(F.cy - xp.y, F.cy - xp.y),

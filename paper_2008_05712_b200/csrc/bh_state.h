@@ -41,8 +41,6 @@ struct gc_bh {
     DBuf<int> d_first_child, d_nchild, d_pstart, d_pcount, d_buckets;
     std::vector<WalkGroup> h_wg;
     std::vector<ForceGroup> h_fg;
-    std::vector<unsigned> h_fgmask;
-    DBuf<unsigned> d_fgmask;
     // device tree
     DBuf<float4> d_recs;  // walk records: float32 com + packed links
     DBuf<double4> d_com64;  // float64 com (exact opening test)
@@ -72,6 +70,8 @@ struct gc_bh {
     DBuf<float4> d_srec;
     DBuf<unsigned> d_smask;
     DBuf<int> d_fg_order, d_next;
+    DBuf<int> d_wg_order, d_wnext, d_fg_lpt;  // walk: heaviest-first group order (valid for this tree / theta / range)
+    bool wg_order_valid = false;
     int64_t staging_cap = 0;
     DBuf<int4> d_ent;
     int pool_chunks = 0;
