@@ -413,7 +413,10 @@ __device__ __forceinline__ float group_origin(float lo, float hi, float cgrid, f
 // slots of scalar FP32 for the same arithmetic.
 // ---------------------------------------------------------------------------
 constexpr int PFLUSH = 16;  // records per fp64 flush (8 per packed half); run granularity
-constexpr int TILE = 64;  // records per cp.async stage
+#ifndef FORCE_TILE
+#define FORCE_TILE 64
+#endif
+constexpr int TILE = FORCE_TILE;  // records per cp.async stage (multiple of 64: 2 records + 2 masks per lane)
 
 struct Staging {
     float4 *rec;  // per record: x, y, z (group frame), m
@@ -579,9 +582,12 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int *_
         auto issue = [&](int t) {
             const int64_t r0 = rb + (int64_t)t * TILE;
             const int buf = t & 1;
-            cp_async16(&t_rec[warp][buf][lane], S.rec + r0 + lane);
-            cp_async16(&t_rec[warp][buf][lane + 32], S.rec + r0 + lane + 32);
-            if (lane < TILE / 4) cp_async16(&t_m[warp][buf][4 * lane], S.mask + r0 + 4 * lane);
+#pragma unroll
+            for (int k = 0; k < TILE / 32; ++k)
+                cp_async16(&t_rec[warp][buf][lane + 32 * k], S.rec + r0 + lane + 32 * k);
+#pragma unroll
+            for (int k = 0; k < TILE / 4; k += 32)
+                if (k + lane < TILE / 4) cp_async16(&t_m[warp][buf][4 * (k + lane)], S.mask + r0 + 4 * (k + lane));
             cp_async_commit();
         };
         if (ntile > 0) issue(0);
@@ -604,9 +610,13 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int *_
             __syncwarp();
             const int buf = t & 1;
             if (!FORCE_SCALAR) {  // transpose the stage into pairs
-                const float4 r0 = t_rec[warp][buf][2 * lane], r1 = t_rec[warp][buf][2 * lane + 1];
-                qa[lane] = make_float4(r0.x, r1.x, r0.y, r1.y);
-                qb[lane] = make_float4(r0.z, r1.z, r0.w, r1.w);
+#pragma unroll
+                for (int k = 0; k < TILE / 64; ++k) {
+                    const int pi = lane + 32 * k;
+                    const float4 r0 = t_rec[warp][buf][2 * pi], r1 = t_rec[warp][buf][2 * pi + 1];
+                    qa[pi] = make_float4(r0.x, r1.x, r0.y, r1.y);
+                    qb[pi] = make_float4(r0.z, r1.z, r0.w, r1.w);
+                }
             }
             __syncwarp();
 #if FORCE_SCALAR
