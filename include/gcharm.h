@@ -177,6 +177,20 @@ gc_status gc_dm_state(gc_dm *dm, int64_t out[4]);
 /* resident table sorted by buffer id (ChareTable, memory.py:50-75) */
 gc_status gc_dm_table(gc_dm *dm, int64_t *bufs, int64_t *slots, double *last_use, int64_t *pins);
 
+/* ---- combined work requests on the device (replaces the cost model at the
+ * GPU launch site, hr/timeline.py:300-321) ----------------------------------
+ * gc_dm_stage_bh: copy the last plan's transferred buffers (tree node ids)
+ * into their slots -- slot = [com hi, mass][com lo, pcount][bucket particles];
+ * the B200 form of the reference's H2D transfer (hr/timeline.py:307-316).
+ * gc_bh_run_members: members = DFS bucket indices of the combined request,
+ * kinds per plan position (0 node_interaction, 1 particle_interaction) in the
+ * plan's position order (per-member id order in REUSE_SORTED); forces of the
+ * members' particles into the tree's force array.  gc_bh_get_forces: D2H. */
+gc_status gc_dm_stage_bh(gc_dm *dm, gc_bh *bh);
+gc_status gc_bh_run_members(gc_bh *bh, gc_dm *dm, const int64_t *member_buckets, int32_t n_members,
+                            const int8_t *kinds, int64_t n_positions, double g, double eps);
+gc_status gc_bh_get_forces(gc_bh *bh, double *out);
+
 /* ---- cell-pair MD (hr/workloads/md.py; 3-D Lennard-Jones extension) --------
  * law 0: soft repulsion, params = {cutoff, stiffness, -} (kernels.py:105-161);
  * law 1: Lennard-Jones, params = {rc, epsilon, sigma} (no reference; oracle/).

@@ -77,6 +77,9 @@ SIGNATURES = {
     "gc_md_run": [vp, C.c_int32, C.c_double],
     "gc_md_get_state": [vp, f64p, f64p, i64p],
     "gc_md_elapsed": [vp, f64p],
+    "gc_dm_stage_bh": [vp, vp],
+    "gc_bh_run_members": [vp, vp, i64p, C.c_int32, i8p, C.c_int64, C.c_double, C.c_double],
+    "gc_bh_get_forces": [vp, f64p],
     "gc_md_set_slab": [vp, C.c_int64, C.c_int64, i64p],
     "gc_md_pack": [vp, C.c_int32, vp, C.c_int64, i64p],
     "gc_md_set_ghosts": [vp, vp, C.c_int64, vp, C.c_int64],

@@ -26,6 +26,7 @@
 #include <climits>
 #include <cstring>
 
+#include "bh_state.h"
 #include "common.cuh"
 
 namespace gc {
@@ -160,6 +161,114 @@ __global__ void dm_iota(int n, int *p)
     if (i < n) p[i] = i;
 }
 
+
+// ---------------------------------------------------------------------------
+// Combined work requests on the device (the launch site of hr/timeline.py:
+// 300-321, where the reference runs a cost model).  The slot pool holds the
+// reorganised payloads: a BH buffer (tree node id) occupies one slot as
+//   [rec_hi (com hi, mass)] [rec_lo (com lo, pcount bits)] [particles (x, y, z, m) ...]
+// so a node interaction reads the first two float4 and a particle
+// interaction the bucket's particles, both from the member's address map.
+// ---------------------------------------------------------------------------
+__global__ void dm_stage_bh_kernel(int nt, const int *__restrict__ transfer, int redundant,
+                                   const int *__restrict__ slot_of, int slot_f4, const float4 *__restrict__ recs,
+                                   const float4 *__restrict__ rec_hi, const float4 *__restrict__ rec_lo,
+                                   const int2 *__restrict__ prange,
+                                   const float4 *__restrict__ parts, float4 *__restrict__ pool, int *__restrict__ bad)
+{
+    const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (k >= nt) return;
+    const int b = transfer[k];
+    const int slot = redundant ? k : slot_of[b];
+    float4 *dst = pool + (int64_t)slot * slot_f4;
+    const int2 pr = prange[b];
+    const int pc = __float_as_int(recs[b].w) < 0 ? pr.y : 0;  // particles of buckets only
+    if (lane == 0) {
+        dst[0] = rec_hi[b];
+        float4 l = rec_lo[b];
+        l.w = __int_as_float(min(pc, slot_f4 - 2));
+        dst[1] = l;
+        if (pc > slot_f4 - 2) atomicOr(bad, 1);
+    }
+    for (int i = lane; i < min(pc, slot_f4 - 2); i += 32) dst[2 + i] = parts[pr.x + i];
+}
+
+// one warp per member bucket: lanes split its address map; up to MAXT targets
+template <bool EPS0>
+__global__ void __launch_bounds__(256)
+force_slot_kernel(int nmember, const int *__restrict__ member_bucket, const int *__restrict__ bounds,
+                  const int *__restrict__ addr, const signed char *__restrict__ kind, const int2 *__restrict__ brange,
+                  const float4 *__restrict__ parts, const int *__restrict__ porder, const float4 *__restrict__ pool,
+                  int slot_f4, float eps2, double g, int dim, double *__restrict__ out)
+{
+    constexpr int MAXT = 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mi = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (mi >= nmember) return;
+    const int2 br = brange[member_bucket[mi]];
+    const int p0 = bounds[mi], p1 = bounds[mi + 1];
+    for (int t0 = 0; t0 < br.y; t0 += MAXT) {
+        const int nt = min(MAXT, br.y - t0);
+        float3 xt[MAXT];
+        double ad[MAXT][3];
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) {
+            const float4 q = t < nt ? parts[br.x + t0 + t] : make_float4(0, 0, 0, 0);
+            xt[t] = make_float3(q.x, q.y, q.z);
+            ad[t][0] = ad[t][1] = ad[t][2] = 0.0;
+        }
+        float pt = 0.f;
+        for (int k0 = p0; k0 < p1; k0 += 32 * 4) {
+            float3 a[MAXT];
+#pragma unroll
+            for (int t = 0; t < MAXT; ++t) a[t] = make_float3(0.f, 0.f, 0.f);
+            for (int k = k0 + lane; k < min(k0 + 32 * 4, p1); k += 32) {
+                const float4 *src = pool + (int64_t)addr[k] * slot_f4;
+                const float4 h = src[0], l = src[1];
+                if (kind[k] == 0) {
+#pragma unroll
+                    for (int t = 0; t < MAXT; ++t)
+                        if (t < nt) interact<EPS0, false>(h, make_float3(l.x, l.y, l.z), h.w, xt[t], eps2, a[t], pt);
+                } else {
+                    const int pc = __float_as_int(l.w);
+                    for (int q = 0; q < pc; ++q) {
+                        const float4 sp = src[2 + q];
+#pragma unroll
+                        for (int t = 0; t < MAXT; ++t)
+                            if (t < nt) interact<EPS0, false>(sp, make_float3(0.f, 0.f, 0.f), sp.w, xt[t], eps2, a[t], pt);
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < MAXT; ++t) {
+                ad[t][0] += a[t].x;
+                ad[t][1] += a[t].y;
+                ad[t][2] += a[t].z;
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) {
+            if (t < nt) {
+                double dx = ad[t][0], dy = ad[t][1], dz = ad[t][2];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    dx += __shfl_xor_sync(0xffffffffu, dx, o);
+                    dy += __shfl_xor_sync(0xffffffffu, dy, o);
+                    dz += __shfl_xor_sync(0xffffffffu, dz, o);
+                }
+                if (lane == 0) {
+                    const int orig = porder[br.x + t0 + t];
+                    const double gm = g * (double)parts[br.x + t0 + t].w;
+                    out[(int64_t)orig * dim] = gm * dx;
+                    if (dim > 1) out[(int64_t)orig * dim + 1] = gm * dy;
+                    if (dim > 2) out[(int64_t)orig * dim + 2] = gm * dz;
+                }
+            }
+        }
+    }
+}
+
 }  // namespace gc
 
 using namespace gc;
@@ -179,6 +288,12 @@ struct gc_dm {
     DBuf<unsigned char> flag;
     DBuf<unsigned long long> tkeys, tkeys_s;
     DBuf<float4> pool;  // staged payloads, slot_bytes per slot
+    // the last plan's transfer list on the device (REDUNDANT: position p -> slot p)
+    const int *last_transfer = nullptr;
+    int last_nt = 0;
+    bool last_redundant = false;
+    DBuf<int> members;  // combined request: member buckets
+    DBuf<signed char> kinds;  // per plan position: 0 node record, 1 bucket particles
     // last plan (host copies)
     std::vector<int64_t> h_transfer, h_addr, h_tx, h_bounds, h_evicted;
     int64_t total_bytes = 0, indirection_bytes = 0;
@@ -380,6 +495,9 @@ gc_status gc_dm_build_plan(gc_dm *dm, const int64_t *ids, const int64_t *bounds,
                        "staging " + std::to_string(P) + " buffers exceeds " + std::to_string(dm->nslots) + " slots");
             dm_iota<<<grid_for(P, DM_TPB), DM_TPB, 0, s>>>(P, dm->addr.p);
             dm->h_transfer.assign(ids, ids + P);
+            dm->last_transfer = dm->ids.p;
+            dm->last_nt = P;
+            dm->last_redundant = true;
             dm->h_addr.resize(P);
             for (int p = 0; p < P; ++p) dm->h_addr[p] = p;
             dm->total_bytes = (int64_t)P * dm->slot_bytes;
@@ -452,6 +570,9 @@ gc_status gc_dm_build_plan(gc_dm *dm, const int64_t *ids, const int64_t *bounds,
             GC_CUDA(cudaStreamSynchronize(s));
             dm->h_addr.assign(a.begin(), a.end());
             dm->h_transfer.assign(t.begin(), t.end());
+            dm->last_transfer = miss;
+            dm->last_nt = K;
+            dm->last_redundant = false;
             dm->total_bytes = (int64_t)K * dm->slot_bytes;
             dm->indirection_bytes = 4 * (int64_t)P;  // ADDRESS_BYTES (memory.py:27)
             dm->indirect = true;
@@ -578,4 +699,77 @@ gc_status gc_dm_lookup(gc_dm *dm, const int64_t *ids, int64_t n, double now, int
     });
 }
 
+
+/* Stage the last plan's transferred buffers (BH tree node ids) into their
+ * slots: the reorganised payload layout of the slot pool (see above). */
+gc_status gc_dm_stage_bh(gc_dm *dm, gc_bh *bh)
+{
+    return guard([&] {
+        GC_REQUIRE(dm && bh && bh->have_tree, GC_E_STATE, "no tree");
+        const int slot_f4 = (int)(dm->slot_bytes / 16);
+        GC_REQUIRE(slot_f4 >= 3, GC_E_VALUE, "slot too small for a node record and a particle");
+        cudaStream_t s = dm->ctx->stream;
+        if (dm->pool.n == 0) {
+            dm->pool.resize((size_t)dm->nslots * slot_f4);
+            dm->pool.zero(s);
+        }
+        dm->nsel.resize(1);
+        dm->nsel.zero(s);
+        if (dm->last_nt > 0)
+            dm_stage_bh_kernel<<<grid_for(dm->last_nt, 8), 256, 0, s>>>(
+                dm->last_nt, dm->last_transfer, dm->last_redundant, dm->slot_of.p, slot_f4, bh->d_recs.p, bh->d_rec_hi.p,
+                bh->d_rec_lo.p, bh->d_prange.p, bh->d_parts.p, dm->pool.p, dm->nsel.p);
+        check_launch("dm_stage_bh_kernel");
+        int bad = 0;
+        dm->nsel.download(&bad, 1, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        GC_REQUIRE(!bad, GC_E_VALUE, "bucket larger than a slot (raise slot_bytes)");
+    });
+}
+
+/* One combined work request on the device: member m = DFS bucket
+ * member_buckets[m], its sources = the last plan's addresses of positions
+ * [bounds[m], bounds[m+1]) with kinds (0 node record, 1 bucket particles) in
+ * the plan's position order.  Forces of the members' particles go to the
+ * tree's force array (gc_bh_get_forces). */
+gc_status gc_bh_run_members(gc_bh *bh, gc_dm *dm, const int64_t *member_buckets, int32_t n_members,
+                            const int8_t *kinds, int64_t n_positions, double g, double eps)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && dm && bh->have_tree && n_members >= 0, GC_E_STATE, "bad argument");
+        GC_REQUIRE((int64_t)dm->addr.n >= n_positions && (int)dm->h_bounds.size() == n_members + 1 &&
+                       dm->h_bounds.back() == n_positions,
+                   GC_E_STATE, "members do not match the last plan");
+        cudaStream_t s = dm->ctx->stream;
+        std::vector<int> mb(std::max(n_members, 1));
+        for (int m = 0; m < n_members; ++m) {
+            GC_REQUIRE(member_buckets[m] >= 0 && member_buckets[m] < bh->n_buckets, GC_E_VALUE, "bad bucket");
+            mb[m] = (int)member_buckets[m];
+        }
+        dm->members.upload(mb.data(), n_members, s);
+        dm->kinds.upload(reinterpret_cast<const signed char *>(kinds), n_positions, s);
+        bh->d_out.resize(bh->n * bh->dim);
+        const float eps2 = (float)(eps * eps);
+        const int slot_f4 = (int)(dm->slot_bytes / 16);
+        GC_CUDA(cudaEventRecord(bh->ev[2], s));
+        if (n_members > 0) {
+            auto k = eps2 == 0.f ? force_slot_kernel<true> : force_slot_kernel<false>;
+            k<<<grid_for(n_members, 8), 256, 0, s>>>(n_members, dm->members.p, dm->bounds.p, dm->addr.p, dm->kinds.p,
+                                                     bh->d_brange.p, bh->d_parts.p, bh->d_porder.p, dm->pool.p, slot_f4,
+                                                     eps2, g, bh->dim, bh->d_out.p);
+            check_launch("force_slot_kernel");
+        }
+        GC_CUDA(cudaEventRecord(bh->ev[3], s));
+        GC_CUDA(cudaEventRecord(bh->ev[4], s));
+    });
+}
+
+gc_status gc_bh_get_forces(gc_bh *bh, double *out)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && out && bh->d_out.n >= (size_t)(bh->n * bh->dim), GC_E_STATE, "no forces");
+        bh->d_out.download(out, bh->n * bh->dim, bh->ctx->stream);
+        GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
+    });
+}
 }  // extern "C"

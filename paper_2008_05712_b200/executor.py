@@ -1,0 +1,151 @@
+"""Real-time launch site for combined work requests (north star (1)-(2),
+SURVEY.md §8f-1).
+
+The reference drives the BH force phase through its message-driven runtime:
+one work request per bucket (buffer_indices = the bucket's walk_order,
+hr/workloads/nbody.py:304-316), the occupancy / arrival-gap trigger combines
+them (hr/aggregator.py:91-110), the data manager plans the batch
+(hr/memory.py:289-360) and ``Timeline._launch_gpu`` charges a COST MODEL for
+the transfer and the kernel (hr/timeline.py:300-321).  Here the same API runs
+for real on the B200:
+
+  * ``Runtime`` / ``AggregatorState`` / ``poll_combine`` unchanged (host);
+    ``max_size`` comes from the occupancy of the real member kernel;
+  * the device data manager plans the batch (residency, LRU, min-free-slot,
+    per-member address maps -- bit-identical to the reference's plans);
+  * ``gc_dm_stage_bh`` moves the missing buffers' payloads (node COM/mass or
+    bucket particles) into their HBM slots: the reorganised staging layout;
+  * ``gc_bh_run_members`` evaluates every member bucket from its address map
+    (one warp per member), and the completion fans out to the owners.
+
+Arrival times are the workload's schedule (the reference's ``_schedule``,
+nbody.py:285-301); batches execute on the device as they are emitted and
+each batch's device time is recorded, so the combine / reuse experiments
+(hr/experiments.py:113-132) run on hardware instead of the cost model.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+from .aggregator import AggregatorState, compute_max_size, poll_combine
+from .devicesim import b200_device_spec, b200_kernel_spec
+from .memory import DeviceMemory, MemoryMode
+from .nbody import DEFAULT_SOFTENING
+from .runtime import CompletionEvent, Runtime
+
+
+@dataclass
+class BatchRecord:
+    """One combined launch (the reference's ScheduleLog row, hr/timeline.py:63-100)."""
+    combined_id: int
+    members: int
+    positions: int
+    transferred: int
+    transfer_bytes: int
+    indirection_bytes: int
+    transactions: int
+    emit_time: float
+    device_ms: float
+
+
+@dataclass
+class RunResult:
+    forces: np.ndarray
+    batches: list = field(default_factory=list)
+    wall_s: float = 0.0
+
+    @property
+    def device_ms(self) -> float:
+        return sum(b.device_ms for b in self.batches)
+
+    @property
+    def transfer_bytes(self) -> int:
+        return sum(b.transfer_bytes for b in self.batches)
+
+
+class GpuForceExecutor:
+    """Runs one BH force phase through the runtime API on the device."""
+
+    def __init__(self, tree, lists, mode: MemoryMode = MemoryMode.REUSE_SORTED, capacity_bytes: int = 8 << 20,
+                 slot_bytes: int = 256, g: float = 1.0, eps: float = DEFAULT_SOFTENING,
+                 timeout_factor: float = 2.0, max_size: int | None = None):
+        self.tree = tree
+        self.ptr, self.ids, self.kind, self.item_count = lists.csr()
+        self.mode = mode
+        self.memory = DeviceMemory(capacity_bytes, slot_bytes, mode)
+        self.g, self.eps = g, eps
+        if max_size is None:
+            max_size = compute_max_size(b200_kernel_spec("force_member"), b200_device_spec())
+        self.state = AggregatorState("force", int(max_size), timeout_factor)
+        self.runtime = Runtime()
+        self.runtime.register_group(self.state)
+        self._next_id = 0
+        self._ev = None
+
+    # -- one combined launch (replaces Timeline._launch_gpu's cost model) ----------
+    def _member_kinds(self, buckets) -> np.ndarray:
+        out = []
+        for b in buckets:
+            ids = self.ids[self.ptr[b]:self.ptr[b + 1]]
+            kd = self.kind[self.ptr[b]:self.ptr[b + 1]]
+            if self.mode is MemoryMode.REUSE_SORTED:  # the plan lists each member's ids ascending
+                kd = kd[np.argsort(ids, kind="stable")]
+            out.append(kd)
+        return np.concatenate(out).astype(np.int8) if out else np.zeros(0, np.int8)
+
+    def launch(self, combined, now: float) -> BatchRecord:
+        import torch
+        members = [wr.buffer_indices for wr in combined.members]
+        buckets = np.array([wr.owner for wr in combined.members], np.int64)
+        plan, layout = self.memory.build_plan(members, now)
+        kinds = self._member_kinds(buckets)
+        npos = int(layout.member_bounds[-1])
+        if self._ev is None:
+            self._ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        stream = torch.cuda.ExternalStream(L.context().stream)
+        self._ev[0].record(stream)
+        L.call("gc_dm_stage_bh", self.memory.handle, self.tree.handle)
+        L.call("gc_bh_run_members", self.tree.handle, self.memory.handle, L.ptr(L.i64(buckets), L.i64p),
+               len(buckets), L.ptr(kinds, L.i8p), npos, float(self.g), float(self.eps))
+        self._ev[1].record(stream)
+        self._ev[1].synchronize()
+        self.memory.release_batch(members)
+        self.runtime.on_completion(CompletionEvent(combined.combined_id, [wr.id for wr in combined.members],
+                                                   "gpu", now))
+        return BatchRecord(combined.combined_id, len(members), npos, len(plan.to_transfer), plan.total_bytes,
+                           plan.indirection_bytes, int(layout.total_transactions()), now,
+                           self._ev[0].elapsed_time(self._ev[1]))
+
+    # -- the force phase ------------------------------------------------------------
+    def run(self, arrival_times=None) -> RunResult:
+        """One work request per bucket (DFS order) at `arrival_times` (default:
+        back to back); returns the forces and the per-batch log."""
+        nb = len(self.ptr) - 1
+        times = np.zeros(nb) if arrival_times is None else np.asarray(arrival_times, float)
+        res = RunResult(forces=None)
+        t0 = time.perf_counter()
+        for b in range(nb):
+            ids = self.ids[self.ptr[b]:self.ptr[b + 1]]
+            wr = self.runtime.make_work_request(b, "force", ids.tolist(), int(self.item_count[b]), times[b])
+            self.runtime.submit_work_request(wr, times[b])
+            c = poll_combine(self.state, times[b], self._next_id)
+            if c is not None:
+                res.batches.append(self.launch(c, times[b]))
+                self._next_id += 1
+        # end of the phase: drain in max_size chunks (hr/timeline.py:276-298)
+        end = float(times[-1]) if nb else 0.0
+        from .aggregator import make_combined
+        while self.state.pending:
+            take = [self.state.pending.popleft() for _ in range(min(self.state.max_size, len(self.state.pending)))]
+            res.batches.append(self.launch(make_combined(take, end, self._next_id), end))
+            self._next_id += 1
+        res.wall_s = time.perf_counter() - t0
+        out = np.zeros((self.tree.n, self.tree.dim))
+        L.call("gc_bh_get_forces", self.tree.handle, L.ptr(out, L.f64p))
+        res.forces = out
+        return res
