@@ -435,6 +435,37 @@ def bench_md(args, world, rank, local, torch):
     }
 
 
+def bench_runtime_path(args):
+    """configs[0] (Plummer 16K, theta 0.7) through the reference's runtime API on
+    the device (executor.py): per memory mode, the combined launches' device
+    time and transfer bytes -- the paper's reuse experiment
+    on hardware instead of the timeline's cost model."""
+    from paper_2008_05712_b200 import generators as gen
+    from paper_2008_05712_b200 import nbody
+    from paper_2008_05712_b200.executor import GpuForceExecutor
+    from paper_2008_05712_b200.memory import MemoryMode
+
+    ps = gen.fp32_exact(gen.gen_plummer(16384, 42))
+    tree = nbody.build_bucket_tree(ps, BUCKET)
+    lists = nbody.build_interaction_lists(tree, THETA, ps)
+    ref = nbody.eval_forces(tree, lists, ps, 1.0, EPS)  # union path
+    out = {"workload": "configs[0] Plummer 16K, theta 0.7, one work request per bucket, arrivals back to back",
+           "modes": {}}
+    for mode in ("redundant", "reuse", "reuse_sorted"):
+        cap = 1 << 30 if mode == "redundant" else 64 << 20
+        ex = GpuForceExecutor(tree, lists, MemoryMode.parse(mode), capacity_bytes=cap, slot_bytes=256, eps=EPS)
+        ex.run()  # warm-up (first plans, allocations)
+        ex = GpuForceExecutor(tree, lists, MemoryMode.parse(mode), capacity_bytes=cap, slot_bytes=256, eps=EPS)
+        r = ex.run()
+        err = float((np.linalg.norm(r.forces - ref, axis=1) / np.linalg.norm(ref, axis=1)).max())
+        out["modes"][mode] = {"batches": len(r.batches), "max_size": ex.state.max_size,
+                              "device_ms": r.device_ms, "wall_ms": r.wall_s * 1e3,
+                              "transfer_bytes": r.transfer_bytes,
+                              "transactions": sum(b.transactions for b in r.batches),
+                              "max_rel_err_vs_union_path": err}
+    return out
+
+
 def run_ours(args, world, rank, local):
     import torch
 
@@ -470,6 +501,8 @@ def run_ours(args, world, rank, local):
                                    "interactions_all_ranks": bh["total_inter"],
                                    "system": f"one shared clustered system of {world} x 1M particles"}
         line["data"] = f"synthetic gen_particles({world}M, seed 42, clustering 0.6, dim 3), fp32-exact"
+    if world == 1:
+        line["runtime_path"] = bench_runtime_path(args)
     if world == 1 and not args.no_cpu_baseline:
         c_inter, c_ts, cores = cpu_bh(bh["ps"], 1)
         line["cpu_baseline"] = {"value": c_inter / c_ts[0], "unit": "interactions/s", "cores": cores,

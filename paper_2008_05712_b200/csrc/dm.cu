@@ -715,11 +715,13 @@ gc_status gc_dm_stage_bh(gc_dm *dm, gc_bh *bh)
         }
         dm->nsel.resize(1);
         dm->nsel.zero(s);
+        GC_CUDA(cudaEventRecord(bh->ev[0], s));  // staging time -> gc_bh_timings out[0]
         if (dm->last_nt > 0)
             dm_stage_bh_kernel<<<grid_for(dm->last_nt, 8), 256, 0, s>>>(
                 dm->last_nt, dm->last_transfer, dm->last_redundant, dm->slot_of.p, slot_f4, bh->d_recs.p, bh->d_rec_hi.p,
                 bh->d_rec_lo.p, bh->d_prange.p, bh->d_parts.p, dm->pool.p, dm->nsel.p);
         check_launch("dm_stage_bh_kernel");
+        GC_CUDA(cudaEventRecord(bh->ev[1], s));
         int bad = 0;
         dm->nsel.download(&bad, 1, s);
         GC_CUDA(cudaStreamSynchronize(s));
@@ -751,7 +753,8 @@ gc_status gc_bh_run_members(gc_bh *bh, gc_dm *dm, const int64_t *member_buckets,
         bh->d_out.resize(bh->n * bh->dim);
         const float eps2 = (float)(eps * eps);
         const int slot_f4 = (int)(dm->slot_bytes / 16);
-        GC_CUDA(cudaEventRecord(bh->ev[2], s));
+        GC_CUDA(cudaEventRecord(bh->ev[2], s));  // member kernel time -> gc_bh_timings out[1]
+        GC_CUDA(cudaEventRecord(bh->ev[4], s));
         if (n_members > 0) {
             auto k = eps2 == 0.f ? force_slot_kernel<true> : force_slot_kernel<false>;
             k<<<grid_for(n_members, 8), 256, 0, s>>>(n_members, dm->members.p, dm->bounds.p, dm->addr.p, dm->kinds.p,
@@ -760,7 +763,6 @@ gc_status gc_bh_run_members(gc_bh *bh, gc_dm *dm, const int64_t *member_buckets,
             check_launch("force_slot_kernel");
         }
         GC_CUDA(cudaEventRecord(bh->ev[3], s));
-        GC_CUDA(cudaEventRecord(bh->ev[4], s));
     });
 }
 

@@ -85,41 +85,37 @@ class GpuForceExecutor:
         self.runtime = Runtime()
         self.runtime.register_group(self.state)
         self._next_id = 0
-        self._ev = None
 
     # -- one combined launch (replaces Timeline._launch_gpu's cost model) ----------
     def _member_kinds(self, buckets) -> np.ndarray:
-        out = []
-        for b in buckets:
-            ids = self.ids[self.ptr[b]:self.ptr[b + 1]]
-            kd = self.kind[self.ptr[b]:self.ptr[b + 1]]
-            if self.mode is MemoryMode.REUSE_SORTED:  # the plan lists each member's ids ascending
-                kd = kd[np.argsort(ids, kind="stable")]
-            out.append(kd)
-        return np.concatenate(out).astype(np.int8) if out else np.zeros(0, np.int8)
+        """Kinds of every plan position: member lists concatenated, each in id
+        order in REUSE_SORTED (the plan sorts every member's ids)."""
+        if len(buckets) == 0:
+            return np.zeros(0, np.int8)
+        lo, hi = self.ptr[buckets], self.ptr[buckets + 1]
+        seg = np.repeat(np.arange(len(buckets)), hi - lo)
+        pos = np.arange(int((hi - lo).sum())) - np.repeat(np.cumsum(hi - lo) - (hi - lo), hi - lo) + np.repeat(lo, hi - lo)
+        kd, ids = self.kind[pos], self.ids[pos]
+        if self.mode is MemoryMode.REUSE_SORTED:
+            kd = kd[np.lexsort((ids, seg))]
+        return np.ascontiguousarray(kd, dtype=np.int8)
 
     def launch(self, combined, now: float) -> BatchRecord:
-        import torch
         members = [wr.buffer_indices for wr in combined.members]
         buckets = np.array([wr.owner for wr in combined.members], np.int64)
         plan, layout = self.memory.build_plan(members, now)
         kinds = self._member_kinds(buckets)
         npos = int(layout.member_bounds[-1])
-        if self._ev is None:
-            self._ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-        stream = torch.cuda.ExternalStream(L.context().stream)
-        self._ev[0].record(stream)
         L.call("gc_dm_stage_bh", self.memory.handle, self.tree.handle)
         L.call("gc_bh_run_members", self.tree.handle, self.memory.handle, L.ptr(L.i64(buckets), L.i64p),
                len(buckets), L.ptr(kinds, L.i8p), npos, float(self.g), float(self.eps))
-        self._ev[1].record(stream)
-        self._ev[1].synchronize()
+        tm = np.zeros(3)
+        L.call("gc_bh_timings", self.tree.handle, L.ptr(tm, L.f64p))  # staging + member kernel (events)
         self.memory.release_batch(members)
         self.runtime.on_completion(CompletionEvent(combined.combined_id, [wr.id for wr in combined.members],
                                                    "gpu", now))
         return BatchRecord(combined.combined_id, len(members), npos, len(plan.to_transfer), plan.total_bytes,
-                           plan.indirection_bytes, int(layout.total_transactions()), now,
-                           self._ev[0].elapsed_time(self._ev[1]))
+                           plan.indirection_bytes, int(layout.total_transactions()), now, float(tm[0] + tm[1]))
 
     # -- the force phase ------------------------------------------------------------
     def run(self, arrival_times=None) -> RunResult:
@@ -131,7 +127,7 @@ class GpuForceExecutor:
         t0 = time.perf_counter()
         for b in range(nb):
             ids = self.ids[self.ptr[b]:self.ptr[b + 1]]
-            wr = self.runtime.make_work_request(b, "force", ids.tolist(), int(self.item_count[b]), times[b])
+            wr = self.runtime.make_work_request(b, "force", ids, int(self.item_count[b]), times[b])
             self.runtime.submit_work_request(wr, times[b])
             c = poll_combine(self.state, times[b], self._next_id)
             if c is not None:

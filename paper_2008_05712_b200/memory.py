@@ -262,10 +262,10 @@ class DeviceMemory:
     # -- planning ----------------------------------------------------------------
     def build_plan(self, member_indices, now: float = 0.0):
         """hr/memory.py:289-360 on the device; returns (TransferPlan, AccessLayout)."""
-        members = [list(m) for m in member_indices]
+        members = [np.asarray(m, dtype=np.int64).reshape(-1) for m in member_indices]
         bounds = np.zeros(len(members) + 1, np.int64)
         bounds[1:] = np.cumsum([len(m) for m in members])
-        ids = L.i64([b for m in members for b in m]) if bounds[-1] else np.zeros(1, np.int64)
+        ids = np.ascontiguousarray(np.concatenate(members)) if bounds[-1] else np.zeros(1, np.int64)
         nt, npos = np.zeros(1, np.int64), np.zeros(1, np.int64)
         L.call("gc_dm_build_plan", self.handle, L.ptr(ids, L.i64p), L.ptr(bounds, L.i64p), len(members),
                float(now), L.ptr(nt, L.i64p), L.ptr(npos, L.i64p))
@@ -284,7 +284,8 @@ class DeviceMemory:
     def release_batch(self, member_indices) -> None:
         if self.mode is MemoryMode.REDUNDANT:
             return
-        ids = L.i64([b for m in member_indices for b in m])
+        parts = [np.asarray(m, dtype=np.int64).reshape(-1) for m in member_indices]
+        ids = np.ascontiguousarray(np.concatenate(parts)) if parts else np.zeros(0, np.int64)
         if len(ids):
             L.call("gc_dm_release", self.handle, L.ptr(ids, L.i64p), len(ids))
 
