@@ -68,6 +68,23 @@ class RunResult:
         return sum(b.transfer_bytes for b in self.batches)
 
 
+def plan_kinds(ptr, ids, kind, buckets, sorted_members: bool) -> np.ndarray:
+    """Kind (0 node, 1 particle interaction) of every position of a combined
+    request's plan: the member buckets' lists concatenated, each member in id
+    order when the plan sorts it (REUSE_SORTED, hr/memory.py:342-347)."""
+    buckets = np.asarray(buckets, np.int64)
+    if len(buckets) == 0:
+        return np.zeros(0, np.int8)
+    lo, hi = ptr[buckets], ptr[buckets + 1]
+    ln = hi - lo
+    seg = np.repeat(np.arange(len(buckets)), ln)
+    pos = np.arange(int(ln.sum())) - np.repeat(np.cumsum(ln) - ln, ln) + np.repeat(lo, ln)
+    kd = kind[pos]
+    if sorted_members:
+        kd = kd[np.lexsort((ids[pos], seg))]
+    return np.ascontiguousarray(kd, dtype=np.int8)
+
+
 class GpuForceExecutor:
     """Runs one BH force phase through the runtime API on the device."""
 
@@ -88,17 +105,7 @@ class GpuForceExecutor:
 
     # -- one combined launch (replaces Timeline._launch_gpu's cost model) ----------
     def _member_kinds(self, buckets) -> np.ndarray:
-        """Kinds of every plan position: member lists concatenated, each in id
-        order in REUSE_SORTED (the plan sorts every member's ids)."""
-        if len(buckets) == 0:
-            return np.zeros(0, np.int8)
-        lo, hi = self.ptr[buckets], self.ptr[buckets + 1]
-        seg = np.repeat(np.arange(len(buckets)), hi - lo)
-        pos = np.arange(int((hi - lo).sum())) - np.repeat(np.cumsum(hi - lo) - (hi - lo), hi - lo) + np.repeat(lo, hi - lo)
-        kd, ids = self.kind[pos], self.ids[pos]
-        if self.mode is MemoryMode.REUSE_SORTED:
-            kd = kd[np.lexsort((ids, seg))]
-        return np.ascontiguousarray(kd, dtype=np.int8)
+        return plan_kinds(self.ptr, self.ids, self.kind, buckets, self.mode is MemoryMode.REUSE_SORTED)
 
     def launch(self, combined, now: float) -> BatchRecord:
         members = [wr.buffer_indices for wr in combined.members]

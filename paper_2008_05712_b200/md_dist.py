@@ -80,14 +80,18 @@ class DistTransport:
         dist = self.dist
         left, right = neighbours(self.rank, self.k)
         dev, w = to_left.device, to_left.shape[1]
-        # counts first (tag 0: travelling left, tag 1: travelling right)
+        # NCCL ignores tags and matches a pair's messages in issue order, and with
+        # two slabs the left and right neighbour are the same rank: every rank
+        # issues [send left, send right, recv right, recv left], so a peer's
+        # k-th receive from us is our k-th send to it (tags kept for gloo).
+        # Counts first (tag 0: travelling left, tag 1: travelling right).
         sl = torch.tensor([to_left.shape[0]], dtype=torch.int64, device=dev)
         sr = torch.tensor([to_right.shape[0]], dtype=torch.int64, device=dev)
         rl, rr = torch.zeros_like(sl), torch.zeros_like(sr)
         ops = [dist.P2POp(dist.isend, sl, self._peer(left), self.group, 0),
                dist.P2POp(dist.isend, sr, self._peer(right), self.group, 1),
-               dist.P2POp(dist.irecv, rl, self._peer(left), self.group, 1),
-               dist.P2POp(dist.irecv, rr, self._peer(right), self.group, 0)]
+               dist.P2POp(dist.irecv, rr, self._peer(right), self.group, 0),
+               dist.P2POp(dist.irecv, rl, self._peer(left), self.group, 1)]
         for q in dist.batch_isend_irecv(ops):
             q.wait()
         fl = torch.empty((int(rl.item()), w), dtype=torch.float64, device=dev)
@@ -97,10 +101,10 @@ class DistTransport:
             ops.append(dist.P2POp(dist.isend, to_left.contiguous(), self._peer(left), self.group, 2))
         if to_right.shape[0]:
             ops.append(dist.P2POp(dist.isend, to_right.contiguous(), self._peer(right), self.group, 3))
-        if fl.shape[0]:
-            ops.append(dist.P2POp(dist.irecv, fl, self._peer(left), self.group, 3))
         if fr.shape[0]:
             ops.append(dist.P2POp(dist.irecv, fr, self._peer(right), self.group, 2))
+        if fl.shape[0]:
+            ops.append(dist.P2POp(dist.irecv, fl, self._peer(left), self.group, 3))
         if ops:
             for q in dist.batch_isend_irecv(ops):
                 q.wait()
