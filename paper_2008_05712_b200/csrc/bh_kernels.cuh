@@ -261,11 +261,10 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
                     sp = -1;
                     break;
                 }
-                if (lane == 0) {
-                    stack[sp] = make_int2(wr_first(wd) | ((wd & 7) << NODE_BITS), (int)(unsigned)open);
-                    sact[sp] = (unsigned)(open >> 32);
-                    slvl[sp] = (unsigned char)(lvl + 1);
-                }
+                // every lane stores the same (warp-uniform) entry: no divergent branch
+                stack[sp] = make_int2(wr_first(wd) | ((wd & 7) << NODE_BITS), (int)(unsigned)open);
+                sact[sp] = (unsigned)(open >> 32);
+                slvl[sp] = (unsigned char)(lvl + 1);
                 ++sp;
             }
             nd = nd_next;
