@@ -1,0 +1,120 @@
+"""Work-request stream capture and replay (mirrors hr/workloads/trace.py).
+
+A trace is line-delimited text, one work request per line
+(hr/workloads/trace.py:1-9, 22-62):
+
+    arrival_time kernel_class idx0,idx1,... item_count bytes_per_item
+
+with ``repr`` floats so a dump / parse round trip is exact.  Here a trace is
+also the fixture feed of the B200 batcher: a recorded BH
+force stream is replayed through the device executor (``replay_forces``) --
+trigger, device data manager, slot staging, member kernel -- without
+re-running the walk that produced it.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from .errors import TraceFormatError
+
+
+@dataclass(frozen=True)
+class TraceRecord:
+    arrival_time: float
+    kernel_class: str
+    buffer_indices: tuple
+    item_count: int
+    bytes_per_item: int
+
+    def to_line(self) -> str:
+        idx = ",".join(str(int(i)) for i in self.buffer_indices)
+        return f"{self.arrival_time!r} {self.kernel_class} {idx} {self.item_count} {self.bytes_per_item}"
+
+
+def dump_trace(records, path) -> None:
+    Path(path).write_text("".join(r.to_line() + "\n" for r in records))
+
+
+def parse_trace(path) -> list:
+    """hr/workloads/trace.py:43-62: 5 fields, >= 1 item and >= 1 buffer."""
+    records = []
+    for line_no, raw in enumerate(Path(path).read_text().splitlines(), start=1):
+        line = raw.strip()
+        if not line or line.startswith("#"):
+            continue
+        parts = line.split()
+        if len(parts) != 5:
+            raise TraceFormatError(line_no, f"expected 5 fields, got {len(parts)}")
+        try:
+            t = float(parts[0])
+            indices = tuple(int(x) for x in parts[2].split(","))
+            items = int(parts[3])
+            bpi = int(parts[4])
+        except ValueError as exc:
+            raise TraceFormatError(line_no, str(exc)) from None
+        if items < 1 or not indices:
+            raise TraceFormatError(line_no, "need at least one item and one buffer")
+        records.append(TraceRecord(t, parts[1], indices, items, bpi))
+    return records
+
+
+def trace_roundtrip(records, path) -> list:
+    """Dump, re-parse and diff (hr/workloads/trace.py:65-76); [] = faithful."""
+    dump_trace(records, path)
+    back = parse_trace(path)
+    problems = []
+    if len(back) != len(records):
+        problems.append(f"length {len(records)} -> {len(back)}")
+    for i, (a, b) in enumerate(zip(records, back)):
+        if a != b:
+            problems.append(f"line {i + 1}: {a} != {b}")
+    return problems
+
+
+def nbody_schedule(item_counts, seed: int = 42, pieces: int = 16, emit_cost: float = 1e-4,
+                   piece_gap: float = 4.0) -> list:
+    """Walk-ordered arrival times of the BH force requests (NBodyWorkload._schedule,
+    hr/workloads/nbody.py:285-301): dense inside a tree piece, lognormal lulls
+    between pieces."""
+    rng = np.random.default_rng(seed + 1)
+    n = len(item_counts)
+    per_piece = max(1, math.ceil(n / pieces))
+    times, t = [], 0.0
+    for i, ic in enumerate(item_counts):
+        if i > 0 and i % per_piece == 0:
+            t += piece_gap * float(rng.lognormal(mean=0.0, sigma=1.0))
+        t += emit_cost * max(1, int(ic))
+        times.append(t)
+    return times
+
+
+def nbody_stream(ptr, ids, item_count, seed: int = 42, pieces: int = 16, emit_cost: float = 1e-4,
+                 piece_gap: float = 4.0, bytes_per_item: int = 48) -> list:
+    """One "force" record per bucket (DFS order): buffers = its walk_order
+    (hr/workloads/trace.py:80-97 without the Ewald class)."""
+    times = nbody_schedule(item_count, seed, pieces, emit_cost, piece_gap)
+    return [TraceRecord(t, "force", tuple(int(x) for x in ids[ptr[b]:ptr[b + 1]]), int(item_count[b]),
+                        bytes_per_item) for b, t in enumerate(times)]
+
+
+def replay_forces(records, tree, lists, **executor_kw):
+    """Replay a recorded BH force stream on the device: the k-th "force" record
+    is bucket k's request (streams are emitted in DFS bucket order); its
+    buffers must equal that bucket's device-walk list.  Returns the executor's
+    RunResult (forces + per-batch log)."""
+    from .executor import GpuForceExecutor
+    force = [r for r in records if r.kernel_class == "force"]
+    ex = GpuForceExecutor(tree, lists, **executor_kw)
+    if len(force) != len(ex.ptr) - 1:
+        raise ValueError(f"trace has {len(force)} force records for {len(ex.ptr) - 1} buckets")
+    for b, r in enumerate(force):
+        if not np.array_equal(np.asarray(r.buffer_indices, np.int64), ex.ids[ex.ptr[b]:ex.ptr[b + 1]]):
+            raise ValueError(f"trace record {b} does not match bucket {b}'s interaction list")
+        if r.item_count != int(ex.item_count[b]):
+            raise ValueError(f"trace record {b}: item_count {r.item_count} != {int(ex.item_count[b])}")
+    return ex.run([r.arrival_time for r in force])
