@@ -573,8 +573,9 @@ __global__ void md_sortgather_kernel(int ncell, const int *__restrict__ cell_sta
     }
     const int v = lane < n ? perm[s + lane] : -1;
     const long long g = lane < n ? gid[v] : LLONG_MAX;
+    const int g32 = lane < n ? (int)g : INT_MAX;  // global ids < 2^31 (gc_md_set_slab / set_system)
     int rank = 0;
-    for (int k = 0; k < n; ++k) rank += __shfl_sync(0xffffffffu, g, k) < g;
+    for (int k = 0; k < n; ++k) rank += __shfl_sync(0xffffffffu, g32, k) < g32;
     __syncwarp();
     if (lane < n) {
         perm[s + rank] = v;
@@ -1049,7 +1050,10 @@ gc_status gc_md_set_slab(gc_md *md, int64_t gx0, int64_t gnx, const int64_t *gid
         cudaStream_t s = md->ctx->stream;
         if (gid) {
             std::vector<long long> g(md->n_owned);
-            for (int i = 0; i < md->n_owned; ++i) g[i] = gid[i];
+            for (int i = 0; i < md->n_owned; ++i) {
+                GC_REQUIRE(gid[i] >= 0 && gid[i] < INT_MAX, GC_E_VALUE, "global atom ids must be in [0, 2^31)");
+                g[i] = gid[i];
+            }
             md->gid.upload(g.data(), md->n_owned, s);
         }
         md->n = md->n_owned;
