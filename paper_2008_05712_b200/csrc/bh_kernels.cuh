@@ -451,7 +451,10 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-static __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK)
+#ifndef EXPAND_MINB
+#define EXPAND_MINB 4
+#endif
+static __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, EXPAND_MINB)
 expand_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U, const float4 *__restrict__ parts,
               const float4 *__restrict__ rec_hi, const float4 *__restrict__ rec_lo, float cgrid, const Staging S,
               int *__restrict__ flag)
