@@ -74,12 +74,12 @@ void upload_tree(gc_bh *bh)
     // walk groups: WG_BUCKETS consecutive buckets; force groups: <= 32 targets
     // of consecutive buckets inside one walk group
     bh->h_wg.clear();
-    bh->h_fg.clear();
+    std::vector<ForceGroup> h_fg;
     for (int64_t b0 = 0; b0 < nb; b0 += WG_BUCKETS) {
         WalkGroup wg;
         wg.bfirst = (int)b0;
         wg.nbucket = (int)std::min<int64_t>(WG_BUCKETS, nb - b0);
-        wg.fg_first = (int)bh->h_fg.size();
+        wg.fg_first = (int)h_fg.size();
         const int wi = (int)bh->h_wg.size();
         for (int64_t b = b0; b < b0 + wg.nbucket;) {
             ForceGroup fg;
@@ -94,9 +94,9 @@ void upload_tree(gc_bh *bh)
             GC_REQUIRE(tg > 0, GC_E_VALUE, "bucket with more than 32 particles (coincident points) on the group path");
             fg.ntarget = tg;
             fg.nb = (int)(b - b0) - fg.boff;
-            bh->h_fg.push_back(fg);
+            h_fg.push_back(fg);
         }
-        wg.nfg = (int)bh->h_fg.size() - wg.fg_first;
+        wg.nfg = (int)h_fg.size() - wg.fg_first;
         GC_REQUIRE(wg.nfg <= 32, GC_E_VALUE, "walk group with more than 32 force groups");
         bh->h_wg.push_back(wg);
     }
@@ -111,11 +111,12 @@ void upload_tree(gc_bh *bh)
     bh->d_bucket_ids.upload(bids.data(), nb, s);
     bh->d_part_bucket.upload(pb.data(), t.n, s);
     bh->d_wg.upload(bh->h_wg.data(), bh->h_wg.size(), s);
-    bh->d_fg.upload(bh->h_fg.data(), bh->h_fg.size(), s);
+    bh->d_fg.upload(h_fg.data(), h_fg.size(), s);
+    bh->n_fg = (int)h_fg.size();
     bh->h2d += nn * (int64_t)(3 * sizeof(float4) + sizeof(double4) + sizeof(int2)) +
                nb * (int64_t)(sizeof(double4) + sizeof(float4) + sizeof(int2) + sizeof(int)) +
                t.n * (int64_t)sizeof(int) + (int64_t)bh->h_wg.size() * (int64_t)sizeof(WalkGroup) +
-               (int64_t)bh->h_fg.size() * (int64_t)sizeof(ForceGroup);
+               (int64_t)h_fg.size() * (int64_t)sizeof(ForceGroup);
     GC_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -237,7 +238,7 @@ void walk_params(gc_bh *bh, double theta)
     bh->params_valid = true;
     bh->cap_theta = theta;
     bh->stats_valid = false;
-    bh->wg_order_valid = false;
+    bh->orders_fresh = false;
     bh->have_union = false;
 }
 
@@ -245,7 +246,7 @@ void walk_params(gc_bh *bh, double theta)
 void launch_walk(gc_bh *bh, bool write, bool stats)
 {
     cudaStream_t s = bh->ctx->stream;
-    const int nf = (int)bh->h_fg.size();
+    const int nf = bh->n_fg;
     const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? (int)bh->h_wg.size() : bh->rg1;
     const int ng = g1 - g0;
     const WalkGroup *wg = bh->d_wg.p + g0;
@@ -280,45 +281,66 @@ void launch_walk(gc_bh *bh, bool write, bool stats)
     bh->d_wnext.zero(s);
     k<<<pgrid, 32 * WARPS_PER_BLOCK, 0, s>>>(ng, wg, bh->d_fg.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p,
                                              bh->d_bgeo32.p, bh->wp, U, bh->d_bstat.p, bh->d_flag.p,
-                                             bh->wg_order_valid ? bh->d_wg_order.p : nullptr, bh->d_wnext.p);
+                                             (bh->order_ng == ng && bh->order_rg0 == g0) ? bh->d_wg_order.p : nullptr,
+                                             bh->d_wnext.p);
     check_launch("walk_group_kernel");
 }
 
-// Heaviest-first walk-group order from a completed walk's union lists (entries
-// per force group ~ nodes visited); reused by later walks of the same tree.
-void make_walk_order(gc_bh *bh)
+__global__ void bh_wg_work_kernel(int ng, const WalkGroup *__restrict__ wg, const int *__restrict__ gcount,
+                                  int *__restrict__ key, int *__restrict__ idx)
+{
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= ng) return;
+    int e = 0;
+    for (int f = wg[g].fg_first; f < wg[g].fg_first + wg[g].nfg; ++f) e += gcount[f];
+    key[g] = e;
+    idx[g] = g;
+}
+
+__global__ void bh_fg_key_kernel(int nf, const int *__restrict__ grec, int *__restrict__ key, int *__restrict__ idx)
+{
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= nf) return;
+    key[f] = grec[f];
+    idx[f] = f;
+}
+
+// Scheduling hints for the persistent walk and force kernels, computed on the
+// device (asynchronously) from a completed walk: walk groups heaviest first
+// (union entries ~ nodes visited), force groups longest staging run first.
+// Exact for later walks of the same tree; after a new tree of the same shape
+// (a time step) they are a stale but close hint -- order never changes results.
+void make_orders(gc_bh *bh)
 {
     cudaStream_t s = bh->ctx->stream;
     const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? (int)bh->h_wg.size() : bh->rg1;
-    const int ng = g1 - g0, nf = (int)bh->h_fg.size();
+    const int ng = g1 - g0, nf = bh->n_fg;
     if (ng <= 0) return;
-    std::vector<int> cnt(nf);
-    bh->d_gcount.download(cnt.data(), nf, s);
-    GC_CUDA(cudaStreamSynchronize(s));
-    std::vector<std::pair<int64_t, int>> w(ng);
-    for (int g = 0; g < ng; ++g) {
-        const WalkGroup &wg = bh->h_wg[g0 + g];
-        int64_t e = 0;
-        for (int f = wg.fg_first; f < wg.fg_first + wg.nfg; ++f) e += cnt[f];
-        w[g] = {-e, g};
-    }
-    std::stable_sort(w.begin(), w.end());
-    std::vector<int> order(ng);
-    for (int g = 0; g < ng; ++g) order[g] = w[g].second;
-    bh->d_wg_order.upload(order.data(), ng, s);
-    // force groups of the range, longest staging run first (force_group_kernel)
     const int f0 = bh->h_wg[g0].fg_first;
     const int f1 = g1 < (int)bh->h_wg.size() ? bh->h_wg[g1].fg_first : nf;
-    std::vector<int> rec(nf);
-    bh->d_grec.download(rec.data(), nf, s);
-    GC_CUDA(cudaStreamSynchronize(s));
-    std::vector<std::pair<int, int>> r(f1 - f0);
-    for (int f = f0; f < f1; ++f) r[f - f0] = {-rec[f], f - f0};
-    std::stable_sort(r.begin(), r.end());
-    std::vector<int> forder(f1 - f0);
-    for (size_t i = 0; i < r.size(); ++i) forder[i] = r[i].second;
-    bh->d_fg_lpt.upload(forder.data(), forder.size(), s);
-    bh->wg_order_valid = true;
+    const int nfr = f1 - f0;
+    auto &k0 = bh->d_okey, &k1 = bh->d_okey2, &i0 = bh->d_oidx;
+    const int m = std::max(ng, nfr);
+    k0.resize(m); k1.resize(m); i0.resize(m);
+    bh->d_wg_order.resize(ng);
+    bh->d_fg_lpt.resize(nfr);
+    bh_wg_work_kernel<<<grid_for(ng, 256), 256, 0, s>>>(ng, bh->d_wg.p + g0, bh->d_gcount.p, k0.p, i0.p);
+    size_t bytes = 0;
+    GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, k0.p, k1.p, i0.p, bh->d_wg_order.p, ng, 0, 32, s));
+    bh->ctx->scratch.resize(bytes);
+    GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(bh->ctx->scratch.p, bytes, k0.p, k1.p, i0.p, bh->d_wg_order.p, ng,
+                                                      0, 32, s));
+    bh_fg_key_kernel<<<grid_for(nfr, 256), 256, 0, s>>>(nfr, bh->d_grec.p + f0, k0.p, i0.p);
+    bytes = 0;
+    GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, k0.p, k1.p, i0.p, bh->d_fg_lpt.p, nfr, 0, 32, s));
+    bh->ctx->scratch.resize(bytes);
+    GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(bh->ctx->scratch.p, bytes, k0.p, k1.p, i0.p, bh->d_fg_lpt.p, nfr,
+                                                      0, 32, s));
+    check_launch("make_orders");
+    bh->order_ng = ng;
+    bh->order_nf = nfr;
+    bh->order_rg0 = g0;
+    bh->orders_fresh = true;
 }
 
 // Synchronise and surface walk failures.  A pool overflow grows the pool to
@@ -364,7 +386,6 @@ void run_walk(gc_bh *bh, double theta, bool want_stats)
         while (walk_overflowed(bh)) launch_walk(bh, true, true);
         bh->stats_valid = true;
         bh->stats_dirty = true;
-        make_walk_order(bh);
     }
 }
 
@@ -413,8 +434,8 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
     GC_CUDA(cudaEventRecord(bh->ev[2], s));
     if (bh->have_union) {
         const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? (int)bh->h_wg.size() : bh->rg1;
-        const int f0 = g0 < (int)bh->h_wg.size() ? bh->h_wg[g0].fg_first : (int)bh->h_fg.size();
-        const int f1 = g1 < (int)bh->h_wg.size() ? bh->h_wg[g1].fg_first : (int)bh->h_fg.size();
+        const int f0 = g0 < (int)bh->h_wg.size() ? bh->h_wg[g0].fg_first : bh->n_fg;
+        const int f1 = g1 < (int)bh->h_wg.size() ? bh->h_wg[g1].fg_first : bh->n_fg;
         const int nfg = f1 - f0;
         const unsigned grid = grid_for(std::max(nfg, 1), WARPS_PER_BLOCK);
         UnionPool U = pool_view(bh);
@@ -438,7 +459,7 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
         // depth-first order (sorting every step costs more than its tail saves)
         bh->d_next.resize(1);
         bh->d_next.zero(s);
-        const bool lpt = bh->wg_order_valid && (int64_t)bh->d_fg_lpt.n == nfg;
+        const bool lpt = bh->order_nf == nfg && bh->order_rg0 == g0;
         if (!lpt) {
             bh->d_fg_order.resize(nfg);
             if (nfg > 0) bb_iota_kernel<<<grid_for(nfg, 256), 256, 0, s>>>(nfg, bh->d_fg_order.p);
@@ -468,6 +489,7 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
                                                      g, bh->dim, bh->d_out.p, bh->d_pot.p);
             check_launch("force_group_kernel");
         }
+        if (!bh->orders_fresh) make_orders(bh);  // hints for the next walk / force launch
     } else if (bh->have_member_lists) {
         GC_REQUIRE(!pot, GC_E_STATE, "potentials need device lists (gc_bh_walk)");
         const int nb = (int)bh->n_buckets;
@@ -531,7 +553,7 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
         bh->params_valid = false;
         bh->stats_valid = false;
         bh->stats_dirty = false;
-        bh->wg_order_valid = false;
+        bh->orders_fresh = false;
         bh->rg0 = 0;
         bh->rg1 = -1;
         if (!bh->device_build) {
@@ -628,7 +650,7 @@ gc_status gc_bh_get_lists(gc_bh *bh, int64_t *ptr, int64_t *ids, int8_t *kind, i
             for (int64_t b = 0; b < nb; ++b) item_count[b] = st[2 * b + 1];
         if (ids || kind) {
             GC_REQUIRE(tot < (1ll << 31), GC_E_VALUE, "more than 2^31 list entries");
-            const int nf = (int)bh->h_fg.size();
+            const int nf = bh->n_fg;
             // preorder (depth-first, children in octant order) index of every node
             ensure_host_tree(bh);
             const HostTree &t = bh->tree;
@@ -766,7 +788,7 @@ gc_status gc_bh_set_range(gc_bh *bh, int64_t wg_begin, int64_t wg_end)
         bh->rg1 = (int)wg_end;
         bh->have_union = false;
         bh->stats_valid = false;  // stats cover the walked range
-        bh->wg_order_valid = false;
+        bh->orders_fresh = false;
     });
 }
 

@@ -95,19 +95,70 @@ __global__ void bb_gather_u64(int n, const int *__restrict__ perm, const unsigne
     if (i < n) dst[i] = src[perm[i]];
 }
 
-// positions that start a child of a splitting node at level L
-__global__ void bb_child_flags(int n, int L, const int *__restrict__ posnode, const unsigned char *__restrict__ split,
-                               const int *__restrict__ lstart, const unsigned long long *__restrict__ k1,
-                               const unsigned long long *__restrict__ k2, unsigned char *__restrict__ flag)
+
+// children of the splitting nodes of level L, per node: within a node's
+// position range the level-L digit is sorted, so child q starts at the lower
+// bound of q (8 binary searches per node instead of per-position passes)
+__device__ __forceinline__ int digit_lower_bound(int lo, int hi, int q, int L, const unsigned long long *__restrict__ k1,
+                                                 const unsigned long long *__restrict__ k2)
 {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int p = posnode[i];
-    unsigned char f = 0;
-    if (p >= 0 && split[p]) {
-        f = i == lstart[p] || key_digit(k1[i], k2[i], L) != key_digit(k1[i - 1], k2[i - 1], L);
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (key_digit(k1[mid], k2[mid], L) < q) lo = mid + 1;
+        else hi = mid;
     }
-    flag[i] = f;
+    return lo;
+}
+
+__global__ void bb_count_children(int m, int L, int nq, const unsigned char *__restrict__ split,
+                                  const int *__restrict__ lstart, const int *__restrict__ lcount,
+                                  const unsigned long long *__restrict__ k1, const unsigned long long *__restrict__ k2,
+                                  int *__restrict__ cpos, int *__restrict__ ccnt)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= m) return;
+    int nonempty = 0;
+    if (split[p]) {
+        const int s = lstart[p], e = s + lcount[p];
+        int lo = s;
+        for (int q = 0; q < nq; ++q) {
+            const int next = q + 1 < nq ? digit_lower_bound(lo, e, q + 1, L, k1, k2) : e;
+            cpos[9 * p + q] = lo;
+            nonempty += next > lo ? 1 : 0;
+            lo = next;
+        }
+        cpos[9 * p + nq] = e;
+    }
+    ccnt[p] = nonempty;
+}
+
+__global__ void bb_make_children(int m, int nq, int next_id, const unsigned char *__restrict__ split,
+                                 const int *__restrict__ lid, const double4 *__restrict__ lcenter, int dim,
+                                 const int *__restrict__ cpos, const int *__restrict__ cbase, int *__restrict__ cstart,
+                                 int *__restrict__ ccount, double4 *__restrict__ ccenter, int *__restrict__ first_child,
+                                 int *__restrict__ nchild)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= m || !split[p]) return;
+    const double4 pc = lcenter[p];
+    const double ch = pc.w * 0.5;  // == pc.w / 2 exactly
+    int c = cbase[p];
+    const int c0 = c;
+    for (int q = 0; q < nq; ++q) {
+        const int a = cpos[9 * p + q], b = cpos[9 * p + q + 1];
+        if (b <= a) continue;
+        cstart[c] = a;
+        ccount[c] = b - a;
+        double4 cc;
+        cc.x = dim > 0 ? __dadd_rn(pc.x, (q & 1) ? ch : -ch) : pc.x;
+        cc.y = dim > 1 ? __dadd_rn(pc.y, (q & 2) ? ch : -ch) : pc.y;
+        cc.z = dim > 2 ? __dadd_rn(pc.z, (q & 4) ? ch : -ch) : pc.z;
+        cc.w = ch;
+        ccenter[c] = cc;
+        ++c;
+    }
+    first_child[lid[p]] = next_id + c0;
+    nchild[lid[p]] = c - c0;
 }
 
 __global__ void bb_level_split(int m, const int *__restrict__ lcount, double half, long long bucket,
@@ -117,54 +168,7 @@ __global__ void bb_level_split(int m, const int *__restrict__ lcount, double hal
     if (p < m) split[p] = lcount[p] > bucket && half >= 1e-9;
 }
 
-// children of level L: counts, centres, global ids and parent links
-__global__ void bb_children(int mc, int L, int next_id, const int *__restrict__ cstart, const int *__restrict__ posnode,
-                            const int *__restrict__ lstart, const int *__restrict__ lcount, const int *__restrict__ lid,
-                            const double4 *__restrict__ lcenter, int dim, const unsigned long long *__restrict__ k1,
-                            const unsigned long long *__restrict__ k2, int *__restrict__ ccount,
-                            double4 *__restrict__ ccenter, int *__restrict__ first_child, int *__restrict__ nchild)
-{
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= mc) return;
-    const int i = cstart[c];
-    const int p = posnode[i];
-    const int pend = lstart[p] + lcount[p];
-    const int nxt = c + 1 < mc ? cstart[c + 1] : pend;
-    const int end = nxt < pend ? nxt : pend;
-    ccount[c] = end - i;
-    const int q = key_digit(k1[i], k2[i], L);
-    const double4 pc = lcenter[p];
-    const double ch = pc.w * 0.5;  // == pc.w / 2 exactly
-    double4 cc;
-    cc.x = dim > 0 ? __dadd_rn(pc.x, (q & 1) ? ch : -ch) : pc.x;
-    cc.y = dim > 1 ? __dadd_rn(pc.y, (q & 2) ? ch : -ch) : pc.y;
-    cc.z = dim > 2 ? __dadd_rn(pc.z, (q & 4) ? ch : -ch) : pc.z;
-    cc.w = ch;
-    ccenter[c] = cc;
-    if (i == lstart[p]) first_child[lid[p]] = next_id + c;
-    atomicAdd(&nchild[lid[p]], 1);
-}
 
-// level-local node of every position after the split (-1: finished in a bucket)
-__global__ void bb_posnode(int n, int *__restrict__ posnode, const unsigned char *__restrict__ split, int mc,
-                           const int *__restrict__ cstart)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int p = posnode[i];
-    if (p < 0) return;
-    if (!split[p]) {
-        posnode[i] = -1;
-        return;
-    }
-    int lo = 0, hi = mc;  // last child start <= i
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (cstart[mid] <= i) lo = mid;
-        else hi = mid;
-    }
-    posnode[i] = lo;
-}
 
 // record the level's nodes in the global arrays; non-splitting ones are buckets
 __global__ void bb_store_level(int m, int id0, const int *__restrict__ lstart, const int *__restrict__ lcount,
@@ -320,37 +324,60 @@ __global__ void bb_buckets(int nb, int dim, const int *__restrict__ buckets, con
 
 // walk groups of 32 buckets; force groups greedily packed (<= 32 targets)
 // inside each walk group, as the host path: pass 0 counts, pass 1 writes
+// Walk / force groups, one warp per walk group: lanes load the group's bucket
+// ranges, the greedy force-group cuts (<= 32 targets of consecutive buckets)
+// are made from registers via shuffles (PASS 0 counts, PASS 1 writes).
 template <int PASS>
 __global__ void bb_groups(int nwg, int nb, const int2 *__restrict__ brange, int *__restrict__ nfg_of,
                           const int *__restrict__ fg_base, WalkGroup *__restrict__ wg, ForceGroup *__restrict__ fg,
                           int *__restrict__ bad)
 {
-    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     if (w >= nwg) return;
     const int b0 = w * WG_BUCKETS, b1 = min(nb, b0 + WG_BUCKETS);
-    int k = 0;
-    for (int b = b0; b < b1;) {
-        ForceGroup g;
-        g.pstart = brange[b].x;
-        g.wg = w;
-        g.boff = b - b0;
-        int tg = 0;
-        while (b < b1 && tg + brange[b].y <= 32) {
-            tg += brange[b].y;
-            ++b;
+    int2 r[BPL];
+#pragma unroll
+    for (int k = 0; k < BPL; ++k) r[k] = b0 + lane + 32 * k < b1 ? brange[b0 + lane + 32 * k] : make_int2(0, 0);
+    int k = 0, start = 0, tg = 0, ps = 0;
+    bool ok = true;
+    for (int j = 0; j <= b1 - b0; ++j) {
+        int cnt = 0, pst = 0;
+        if (j < b1 - b0) {
+            const int2 v = j < 32 ? make_int2(__shfl_sync(0xffffffffu, r[0].x, j), __shfl_sync(0xffffffffu, r[0].y, j))
+                                  : make_int2(__shfl_sync(0xffffffffu, r[1].x, j - 32),
+                                              __shfl_sync(0xffffffffu, r[1].y, j - 32));
+            cnt = v.y;
+            pst = v.x;
         }
-        if (tg == 0) {
-            atomicOr(bad, 1);
-            return;
+        // close the current group before bucket j if it would exceed 32 targets (or at the end)
+        if (j == b1 - b0 || (j > start && tg + cnt > 32)) {
+            if (tg == 0) ok = false;
+            if (PASS == 1 && lane == 0) {
+                ForceGroup g;
+                g.pstart = ps;
+                g.ntarget = tg;
+                g.wg = w;
+                g.boff = start;
+                g.nb = j - start;
+                fg[fg_base[w] + k] = g;
+            }
+            ++k;
+            start = j;
+            tg = 0;
         }
-        g.ntarget = tg;
-        g.nb = b - b0 - g.boff;
-        if (PASS == 1) fg[fg_base[w] + k] = g;
-        ++k;
+        if (j < b1 - b0) {
+            if (tg == 0) ps = pst;
+            tg += cnt;
+            if (cnt > 32) ok = false;
+        }
     }
-    if (k > 32) atomicOr(bad, 2);
-    if (PASS == 0) nfg_of[w] = k;
-    else wg[w] = WalkGroup{b0, b1 - b0, fg_base[w], k};
+    if (lane == 0) {
+        if (!ok) atomicOr(bad, 1);
+        if (k > 32) atomicOr(bad, 2);
+        if (PASS == 0) nfg_of[w] = k;
+        else wg[w] = WalkGroup{b0, b1 - b0, fg_base[w], k};
+    }
 }
 
 template <class F>
@@ -431,15 +458,12 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     auto &lid = bh->ws.lid;
     auto &cstart = bh->ws.cstart;
     auto &ccount = bh->ws.ccount;
-    auto &posnode = bh->ws.posnode;
-    auto &nsel = bh->ws.nsel;
     auto &leaf_key = bh->ws.leaf_key;
     auto &leaf_id = bh->ws.leaf_id;
     auto &nleaf = bh->ws.nleaf;
     auto &lcenter = bh->ws.lcenter;
     auto &ccenter = bh->ws.ccenter;
     auto &split = bh->ws.split;
-    auto &flag = bh->ws.flag;
     const int cap_nodes = 3 * n + 1024;
     bh->d_ncenter.resize(cap_nodes);
     bh->d_pstart.resize(cap_nodes);
@@ -452,11 +476,9 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     leaf_id.resize(n + 1);
     nleaf.resize(1);
     nleaf.zero(s);
-    posnode.resize(n);
-    GC_CUDA(cudaMemsetAsync(posnode.p, 0, sizeof(int) * n, s));
-    flag.resize(n);
-    cstart.resize(n);
-    nsel.resize(1);
+    auto &cpos = bh->ws.cpos;
+    auto &cnt = bh->ws.ccnt;
+    auto &cbase = bh->ws.cbase;
     // level 0: the root
     {
         int z = 0;
@@ -475,33 +497,32 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
                                                               split.p, bh->d_ncenter.p, bh->d_pstart.p,
                                                               bh->d_pcount.p, leaf_key.p, leaf_id.p, nleaf.p);
         if (L >= nlev) break;  // no node of this level can split (half < 1e-9)
-        bb_child_flags<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, L, posnode.p, split.p, lstart.p, k1s.p, k2s.p,
-                                                               flag.p);
+        const int nq = 1 << dim;
+        cpos.resize((size_t)9 * m + 9);  // nq + 1 boundaries per node
+        cnt.resize(m + 1);
+        cbase.resize(m + 1);
+        bb_count_children<<<grid_for(m, BB_TPB), BB_TPB, 0, s>>>(m, L, nq, split.p, lstart.p, lcount.p, k1s.p, k2s.p,
+                                                                 cpos.p, cnt.p);
+        GC_CUDA(cudaMemsetAsync(cnt.p + m, 0, sizeof(int), s));
+        cubc(ctx, [&](void *t, size_t &b) { return cub::DeviceScan::ExclusiveSum(t, b, cnt.p, cbase.p, m + 1, s); });
         check_launch("bb level");
-        {
-            auto it = cub::CountingInputIterator<int>(0);
-            cubc(ctx, [&](void *t, size_t &b) {
-                return cub::DeviceSelect::Flagged(t, b, it, flag.p, cstart.p, nsel.p, n, s);
-            });
-        }
         int mc = 0;
-        GC_CUDA(cudaMemcpyAsync(&mc, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        GC_CUDA(cudaMemcpyAsync(&mc, cbase.p + m, sizeof(int), cudaMemcpyDeviceToHost, s));
         GC_CUDA(cudaStreamSynchronize(s));
         if (mc == 0) break;
         GC_REQUIRE(next_id + mc <= cap_nodes, GC_E_VALUE, "node capacity exceeded");
+        cstart.resize(mc);
         ccount.resize(mc);
         ccenter.resize(mc);
-        bb_children<<<grid_for(mc, BB_TPB), BB_TPB, 0, s>>>(mc, L, next_id, cstart.p, posnode.p, lstart.p, lcount.p,
-                                                            lid.p, lcenter.p, dim, k1s.p, k2s.p, ccount.p, ccenter.p,
-                                                            bh->d_first_child.p, bh->d_nchild.p);
-        bb_posnode<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, posnode.p, split.p, mc, cstart.p);
+        bb_make_children<<<grid_for(m, BB_TPB), BB_TPB, 0, s>>>(m, nq, next_id, split.p, lid.p, lcenter.p, dim, cpos.p,
+                                                                cbase.p, cstart.p, ccount.p, ccenter.p,
+                                                                bh->d_first_child.p, bh->d_nchild.p);
         check_launch("bb children");
         // the children become the next level
         lvl_first.push_back(next_id);
         std::swap(lstart.p, cstart.p);
         std::swap(lstart.n, cstart.n);
         std::swap(lstart.cap, cstart.cap);
-        cstart.resize(n);
         std::swap(lcount.p, ccount.p);
         std::swap(lcount.n, ccount.n);
         std::swap(lcount.cap, ccount.cap);
@@ -592,7 +613,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     fg_base.resize(nwg + 1);
     bad.resize(1);
     bad.zero(s);
-    bb_groups<0><<<grid_for(nwg, BB_TPB), BB_TPB, 0, s>>>(nwg, nb, bh->d_brange.p, nfg_of.p, nullptr, nullptr,
+    bb_groups<0><<<grid_for(nwg, BB_TPB / 32), BB_TPB, 0, s>>>(nwg, nb, bh->d_brange.p, nfg_of.p, nullptr, nullptr,
                                                           nullptr, bad.p);
     GC_CUDA(cudaMemsetAsync(nfg_of.p + nwg, 0, sizeof(int), s));
     cubc(ctx, [&](void *t, size_t &b) {
@@ -608,15 +629,14 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     GC_REQUIRE(!(badh & 2), GC_E_VALUE, "walk group with more than 32 force groups");
     bh->d_wg.resize(nwg);
     bh->d_fg.resize(nfg);
-    bb_groups<1><<<grid_for(nwg, BB_TPB), BB_TPB, 0, s>>>(nwg, nb, bh->d_brange.p, nullptr, fg_base.p, bh->d_wg.p,
+    bb_groups<1><<<grid_for(nwg, BB_TPB / 32), BB_TPB, 0, s>>>(nwg, nb, bh->d_brange.p, nullptr, fg_base.p, bh->d_wg.p,
                                                           bh->d_fg.p, bad.p);
     check_launch("bb groups");
     bh->h_wg.resize(nwg);
-    bh->h_fg.resize(nfg);
+    bh->n_fg = nfg;
     bh->d_wg.download(bh->h_wg.data(), nwg, s);
-    bh->d_fg.download(bh->h_fg.data(), nfg, s);
     GC_CUDA(cudaStreamSynchronize(s));
-    bh->d2h += (int64_t)nwg * sizeof(WalkGroup) + (int64_t)nfg * sizeof(ForceGroup);
+    bh->d2h += (int64_t)nwg * sizeof(WalkGroup);
     set_tree_bounds(bh, cm);
     bh->n = n;
     bh->dim = dim;

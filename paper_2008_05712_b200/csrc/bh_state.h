@@ -11,11 +11,11 @@
 using namespace gc;
 
 struct BuildWs {  // device-build scratch, kept across builds (no per-step cudaMalloc/cudaFree)
-    DBuf<int> nsel2;
+    DBuf<int> nsel2, cpos, ccnt, cbase;
     DBuf<double> pos, mass, scratch;
     DBuf<unsigned long long> k1, k2, k1p, k1s, k2s;
     DBuf<int> idx, perm1, perm;
-    DBuf<int> lstart, lcount, lid, cstart, ccount, posnode, nsel, leaf_key, leaf_id, nleaf;
+    DBuf<int> lstart, lcount, lid, cstart, ccount, leaf_key, leaf_id, nleaf;
     DBuf<double4> lcenter, ccenter;
     DBuf<unsigned char> split, flag;
     DBuf<int> lk_s;
@@ -40,7 +40,7 @@ struct gc_bh {
     DBuf<double> d_nmass;
     DBuf<int> d_first_child, d_nchild, d_pstart, d_pcount, d_buckets;
     std::vector<WalkGroup> h_wg;
-    std::vector<ForceGroup> h_fg;
+    int n_fg = 0;  // force groups (device array d_fg)
     // device tree
     DBuf<float4> d_recs;  // walk records: float32 com + packed links
     DBuf<double4> d_com64;  // float64 com (exact opening test)
@@ -70,8 +70,11 @@ struct gc_bh {
     DBuf<float4> d_srec;
     DBuf<unsigned> d_smask;
     DBuf<int> d_fg_order, d_next;
-    DBuf<int> d_wg_order, d_wnext, d_fg_lpt;  // walk: heaviest-first group order (valid for this tree / theta / range)
-    bool wg_order_valid = false;
+    // scheduling hints (make_orders): heaviest-first walk groups, longest-run-first
+    // force groups of the last completed walk; used while the sizes match
+    DBuf<int> d_wg_order, d_wnext, d_fg_lpt, d_okey, d_okey2, d_oidx;
+    int order_ng = -1, order_nf = -1, order_rg0 = -1;
+    bool orders_fresh = false;
     int64_t staging_cap = 0;
     DBuf<int4> d_ent;
     int pool_chunks = 0;
