@@ -8,16 +8,18 @@
 //  2. One stable radix sort by (key, original id): every node of the
 //     reference is a contiguous range of this order, its children are the
 //     sub-ranges of equal next digit in ascending digit (= octant) order.
-//  3. Level-synchronous expansion: at each level the splitting nodes
-//     (count > bucket_size and half >= 1e-9) are cut where the level digit
-//     changes; children are numbered in position order, which is the
-//     reference's breadth-first id order.  Non-splitting nodes are buckets.
+//  3. Level-synchronous expansion in ONE cooperative launch: at each level a
+//     splitting node (count > bucket_size and half >= 1e-9) is cut by 8 binary
+//     searches of its sorted level digit; a grid-wide scan numbers the
+//     children in position order, which is the reference's breadth-first id
+//     order.  Non-splitting nodes are buckets.
 //  4. Buckets sorted by position = depth-first order; each bucket's particles
 //     re-sorted by original id (the reference keeps ascending particle_idx).
 //  5. Masses/centres of mass with the reference's float64 rounding sequence:
 //     bucket mass = numpy pairwise sum, COM = sequential column sum / mass;
 //     internal nodes add children in order, deepest level first.
 //  6. Force/walk records, bucket geometry and walk/force groups in HBM.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -82,11 +84,6 @@ __global__ void bb_fill(int n, int *p, int v)
     if (i < n) p[i] = v;
 }
 
-__global__ void bb_iota(int n, int v0, int *p)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) p[i] = v0 + i;
-}
 
 __global__ void bb_gather_u64(int n, const int *__restrict__ perm, const unsigned long long *__restrict__ src,
                               unsigned long long *__restrict__ dst)
@@ -110,84 +107,168 @@ __device__ __forceinline__ int digit_lower_bound(int lo, int hi, int q, int L, c
     return lo;
 }
 
-__global__ void bb_count_children(int m, int L, int nq, const unsigned char *__restrict__ split,
-                                  const int *__restrict__ lstart, const int *__restrict__ lcount,
-                                  const unsigned long long *__restrict__ k1, const unsigned long long *__restrict__ k2,
-                                  int *__restrict__ cpos, int *__restrict__ ccnt)
+
+
+// ---------------------------------------------------------------------------
+// All levels of the expansion in ONE cooperative launch (grid-wide syncs
+// replace a host round trip per level).  Per level: store the level's nodes
+// (buckets = non-splitting), count each splitting node's children by digit
+// lower bounds, grid-wide exclusive scan of the counts, emit the children as
+// the next level (level-order ids = position order, children in octant order).
+// ---------------------------------------------------------------------------
+struct LevelArgs {
+    int n, dim, nlev, cap_nodes;
+    long long bucket;
+    double box;
+    const unsigned long long *k1, *k2;
+    int *start[2], *count[2];
+    double4 *center[2];
+    int *cpos, *cnt, *cbase, *bsum;
+    double4 *ncenter;
+    int *pstart, *pcount, *first_child, *nchild;
+    int *leaf_key, *leaf_id, *nleaf;
+    int *lvl_first, *nlevels, *overflow;
+};
+
+__device__ __forceinline__ int block_sum(int v, int *red)
 {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= m) return;
-    int nonempty = 0;
-    if (split[p]) {
-        const int s = lstart[p], e = s + lcount[p];
-        int lo = s;
-        for (int q = 0; q < nq; ++q) {
-            const int next = q + 1 < nq ? digit_lower_bound(lo, e, q + 1, L, k1, k2) : e;
-            cpos[9 * p + q] = lo;
-            nonempty += next > lo ? 1 : 0;
-            lo = next;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    int t = 0;
+    for (int w = 0; w < nw; ++w) t += red[w];
+    __syncthreads();
+    return t;
+}
+
+__global__ void __launch_bounds__(BB_TPB) bb_levels_coop(LevelArgs A)
+{
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int red[BB_TPB / 32];
+    __shared__ int wsum[BB_TPB / 32];
+    const int T = (int)grid.size(), tid = (int)grid.thread_rank();
+    const int nb = (int)gridDim.x, b = (int)blockIdx.x;
+    const int nq = 1 << A.dim;
+    int m = 1, id0 = 0, cur = 0, L = 0;
+    double half = A.box * 0.5;
+    for (;; ++L) {
+        if (tid == 0) A.lvl_first[L] = id0;
+        // 1: store this level, count the children of splitting nodes
+        for (int p = tid; p < m; p += T) {
+            const int st = A.start[cur][p], ct = A.count[cur][p];
+            const bool sp = ct > A.bucket && half >= 1e-9;  // nbody.py:94
+            const int id = id0 + p;
+            A.ncenter[id] = A.center[cur][p];
+            A.pstart[id] = st;
+            A.pcount[id] = sp ? 0 : ct;
+            if (!sp) {
+                const int k = atomicAdd(A.nleaf, 1);
+                A.leaf_key[k] = st;
+                A.leaf_id[k] = id;
+            }
+            int nonempty = 0;
+            if (sp && L < A.nlev) {
+                const int e = st + ct;
+                int lo = st;
+                for (int q = 0; q < nq; ++q) {
+                    const int next = q + 1 < nq ? digit_lower_bound(lo, e, q + 1, L, A.k1, A.k2) : e;
+                    A.cpos[9 * p + q] = lo;
+                    nonempty += next > lo ? 1 : 0;
+                    lo = next;
+                }
+                A.cpos[9 * p + nq] = e;
+            }
+            A.cnt[p] = nonempty;
         }
-        cpos[9 * p + nq] = e;
+        if (L >= A.nlev) break;  // no node of this level can split (half < 1e-9)
+        grid.sync();
+        // 2: grid-wide exclusive scan of cnt[0, m) in per-block chunks
+        const int chunk = (m + nb - 1) / nb;
+        const int c0 = min(m, b * chunk), c1 = min(m, c0 + chunk);
+        int local = 0;
+        for (int p = c0 + (int)threadIdx.x; p < c1; p += blockDim.x) local += A.cnt[p];
+        const int bs = block_sum(local, red);
+        if (threadIdx.x == 0) A.bsum[b] = bs;
+        grid.sync();
+        int off = 0, mc = 0;
+        for (int k = (int)threadIdx.x; k < nb; k += blockDim.x) {
+            const int v = A.bsum[k];
+            mc += v;
+            off += k < b ? v : 0;
+        }
+        off = block_sum(off, red);
+        mc = block_sum(mc, red);
+        for (int t0 = c0; t0 < c1; t0 += blockDim.x) {  // block-wide scan of the chunk, tile by tile
+            const int p = t0 + (int)threadIdx.x;
+            const int v = p < c1 ? A.cnt[p] : 0;
+            int incl = v;
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            if (lane == 31) wsum[warp] = incl;
+            __syncthreads();
+            int wo = 0, tile = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+                wo += w < warp ? wsum[w] : 0;
+                tile += wsum[w];
+            }
+            if (p < c1) A.cbase[p] = off + wo + incl - v;
+            off += tile;
+            __syncthreads();
+        }
+        if (mc == 0) break;
+        if (id0 + m + mc > A.cap_nodes) {
+            if (tid == 0) *A.overflow = 1;
+            break;
+        }
+        grid.sync();
+        // 3: the children become level L + 1
+        const int nxt = cur ^ 1;
+        for (int p = tid; p < m; p += T) {
+            const int ct = A.count[cur][p];
+            if (!(ct > A.bucket && half >= 1e-9)) continue;
+            const double4 pc = A.center[cur][p];
+            const double ch = pc.w * 0.5;  // == pc.w / 2 exactly
+            int c = A.cbase[p];
+            const int cfirst = c;
+            for (int q = 0; q < nq; ++q) {
+                const int a = A.cpos[9 * p + q], e = A.cpos[9 * p + q + 1];
+                if (e <= a) continue;
+                A.start[nxt][c] = a;
+                A.count[nxt][c] = e - a;
+                double4 cc;
+                cc.x = A.dim > 0 ? __dadd_rn(pc.x, (q & 1) ? ch : -ch) : pc.x;
+                cc.y = A.dim > 1 ? __dadd_rn(pc.y, (q & 2) ? ch : -ch) : pc.y;
+                cc.z = A.dim > 2 ? __dadd_rn(pc.z, (q & 4) ? ch : -ch) : pc.z;
+                cc.w = ch;
+                A.center[nxt][c] = cc;
+                ++c;
+            }
+            A.first_child[id0 + p] = id0 + m + cfirst;
+            A.nchild[id0 + p] = c - cfirst;
+        }
+        grid.sync();
+        id0 += m;
+        m = mc;
+        cur = nxt;
+        half *= 0.5;
     }
-    ccnt[p] = nonempty;
-}
-
-__global__ void bb_make_children(int m, int nq, int next_id, const unsigned char *__restrict__ split,
-                                 const int *__restrict__ lid, const double4 *__restrict__ lcenter, int dim,
-                                 const int *__restrict__ cpos, const int *__restrict__ cbase, int *__restrict__ cstart,
-                                 int *__restrict__ ccount, double4 *__restrict__ ccenter, int *__restrict__ first_child,
-                                 int *__restrict__ nchild)
-{
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= m || !split[p]) return;
-    const double4 pc = lcenter[p];
-    const double ch = pc.w * 0.5;  // == pc.w / 2 exactly
-    int c = cbase[p];
-    const int c0 = c;
-    for (int q = 0; q < nq; ++q) {
-        const int a = cpos[9 * p + q], b = cpos[9 * p + q + 1];
-        if (b <= a) continue;
-        cstart[c] = a;
-        ccount[c] = b - a;
-        double4 cc;
-        cc.x = dim > 0 ? __dadd_rn(pc.x, (q & 1) ? ch : -ch) : pc.x;
-        cc.y = dim > 1 ? __dadd_rn(pc.y, (q & 2) ? ch : -ch) : pc.y;
-        cc.z = dim > 2 ? __dadd_rn(pc.z, (q & 4) ? ch : -ch) : pc.z;
-        cc.w = ch;
-        ccenter[c] = cc;
-        ++c;
-    }
-    first_child[lid[p]] = next_id + c0;
-    nchild[lid[p]] = c - c0;
-}
-
-__global__ void bb_level_split(int m, const int *__restrict__ lcount, double half, long long bucket,
-                               unsigned char *__restrict__ split)
-{
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < m) split[p] = lcount[p] > bucket && half >= 1e-9;
-}
-
-
-
-// record the level's nodes in the global arrays; non-splitting ones are buckets
-__global__ void bb_store_level(int m, int id0, const int *__restrict__ lstart, const int *__restrict__ lcount,
-                               const double4 *__restrict__ lcenter, const unsigned char *__restrict__ split,
-                               double4 *__restrict__ ncenter, int *__restrict__ pstart, int *__restrict__ pcount,
-                               int *__restrict__ leaf_key, int *__restrict__ leaf_id, int *__restrict__ nleaf)
-{
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= m) return;
-    const int id = id0 + p;
-    ncenter[id] = lcenter[p];
-    pstart[id] = lstart[p];
-    pcount[id] = split[p] ? 0 : lcount[p];
-    if (!split[p]) {
-        const int k = atomicAdd(nleaf, 1);
-        leaf_key[k] = lstart[p];
-        leaf_id[k] = id;
+    if (tid == 0) {
+        A.lvl_first[L + 1] = id0 + m;
+        *A.nlevels = L + 1;
     }
 }
+
+
+
+
 
 // numpy pairwise summation (np.sum of a 1-D float64 array)
 __device__ double np_pairwise(const double *a, int n)
@@ -452,10 +533,8 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     check_launch("bb sort");
 
     // level-synchronous expansion
-    std::vector<int> lvl_first{0};
     auto &lstart = bh->ws.lstart;
     auto &lcount = bh->ws.lcount;
-    auto &lid = bh->ws.lid;
     auto &cstart = bh->ws.cstart;
     auto &ccount = bh->ws.ccount;
     auto &leaf_key = bh->ws.leaf_key;
@@ -463,7 +542,6 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     auto &nleaf = bh->ws.nleaf;
     auto &lcenter = bh->ws.lcenter;
     auto &ccenter = bh->ws.ccenter;
-    auto &split = bh->ws.split;
     const int cap_nodes = 3 * n + 1024;
     bh->d_ncenter.resize(cap_nodes);
     bh->d_pstart.resize(cap_nodes);
@@ -479,63 +557,74 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     auto &cpos = bh->ws.cpos;
     auto &cnt = bh->ws.ccnt;
     auto &cbase = bh->ws.cbase;
-    // level 0: the root
+    // level arrays (ping-pong, <= n nodes per level), the root as level 0
+    lstart.resize(n);
+    lcount.resize(n);
+    lcenter.resize(n);
+    cstart.resize(n);
+    ccount.resize(n);
+    ccenter.resize(n);
+    cpos.resize((size_t)9 * n + 9);
+    cnt.resize(n + 1);
+    cbase.resize(n + 1);
     {
         int z = 0;
-        lstart.upload(&z, 1, s);
-        lcount.upload(&n, 1, s);
-        lid.upload(&z, 1, s);
+        GC_CUDA(cudaMemcpyAsync(lstart.p, &z, sizeof(int), cudaMemcpyHostToDevice, s));
+        GC_CUDA(cudaMemcpyAsync(lcount.p, &n, sizeof(int), cudaMemcpyHostToDevice, s));
         const double4 root = make_double4(box / 2.0, dim > 1 ? box / 2.0 : 0.0, dim > 2 ? box / 2.0 : 0.0, box / 2.0);
-        lcenter.upload(&root, 1, s);
+        GC_CUDA(cudaMemcpyAsync(lcenter.p, &root, sizeof(double4), cudaMemcpyHostToDevice, s));
     }
-    int m = 1, next_id = 1;
-    double half = box / 2.0;
-    for (int L = 0;; ++L) {
-        split.resize(m);
-        bb_level_split<<<grid_for(m, BB_TPB), BB_TPB, 0, s>>>(m, lcount.p, half, bucket, split.p);
-        bb_store_level<<<grid_for(m, BB_TPB), BB_TPB, 0, s>>>(m, lvl_first.back(), lstart.p, lcount.p, lcenter.p,
-                                                              split.p, bh->d_ncenter.p, bh->d_pstart.p,
-                                                              bh->d_pcount.p, leaf_key.p, leaf_id.p, nleaf.p);
-        if (L >= nlev) break;  // no node of this level can split (half < 1e-9)
-        const int nq = 1 << dim;
-        cpos.resize((size_t)9 * m + 9);  // nq + 1 boundaries per node
-        cnt.resize(m + 1);
-        cbase.resize(m + 1);
-        bb_count_children<<<grid_for(m, BB_TPB), BB_TPB, 0, s>>>(m, L, nq, split.p, lstart.p, lcount.p, k1s.p, k2s.p,
-                                                                 cpos.p, cnt.p);
-        GC_CUDA(cudaMemsetAsync(cnt.p + m, 0, sizeof(int), s));
-        cubc(ctx, [&](void *t, size_t &b) { return cub::DeviceScan::ExclusiveSum(t, b, cnt.p, cbase.p, m + 1, s); });
-        check_launch("bb level");
-        int mc = 0;
-        GC_CUDA(cudaMemcpyAsync(&mc, cbase.p + m, sizeof(int), cudaMemcpyDeviceToHost, s));
-        GC_CUDA(cudaStreamSynchronize(s));
-        if (mc == 0) break;
-        GC_REQUIRE(next_id + mc <= cap_nodes, GC_E_VALUE, "node capacity exceeded");
-        cstart.resize(mc);
-        ccount.resize(mc);
-        ccenter.resize(mc);
-        bb_make_children<<<grid_for(m, BB_TPB), BB_TPB, 0, s>>>(m, nq, next_id, split.p, lid.p, lcenter.p, dim, cpos.p,
-                                                                cbase.p, cstart.p, ccount.p, ccenter.p,
-                                                                bh->d_first_child.p, bh->d_nchild.p);
-        check_launch("bb children");
-        // the children become the next level
-        lvl_first.push_back(next_id);
-        std::swap(lstart.p, cstart.p);
-        std::swap(lstart.n, cstart.n);
-        std::swap(lstart.cap, cstart.cap);
-        std::swap(lcount.p, ccount.p);
-        std::swap(lcount.n, ccount.n);
-        std::swap(lcount.cap, ccount.cap);
-        std::swap(lcenter.p, ccenter.p);
-        std::swap(lcenter.n, ccenter.n);
-        std::swap(lcenter.cap, ccenter.cap);
-        lid.resize(mc);
-        bb_iota<<<grid_for(mc, BB_TPB), BB_TPB, 0, s>>>(mc, next_id, lid.p);
-        next_id += mc;
-        m = mc;
-        half = half / 2.0;
+    static int coop_blocks = 0;  // co-resident grid of the cooperative level kernel
+    if (!coop_blocks) {
+        int per_sm = 0;
+        GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bb_levels_coop, BB_TPB, 0));
+        coop_blocks = std::max(1, std::min(per_sm, 2)) * ctx->prop.multiProcessorCount;
     }
-    lvl_first.push_back(next_id);
+    auto &bsum = bh->ws.bsum;
+    auto &lvlf = bh->ws.lvlf;
+    bsum.resize(coop_blocks);
+    lvlf.resize(MAX_KEY_LEVELS + 4);
+    LevelArgs A;
+    A.n = n;
+    A.dim = dim;
+    A.nlev = nlev;
+    A.cap_nodes = cap_nodes;
+    A.bucket = bucket;
+    A.box = box;
+    A.k1 = k1s.p;
+    A.k2 = k2s.p;
+    A.start[0] = lstart.p;
+    A.start[1] = cstart.p;
+    A.count[0] = lcount.p;
+    A.count[1] = ccount.p;
+    A.center[0] = lcenter.p;
+    A.center[1] = ccenter.p;
+    A.cpos = cpos.p;
+    A.cnt = cnt.p;
+    A.cbase = cbase.p;
+    A.bsum = bsum.p;
+    A.ncenter = bh->d_ncenter.p;
+    A.pstart = bh->d_pstart.p;
+    A.pcount = bh->d_pcount.p;
+    A.first_child = bh->d_first_child.p;
+    A.nchild = bh->d_nchild.p;
+    A.leaf_key = leaf_key.p;
+    A.leaf_id = leaf_id.p;
+    A.nleaf = nleaf.p;
+    A.lvl_first = lvlf.p;
+    A.nlevels = lvlf.p + MAX_KEY_LEVELS + 2;
+    A.overflow = lvlf.p + MAX_KEY_LEVELS + 3;
+    GC_CUDA(cudaMemsetAsync(lvlf.p, 0, sizeof(int) * (MAX_KEY_LEVELS + 4), s));
+    void *kargs[] = {&A};
+    GC_CUDA(cudaLaunchCooperativeKernel((void *)bb_levels_coop, coop_blocks, BB_TPB, kargs, 0, s));
+    check_launch("bb_levels_coop");
+    std::vector<int> lf(MAX_KEY_LEVELS + 4);
+    lvlf.download(lf.data(), MAX_KEY_LEVELS + 4, s);
+    GC_CUDA(cudaStreamSynchronize(s));
+    GC_REQUIRE(!lf[MAX_KEY_LEVELS + 3], GC_E_VALUE, "node capacity exceeded");
+    const int nlevels = lf[MAX_KEY_LEVELS + 2];
+    std::vector<int> lvl_first(lf.begin(), lf.begin() + nlevels + 1);
+    const int next_id = lvl_first.back();
     const int nn = next_id;
     int nb = 0;
     GC_CUDA(cudaMemcpyAsync(&nb, nleaf.p, sizeof(int), cudaMemcpyDeviceToHost, s));

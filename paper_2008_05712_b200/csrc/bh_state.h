@@ -11,13 +11,12 @@
 using namespace gc;
 
 struct BuildWs {  // device-build scratch, kept across builds (no per-step cudaMalloc/cudaFree)
-    DBuf<int> nsel2, cpos, ccnt, cbase;
+    DBuf<int> nsel2, cpos, ccnt, cbase, bsum, lvlf;
     DBuf<double> pos, mass, scratch;
     DBuf<unsigned long long> k1, k2, k1p, k1s, k2s;
     DBuf<int> idx, perm1, perm;
-    DBuf<int> lstart, lcount, lid, cstart, ccount, leaf_key, leaf_id, nleaf;
+    DBuf<int> lstart, lcount, cstart, ccount, leaf_key, leaf_id, nleaf;
     DBuf<double4> lcenter, ccenter;
-    DBuf<unsigned char> split, flag;
     DBuf<int> lk_s;
     DBuf<int> offs, pidx;
     DBuf<double4> com;
