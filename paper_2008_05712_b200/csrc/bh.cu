@@ -111,6 +111,8 @@ void upload_tree(gc_bh *bh)
     bh->d_bucket_ids.upload(bids.data(), nb, s);
     bh->d_part_bucket.upload(pb.data(), t.n, s);
     bh->d_wg.upload(bh->h_wg.data(), bh->h_wg.size(), s);
+    bh->n_wg = (int)bh->h_wg.size();
+    bh->h_wg_valid = true;
     bh->d_fg.upload(h_fg.data(), h_fg.size(), s);
     bh->n_fg = (int)h_fg.size();
     bh->h2d += nn * (int64_t)(3 * sizeof(float4) + sizeof(double4) + sizeof(int2)) +
@@ -145,6 +147,25 @@ void exclusive_scan(gc_ctx *ctx, const T *in, T *out, int64_t n)
     GC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, ctx->stream));
     ctx->scratch.resize(bytes);
     GC_CUDA(cub::DeviceScan::ExclusiveSum(ctx->scratch.p, bytes, in, out, n, ctx->stream));
+}
+
+// host copy of the walk groups (device builds fetch it only for sub-ranges)
+void ensure_h_wg(gc_bh *bh)
+{
+    if (bh->h_wg_valid) return;
+    bh->h_wg.resize(bh->n_wg);
+    bh->d_wg.download(bh->h_wg.data(), bh->n_wg, bh->ctx->stream);
+    GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
+    bh->h_wg_valid = true;
+}
+
+// first force group of walk group g (g == n_wg: one past the last)
+int wg_fg_first(gc_bh *bh, int g)
+{
+    if (g <= 0) return 0;
+    if (g >= bh->n_wg) return bh->n_fg;
+    ensure_h_wg(bh);
+    return bh->h_wg[g].fg_first;
 }
 
 UnionPool pool_view(gc_bh *bh)
@@ -247,7 +268,7 @@ void launch_walk(gc_bh *bh, bool write, bool stats)
 {
     cudaStream_t s = bh->ctx->stream;
     const int nf = bh->n_fg;
-    const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? (int)bh->h_wg.size() : bh->rg1;
+    const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? bh->n_wg : bh->rg1;
     const int ng = g1 - g0;
     const WalkGroup *wg = bh->d_wg.p + g0;
     const unsigned grid = grid_for(std::max(ng, 1), WARPS_PER_BLOCK);
@@ -313,11 +334,11 @@ __global__ void bh_fg_key_kernel(int nf, const int *__restrict__ grec, int *__re
 void make_orders(gc_bh *bh)
 {
     cudaStream_t s = bh->ctx->stream;
-    const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? (int)bh->h_wg.size() : bh->rg1;
+    const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? bh->n_wg : bh->rg1;
     const int ng = g1 - g0, nf = bh->n_fg;
     if (ng <= 0) return;
-    const int f0 = bh->h_wg[g0].fg_first;
-    const int f1 = g1 < (int)bh->h_wg.size() ? bh->h_wg[g1].fg_first : nf;
+    const int f0 = wg_fg_first(bh, g0);
+    const int f1 = wg_fg_first(bh, g1);
     const int nfr = f1 - f0;
     auto &k0 = bh->d_okey, &k1 = bh->d_okey2, &i0 = bh->d_oidx;
     const int m = std::max(ng, nfr);
@@ -433,9 +454,9 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
     const bool eps0 = eps2 == 0.f;
     GC_CUDA(cudaEventRecord(bh->ev[2], s));
     if (bh->have_union) {
-        const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? (int)bh->h_wg.size() : bh->rg1;
-        const int f0 = g0 < (int)bh->h_wg.size() ? bh->h_wg[g0].fg_first : bh->n_fg;
-        const int f1 = g1 < (int)bh->h_wg.size() ? bh->h_wg[g1].fg_first : bh->n_fg;
+        const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? bh->n_wg : bh->rg1;
+        const int f0 = wg_fg_first(bh, g0);
+        const int f1 = wg_fg_first(bh, g1);
         const int nfg = f1 - f0;
         const unsigned grid = grid_for(std::max(nfg, 1), WARPS_PER_BLOCK);
         UnionPool U = pool_view(bh);
@@ -782,7 +803,7 @@ gc_status gc_bh_set_range(gc_bh *bh, int64_t wg_begin, int64_t wg_end)
 {
     return guard([&] {
         GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
-        const int64_t ng = (int64_t)bh->h_wg.size();
+        const int64_t ng = (int64_t)bh->n_wg;
         GC_REQUIRE(wg_begin >= 0 && wg_begin <= wg_end && wg_end <= ng, GC_E_VALUE, "bad walk-group range");
         bh->rg0 = (int)wg_begin;
         bh->rg1 = (int)wg_end;
@@ -796,8 +817,9 @@ gc_status gc_bh_groups(gc_bh *bh, int64_t *n_walk_groups, int64_t *wg_first_buck
 {
     return guard([&] {
         GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
-        *n_walk_groups = (int64_t)bh->h_wg.size();
+        *n_walk_groups = (int64_t)bh->n_wg;
         if (wg_first_bucket) {
+            ensure_h_wg(bh);
             for (size_t g = 0; g < bh->h_wg.size(); ++g) wg_first_bucket[g] = bh->h_wg[g].bfirst;
             wg_first_bucket[bh->h_wg.size()] = bh->n_buckets;
         }

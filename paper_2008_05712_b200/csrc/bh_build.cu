@@ -721,11 +721,10 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     bb_groups<1><<<grid_for(nwg, BB_TPB / 32), BB_TPB, 0, s>>>(nwg, nb, bh->d_brange.p, nullptr, fg_base.p, bh->d_wg.p,
                                                           bh->d_fg.p, bad.p);
     check_launch("bb groups");
-    bh->h_wg.resize(nwg);
+    bh->n_wg = nwg;
+    bh->h_wg_valid = false;  // fetched on demand (sub-range launches, gc_bh_groups)
     bh->n_fg = nfg;
-    bh->d_wg.download(bh->h_wg.data(), nwg, s);
     GC_CUDA(cudaStreamSynchronize(s));
-    bh->d2h += (int64_t)nwg * sizeof(WalkGroup);
     set_tree_bounds(bh, cm);
     bh->n = n;
     bh->dim = dim;

@@ -38,7 +38,9 @@ struct gc_bh {
     DBuf<double4> d_ncenter;  // per node: center.xyz, half
     DBuf<double> d_nmass;
     DBuf<int> d_first_child, d_nchild, d_pstart, d_pcount, d_buckets;
-    std::vector<WalkGroup> h_wg;
+    std::vector<WalkGroup> h_wg;  // host copy, valid when h_wg_valid
+    int n_wg = 0;
+    bool h_wg_valid = false;
     int n_fg = 0;  // force groups (device array d_fg)
     // device tree
     DBuf<float4> d_recs;  // walk records: float32 com + packed links
