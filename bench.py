@@ -466,6 +466,38 @@ def bench_runtime_path(args):
     return out
 
 
+def bench_plummer16m(args):
+    """configs[3]'s system on ONE B200: Plummer 2^24 particles, theta 0.7 (the
+    N > 1 runs shard this kind of tree; here the single-GPU step)."""
+    import torch
+
+    from paper_2008_05712_b200 import _lib as L
+    from paper_2008_05712_b200 import generators as gen
+    from paper_2008_05712_b200 import nbody
+
+    ps = gen.fp32_exact(gen.gen_plummer(1 << 24, 42))
+    tree = nbody.build_bucket_tree(ps, BUCKET)
+    tm = np.zeros(3)
+    w, r, f = [], [], []
+    for i in range(max(2, min(args.steps, 5)) + 1):
+        L.call("gc_bh_walk", tree.handle, THETA)
+        L.call("gc_bh_forces_async", tree.handle, 1.0, EPS)
+        L.call("gc_bh_timings", tree.handle, L.ptr(tm, L.f64p))
+        if i:
+            w.append(tm[0])
+            f.append(tm[1])
+            r.append(tm[2])
+    inter = nbody.interactions(tree)
+    ms = statistics.median(w) + statistics.median(r) + statistics.median(f)
+    fp = FLOPS_PER_INTERACTION * inter / (statistics.median(f) * 1e-3) / 1e12
+    out = {"workload": "configs[3] system on 1 GPU: Plummer 16,777,216 particles, theta 0.7, bucket 8",
+           "interactions": inter, "ms_per_step": ms, "value": inter / (ms * 1e-3), "unit": "interactions/s",
+           "walk_ms": statistics.median(w), "reorg_ms": statistics.median(r), "force_ms": statistics.median(f),
+           "force_tflops": fp, "device_gib": (torch.cuda.mem_get_info()[1] - torch.cuda.mem_get_info()[0]) / 2**30}
+    del tree
+    return out
+
+
 def run_ours(args, world, rank, local):
     import torch
 
@@ -504,6 +536,7 @@ def run_ours(args, world, rank, local):
         line["data"] = f"synthetic gen_particles({world}M, seed 42, clustering 0.6, dim 3), fp32-exact"
     if world == 1:
         line["runtime_path"] = bench_runtime_path(args)
+        line["plummer16m"] = bench_plummer16m(args)
     if world == 1 and not args.no_cpu_baseline:
         c_inter, c_ts, cores = cpu_bh(bh["ps"], 1)
         line["cpu_baseline"] = {"value": c_inter / c_ts[0], "unit": "interactions/s", "cores": cores,

@@ -407,6 +407,13 @@ void run_walk(gc_bh *bh, double theta, bool want_stats)
         while (walk_overflowed(bh)) launch_walk(bh, true, true);
         bh->stats_valid = true;
         bh->stats_dirty = true;
+        // exact staging size of this tree / theta (the asynchronous steady state never overflows)
+        std::vector<int> rec(bh->n_fg);
+        bh->d_grec.download(rec.data(), bh->n_fg, bh->ctx->stream);
+        GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
+        int64_t need = 0;
+        for (int r : rec) need += (r + PFLUSH - 1) & ~(PFLUSH - 1);
+        if (need > bh->staging_cap) size_staging(bh, need + need / 16);
     }
 }
 

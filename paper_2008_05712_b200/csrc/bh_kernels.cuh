@@ -315,7 +315,7 @@ union_to_lists_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const Wal
     int chunk = n > 0 ? U.gfirst[f] : 0;
     for (int e = 0; e < n; ++e) {
         if (e > 0 && (e & (CHUNK - 1)) == 0) chunk = U.cnext[chunk];
-        const int4 en = U.ent[chunk * CHUNK + (e & (CHUNK - 1))];
+        const int4 en = U.ent[(int64_t)chunk * CHUNK + (e & (CHUNK - 1))];
         if (mine && ((unsigned)(en.y | en.z) & bit)) {
             key[cur] = preorder[en.x];
             val[cur] = 2 * en.x + (((unsigned)en.y & bit) ? 0 : 1);
@@ -579,7 +579,8 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int *_
         const ForceGroup fg = fgroups[gi];
         const int64_t rb = S.rbase[gi];
         const int padded = (grec[gi] + PFLUSH - 1) & ~(PFLUSH - 1);
-        const int ntile = (padded + TILE - 1) / TILE;
+        // a run beyond the staging capacity was not written (expand flagged it; the host re-runs)
+        const int ntile = rb + padded > S.cap ? 0 : (padded + TILE - 1) / TILE;
         // stage tile t of the run into buffer t & 1 (2 records + 2 masks per lane)
         auto issue = [&](int t) {
             const int64_t r0 = rb + (int64_t)t * TILE;
