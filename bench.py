@@ -498,6 +498,26 @@ def bench_plummer16m(args):
     return out
 
 
+def bench_md8m(args):
+    """configs[4]'s system on ONE B200: LJ FCC 126^3 x 4 = 8,001,504 atoms, 84^3
+    cells (the N > 1 runs decompose this kind of box into slabs)."""
+    from paper_2008_05712_b200 import md
+    from paper_2008_05712_b200.generators import gen_lj_fcc
+
+    sysin = gen_lj_fcc(126, seed=7)
+    sysd = md.LJSystem(sysin)
+    sysd.run(10)  # graph capture + warm-up
+    runs = [sysd.run(10) for _ in range(2)]
+    ms = statistics.mean(runs) / 10
+    _, _, cells = sysd.state()
+    task_bytes = md_task_bytes(cells, sysin.cells)
+    hbm, src = measured_hbm()
+    return {"workload": "configs[4] system on 1 GPU: LJ FCC 8,001,504 atoms, 84^3 cells, rc 2.5, periodic",
+            "ms_per_step": ms, "unit": "ms/step",
+            "task_model_gbs": task_bytes / (ms * 1e-3) / 1e9, "task_model_frac": task_bytes / (ms * 1e-3) / 1e9 / hbm,
+            "algorithmic_bytes_per_step": task_bytes}
+
+
 def run_ours(args, world, rank, local):
     import torch
 
@@ -537,6 +557,7 @@ def run_ours(args, world, rank, local):
     if world == 1:
         line["runtime_path"] = bench_runtime_path(args)
         line["plummer16m"] = bench_plummer16m(args)
+        line["md8m"] = bench_md8m(args)
     if world == 1 and not args.no_cpu_baseline:
         c_inter, c_ts, cores = cpu_bh(bh["ps"], 1)
         line["cpu_baseline"] = {"value": c_inter / c_ts[0], "unit": "interactions/s", "cores": cores,
