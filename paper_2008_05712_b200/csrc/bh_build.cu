@@ -116,6 +116,30 @@ __device__ __forceinline__ int digit_lower_bound(int lo, int hi, int q, int L, c
 // lower bounds, grid-wide exclusive scan of the counts, emit the children as
 // the next level (level-order ids = position order, children in octant order).
 // ---------------------------------------------------------------------------
+// warp-cooperative lower bound (32 probes per round: log32 instead of log2
+// dependent loads; the top levels' nodes span most of the particles)
+__device__ __forceinline__ int warp_digit_lower_bound(int lo, int hi, int q, int L,
+                                                      const unsigned long long *__restrict__ k1,
+                                                      const unsigned long long *__restrict__ k2)
+{
+    const int lane = threadIdx.x & 31;
+    while (hi - lo > 32) {
+        const int step = (hi - lo + 31) / 32;
+        const int pos = lo + lane * step;
+        const bool lt = pos < hi && key_digit(k1[pos], k2[pos], L) < q;
+        const int k = __popc(__ballot_sync(0xffffffffu, lt));  // samples 0..k-1 lie below q
+        if (k == 0) return lo;
+        const int nlo = lo + (k - 1) * step + 1;
+        hi = min(hi, lo + k * step);
+        lo = nlo;
+    }
+    const int pos = lo + lane;
+    const bool lt = pos < hi && key_digit(k1[pos], k2[pos], L) < q;
+    return lo + __popc(__ballot_sync(0xffffffffu, lt));
+}
+
+constexpr int BIG_NODE = 512;  // nodes wider than this are cut by a whole warp
+
 struct LevelArgs {
     int n, dim, nlev, cap_nodes;
     long long bucket;
@@ -128,6 +152,7 @@ struct LevelArgs {
     int *pstart, *pcount, *first_child, *nchild;
     int *leaf_key, *leaf_id, *nleaf;
     int *lvl_first, *nlevels, *overflow;
+    int *big, *nbig;  // this level's wide splitting nodes (warp-cooperative cuts)
 };
 
 __device__ __forceinline__ int block_sum(int v, int *red)
@@ -171,7 +196,9 @@ __global__ void __launch_bounds__(BB_TPB) bb_levels_coop(LevelArgs A)
                 A.leaf_id[k] = id;
             }
             int nonempty = 0;
-            if (sp && L < A.nlev) {
+            if (sp && L < A.nlev && ct > BIG_NODE) {
+                A.big[atomicAdd(A.nbig, 1)] = p;  // cut below by a warp
+            } else if (sp && L < A.nlev) {
                 const int e = st + ct;
                 int lo = st;
                 for (int q = 0; q < nq; ++q) {
@@ -186,6 +213,28 @@ __global__ void __launch_bounds__(BB_TPB) bb_levels_coop(LevelArgs A)
         }
         if (L >= A.nlev) break;  // no node of this level can split (half < 1e-9)
         grid.sync();
+        // 1b: wide nodes, one warp each
+        {
+            const int nbig = *A.nbig;
+            const int gw = tid >> 5, nw = T >> 5, lane = tid & 31;
+            for (int k = gw; k < nbig; k += nw) {
+                const int p = A.big[k];
+                const int st = A.start[cur][p], e = st + A.count[cur][p];
+                int lo = st, nonempty = 0;
+                for (int q = 0; q < nq; ++q) {
+                    const int next = q + 1 < nq ? warp_digit_lower_bound(lo, e, q + 1, L, A.k1, A.k2) : e;
+                    if (lane == 0) A.cpos[9 * p + q] = lo;
+                    nonempty += next > lo ? 1 : 0;
+                    lo = next;
+                }
+                if (lane == 0) {
+                    A.cpos[9 * p + nq] = e;
+                    A.cnt[p] = nonempty;
+                }
+            }
+        }
+        grid.sync();
+        if (tid == 0) *A.nbig = 0;  // read by every warp above; reset for the next level
         // 2: grid-wide exclusive scan of cnt[0, m) in per-block chunks
         const int chunk = (m + nb - 1) / nb;
         const int c0 = min(m, b * chunk), c1 = min(m, c0 + chunk);
@@ -611,6 +660,11 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     A.leaf_key = leaf_key.p;
     A.leaf_id = leaf_id.p;
     A.nleaf = nleaf.p;
+    auto &big = bh->ws.big;
+    big.resize(n + 1);
+    A.big = big.p;
+    A.nbig = big.p + n;
+    GC_CUDA(cudaMemsetAsync(big.p + n, 0, sizeof(int), s));
     A.lvl_first = lvlf.p;
     A.nlevels = lvlf.p + MAX_KEY_LEVELS + 2;
     A.overflow = lvlf.p + MAX_KEY_LEVELS + 3;

@@ -11,7 +11,7 @@
 using namespace gc;
 
 struct BuildWs {  // device-build scratch, kept across builds (no per-step cudaMalloc/cudaFree)
-    DBuf<int> nsel2, cpos, ccnt, cbase, bsum, lvlf;
+    DBuf<int> nsel2, cpos, ccnt, cbase, bsum, lvlf, big;
     DBuf<double> pos, mass, scratch;
     DBuf<unsigned long long> k1, k2, k1p, k1s, k2s;
     DBuf<int> idx, perm1, perm;
