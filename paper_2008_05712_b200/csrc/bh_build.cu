@@ -627,7 +627,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     if (!coop_blocks) {
         int per_sm = 0;
         GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bb_levels_coop, BB_TPB, 0));
-        coop_blocks = std::max(1, std::min(per_sm, 2)) * ctx->prop.multiProcessorCount;
+        coop_blocks = std::max(1, std::min(per_sm, 1)) * ctx->prop.multiProcessorCount;
     }
     auto &bsum = bh->ws.bsum;
     auto &lvlf = bh->ws.lvlf;
