@@ -535,7 +535,18 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     auto &mass = bh->ws.mass;
     auto &scratch = bh->ws.scratch;
     pos.upload(pos_h, (size_t)n * dim, s);
-    mass.upload(mass_h, n, s);
+    // masses are first needed by the bucket masses: copy them on a side stream
+    // while the keys, the sort and the level expansion run
+    if (!bh->side) {
+        GC_CUDA(cudaStreamCreateWithFlags(&bh->side, cudaStreamNonBlocking));
+        GC_CUDA(cudaEventCreateWithFlags(&bh->side_done, cudaEventDisableTiming));
+        GC_CUDA(cudaEventCreateWithFlags(&bh->main_ready, cudaEventDisableTiming));
+    }
+    mass.resize(n);
+    GC_CUDA(cudaEventRecord(bh->main_ready, s));  // earlier work on `mass` (previous build) is done
+    GC_CUDA(cudaStreamWaitEvent(bh->side, bh->main_ready, 0));
+    GC_CUDA(cudaMemcpyAsync(mass.p, mass_h, sizeof(double) * n, cudaMemcpyHostToDevice, bh->side));
+    GC_CUDA(cudaEventRecord(bh->side_done, bh->side));
     bh->h2d += (int64_t)n * (dim + 1) * (int64_t)sizeof(double);
     auto &k1 = bh->ws.k1;
     auto &k2 = bh->ws.k2;
@@ -711,6 +722,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     auto &com = bh->ws.com;
     com.resize(nn);
     scratch.resize(n);
+    GC_CUDA(cudaStreamWaitEvent(s, bh->side_done, 0));
     bb_bucket_mass<<<grid_for(nb, BB_TPB), BB_TPB, 0, s>>>(nb, dim, bh->d_buckets.p, bh->d_pstart.p, bh->d_pcount.p,
                                                            pidx.p, pos.p, mass.p, bh->d_nmass.p, com.p, scratch.p);
     for (int L = (int)lvl_first.size() - 2; L >= 0; --L) {
@@ -780,6 +792,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     bh->n_fg = nfg;
     GC_CUDA(cudaStreamSynchronize(s));
     set_tree_bounds(bh, cm);
+    GC_CUDA(cudaEventSynchronize(bh->side_done));  // long done: the caller may reuse its mass buffer
     bh->n = n;
     bh->dim = dim;
     bh->box = box;

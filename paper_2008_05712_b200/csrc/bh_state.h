@@ -99,10 +99,15 @@ struct gc_bh {
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     BuildWs ws;
     int64_t h2d = 0, d2h = 0;  // bytes moved host<->device since the last reset
+    cudaStream_t side = nullptr;  // device build: mass upload overlapping the sort
+    cudaEvent_t side_done = nullptr, main_ready = nullptr;
     ~gc_bh()
     {
         for (auto &e : ev)
             if (e) cudaEventDestroy(e);
+        if (side_done) cudaEventDestroy(side_done);
+        if (main_ready) cudaEventDestroy(main_ready);
+        if (side) cudaStreamDestroy(side);
     }
 };
 
