@@ -423,7 +423,7 @@ def bench_md(args, world, rank, local, torch):
                    "timed": "CUDA-graph of 100 full steps (fused force+integrator+cell count kernel, cell sort), "
                             "events"},
         "roofline": {"bound": "hbm", "kernel": "md step (task model)", "achieved": achieved, "peak": hbm,
-                     "peak_source": src, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                     "peak_source": src, "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic("md_cell_kernel"),
                      "algorithmic_bytes_per_step": task_bytes,
                      "note": "the 3.5 MB system is L2-resident: ncu measures ~3.5 MB DRAM per step, the task-model "
                              "bytes are served from L2 (profiles/r01_md_ncu_summary.txt)"},
