@@ -229,6 +229,49 @@ gc_status gc_md_slab_step(gc_md *md, double dt);
 gc_status gc_md_migrate(gc_md *md, const void *in_left, int64_t n_left, const void *in_right, int64_t n_right);
 gc_status gc_md_owned(gc_md *md, int64_t *n_owned, double *pos, double *vel, int64_t *gid /* host; may be NULL */);
 
+/* ---- closed-loop MD ----------------------------------------
+ * hr/workloads/md.py MDWorkload (md.py:209-271) run on the device as one
+ * persistent kernel: per step, patch "interact" messages complete pair
+ * entries through readiness counters (hr/runtime.py:95-118), completed
+ * entries enqueue their work request, blocks execute requests as they become
+ * ready, and the completion count is the step barrier that triggers md_step
+ * (md.py:166-190).  Float64, bit-identical to the reference's numba kernels. */
+typedef struct gc_mdloop gc_mdloop;
+gc_status gc_mdloop_create(gc_ctx *ctx, gc_mdloop **out);
+gc_status gc_mdloop_destroy(gc_mdloop *loop);
+/* PatchGrid (md.py:29-50): pos/vel (n x 2), patch_of (n); MDParams cutoff / stiffness / periodic */
+gc_status gc_mdloop_set(gc_mdloop *loop, int64_t n, const double *pos, const double *vel, const int64_t *patch_of,
+                        int32_t rows, int32_t cols, double patch_size, double cutoff, double stiffness,
+                        int32_t periodic);
+/* `steps` step barriers = steps - 1 md_step updates (MDParams.steps, md.py:263-271);
+ * stats (optional, steps x 4): work requests, interact messages, completions, barrier fired */
+gc_status gc_mdloop_run(gc_mdloop *loop, int32_t steps, double dt, int64_t *stats);
+gc_status gc_mdloop_get_state(gc_mdloop *loop, double *pos, double *vel, int64_t *patch_of);
+/* out[3]: patches, pair chares (neighbor_pairs), compute_forces segments */
+gc_status gc_mdloop_topology(gc_mdloop *loop, int64_t out[3]);
+gc_status gc_mdloop_elapsed(gc_mdloop *loop, double *ms);
+/* per step of the last run (steps x 5, ns): counts + scans, scatter, patch
+ * sort / gather / messages, execution + barrier, md_step + resets */
+gc_status gc_mdloop_phases(gc_mdloop *loop, double *out);
+
+/* ---- Ewald kernel class ------------------------------------
+ * The reference models an "ewald" class (one request per bucket, buffers
+ * [bucket], item_count max(1, n_b): hr/workloads/nbody.py:317-323; cost
+ * hr/devicesim.py:92-99) without computing it.  Here it is the periodic
+ * correction of each particle from the root multipole, Hernquist-Bouchet-Suto
+ * Ewald summation, float64.  moments[10] = M, com(3), traceless quadrupole
+ * Q xx yy zz xy xz yz; params[5] = box L, alpha (<= 0: 2/L), nrep, ewcut, hcut.
+ * acc: correction acceleration per unit mass (G = 1); pot: potential. */
+gc_status gc_ewald_moments(gc_ctx *ctx, int64_t n, const double *pos, const double *mass, double moments[10]);
+gc_status gc_ewald_correction(gc_ctx *ctx, int64_t n, const double *pos, const double moments[10],
+                              const double params[5], double *acc, double *pot);
+gc_status gc_bh_ewald_moments(gc_bh *bh, double moments[10]);
+/* one combined "ewald" request: members = DFS buckets, one buffer each (the
+ * last gc_dm plan), payloads staged by gc_dm_stage_bh; forces g m_i a_i */
+gc_status gc_bh_run_ewald(gc_bh *bh, gc_dm *dm, const int64_t *member_buckets, int32_t n_members,
+                          const double params[5], double g);
+gc_status gc_bh_get_ewald(gc_bh *bh, double *forces /* n x 3 */, double *pot /* n; may be NULL */);
+
 #ifdef __cplusplus
 }
 #endif

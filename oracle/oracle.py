@@ -72,6 +72,9 @@ def lib():
         L.orc_pairwise_sum.argtypes = [f64p, C.c_int64]
         L.orc_pairwise_sum.restype = C.c_double
         L.orc_num_threads.restype = C.c_int
+        L.orc_ewald_moments.argtypes = [C.c_int64, f64p, f64p, f64p]
+        L.orc_ewald_correction.argtypes = [C.c_int64, f64p, f64p, C.c_double, C.c_double, C.c_int, C.c_double,
+                                           C.c_double, f64p, f64p]
         L.free.argtypes = [C.c_void_p]
         _lib = L
     return _lib
@@ -307,6 +310,27 @@ def lj3d_step(positions, velocities, dims, cell_size, dt, rc=2.5, eps=1.0, sigma
     box = np.asarray(dims, np.float64) * cell_size
     pos = pos % box
     return pos, vel, f, e
+
+
+def ewald_moments(pos, mass):
+    """Root multipole of a 3-D distribution: [M, com(3), traceless Q (xx, yy, zz, xy, xz, yz)]."""
+    pos, mass = _f64(pos), _f64(mass)
+    out = np.zeros(10)
+    lib().orc_ewald_moments(pos.shape[0], _p(pos, f64p), _p(mass, f64p), _p(out, f64p))
+    return out
+
+
+def ewald_correction(pos, moments, L=1.0, alpha=None, nrep=3, ewcut=2.6, hcut=2.8):
+    """Periodic (Ewald) correction acceleration + potential at `pos` from the
+    multipole `moments` (restatement in gcharm_oracle.c; parity unpinned --
+    the reference only models the ewald class)."""
+    pos, mom = _f64(pos), _f64(moments)
+    n = pos.shape[0]
+    acc, pot = np.zeros((n, 3)), np.zeros(n)
+    alpha = 2.0 / L if alpha is None else alpha
+    lib().orc_ewald_correction(n, _p(pos, f64p), _p(mom, f64p), float(L), float(alpha), int(nrep), float(ewcut),
+                               float(hcut), _p(acc, f64p), _p(pot, f64p))
+    return acc, pot
 
 
 def count_address_runs(addresses, group=16):

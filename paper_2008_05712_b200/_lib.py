@@ -38,6 +38,20 @@ SIGNATURES = {
     "gc_md_cross_forces": [vp, C.c_int64, C.c_int64, C.c_int32, f64p, f64p, C.c_double, C.c_double, f64p, f64p],
     "gc_md_self_forces": [vp, C.c_int64, C.c_int32, f64p, C.c_double, C.c_double, f64p],
     "gc_count_address_runs": [vp, i64p, C.c_int64, C.c_int64, i64p],
+    "gc_mdloop_create": [vp, C.POINTER(vp)],
+    "gc_mdloop_destroy": [vp],
+    "gc_mdloop_set": [vp, C.c_int64, f64p, f64p, i64p, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
+                      C.c_int32],
+    "gc_mdloop_run": [vp, C.c_int32, C.c_double, i64p],
+    "gc_mdloop_get_state": [vp, f64p, f64p, i64p],
+    "gc_mdloop_topology": [vp, i64p],
+    "gc_mdloop_elapsed": [vp, f64p],
+    "gc_mdloop_phases": [vp, f64p],
+    "gc_ewald_moments": [vp, C.c_int64, f64p, f64p, f64p],
+    "gc_ewald_correction": [vp, C.c_int64, f64p, f64p, f64p, f64p, f64p],
+    "gc_bh_ewald_moments": [vp, f64p],
+    "gc_bh_run_ewald": [vp, vp, i64p, C.c_int32, f64p, C.c_double],
+    "gc_bh_get_ewald": [vp, f64p, f64p],
     "gc_bh_create": [vp, C.POINTER(vp)],
     "gc_bh_destroy": [vp],
     "gc_bh_set_particles": [vp, C.c_int64, C.c_int32, f64p, f64p, C.c_double, C.c_int64],

@@ -18,6 +18,7 @@ void set_error(const std::string &msg) { g_last_error = msg; }
 
 void bh_kernel_spec(const char *cls, int64_t out[5]);  // bh.cu
 void md_kernel_spec(const char *cls, int64_t out[5]);  // md.cu
+void dm_kernel_spec(const char *cls, int64_t out[5]);  // dm.cu (ewald_member)
 
 constexpr int TPB = 128;
 
@@ -231,6 +232,7 @@ gc_status gc_kernel_spec(gc_ctx *ctx, const char *kernel_class, int64_t out[5])
         GC_REQUIRE(ctx && kernel_class, GC_E_VALUE, "null argument");
         GC_CUDA(cudaSetDevice(ctx->device));
         if (!strcmp(kernel_class, "md")) md_kernel_spec(kernel_class, out);
+        else if (!strcmp(kernel_class, "ewald_member")) dm_kernel_spec(kernel_class, out);
         else bh_kernel_spec(kernel_class, out);
     });
 }

@@ -578,6 +578,7 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
         }
         bh->have_tree = true;
         bh->have_union = bh->have_member_lists = false;
+        bh->ew_mom_valid = false;
         bh->params_valid = false;
         bh->stats_valid = false;
         bh->stats_dirty = false;
@@ -587,6 +588,8 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
         if (!bh->device_build) {
             upload_tree(bh);
             upload_particles(bh, pos, mass);
+            bh->ws.pos.upload(pos, (size_t)n * dim, bh->ctx->stream);  // float64 copies (Ewald moments)
+            bh->ws.mass.upload(mass, (size_t)n, bh->ctx->stream);
         }
     });
 }

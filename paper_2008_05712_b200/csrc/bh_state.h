@@ -88,6 +88,10 @@ struct gc_bh {
     DBuf<int> d_naddr, d_paddr;
     // outputs
     DBuf<double> d_out, d_pot;
+    // Ewald kernel class: root moments, staging of the reduction, tables, outputs
+    DBuf<double> d_ew_mom, d_ew_part, d_ewf, d_ewp;
+    DBuf<double4> d_ew_real, d_ew_k;
+    bool ew_mom_valid = false;
     std::vector<int64_t> h_item_count;
     int64_t n_list_entries = 0;
     DBuf<int64_t> d_bptr;

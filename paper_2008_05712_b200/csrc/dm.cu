@@ -28,6 +28,7 @@
 
 #include "bh_state.h"
 #include "common.cuh"
+#include "ewald.cuh"
 
 namespace gc {
 
@@ -267,6 +268,54 @@ force_slot_kernel(int nmember, const int *__restrict__ member_bucket, const int 
             }
         }
     }
+}
+
+// "ewald" kernel class: one warp per member request, whose
+// single buffer is its bucket (nbody.py:317-323); the bucket's particles come
+// from the member's data-manager slot (payload staged by gc_dm_stage_bh) and
+// each gets the periodic correction of the root multipole (ewald.cuh).
+__global__ void __launch_bounds__(256)
+ewald_slot_kernel(int nmember, const int *__restrict__ member_bucket, const int *__restrict__ bounds,
+                  const int *__restrict__ addr, const int2 *__restrict__ brange, const int *__restrict__ porder,
+                  const double *__restrict__ mass, const float4 *__restrict__ pool, int slot_f4,
+                  const double *__restrict__ mom, const EwaldParams P, const double4 *__restrict__ real,
+                  const double4 *__restrict__ kv, double g, double *__restrict__ outf, double *__restrict__ outp)
+{
+    const int mi = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (mi >= nmember) return;
+    const float4 *src = pool + (int64_t)addr[bounds[mi]] * slot_f4;
+    const int pc = __float_as_int(src[1].w);
+    const int2 br = brange[member_bucket[mi]];
+    for (int i = 0; i < pc; ++i) {
+        const float4 q = src[2 + i];
+        const double d[3] = {(double)q.x - mom[1], (double)q.y - mom[2], (double)q.z - mom[3]};
+        double a[3], phi;
+        ewald_warp(d, mom, P, real, kv, lane, a, phi);
+        if (lane == 0) {
+            const int id = porder[br.x + i];
+            const double gm = g * mass[id];
+            outf[3 * id] = gm * a[0];
+            outf[3 * id + 1] = gm * a[1];
+            outf[3 * id + 2] = gm * a[2];
+            outp[id] = gm * phi;
+        }
+    }
+}
+
+void dm_kernel_spec(const char *cls, int64_t out[5])
+{
+    (void)cls;  // "ewald_member"
+    const void *fn = (const void *)ewald_slot_kernel;
+    cudaFuncAttributes a;
+    GC_CUDA(cudaFuncGetAttributes(&a, fn));
+    int blocks = 0;
+    GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, 256, 0));
+    out[0] = 256;
+    out[1] = a.numRegs;
+    out[2] = (int64_t)a.sharedSizeBytes;
+    out[3] = 8;  // one member request per warp
+    out[4] = blocks;
 }
 
 }  // namespace gc
@@ -763,6 +812,53 @@ gc_status gc_bh_run_members(gc_bh *bh, gc_dm *dm, const int64_t *member_buckets,
             check_launch("force_slot_kernel");
         }
         GC_CUDA(cudaEventRecord(bh->ev[3], s));
+    });
+}
+
+/* One combined "ewald" request on the device: member m = DFS bucket
+ * member_buckets[m], its one buffer (the bucket) at the last plan's address
+ * bounds[m]; corrections go to the handle's Ewald arrays (gc_bh_get_ewald). */
+gc_status gc_bh_run_ewald(gc_bh *bh, gc_dm *dm, const int64_t *member_buckets, int32_t n_members,
+                          const double params[5], double g)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && dm && params && bh->have_tree && n_members >= 0, GC_E_STATE, "bad argument");
+        GC_REQUIRE((int)dm->h_bounds.size() == n_members + 1, GC_E_STATE, "members do not match the last plan");
+        for (int m = 0; m < n_members; ++m)
+            GC_REQUIRE(dm->h_bounds[m + 1] - dm->h_bounds[m] == 1, GC_E_VALUE, "an ewald request has one buffer");
+        GC_REQUIRE(params[0] > 0 && params[2] >= 0 && params[3] > 0 && params[4] > 0, GC_E_VALUE, "bad Ewald parameters");
+        {
+            const gc_status st = gc_bh_ewald_moments(bh, nullptr);
+            GC_REQUIRE(st == GC_OK, st, gc_last_error());
+        }
+        cudaStream_t s = dm->ctx->stream;
+        std::vector<int> mb(std::max(n_members, 1));
+        for (int m = 0; m < n_members; ++m) {
+            GC_REQUIRE(member_buckets[m] >= 0 && member_buckets[m] < bh->n_buckets, GC_E_VALUE, "bad bucket");
+            mb[m] = (int)member_buckets[m];
+        }
+        dm->members.upload(mb.data(), n_members, s);
+        std::vector<double4> real, kv;
+        const EwaldParams P = ewald_setup(params, real, kv);
+        bh->d_ew_real.upload(real.data(), real.size(), s);
+        bh->d_ew_k.upload(kv.data(), std::max<size_t>(kv.size(), 1), s);
+        if (bh->d_ewf.n != (size_t)(3 * bh->n)) {
+            bh->d_ewf.resize(3 * bh->n);
+            bh->d_ewp.resize(bh->n);
+            bh->d_ewf.zero(s);
+            bh->d_ewp.zero(s);
+        }
+        const int slot_f4 = (int)(dm->slot_bytes / 16);
+        GC_CUDA(cudaEventRecord(bh->ev[2], s));  // member kernel time -> gc_bh_timings out[1]
+        GC_CUDA(cudaEventRecord(bh->ev[4], s));
+        if (n_members > 0) {
+            ewald_slot_kernel<<<grid_for(n_members, 8), 256, 0, s>>>(
+                n_members, dm->members.p, dm->bounds.p, dm->addr.p, bh->d_brange.p, bh->d_porder.p, bh->ws.mass.p,
+                dm->pool.p, slot_f4, bh->d_ew_mom.p, P, bh->d_ew_real.p, bh->d_ew_k.p, g, bh->d_ewf.p, bh->d_ewp.p);
+            check_launch("ewald_slot_kernel");
+        }
+        GC_CUDA(cudaEventRecord(bh->ev[3], s));
+        GC_CUDA(cudaStreamSynchronize(s));  // the host tables go out of scope
     });
 }
 

@@ -25,6 +25,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "md_common.cuh"
 
 namespace gc {
 
@@ -60,33 +61,6 @@ __device__ __forceinline__ bool md_forward(int dx, int dy, int dz)
 {
     // half shell (md.py:21 in 2-D; its 3-D analogue in the oracle)
     return dx > 0 || (dx == 0 && dy > 0) || (dx == 0 && dy == 0 && dz > 0);
-}
-
-// numpy floor_divide / remainder for floats (npy_divmod)
-__device__ __forceinline__ double np_floordiv(double a, double b)
-{
-    const double mod = fmod(a, b);
-    double div = __ddiv_rn(__dsub_rn(a, mod), b);
-    if (mod != 0.0 && ((b < 0) != (mod < 0))) div = __dsub_rn(div, 1.0);
-    double fd;
-    if (div != 0.0) {
-        fd = floor(div);
-        if (__dsub_rn(div, fd) > 0.5) fd = __dadd_rn(fd, 1.0);
-    } else {
-        fd = copysign(0.0, __ddiv_rn(a, b));
-    }
-    return fd;
-}
-
-__device__ __forceinline__ double np_remainder(double a, double b)
-{
-    double mod = fmod(a, b);
-    if (mod != 0.0) {
-        if ((b < 0) != (mod < 0)) mod = __dadd_rn(mod, b);
-    } else {
-        mod = copysign(0.0, b);
-    }
-    return mod;
 }
 
 // md_step integrator (md.py:171-189): v += F dt (unit mass); x += v dt; then

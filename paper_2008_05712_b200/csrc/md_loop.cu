@@ -1,0 +1,745 @@
+// md_loop.cu -- the reference's closed-loop MD (hr/workloads/md.py MDWorkload,
+// md.py:209-271) as ONE persistent cooperative kernel: the message-driven
+// runtime's entry-method counting (hr/runtime.py:95-118) and the step barrier
+// (md.py:238-240, 263-271) run as device-side readiness counters, so the whole
+// run chains its steps without a host round trip.
+//
+// Per step k (the reference's _begin_step ... _on_barrier):
+//   1. patch populations + deterministic patch lists (ascending particle id,
+//      `np.nonzero(patch_of == p)`, md.py:45-46), positions gathered per patch;
+//   2. each non-empty patch delivers its "interact" message to every pair
+//      chare it belongs to (md.py:244-253): atomicAdd on the pair's readiness
+//      counter; the message that completes the entry (1 input for a self pair,
+//      2 for a cross pair, runtime.py:108-110) enqueues the pair's work request
+//      on a device ready queue -- only pairs with items = pop_a * pop_b > 0
+//      exist (pair_work, md.py:82-89);
+//   3. every warp, once its own patches are published, pops work requests
+//      as they become ready and executes them (one warp per request: a pair
+//      of ~24-atom patches is 48 lanes of work, a block would idle): the pair's
+//      force segments of compute_forces (md.py:121-163) in the numba loop order
+//      of md_self_forces / md_cross_forces (kernels.py:104-161), so every sum
+//      is bit-identical to the reference's;
+//   4. each completion is a "work_done" -> "step_barrier" message (md.py:
+//      258-260); the barrier fires when all len(work) requests completed
+//      (a grid-wide sync here), then md_step (md.py:166-190) runs: forces
+//      assembled per atom in compute_forces' accumulation order, Euler update,
+//      walls / wrap, patch reassignment -- and the next step begins.
+//
+// Bit-exactness: every floating-point operation is the reference's, in its
+// order, with explicit round-to-nearest intrinsics (no FMA contraction); the
+// per-atom force is the reference's left-to-right sum over the segments that
+// touch its patch.  The goldens (tests/golden/mdloop.npz) are the reference
+// MDWorkload run through hr/timeline.py.
+#include <cooperative_groups.h>
+#include <cub/cub.cuh>
+
+#include <climits>
+#include <map>
+#include <vector>
+
+#include "common.cuh"
+#include "md_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace gc {
+
+#ifndef ML_TPB_SET
+#define ML_TPB_SET 512
+#endif
+constexpr int ML_TPB = ML_TPB_SET;
+#ifndef ML_MINB
+#define ML_MINB 2
+#endif
+constexpr int ML_WARPS = ML_TPB / 32;
+
+struct LoopArgs {
+    // topology (static; host-built from neighbor_pairs / compute_forces)
+    int n, np, npair, nseg, rows, cols, periodic, steps;
+    double ps, cutoff, c2, stiffness, dt, hx, hy;
+    const int2 *pair;  // neighbor_pairs order (a, b)
+    const int *pair_seg_ptr, *pair_seg;  // pair -> its compute_forces segments
+    const int *patch_pair_ptr, *patch_pair;  // patch -> pairs it sends "interact" to
+    const int2 *seg;  // compute_forces segment (P, q); q == P: self
+    const double2 *seg_shift;  // periodic image shift of q
+    const int *patch_seg_ptr, *patch_seg;  // patch -> (seg << 1 | side) in accumulation order
+    const int *own_seg_ptr, *own_pair_ptr;  // segments / pairs listed under each patch (contiguous)
+    // state
+    double2 *pos, *vel;
+    int *patch_of, *slot_of;
+    // per-step scratch
+    int *pop2;  // [2][np]: populations, double-buffered by step parity
+    int *fill, *start, *tmp, *order;
+    double2 *spos;  // positions in patch order
+    int *seg_off;  // [nseg + 1]
+    double2 *out;  // per-segment contributions: side a then side b
+    int *ready, *queue;  // per pair: readiness counter; ready queue (pair ids, -1 = empty)
+    int *ctr2;  // [2][4]: head, tail, done, messages; [2][4 + 0] ntask at +4
+    long long *stats;  // [steps][4]: work requests, interact messages, completions, barrier
+    long long *phase_ns;  // [steps][6]: %globaltimer at the phase boundaries (block 0)
+};
+
+__device__ __forceinline__ long long ml_now()
+{
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ double2 ml_ld(const double2 *p) { return __ldcg(p); }
+__device__ __forceinline__ int ml_ld(const int *p) { return __ldcg(p); }
+
+// the reference's pair force (kernels.py:112-122): f = (a - b) * mag, or
+// nothing when r2 >= c2 or r2 < 1e-12 (most candidate pairs: the square root
+// and division run only inside the cutoff)
+__device__ __forceinline__ bool ml_pair(const double2 a, const double2 b, const LoopArgs &A, double2 &f)
+{
+    const double dx = __dsub_rn(a.x, b.x), dy = __dsub_rn(a.y, b.y);
+    const double r2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+    if (r2 >= A.c2 || r2 < 1e-12) return false;
+    const double r = __dsqrt_rn(r2);
+    const double mag = __ddiv_rn(__dmul_rn(A.stiffness, __dsub_rn(A.cutoff, r)), r);
+    f.x = __dmul_rn(dx, mag);
+    f.y = __dmul_rn(dy, mag);
+    return true;
+}
+
+// acc +/-= f over partners p[t0..t1) in order (the reference's loop order);
+// PFIRST: the partner is the pair's first atom, f(p[t], x); SHIFT: partner + sh
+template <bool PFIRST, bool SUB, bool SHIFT>
+__device__ __forceinline__ void ml_accum(double2 &acc, const double2 x, const double2 *p, int t0, int t1,
+                                         const double2 sh, const LoopArgs &A)
+{
+    auto get = [&](int t) {
+        double2 y = ml_ld(p + t);
+        if (SHIFT) {
+            y.x = __dadd_rn(y.x, sh.x);
+            y.y = __dadd_rn(y.y, sh.y);
+        }
+        return y;
+    };
+    auto add = [&](bool h, const double2 f) {
+        if (!h) return;
+        acc.x = SUB ? __dsub_rn(acc.x, f.x) : __dadd_rn(acc.x, f.x);
+        acc.y = SUB ? __dsub_rn(acc.y, f.y) : __dadd_rn(acc.y, f.y);
+    };
+    for (int t = t0; t < t1; ++t) {
+        double2 f;
+        const double2 y = get(t);
+        add(PFIRST ? ml_pair(y, x, A, f) : ml_pair(x, y, A, f), f);
+    }
+}
+
+// one work request (one warp): all compute_forces segments of pair k
+__device__ void ml_execute(int k, const LoopArgs &A, const int *pop, const int lane)
+{
+    const double2 zero = make_double2(0.0, 0.0);
+    for (int t = A.pair_seg_ptr[k]; t < A.pair_seg_ptr[k + 1]; ++t) {
+        const int s = A.pair_seg[t];
+        const int2 sg = A.seg[s];
+        const int na = ml_ld(pop + sg.x), s0 = ml_ld(A.start + sg.x);
+        const double2 *pa = A.spos + s0;
+        double2 *o = A.out + ml_ld(A.seg_off + s);
+        if (sg.y == sg.x) {
+            // md_self_forces loop: atom m receives -= f(i, m) for i < m, then += f(m, j) for j > m
+            for (int m = lane; m < na; m += 32) {
+                const double2 am = ml_ld(pa + m);
+                double2 acc = zero;
+                ml_accum<true, true, false>(acc, am, pa, 0, m, zero, A);
+                ml_accum<false, false, false>(acc, am, pa, m + 1, na, zero, A);
+                o[m] = acc;
+            }
+        } else {
+            // md_cross_forces loop with pb = positions[ib] + shift (md.py:157-159):
+            // fa[i] += f(a_i, b_j) over j, fb[j] -= f(a_i, b_j) over i
+            const int nb = ml_ld(pop + sg.y);
+            const double2 *pb = A.spos + ml_ld(A.start + sg.y);
+            const double2 sh = A.seg_shift[s];
+            for (int m = lane; m < na + nb; m += 32) {
+                double2 acc = zero;
+                if (m < na) {
+                    ml_accum<false, false, true>(acc, ml_ld(pa + m), pb, 0, nb, sh, A);
+                } else {
+                    double2 b = ml_ld(pb + (m - na));
+                    b.x = __dadd_rn(b.x, sh.x);
+                    b.y = __dadd_rn(b.y, sh.y);
+                    ml_accum<true, true, false>(acc, b, pa, 0, na, zero, A);
+                }
+                o[m] = acc;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(ML_TPB, ML_MINB) md_loop_kernel(const LoopArgs A)
+{
+    cg::grid_group grid = cg::this_grid();
+    const int gtid = blockIdx.x * ML_TPB + threadIdx.x;
+    const int gsize = gridDim.x * ML_TPB;
+    const int lane = threadIdx.x & 31;
+    const int gwarp = blockIdx.x * ML_WARPS + (threadIdx.x >> 5);
+    const int nwarps = gridDim.x * ML_WARPS;
+
+    for (int k = 0; k < A.steps; ++k) {
+        const int par = k & 1;
+        int *pop = A.pop2 + par * A.np;
+        int *ctr = A.ctr2 + par * 8;  // head, tail, done, messages, ntask
+
+        long long *tm = A.phase_ns + 6ll * k;
+        if (gtid == 0) tm[0] = ml_now();
+        // 1a. populations (PatchGrid.populations, md.py:47)
+        for (int i = gtid; i < A.n; i += gsize) atomicAdd(pop + ml_ld(A.patch_of + i), 1);
+        grid.sync();
+        // 1b. one block: patch starts, segment output offsets and the number of
+        // work requests, all from one chunked pass over the patches (segments
+        // and pairs are listed patch by patch)
+        if (blockIdx.x == 0) {
+            typedef cub::BlockScan<int, ML_TPB> Scan;
+            __shared__ typename Scan::TempStorage ts;
+            const int chunk = (A.np + ML_TPB - 1) / ML_TPB;
+            const int p0 = min(A.np, (int)threadIdx.x * chunk), p1 = min(A.np, p0 + chunk);
+            auto seg_size = [&](int sidx, int na) {
+                const int2 sg = A.seg[sidx];
+                if (sg.y == sg.x) return na;
+                const int nb = ml_ld(pop + sg.y);
+                return nb > 0 ? na + nb : 0;
+            };
+            int cp = 0, cs = 0, ct = 0;
+            for (int p = p0; p < p1; ++p) {
+                const int na = ml_ld(pop + p);
+                cp += na;
+                if (na > 0) {
+                    for (int sidx = A.own_seg_ptr[p]; sidx < A.own_seg_ptr[p + 1]; ++sidx) cs += seg_size(sidx, na);
+                    for (int q = A.own_pair_ptr[p]; q < A.own_pair_ptr[p + 1]; ++q) ct += ml_ld(pop + A.pair[q].y) > 0;
+                }
+            }
+            int xp, xs, xt, tp, tsg, tt;
+            Scan(ts).ExclusiveSum(cp, xp, tp);
+            __syncthreads();
+            Scan(ts).ExclusiveSum(cs, xs, tsg);
+            __syncthreads();
+            Scan(ts).ExclusiveSum(ct, xt, tt);
+            for (int p = p0; p < p1; ++p) {
+                const int na = ml_ld(pop + p);
+                A.start[p] = xp;
+                xp += na;
+                for (int sidx = A.own_seg_ptr[p]; sidx < A.own_seg_ptr[p + 1]; ++sidx) {
+                    A.seg_off[sidx] = xs;
+                    if (na > 0) xs += seg_size(sidx, na);
+                }
+            }
+            if (threadIdx.x == 0) {
+                A.start[A.np] = tp;
+                A.seg_off[A.nseg] = tsg;
+                ctr[4] = tt;
+            }
+        }
+        grid.sync();
+        if (gtid == 0) tm[1] = ml_now();
+        // 1c. scatter particle ids into their patch's range
+        for (int i = gtid; i < A.n; i += gsize) {
+            const int p = ml_ld(A.patch_of + i);
+            A.tmp[ml_ld(A.start + p) + atomicAdd(A.fill + p, 1)] = i;
+        }
+        grid.sync();
+        if (gtid == 0) tm[2] = ml_now();
+        const int ntask = ml_ld(ctr + 4);
+        // 1d + 2. per patch (one warp): ascending-id order, gather, then the
+        // "interact" messages to its pair chares
+        for (int p = gwarp; p < A.np; p += nwarps) {
+            const int m = ml_ld(pop + p), s0 = ml_ld(A.start + p);
+            if (m <= 32) {  // rank by ascending id in registers
+                const int id = lane < m ? ml_ld(A.tmp + s0 + lane) : INT_MAX;
+                int rank = 0;
+                for (int f = 0; f < m; ++f) rank += __shfl_sync(0xffffffffu, id, f) < id;
+                if (lane < m) {
+                    A.order[s0 + rank] = id;
+                    A.spos[s0 + rank] = ml_ld(A.pos + id);
+                    A.slot_of[id] = rank;
+                }
+            } else {
+                for (int e = lane; e < m; e += 32) {
+                    const int id = ml_ld(A.tmp + s0 + e);
+                    int rank = 0;
+                    for (int f = 0; f < m; ++f) rank += ml_ld(A.tmp + s0 + f) < id;
+                    A.order[s0 + rank] = id;
+                    A.spos[s0 + rank] = ml_ld(A.pos + id);
+                    A.slot_of[id] = rank;
+                }
+            }
+            __syncwarp();
+            __threadfence();
+            if (m == 0) continue;
+            for (int t = A.patch_pair_ptr[p] + lane; t < A.patch_pair_ptr[p + 1]; t += 32) {
+                const int q = A.patch_pair[t];
+                const int2 pr = A.pair[q];
+                if (ml_ld(pop + pr.x) == 0 || ml_ld(pop + pr.y) == 0) continue;  // no work request (items 0)
+                atomicAdd(ctr + 3, 1);
+                const int need = pr.x == pr.y ? 1 : 2;
+                if (atomicAdd(A.ready + q, 1) + 1 == need) {  // entry complete: submit the work request
+                    __threadfence();
+                    const int slot = atomicAdd(ctr + 1, 1);
+                    atomicExch(A.queue + slot, q);
+                }
+            }
+        }
+        if (gtid == 0) tm[3] = ml_now();
+        // 3. execute work requests as they become ready (one warp each)
+        for (;;) {
+            int q = -1;
+            if (lane == 0) {
+                const int h = atomicAdd(ctr + 0, 1);
+                if (h < ntask) {
+                    while ((q = atomicAdd(A.queue + h, 0)) < 0) __nanosleep(32);
+                    __threadfence();
+                }
+            }
+            q = __shfl_sync(0xffffffffu, q, 0);
+            if (q < 0) break;
+            ml_execute(q, A, pop, lane);
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(ctr + 2, 1);  // work_done -> step_barrier
+        }
+        // 4. the step barrier: every work request completed
+        grid.sync();
+        if (gtid == 0) {
+            tm[4] = ml_now();
+            long long *st = A.stats + 4ll * k;
+            st[0] = ntask;
+            st[1] = ml_ld(ctr + 3);
+            st[2] = ml_ld(ctr + 2);
+            st[3] = ntask > 0;  // with no work the barrier never fires (max(1, 0) inputs)
+        }
+        if (ntask == 0 || k == A.steps - 1) break;  // the reference stops after `steps` barriers
+        // md_step (md.py:166-190): forces in compute_forces' order, Euler, walls /
+        // wrap, reassignment.  One warp per patch: lane e resolves the patch's
+        // e-th (segment, side) output base, lanes then take the atoms.
+        for (int p = gwarp; p < A.np; p += nwarps) {
+            const int m = ml_ld(pop + p);
+            if (m == 0) continue;
+            const int s0 = ml_ld(A.start + p), e0 = A.patch_seg_ptr[p], ne = A.patch_seg_ptr[p + 1] - e0;
+            int base = -1;
+            if (lane < ne) {
+                const int code = A.patch_seg[e0 + lane], sidx = code >> 1;
+                const int2 sg = A.seg[sidx];
+                const int partner = (code & 1) ? sg.x : sg.y;
+                if (ml_ld(pop + partner) > 0)  // an empty neighbour's segment is skipped
+                    base = ml_ld(A.seg_off + sidx) + ((code & 1) ? ml_ld(pop + sg.x) : 0);
+            }
+            for (int r0 = 0; r0 < m; r0 += 32) {
+                const int r = r0 + lane;
+                double2 f = make_double2(0.0, 0.0);
+                for (int e = 0; e < ne; ++e) {
+                    const int b = __shfl_sync(0xffffffffu, base, e);
+                    if (b >= 0 && r < m) {
+                        const double2 c = ml_ld(A.out + b + r);
+                        f.x = __dadd_rn(f.x, c.x);
+                        f.y = __dadd_rn(f.y, c.y);
+                    }
+                }
+                if (r >= m) continue;
+                const int i = ml_ld(A.order + s0 + r);
+                double2 x = ml_ld(A.spos + s0 + r), v = ml_ld(A.vel + i);
+                v.x = __dadd_rn(v.x, __dmul_rn(f.x, A.dt));
+                v.y = __dadd_rn(v.y, __dmul_rn(f.y, A.dt));
+                x.x = __dadd_rn(x.x, __dmul_rn(v.x, A.dt));
+                x.y = __dadd_rn(x.y, __dmul_rn(v.y, A.dt));
+                double xs[2] = {x.x, x.y}, vs[2] = {v.x, v.y};
+                const double hi[2] = {A.hx, A.hy};
+#pragma unroll
+                for (int d = 0; d < 2; ++d) {
+                    if (A.periodic) {
+                        xs[d] = np_remainder(xs[d], hi[d]);
+                    } else {
+                        if (xs[d] < 0.0) {
+                            xs[d] = -xs[d];
+                            vs[d] = -vs[d];
+                        }
+                        if (xs[d] > hi[d]) {
+                            xs[d] = __dsub_rn(__dmul_rn(2.0, hi[d]), xs[d]);
+                            vs[d] = -vs[d];
+                        }
+                    }
+                }
+                if (!A.periodic)
+#pragma unroll
+                    for (int d = 0; d < 2; ++d) xs[d] = fmin(fmax(xs[d], 0.0), __dsub_rn(hi[d], 1e-12));
+                A.pos[i] = make_double2(xs[0], xs[1]);
+                A.vel[i] = make_double2(vs[0], vs[1]);
+                long long rr = (long long)np_floordiv(xs[0], A.ps), cc = (long long)np_floordiv(xs[1], A.ps);
+                rr = rr < A.rows - 1 ? rr : A.rows - 1;
+                cc = cc < A.cols - 1 ? cc : A.cols - 1;
+                A.patch_of[i] = (int)(rr * A.cols + cc);
+            }
+        }
+        // reset the counters of the next step (the other parity is idle now)
+        int *pop_next = A.pop2 + (par ^ 1) * A.np;
+        for (int p = gtid; p < A.np; p += gsize) {
+            pop_next[p] = 0;
+            A.fill[p] = 0;
+        }
+        for (int q = gtid; q < A.npair; q += gsize) {
+            A.ready[q] = 0;
+            A.queue[q] = -1;
+        }
+        if (gtid < 8) A.ctr2[(par ^ 1) * 8 + gtid] = 0;
+        grid.sync();
+        if (gtid == 0) tm[5] = ml_now();
+    }
+}
+
+}  // namespace gc
+
+using namespace gc;
+
+struct gc_mdloop {
+    gc_ctx *ctx = nullptr;
+    int n = 0, rows = 0, cols = 0, periodic = 0, np = 0, npair = 0, nseg = 0;
+    double ps = 0, cutoff = 0, stiffness = 0;
+    DBuf<int2> pair, seg;
+    DBuf<double2> seg_shift, pos, vel, spos, out;
+    DBuf<int> pair_seg_ptr, pair_seg, patch_pair_ptr, patch_pair, patch_seg_ptr, patch_seg, own_seg_ptr, own_pair_ptr;
+    DBuf<int> patch_of, slot_of, pop2, fill, start, tmp, order, seg_off, ready, queue, ctr2;
+    DBuf<long long> stats, phase_ns;
+    int last_steps = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ~gc_mdloop()
+    {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+    }
+};
+
+namespace {
+
+const int kSteps[4][2] = {{0, 1}, {1, -1}, {1, 0}, {1, 1}};  // md.py:21
+
+// neighbor_pairs (md.py:55-73) and compute_forces' segment enumeration
+// (md.py:129-162), with the maps between them
+void build_topology(gc_mdloop *L)
+{
+    const int R = L->rows, Cn = L->cols, P = L->periodic;
+    const double bx = R * L->ps, by = Cn * L->ps;
+    std::vector<int2> pairs;
+    std::map<std::pair<int, int>, int> key;
+    for (int r = 0; r < R; ++r)
+        for (int c = 0; c < Cn; ++c) {
+            const int p = r * Cn + c;
+            key[{p, p}] = (int)pairs.size();
+            pairs.push_back(make_int2(p, p));
+            for (auto &st : kSteps) {
+                int rr = r + st[0], cc = c + st[1];
+                if (P) {
+                    rr = ((rr % R) + R) % R;
+                    cc = ((cc % Cn) + Cn) % Cn;
+                } else if (!(rr >= 0 && rr < R && cc >= 0 && cc < Cn)) {
+                    continue;
+                }
+                const int q = rr * Cn + cc;
+                const std::pair<int, int> kk{std::min(p, q), std::max(p, q)};
+                if (!key.count(kk)) {
+                    key[kk] = (int)pairs.size();
+                    pairs.push_back(make_int2(p, q));
+                }
+            }
+        }
+    std::vector<int2> segs;
+    std::vector<double2> shifts;
+    for (int r = 0; r < R; ++r)
+        for (int c = 0; c < Cn; ++c) {
+            const int p = r * Cn + c;
+            segs.push_back(make_int2(p, p));
+            shifts.push_back(make_double2(0.0, 0.0));
+            for (auto &st : kSteps) {
+                int rr = r + st[0], cc = c + st[1];
+                double sx = 0.0, sy = 0.0;
+                if (P) {
+                    if (rr == R) {
+                        rr = 0;
+                        sx += bx;
+                    }
+                    if (cc == Cn) {
+                        cc = 0;
+                        sy += by;
+                    } else if (cc == -1) {
+                        cc = Cn - 1;
+                        sy -= by;
+                    }
+                } else if (!(rr >= 0 && rr < R && cc >= 0 && cc < Cn)) {
+                    continue;
+                }
+                const int q = rr * Cn + cc;
+                if (q == p) continue;  // 1-wide periodic grid: no self images (md.py:154-155)
+                segs.push_back(make_int2(p, q));
+                shifts.push_back(make_double2(sx, sy));
+            }
+        }
+    const int np = R * Cn, npair = (int)pairs.size(), nseg = (int)segs.size();
+    // segments and pairs are listed patch by patch: owner ranges
+    std::vector<int> own_seg(np + 1, 0), own_pair(np + 1, 0);
+    for (int sidx = 0; sidx < nseg; ++sidx) own_seg[segs[sidx].x + 1] = sidx + 1;
+    for (int k = 0; k < npair; ++k) own_pair[pairs[k].x + 1] = k + 1;
+    for (int p = 0; p < np; ++p) {
+        own_seg[p + 1] = std::max(own_seg[p + 1], own_seg[p]);
+        own_pair[p + 1] = std::max(own_pair[p + 1], own_pair[p]);
+    }
+    std::vector<std::vector<int>> pseg(npair), ppair(np), patseg(np);
+    for (int s = 0; s < nseg; ++s) {
+        const int a = segs[s].x, b = segs[s].y;
+        pseg[key.at({std::min(a, b), std::max(a, b)})].push_back(s);
+        patseg[a].push_back(s << 1);
+        if (b != a) patseg[b].push_back(s << 1 | 1);
+    }
+    for (int k = 0; k < npair; ++k) {
+        ppair[pairs[k].x].push_back(k);
+        if (pairs[k].y != pairs[k].x) ppair[pairs[k].y].push_back(k);
+    }
+    auto csr = [](const std::vector<std::vector<int>> &v, std::vector<int> &ptr, std::vector<int> &idx) {
+        ptr.assign(1, 0);
+        idx.clear();
+        for (auto &x : v) {
+            idx.insert(idx.end(), x.begin(), x.end());
+            ptr.push_back((int)idx.size());
+        }
+    };
+    std::vector<int> a, b;
+    cudaStream_t s = L->ctx->stream;
+    L->pair.upload(pairs.data(), npair, s);
+    L->seg.upload(segs.data(), nseg, s);
+    L->seg_shift.upload(shifts.data(), nseg, s);
+    csr(pseg, a, b);
+    L->pair_seg_ptr.upload(a.data(), a.size(), s);
+    L->pair_seg.upload(b.data(), b.size(), s);
+    csr(ppair, a, b);
+    L->patch_pair_ptr.upload(a.data(), a.size(), s);
+    L->patch_pair.upload(b.data(), b.size(), s);
+    csr(patseg, a, b);
+    L->patch_seg_ptr.upload(a.data(), a.size(), s);
+    L->patch_seg.upload(b.data(), b.size(), s);
+    L->own_seg_ptr.upload(own_seg.data(), own_seg.size(), s);
+    L->own_pair_ptr.upload(own_pair.data(), own_pair.size(), s);
+    GC_CUDA(cudaStreamSynchronize(s));  // host vectors go out of scope
+    L->np = np;
+    L->npair = npair;
+    L->nseg = nseg;
+}
+
+}  // namespace
+
+extern "C" {
+
+gc_status gc_mdloop_create(gc_ctx *ctx, gc_mdloop **out)
+{
+    return guard([&] {
+        GC_REQUIRE(ctx && out, GC_E_VALUE, "null argument");
+        gc_mdloop *L = new gc_mdloop();
+        L->ctx = ctx;
+        GC_CUDA(cudaEventCreate(&L->e0));
+        GC_CUDA(cudaEventCreate(&L->e1));
+        *out = L;
+    });
+}
+
+gc_status gc_mdloop_destroy(gc_mdloop *L)
+{
+    return guard([&] { delete L; });
+}
+
+gc_status gc_mdloop_set(gc_mdloop *L, int64_t n, const double *pos, const double *vel, const int64_t *patch_of,
+                        int32_t rows, int32_t cols, double patch_size, double cutoff, double stiffness,
+                        int32_t periodic)
+{
+    return guard([&] {
+        GC_REQUIRE(L && n >= 0 && n < (1ll << 28) && (n == 0 || (pos && vel && patch_of)), GC_E_VALUE,
+                   "bad argument");
+        GC_REQUIRE(rows >= 1 && cols >= 1 && (int64_t)rows * cols < (1 << 26), GC_E_VALUE, "bad grid");
+        GC_REQUIRE(patch_size >= cutoff, GC_E_VALUE, "patch size must cover the cutoff distance");
+        L->n = (int)n;
+        L->rows = rows;
+        L->cols = cols;
+        L->ps = patch_size;
+        L->cutoff = cutoff;
+        L->stiffness = stiffness;
+        L->periodic = periodic ? 1 : 0;
+        build_topology(L);
+        std::vector<double2> hp(n), hv(n);
+        std::vector<int> hc(n);
+        for (int64_t i = 0; i < n; ++i) {
+            hp[i] = make_double2(pos[2 * i], pos[2 * i + 1]);
+            hv[i] = make_double2(vel[2 * i], vel[2 * i + 1]);
+            GC_REQUIRE(patch_of[i] >= 0 && patch_of[i] < L->np, GC_E_VALUE, "patch id out of range");
+            hc[i] = (int)patch_of[i];
+        }
+        cudaStream_t s = L->ctx->stream;
+        L->pos.upload(hp.data(), n, s);
+        L->vel.upload(hv.data(), n, s);
+        L->patch_of.upload(hc.data(), n, s);
+        L->slot_of.resize(n);
+        L->tmp.resize(n);
+        L->order.resize(n);
+        L->spos.resize(n);
+        L->out.resize(9 * (size_t)n + 1);  // a patch is in <= 5 segments as side a, <= 4 as side b
+        L->pop2.resize(2 * (size_t)L->np);
+        L->fill.resize(L->np);
+        L->start.resize(L->np + 1);
+        L->seg_off.resize(L->nseg + 1);
+        L->ready.resize(L->npair);
+        L->queue.resize(L->npair);
+        L->ctr2.resize(16);
+        GC_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+// run the closed loop for `steps` barriers (steps - 1 md_step updates, as
+// MDWorkload with MDParams.steps); stats (optional, [steps][4]): work
+// requests, "interact" messages, completions, barrier fired
+gc_status gc_mdloop_run(gc_mdloop *L, int32_t steps, double dt, int64_t *stats)
+{
+    return guard([&] {
+        GC_REQUIRE(L && steps >= 0, GC_E_VALUE, "bad argument");
+        cudaStream_t s = L->ctx->stream;
+        L->stats.resize(4 * (size_t)std::max(steps, 1));
+        L->stats.zero(s);
+        L->phase_ns.resize(6 * (size_t)std::max(steps, 1));
+        L->phase_ns.zero(s);
+        L->last_steps = steps;
+        if (steps == 0 || L->n == 0) {
+            GC_CUDA(cudaEventRecord(L->e0, s));
+            GC_CUDA(cudaEventRecord(L->e1, s));
+            if (stats && steps) std::fill(stats, stats + 4 * (size_t)steps, 0);
+            GC_CUDA(cudaStreamSynchronize(s));
+            return;
+        }
+        L->pop2.zero(s);
+        L->fill.zero(s);
+        L->ready.zero(s);
+        L->ctr2.zero(s);
+        GC_CUDA(cudaMemsetAsync(L->queue.p, 0xff, L->npair * sizeof(int), s));
+        LoopArgs A{};
+        A.n = L->n;
+        A.np = L->np;
+        A.npair = L->npair;
+        A.nseg = L->nseg;
+        A.rows = L->rows;
+        A.cols = L->cols;
+        A.periodic = L->periodic;
+        A.steps = steps;
+        A.ps = L->ps;
+        A.cutoff = L->cutoff;
+        A.c2 = L->cutoff * L->cutoff;
+        A.stiffness = L->stiffness;
+        A.dt = dt;
+        A.hx = L->rows * L->ps;  // PatchGrid.box (md.py:43-44)
+        A.hy = L->cols * L->ps;
+        A.pair = L->pair.p;
+        A.pair_seg_ptr = L->pair_seg_ptr.p;
+        A.pair_seg = L->pair_seg.p;
+        A.patch_pair_ptr = L->patch_pair_ptr.p;
+        A.patch_pair = L->patch_pair.p;
+        A.seg = L->seg.p;
+        A.seg_shift = L->seg_shift.p;
+        A.patch_seg_ptr = L->patch_seg_ptr.p;
+        A.patch_seg = L->patch_seg.p;
+        A.own_seg_ptr = L->own_seg_ptr.p;
+        A.own_pair_ptr = L->own_pair_ptr.p;
+        A.pos = L->pos.p;
+        A.vel = L->vel.p;
+        A.patch_of = L->patch_of.p;
+        A.slot_of = L->slot_of.p;
+        A.pop2 = L->pop2.p;
+        A.fill = L->fill.p;
+        A.start = L->start.p;
+        A.tmp = L->tmp.p;
+        A.order = L->order.p;
+        A.spos = L->spos.p;
+        A.seg_off = L->seg_off.p;
+        A.out = L->out.p;
+        A.ready = L->ready.p;
+        A.queue = L->queue.p;
+        A.ctr2 = L->ctr2.p;
+        A.stats = L->stats.p;
+        A.phase_ns = L->phase_ns.p;
+        int per_sm = 0;
+        GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, md_loop_kernel, ML_TPB, 0));
+        GC_REQUIRE(per_sm > 0, GC_E_KERNELFIT, "md_loop_kernel does not fit on an SM");
+        const int blocks = per_sm * L->ctx->prop.multiProcessorCount;
+        void *kargs[] = {(void *)&A};
+        GC_CUDA(cudaEventRecord(L->e0, s));
+        GC_CUDA(cudaLaunchCooperativeKernel((void *)md_loop_kernel, blocks, ML_TPB, kargs, 0, s));
+        check_launch("md_loop_kernel");
+        GC_CUDA(cudaEventRecord(L->e1, s));
+        if (stats) L->stats.download(reinterpret_cast<long long *>(stats), 4 * (size_t)steps, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+gc_status gc_mdloop_get_state(gc_mdloop *L, double *pos, double *vel, int64_t *patch_of)
+{
+    return guard([&] {
+        GC_REQUIRE(L, GC_E_VALUE, "null argument");
+        cudaStream_t s = L->ctx->stream;
+        const int n = L->n;
+        std::vector<double2> p(n), v(n);
+        std::vector<int> c(n);
+        L->pos.download(p.data(), n, s);
+        L->vel.download(v.data(), n, s);
+        L->patch_of.download(c.data(), n, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        for (int i = 0; i < n; ++i) {
+            if (pos) {
+                pos[2 * i] = p[i].x;
+                pos[2 * i + 1] = p[i].y;
+            }
+            if (vel) {
+                vel[2 * i] = v[i].x;
+                vel[2 * i + 1] = v[i].y;
+            }
+            if (patch_of) patch_of[i] = c[i];
+        }
+    });
+}
+
+gc_status gc_mdloop_topology(gc_mdloop *L, int64_t out[3])
+{
+    return guard([&] {
+        GC_REQUIRE(L && out, GC_E_VALUE, "null argument");
+        out[0] = L->np;
+        out[1] = L->npair;
+        out[2] = L->nseg;
+    });
+}
+
+// per step: ns spent in (counts + scans, scatter, sort/gather/signal, execute
+// + barrier, md_step + resets); out has 5 * steps entries
+gc_status gc_mdloop_phases(gc_mdloop *L, double *out)
+{
+    return guard([&] {
+        GC_REQUIRE(L && out, GC_E_VALUE, "null argument");
+        const int st = L->last_steps;
+        std::vector<long long> t(6 * (size_t)std::max(st, 1));
+        L->phase_ns.download(t.data(), 6 * (size_t)st, L->ctx->stream);
+        GC_CUDA(cudaStreamSynchronize(L->ctx->stream));
+        for (int k = 0; k < st; ++k) {
+            const long long *a = t.data() + 6 * k;
+            const long long end = (k + 1 < st && t[6 * (k + 1)]) ? t[6 * (k + 1)] : a[5];
+            out[5 * k + 0] = double(a[1] - a[0]);
+            out[5 * k + 1] = double(a[2] - a[1]);
+            out[5 * k + 2] = double(a[3] - a[2]);
+            out[5 * k + 3] = double(a[4] - a[3]);
+            out[5 * k + 4] = a[5] ? double(end - a[4]) : 0.0;
+        }
+    });
+}
+
+gc_status gc_mdloop_elapsed(gc_mdloop *L, double *ms)
+{
+    return guard([&] {
+        GC_REQUIRE(L && ms, GC_E_VALUE, "null argument");
+        float t = 0.f;
+        GC_CUDA(cudaEventElapsedTime(&t, L->e0, L->e1));
+        *ms = t;
+    });
+}
+
+}  // extern "C"

@@ -22,6 +22,13 @@ Arrival times are the workload's schedule (the reference's ``_schedule``,
 nbody.py:285-301); batches execute on the device as they are emitted and
 each batch's device time is recorded, so the combine / reuse experiments
 (hr/experiments.py:113-132) run on hardware instead of the cost model.
+
+With ``ewald`` set, every bucket also submits the second kernel class of
+NBodyParams(ewald=True) (nbody.py:317-323): buffers [bucket], item_count
+max(1, n_b), its own trigger state (max_size from the real ewald member
+kernel's occupancy) and its own data manager (the Timeline splits the
+capacity per class, hr/timeline.py:153-155); classes are polled in sorted
+order (hr/timeline.py:262-266).
 """
 
 from __future__ import annotations
@@ -51,6 +58,7 @@ class BatchRecord:
     transactions: int
     emit_time: float
     device_ms: float
+    kernel_class: str = "force"
 
 
 @dataclass
@@ -58,6 +66,8 @@ class RunResult:
     forces: np.ndarray
     batches: list = field(default_factory=list)
     wall_s: float = 0.0
+    ewald_forces: np.ndarray | None = None  # g m_i a_corr (periodic correction), ewald class only
+    ewald_pot: np.ndarray | None = None
 
     @property
     def device_ms(self) -> float:
@@ -90,17 +100,32 @@ class GpuForceExecutor:
 
     def __init__(self, tree, lists, mode: MemoryMode = MemoryMode.REUSE_SORTED, capacity_bytes: int = 8 << 20,
                  slot_bytes: int = 256, g: float = 1.0, eps: float = DEFAULT_SOFTENING,
-                 timeout_factor: float = 2.0, max_size: int | None = None):
+                 timeout_factor: float = 2.0, max_size: int | None = None, ewald=None,
+                 ewald_max_size: int | None = None):
         self.tree = tree
         self.ptr, self.ids, self.kind, self.item_count = lists.csr()
         self.mode = mode
-        self.memory = DeviceMemory(capacity_bytes, slot_bytes, mode)
         self.g, self.eps = g, eps
+        self.ewald = ewald
+        classes = ["ewald", "force"] if ewald is not None else ["force"]
+        per_class = max(slot_bytes, capacity_bytes // len(classes))  # hr/timeline.py:153-155
+        self.memories = {c: DeviceMemory(per_class, slot_bytes, mode) for c in classes}
+        self.memory = self.memories["force"]
         if max_size is None:
             max_size = compute_max_size(b200_kernel_spec("force_member"), b200_device_spec())
-        self.state = AggregatorState("force", int(max_size), timeout_factor)
         self.runtime = Runtime()
-        self.runtime.register_group(self.state)
+        self.states = {"force": AggregatorState("force", int(max_size), timeout_factor)}
+        if ewald is not None:
+            if tree.dim != 3:
+                raise ValueError("the ewald class needs a 3-D tree")
+            if ewald_max_size is None:
+                ewald_max_size = compute_max_size(b200_kernel_spec("ewald_member"), b200_device_spec())
+            self.states["ewald"] = AggregatorState("ewald", int(ewald_max_size), timeout_factor)
+            self.bucket_node = np.asarray(tree.bucket_ids, np.int64)
+            self.bucket_n = np.asarray(tree._load()["pcount"], np.int64)[self.bucket_node]
+        for c in sorted(self.states):
+            self.runtime.register_group(self.states[c])
+        self.state = self.states["force"]
         self._next_id = 0
 
     # -- one combined launch (replaces Timeline._launch_gpu's cost model) ----------
@@ -108,26 +133,34 @@ class GpuForceExecutor:
         return plan_kinds(self.ptr, self.ids, self.kind, buckets, self.mode is MemoryMode.REUSE_SORTED)
 
     def launch(self, combined, now: float) -> BatchRecord:
+        cls = combined.members[0].kernel_class
+        mem = self.memories[cls]
         members = [wr.buffer_indices for wr in combined.members]
         buckets = np.array([wr.owner for wr in combined.members], np.int64)
-        plan, layout = self.memory.build_plan(members, now)
-        kinds = self._member_kinds(buckets)
+        plan, layout = mem.build_plan(members, now)
         npos = int(layout.member_bounds[-1])
-        L.call("gc_dm_stage_bh", self.memory.handle, self.tree.handle)
-        L.call("gc_bh_run_members", self.tree.handle, self.memory.handle, L.ptr(L.i64(buckets), L.i64p),
-               len(buckets), L.ptr(kinds, L.i8p), npos, float(self.g), float(self.eps))
+        L.call("gc_dm_stage_bh", mem.handle, self.tree.handle)
+        if cls == "force":
+            kinds = self._member_kinds(buckets)
+            L.call("gc_bh_run_members", self.tree.handle, mem.handle, L.ptr(L.i64(buckets), L.i64p),
+                   len(buckets), L.ptr(kinds, L.i8p), npos, float(self.g), float(self.eps))
+        else:
+            L.call("gc_bh_run_ewald", self.tree.handle, mem.handle, L.ptr(L.i64(buckets), L.i64p), len(buckets),
+                   L.ptr(self.ewald.array(), L.f64p), float(self.g))
         tm = np.zeros(3)
         L.call("gc_bh_timings", self.tree.handle, L.ptr(tm, L.f64p))  # staging + member kernel (events)
-        self.memory.release_batch(members)
+        mem.release_batch(members)
         self.runtime.on_completion(CompletionEvent(combined.combined_id, [wr.id for wr in combined.members],
                                                    "gpu", now))
         return BatchRecord(combined.combined_id, len(members), npos, len(plan.to_transfer), plan.total_bytes,
-                           plan.indirection_bytes, int(layout.total_transactions()), now, float(tm[0] + tm[1]))
+                           plan.indirection_bytes, int(layout.total_transactions()), now, float(tm[0] + tm[1]), cls)
 
     # -- the force phase ------------------------------------------------------------
     def run(self, arrival_times=None) -> RunResult:
         """One work request per bucket (DFS order) at `arrival_times` (default:
-        back to back); returns the forces and the per-batch log."""
+        back to back) -- plus its ewald request when enabled; returns the
+        forces and the per-batch log."""
+        from .aggregator import make_combined
         nb = len(self.ptr) - 1
         times = np.zeros(nb) if arrival_times is None else np.asarray(arrival_times, float)
         res = RunResult(forces=None)
@@ -136,19 +169,29 @@ class GpuForceExecutor:
             ids = self.ids[self.ptr[b]:self.ptr[b + 1]]
             wr = self.runtime.make_work_request(b, "force", ids, int(self.item_count[b]), times[b])
             self.runtime.submit_work_request(wr, times[b])
-            c = poll_combine(self.state, times[b], self._next_id)
-            if c is not None:
-                res.batches.append(self.launch(c, times[b]))
-                self._next_id += 1
+            if self.ewald is not None:
+                node = int(self.bucket_node[b])
+                ew = self.runtime.make_work_request(b, "ewald", (node,), max(1, int(self.bucket_n[b])), times[b])
+                self.runtime.submit_work_request(ew, times[b])
+            for cls in sorted(self.states):  # hr/timeline.py:262-266
+                c = poll_combine(self.states[cls], times[b], self._next_id)
+                if c is not None:
+                    res.batches.append(self.launch(c, times[b]))
+                    self._next_id += 1
         # end of the phase: drain in max_size chunks (hr/timeline.py:276-298)
         end = float(times[-1]) if nb else 0.0
-        from .aggregator import make_combined
-        while self.state.pending:
-            take = [self.state.pending.popleft() for _ in range(min(self.state.max_size, len(self.state.pending)))]
-            res.batches.append(self.launch(make_combined(take, end, self._next_id), end))
-            self._next_id += 1
+        for cls in sorted(self.states):
+            st = self.states[cls]
+            while st.pending:
+                take = [st.pending.popleft() for _ in range(min(st.max_size, len(st.pending)))]
+                res.batches.append(self.launch(make_combined(take, end, self._next_id), end))
+                self._next_id += 1
         res.wall_s = time.perf_counter() - t0
         out = np.zeros((self.tree.n, self.tree.dim))
         L.call("gc_bh_get_forces", self.tree.handle, L.ptr(out, L.f64p))
         res.forces = out
+        if self.ewald is not None:
+            f, p = np.zeros((self.tree.n, 3)), np.zeros(self.tree.n)
+            L.call("gc_bh_get_ewald", self.tree.handle, L.ptr(f, L.f64p), L.ptr(p, L.f64p))
+            res.ewald_forces, res.ewald_pot = f, p
         return res

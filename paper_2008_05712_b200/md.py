@@ -184,3 +184,98 @@ class LJSystem:
     def task_count(self) -> int:
         """Cell-pair work requests per step: self + 13 half-shell pairs per cell."""
         return 14 * self.dims[0] * self.dims[1] * self.dims[2]
+
+
+# -- closed-loop MD on the device (SURVEY.md §8f-3) ---------------------------------
+
+@dataclass
+class MDParams:
+    """hr/workloads/md.py:193-206 (the timing fields drive only the
+    reference's simulated clock; the device loop runs as fast as it can)."""
+    rows: int = 10
+    cols: int = 10
+    particles_per_patch: int = 24
+    cutoff: float = 1.0
+    steps: int = 12
+    dt: float = 0.08
+    stiffness: float = 25.0
+    seed: int = 7
+    ready_cost: float = 0.01
+    migrate_cost: float = 2.0
+    bytes_per_item: int = 16
+    periodic: bool = False
+
+
+@dataclass
+class ClosedLoopResult:
+    """Per-step counts of the device's message-driven loop and the runtime's
+    invocation totals (hr/runtime.py InvocationRecord, per entry method)."""
+    work_requests: np.ndarray  # per step: len(pair_work) submitted
+    interact_messages: np.ndarray  # per step: "interact" messages delivered
+    completions: np.ndarray  # per step: work_done messages into the barrier
+    barriers: int  # step_barrier invocations
+    device_ms: float
+
+    @property
+    def invocations(self) -> dict:
+        return {"interact": int(self.work_requests.sum()), "work_done": int(self.completions.sum()),
+                "step_barrier": int(self.barriers)}
+
+
+class MDWorkload:
+    """Closed-loop MD run (md.py:209-271) executed on the device: step k+1's
+    requests only arrive after step k's barrier, all inside one persistent
+    kernel (csrc/md_loop.cu).  ``run()`` replaces ``setup(tl)`` + ``tl.run()``
+    of the simulator; ``grid`` and ``step`` end as the reference's do."""
+
+    kernel_class = "md"
+
+    def __init__(self, params: MDParams):
+        self.params = params
+        self.grid, _ = gen_md_system((params.rows, params.cols), params.particles_per_patch, params.cutoff,
+                                     params.seed)
+        self.step = 0
+        self._ctx = L.context()
+        self.handle = C.c_void_p()
+        L.call("gc_mdloop_create", self._ctx.handle, C.byref(self.handle))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                L.load().gc_mdloop_destroy(self.handle)
+        except Exception:
+            pass
+
+    def kernel_classes(self) -> list:
+        return ["md"]
+
+    def topology(self) -> tuple:
+        """(patches, pair chares, compute_forces segments)."""
+        out = np.zeros(3, np.int64)
+        L.call("gc_mdloop_topology", self.handle, L.ptr(out, L.i64p))
+        return tuple(int(x) for x in out)
+
+    def phases_ns(self) -> np.ndarray:
+        """(steps, 5) ns per phase of the last run: counts + scans, scatter,
+        patch sort / gather / messages, execution + barrier, md_step."""
+        out = np.zeros((max(self.params.steps, 1), 5))
+        L.call("gc_mdloop_phases", self.handle, L.ptr(out, L.f64p))
+        return out[:self.params.steps]
+
+    def run(self) -> ClosedLoopResult:
+        p, g = self.params, self.grid
+        pos, vel, pc = L.f64(g.positions), L.f64(g.velocities), L.i64(g.patch_of)
+        L.call("gc_mdloop_set", self.handle, len(pos), L.ptr(pos, L.f64p), L.ptr(vel, L.f64p), L.ptr(pc, L.i64p),
+               int(g.rows), int(g.cols), float(g.patch_size), float(g.cutoff), float(p.stiffness),
+               int(bool(p.periodic)))
+        stats = np.zeros((max(p.steps, 1), 4), np.int64)
+        L.call("gc_mdloop_run", self.handle, int(p.steps), float(p.dt), L.ptr(stats, L.i64p))
+        n = len(pos)
+        g.positions, g.velocities, g.patch_of = np.zeros((n, 2)), np.zeros((n, 2)), np.zeros(n, np.int64)
+        L.call("gc_mdloop_get_state", self.handle, L.ptr(g.positions, L.f64p), L.ptr(g.velocities, L.f64p),
+               L.ptr(g.patch_of, L.i64p))
+        ms = np.zeros(1)
+        L.call("gc_mdloop_elapsed", self.handle, L.ptr(ms, L.f64p))
+        stats = stats[:p.steps]
+        self.step = int(stats[:, 3].sum())
+        return ClosedLoopResult(stats[:, 0].copy(), stats[:, 1].copy(), stats[:, 2].copy(), self.step, float(ms[0]))
