@@ -518,6 +518,47 @@ def bench_md8m(args):
             "algorithmic_bytes_per_step": task_bytes}
 
 
+def bench_md_closed_loop(args):
+    """the reference's closed-loop MDWorkload (67 x 67 x 24 =
+    107,736 atoms, 22,045 work requests per step) run entirely on the device
+    (readiness counters, ready queue, step barrier, md_step in one kernel),
+    against the oracle's md2d_step (the reference's float64 arithmetic, C)."""
+    from oracle import oracle as orc
+    from paper_2008_05712_b200.md import MDParams, MDWorkload
+
+    p = MDParams(rows=67, cols=67, steps=101, dt=0.02)
+    MDWorkload(MDParams(rows=67, cols=67, steps=3, dt=0.02)).run()  # warm-up
+    wl = MDWorkload(p)
+    g0 = (wl.grid.positions.copy(), wl.grid.velocities.copy(), wl.grid.patch_of.copy())
+    res = wl.run()
+    t = time.perf_counter()
+    orc.md2d_step(*g0, 67, 67, 1.0, 1.0, p.dt, p.stiffness, False)
+    cpu_ms = (time.perf_counter() - t) * 1e3
+    return {"workload": "MDWorkload 67x67x24 (107,736 atoms), 101 barriers / 100 md_step updates, one kernel",
+            "ms_per_step": res.device_ms / p.steps, "work_requests_per_step": int(res.work_requests.mean()),
+            "interact_messages_per_step": int(res.interact_messages.mean()),
+            "cpu_oracle_ms_per_md_step": cpu_ms, "parity": "bit-identical to the reference MDWorkload (goldens)"}
+
+
+def bench_ewald(args):
+    """Ewald correction of 1M points from a root multipole
+    (float64; 343 real-space replicas + 80 Fourier vectors per point)."""
+    from paper_2008_05712_b200 import ewald
+
+    import torch
+
+    rng = np.random.default_rng(3)
+    x = rng.random((1 << 20, 3))
+    mom = ewald.multipole_moments(x[:4096], np.ones(4096))
+    ewald.ewald_correction(x[:1024], mom)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    ewald.ewald_correction(x, mom)
+    wall = time.perf_counter() - t
+    return {"workload": "1,048,576 points, ChaNGa defaults (alpha 2/L, nrep 3, ewcut 2.6, hcut 2.8)",
+            "wall_ms_incl_h2d_d2h": wall * 1e3, "points_per_s": len(x) / wall}
+
+
 def run_ours(args, world, rank, local):
     import torch
 
@@ -558,6 +599,8 @@ def run_ours(args, world, rank, local):
         line["runtime_path"] = bench_runtime_path(args)
         line["plummer16m"] = bench_plummer16m(args)
         line["md8m"] = bench_md8m(args)
+        line["md_closed_loop"] = bench_md_closed_loop(args)
+        line["ewald"] = bench_ewald(args)
     if world == 1 and not args.no_cpu_baseline:
         c_inter, c_ts, cores = cpu_bh(bh["ps"], 1)
         line["cpu_baseline"] = {"value": c_inter / c_ts[0], "unit": "interactions/s", "cores": cores,

@@ -72,6 +72,8 @@ struct LoopArgs {
     int *fill, *start, *tmp, *order;
     double2 *spos;  // positions in patch order
     int *seg_off;  // [nseg + 1]
+    int2 *psz;  // per patch: owned segment output size, owned work requests
+    int *segbase;  // per patch: first output slot of its owned segments
     double2 *out;  // per-segment contributions: side a then side b
     int *ready, *queue;  // per pair: readiness counter; ready queue (pair ids, -1 = empty)
     int *ctr2;  // [2][4]: head, tail, done, messages; [2][4 + 0] ntask at +4
@@ -88,6 +90,7 @@ __device__ __forceinline__ long long ml_now()
 
 __device__ __forceinline__ double2 ml_ld(const double2 *p) { return __ldcg(p); }
 __device__ __forceinline__ int ml_ld(const int *p) { return __ldcg(p); }
+__device__ __forceinline__ int2 ml_ld(const int2 *p) { return __ldcg(p); }
 
 // the reference's pair force (kernels.py:112-122): f = (a - b) * mag, or
 // nothing when r2 >= c2 or r2 < 1e-12 (most candidate pairs: the square root
@@ -130,8 +133,106 @@ __device__ __forceinline__ void ml_accum(double2 &acc, const double2 x, const do
     }
 }
 
+constexpr int ML_R = 4, ML_C = 64;  // pair-matrix tile per warp: ML_R rows x ML_C partners (double2)
+
+// One cross segment on the pair matrix: each pair is evaluated once (lanes
+// over the tile), then fa[i] = sum_j f(a_i, b_j) and fb[j] = -sum_i f(a_i, b_j)
+// are summed in the reference's order (rows: j ascending; columns: i
+// ascending, tile by tile).  A skipped pair contributes an exact +0.0, the
+// identity on sums that start at +0.0.  nb <= ML_C.
+__device__ __forceinline__ void ml_cross_tile(const double2 *pa, int na, const double2 *pb, int nb, const double2 sh,
+                                              double2 *o, double2 *buf, const LoopArgs &A, int lane)
+{
+    double2 cb0 = make_double2(0.0, 0.0), cb1 = cb0;
+    double2 bj0 = cb0, bj1 = cb0;
+    if (lane < nb) {
+        bj0 = ml_ld(pb + lane);
+        bj0.x = __dadd_rn(bj0.x, sh.x);
+        bj0.y = __dadd_rn(bj0.y, sh.y);
+    }
+    if (lane + 32 < nb) {
+        bj1 = ml_ld(pb + lane + 32);
+        bj1.x = __dadd_rn(bj1.x, sh.x);
+        bj1.y = __dadd_rn(bj1.y, sh.y);
+    }
+    for (int i0 = 0; i0 < na; i0 += ML_R) {
+        const int rows = min(ML_R, na - i0);
+        for (int r = 0; r < rows; ++r) {
+            const double2 ai = ml_ld(pa + i0 + r);
+            double2 f0 = make_double2(0.0, 0.0), f1 = f0, f;
+            if (lane < nb && ml_pair(ai, bj0, A, f)) f0 = f;
+            if (lane + 32 < nb && ml_pair(ai, bj1, A, f)) f1 = f;
+            buf[r * ML_C + lane] = f0;
+            buf[r * ML_C + lane + 32] = f1;
+            cb0.x = __dsub_rn(cb0.x, f0.x);
+            cb0.y = __dsub_rn(cb0.y, f0.y);
+            cb1.x = __dsub_rn(cb1.x, f1.x);
+            cb1.y = __dsub_rn(cb1.y, f1.y);
+        }
+        __syncwarp();
+        if (lane < rows) {
+            double2 acc = make_double2(0.0, 0.0);
+            const double2 *row = buf + lane * ML_C;
+            for (int j = 0; j < nb; ++j) {
+                const double2 f = row[j];
+                acc.x = __dadd_rn(acc.x, f.x);
+                acc.y = __dadd_rn(acc.y, f.y);
+            }
+            o[i0 + lane] = acc;
+        }
+        __syncwarp();
+    }
+    if (lane < nb) o[na + lane] = cb0;
+    if (lane + 32 < nb) o[na + lane + 32] = cb1;
+}
+
+// One self segment on the pair matrix (md_self_forces order for atom m:
+// -f(i, m) for i < m ascending, then +f(m, j) for j > m ascending).  na <= ML_C.
+__device__ __forceinline__ void ml_self_tile(const double2 *pa, int na, double2 *o, double2 *buf, const LoopArgs &A,
+                                             int lane)
+{
+    double2 c0 = make_double2(0.0, 0.0), c1 = c0;  // running sums of atoms lane, lane + 32
+    const double2 x0 = lane < na ? ml_ld(pa + lane) : c0;
+    const double2 x1 = lane + 32 < na ? ml_ld(pa + lane + 32) : c0;
+    for (int i0 = 0; i0 < na; i0 += ML_R) {
+        const int rows = min(ML_R, na - i0);
+        for (int r = 0; r < rows; ++r) {
+            const int i = i0 + r;
+            const double2 ai = ml_ld(pa + i);
+            double2 f0 = make_double2(0.0, 0.0), f1 = f0, f;
+            if (lane > i && lane < na && ml_pair(ai, x0, A, f)) f0 = f;
+            if (lane + 32 > i && lane + 32 < na && ml_pair(ai, x1, A, f)) f1 = f;
+            buf[r * ML_C + lane] = f0;
+            buf[r * ML_C + lane + 32] = f1;
+            if (lane > i) {  // column part: atom j = lane receives -f(i, j)
+                c0.x = __dsub_rn(c0.x, f0.x);
+                c0.y = __dsub_rn(c0.y, f0.y);
+            }
+            if (lane + 32 > i) {
+                c1.x = __dsub_rn(c1.x, f1.x);
+                c1.y = __dsub_rn(c1.y, f1.y);
+            }
+        }
+        __syncwarp();
+        // row part of the tile's atoms m = i0 + r, on the lane that holds m's sum
+        for (int r = 0; r < rows; ++r) {
+            const int m = i0 + r;
+            if ((m & 31) != lane) continue;
+            double2 acc = m < 32 ? c0 : c1;
+            const double2 *row = buf + r * ML_C;
+            for (int j = m + 1; j < na; ++j) {
+                const double2 f = row[j];
+                acc.x = __dadd_rn(acc.x, f.x);
+                acc.y = __dadd_rn(acc.y, f.y);
+            }
+            o[m] = acc;
+        }
+        __syncwarp();
+    }
+}
+
 // one work request (one warp): all compute_forces segments of pair k
-__device__ void ml_execute(int k, const LoopArgs &A, const int *pop, const int lane)
+__device__ void ml_execute(int k, const LoopArgs &A, const int *pop, const int lane, double2 *buf)
 {
     const double2 zero = make_double2(0.0, 0.0);
     for (int t = A.pair_seg_ptr[k]; t < A.pair_seg_ptr[k + 1]; ++t) {
@@ -141,6 +242,10 @@ __device__ void ml_execute(int k, const LoopArgs &A, const int *pop, const int l
         const double2 *pa = A.spos + s0;
         double2 *o = A.out + ml_ld(A.seg_off + s);
         if (sg.y == sg.x) {
+            if (na <= ML_C) {
+                ml_self_tile(pa, na, o, buf, A, lane);
+                continue;
+            }
             // md_self_forces loop: atom m receives -= f(i, m) for i < m, then += f(m, j) for j > m
             for (int m = lane; m < na; m += 32) {
                 const double2 am = ml_ld(pa + m);
@@ -155,6 +260,10 @@ __device__ void ml_execute(int k, const LoopArgs &A, const int *pop, const int l
             const int nb = ml_ld(pop + sg.y);
             const double2 *pb = A.spos + ml_ld(A.start + sg.y);
             const double2 sh = A.seg_shift[s];
+            if (nb <= ML_C) {
+                ml_cross_tile(pa, na, pb, nb, sh, o, buf, A, lane);
+                continue;
+            }
             for (int m = lane; m < na + nb; m += 32) {
                 double2 acc = zero;
                 if (m < na) {
@@ -179,6 +288,7 @@ __global__ void __launch_bounds__(ML_TPB, ML_MINB) md_loop_kernel(const LoopArgs
     const int lane = threadIdx.x & 31;
     const int gwarp = blockIdx.x * ML_WARPS + (threadIdx.x >> 5);
     const int nwarps = gridDim.x * ML_WARPS;
+    extern __shared__ double2 ml_buf[];  // ML_WARPS pair-matrix tiles
 
     for (int k = 0; k < A.steps; ++k) {
         const int par = k & 1;
@@ -190,28 +300,37 @@ __global__ void __launch_bounds__(ML_TPB, ML_MINB) md_loop_kernel(const LoopArgs
         // 1a. populations (PatchGrid.populations, md.py:47)
         for (int i = gtid; i < A.n; i += gsize) atomicAdd(pop + ml_ld(A.patch_of + i), 1);
         grid.sync();
-        // 1b. one block: patch starts, segment output offsets and the number of
-        // work requests, all from one chunked pass over the patches (segments
-        // and pairs are listed patch by patch)
+        // 1b. per patch (all threads): atoms, output size of the segments it
+        // owns, work requests it owns (segments and pairs are listed patch by
+        // patch); then one block scans the three columns
+        auto seg_size = [&](int sidx, int na) {
+            const int2 sg = A.seg[sidx];
+            if (sg.y == sg.x) return na;
+            const int nb = ml_ld(pop + sg.y);
+            return nb > 0 ? na + nb : 0;
+        };
+        for (int p = gtid; p < A.np; p += gsize) {
+            const int na = ml_ld(pop + p);
+            int cs = 0, ct = 0;
+            if (na > 0) {
+                for (int sidx = A.own_seg_ptr[p]; sidx < A.own_seg_ptr[p + 1]; ++sidx) cs += seg_size(sidx, na);
+                for (int q = A.own_pair_ptr[p]; q < A.own_pair_ptr[p + 1]; ++q) ct += ml_ld(pop + A.pair[q].y) > 0;
+            }
+            A.psz[p] = make_int2(cs, ct);
+        }
+        grid.sync();
         if (blockIdx.x == 0) {
             typedef cub::BlockScan<int, ML_TPB> Scan;
             __shared__ typename Scan::TempStorage ts;
             const int chunk = (A.np + ML_TPB - 1) / ML_TPB;
             const int p0 = min(A.np, (int)threadIdx.x * chunk), p1 = min(A.np, p0 + chunk);
-            auto seg_size = [&](int sidx, int na) {
-                const int2 sg = A.seg[sidx];
-                if (sg.y == sg.x) return na;
-                const int nb = ml_ld(pop + sg.y);
-                return nb > 0 ? na + nb : 0;
-            };
             int cp = 0, cs = 0, ct = 0;
+#pragma unroll 4
             for (int p = p0; p < p1; ++p) {
-                const int na = ml_ld(pop + p);
-                cp += na;
-                if (na > 0) {
-                    for (int sidx = A.own_seg_ptr[p]; sidx < A.own_seg_ptr[p + 1]; ++sidx) cs += seg_size(sidx, na);
-                    for (int q = A.own_pair_ptr[p]; q < A.own_pair_ptr[p + 1]; ++q) ct += ml_ld(pop + A.pair[q].y) > 0;
-                }
+                const int2 z = ml_ld(A.psz + p);
+                cp += ml_ld(pop + p);
+                cs += z.x;
+                ct += z.y;
             }
             int xp, xs, xt, tp, tsg, tt;
             Scan(ts).ExclusiveSum(cp, xp, tp);
@@ -219,14 +338,12 @@ __global__ void __launch_bounds__(ML_TPB, ML_MINB) md_loop_kernel(const LoopArgs
             Scan(ts).ExclusiveSum(cs, xs, tsg);
             __syncthreads();
             Scan(ts).ExclusiveSum(ct, xt, tt);
+#pragma unroll 4
             for (int p = p0; p < p1; ++p) {
-                const int na = ml_ld(pop + p);
                 A.start[p] = xp;
-                xp += na;
-                for (int sidx = A.own_seg_ptr[p]; sidx < A.own_seg_ptr[p + 1]; ++sidx) {
-                    A.seg_off[sidx] = xs;
-                    if (na > 0) xs += seg_size(sidx, na);
-                }
+                A.segbase[p] = xs;
+                xp += ml_ld(pop + p);
+                xs += ml_ld(A.psz + p).x;
             }
             if (threadIdx.x == 0) {
                 A.start[A.np] = tp;
@@ -236,7 +353,15 @@ __global__ void __launch_bounds__(ML_TPB, ML_MINB) md_loop_kernel(const LoopArgs
         }
         grid.sync();
         if (gtid == 0) tm[1] = ml_now();
-        // 1c. scatter particle ids into their patch's range
+        // 1c. scatter particle ids into their patch's range; segment offsets
+        for (int p = gtid; p < A.np; p += gsize) {
+            const int na = ml_ld(pop + p);
+            int x = ml_ld(A.segbase + p);
+            for (int sidx = A.own_seg_ptr[p]; sidx < A.own_seg_ptr[p + 1]; ++sidx) {
+                A.seg_off[sidx] = x;
+                if (na > 0) x += seg_size(sidx, na);
+            }
+        }
         for (int i = gtid; i < A.n; i += gsize) {
             const int p = ml_ld(A.patch_of + i);
             A.tmp[ml_ld(A.start + p) + atomicAdd(A.fill + p, 1)] = i;
@@ -246,6 +371,7 @@ __global__ void __launch_bounds__(ML_TPB, ML_MINB) md_loop_kernel(const LoopArgs
         const int ntask = ml_ld(ctr + 4);
         // 1d + 2. per patch (one warp): ascending-id order, gather, then the
         // "interact" messages to its pair chares
+        int msgs = 0;
         for (int p = gwarp; p < A.np; p += nwarps) {
             const int m = ml_ld(pop + p), s0 = ml_ld(A.start + p);
             if (m <= 32) {  // rank by ascending id in registers
@@ -270,36 +396,58 @@ __global__ void __launch_bounds__(ML_TPB, ML_MINB) md_loop_kernel(const LoopArgs
             __syncwarp();
             __threadfence();
             if (m == 0) continue;
-            for (int t = A.patch_pair_ptr[p] + lane; t < A.patch_pair_ptr[p + 1]; t += 32) {
-                const int q = A.patch_pair[t];
-                const int2 pr = A.pair[q];
-                if (ml_ld(pop + pr.x) == 0 || ml_ld(pop + pr.y) == 0) continue;  // no work request (items 0)
-                atomicAdd(ctr + 3, 1);
-                const int need = pr.x == pr.y ? 1 : 2;
-                if (atomicAdd(A.ready + q, 1) + 1 == need) {  // entry complete: submit the work request
+            // warp-aggregated: one queue reservation per 32 pairs
+            const int t0 = A.patch_pair_ptr[p], t1 = A.patch_pair_ptr[p + 1];
+            for (int tb = t0; tb < t1; tb += 32) {
+                const int t = tb + lane;
+                int q = -1;
+                bool done = false;
+                if (t < t1) {
+                    q = A.patch_pair[t];
+                    const int2 pr = A.pair[q];
+                    if (ml_ld(pop + pr.x) > 0 && ml_ld(pop + pr.y) > 0) {  // a work request exists (items > 0)
+                        ++msgs;
+                        const int need = pr.x == pr.y ? 1 : 2;
+                        done = atomicAdd(A.ready + q, 1) + 1 == need;  // entry complete: submit the request
+                    }
+                }
+                const unsigned dm = __ballot_sync(0xffffffffu, done);
+                if (dm) {
                     __threadfence();
-                    const int slot = atomicAdd(ctr + 1, 1);
-                    atomicExch(A.queue + slot, q);
+                    int base = 0;
+                    if (lane == 0) base = atomicAdd(ctr + 1, __popc(dm));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (done) atomicExch(A.queue + base + __popc(dm & ((1u << lane) - 1)), q);
                 }
             }
         }
+        {
+            int w = msgs;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+            if (lane == 0 && w) atomicAdd(ctr + 3, w);
+        }
         if (gtid == 0) tm[3] = ml_now();
         // 3. execute work requests as they become ready (one warp each)
-        for (;;) {
-            int q = -1;
-            if (lane == 0) {
-                const int h = atomicAdd(ctr + 0, 1);
-                if (h < ntask) {
-                    while ((q = atomicAdd(A.queue + h, 0)) < 0) __nanosleep(32);
-                    __threadfence();
+        {
+            int ndone = 0;
+            for (;;) {
+                int q = -1;
+                if (lane == 0) {
+                    const int h = atomicAdd(ctr + 0, 1);
+                    if (h < ntask) {
+                        while ((q = atomicAdd(A.queue + h, 0)) < 0) __nanosleep(32);
+                        __threadfence();
+                    }
                 }
+                q = __shfl_sync(0xffffffffu, q, 0);
+                if (q < 0) break;
+                ml_execute(q, A, pop, lane, ml_buf + (threadIdx.x >> 5) * (ML_R * ML_C));
+                ++ndone;
             }
-            q = __shfl_sync(0xffffffffu, q, 0);
-            if (q < 0) break;
-            ml_execute(q, A, pop, lane);
             __threadfence();
             __syncwarp();
-            if (lane == 0) atomicAdd(ctr + 2, 1);  // work_done -> step_barrier
+            if (lane == 0 && ndone) atomicAdd(ctr + 2, ndone);  // work_done -> step_barrier
         }
         // 4. the step barrier: every work request completed
         grid.sync();
@@ -400,7 +548,8 @@ struct gc_mdloop {
     DBuf<int2> pair, seg;
     DBuf<double2> seg_shift, pos, vel, spos, out;
     DBuf<int> pair_seg_ptr, pair_seg, patch_pair_ptr, patch_pair, patch_seg_ptr, patch_seg, own_seg_ptr, own_pair_ptr;
-    DBuf<int> patch_of, slot_of, pop2, fill, start, tmp, order, seg_off, ready, queue, ctr2;
+    DBuf<int> patch_of, slot_of, pop2, fill, start, tmp, order, seg_off, ready, queue, ctr2, segbase;
+    DBuf<int2> psz;
     DBuf<long long> stats, phase_ns;
     int last_steps = 0;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -584,6 +733,8 @@ gc_status gc_mdloop_set(gc_mdloop *L, int64_t n, const double *pos, const double
         L->fill.resize(L->np);
         L->start.resize(L->np + 1);
         L->seg_off.resize(L->nseg + 1);
+        L->psz.resize(L->np);
+        L->segbase.resize(L->np);
         L->ready.resize(L->npair);
         L->queue.resize(L->npair);
         L->ctr2.resize(16);
@@ -654,19 +805,23 @@ gc_status gc_mdloop_run(gc_mdloop *L, int32_t steps, double dt, int64_t *stats)
         A.order = L->order.p;
         A.spos = L->spos.p;
         A.seg_off = L->seg_off.p;
+        A.psz = L->psz.p;
+        A.segbase = L->segbase.p;
         A.out = L->out.p;
         A.ready = L->ready.p;
         A.queue = L->queue.p;
         A.ctr2 = L->ctr2.p;
         A.stats = L->stats.p;
         A.phase_ns = L->phase_ns.p;
+        const size_t smem = sizeof(double2) * ML_WARPS * ML_R * ML_C;
+        GC_CUDA(cudaFuncSetAttribute(md_loop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
-        GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, md_loop_kernel, ML_TPB, 0));
+        GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, md_loop_kernel, ML_TPB, smem));
         GC_REQUIRE(per_sm > 0, GC_E_KERNELFIT, "md_loop_kernel does not fit on an SM");
         const int blocks = per_sm * L->ctx->prop.multiProcessorCount;
         void *kargs[] = {(void *)&A};
         GC_CUDA(cudaEventRecord(L->e0, s));
-        GC_CUDA(cudaLaunchCooperativeKernel((void *)md_loop_kernel, blocks, ML_TPB, kargs, 0, s));
+        GC_CUDA(cudaLaunchCooperativeKernel((void *)md_loop_kernel, blocks, ML_TPB, kargs, smem, s));
         check_launch("md_loop_kernel");
         GC_CUDA(cudaEventRecord(L->e1, s));
         if (stats) L->stats.download(reinterpret_cast<long long *>(stats), 4 * (size_t)steps, s);
