@@ -100,6 +100,11 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
 /* Tree build on the GPU (device != 0, the default) or the host C++ build;
  * both are bit-identical to build_bucket_tree.  Applies to the next
  * gc_bh_set_particles / gc_bh_step. */
+/* 1 (default): the reorganisation into per-force-group source runs happens in
+ * shared memory inside the force kernel; 0: expand_kernel writes the runs to an
+ * HBM staging buffer first (A/B and the HBM roofline of the staging layer).
+ * Forces are bit-identical either way. */
+gc_status gc_bh_set_force_mode(gc_bh *bh, int32_t fused);
 gc_status gc_bh_set_build_mode(gc_bh *bh, int32_t device);
 /* Sizes: out[0..4] = n_nodes, n_buckets, per-bucket list entries, union
  * entries of the last device walk, source records they expand to (staging) */

@@ -57,6 +57,7 @@ SIGNATURES = {
     "gc_bh_set_particles": [vp, C.c_int64, C.c_int32, f64p, f64p, C.c_double, C.c_int64],
     "gc_bh_sizes": [vp, i64p],
     "gc_bh_set_build_mode": [vp, C.c_int32],
+    "gc_bh_set_force_mode": [vp, C.c_int32],
     "gc_bh_get_tree": [vp, f64p, f64p, f64p, f64p, i64p, i32p, i64p, i64p, i64p],
     "gc_bh_walk": [vp, C.c_double],
     "gc_bh_get_lists": [vp, i64p, i64p, i8p, i64p],

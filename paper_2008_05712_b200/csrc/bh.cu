@@ -470,6 +470,35 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
         U.gfirst += f0;
         U.gcount += f0;
         U.grec += f0;
+        if (bh->force_fused) {  // reorganisation into shared memory inside the force kernel
+            bh->d_next.resize(1);
+            bh->d_next.zero(s);
+            const bool lpt = bh->order_nf == nfg && bh->order_rg0 == g0;
+            if (!lpt) {
+                bh->d_fg_order.resize(nfg);
+                if (nfg > 0) bb_iota_kernel<<<grid_for(nfg, 256), 256, 0, s>>>(nfg, bh->d_fg_order.p);
+            }
+            Staging S{};
+            S.order = lpt ? bh->d_fg_lpt.p : bh->d_fg_order.p;
+            S.next = bh->d_next.p;
+            GC_CUDA(cudaEventRecord(bh->ev[4], s));
+            auto k = eps0 ? (pot ? force_fused_kernel<true, true> : force_fused_kernel<true, false>)
+                          : (pot ? force_fused_kernel<false, true> : force_fused_kernel<false, false>);
+            if (nfg > 0) {
+                int per_sm = 0;
+                GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * WARPS_PER_BLOCK, 0));
+                const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(
+                    (int64_t)per_sm * ctx->prop.multiProcessorCount, grid_for(nfg, WARPS_PER_BLOCK)));
+                k<<<pgrid, 32 * WARPS_PER_BLOCK, 0, s>>>(nfg, bh->d_fg.p + f0, U, S, bh->d_parts.p, bh->d_rec_hi.p,
+                                                         bh->d_rec_lo.p, bh->d_part_bucket.p, bh->d_porder.p,
+                                                         bh->d_wg.p, bh->cgrid, eps2, g, bh->dim, bh->d_out.p,
+                                                         bh->d_pot.p);
+                check_launch("force_fused_kernel");
+            }
+            if (!bh->orders_fresh) make_orders(bh);
+            GC_CUDA(cudaEventRecord(bh->ev[3], s));
+            return;
+        }
         // staging runs: exclusive scan of the rounded record counts
         bh->d_rbase.resize(nfg + 1);
         {
@@ -591,6 +620,14 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
             bh->ws.pos.upload(pos, (size_t)n * dim, bh->ctx->stream);  // float64 copies (Ewald moments)
             bh->ws.mass.upload(mass, (size_t)n, bh->ctx->stream);
         }
+    });
+}
+
+gc_status gc_bh_set_force_mode(gc_bh *bh, int32_t fused)
+{
+    return guard([&] {
+        GC_REQUIRE(bh, GC_E_VALUE, "null argument");
+        bh->force_fused = fused != 0;
     });
 }
 

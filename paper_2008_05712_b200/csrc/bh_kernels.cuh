@@ -35,7 +35,13 @@ constexpr int QWIN = 128;  // window of expanded source records per warp
 constexpr int FLUSH = 8;  // fp32 partial sums are flushed to fp64 every FLUSH records (the mask loads assume 8)
 constexpr int NODE_BITS = 26;  // stack entries pack node | level << NODE_BITS
 
-constexpr int BPL = 2;  // buckets per lane in the walk
+#ifndef GC_BPL
+#define GC_BPL 2
+#endif
+#ifndef WALK_HALF_SKIP
+#define WALK_HALF_SKIP 0
+#endif
+constexpr int BPL = GC_BPL;  // buckets per lane in the walk
 constexpr int WG_BUCKETS = 32 * BPL;  // buckets per walk group (lane l holds buckets l, l + 32, ...)
 
 struct WalkGroup {
@@ -157,14 +163,16 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
     const WalkGroup gd = groups[g];
     // lane holds buckets lane and lane + 32 of the group
     float4 bf[BPL];
-    float s0[BPL];  // NaN: geometry not float32-exact, always take the float64 test
+    u64 inexact = 0ull;  // geometry not float32-exact: always take the float64 test
 #pragma unroll
     for (int k = 0; k < BPL; ++k) {
         const int j = lane + 32 * k;
         bf[k] = j < gd.nbucket ? bgeo32[gd.bfirst + j] : make_float4(0.f, 0.f, 0.f, -1.f);
-        s0[k] = bf[k].w >= 0.f ? 0.f : __int_as_float(0x7fc00000);
+        inexact |= (u64)__ballot_sync(0xffffffffu, bf[k].w < 0.f) << (32 * k);
+        bf[k].w = fabsf(bf[k].w);
     }
     const u64 full = gd.nbucket >= 64 ? ~0ull : ((1ull << gd.nbucket) - 1ull);
+    const u64 exact = ~inexact;
     int2 *stack = stack_s[warp];
     unsigned *sact = act_hi_s[warp];
     unsigned char *slvl = lvl_s[warp];
@@ -208,14 +216,18 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
             u64 acc = 0ull, rej = 0ull;
 #pragma unroll
             for (int k = 0; k < BPL; ++k) {
+#if WALK_HALF_SKIP
+                if (BPL > 1 && (unsigned)(act >> (32 * k)) == 0u) continue;  // warp-uniform: no active bucket here
+#endif
                 const float v0 = fmaxf(fabsf(nd.x - bf[k].x) - bf[k].w, 0.f);
                 const float v1 = fmaxf(fabsf(nd.y - bf[k].y) - bf[k].w, 0.f);
                 const float v2 = fmaxf(fabsf(nd.z - bf[k].z) - bf[k].w, 0.f);
-                const float sv = fmaf(v2, v2, fmaf(v1, v1, fmaf(v0, v0, s0[k])));
+                const float sv = fmaf(v2, v2, fmaf(v1, v1, v0 * v0));
                 acc |= (u64)__ballot_sync(0xffffffffu, sv > th.x) << (32 * k);
                 rej |= (u64)__ballot_sync(0xffffffffu, sv < th.y) << (32 * k);
             }
-            acc &= act;
+            acc &= act & exact;
+            rej &= exact;
             const u64 unsure = ~rej & ~acc & act;
             if (unsure) {  // rare: the reference's float64 test (warp-uniform branch)
 #pragma unroll
@@ -700,6 +712,206 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int *_
             if (dim > 2) out[(int64_t)orig * dim + 2] = gm * az;
             if (POT) pot_out[orig] = -gm * ap;  // -G m_i sum_j m_j / sqrt(r^2 + eps^2)
         }
+        if (lane == 0) slot = atomicAdd(S.next, 1);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// FUSED reorganisation + force (the default step): the same record sequence
+// EXPAND would write into the group's HBM staging run is produced straight
+// into a per-warp shared-memory ring, already in the PAIR layout the packed
+// force loop reads, and consumed PFLUSH records at a time.  Record order,
+// PFLUSH grouping and end padding equal the staged path's, so forces are
+// bit-identical to expand_kernel + force_group_kernel; the 1.4 GB staging
+// round trip through HBM disappears (sources are gathered from the
+// L2-resident tree records and particles).
+// ---------------------------------------------------------------------------
+#ifndef FUSED_PREFETCH
+#define FUSED_PREFETCH 1
+#endif
+#ifndef FUSED_RING
+#define FUSED_RING 128
+#endif
+constexpr int RING = FUSED_RING;
+constexpr int RING_LOW = RING / 2;  // produce while fewer records wait (RING >= RING_LOW + 33: one entry always fits)
+template <bool EPS0, bool POT>
+__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, FORCE_MINB)
+force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U, const Staging S,
+                   const float4 *__restrict__ parts, const float4 *__restrict__ rec_hi,
+                   const float4 *__restrict__ rec_lo, const int *__restrict__ part_bucket,
+                   const int *__restrict__ porder, const WalkGroup *__restrict__ wgroups, float cgrid, float eps2,
+                   double g, int dim, double *__restrict__ out, double *__restrict__ pot_out)
+{
+    __shared__ __align__(16) float4 r_a[WARPS_PER_BLOCK][RING / 2];  // pairs: x0 x1 y0 y1
+    __shared__ __align__(16) float4 r_b[WARPS_PER_BLOCK][RING / 2];  // pairs: z0 z1 m0 m1
+    __shared__ __align__(16) unsigned r_m[WARPS_PER_BLOCK][RING];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float *ra = reinterpret_cast<float *>(r_a[warp]);
+    float *rb = reinterpret_cast<float *>(r_b[warp]);
+    unsigned *rm = r_m[warp];
+    const float2 e2 = f2(eps2, eps2);
+    // record pos -> ring: pair (pos % RING) / 2, half pos & 1
+    auto put = [&](int pos, float x, float y, float z, float m, unsigned msk) {
+        const int q = pos & (RING - 1), o = (q >> 1) * 4 + (q & 1);
+        ra[o] = x;
+        ra[o + 2] = y;
+        rb[o] = z;
+        rb[o + 2] = m;
+        rm[q] = msk;
+    };
+    for (int slot = lane == 0 ? atomicAdd(S.next, 1) : 0;;) {
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if (slot >= nfg) break;
+        const int gi = S.order[slot];
+        const ForceGroup fg = fgroups[gi];
+        const bool tgt = lane < fg.ntarget;
+        const int p = fg.pstart + (tgt ? lane : 0);
+        const float4 xp = parts[p];
+        const unsigned mybit = tgt ? (1u << (part_bucket[p] - wgroups[fg.wg].bfirst - fg.boff)) : 0u;
+        const GroupFrame F = group_frame(xp, cgrid);
+        const float2 nx = f2(F.cx - xp.x, F.cx - xp.x), ny = f2(F.cy - xp.y, F.cy - xp.y),
+                     nz = f2(F.cz - xp.z, F.cz - xp.z);
+        double ax = 0.0, ay = 0.0, az = 0.0, ap = 0.0;
+        const int n = U.gcount[gi];
+        int chunk_cur = n > 0 ? U.gfirst[gi] : 0, cur_ci = 0;
+        int chunk_nxt = (n > CHUNK) ? U.cnext[chunk_cur] : 0;
+        int ebase = 0, wr = 0, rd = 0;
+        auto load_entry = [&](int e) {
+            int4 en = make_int4(0, 0, 0, 0);
+            if (e < n) {
+                const int c = (e / CHUNK == cur_ci) ? chunk_cur : chunk_nxt;
+                en = U.ent[(int64_t)c * CHUNK + (e & (CHUNK - 1))];
+            }
+            return en;
+        };
+#if FUSED_PREFETCH
+        int pf_base = -1;
+        int4 en_pf = make_int4(0, 0, 0, 0);
+#if FUSED_PREFETCH > 1
+        float4 h_pf = make_float4(0.f, 0.f, 0.f, 0.f), l_pf = h_pf;
+#endif
+#endif
+        for (;;) {
+            // produce: whole entries, in order, while the ring holds < RING_LOW records
+            while (ebase < n && wr - rd < RING_LOW) {
+                const int e = ebase + lane;
+#if FUSED_PREFETCH
+                const int4 en = pf_base == ebase ? en_pf : load_entry(e);
+#else
+                const int4 en = load_entry(e);
+#endif
+                const unsigned mx = (unsigned)en.y, my = (unsigned)en.z;
+                const int hasnode = mx ? 1 : 0;
+                const int pc = my ? wr_pcount(en.w) : 0;
+                const int cnt = hasnode + pc;
+                int incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                const bool take = e < n && incl <= RING - (wr - rd);
+                const unsigned tm = __ballot_sync(0xffffffffu, take);
+                const int ntake = __popc(tm);  // incl is nondecreasing: the taken lanes are a prefix
+                const int total = ntake ? __shfl_sync(0xffffffffu, incl, ntake - 1) : 0;
+                if (take) {
+                    const int r = wr + incl - cnt;
+                    if (mx) {
+#if FUSED_PREFETCH > 1
+                        const bool pre = pf_base == ebase;
+                        const float4 h = pre ? h_pf : rec_hi[en.x], l = pre ? l_pf : rec_lo[en.x];
+#else
+                        const float4 h = rec_hi[en.x], l = rec_lo[en.x];
+#endif
+                        put(r, (h.x - F.cx) + l.x, (h.y - F.cy) + l.y, (h.z - F.cz) + l.z, h.w, mx);
+                    }
+                    const float4 *src = parts + wr_pstart(en.w);
+                    for (int k = 0; k < pc; ++k) {
+                        const float4 q = src[k];
+                        put(r + hasnode + k, q.x - F.cx, q.y - F.cy, q.z - F.cz, q.w, my);
+                    }
+                }
+                wr += total;
+                ebase += ntake;
+                if (ebase / CHUNK != cur_ci && ebase < n) {  // moved into the next chunk of the chain
+                    chunk_cur = chunk_nxt;
+                    cur_ci = ebase / CHUNK;
+                    chunk_nxt = ((cur_ci + 1) * CHUNK < n) ? U.cnext[chunk_cur] : 0;
+                }
+            }
+#if FUSED_PREFETCH
+            if (ebase < n) {  // the next batch's entries load while this one is consumed
+                en_pf = load_entry(ebase + lane);
+                pf_base = ebase;
+#if FUSED_PREFETCH > 1
+                if (en_pf.y) {
+                    h_pf = rec_hi[en_pf.x];
+                    l_pf = rec_lo[en_pf.x];
+                }
+#endif
+            }
+#endif
+            if (ebase >= n && wr - rd < PFLUSH && wr > rd) {  // end of the run: pad the last group
+                const int padded = (wr + PFLUSH - 1) & ~(PFLUSH - 1);
+                if (wr + lane < padded) put(wr + lane, 0.f, 0.f, 0.f, 0.f, 0u);
+                wr = padded;
+            }
+            if (wr - rd < PFLUSH) break;  // ebase == n and the ring is empty
+            __syncwarp();
+            // consume every complete PFLUSH group
+            for (; wr - rd >= PFLUSH; rd += PFLUSH) {
+                const int q0 = rd & (RING - 1);
+                const float4 *qa = r_a[warp] + q0 / 2;
+                const float4 *qb = r_b[warp] + q0 / 2;
+                const unsigned *qm = rm + q0;
+                float2 sx = f2(0.f, 0.f), sy = f2(0.f, 0.f), sz = f2(0.f, 0.f), sp = f2(0.f, 0.f);
+#pragma unroll
+                for (int kk = 0; kk < PFLUSH; kk += 4) {
+                    const uint4 k4 = *reinterpret_cast<const uint4 *>(qm + kk);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const float4 A = qa[kk / 2 + h];
+                        const float4 B = qb[kk / 2 + h];
+                        const unsigned k0 = h ? k4.z : k4.x, k1 = h ? k4.w : k4.y;
+                        const float2 dx = __fadd2_rn(f2(A.x, A.y), nx);
+                        const float2 dy = __fadd2_rn(f2(A.z, A.w), ny);
+                        const float2 dz = __fadd2_rn(f2(B.x, B.y), nz);
+                        float2 r2 = __ffma2_rn(dz, dz, e2);
+                        r2 = __ffma2_rn(dy, dy, r2);
+                        r2 = __ffma2_rn(dx, dx, r2);
+                        const float2 r6 = __fmul2_rn(__fmul2_rn(r2, r2), r2);
+                        float i0 = rsqrt_approx(r6.x), i1 = rsqrt_approx(r6.y);
+                        if (EPS0) {  // coincident source (kernels.py:83-84)
+                            i0 = r2.x > 0.f ? i0 : 0.f;
+                            i1 = r2.y > 0.f ? i1 : 0.f;
+                        }
+                        const float2 me = f2((k0 & mybit) ? B.z : 0.f, (k1 & mybit) ? B.w : 0.f);
+                        const float2 w = __fmul2_rn(me, f2(i0, i1));
+                        sx = __ffma2_rn(dx, w, sx);
+                        sy = __ffma2_rn(dy, w, sy);
+                        sz = __ffma2_rn(dz, w, sz);
+                        if (POT) {
+                            const float2 wp = f2(r2.x != eps2 ? w.x : 0.f, r2.y != eps2 ? w.y : 0.f);
+                            sp = __ffma2_rn(wp, r2, sp);
+                        }
+                    }
+                }
+                ax += (double)(sx.x + sx.y);
+                ay += (double)(sy.x + sy.y);
+                az += (double)(sz.x + sz.y);
+                if (POT) ap += (double)(sp.x + sp.y);
+            }
+            __syncwarp();  // consumed slots are rewritten by the next production
+        }
+        if (tgt) {
+            const int orig = porder[p];
+            const double gm = g * (double)xp.w;
+            out[(int64_t)orig * dim + 0] = gm * ax;
+            if (dim > 1) out[(int64_t)orig * dim + 1] = gm * ay;
+            if (dim > 2) out[(int64_t)orig * dim + 2] = gm * az;
+            if (POT) pot_out[orig] = -gm * ap;
+        }
+        __syncwarp();
         if (lane == 0) slot = atomicAdd(S.next, 1);
     }
 }

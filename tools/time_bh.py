@@ -9,10 +9,12 @@ from paper_2008_05712_b200 import _lib as L  # noqa: E402
 from paper_2008_05712_b200 import generators as gen  # noqa: E402
 from paper_2008_05712_b200 import nbody  # noqa: E402
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
+n = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 1_000_000
 ps = gen.fp32_exact(gen.gen_particles(n, 42, clustering=0.6, dim=3))
 tree = nbody.build_bucket_tree(ps, 8)
 ctx = L.context()
+staged = "staged" in sys.argv
+L.call("gc_bh_set_force_mode", tree.handle, 0 if staged else 1)
 tm = np.zeros(3)
 w, f, r = [], [], []
 for i in range(12):
@@ -25,5 +27,5 @@ for i in range(12):
         r.append(tm[2])
 inter = nbody.interactions(tree)
 fm = statistics.median(f)
-print(f"{L.LIB_PATH.split('/')[-1]}: walk {statistics.median(w):.3f} ms  reorg {statistics.median(r):.3f} ms  force {fm:.3f} ms  "
+print(f"{L.LIB_PATH.split('/')[-1]} {'staged' if staged else 'fused'}: walk {statistics.median(w):.3f} ms  reorg {statistics.median(r):.3f} ms  force {fm:.3f} ms  "
       f"{20 * inter / fm / 1e9:.2f} TFLOP/s ({inter} interactions)")
