@@ -105,6 +105,9 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
  * HBM staging buffer first (A/B and the HBM roofline of the staging layer).
  * Forces are bit-identical either way. */
 gc_status gc_bh_set_force_mode(gc_bh *bh, int32_t fused);
+/* walk instrumentation, only in builds with -DWALK_PROF=1 (zeros otherwise):
+ * out = node visits, sum of active buckets, visits with an empty half, decisions */
+gc_status gc_debug_walk_prof(int64_t out[4], int32_t reset);
 gc_status gc_bh_set_build_mode(gc_bh *bh, int32_t device);
 /* Sizes: out[0..4] = n_nodes, n_buckets, per-bucket list entries, union
  * entries of the last device walk, source records they expand to (staging) */

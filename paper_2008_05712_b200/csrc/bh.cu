@@ -623,6 +623,27 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
     });
 }
 
+// walk instrumentation (builds with -DWALK_PROF=1 only; zeros otherwise):
+// node visits, sum of active buckets, visits with an empty half, decisions emitted
+gc_status gc_debug_walk_prof(int64_t out[4], int32_t reset)
+{
+    return guard([&] {
+        GC_REQUIRE(out, GC_E_VALUE, "null argument");
+#if WALK_PROF
+        unsigned long long v[4];
+        GC_CUDA(cudaMemcpyFromSymbol(v, g_walk_prof, sizeof(v)));
+        for (int k = 0; k < 4; ++k) out[k] = (int64_t)v[k];
+        if (reset) {
+            const unsigned long long z[4] = {0, 0, 0, 0};
+            GC_CUDA(cudaMemcpyToSymbol(g_walk_prof, z, sizeof(z)));
+        }
+#else
+        (void)reset;
+        for (int k = 0; k < 4; ++k) out[k] = 0;
+#endif
+    });
+}
+
 gc_status gc_bh_set_force_mode(gc_bh *bh, int32_t fused)
 {
     return guard([&] {

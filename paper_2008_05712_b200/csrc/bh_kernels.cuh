@@ -41,6 +41,13 @@ constexpr int NODE_BITS = 26;  // stack entries pack node | level << NODE_BITS
 #ifndef WALK_HALF_SKIP
 #define WALK_HALF_SKIP 0
 #endif
+#ifndef WALK_PROF
+#define WALK_PROF 0
+#endif
+#if WALK_PROF
+// [node visits, sum popc(act), visits with one half of act empty, sum popc(acc | part)]
+__device__ unsigned long long g_walk_prof[4];
+#endif
 constexpr int BPL = GC_BPL;  // buckets per lane in the walk
 constexpr int WG_BUCKETS = 32 * BPL;  // buckets per walk group (lane l holds buckets l, l + 32, ...)
 
@@ -200,6 +207,9 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
         wp = U.ent + (int64_t)chunk * CHUNK;
     }
     int my_entries[BPL] = {}, my_items[BPL] = {};
+#if WALK_PROF
+    unsigned long long pv = 0, pa = 0, ph = 0, pe = 0;
+#endif
     // the root is a sibling group of one, tested by every bucket
     int first = 0, nc = 1, lvl = 0;
     u64 act = full;
@@ -240,6 +250,12 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
                 }
             }
             const u64 part = is_bucket ? (act & ~acc) : 0ull;
+#if WALK_PROF
+            pv += 1;
+            pa += __popcll(act);
+            ph += ((unsigned)act == 0u || (unsigned)(act >> 32) == 0u) ? 1 : 0;
+            pe += __popcll(acc | part);
+#endif
             if (WRITE) {
                 const unsigned ma = (unsigned)((acc & fgm) >> boff), mp = (unsigned)((part & fgm) >> boff);
                 const bool hit = (ma | mp) != 0u;
@@ -291,6 +307,14 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
         lvl = slvl[sp];
         __syncwarp();
     }
+#if WALK_PROF
+    if (lane == 0) {
+        atomicAdd(&g_walk_prof[0], pv);
+        atomicAdd(&g_walk_prof[1], pa);
+        atomicAdd(&g_walk_prof[2], ph);
+        atomicAdd(&g_walk_prof[3], pe);
+    }
+#endif
     if (WRITE && emits) {
         U.gcount[my_fg] = w;
         U.grec[my_fg] = nrec;

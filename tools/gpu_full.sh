@@ -8,5 +8,5 @@ echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1
 echo "bench rc=$?" >> gpurun_out/bench.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_bench.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"force_group|walk_group|expand_kernel" -s 3 -c 3 -o gpurun_out/prof_bh python tools/prof_bh.py > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"force_fused|force_group|walk_group|expand_kernel" -s 2 -c 8 -o gpurun_out/prof_bh python tools/prof_bh.py > gpurun_out/ncu_full.log 2>&1
 echo done >> gpurun_out/ncu_full.log

@@ -1,4 +1,6 @@
-"""Minimal BH driver for ncu captures: 1M clustered, theta 0.7; walk + forces x3."""
+"""Minimal BH driver for ncu captures: 1M clustered, theta 0.7; walk + forces x3
+(fused force path), then walk + forces once in the staged mode (expand_kernel +
+force_group_kernel) so one capture covers both."""
 import sys
 
 sys.path.insert(0, ".")
@@ -13,5 +15,8 @@ ctx = L.context()
 for _ in range(3):
     L.call("gc_bh_walk", tree.handle, 0.7)
     L.call("gc_bh_forces_async", tree.handle, 1.0, 1e-4)
+L.call("gc_bh_set_force_mode", tree.handle, 0)
+L.call("gc_bh_walk", tree.handle, 0.7)
+L.call("gc_bh_forces_async", tree.handle, 1.0, 1e-4)
 ctx.sync()
 print("interactions", nbody.interactions(tree))
