@@ -341,6 +341,9 @@ def bench_bh(args, world, rank, local, ctx, torch):
         L.call("gc_bh_interactions", stepper.handle, L.ptr(cnt, L.i64p))
         e2e_inter = int(cnt[0])
     achieved = FLOPS_PER_INTERACTION * inter / (f_ms * 1e-3) / 1e12
+    pst = np.zeros(2, np.int64)
+    L.call("gc_bh_pair_stats", tree.handle, L.ptr(pst, L.i64p))
+    issued = FLOPS_PER_INTERACTION * float(pst[0]) / (f_ms * 1e-3) / 1e12
     # reorganisation: union entries read (16 B) + staged records written (16 B record + 4 B mask)
     reorg_bytes = 16 * n_union + 20 * n_records
     sr_ms, sf_ms = statistics.median(st_r), statistics.median(st_f)
@@ -355,6 +358,12 @@ def bench_bh(args, world, rank, local, ctx, torch):
                                     "MEASURED_PEAKS.json", "nominal_peak": NOMINAL_FP32_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / fp32_peak, "traffic": ncu_traffic("force_fused_kernel"),
                      "flops_per_interaction": FLOPS_PER_INTERACTION,
+                     "issued_pairs_per_launch": int(pst[0]) if world == 1 else None,
+                     "issued_frac": issued / fp32_peak if world == 1 else None,
+                     "mask_efficiency": inter / float(pst[1]) if world == 1 and pst[1] else None,
+                     "note": "achieved counts useful interactions only; issued_frac counts every evaluated "
+                             "(lane, record) pair -- lanes without a target and records another bucket of the "
+                             "force group needs are evaluated with mass 0",
                      "interactions_per_launch": inter, "kernel_ms": f_ms},
         "reorg_roofline": {"bound": "hbm", "kernel": "expand_kernel (+ run scan), staged mode", "unit": "GB/s",
                            "achieved": reorg_bytes / (sr_ms * 1e-3) / 1e9, "peak": hbm, "peak_source": hbm_src,

@@ -108,6 +108,10 @@ gc_status gc_bh_set_force_mode(gc_bh *bh, int32_t fused);
 /* walk instrumentation, only in builds with -DWALK_PROF=1 (zeros otherwise):
  * out = node visits, sum of active buckets, visits with an empty half, decisions */
 gc_status gc_debug_walk_prof(int64_t out[4], int32_t reset);
+/* pairs the force kernel evaluates for the current lists: out[0] = padded
+ * source records x 32 lanes summed over force groups, out[1] = padded records
+ * x targets; useful pairs = gc_bh_interactions (full walk-group range) */
+gc_status gc_bh_pair_stats(gc_bh *bh, int64_t out[2]);
 gc_status gc_bh_set_build_mode(gc_bh *bh, int32_t device);
 /* Sizes: out[0..4] = n_nodes, n_buckets, per-bucket list entries, union
  * entries of the last device walk, source records they expand to (staging) */

@@ -867,6 +867,32 @@ gc_status gc_bh_interactions(gc_bh *bh, int64_t *out)
     });
 }
 
+// Pairs the force kernel evaluates for the current union lists: out[0] = sum
+// over force groups of padded records x 32 lanes (issued), out[1] = padded
+// records x targets (lanes with a target); useful interactions are
+// gc_bh_interactions (mask efficiency = useful / out[1]).
+gc_status gc_bh_pair_stats(gc_bh *bh, int64_t out[2])
+{
+    return guard([&] {
+        GC_REQUIRE(bh && bh->have_union && out, GC_E_STATE, "no device walk has run");
+        cudaStream_t s = bh->ctx->stream;
+        const int nf = bh->n_fg;
+        std::vector<int> rec(nf);
+        std::vector<ForceGroup> fg(nf);
+        bh->d_grec.download(rec.data(), nf, s);
+        bh->d_fg.download(fg.data(), nf, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        int64_t issued = 0, lanes = 0;
+        for (int f = 0; f < nf; ++f) {
+            const int64_t padded = (rec[f] + PFLUSH - 1) & ~(PFLUSH - 1);
+            issued += 32 * padded;
+            lanes += (int64_t)fg[f].ntarget * padded;
+        }
+        out[0] = issued;
+        out[1] = lanes;
+    });
+}
+
 gc_status gc_bh_set_range(gc_bh *bh, int64_t wg_begin, int64_t wg_end)
 {
     return guard([&] {
