@@ -41,6 +41,9 @@ constexpr int NODE_BITS = 26;  // stack entries pack node | level << NODE_BITS
 #ifndef WALK_HALF_SKIP
 #define WALK_HALF_SKIP 0
 #endif
+#ifndef WALK_EMIT_SKIP
+#define WALK_EMIT_SKIP 0
+#endif
 #ifndef WALK_PROF
 #define WALK_PROF 0
 #endif
@@ -143,8 +146,15 @@ struct UnionPool {
 // preorder index) for the per-bucket API.  One pass per sibling group
 // amortises the stack traffic over ~7 children.
 // ---------------------------------------------------------------------------
+#ifndef WALK_MINB
+#define WALK_MINB 3
+#endif
+#ifndef WALK_UNROLL
+#define WALK_UNROLL 2
+#endif
+constexpr int kWalkUnroll = WALK_UNROLL;  // sibling-loop unroll
 template <bool WRITE, bool STATS>
-__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, 4)
+__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, WALK_MINB)
 walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const ForceGroup *__restrict__ fgroups,
                   const float4 *__restrict__ recs, const double4 *__restrict__ com64,
                   const double4 *__restrict__ bgeo, const float4 *__restrict__ bgeo32, const WalkParams P,
@@ -217,7 +227,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
         const float2 th = tt_s[lvl];
         const int last = first + nc - 1;
         float4 nd = recs[first];
-#pragma unroll 2
+#pragma unroll kWalkUnroll
         for (int node = first; node <= last; ++node) {
             const float4 nd_next = recs[min(node + 1, last)];  // prefetch the next sibling
             const int wd = __float_as_int(nd.w);
@@ -256,7 +266,11 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
             ph += ((unsigned)act == 0u || (unsigned)(act >> 32) == 0u) ? 1 : 0;
             pe += __popcll(acc | part);
 #endif
+#if WALK_EMIT_SKIP
+            if (WRITE && (acc | part)) {  // warp-uniform: nodes every active bucket opens emit nothing
+#else
             if (WRITE) {
+#endif
                 const unsigned ma = (unsigned)((acc & fgm) >> boff), mp = (unsigned)((part & fgm) >> boff);
                 const bool hit = (ma | mp) != 0u;
                 if (emits) *wp = make_int4(node, (int)ma, (int)mp, wd);
