@@ -9,6 +9,10 @@
 
 #include "bh_state.h"
 
+#ifndef WALK_LPT
+#define WALK_LPT 1  // walk groups heaviest first (0: depth-first order)
+#endif
+
 using namespace gc;
 
 
@@ -302,7 +306,7 @@ void launch_walk(gc_bh *bh, bool write, bool stats)
     bh->d_wnext.zero(s);
     k<<<pgrid, 32 * WARPS_PER_BLOCK, 0, s>>>(ng, wg, bh->d_fg.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p,
                                              bh->d_bgeo32.p, bh->wp, U, bh->d_bstat.p, bh->d_flag.p,
-                                             (bh->order_ng == ng && bh->order_rg0 == g0) ? bh->d_wg_order.p : nullptr,
+                                             (WALK_LPT && bh->order_ng == ng && bh->order_rg0 == g0) ? bh->d_wg_order.p : nullptr,
                                              bh->d_wnext.p);
     check_launch("walk_group_kernel");
 }

@@ -392,9 +392,13 @@ __device__ __forceinline__ void interact(const float4 h, const float3 l, const f
 {
     const float dx = (h.x - xi.x) + l.x, dy = (h.y - xi.y) + l.y, dz = (h.z - xi.z) + l.z;
     const float r2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, eps2)));
-    const float r6 = r2 * r2 * r2;
-    float inv3 = rsqrt_approx(r6);
-    if (EPS0) inv3 = r2 > 0.f ? inv3 : 0.f;  // coincident source (kernels.py:83-84)
+    float inv3;
+    if (EPS0) {  // no softening floor: r^6 may leave the float range, cube 1/r instead
+        const float ir = rsqrt_approx(r2);
+        inv3 = r2 > 0.f ? ir * ir * ir : 0.f;  // coincident source (kernels.py:83-84)
+    } else {
+        inv3 = rsqrt_approx(r2 * r2 * r2);
+    }
     const float w = m_eff * inv3;
     a.x = fmaf(dx, w, a.x);
     a.y = fmaf(dy, w, a.y);
@@ -409,9 +413,13 @@ __device__ __forceinline__ void interact_rel(const float4 q, const float m_eff, 
 {
     const float dx = q.x - xi.x, dy = q.y - xi.y, dz = q.z - xi.z;
     const float r2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, eps2)));
-    const float r6 = r2 * r2 * r2;
-    float inv3 = rsqrt_approx(r6);
-    if (EPS0) inv3 = r2 > 0.f ? inv3 : 0.f;  // coincident source (kernels.py:83-84)
+    float inv3;
+    if (EPS0) {  // no softening floor: r^6 may leave the float range, cube 1/r instead
+        const float ir = rsqrt_approx(r2);
+        inv3 = r2 > 0.f ? ir * ir * ir : 0.f;  // coincident source (kernels.py:83-84)
+    } else {
+        inv3 = rsqrt_approx(r2 * r2 * r2);
+    }
     const float w = m_eff * inv3;
     a.x = fmaf(dx, w, a.x);
     a.y = fmaf(dy, w, a.y);
@@ -716,11 +724,15 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int *_
                         float2 r2 = __ffma2_rn(dz, dz, e2);
                         r2 = __ffma2_rn(dy, dy, r2);
                         r2 = __ffma2_rn(dx, dx, r2);
-                        const float2 r6 = __fmul2_rn(__fmul2_rn(r2, r2), r2);
-                        float i0 = rsqrt_approx(r6.x), i1 = rsqrt_approx(r6.y);
-                        if (EPS0) {  // coincident source (kernels.py:83-84)
-                            i0 = r2.x > 0.f ? i0 : 0.f;
-                            i1 = r2.y > 0.f ? i1 : 0.f;
+                        float i0, i1;
+                        if (EPS0) {  // no softening floor: cube 1/r (r^6 may leave the float range)
+                            const float j0 = rsqrt_approx(r2.x), j1 = rsqrt_approx(r2.y);
+                            i0 = r2.x > 0.f ? j0 * j0 * j0 : 0.f;  // coincident source (kernels.py:83-84)
+                            i1 = r2.y > 0.f ? j1 * j1 * j1 : 0.f;
+                        } else {
+                            const float2 r6 = __fmul2_rn(__fmul2_rn(r2, r2), r2);
+                            i0 = rsqrt_approx(r6.x);
+                            i1 = rsqrt_approx(r6.y);
                         }
                         const float2 me = f2((k0 & mybit) ? B.z : 0.f, (k1 & mybit) ? B.w : 0.f);
                         const float2 w = __fmul2_rn(me, f2(i0, i1));
@@ -917,11 +929,15 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
                         float2 r2 = __ffma2_rn(dz, dz, e2);
                         r2 = __ffma2_rn(dy, dy, r2);
                         r2 = __ffma2_rn(dx, dx, r2);
-                        const float2 r6 = __fmul2_rn(__fmul2_rn(r2, r2), r2);
-                        float i0 = rsqrt_approx(r6.x), i1 = rsqrt_approx(r6.y);
-                        if (EPS0) {  // coincident source (kernels.py:83-84)
-                            i0 = r2.x > 0.f ? i0 : 0.f;
-                            i1 = r2.y > 0.f ? i1 : 0.f;
+                        float i0, i1;
+                        if (EPS0) {  // no softening floor: cube 1/r (r^6 may leave the float range)
+                            const float j0 = rsqrt_approx(r2.x), j1 = rsqrt_approx(r2.y);
+                            i0 = r2.x > 0.f ? j0 * j0 * j0 : 0.f;  // coincident source (kernels.py:83-84)
+                            i1 = r2.y > 0.f ? j1 * j1 * j1 : 0.f;
+                        } else {
+                            const float2 r6 = __fmul2_rn(__fmul2_rn(r2, r2), r2);
+                            i0 = rsqrt_approx(r6.x);
+                            i1 = rsqrt_approx(r6.y);
                         }
                         const float2 me = f2((k0 & mybit) ? B.z : 0.f, (k1 & mybit) ? B.w : 0.f);
                         const float2 w = __fmul2_rn(me, f2(i0, i1));

@@ -207,6 +207,34 @@ def test_device_build_equals_host_build(nb, name, n, seed, cl, dim):
     np.testing.assert_array_equal(fa, fb)
 
 
+@pytest.mark.parametrize("bucket,eps,n", [(32, 0.0, 20_000), (1, 1e-4, 5_000), (8, 0.0, 3)])
+def test_fused_ring_edge_cases(bucket, eps, n):
+    """Opened buckets of 32 particles (33 records from one union entry: the
+    ring's largest unit), one-particle buckets, eps = 0 (coincident-source
+    guard) and a 3-particle system: fused == staged bit for bit, and both
+    within 1e-5 of the oracle."""
+    from oracle import oracle as orc
+    from paper_2008_05712_b200 import _lib as L
+    from paper_2008_05712_b200 import generators as gen
+    from paper_2008_05712_b200 import nbody
+    ps = gen.fp32_exact(gen.gen_particles(n, 21, clustering=0.8, dim=3))
+    tree = nbody.build_bucket_tree(ps, bucket)
+    L.call("gc_bh_walk", tree.handle, 0.5)
+    res = []
+    for mode in (1, 0):
+        L.call("gc_bh_set_force_mode", tree.handle, mode)
+        f = np.zeros((n, 3))
+        L.call("gc_bh_forces", tree.handle, 1.0, eps, L.ptr(f, L.f64p))
+        res.append(f)
+    np.testing.assert_array_equal(res[0], res[1])
+    ot = orc.build_bucket_tree(ps.positions, ps.masses, bucket)
+    ol = orc.build_interaction_lists(ot, 0.5)
+    ref = orc.eval_forces(ot, ol, ps.positions, ps.masses, 1.0, eps)
+    nrm = np.linalg.norm(ref, axis=1)
+    err = np.linalg.norm(res[0] - ref, axis=1) / np.where(nrm > 0, nrm, 1.0)
+    assert err.max() <= 1e-5
+
+
 def test_fused_and_staged_reorganisation_bit_identical():
     """The default force path reorganises each force group's sources into
     shared memory inside the force kernel; the staged path writes the same
