@@ -270,6 +270,7 @@ void walk_params(gc_bh *bh, double theta)
 // One walk launch over the handle's walk-group range (asynchronous).
 void launch_walk(gc_bh *bh, bool write, bool stats)
 {
+    wait_orders(bh);
     cudaStream_t s = bh->ctx->stream;
     const int nf = bh->n_fg;
     const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? bh->n_wg : bh->rg1;
@@ -337,7 +338,15 @@ __global__ void bh_fg_key_kernel(int nf, const int *__restrict__ grec, int *__re
 // (a time step) they are a stale but close hint -- order never changes results.
 void make_orders(gc_bh *bh)
 {
-    cudaStream_t s = bh->ctx->stream;
+    if (!bh->order_stream) {
+        GC_CUDA(cudaStreamCreateWithFlags(&bh->order_stream, cudaStreamNonBlocking));
+        GC_CUDA(cudaEventCreateWithFlags(&bh->order_ready, cudaEventDisableTiming));
+        GC_CUDA(cudaEventCreateWithFlags(&bh->order_done, cudaEventDisableTiming));
+    }
+    wait_orders(bh);
+    GC_CUDA(cudaEventRecord(bh->order_ready, bh->ctx->stream));  // the walk / force launch just enqueued
+    cudaStream_t s = bh->order_stream;
+    GC_CUDA(cudaStreamWaitEvent(s, bh->order_ready, 0));
     const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? bh->n_wg : bh->rg1;
     const int ng = g1 - g0, nf = bh->n_fg;
     if (ng <= 0) return;
@@ -352,16 +361,18 @@ void make_orders(gc_bh *bh)
     bh_wg_work_kernel<<<grid_for(ng, 256), 256, 0, s>>>(ng, bh->d_wg.p + g0, bh->d_gcount.p, k0.p, i0.p);
     size_t bytes = 0;
     GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, k0.p, k1.p, i0.p, bh->d_wg_order.p, ng, 0, 32, s));
-    bh->ctx->scratch.resize(bytes);
-    GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(bh->ctx->scratch.p, bytes, k0.p, k1.p, i0.p, bh->d_wg_order.p, ng,
+    bh->order_scratch.resize(bytes);
+    GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(bh->order_scratch.p, bytes, k0.p, k1.p, i0.p, bh->d_wg_order.p, ng,
                                                       0, 32, s));
     bh_fg_key_kernel<<<grid_for(nfr, 256), 256, 0, s>>>(nfr, bh->d_grec.p + f0, k0.p, i0.p);
     bytes = 0;
     GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, k0.p, k1.p, i0.p, bh->d_fg_lpt.p, nfr, 0, 32, s));
-    bh->ctx->scratch.resize(bytes);
-    GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(bh->ctx->scratch.p, bytes, k0.p, k1.p, i0.p, bh->d_fg_lpt.p, nfr,
+    bh->order_scratch.resize(bytes);
+    GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(bh->order_scratch.p, bytes, k0.p, k1.p, i0.p, bh->d_fg_lpt.p, nfr,
                                                       0, 32, s));
     check_launch("make_orders");
+    GC_CUDA(cudaEventRecord(bh->order_done, s));
+    bh->order_pending = true;
     bh->order_ng = ng;
     bh->order_nf = nfr;
     bh->order_rg0 = g0;
@@ -457,6 +468,7 @@ void ensure_union_complete(gc_bh *bh)
 
 void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
 {
+    wait_orders(bh);
     gc_ctx *ctx = bh->ctx;
     cudaStream_t s = ctx->stream;
     bh->d_out.resize(bh->n * bh->dim);
@@ -597,6 +609,7 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
         GC_REQUIRE(bucket_size >= 1, GC_E_VALUE, "bucket_size must be >= 1");
         GC_REQUIRE(bucket_size <= 32, GC_E_VALUE, "bucket_size must be <= 32 on the B200 path");
         GC_REQUIRE(dim >= 1 && dim <= 3, GC_E_VALUE, "dim must be 1..3");
+        wait_orders(bh);  // make_orders may still read the previous tree's groups
         if (bh->device_build) {
             device_build_tree(bh, pos, mass, n, dim, box, bucket_size);
         } else {

@@ -106,6 +106,12 @@ struct gc_bh {
     int64_t h2d = 0, d2h = 0;  // bytes moved host<->device since the last reset
     cudaStream_t side = nullptr;  // device build: mass upload overlapping the sort
     cudaEvent_t side_done = nullptr, main_ready = nullptr;
+    // scheduling hints (make_orders) run on their own stream, overlapping the
+    // force download; the next build / walk / force launch waits for them
+    cudaStream_t order_stream = nullptr;
+    cudaEvent_t order_ready = nullptr, order_done = nullptr;
+    bool order_pending = false;
+    DBuf<unsigned char> order_scratch;
     ~gc_bh()
     {
         for (auto &e : ev)
@@ -113,6 +119,12 @@ struct gc_bh {
         if (side_done) cudaEventDestroy(side_done);
         if (main_ready) cudaEventDestroy(main_ready);
         if (side) cudaStreamDestroy(side);
+        if (order_stream) {
+            cudaStreamSynchronize(order_stream);
+            cudaStreamDestroy(order_stream);
+        }
+        if (order_ready) cudaEventDestroy(order_ready);
+        if (order_done) cudaEventDestroy(order_done);
     }
 };
 
@@ -130,6 +142,14 @@ inline void set_tree_bounds(gc_bh *bh, double cmax)
     int e = 0;
     std::frexp(cmax, &e);  // cmax < 2^e, so ulp32(x) <= 2^(e-24) for every |x| <= cmax
     bh->cgrid = (float)std::ldexp(1.0, e - 24);
+}
+// the main stream waits for the last asynchronous make_orders
+inline void wait_orders(gc_bh *bh)
+{
+    if (bh->order_pending) {
+        GC_CUDA(cudaStreamWaitEvent(bh->ctx->stream, bh->order_done, 0));
+        bh->order_pending = false;
+    }
 }
 void device_build_tree(gc_bh *bh, const double *pos, const double *mass, int64_t n, int dim, double box,
                        int64_t bucket_size);
