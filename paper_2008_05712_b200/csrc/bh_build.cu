@@ -213,9 +213,9 @@ __global__ void __launch_bounds__(BB_TPB) bb_levels_coop(LevelArgs A)
         }
         if (L >= A.nlev) break;  // no node of this level can split (half < 1e-9)
         grid.sync();
-        // 1b: wide nodes, one warp each
-        {
-            const int nbig = *A.nbig;
+        // 1b: wide nodes, one warp each (deep levels have none: no extra barrier)
+        const int nbig = *(volatile int *)A.nbig;
+        if (nbig > 0) {
             const int gw = tid >> 5, nw = T >> 5, lane = tid & 31;
             for (int k = gw; k < nbig; k += nw) {
                 const int p = A.big[k];
@@ -232,9 +232,9 @@ __global__ void __launch_bounds__(BB_TPB) bb_levels_coop(LevelArgs A)
                     A.cnt[p] = nonempty;
                 }
             }
+            grid.sync();
+            if (tid == 0) *A.nbig = 0;  // read by every thread above; reset for the next level
         }
-        grid.sync();
-        if (tid == 0) *A.nbig = 0;  // read by every warp above; reset for the next level
         // 2: grid-wide exclusive scan of cnt[0, m) in per-block chunks
         const int chunk = (m + nb - 1) / nb;
         const int c0 = min(m, b * chunk), c1 = min(m, c0 + chunk);
@@ -277,10 +277,10 @@ __global__ void __launch_bounds__(BB_TPB) bb_levels_coop(LevelArgs A)
             if (tid == 0) *A.overflow = 1;
             break;
         }
-        grid.sync();
-        // 3: the children become level L + 1
+        __syncthreads();
+        // 3: the children become level L + 1 (same chunk as the scan: cbase is this block's)
         const int nxt = cur ^ 1;
-        for (int p = tid; p < m; p += T) {
+        for (int p = c0 + (int)threadIdx.x; p < c1; p += blockDim.x) {
             const int ct = A.count[cur][p];
             if (!(ct > A.bucket && half >= 1e-9)) continue;
             const double4 pc = A.center[cur][p];
