@@ -457,6 +457,9 @@ __global__ void bb_buckets(int nb, int dim, const int *__restrict__ buckets, con
 // Walk / force groups, one warp per walk group: lanes load the group's bucket
 // ranges, the greedy force-group cuts (<= 32 targets of consecutive buckets)
 // are made from registers via shuffles (PASS 0 counts, PASS 1 writes).
+#ifndef FG_MAXB
+#define FG_MAXB 32  // buckets per force group (<= 32 targets in any case)
+#endif
 template <int PASS>
 __global__ void bb_groups(int nwg, int nb, const int2 *__restrict__ brange, int *__restrict__ nfg_of,
                           const int *__restrict__ fg_base, WalkGroup *__restrict__ wg, ForceGroup *__restrict__ fg,
@@ -481,7 +484,7 @@ __global__ void bb_groups(int nwg, int nb, const int2 *__restrict__ brange, int 
             pst = v.x;
         }
         // close the current group before bucket j if it would exceed 32 targets (or at the end)
-        if (j == b1 - b0 || (j > start && tg + cnt > 32)) {
+        if (j == b1 - b0 || (j > start && (tg + cnt > 32 || j - start >= FG_MAXB))) {
             if (tg == 0) ok = false;
             if (PASS == 1 && lane == 0) {
                 ForceGroup g;

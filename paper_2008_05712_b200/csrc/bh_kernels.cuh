@@ -44,6 +44,9 @@ constexpr int NODE_BITS = 26;  // stack entries pack node | level << NODE_BITS
 #ifndef WALK_EMIT_SKIP
 #define WALK_EMIT_SKIP 0
 #endif
+#ifndef WALK_RELU_ADD
+#define WALK_RELU_ADD 1
+#endif
 #ifndef WALK_PROF
 #define WALK_PROF 0
 #endif
@@ -166,7 +169,8 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
     __shared__ unsigned act_hi_s[WARPS_PER_BLOCK][STACK_CAP];  // active buckets 32-63
     __shared__ unsigned char lvl_s[WARPS_PER_BLOCK][STACK_CAP];
     __shared__ float2 tt_s[MAX_LEVELS];
-    for (int i = threadIdx.x; i < MAX_LEVELS; i += blockDim.x) tt_s[i] = P.tt[i];
+    for (int i = threadIdx.x; i < MAX_LEVELS; i += blockDim.x)
+        tt_s[i] = WALK_RELU_ADD ? make_float2(4.f * P.tt[i].x, 4.f * P.tt[i].y) : P.tt[i];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // persistent warps: walk groups handed out dynamically, in `order` (heaviest
@@ -239,9 +243,19 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
 #if WALK_HALF_SKIP
                 if (BPL > 1 && (unsigned)(act >> (32 * k)) == 0u) continue;  // warp-uniform: no active bucket here
 #endif
+#if WALK_RELU_ADD
+                // 2 max(u, 0) = u + |u| exactly: an FADD (FMA pipe) instead of an
+                // FMNMX (ALU pipe, the walk's bottleneck); sv = 4 s exactly, and
+                // the level thresholds are stored x4 (tt_s)
+                const float u0 = fabsf(nd.x - bf[k].x) - bf[k].w;
+                const float u1 = fabsf(nd.y - bf[k].y) - bf[k].w;
+                const float u2 = fabsf(nd.z - bf[k].z) - bf[k].w;
+                const float v0 = u0 + fabsf(u0), v1 = u1 + fabsf(u1), v2 = u2 + fabsf(u2);
+#else
                 const float v0 = fmaxf(fabsf(nd.x - bf[k].x) - bf[k].w, 0.f);
                 const float v1 = fmaxf(fabsf(nd.y - bf[k].y) - bf[k].w, 0.f);
                 const float v2 = fmaxf(fabsf(nd.z - bf[k].z) - bf[k].w, 0.f);
+#endif
                 const float sv = fmaf(v2, v2, fmaf(v1, v1, v0 * v0));
                 acc |= (u64)__ballot_sync(0xffffffffu, sv > th.x) << (32 * k);
                 rej |= (u64)__ballot_sync(0xffffffffu, sv < th.y) << (32 * k);
