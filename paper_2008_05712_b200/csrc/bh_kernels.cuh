@@ -190,6 +190,10 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
         const int j = lane + 32 * k;
         bf[k] = j < gd.nbucket ? bgeo32[gd.bfirst + j] : make_float4(0.f, 0.f, 0.f, -1.f);
         inexact |= (u64)__ballot_sync(0xffffffffu, bf[k].w < 0.f) << (32 * k);
+#if WALK_RELU_ADD
+        // NaN propagates through u + |u|: sv = NaN fails both tests -> float64 path
+        if (bf[k].w < 0.f) bf[k].x = __int_as_float(0x7fc00000);
+#endif
         bf[k].w = fabsf(bf[k].w);
     }
     const u64 full = gd.nbucket >= 64 ? ~0ull : ((1ull << gd.nbucket) - 1ull);
@@ -260,8 +264,12 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
                 acc |= (u64)__ballot_sync(0xffffffffu, sv > th.x) << (32 * k);
                 rej |= (u64)__ballot_sync(0xffffffffu, sv < th.y) << (32 * k);
             }
+#if WALK_RELU_ADD
+            acc &= act;  // inexact buckets: NaN, in neither mask
+#else
             acc &= act & exact;
             rej &= exact;
+#endif
             const u64 unsure = ~rej & ~acc & act;
             if (unsure) {  // rare: the reference's float64 test (warp-uniform branch)
 #pragma unroll

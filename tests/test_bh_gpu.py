@@ -257,3 +257,24 @@ def test_fused_and_staged_reorganisation_bit_identical():
         out[mode] = (f, pot)
     np.testing.assert_array_equal(out[1][0], out[0][0])
     np.testing.assert_array_equal(out[1][1], out[0][1])
+
+
+@pytest.mark.parametrize("box", [0.7, 3.3])
+def test_inexact_bucket_geometry_lists_bit_exact(box):
+    """A box that is not a power of two makes bucket centres / half sizes
+    inexact in float32: those buckets skip the float32 certain-accept /
+    certain-reject test and take the reference's float64 test for every
+    node.  Lists must still equal the oracle's bit for bit."""
+    from oracle import oracle as orc
+    from paper_2008_05712_b200 import generators as gen
+    from paper_2008_05712_b200 import nbody
+    ps = gen.gen_particles(6000, 17, clustering=0.6, dim=3, box=box)
+    tree = nbody.build_bucket_tree(ps, 8)
+    lists = nbody.build_interaction_lists(tree, 0.6, ps)
+    ot = orc.build_bucket_tree(ps.positions, ps.masses, 8, box=box)
+    ol = orc.build_interaction_lists(ot, 0.6)
+    ptr, ids, kind, ic = lists.csr()
+    np.testing.assert_array_equal(ptr, ol.ptr)
+    np.testing.assert_array_equal(ids, ol.ids)
+    np.testing.assert_array_equal(kind, ol.kind)
+    np.testing.assert_array_equal(ic, ol.item_count)
