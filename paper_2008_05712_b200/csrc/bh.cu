@@ -199,6 +199,19 @@ __global__ void bb_iota_kernel(int n, int *p)
     if (i < n) p[i] = i;
 }
 
+// d_grec for the current union lists (all force groups)
+void ensure_grec(gc_bh *bh)
+{
+    if (bh->grec_valid || !bh->have_union) return;
+    const int nf = bh->n_fg;
+    bh->d_grec.resize(std::max(nf, 1));
+    if (nf > 0) {
+        grec_kernel<<<grid_for(nf, WARPS_PER_BLOCK), 32 * WARPS_PER_BLOCK, 0, bh->ctx->stream>>>(nf, pool_view(bh));
+        check_launch("grec_kernel");
+    }
+    bh->grec_valid = true;
+}
+
 struct RoundRun {  // records of a force group's staging run (multiple of PFLUSH); 0 past the end
     const int *grec;
     int n;
@@ -297,7 +310,11 @@ void launch_walk(gc_bh *bh, bool write, bool stats)
     }
     if (ng <= 0) return;
     const UnionPool U = pool_view(bh);
-    auto k = write ? (stats ? walk_group_kernel<true, true> : walk_group_kernel<true, false>)
+    // the staged mode needs every force group's record count (its run length);
+    // the fused force kernel does not, and the walk skips counting
+    const bool nrec = !bh->force_fused;
+    auto k = write ? (stats ? (nrec ? walk_group_kernel<true, true, true> : walk_group_kernel<true, true, false>)
+                            : (nrec ? walk_group_kernel<true, false, true> : walk_group_kernel<true, false, false>))
                    : walk_group_kernel<false, true>;
     int per_sm = 0;
     GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * WARPS_PER_BLOCK, 0));
@@ -364,7 +381,8 @@ void make_orders(gc_bh *bh)
     bh->order_scratch.resize(bytes);
     GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(bh->order_scratch.p, bytes, k0.p, k1.p, i0.p, bh->d_wg_order.p, ng,
                                                       0, 32, s));
-    bh_fg_key_kernel<<<grid_for(nfr, 256), 256, 0, s>>>(nfr, bh->d_grec.p + f0, k0.p, i0.p);
+    // force groups longest first by union entries (a proxy of the run length: the walk does not count records)
+    bh_fg_key_kernel<<<grid_for(nfr, 256), 256, 0, s>>>(nfr, bh->d_gcount.p + f0, k0.p, i0.p);
     bytes = 0;
     GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, k0.p, k1.p, i0.p, bh->d_fg_lpt.p, nfr, 0, 32, s));
     bh->order_scratch.resize(bytes);
@@ -418,17 +436,21 @@ void run_walk(gc_bh *bh, double theta, bool want_stats)
     GC_CUDA(cudaEventRecord(bh->ev[1], bh->ctx->stream));
     bh->have_union = true;
     bh->have_member_lists = false;
+    bh->grec_valid = !bh->force_fused;  // the staged mode's walk counted the records
+    if (stats) bh->staging_sized = false;  // a new tree / theta (else the lists repeat)
     if (stats) {
         while (walk_overflowed(bh)) launch_walk(bh, true, true);
         bh->stats_valid = true;
         bh->stats_dirty = true;
-        // exact staging size of this tree / theta (the asynchronous steady state never overflows)
+        // exact staging size of this tree / theta (staged mode; the asynchronous steady state never overflows)
+        if (bh->force_fused) return;
         std::vector<int> rec(bh->n_fg);
         bh->d_grec.download(rec.data(), bh->n_fg, bh->ctx->stream);
         GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
         int64_t need = 0;
         for (int r : rec) need += (r + PFLUSH - 1) & ~(PFLUSH - 1);
         if (need > bh->staging_cap) size_staging(bh, need + need / 16);
+        bh->staging_sized = true;
     }
 }
 
@@ -516,6 +538,7 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
             return;
         }
         // staging runs: exclusive scan of the rounded record counts
+        ensure_grec(bh);
         bh->d_rbase.resize(nfg + 1);
         {
             auto it = cub::TransformInputIterator<int64_t, RoundRun, cub::CountingInputIterator<int>>(
@@ -525,8 +548,15 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
             ctx->scratch.resize(bytes);
             GC_CUDA(cub::DeviceScan::ExclusiveSum(ctx->scratch.p, bytes, it, bh->d_rbase.p, nfg + 1, s));
         }
-        // first guess ~160 records per bucket; an overflow grows it to the walk's demand
-        if (bh->staging_cap == 0) size_staging(bh, 160 * bh->n_buckets + 1024);
+        // the staging must hold every run: sized exactly by a staged stats walk,
+        // else (lists from a fused-mode walk) from the scan's total, once per walk
+        if (!bh->staging_sized) {
+            int64_t need = 0;
+            bh->d_rbase.download(&need, 1, s, nfg);
+            GC_CUDA(cudaStreamSynchronize(s));
+            if (need > bh->staging_cap) size_staging(bh, need + need / 16 + 1024);
+            bh->staging_sized = true;
+        }
         // the persistent force kernel hands out force groups longest run first
         // when a previous walk of this tree/range fixed that order, else in
         // depth-first order (sorting every step costs more than its tail saves)
@@ -692,6 +722,7 @@ gc_status gc_bh_sizes(gc_bh *bh, int64_t out[5])
             ensure_union_complete(bh);
             const size_t nf = bh->d_gcount.n;
             std::vector<int> cnt(nf), rec(nf);
+            ensure_grec(bh);
             bh->d_gcount.download(cnt.data(), nf, bh->ctx->stream);
             bh->d_grec.download(rec.data(), nf, bh->ctx->stream);
             GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
@@ -896,6 +927,7 @@ gc_status gc_bh_pair_stats(gc_bh *bh, int64_t out[2])
         const int nf = bh->n_fg;
         std::vector<int> rec(nf);
         std::vector<ForceGroup> fg(nf);
+        ensure_grec(bh);
         bh->d_grec.download(rec.data(), nf, s);
         bh->d_fg.download(fg.data(), nf, s);
         GC_CUDA(cudaStreamSynchronize(s));

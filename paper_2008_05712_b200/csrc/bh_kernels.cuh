@@ -156,7 +156,7 @@ struct UnionPool {
 #define WALK_UNROLL 2
 #endif
 constexpr int kWalkUnroll = WALK_UNROLL;  // sibling-loop unroll
-template <bool WRITE, bool STATS>
+template <bool WRITE, bool STATS, bool NREC = false>
 __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, WALK_MINB)
 walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const ForceGroup *__restrict__ fgroups,
                   const float4 *__restrict__ recs, const double4 *__restrict__ com64,
@@ -298,7 +298,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
                 if (emits) *wp = make_int4(node, (int)ma, (int)mp, wd);
                 w += hit ? 1 : 0;
                 wp += hit ? 1 : 0;
-                nrec += (ma ? 1 : 0) + (mp ? wr_pcount(wd) : 0);
+                if (NREC) nrec += (ma ? 1 : 0) + (mp ? wr_pcount(wd) : 0);
                 if (hit && (w & (CHUNK - 1)) == 0) {  // chunk full: link the next one
                     int cn = atomicAdd(U.top, 1);
                     if (cn >= U.nchunks) {
@@ -353,7 +353,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
 #endif
     if (WRITE && emits) {
         U.gcount[my_fg] = w;
-        U.grec[my_fg] = nrec;
+        if (NREC) U.grec[my_fg] = nrec;
     }
     if (STATS) {
 #pragma unroll
@@ -394,6 +394,28 @@ union_to_lists_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const Wal
             ++cur;
         }
     }
+}
+
+// Source records per force group (node records + opened-bucket particles)
+// from its union list, one warp per force group: the staged mode's run
+// lengths and the pair statistics (the walk itself does not count them).
+static __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK) grec_kernel(int nfg, const UnionPool U)
+{
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int f = blockIdx.x * WARPS_PER_BLOCK + warp;
+    if (f >= nfg) return;
+    const int n = U.gcount[f];
+    int chunk = n > 0 ? U.gfirst[f] : 0, r = 0;
+    for (int e0 = 0; e0 < n; e0 += CHUNK) {
+        if (e0 > 0) chunk = U.cnext[chunk];
+        for (int e = e0 + lane; e < min(n, e0 + CHUNK); e += 32) {
+            const int4 en = U.ent[(int64_t)chunk * CHUNK + (e & (CHUNK - 1))];
+            r += (en.y ? 1 : 0) + (en.z ? wr_pcount(en.w) : 0);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (lane == 0) U.grec[f] = r;
 }
 
 // ---------------------------------------------------------------------------

@@ -30,7 +30,9 @@ struct gc_bh {
     bool have_tree = false;
     bool host_tree_valid = false;
     bool device_build = true;  // build the tree on the GPU (gc_bh_set_build_mode)
-    bool force_fused = true;  // reorganise into shared memory inside the force kernel (gc_bh_set_force_mode)
+    bool force_fused = true;
+    bool grec_valid = false;  // d_grec matches the current union lists
+    bool staging_sized = false;  // the staging buffer holds the current lists' runs  // reorganise into shared memory inside the force kernel (gc_bh_set_force_mode)
     // tree metadata (always valid once particles are set)
     int64_t n = 0, n_nodes = 0, n_buckets = 0, bucket_size = 8;
     int dim = 3;
