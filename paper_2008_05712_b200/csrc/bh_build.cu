@@ -460,10 +460,13 @@ __global__ void bb_buckets(int nb, int dim, const int *__restrict__ buckets, con
 #ifndef FG_MAXB
 #define FG_MAXB 32  // buckets per force group (<= 32 targets in any case)
 #endif
+#ifndef FG_MINT
+#define FG_MINT 0  // > 0: also cut a force group of >= FG_MINT targets where the next bucket does not touch the last
+#endif
 template <int PASS>
 __global__ void bb_groups(int nwg, int nb, const int2 *__restrict__ brange, int *__restrict__ nfg_of,
                           const int *__restrict__ fg_base, WalkGroup *__restrict__ wg, ForceGroup *__restrict__ fg,
-                          int *__restrict__ bad)
+                          int *__restrict__ bad, const double4 *__restrict__ bgeo)
 {
     const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -474,17 +477,36 @@ __global__ void bb_groups(int nwg, int nb, const int2 *__restrict__ brange, int 
     for (int k = 0; k < BPL; ++k) r[k] = b0 + lane + 32 * k < b1 ? brange[b0 + lane + 32 * k] : make_int2(0, 0);
     int k = 0, start = 0, tg = 0, ps = 0;
     bool ok = true;
+#if FG_MINT
+    float4 gq[BPL];
+#pragma unroll
+    for (int q = 0; q < BPL; ++q) {
+        const int bj = b0 + lane + 32 * q;
+        const double4 g = bj < b1 ? bgeo[bj] : make_double4(0, 0, 0, 0);
+        gq[q] = make_float4((float)g.x, (float)g.y, (float)g.z, (float)g.w);
+    }
+    float4 prev = make_float4(0.f, 0.f, 0.f, 0.f);
+#endif
     for (int j = 0; j <= b1 - b0; ++j) {
         int cnt = 0, pst = 0;
+        bool jump = false;
         if (j < b1 - b0) {
             const int2 v = j < 32 ? make_int2(__shfl_sync(0xffffffffu, r[0].x, j), __shfl_sync(0xffffffffu, r[0].y, j))
                                   : make_int2(__shfl_sync(0xffffffffu, r[1].x, j - 32),
                                               __shfl_sync(0xffffffffu, r[1].y, j - 32));
             cnt = v.y;
             pst = v.x;
+#if FG_MINT
+            const int q = j < 32 ? 0 : 1, src = j & 31;
+            const float4 cur = make_float4(__shfl_sync(0xffffffffu, gq[q].x, src), __shfl_sync(0xffffffffu, gq[q].y, src),
+                                           __shfl_sync(0xffffffffu, gq[q].z, src), __shfl_sync(0xffffffffu, gq[q].w, src));
+            const float d = fmaxf(fmaxf(fabsf(cur.x - prev.x), fabsf(cur.y - prev.y)), fabsf(cur.z - prev.z));
+            jump = j > 0 && d > 1.001f * (cur.w + prev.w);  // the cells do not touch
+            prev = cur;
+#endif
         }
         // close the current group before bucket j if it would exceed 32 targets (or at the end)
-        if (j == b1 - b0 || (j > start && (tg + cnt > 32 || j - start >= FG_MAXB))) {
+        if (j == b1 - b0 || (j > start && (tg + cnt > 32 || j - start >= FG_MAXB || (FG_MINT && jump && tg >= FG_MINT)))) {
             if (tg == 0) ok = false;
             if (PASS == 1 && lane == 0) {
                 ForceGroup g;
@@ -772,7 +794,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     bad.resize(1);
     bad.zero(s);
     bb_groups<0><<<grid_for(nwg, BB_TPB / 32), BB_TPB, 0, s>>>(nwg, nb, bh->d_brange.p, nfg_of.p, nullptr, nullptr,
-                                                          nullptr, bad.p);
+                                                          nullptr, bad.p, bh->d_bgeo.p);
     GC_CUDA(cudaMemsetAsync(nfg_of.p + nwg, 0, sizeof(int), s));
     cubc(ctx, [&](void *t, size_t &b) {
         return cub::DeviceScan::ExclusiveSum(t, b, nfg_of.p, fg_base.p, nwg + 1, s);
@@ -788,7 +810,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     bh->d_wg.resize(nwg);
     bh->d_fg.resize(nfg);
     bb_groups<1><<<grid_for(nwg, BB_TPB / 32), BB_TPB, 0, s>>>(nwg, nb, bh->d_brange.p, nullptr, fg_base.p, bh->d_wg.p,
-                                                          bh->d_fg.p, bad.p);
+                                                          bh->d_fg.p, bad.p, bh->d_bgeo.p);
     check_launch("bb groups");
     bh->n_wg = nwg;
     bh->h_wg_valid = false;  // fetched on demand (sub-range launches, gc_bh_groups)
