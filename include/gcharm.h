@@ -106,8 +106,9 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
  * Forces are bit-identical either way. */
 gc_status gc_bh_set_force_mode(gc_bh *bh, int32_t fused);
 /* walk instrumentation, only in builds with -DWALK_PROF=1 (zeros otherwise):
- * out = node visits, sum of active buckets, visits with an empty half, decisions */
-gc_status gc_debug_walk_prof(int64_t out[4], int32_t reset);
+ * out = node visits, sum of active buckets, visits with an empty half, decisions,
+ * ns from the first warp's start to the first warp without work, to the last warp's exit */
+gc_status gc_debug_walk_prof(int64_t out[6], int32_t reset);
 /* pairs the force kernel evaluates for the current lists: out[0] = padded
  * source records x 32 lanes summed over force groups, out[1] = padded records
  * x targets; useful pairs = gc_bh_interactions (full walk-group range) */

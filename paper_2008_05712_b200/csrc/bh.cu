@@ -12,6 +12,9 @@
 #ifndef WALK_LPT
 #define WALK_LPT 1  // walk groups heaviest first (0: depth-first order)
 #endif
+#ifndef WALK_COST_LPT
+#define WALK_COST_LPT 1  // heaviest = most cycles in the last walk (0: most union entries)
+#endif
 
 using namespace gc;
 
@@ -309,6 +312,7 @@ void launch_walk(gc_bh *bh, bool write, bool stats)
         bh->d_top.zero(s);
     }
     if (ng <= 0) return;
+    if (WALK_COST_LPT) bh->d_wcost.resize(std::max<int64_t>(bh->n_wg, 1));
     const UnionPool U = pool_view(bh);
     // the staged mode needs every force group's record count (its run length);
     // the fused force kernel does not, and the walk skips counting
@@ -325,17 +329,21 @@ void launch_walk(gc_bh *bh, bool write, bool stats)
     k<<<pgrid, 32 * WARPS_PER_BLOCK, 0, s>>>(ng, wg, bh->d_fg.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p,
                                              bh->d_bgeo32.p, bh->wp, U, bh->d_bstat.p, bh->d_flag.p,
                                              (WALK_LPT && bh->order_ng == ng && bh->order_rg0 == g0) ? bh->d_wg_order.p : nullptr,
-                                             bh->d_wnext.p);
+                                             bh->d_wnext.p, WALK_COST_LPT ? bh->d_wcost.p + g0 : nullptr);
     check_launch("walk_group_kernel");
 }
 
 __global__ void bh_wg_work_kernel(int ng, const WalkGroup *__restrict__ wg, const int *__restrict__ gcount,
-                                  int *__restrict__ key, int *__restrict__ idx)
+                                  const int *__restrict__ wcost, int *__restrict__ key, int *__restrict__ idx)
 {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= ng) return;
     int e = 0;
-    for (int f = wg[g].fg_first; f < wg[g].fg_first + wg[g].nfg; ++f) e += gcount[f];
+    if (wcost) {
+        e = wcost[g];  // measured cycles of the last walk (/16)
+    } else {
+        for (int f = wg[g].fg_first; f < wg[g].fg_first + wg[g].nfg; ++f) e += gcount[f];
+    }
     key[g] = e;
     idx[g] = g;
 }
@@ -375,7 +383,8 @@ void make_orders(gc_bh *bh)
     k0.resize(m); k1.resize(m); i0.resize(m);
     bh->d_wg_order.resize(ng);
     bh->d_fg_lpt.resize(nfr);
-    bh_wg_work_kernel<<<grid_for(ng, 256), 256, 0, s>>>(ng, bh->d_wg.p + g0, bh->d_gcount.p, k0.p, i0.p);
+    bh_wg_work_kernel<<<grid_for(ng, 256), 256, 0, s>>>(ng, bh->d_wg.p + g0, bh->d_gcount.p,
+                                                         WALK_COST_LPT ? bh->d_wcost.p + g0 : nullptr, k0.p, i0.p);
     size_t bytes = 0;
     GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, k0.p, k1.p, i0.p, bh->d_wg_order.p, ng, 0, 32, s));
     bh->order_scratch.resize(bytes);
@@ -672,21 +681,23 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
 
 // walk instrumentation (builds with -DWALK_PROF=1 only; zeros otherwise):
 // node visits, sum of active buckets, visits with an empty half, decisions emitted
-gc_status gc_debug_walk_prof(int64_t out[4], int32_t reset)
+gc_status gc_debug_walk_prof(int64_t out[6], int32_t reset)
 {
     return guard([&] {
         GC_REQUIRE(out, GC_E_VALUE, "null argument");
 #if WALK_PROF
-        unsigned long long v[4];
+        unsigned long long v[8];
         GC_CUDA(cudaMemcpyFromSymbol(v, g_walk_prof, sizeof(v)));
         for (int k = 0; k < 4; ++k) out[k] = (int64_t)v[k];
+        out[4] = (int64_t)(v[5] - v[4]);  // first warp out of groups, ns after the first start
+        out[5] = (int64_t)(v[6] - v[4]);  // last warp done
         if (reset) {
-            const unsigned long long z[4] = {0, 0, 0, 0};
+            const unsigned long long z[8] = {0, 0, 0, 0, ~0ull, ~0ull, 0, 0};
             GC_CUDA(cudaMemcpyToSymbol(g_walk_prof, z, sizeof(z)));
         }
 #else
         (void)reset;
-        for (int k = 0; k < 4; ++k) out[k] = 0;
+        for (int k = 0; k < 6; ++k) out[k] = 0;
 #endif
     });
 }

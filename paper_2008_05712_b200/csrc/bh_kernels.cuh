@@ -52,7 +52,7 @@ constexpr int NODE_BITS = 26;  // stack entries pack node | level << NODE_BITS
 #endif
 #if WALK_PROF
 // [node visits, sum popc(act), visits with one half of act empty, sum popc(acc | part)]
-__device__ unsigned long long g_walk_prof[4];
+__device__ unsigned long long g_walk_prof[8];  // + [4] first warp start, [5] first warp exit, [6] last warp exit
 #endif
 constexpr int BPL = GC_BPL;  // buckets per lane in the walk
 constexpr int WG_BUCKETS = 32 * BPL;  // buckets per walk group (lane l holds buckets l, l + 32, ...)
@@ -162,7 +162,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
                   const float4 *__restrict__ recs, const double4 *__restrict__ com64,
                   const double4 *__restrict__ bgeo, const float4 *__restrict__ bgeo32, const WalkParams P,
                   UnionPool U, int64_t *__restrict__ bstat, int *__restrict__ flag, const int *__restrict__ order,
-                  int *__restrict__ next)
+                  int *__restrict__ next, int *__restrict__ wcost)
 {
     using u64 = unsigned long long;
     __shared__ int2 stack_s[WARPS_PER_BLOCK][STACK_CAP];  // (first | (nc - 1) << NODE_BITS, active buckets 0-31)
@@ -175,12 +175,30 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // persistent warps: walk groups handed out dynamically, in `order` (heaviest
     // first, from the previous walk of this tree) when known
+#if WALK_PROF
+    {
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        if (lane == 0) atomicMin(&g_walk_prof[4], t0);
+    }
+#endif
     for (;;) {
     int gi = 0;
     if (lane == 0) gi = atomicAdd(next, 1);
     gi = __shfl_sync(0xffffffffu, gi, 0);
-    if (gi >= ngroups) break;
+    if (gi >= ngroups) {
+#if WALK_PROF
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (lane == 0) {
+            atomicMin(&g_walk_prof[5], t1);
+            atomicMax(&g_walk_prof[6], t1);
+        }
+#endif
+        break;
+    }
     const int g = order ? order[gi] : gi;
+    const long long tg0 = clock64();
     const WalkGroup gd = groups[g];
     // lane holds buckets lane and lane + 32 of the group
     float4 bf[BPL];
@@ -351,6 +369,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
         atomicAdd(&g_walk_prof[3], pe);
     }
 #endif
+    if (wcost && lane == 0) wcost[g] = (int)min((clock64() - tg0) >> 4, (long long)INT_MAX);  // next walk's LPT key
     if (WRITE && emits) {
         U.gcount[my_fg] = w;
         if (NREC) U.grec[my_fg] = nrec;

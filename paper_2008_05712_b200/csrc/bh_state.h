@@ -76,6 +76,7 @@ struct gc_bh {
     DBuf<int> d_fg_order, d_next;
     // scheduling hints (make_orders): heaviest-first walk groups, longest-run-first
     // force groups of the last completed walk; used while the sizes match
+    DBuf<int> d_wcost;  // cycles / 16 of each walk group in the last walk (LPT key)
     DBuf<int> d_wg_order, d_wnext, d_fg_lpt, d_okey, d_okey2, d_oidx;
     int order_ng = -1, order_nf = -1, order_rg0 = -1;
     bool orders_fresh = false;
