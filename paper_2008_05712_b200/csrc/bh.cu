@@ -326,15 +326,21 @@ void launch_walk(gc_bh *bh, bool write, bool stats)
         1, std::min<int64_t>((int64_t)per_sm * bh->ctx->prop.multiProcessorCount, grid));
     bh->d_wnext.resize(1);
     bh->d_wnext.zero(s);
-    k<<<pgrid, 32 * WARPS_PER_BLOCK, 0, s>>>(ng, wg, bh->d_fg.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p,
-                                             bh->d_bgeo32.p, bh->wp, U, bh->d_bstat.p, bh->d_flag.p,
-                                             (WALK_LPT && bh->order_ng == ng && bh->order_rg0 == g0) ? bh->d_wg_order.p : nullptr,
-                                             bh->d_wnext.p, WALK_COST_LPT ? bh->d_wcost.p + g0 : nullptr);
+    const bool ordered = WALK_LPT && bh->order_ng == ng && bh->order_rg0 == g0;
+    if (WALK_COST_LPT) GC_CUDA(cudaMemsetAsync(bh->d_wcost.p + g0, 0, sizeof(int) * ng, s));
+    // with hints: 2 ng work items (heavy groups split in two, -1 padding)
+    k<<<pgrid, 32 * WARPS_PER_BLOCK, 0, s>>>(ordered ? 2 * ng : ng, wg, bh->d_fg.p, bh->d_recs.p, bh->d_com64.p,
+                                             bh->d_bgeo.p, bh->d_bgeo32.p, bh->wp, U, bh->d_bstat.p, bh->d_flag.p,
+                                             ordered ? bh->d_wg_order.p : nullptr, bh->d_wnext.p,
+                                             WALK_COST_LPT ? bh->d_wcost.p + g0 : nullptr);
     check_launch("walk_group_kernel");
 }
 
-__global__ void bh_wg_work_kernel(int ng, const WalkGroup *__restrict__ wg, const int *__restrict__ gcount,
-                                  const int *__restrict__ wcost, int *__restrict__ key, int *__restrict__ idx)
+#ifndef WALK_SPLIT
+#define WALK_SPLIT 0  // > 0: split walk groups costing more than this x the mean into two work items (measured slower: each half re-walks most of the tree)
+#endif
+__global__ void bh_wg_cost_kernel(int ng, const WalkGroup *__restrict__ wg, const int *__restrict__ gcount,
+                                  const int *__restrict__ wcost, int *__restrict__ cost)
 {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= ng) return;
@@ -344,8 +350,32 @@ __global__ void bh_wg_work_kernel(int ng, const WalkGroup *__restrict__ wg, cons
     } else {
         for (int f = wg[g].fg_first; f < wg[g].fg_first + wg[g].nfg; ++f) e += gcount[f];
     }
-    key[g] = e;
-    idx[g] = g;
+    cost[g] = e;
+}
+
+__global__ void bh_sum_kernel(int n, const int *__restrict__ v, long long *__restrict__ out)
+{
+    typedef cub::BlockReduce<long long, 1024> Red;
+    __shared__ typename Red::TempStorage ts;
+    long long t = 0;
+    for (int i = threadIdx.x; i < n; i += 1024) t += v[i];
+    t = Red(ts).Sum(t);
+    if (threadIdx.x == 0) *out = t;
+}
+
+// work items of the next walk: a group, or its two halves (by force groups)
+// when it costs more than WALK_SPLIT x the mean; keys for the LPT sort
+__global__ void bh_wg_items_kernel(int ng, const WalkGroup *__restrict__ wg, const int *__restrict__ cost,
+                                   const long long *__restrict__ total, int *__restrict__ key, int *__restrict__ code)
+{
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= ng) return;
+    const int c = cost[g];
+    const bool split = WALK_SPLIT > 0 && wg[g].nfg >= 2 && (double)c * ng > WALK_SPLIT * (double)*total;
+    key[2 * g] = split ? c / 2 : c;
+    code[2 * g] = 4 * g + (split ? 1 : 0);
+    key[2 * g + 1] = split ? c / 2 : -1;
+    code[2 * g + 1] = split ? 4 * g + 2 : -1;
 }
 
 __global__ void bh_fg_key_kernel(int nf, const int *__restrict__ grec, int *__restrict__ key, int *__restrict__ idx)
@@ -379,17 +409,22 @@ void make_orders(gc_bh *bh)
     const int f1 = wg_fg_first(bh, g1);
     const int nfr = f1 - f0;
     auto &k0 = bh->d_okey, &k1 = bh->d_okey2, &i0 = bh->d_oidx;
-    const int m = std::max(ng, nfr);
+    const int m = std::max(2 * ng, nfr);
     k0.resize(m); k1.resize(m); i0.resize(m);
-    bh->d_wg_order.resize(ng);
+    bh->d_wg_order.resize(2 * ng);
     bh->d_fg_lpt.resize(nfr);
-    bh_wg_work_kernel<<<grid_for(ng, 256), 256, 0, s>>>(ng, bh->d_wg.p + g0, bh->d_gcount.p,
-                                                         WALK_COST_LPT ? bh->d_wcost.p + g0 : nullptr, k0.p, i0.p);
+    bh->d_wg_total.resize(1);
+    bh_wg_cost_kernel<<<grid_for(ng, 256), 256, 0, s>>>(ng, bh->d_wg.p + g0, bh->d_gcount.p,
+                                                         WALK_COST_LPT ? bh->d_wcost.p + g0 : nullptr, k1.p);
+    bh_sum_kernel<<<1, 1024, 0, s>>>(ng, k1.p, bh->d_wg_total.p);
     size_t bytes = 0;
-    GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, k0.p, k1.p, i0.p, bh->d_wg_order.p, ng, 0, 32, s));
+    bh_wg_items_kernel<<<grid_for(ng, 256), 256, 0, s>>>(ng, bh->d_wg.p + g0, k1.p, bh->d_wg_total.p, k0.p, i0.p);
+    bytes = 0;
+    GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, k0.p, k1.p, i0.p, bh->d_wg_order.p, 2 * ng, 0, 32,
+                                                      s));
     bh->order_scratch.resize(bytes);
-    GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(bh->order_scratch.p, bytes, k0.p, k1.p, i0.p, bh->d_wg_order.p, ng,
-                                                      0, 32, s));
+    GC_CUDA(cub::DeviceRadixSort::SortPairsDescending(bh->order_scratch.p, bytes, k0.p, k1.p, i0.p, bh->d_wg_order.p,
+                                                      2 * ng, 0, 32, s));
     // force groups longest first by union entries (a proxy of the run length: the walk does not count records)
     bh_fg_key_kernel<<<grid_for(nfr, 256), 256, 0, s>>>(nfr, bh->d_gcount.p + f0, k0.p, i0.p);
     bytes = 0;

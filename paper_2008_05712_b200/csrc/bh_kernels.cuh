@@ -197,9 +197,16 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
 #endif
         break;
     }
-    const int g = order ? order[gi] : gi;
+    // work item: a walk group, or one half of a heavy group's force groups
+    // (order entries g * 4 + part, part 0 = all, 1 / 2 = first / second half;
+    // negative = no item)
+    const int code = order ? order[gi] : 4 * gi;
+    if (code < 0) continue;
+    const int g = code >> 2, part = code & 3;
     const long long tg0 = clock64();
     const WalkGroup gd = groups[g];
+    const int fhalf = (gd.nfg + 1) >> 1;
+    const int fa = part == 2 ? fhalf : 0, fb = part == 1 ? fhalf : gd.nfg;  // force groups [fa, fb)
     // lane holds buckets lane and lane + 32 of the group
     float4 bf[BPL];
     u64 inexact = 0ull;  // geometry not float32-exact: always take the float64 test
@@ -214,7 +221,14 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
 #endif
         bf[k].w = fabsf(bf[k].w);
     }
-    const u64 full = gd.nbucket >= 64 ? ~0ull : ((1ull << gd.nbucket) - 1ull);
+    u64 full = gd.nbucket >= 64 ? ~0ull : ((1ull << gd.nbucket) - 1ull);
+    int blo = 0, bhi = gd.nbucket;  // buckets of this item
+    if (part) {
+        const ForceGroup f0 = fgroups[gd.fg_first + fa], f1 = fgroups[gd.fg_first + fb - 1];
+        blo = f0.boff;
+        bhi = f1.boff + f1.nb;
+        full &= (bhi >= 64 ? ~0ull : ((1ull << bhi) - 1ull)) & ~((1ull << blo) - 1ull);
+    }
     const u64 exact = ~inexact;
     int2 *stack = stack_s[warp];
     unsigned *sact = act_hi_s[warp];
@@ -222,8 +236,8 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
     int sp = 0;
     // lane f < nfg emits the list of force group fg_first + f (masks shifted to
     // its own buckets); its current chunk always has room for slot w % CHUNK
-    const bool emits = lane < gd.nfg;
-    const int my_fg = gd.fg_first + (emits ? lane : 0);
+    const bool emits = lane < fb - fa;
+    const int my_fg = gd.fg_first + fa + (emits ? lane : 0);
     int boff = 0;
     u64 fgm = 0ull;
     if (emits) {
@@ -369,7 +383,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
         atomicAdd(&g_walk_prof[3], pe);
     }
 #endif
-    if (wcost && lane == 0) wcost[g] = (int)min((clock64() - tg0) >> 4, (long long)INT_MAX);  // next walk's LPT key
+    if (wcost && lane == 0) atomicAdd(wcost + g, (int)min((clock64() - tg0) >> 4, (long long)(INT_MAX / 4)));  // next LPT key
     if (WRITE && emits) {
         U.gcount[my_fg] = w;
         if (NREC) U.grec[my_fg] = nrec;
@@ -378,7 +392,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
 #pragma unroll
         for (int k = 0; k < BPL; ++k) {
             const int j = lane + 32 * k;
-            if (j < gd.nbucket) {
+            if (j >= blo && j < bhi) {
                 bstat[2 * (int64_t)(gd.bfirst + j)] = my_entries[k];
                 bstat[2 * (int64_t)(gd.bfirst + j) + 1] = my_items[k];
             }

@@ -77,6 +77,7 @@ struct gc_bh {
     // scheduling hints (make_orders): heaviest-first walk groups, longest-run-first
     // force groups of the last completed walk; used while the sizes match
     DBuf<int> d_wcost;  // cycles / 16 of each walk group in the last walk (LPT key)
+    DBuf<long long> d_wg_total;  // their sum (split threshold)
     DBuf<int> d_wg_order, d_wnext, d_fg_lpt, d_okey, d_okey2, d_oidx;
     int order_ng = -1, order_nf = -1, order_rg0 = -1;
     bool orders_fresh = false;
