@@ -278,3 +278,20 @@ def test_inexact_bucket_geometry_lists_bit_exact(box):
     np.testing.assert_array_equal(ids, ol.ids)
     np.testing.assert_array_equal(kind, ol.kind)
     np.testing.assert_array_equal(ic, ol.item_count)
+
+
+def test_pair_stats_bounds():
+    """gc_bh_pair_stats: useful interactions <= pairs of target lanes <= issued
+    pairs (32 lanes per padded record); gc_bh_sizes' record total matches."""
+    from paper_2008_05712_b200 import _lib as L
+    from paper_2008_05712_b200 import generators as gen
+    from paper_2008_05712_b200 import nbody
+    ps = gen.fp32_exact(gen.gen_particles(50_000, 3, clustering=0.6, dim=3))
+    tree = nbody.build_bucket_tree(ps, 8)
+    L.call("gc_bh_walk", tree.handle, 0.7)
+    st = np.zeros(2, np.int64)
+    L.call("gc_bh_pair_stats", tree.handle, L.ptr(st, L.i64p))
+    inter = nbody.interactions(tree)
+    assert 0 < inter <= st[1] <= st[0]
+    sz = tree.sizes()
+    assert st[0] >= 32 * int(sz[4])  # padded records >= records
