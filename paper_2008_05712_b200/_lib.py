@@ -58,6 +58,8 @@ SIGNATURES = {
     "gc_bh_sizes": [vp, i64p],
     "gc_bh_set_build_mode": [vp, C.c_int32],
     "gc_bh_set_force_mode": [vp, C.c_int32],
+    "gc_bh_set_overlap": [vp, C.c_int32],
+    "gc_bh_walk_forces_async": [vp, C.c_double, C.c_double, C.c_double],
     "gc_bh_pair_stats": [vp, i64p],
     "gc_debug_walk_prof": [i64p, C.c_int32],
     "gc_bh_get_tree": [vp, f64p, f64p, f64p, f64p, i64p, i32p, i64p, i64p, i64p],

@@ -284,7 +284,7 @@ void walk_params(gc_bh *bh, double theta)
 }
 
 // One walk launch over the handle's walk-group range (asynchronous).
-void launch_walk(gc_bh *bh, bool write, bool stats)
+void launch_walk(gc_bh *bh, bool write, bool stats, int *fq = nullptr, int *fq_tail = nullptr, int fq_base = 0)
 {
     wait_orders(bh);
     cudaStream_t s = bh->ctx->stream;
@@ -332,7 +332,7 @@ void launch_walk(gc_bh *bh, bool write, bool stats)
     k<<<pgrid, 32 * WARPS_PER_BLOCK, 0, s>>>(ordered ? 2 * ng : ng, wg, bh->d_fg.p, bh->d_recs.p, bh->d_com64.p,
                                              bh->d_bgeo.p, bh->d_bgeo32.p, bh->wp, U, bh->d_bstat.p, bh->d_flag.p,
                                              ordered ? bh->d_wg_order.p : nullptr, bh->d_wnext.p,
-                                             WALK_COST_LPT ? bh->d_wcost.p + g0 : nullptr);
+                                             WALK_COST_LPT ? bh->d_wcost.p + g0 : nullptr, fq, fq_tail, fq_base);
     check_launch("walk_group_kernel");
 }
 
@@ -656,6 +656,81 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
 
 }  // namespace
 
+// Walk and forces of one step overlapped (fused mode): the walk publishes
+// each finished walk group's force groups to a device queue and the force
+// kernel, launched concurrently on a second stream, consumes them in that
+// order -- its blocks take the SM slots the walk's tail frees.
+void run_overlapped(gc_bh *bh, double theta, double g, double eps)
+{
+    GC_REQUIRE(theta >= 0.0, GC_E_VALUE, "theta must be >= 0");
+    GC_REQUIRE(bh->have_tree, GC_E_STATE, "no particles set");
+    walk_params(bh, theta);
+    wait_orders(bh);
+    gc_ctx *ctx = bh->ctx;
+    cudaStream_t s = ctx->stream;
+    if (!bh->force_stream) {
+        GC_CUDA(cudaStreamCreateWithFlags(&bh->force_stream, cudaStreamNonBlocking));
+        GC_CUDA(cudaEventCreateWithFlags(&bh->ov_pre, cudaEventDisableTiming));
+        GC_CUDA(cudaEventCreateWithFlags(&bh->ov_done, cudaEventDisableTiming));
+    }
+    const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? bh->n_wg : bh->rg1;
+    const int f0 = wg_fg_first(bh, g0), f1 = wg_fg_first(bh, g1), nfg = f1 - f0;
+    bh->d_fq.resize(std::max(nfg, 1));
+    GC_CUDA(cudaMemsetAsync(bh->d_fq.p, 0xff, sizeof(int) * std::max(nfg, 1), s));
+    bh->d_fq_tail.resize(1);
+    bh->d_fq_tail.zero(s);
+    bh->d_out.resize(bh->n * bh->dim);
+    bh->d_next.resize(1);
+    bh->d_next.zero(s);
+    GC_CUDA(cudaEventRecord(bh->ev[0], s));
+    launch_walk(bh, true, false, bh->d_fq.p, bh->d_fq_tail.p, f0);
+    bh->have_union = true;
+    bh->have_member_lists = false;
+    bh->grec_valid = false;
+    // the force kernel: programmatic dependent launch on the same stream -- it
+    // may start once every walk block has a warp out of work (the walk's
+    // tail); readiness per force group comes from the queue, not grid order
+    cudaStream_t fs = s;  // nothing may sit between the two launches
+    if (nfg > 0) {
+        UnionPool U = pool_view(bh);
+        U.gfirst += f0;
+        U.gcount += f0;
+        U.grec += f0;
+        Staging S{};
+        S.next = bh->d_next.p;
+        S.fq = bh->d_fq.p;
+        const float eps2 = (float)(eps * eps);
+        auto k = eps2 == 0.f ? force_fused_kernel<true, false> : force_fused_kernel<false, false>;
+        int per_sm = 0;
+        GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * WARPS_PER_BLOCK, 0));
+        const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(
+            (int64_t)per_sm * ctx->prop.multiProcessorCount, grid_for(nfg, WARPS_PER_BLOCK)));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(pgrid);
+        cfg.blockDim = dim3(32 * WARPS_PER_BLOCK);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = fs;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const ForceGroup *fgp = bh->d_fg.p + f0;
+        GC_CUDA(cudaLaunchKernelEx(&cfg, k, nfg, fgp, U, S, (const float4 *)bh->d_parts.p,
+                                   (const float4 *)bh->d_rec_hi.p, (const float4 *)bh->d_rec_lo.p,
+                                   (const int *)bh->d_part_bucket.p, (const int *)bh->d_porder.p,
+                                   (const WalkGroup *)bh->d_wg.p, bh->cgrid, eps2, g, bh->dim, bh->d_out.p,
+                                   bh->d_pot.p));
+        check_launch("force_fused_kernel (overlap)");
+    }
+    // timings in this mode: walk = the whole overlapped step, force = 0
+    GC_CUDA(cudaEventRecord(bh->ev[1], fs));
+    GC_CUDA(cudaEventRecord(bh->ev[2], fs));
+    GC_CUDA(cudaEventRecord(bh->ev[4], fs));
+    GC_CUDA(cudaEventRecord(bh->ev[3], fs));
+    if (!bh->orders_fresh) make_orders(bh);  // the next walk's order
+}
+
 extern "C" {
 
 gc_status gc_bh_create(gc_ctx *ctx, gc_bh **out)
@@ -734,6 +809,29 @@ gc_status gc_debug_walk_prof(int64_t out[6], int32_t reset)
         (void)reset;
         for (int k = 0; k < 6; ++k) out[k] = 0;
 #endif
+    });
+}
+
+gc_status gc_bh_set_overlap(gc_bh *bh, int32_t on)
+{
+    return guard([&] {
+        GC_REQUIRE(bh, GC_E_VALUE, "null argument");
+        bh->overlap = on != 0;
+    });
+}
+
+// One step's walk + forces, asynchronous (gc_bh_walk + gc_bh_forces_async;
+// overlapped when gc_bh_set_overlap(1) and the force path is fused).
+gc_status gc_bh_walk_forces_async(gc_bh *bh, double theta, double g, double eps)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
+        if (bh->overlap && bh->force_fused && bh->stats_valid && bh->params_valid) {
+            run_overlapped(bh, theta, g, eps);
+        } else {
+            run_walk(bh, theta, true);
+            launch_forces(bh, g, eps);
+        }
     });
 }
 
@@ -1058,6 +1156,20 @@ gc_status gc_bh_step(gc_bh *bh, int64_t n, int32_t dim, const double *pos, const
     if (bh) bh->h2d = bh->d2h = 0;
     gc_status st = gc_bh_set_particles(bh, n, dim, pos, mass, box, bucket_size);
     if (st) return st;
+    if (bh->overlap && bh->force_fused) {
+        st = guard([&] {
+            run_overlapped(bh, theta, g, eps);
+            // a walk that overflowed the union pool is re-run (pool grown) before its forces count
+            while (walk_overflowed(bh)) {
+                launch_walk(bh, true, false);
+                launch_forces(bh, g, eps);
+            }
+            bh->d_out.download(out, bh->n * bh->dim, bh->ctx->stream);
+            bh->d2h += bh->n * bh->dim * (int64_t)sizeof(double);
+            GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
+        });
+        return st;
+    }
     st = guard([&] { run_walk(bh, theta, false); });  // no per-bucket stats on the step path
     if (st) return st;
     return gc_bh_forces(bh, g, eps, out);

@@ -162,7 +162,8 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
                   const float4 *__restrict__ recs, const double4 *__restrict__ com64,
                   const double4 *__restrict__ bgeo, const float4 *__restrict__ bgeo32, const WalkParams P,
                   UnionPool U, int64_t *__restrict__ bstat, int *__restrict__ flag, const int *__restrict__ order,
-                  int *__restrict__ next, int *__restrict__ wcost)
+                  int *__restrict__ next, int *__restrict__ wcost, int *__restrict__ fq = nullptr,
+                  int *__restrict__ fq_tail = nullptr, int fq_base = 0)
 {
     using u64 = unsigned long long;
     __shared__ int2 stack_s[WARPS_PER_BLOCK][STACK_CAP];  // (first | (nc - 1) << NODE_BITS, active buckets 0-31)
@@ -187,6 +188,9 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
     if (lane == 0) gi = atomicAdd(next, 1);
     gi = __shfl_sync(0xffffffffu, gi, 0);
     if (gi >= ngroups) {
+        // no work left for this warp: a programmatically dependent force
+        // kernel (overlap mode) may start taking SM slots
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #if WALK_PROF
         unsigned long long t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
@@ -388,6 +392,14 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
         U.gcount[my_fg] = w;
         if (NREC) U.grec[my_fg] = nrec;
     }
+    if (WRITE && fq) {  // overlap mode: the item's force groups are ready for the force kernel
+        __syncwarp();
+        __threadfence();
+        int base = 0;
+        if (lane == 0) base = atomicAdd(fq_tail, fb - fa);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (emits) atomicExch(fq + base + lane, my_fg - fq_base);
+    }
     if (STATS) {
 #pragma unroll
         for (int k = 0; k < BPL; ++k) {
@@ -558,6 +570,7 @@ struct Staging {
     const int64_t *rbase;  // first record of each force group's run (multiple of PFLUSH)
     const int *order;  // force groups in processing order
     int *next;  // dynamic work counter of the force kernel
+    int *fq;  // overlap mode: force groups in walk-completion order (-1: not yet published)
     int64_t cap;  // records
 };
 
@@ -889,7 +902,15 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
     for (int slot = lane == 0 ? atomicAdd(S.next, 1) : 0;;) {
         slot = __shfl_sync(0xffffffffu, slot, 0);
         if (slot >= nfg) break;
-        const int gi = S.order[slot];
+        int gi;
+        if (S.fq) {  // overlap mode: wait until the walk published this slot
+            if (lane == 0)
+                while ((gi = atomicAdd(S.fq + slot, 0)) < 0) __nanosleep(64);
+            gi = __shfl_sync(0xffffffffu, gi, 0);
+            __threadfence();
+        } else {
+            gi = S.order[slot];
+        }
         const ForceGroup fg = fgroups[gi];
         const bool tgt = lane < fg.ntarget;
         const int p = fg.pstart + (tgt ? lane : 0);
@@ -899,15 +920,16 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
         const float2 nx = f2(F.cx - xp.x, F.cx - xp.x), ny = f2(F.cy - xp.y, F.cy - xp.y),
                      nz = f2(F.cz - xp.z, F.cz - xp.z);
         double ax = 0.0, ay = 0.0, az = 0.0, ap = 0.0;
-        const int n = U.gcount[gi];
-        int chunk_cur = n > 0 ? U.gfirst[gi] : 0, cur_ci = 0;
-        int chunk_nxt = (n > CHUNK) ? U.cnext[chunk_cur] : 0;
+        // union lists via L2 (__ldcg): in the overlap mode the walk writes them while this kernel runs
+        const int n = __ldcg(U.gcount + gi);
+        int chunk_cur = n > 0 ? __ldcg(U.gfirst + gi) : 0, cur_ci = 0;
+        int chunk_nxt = (n > CHUNK) ? __ldcg(U.cnext + chunk_cur) : 0;
         int ebase = 0, wr = 0, rd = 0;
         auto load_entry = [&](int e) {
             int4 en = make_int4(0, 0, 0, 0);
             if (e < n) {
                 const int c = (e / CHUNK == cur_ci) ? chunk_cur : chunk_nxt;
-                en = U.ent[(int64_t)c * CHUNK + (e & (CHUNK - 1))];
+                en = __ldcg(U.ent + (int64_t)c * CHUNK + (e & (CHUNK - 1)));
             }
             return en;
         };
@@ -963,7 +985,7 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
                 if (ebase / CHUNK != cur_ci && ebase < n) {  // moved into the next chunk of the chain
                     chunk_cur = chunk_nxt;
                     cur_ci = ebase / CHUNK;
-                    chunk_nxt = ((cur_ci + 1) * CHUNK < n) ? U.cnext[chunk_cur] : 0;
+                    chunk_nxt = ((cur_ci + 1) * CHUNK < n) ? __ldcg(U.cnext + chunk_cur) : 0;
                 }
             }
 #if FUSED_PREFETCH

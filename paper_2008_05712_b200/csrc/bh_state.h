@@ -31,6 +31,10 @@ struct gc_bh {
     bool host_tree_valid = false;
     bool device_build = true;  // build the tree on the GPU (gc_bh_set_build_mode)
     bool force_fused = true;
+    bool overlap = true;  // walk and force kernel of a step overlap (gc_bh_set_overlap; fused mode)
+    cudaStream_t force_stream = nullptr;
+    cudaEvent_t ov_pre = nullptr, ov_done = nullptr;
+    DBuf<int> d_fq, d_fq_tail;
     bool grec_valid = false;  // d_grec matches the current union lists
     bool staging_sized = false;  // the staging buffer holds the current lists' runs  // reorganise into shared memory inside the force kernel (gc_bh_set_force_mode)
     // tree metadata (always valid once particles are set)
@@ -128,6 +132,12 @@ struct gc_bh {
             cudaStreamDestroy(order_stream);
         }
         if (order_ready) cudaEventDestroy(order_ready);
+        if (force_stream) {
+            cudaStreamSynchronize(force_stream);
+            cudaStreamDestroy(force_stream);
+        }
+        if (ov_pre) cudaEventDestroy(ov_pre);
+        if (ov_done) cudaEventDestroy(ov_done);
         if (order_done) cudaEventDestroy(order_done);
     }
 };
