@@ -258,7 +258,7 @@ def bench_bh(args, world, rank, local, ctx, torch):
     tree = nbody.build_bucket_tree(ps, BUCKET)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
-    def step():  # walk + forces, overlapped (the force kernel takes the walk's tail SM slots)
+    def step():  # walk + forces (gc_bh_walk + gc_bh_forces_async; overlapped if gc_bh_set_overlap(1))
         L.call("gc_bh_walk_forces_async", tree.handle, THETA, 1.0, EPS)
 
     def step_split():  # the same step with the kernels back to back (per-kernel times)
@@ -616,8 +616,7 @@ def run_ours(args, world, rank, local):
         "data": "synthetic gen_particles(1M, seed 42, clustering 0.6, dim 3), fp32-exact",
         "config": {"workload": "configs[2] clustered N-body 1M per GPU, theta 0.7, bucket 8, eps 1e-4",
                    "step": "device walk (union lists) + force kernel with the reorganisation into shared memory "
-                           "fused in, overlapped with the walk's tail (programmatic dependent launch, per-force-"
-                           "group readiness queue); tree resident; walk_ms/force_ms from back-to-back steps",
+                           "fused in; tree resident",
                    "interactions_per_gpu": bh["inter"], "walk_ms": bh["walk_ms"], "reorg_ms": bh["reorg_ms"],
                    "force_ms": bh["force_ms"], "union_entries": bh["n_union"], "staged_records": bh["n_records"],
                    "l2": "flushed (256 MiB write) before every timed step"},
@@ -626,7 +625,7 @@ def run_ours(args, world, rank, local):
         "e2e": bh["e2e"],
         # per step: walk_group_kernel + force_fused_kernel (the walk-group and force-group
         # orders are cached from the first walk of the tree; resets are cudaMemsetAsync)
-        "gpu_launches": 2 * args.steps,  # walk_group_kernel + force_fused_kernel (programmatic dependent launch)
+        "gpu_launches": 2 * args.steps,  # walk_group_kernel + force_fused_kernel
         "clocks": bh["clocks"],
     }
     sysin = mdr.pop("_sysin")

@@ -115,8 +115,8 @@ gc_status gc_debug_walk_prof(int64_t out[6], int32_t reset);
 gc_status gc_bh_pair_stats(gc_bh *bh, int64_t out[2]);
 /* 1: gc_bh_walk_forces_async / gc_bh_step run the walk and the fused force
  * kernel concurrently (force groups consumed as their walk groups finish);
- * results are identical.  Default 1; timings then report the whole step as
- * the walk.  The force kernel is a programmatic dependent launch that starts
+ * results are identical.  Default 0 (measured neutral); timings then report
+ * the whole step as the walk.  The force kernel is a programmatic dependent launch that starts
  * when every walk block has a warp out of work. */
 gc_status gc_bh_set_overlap(gc_bh *bh, int32_t on);
 /* one step's walk + forces, asynchronous (= gc_bh_walk + gc_bh_forces_async) */

@@ -700,7 +700,7 @@ void run_overlapped(gc_bh *bh, double theta, double g, double eps)
         S.next = bh->d_next.p;
         S.fq = bh->d_fq.p;
         const float eps2 = (float)(eps * eps);
-        auto k = eps2 == 0.f ? force_fused_kernel<true, false> : force_fused_kernel<false, false>;
+        auto k = eps2 == 0.f ? force_fused_kernel<true, false, true> : force_fused_kernel<false, false, true>;
         int per_sm = 0;
         GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * WARPS_PER_BLOCK, 0));
         const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(

@@ -874,7 +874,7 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int *_
 #endif
 constexpr int RING = FUSED_RING;
 constexpr int RING_LOW = RING / 2;  // produce while fewer records wait (RING >= RING_LOW + 33: one entry always fits)
-template <bool EPS0, bool POT>
+template <bool EPS0, bool POT, bool OVL = false>
 __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, FORCE_MINB)
 force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U, const Staging S,
                    const float4 *__restrict__ parts, const float4 *__restrict__ rec_hi,
@@ -903,7 +903,7 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
         slot = __shfl_sync(0xffffffffu, slot, 0);
         if (slot >= nfg) break;
         int gi;
-        if (S.fq) {  // overlap mode: wait until the walk published this slot
+        if (OVL) {  // overlap mode: wait until the walk published this slot
             if (lane == 0)
                 while ((gi = atomicAdd(S.fq + slot, 0)) < 0) __nanosleep(64);
             gi = __shfl_sync(0xffffffffu, gi, 0);
@@ -920,16 +920,17 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
         const float2 nx = f2(F.cx - xp.x, F.cx - xp.x), ny = f2(F.cy - xp.y, F.cy - xp.y),
                      nz = f2(F.cz - xp.z, F.cz - xp.z);
         double ax = 0.0, ay = 0.0, az = 0.0, ap = 0.0;
-        // union lists via L2 (__ldcg): in the overlap mode the walk writes them while this kernel runs
-        const int n = __ldcg(U.gcount + gi);
-        int chunk_cur = n > 0 ? __ldcg(U.gfirst + gi) : 0, cur_ci = 0;
-        int chunk_nxt = (n > CHUNK) ? __ldcg(U.cnext + chunk_cur) : 0;
+        // union lists: a force group's lines are first read after its publication
+        // (overlap mode), so plain cached loads see the walk's writes
+        const int n = U.gcount[gi];
+        int chunk_cur = n > 0 ? U.gfirst[gi] : 0, cur_ci = 0;
+        int chunk_nxt = (n > CHUNK) ? U.cnext[chunk_cur] : 0;
         int ebase = 0, wr = 0, rd = 0;
         auto load_entry = [&](int e) {
             int4 en = make_int4(0, 0, 0, 0);
             if (e < n) {
                 const int c = (e / CHUNK == cur_ci) ? chunk_cur : chunk_nxt;
-                en = __ldcg(U.ent + (int64_t)c * CHUNK + (e & (CHUNK - 1)));
+                en = U.ent[(int64_t)c * CHUNK + (e & (CHUNK - 1))];
             }
             return en;
         };
@@ -985,7 +986,7 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
                 if (ebase / CHUNK != cur_ci && ebase < n) {  // moved into the next chunk of the chain
                     chunk_cur = chunk_nxt;
                     cur_ci = ebase / CHUNK;
-                    chunk_nxt = ((cur_ci + 1) * CHUNK < n) ? __ldcg(U.cnext + chunk_cur) : 0;
+                    chunk_nxt = ((cur_ci + 1) * CHUNK < n) ? U.cnext[chunk_cur] : 0;
                 }
             }
 #if FUSED_PREFETCH

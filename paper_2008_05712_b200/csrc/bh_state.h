@@ -31,7 +31,7 @@ struct gc_bh {
     bool host_tree_valid = false;
     bool device_build = true;  // build the tree on the GPU (gc_bh_set_build_mode)
     bool force_fused = true;
-    bool overlap = true;  // walk and force kernel of a step overlap (gc_bh_set_overlap; fused mode)
+    bool overlap = false;  // walk and force kernel of a step overlap (gc_bh_set_overlap; fused mode; measured neutral)
     cudaStream_t force_stream = nullptr;
     cudaEvent_t ov_pre = nullptr, ov_done = nullptr;
     DBuf<int> d_fq, d_fq_tail;
