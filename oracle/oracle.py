@@ -53,8 +53,11 @@ def lib():
         L.orc_free_tree.argtypes = [C.POINTER(_Tree)]
         L.orc_build_lists.argtypes = [C.POINTER(_Tree), C.c_int, C.c_double, i64p,
                                       C.POINTER(i64p), C.POINTER(i8p), i64p, C.c_int]
+        L.orc_build_lists_range.argtypes = [C.POINTER(_Tree), C.c_int, C.c_double, C.c_int64, C.c_int64, i64p,
+                                            C.POINTER(i64p), C.POINTER(i8p), i64p, C.c_int]
         L.orc_eval_forces.argtypes = [C.POINTER(_Tree), C.c_int, f64p, f64p, i64p, i64p, i8p,
                                       C.c_int64, C.c_int64, C.c_double, C.c_double, f64p, C.c_int]
+        L.orc_eval_potentials.argtypes = L.orc_eval_forces.argtypes
         L.orc_forces_from_points.argtypes = [C.c_int64, C.c_int64, C.c_int, f64p, f64p, f64p, f64p,
                                              C.c_double, C.c_double, f64p]
         L.orc_direct_forces.argtypes = [C.c_int64, C.c_int, f64p, f64p, C.c_double, C.c_double, f64p, C.c_int]
@@ -180,15 +183,17 @@ def build_bucket_tree(positions, masses, bucket_size, box=1.0) -> OracleTree:
     return out
 
 
-def build_interaction_lists(tree: OracleTree, theta, nthreads=0) -> OracleLists:
+def build_interaction_lists(tree: OracleTree, theta, nthreads=0, bucket_range=None) -> OracleLists:
+    """bucket_range=(b0, b1): walk only those DFS buckets (the rest get empty lists)."""
     L = lib()
     ct = tree._ctree()
     nb = len(tree.buckets)
     ptr = np.zeros(nb + 1, np.int64)
     ic = np.zeros(nb, np.int64)
     ids_p, kind_p = i64p(), i8p()
-    rc = L.orc_build_lists(C.byref(ct), tree.dim, float(theta), _p(ptr, i64p), C.byref(ids_p),
-                           C.byref(kind_p), _p(ic, i64p), int(nthreads))
+    b0, b1 = (0, nb) if bucket_range is None else bucket_range
+    rc = L.orc_build_lists_range(C.byref(ct), tree.dim, float(theta), int(b0), int(b1), _p(ptr, i64p),
+                                 C.byref(ids_p), C.byref(kind_p), _p(ic, i64p), int(nthreads))
     if rc != 0:
         raise ValueError("theta must be >= 0")
     tot = int(ptr[-1])
@@ -212,6 +217,25 @@ def eval_forces(tree: OracleTree, lists: OracleLists, positions, masses, g=1.0, 
     kind = np.ascontiguousarray(lists.kind, np.int8)
     L.orc_eval_forces(C.byref(ct), tree.dim, _p(pos, f64p), _p(m, f64p), _p(ptr, i64p), _p(ids, i64p),
                       _p(kind, i8p), int(b0), int(b1), float(g), float(eps), _p(out, f64p), int(nthreads))
+    return out
+
+
+def eval_potentials(tree: OracleTree, lists: OracleLists, positions, masses, g=1.0, eps=1e-4,
+                    bucket_range=None, nthreads=0):
+    """Per-particle potential -g m_i sum_j m_j / sqrt(r^2 + eps^2) over the
+    interaction lists (restated beside forces_from_points, hr/kernels.py:70-88;
+    no reference counterpart: parity unpinned, pinned by the direct sum at
+    theta = 0 in tests/test_oracle_golden.py)."""
+    L = lib()
+    ct = tree._ctree()
+    pos, m = _f64(positions), _f64(masses)
+    out = np.zeros(pos.shape[0])
+    b0, b1 = (0, len(tree.buckets)) if bucket_range is None else bucket_range
+    ptr = np.ascontiguousarray(lists.ptr, np.int64)
+    ids = np.ascontiguousarray(lists.ids, np.int64)
+    kind = np.ascontiguousarray(lists.kind, np.int8)
+    L.orc_eval_potentials(C.byref(ct), tree.dim, _p(pos, f64p), _p(m, f64p), _p(ptr, i64p), _p(ids, i64p),
+                          _p(kind, i8p), int(b0), int(b1), float(g), float(eps), _p(out, f64p), int(nthreads))
     return out
 
 

@@ -540,7 +540,7 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
     bh->d_out.resize(bh->n * bh->dim);
     if (pot) bh->d_pot.resize(bh->n);
     const float eps2 = (float)(eps * eps);
-    const bool eps0 = eps2 == 0.f;
+    const bool eps0 = bh_use_cube(eps2);
     GC_CUDA(cudaEventRecord(bh->ev[2], s));
     if (bh->have_union) {
         const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? bh->n_wg : bh->rg1;
@@ -700,7 +700,7 @@ void run_overlapped(gc_bh *bh, double theta, double g, double eps)
         S.next = bh->d_next.p;
         S.fq = bh->d_fq.p;
         const float eps2 = (float)(eps * eps);
-        auto k = eps2 == 0.f ? force_fused_kernel<true, false, true> : force_fused_kernel<false, false, true>;
+        auto k = bh_use_cube(eps2) ? force_fused_kernel<true, false, true> : force_fused_kernel<false, false, true>;
         int per_sm = 0;
         GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * WARPS_PER_BLOCK, 0));
         const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(
@@ -826,7 +826,9 @@ gc_status gc_bh_walk_forces_async(gc_bh *bh, double theta, double g, double eps)
 {
     return guard([&] {
         GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
-        if (bh->overlap && bh->force_fused && bh->stats_valid && bh->params_valid) {
+        // the overlapped walk has no overflow re-walk: only for a (tree, theta)
+        // whose pool was sized by a completed stats walk
+        if (bh->overlap && bh->force_fused && bh->stats_valid && bh->params_valid && bh->cap_theta == theta) {
             run_overlapped(bh, theta, g, eps);
         } else {
             run_walk(bh, theta, true);
@@ -915,7 +917,7 @@ gc_status gc_bh_get_lists(gc_bh *bh, int64_t *ptr, int64_t *ids, int8_t *kind, i
 {
     return guard([&] {
         GC_REQUIRE(bh && bh->have_union, GC_E_STATE, "no device walk has run");
-        GC_REQUIRE(bh->rg0 == 0 && bh->rg1 < 0, GC_E_STATE, "per-bucket lists need the full walk-group range");
+        // with a walk-group range (gc_bh_set_range) the buckets outside it get empty lists
         ensure_union_complete(bh);
         sync_walk_stats(bh);
         cudaStream_t s = bh->ctx->stream;
@@ -931,7 +933,10 @@ gc_status gc_bh_get_lists(gc_bh *bh, int64_t *ptr, int64_t *ids, int8_t *kind, i
             for (int64_t b = 0; b < nb; ++b) item_count[b] = st[2 * b + 1];
         if (ids || kind) {
             GC_REQUIRE(tot < (1ll << 31), GC_E_VALUE, "more than 2^31 list entries");
-            const int nf = bh->n_fg;
+            const int f0 = wg_fg_first(bh, bh->rg0), nf = wg_fg_first(bh, bh->rg1 < 0 ? bh->n_wg : bh->rg1) - f0;
+            UnionPool U = pool_view(bh);
+            U.gfirst += f0;
+            U.gcount += f0;
             // preorder (depth-first, children in octant order) index of every node
             ensure_host_tree(bh);
             const HostTree &t = bh->tree;
@@ -949,7 +954,7 @@ gc_status gc_bh_get_lists(gc_bh *bh, int64_t *ptr, int64_t *ids, int8_t *kind, i
             auto &k0 = bh->d_list_key, &k1 = bh->d_list_key2, &v0 = bh->d_list_val, &v1 = bh->d_list_val2;
             k0.resize(tot); k1.resize(tot); v0.resize(tot); v1.resize(tot);
             union_to_lists_kernel<<<grid_for(nf, WARPS_PER_BLOCK), 32 * WARPS_PER_BLOCK, 0, s>>>(
-                nf, bh->d_fg.p, bh->d_wg.p, pool_view(bh), bh->d_bptr.p, bh->d_pre.p, k0.p, v0.p);
+                nf, bh->d_fg.p + f0, bh->d_wg.p, U, bh->d_bptr.p, bh->d_pre.p, k0.p, v0.p);
             check_launch("union_to_lists_kernel");
             size_t bytes = 0;
             GC_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, k0.p, k1.p, v0.p, v1.p, (int)tot, (int)nb,

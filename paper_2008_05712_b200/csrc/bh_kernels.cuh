@@ -466,7 +466,14 @@ static __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK) grec_kernel(int n
 // ---------------------------------------------------------------------------
 // force kernels
 // ---------------------------------------------------------------------------
-// single MUFU.RSQ (r^6 >= eps^6 is a normal float whenever eps > 0)
+// single MUFU.RSQ of r^6 when eps^6 is a normal float (r^6 >= eps^6); otherwise
+// (eps = 0 or tiny, bh_use_cube) the EPS0 instances cube rsqrt(r^2), taking 0
+// for r^2 <= kCubeFloor (coincident sources: dx = 0, and 1/r^3 would overflow)
+constexpr float kCubeFloor = 1e-25f;
+__host__ __device__ inline bool bh_use_cube(float eps2)
+{
+    return (double)eps2 * (double)eps2 * (double)eps2 < 1.1754943508222875e-38;  // FLT_MIN
+}
 __device__ __forceinline__ float rsqrt_approx(float x)
 {
     float y;
@@ -484,7 +491,7 @@ __device__ __forceinline__ void interact(const float4 h, const float3 l, const f
     float inv3;
     if (EPS0) {  // no softening floor: r^6 may leave the float range, cube 1/r instead
         const float ir = rsqrt_approx(r2);
-        inv3 = r2 > 0.f ? ir * ir * ir : 0.f;  // coincident source (kernels.py:83-84)
+        inv3 = r2 > kCubeFloor ? ir * ir * ir : 0.f;  // coincident source (kernels.py:83-84)
     } else {
         inv3 = rsqrt_approx(r2 * r2 * r2);
     }
@@ -492,7 +499,7 @@ __device__ __forceinline__ void interact(const float4 h, const float3 l, const f
     a.x = fmaf(dx, w, a.x);
     a.y = fmaf(dy, w, a.y);
     a.z = fmaf(dz, w, a.z);
-    if (POT) pot = fmaf(r2 != eps2 ? w : 0.f, r2, pot);  // m / sqrt(r^2 + eps^2); coincident skipped
+    if (POT) pot = fmaf((dx != 0.f || dy != 0.f || dz != 0.f) ? w : 0.f, r2, pot);  // m / sqrt(r^2 + eps^2); coincident skipped (kernels.py:78-84)
 }
 
 // One group-relative source record (x, y, z, m) against one target.
@@ -505,7 +512,7 @@ __device__ __forceinline__ void interact_rel(const float4 q, const float m_eff, 
     float inv3;
     if (EPS0) {  // no softening floor: r^6 may leave the float range, cube 1/r instead
         const float ir = rsqrt_approx(r2);
-        inv3 = r2 > 0.f ? ir * ir * ir : 0.f;  // coincident source (kernels.py:83-84)
+        inv3 = r2 > kCubeFloor ? ir * ir * ir : 0.f;  // coincident source (kernels.py:83-84)
     } else {
         inv3 = rsqrt_approx(r2 * r2 * r2);
     }
@@ -513,7 +520,7 @@ __device__ __forceinline__ void interact_rel(const float4 q, const float m_eff, 
     a.x = fmaf(dx, w, a.x);
     a.y = fmaf(dy, w, a.y);
     a.z = fmaf(dz, w, a.z);
-    if (POT) pot = fmaf(r2 != eps2 ? w : 0.f, r2, pot);  // m / sqrt(r^2 + eps^2); coincident skipped
+    if (POT) pot = fmaf((dx != 0.f || dy != 0.f || dz != 0.f) ? w : 0.f, r2, pot);  // m / sqrt(r^2 + eps^2); coincident skipped (kernels.py:78-84)
 }
 
 __device__ __forceinline__ float warp_min(float v)
@@ -817,8 +824,8 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int *_
                         float i0, i1;
                         if (EPS0) {  // no softening floor: cube 1/r (r^6 may leave the float range)
                             const float j0 = rsqrt_approx(r2.x), j1 = rsqrt_approx(r2.y);
-                            i0 = r2.x > 0.f ? j0 * j0 * j0 : 0.f;  // coincident source (kernels.py:83-84)
-                            i1 = r2.y > 0.f ? j1 * j1 * j1 : 0.f;
+                            i0 = r2.x > kCubeFloor ? j0 * j0 * j0 : 0.f;  // coincident source (kernels.py:83-84)
+                            i1 = r2.y > kCubeFloor ? j1 * j1 * j1 : 0.f;
                         } else {
                             const float2 r6 = __fmul2_rn(__fmul2_rn(r2, r2), r2);
                             i0 = rsqrt_approx(r6.x);
@@ -830,7 +837,9 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int *_
                         sy = __ffma2_rn(dy, w, sy);
                         sz = __ffma2_rn(dz, w, sz);
                         if (POT) {  // m / sqrt(r^2 + eps^2); coincident skipped
-                            const float2 wp = f2(r2.x != eps2 ? w.x : 0.f, r2.y != eps2 ? w.y : 0.f);
+                            // coincident sources skipped exactly as kernels.py:78-84 (all dx == 0)
+                            const float2 wp = f2((dx.x != 0.f || dy.x != 0.f || dz.x != 0.f) ? w.x : 0.f,
+                                                 (dx.y != 0.f || dy.y != 0.f || dz.y != 0.f) ? w.y : 0.f);
                             sp = __ffma2_rn(wp, r2, sp);
                         }
                     }
@@ -873,6 +882,17 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int *_
 #define FUSED_RING 128
 #endif
 constexpr int RING = FUSED_RING;
+__device__ __forceinline__ int ld_acquire_gpu(const int *p)
+{
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+template <bool CG>
+__device__ __forceinline__ int ld_list(const int *p)
+{
+    return CG ? __ldcg(p) : *p;
+}
 constexpr int RING_LOW = RING / 2;  // produce while fewer records wait (RING >= RING_LOW + 33: one entry always fits)
 template <bool EPS0, bool POT, bool OVL = false>
 __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, FORCE_MINB)
@@ -903,11 +923,10 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
         slot = __shfl_sync(0xffffffffu, slot, 0);
         if (slot >= nfg) break;
         int gi;
-        if (OVL) {  // overlap mode: wait until the walk published this slot
+        if (OVL) {  // overlap mode: wait until the walk published this slot (acquire)
             if (lane == 0)
-                while ((gi = atomicAdd(S.fq + slot, 0)) < 0) __nanosleep(64);
+                while ((gi = ld_acquire_gpu(S.fq + slot)) < 0) __nanosleep(64);
             gi = __shfl_sync(0xffffffffu, gi, 0);
-            __threadfence();
         } else {
             gi = S.order[slot];
         }
@@ -920,17 +939,18 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
         const float2 nx = f2(F.cx - xp.x, F.cx - xp.x), ny = f2(F.cy - xp.y, F.cy - xp.y),
                      nz = f2(F.cz - xp.z, F.cz - xp.z);
         double ax = 0.0, ay = 0.0, az = 0.0, ap = 0.0;
-        // union lists: a force group's lines are first read after its publication
-        // (overlap mode), so plain cached loads see the walk's writes
-        const int n = U.gcount[gi];
-        int chunk_cur = n > 0 ? U.gfirst[gi] : 0, cur_ci = 0;
-        int chunk_nxt = (n > CHUNK) ? U.cnext[chunk_cur] : 0;
+        // union lists: in overlap mode the walk wrote them during this launch,
+        // and neighbouring force groups share lines an SM may have cached in
+        // L1 before this group was published -- read them L2-coherent (.cg)
+        const int n = ld_list<OVL>(U.gcount + gi);
+        int chunk_cur = n > 0 ? ld_list<OVL>(U.gfirst + gi) : 0, cur_ci = 0;
+        int chunk_nxt = (n > CHUNK) ? ld_list<OVL>(U.cnext + chunk_cur) : 0;
         int ebase = 0, wr = 0, rd = 0;
         auto load_entry = [&](int e) {
             int4 en = make_int4(0, 0, 0, 0);
             if (e < n) {
                 const int c = (e / CHUNK == cur_ci) ? chunk_cur : chunk_nxt;
-                en = U.ent[(int64_t)c * CHUNK + (e & (CHUNK - 1))];
+                en = OVL ? __ldcg(U.ent + (int64_t)c * CHUNK + (e & (CHUNK - 1))) : U.ent[(int64_t)c * CHUNK + (e & (CHUNK - 1))];
             }
             return en;
         };
@@ -986,7 +1006,7 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
                 if (ebase / CHUNK != cur_ci && ebase < n) {  // moved into the next chunk of the chain
                     chunk_cur = chunk_nxt;
                     cur_ci = ebase / CHUNK;
-                    chunk_nxt = ((cur_ci + 1) * CHUNK < n) ? U.cnext[chunk_cur] : 0;
+                    chunk_nxt = ((cur_ci + 1) * CHUNK < n) ? ld_list<OVL>(U.cnext + chunk_cur) : 0;
                 }
             }
 #if FUSED_PREFETCH
@@ -1032,8 +1052,8 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
                         float i0, i1;
                         if (EPS0) {  // no softening floor: cube 1/r (r^6 may leave the float range)
                             const float j0 = rsqrt_approx(r2.x), j1 = rsqrt_approx(r2.y);
-                            i0 = r2.x > 0.f ? j0 * j0 * j0 : 0.f;  // coincident source (kernels.py:83-84)
-                            i1 = r2.y > 0.f ? j1 * j1 * j1 : 0.f;
+                            i0 = r2.x > kCubeFloor ? j0 * j0 * j0 : 0.f;  // coincident source (kernels.py:83-84)
+                            i1 = r2.y > kCubeFloor ? j1 * j1 * j1 : 0.f;
                         } else {
                             const float2 r6 = __fmul2_rn(__fmul2_rn(r2, r2), r2);
                             i0 = rsqrt_approx(r6.x);
@@ -1045,7 +1065,9 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
                         sy = __ffma2_rn(dy, w, sy);
                         sz = __ffma2_rn(dz, w, sz);
                         if (POT) {
-                            const float2 wp = f2(r2.x != eps2 ? w.x : 0.f, r2.y != eps2 ? w.y : 0.f);
+                            // coincident sources skipped exactly as kernels.py:78-84 (all dx == 0)
+                            const float2 wp = f2((dx.x != 0.f || dy.x != 0.f || dz.x != 0.f) ? w.x : 0.f,
+                                                 (dx.y != 0.f || dy.y != 0.f || dz.y != 0.f) ? w.y : 0.f);
                             sp = __ffma2_rn(wp, r2, sp);
                         }
                     }

@@ -305,8 +305,9 @@ ewald_slot_kernel(int nmember, const int *__restrict__ member_bucket, const int 
 
 void dm_kernel_spec(const char *cls, int64_t out[5])
 {
-    (void)cls;  // "ewald_member"
-    const void *fn = (const void *)ewald_slot_kernel;
+    // "ewald_member": ewald_slot_kernel; "force_slot": the member kernel
+    // gc_bh_run_members actually launches (one warp per request)
+    const void *fn = !strcmp(cls, "force_slot") ? (const void *)force_slot_kernel<false> : (const void *)ewald_slot_kernel;
     cudaFuncAttributes a;
     GC_CUDA(cudaFuncGetAttributes(&a, fn));
     int blocks = 0;
@@ -805,7 +806,7 @@ gc_status gc_bh_run_members(gc_bh *bh, gc_dm *dm, const int64_t *member_buckets,
         GC_CUDA(cudaEventRecord(bh->ev[2], s));  // member kernel time -> gc_bh_timings out[1]
         GC_CUDA(cudaEventRecord(bh->ev[4], s));
         if (n_members > 0) {
-            auto k = eps2 == 0.f ? force_slot_kernel<true> : force_slot_kernel<false>;
+            auto k = bh_use_cube(eps2) ? force_slot_kernel<true> : force_slot_kernel<false>;
             k<<<grid_for(n_members, 8), 256, 0, s>>>(n_members, dm->members.p, dm->bounds.p, dm->addr.p, dm->kinds.p,
                                                      bh->d_brange.p, bh->d_parts.p, bh->d_porder.p, dm->pool.p, slot_f4,
                                                      eps2, g, bh->dim, bh->d_out.p);

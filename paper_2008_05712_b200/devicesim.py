@@ -80,7 +80,8 @@ def b200_device_spec(ctx=None) -> DeviceSpec:
 
 def b200_kernel_spec(kernel_class: str, ctx=None) -> KernelSpec:
     """KernelSpec of a real sm_100a kernel: "force" (BH group force), "walk",
-    "force_member" (one warp per work request), "md" (cell kernel)."""
+    "force_member" (one warp per work request), "force_slot" (the data-manager
+    member kernel gc_bh_run_members launches), "ewald_member", "md" (cell kernel)."""
     from . import _lib as L
     v = (ctx or L.context()).kernel_spec(kernel_class)
     return KernelSpec(kernel_class, int(v[0]), int(v[1]), int(v[2]), members_per_block=int(v[3]))

@@ -112,7 +112,7 @@ class GpuForceExecutor:
         self.memories = {c: DeviceMemory(per_class, slot_bytes, mode) for c in classes}
         self.memory = self.memories["force"]
         if max_size is None:
-            max_size = compute_max_size(b200_kernel_spec("force_member"), b200_device_spec())
+            max_size = compute_max_size(b200_kernel_spec("force_slot"), b200_device_spec())
         self.runtime = Runtime()
         self.states = {"force": AggregatorState("force", int(max_size), timeout_factor)}
         if ewald is not None:
@@ -127,6 +127,7 @@ class GpuForceExecutor:
             self.runtime.register_group(self.states[c])
         self.state = self.states["force"]
         self._next_id = 0
+        self.plan_log = None  # set to a list to record every plan
 
     # -- one combined launch (replaces Timeline._launch_gpu's cost model) ----------
     def _member_kinds(self, buckets) -> np.ndarray:
@@ -138,6 +139,8 @@ class GpuForceExecutor:
         members = [wr.buffer_indices for wr in combined.members]
         buckets = np.array([wr.owner for wr in combined.members], np.int64)
         plan, layout = mem.build_plan(members, now)
+        if self.plan_log is not None:  # parity instrumentation: (class, members, now, transfers, addresses)
+            self.plan_log.append((cls, members, now, [b for b, _ in plan.to_transfer], layout.addresses.copy()))
         npos = int(layout.member_bounds[-1])
         L.call("gc_dm_stage_bh", mem.handle, self.tree.handle)
         if cls == "force":

@@ -270,6 +270,20 @@ def eval_forces(tree: BucketTree, lists, ps: ParticleSet | None = None, g: float
     return out
 
 
+def eval_forces_potential(tree: BucketTree, lists: "InteractionLists", g: float = 1.0,
+                          eps: float = DEFAULT_SOFTENING):
+    """Forces (as eval_forces) plus per-particle potential energy
+    -g m_i sum_j m_j / sqrt(r^2 + eps^2) over the same lists (no reference
+    counterpart; the oracle restates it beside forces_from_points,
+    hr/kernels.py:70-88).  Device lists only."""
+    if not (isinstance(lists, InteractionLists) and lists.tree is tree):
+        raise ValueError("eval_forces_potential: needs the tree's own device lists")
+    _ensure_walk(tree, lists)
+    f, pot = np.zeros((tree.n, tree.dim)), np.zeros(tree.n)
+    L.call("gc_bh_forces_potential", tree.handle, float(g), float(eps), L.ptr(f, L.f64p), L.ptr(pot, L.f64p))
+    return f, pot
+
+
 def interactions(tree: BucketTree) -> int:
     """Sum over buckets of n_b * item_count_b for the current lists."""
     out = np.zeros(1, np.int64)

@@ -324,3 +324,129 @@ def test_overlapped_step_bit_identical():
         L.call("gc_bh_set_overlap", st.handle, ov)
         st(ps.positions, ps.masses, 1.0, g)
         np.testing.assert_array_equal(g, out[0])
+
+
+@pytest.mark.parametrize("case", ["plummer16k", "clustered1m"])
+def test_potential_energy_parity(nb, case):
+    """north_star: per-particle forces AND energies within 1e-5 of float64.
+    The potential is checked against the oracle's float64 restatement
+    (orc_eval_potentials, beside forces_from_points kernels.py:70-88) at
+    configs[0] (Plummer 16K) and configs[2] (clustered 1M) full size."""
+    from paper_2008_05712_b200 import generators as gen
+    from oracle import oracle as orc
+    ps = gen.fp32_exact(gen.gen_plummer(16384, 42) if case == "plummer16k"
+                        else gen.gen_particles(1_000_000, 42, clustering=0.6, dim=3))
+    tree = nb.build_bucket_tree(ps, 8)
+    lists = nb.build_interaction_lists(tree, 0.7, ps)
+    f, pot = nb.eval_forces_potential(tree, lists, 1.0, 1e-4)
+    ot = orc.build_bucket_tree(ps.positions, ps.masses, 8)
+    ol = orc.build_interaction_lists(ot, 0.7)
+    ref_f = orc.eval_forces(ot, ol, ps.positions, ps.masses, 1.0, 1e-4)
+    ref_p = orc.eval_potentials(ot, ol, ps.positions, ps.masses, 1.0, 1e-4)
+    assert rel_err(f, ref_f).max() <= FORCE_RTOL
+    ep = np.abs(pot - ref_p) / np.abs(ref_p)
+    print(f"{case}: potential rel err median {np.median(ep):.2e} max {ep.max():.2e}")
+    assert ep.max() <= FORCE_RTOL
+
+
+@pytest.mark.parametrize("eps", [1e-7, 1e-12, 0.0])
+def test_tiny_softening_finite_and_exact(eps):
+    """0 < eps < ~5e-7 makes eps^6 subnormal in float32: the kernels must take
+    the cube-of-rsqrt form (finite, coincident sources skipped) and still
+    match the oracle.  Includes a duplicated particle."""
+    from oracle import oracle as orc
+    from paper_2008_05712_b200 import generators as gen
+    from paper_2008_05712_b200 import nbody
+    ps = gen.fp32_exact(gen.gen_particles(6000, 5, clustering=0.6, dim=3))
+    pos = ps.positions.copy()
+    if eps > 0:
+        pos[17] = pos[3]  # coincident pair: needs eps > 0 in the reference
+    ps = gen.ParticleSet(pos, ps.masses, np.zeros_like(pos), 1.0)
+    tree = nbody.build_bucket_tree(ps, 8)
+    lists = nbody.build_interaction_lists(tree, 0.6, ps)
+    f, pot = nbody.eval_forces_potential(tree, lists, 1.0, eps)
+    assert np.isfinite(f).all() and np.isfinite(pot).all()
+    ot = orc.build_bucket_tree(ps.positions, ps.masses, 8)
+    ol = orc.build_interaction_lists(ot, 0.6)
+    ref = orc.eval_forces(ot, ol, ps.positions, ps.masses, 1.0, eps)
+    refp = orc.eval_potentials(ot, ol, ps.positions, ps.masses, 1.0, eps)
+    assert rel_err(f, ref).max() <= FORCE_RTOL
+    assert (np.abs(pot - refp) / np.abs(refp)).max() <= FORCE_RTOL
+    f2 = nbody.eval_forces(tree, lists, ps, 1.0, eps)  # force-only instance
+    assert rel_err(f2, ref).max() <= FORCE_RTOL
+
+
+def test_overlap_theta_change_rewalks():
+    """Overlap mode with a new theta must not reuse the old theta's pool sizing
+    (ADVICE r1): it falls back to the checked walk, forces equal the plain path."""
+    from paper_2008_05712_b200 import _lib as L
+    from paper_2008_05712_b200 import generators as gen
+    from paper_2008_05712_b200 import nbody
+    ps = gen.fp32_exact(gen.gen_particles(100_000, 4, clustering=0.6, dim=3))
+    n = len(ps.positions)
+    tree = nbody.build_bucket_tree(ps, 8)
+    L.call("gc_bh_walk", tree.handle, 0.9)
+    L.call("gc_bh_set_overlap", tree.handle, 1)
+    outs = []
+    for th in (0.9, 0.3, 0.3):  # 0.3 needs far more list entries than 0.9
+        L.call("gc_bh_walk_forces_async", tree.handle, th, 1.0, 1e-4)
+        f = np.zeros((n, 3))
+        L.call("gc_bh_get_forces", tree.handle, L.ptr(f, L.f64p))
+        outs.append(f)
+    L.call("gc_bh_set_overlap", tree.handle, 0)
+    L.call("gc_bh_walk_forces_async", tree.handle, 0.3, 1.0, 1e-4)
+    f = np.zeros((n, 3))
+    L.call("gc_bh_get_forces", tree.handle, L.ptr(f, L.f64p))
+    np.testing.assert_array_equal(outs[1], f)
+    np.testing.assert_array_equal(outs[2], f)
+
+
+def test_plummer16m_config4_sampled_parity(nb):
+    """configs[3] system (Plummer 16M = 2^24, theta 0.7): the device tree is
+    bit-identical to the oracle's (float64 arrays), and on three walk-group
+    windows (4096 DFS buckets each, at 10 / 50 / 90 % of the tree) the lists
+    are bit-exact and forces + potentials are within 1e-5 of float64."""
+    from oracle import oracle as orc
+    from paper_2008_05712_b200 import _lib as L
+    from paper_2008_05712_b200 import generators as gen
+    n = 1 << 24
+    ps = gen.fp32_exact(gen.gen_plummer(n, 42))
+    tree = nb.build_bucket_tree(ps, 8)
+    ot = orc.build_bucket_tree(ps.positions, ps.masses, 8)
+    for k in ("half", "mass", "com", "first_child", "n_child"):
+        np.testing.assert_array_equal(getattr(tree, k), getattr(ot, k), err_msg=k)
+    np.testing.assert_array_equal(tree.bucket_ids, ot.buckets)
+    ngr = np.zeros(1, np.int64)
+    L.call("gc_bh_groups", tree.handle, L.ptr(ngr, L.i64p), None)
+    wfb = np.zeros(int(ngr[0]) + 1, np.int64)
+    L.call("gc_bh_groups", tree.handle, L.ptr(ngr, L.i64p), L.ptr(wfb, L.i64p))
+    nbk = len(ot.buckets)
+    ntot = 0
+    for frac in (0.1, 0.5, 0.9):
+        g0 = int(frac * ngr[0])
+        g1 = min(int(ngr[0]), g0 + 64)
+        b0, b1 = int(wfb[g0]), int(wfb[g1])
+        L.call("gc_bh_set_range", tree.handle, g0, g1)
+        L.call("gc_bh_walk", tree.handle, 0.7)
+        ptr = np.zeros(nbk + 1, np.int64)
+        ic = np.zeros(nbk, np.int64)
+        L.call("gc_bh_get_lists", tree.handle, L.ptr(ptr, L.i64p), None, None, L.ptr(ic, L.i64p))
+        ids = np.zeros(int(ptr[-1]), np.int64)
+        kind = np.zeros(int(ptr[-1]), np.int8)
+        L.call("gc_bh_get_lists", tree.handle, L.ptr(ptr, L.i64p), L.ptr(ids, L.i64p), L.ptr(kind, L.i8p),
+               L.ptr(ic, L.i64p))
+        ol = orc.build_interaction_lists(ot, 0.7, bucket_range=(b0, b1))
+        np.testing.assert_array_equal(ptr, ol.ptr)
+        np.testing.assert_array_equal(ids, ol.ids)
+        np.testing.assert_array_equal(kind, ol.kind)
+        np.testing.assert_array_equal(ic, ol.item_count)
+        f, pot = np.zeros((n, 3)), np.zeros(n)
+        L.call("gc_bh_forces_potential", tree.handle, 1.0, 1e-4, L.ptr(f, L.f64p), L.ptr(pot, L.f64p))
+        sel = np.concatenate([ot.particle_idx(b) for b in ot.buckets[b0:b1]])
+        ref = orc.eval_forces(ot, ol, ps.positions, ps.masses, 1.0, 1e-4, bucket_range=(b0, b1))
+        refp = orc.eval_potentials(ot, ol, ps.positions, ps.masses, 1.0, 1e-4, bucket_range=(b0, b1))
+        assert rel_err(f[sel], ref[sel]).max() <= FORCE_RTOL
+        assert (np.abs(pot[sel] - refp[sel]) / np.abs(refp[sel])).max() <= FORCE_RTOL
+        ntot += len(sel)
+    L.call("gc_bh_set_range", tree.handle, 0, int(ngr[0]))
+    assert ntot > 3 * 4096

@@ -60,3 +60,39 @@ def test_executor_evictions_and_timeouts(problem):
     sizes = [b.members for b in res.batches]
     assert max(sizes) <= 48 and min(sizes) < 48  # size-rule and timeout flushes both occurred
     assert ex.runtime.completed_count == nb
+
+
+@pytest.mark.parametrize("mode,cap,max_size", [("redundant", 1 << 30, None), ("reuse", 64 << 20, None),
+                                               ("reuse_sorted", 64 << 20, None), ("reuse", 1 << 19, 64),
+                                               ("reuse_sorted", 1 << 19, 64)])
+def test_config1_runtime_path_plans_match_oracle(mode, cap, max_size):
+    """configs[0] at the runtime path's own scale (Plummer 16K, theta 0.7,
+    one request per bucket, max_size from the real member kernel's
+    occupancy, or 64 with a 512 KiB heap to force LRU evictions): every
+    device plan -- transfers in order, address maps -- equals the oracle data
+    manager (oracle/dm.py, pinned to hr/memory.py); forces within 1e-5."""
+    from oracle import dm as odm
+    from oracle import oracle as orc
+    from paper_2008_05712_b200 import generators as gen
+    from paper_2008_05712_b200 import nbody
+    from paper_2008_05712_b200.executor import GpuForceExecutor
+    from paper_2008_05712_b200.memory import MemoryMode
+    ps = gen.fp32_exact(gen.gen_plummer(16384, 42))
+    tree = nbody.build_bucket_tree(ps, 8)
+    lists = nbody.build_interaction_lists(tree, 0.7, ps)
+    ex = GpuForceExecutor(tree, lists, MemoryMode.parse(mode), capacity_bytes=cap, slot_bytes=256,
+                          max_size=max_size)
+    ex.plan_log = []
+    res = ex.run()
+    assert len(ex.plan_log) == len(res.batches) >= 1
+    if max_size:
+        assert len(res.batches) >= 5730 // 64
+    ora = odm.OracleDM(cap, 256, mode)
+    for cls, members, now, transfers, addresses in ex.plan_log:
+        q = ora.plan(members, now=now)
+        assert transfers == q["to_transfer"]
+        assert addresses.tolist() == q["addresses"]
+        ora.release(members)
+    ot = orc.build_bucket_tree(ps.positions, ps.masses, 8)
+    ref = orc.eval_forces(ot, orc.build_interaction_lists(ot, 0.7), ps.positions, ps.masses)
+    assert rel_err(res.forces, ref).max() <= FORCE_RTOL

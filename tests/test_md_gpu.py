@@ -161,3 +161,18 @@ def test_lj_108k_config2_forces(md):
     e1 = 0.5 * (v ** 2).sum() + e2.sum()
     assert abs(e1 - e0) / abs(e0) < 2e-2
     assert np.abs(v.sum(axis=0)).max() < 1e-6 * len(v)
+
+
+def test_lj_8m_config5_forces(md):
+    """configs[4] system at full size: FCC 126^3 x 4 = 8,001,504 atoms, 84^3
+    cells -- every atom's force and energy against the float64 oracle (the
+    system bench.py times as configs[4] on one GPU)."""
+    from oracle import oracle as orc
+    from paper_2008_05712_b200.generators import gen_lj_fcc
+    s = jitter(gen_lj_fcc(126), seed=5)
+    assert s.positions.shape[0] == 8_001_504 and s.cells == 84
+    sysd = md.LJSystem(s)
+    f, e = sysd.forces()
+    fo, eo = orc.lj3d_compute_forces(s.positions, (84, 84, 84), s.cell_size, s.rc, s.eps, s.sigma, True)
+    assert rel_err(f, fo).max() <= FORCE_RTOL
+    np.testing.assert_allclose(e, eo, rtol=1e-10, atol=1e-12)

@@ -133,3 +133,40 @@ def test_aggregator_golden():
         assert [[t, list(ids)] for t, ids in got] == e["emissions"]
     for p in g["partitions"]:
         assert odm.partition(p["items"], p["share"], p["nearest"]) == p["cut"]
+
+
+def _direct_potential(pos, mass, g, eps):
+    """Independent numpy float64 direct sum -g m_i sum_{j: x_j != x_i} m_j / sqrt(r^2 + eps^2)."""
+    d = pos[None, :, :] - pos[:, None, :]
+    r2 = eps * eps + (d * d).sum(axis=2)
+    same = np.all(d == 0.0, axis=2)
+    w = np.where(same, 0.0, mass[None, :] / np.sqrt(r2))
+    return -g * mass * w.sum(axis=1)
+
+
+@pytest.mark.parametrize("name,dim", [("nbody2d_300", 2), ("nbody3d_2048", 3)])
+def test_potential_oracle_pinned_by_direct_sum(name, dim):
+    """The BH potential restatement (no reference counterpart) is pinned by a
+    known answer: at theta = 0 every list is opened particles only, so the
+    list potential equals the direct sum (up to summation order)."""
+    g = load(name)
+    pos, m = g["positions"], g["masses"]
+    t = orc.build_bucket_tree(pos, m, int(g["bucket_size"]), box=float(g["box"]))
+    ol = orc.build_interaction_lists(t, 0.0)
+    phi = orc.eval_potentials(t, ol, pos, m, 1.0, 1e-4)
+    ref = _direct_potential(pos, m, 1.0, 1e-4)
+    np.testing.assert_allclose(phi, ref, rtol=1e-12)
+    # theta > 0: monopole approximation, within the acceptance-10 tolerance scale
+    ol7 = orc.build_interaction_lists(t, 0.7)
+    phi7 = orc.eval_potentials(t, ol7, pos, m, 1.0, 1e-4)
+    assert np.median(np.abs(phi7 - ref) / np.abs(ref)) < 4e-3
+
+
+def test_potential_oracle_coincident_skip():
+    """Coincident sources are skipped exactly as in forces_from_points (kernels.py:78-84)."""
+    pos = np.array([[0.25, 0.25, 0.25], [0.25, 0.25, 0.25], [0.75, 0.25, 0.25]])
+    m = np.array([1.0, 2.0, 3.0])
+    t = orc.build_bucket_tree(pos, m, 8)
+    ol = orc.build_interaction_lists(t, 0.5)
+    phi = orc.eval_potentials(t, ol, pos, m, 1.0, 0.0)
+    np.testing.assert_allclose(phi, [-1.0 * 3.0 / 0.5, -2.0 * 3.0 / 0.5, -3.0 * 3.0 / 0.5], rtol=1e-15)
