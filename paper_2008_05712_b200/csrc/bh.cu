@@ -532,6 +532,25 @@ void ensure_union_complete(gc_bh *bh)
     while (walk_overflowed(bh)) launch_walk(bh, true, false);
 }
 
+// The default (fused) force kernel: sub-groups of FORCE_SUBT targets per warp
+// (force_sub_kernel), or FORCE_SUBT = 32: one warp per force group
+// (force_fused_kernel, the round-1 kernel; kept for A/B).
+using FusedFn = void (*)(int, const ForceGroup *, const UnionPool, const Staging, const float4 *, const float4 *,
+                         const float4 *, const int *, const int *, const WalkGroup *, float, float, double, int,
+                         double *, double *);
+constexpr int kFusedItems = FORCE_SUBT >= 32 ? 1 : 32 / FORCE_SUBT;  // warp work items per force group
+template <bool OVL>
+FusedFn fused_kernel(bool eps0, bool pot)
+{
+#if FORCE_SUBT >= 32
+    return eps0 ? (pot ? force_fused_kernel<true, true, OVL> : force_fused_kernel<true, false, OVL>)
+                : (pot ? force_fused_kernel<false, true, OVL> : force_fused_kernel<false, false, OVL>);
+#else
+    return eps0 ? (pot ? force_sub_kernel<true, true, OVL, FORCE_SUBT> : force_sub_kernel<true, false, OVL, FORCE_SUBT>)
+                : (pot ? force_sub_kernel<false, true, OVL, FORCE_SUBT> : force_sub_kernel<false, false, OVL, FORCE_SUBT>);
+#endif
+}
+
 void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
 {
     wait_orders(bh);
@@ -564,13 +583,12 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
             S.order = lpt ? bh->d_fg_lpt.p : bh->d_fg_order.p;
             S.next = bh->d_next.p;
             GC_CUDA(cudaEventRecord(bh->ev[4], s));
-            auto k = eps0 ? (pot ? force_fused_kernel<true, true> : force_fused_kernel<true, false>)
-                          : (pot ? force_fused_kernel<false, true> : force_fused_kernel<false, false>);
+            auto k = fused_kernel<false>(eps0, pot);
             if (nfg > 0) {
                 int per_sm = 0;
                 GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * WARPS_PER_BLOCK, 0));
                 const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(
-                    (int64_t)per_sm * ctx->prop.multiProcessorCount, grid_for(nfg, WARPS_PER_BLOCK)));
+                    (int64_t)per_sm * ctx->prop.multiProcessorCount, grid_for(nfg * kFusedItems, WARPS_PER_BLOCK)));
                 k<<<pgrid, 32 * WARPS_PER_BLOCK, 0, s>>>(nfg, bh->d_fg.p + f0, U, S, bh->d_parts.p, bh->d_rec_hi.p,
                                                          bh->d_rec_lo.p, bh->d_part_bucket.p, bh->d_porder.p,
                                                          bh->d_wg.p, bh->cgrid, eps2, g, bh->dim, bh->d_out.p,
@@ -700,11 +718,11 @@ void run_overlapped(gc_bh *bh, double theta, double g, double eps)
         S.next = bh->d_next.p;
         S.fq = bh->d_fq.p;
         const float eps2 = (float)(eps * eps);
-        auto k = bh_use_cube(eps2) ? force_fused_kernel<true, false, true> : force_fused_kernel<false, false, true>;
+        auto k = fused_kernel<true>(bh_use_cube(eps2), false);
         int per_sm = 0;
         GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * WARPS_PER_BLOCK, 0));
         const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(
-            (int64_t)per_sm * ctx->prop.multiProcessorCount, grid_for(nfg, WARPS_PER_BLOCK)));
+            (int64_t)per_sm * ctx->prop.multiProcessorCount, grid_for(nfg * kFusedItems, WARPS_PER_BLOCK)));
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(pgrid);
         cfg.blockDim = dim3(32 * WARPS_PER_BLOCK);
@@ -1074,6 +1092,25 @@ gc_status gc_bh_pair_stats(gc_bh *bh, int64_t out[2])
         GC_REQUIRE(bh && bh->have_union && out, GC_E_STATE, "no device walk has run");
         cudaStream_t s = bh->ctx->stream;
         const int nf = bh->n_fg;
+#if FORCE_SUBT < 32
+        if (bh->force_fused) {  // the sub-group kernel's own accounting
+            ensure_union_complete(bh);
+            DBuf<unsigned long long> acc;
+            acc.resize(2);
+            acc.zero(s);
+            const int ni = nf * kFusedItems;
+            if (ni > 0)
+                sub_stats_kernel<FORCE_SUBT><<<grid_for(ni, WARPS_PER_BLOCK), 32 * WARPS_PER_BLOCK, 0, s>>>(
+                    nf, bh->d_fg.p, pool_view(bh), bh->d_part_bucket.p, bh->d_wg.p, acc.p);
+            check_launch("sub_stats_kernel");
+            unsigned long long h[2];
+            acc.download(h, 2, s);
+            GC_CUDA(cudaStreamSynchronize(s));
+            out[0] = (int64_t)h[0];
+            out[1] = (int64_t)h[1];
+            return;
+        }
+#endif
         std::vector<int> rec(nf);
         std::vector<ForceGroup> fg(nf);
         ensure_grec(bh);

@@ -30,6 +30,9 @@
 namespace gc {
 
 constexpr int MD_TPB = 128;
+#ifndef MD_LJ_FAST
+#define MD_LJ_FAST 1
+#endif
 
 enum { LAW_SOFT = 0, LAW_LJ = 1 };
 
@@ -483,6 +486,194 @@ md_cell_kernel(const double4 *__restrict__ spos, const int *__restrict__ sidx, c
     }
 }
 
+// ---------------------------------------------------------------------------
+// 3-D Lennard-Jones cell kernel (the configs[1] / configs[4] throughput path).
+// One block per home cell, as md_cell_kernel, rebuilt for instruction count:
+//   staging: half a warp per neighbour cell copies its atoms (coalesced) into
+//            shared memory twice -- float64 raw positions + global id for the
+//            pair math (nbd) and float32 image-shifted offsets from the home
+//            corner in PAIR layout (x0 x1 y0 y1 | z0 z1) for the filter;
+//   filter:  thread = (home atom, part); HOME = 8/16/32 home atoms (next power
+//            of two of the cell's population) x PARTS = 128 / HOME parts; two
+//            candidates per step with FADD2/FFMA2; a survivor of the widened
+//            float32 test sets one bit of a per-thread mask (32 steps per
+//            chunk), no list traffic;
+//   pairs:   the same thread walks the set bits and evaluates each survivor in
+//            float64 from shared memory in its own orientation; pairs whose
+//            float64 r^2 lies within 1e-12 of the cutoff (or below 1e-6) take
+//            md_pair_exact -- the reference's canonical orientation, cutoff
+//            decision bit for bit.  Parts are summed by shuffles in fixed
+//            order, so results are deterministic (slab runs bit-identical).
+// ---------------------------------------------------------------------------
+constexpr int MDL_THREADS = 128;
+constexpr int MDL_NB = 512;  // staged neighbour slots (27 cells)
+constexpr int MDL_PADP = 16;  // far-away pad pairs after the last staged pair (>= max parts)
+__global__ void __launch_bounds__(MDL_THREADS, 7)
+md_lj3_kernel(const double4 *__restrict__ spos, const int *__restrict__ sidx, const int *__restrict__ cell_start,
+              const MDParams P, float band, double4 *__restrict__ out)
+{
+    __shared__ double4 nbd[MDL_NB];  // raw float64 position, w = global id bits
+    __shared__ float4 nba[MDL_NB / 2 + MDL_PADP];  // pairs: x0 x1 y0 y1 (shifted, relative to the home corner)
+    __shared__ float2 nbz[MDL_NB / 2 + MDL_PADP];  // pairs: z0 z1
+    __shared__ unsigned char nbc[MDL_NB];  // neighbour-cell offset code
+    __shared__ int pre[28], qs[27], qst[27];
+    __shared__ double4 shtab[27];
+    const int c = blockIdx.x + (P.slab ? P.ny * P.nz : 0);  // slabs: owned cells only
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int cz = c % P.nz, cy = (c / P.nz) % P.ny, cx = c / (P.nz * P.ny);
+    const double orx = cx * P.cell, ory = cy * P.cell, orz = cz * P.cell;
+    if (tid < 27) {
+        int ox, oy, oz;
+        md_offset_of(tid, ox, oy, oz);
+        int qx = cx + ox, qy = cy + oy, qz = cz + oz;
+        bool ok = true;
+        if (qx < 0 || qx >= P.nx) { ok = P.periodic && !P.slab; qx = (qx + P.nx) % P.nx; }
+        if (qy < 0 || qy >= P.ny) { ok = ok && P.periodic; qy = (qy + P.ny) % P.ny; }
+        if (qz < 0 || qz >= P.nz) { ok = ok && P.periodic; qz = (qz + P.nz) % P.nz; }
+        const int q = (qx * P.ny + qy) * P.nz + qz;
+        qs[tid] = ok ? q : -1;
+        qst[tid] = ok ? cell_start[q] : 0;
+        pre[tid + 1] = ok ? cell_start[q + 1] - cell_start[q] : 0;
+        const int rx = cx + ox, ry = cy + oy, rz = cz + oz;
+        shtab[tid] = make_double4(md_xshift(rx, P), ry < 0 ? -P.by : (ry >= P.ny ? P.by : 0.0),
+                                  rz < 0 ? -P.bz : (rz >= P.nz ? P.bz : 0.0),
+                                  tid == 13 ? 2.0 : (md_forward(ox, oy, oz) ? 1.0 : 0.0));
+    }
+    __syncthreads();
+    if (warp == 0) {  // inclusive scan of the populations
+        int v = lane < 27 ? pre[lane + 1] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        if (lane < 27) pre[lane + 1] = v;
+        if (lane == 0) pre[0] = 0;
+    }
+    __syncthreads();
+    const int nnb = pre[27];
+    const int h0 = cell_start[c], nh = cell_start[c + 1] - h0;
+    const int self0 = pre[13];
+    if (nnb > MDL_NB) {  // staging overflow (pathological density): exact scan from global memory
+        for (int i = tid; i < nh; i += MDL_THREADS) {
+            const double4 a = spos[h0 + i];
+            const long long ia = __double_as_longlong(a.w);
+            double fx = 0.0, fy = 0.0, fz = 0.0, en = 0.0;
+            for (int k = 0; k < 27; ++k) {
+                if (qs[k] < 0) continue;
+                for (int j = cell_start[qs[k]]; j < cell_start[qs[k] + 1]; ++j)
+                    if (j != h0 + i) md_pair_exact<LAW_LJ, 3>(a, ia, spos[j], shtab[k], P, fx, fy, fz, en);
+            }
+            out[sidx[h0 + i]] = make_double4(fx, fy, fz, en);
+        }
+        return;
+    }
+    // staging: half-warp h of warp w copies neighbour cells 2 w + h, 2 w + h + 8, ...
+    float *fa = reinterpret_cast<float *>(nba);
+    float *fzp = reinterpret_cast<float *>(nbz);
+    const int hl = lane & 15;
+    for (int k = 2 * warp + (lane >> 4); k < 27; k += 2 * (MDL_THREADS / 32)) {
+        const int n = pre[k + 1] - pre[k], s0 = pre[k];
+        const double4 sh = shtab[k];
+        const double ox = orx - sh.x, oy = ory - sh.y, oz = orz - sh.z;  // filter offsets only
+        for (int j = hl; j < n; j += 16) {
+            const double4 b = spos[qst[k] + j];
+            const int s = s0 + j;
+            nbd[s] = b;
+            nbc[s] = (unsigned char)k;
+            const int o = (s >> 1) * 4 + (s & 1);
+            fa[o] = (float)(b.x - ox);
+            fa[o + 2] = (float)(b.y - oy);
+            fzp[(s >> 1) * 2 + (s & 1)] = (float)(b.z - oz);
+        }
+    }
+    // far-away pads: the odd last slot and MDL_PADP whole pairs (filter reads past npair)
+    for (int s = nnb + tid; s < 2 * ((nnb + 1) / 2 + MDL_PADP); s += MDL_THREADS) {
+        const int o = (s >> 1) * 4 + (s & 1);
+        fa[o] = 1e30f;
+        fa[o + 2] = 1e30f;
+        fzp[(s >> 1) * 2 + (s & 1)] = 1e30f;
+    }
+    __syncthreads();
+    const int npair = (nnb + 1) >> 1;
+    const double lo = P.c2 * (1.0 - 1e-12), hi = P.c2 * (1.0 + 1e-12);
+    const double e24 = 24.0 * P.eps, e2 = 2.0 * P.eps;
+    for (int hb = 0; hb < nh; hb += 32) {
+        const int nhc = min(32, nh - hb);
+        const int lg = nhc <= 8 ? 3 : (nhc <= 16 ? 4 : 5);  // HOME = 2^lg home atoms x PARTS parts
+        const int parts = MDL_THREADS >> lg;
+        const int hi_ = tid >> (7 - lg), part = tid & (parts - 1);
+        const bool act = hi_ < nhc;
+        const int si = self0 + hb + (act ? hi_ : 0);
+        const float xi = fa[(si >> 1) * 4 + (si & 1)], yi = fa[(si >> 1) * 4 + (si & 1) + 2],
+                    zi = fzp[(si >> 1) * 2 + (si & 1)];
+        const float2 nx2 = make_float2(-xi, -xi), ny2 = make_float2(-yi, -yi), nz2 = make_float2(-zi, -zi);
+        const double4 a = nbd[si];
+        const long long ia = __double_as_longlong(a.w);
+        double fx = 0.0, fy = 0.0, fzz = 0.0, en = 0.0;
+        const int nstep = (npair + parts - 1) / parts;  // block-uniform
+        for (int c0 = 0; c0 < nstep; c0 += 32) {
+            // filter 32 steps: bit k of w0 / w1 = slot 2 pr / 2 pr + 1 of step c0 + k survives
+            unsigned w0 = 0u, w1 = 0u;
+            const int ks = min(32, nstep - c0);
+            int pr = part + parts * c0;
+#pragma unroll 4
+            for (int k = 0; k < ks; ++k, pr += parts) {
+                const float4 A = nba[pr];
+                const float2 Z = nbz[pr];
+                const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nx2);
+                const float2 dy = __fadd2_rn(make_float2(A.z, A.w), ny2);
+                const float2 dz = __fadd2_rn(Z, nz2);
+                float2 r2 = __fmul2_rn(dz, dz);
+                r2 = __ffma2_rn(dy, dy, r2);
+                r2 = __ffma2_rn(dx, dx, r2);
+                w0 |= (r2.x < band ? 1u : 0u) << k;
+                w1 |= (r2.y < band ? 1u : 0u) << k;
+            }
+            if (!act) w0 = w1 = 0u;
+            // survivors in float64 from shared memory
+            while (w0 | w1) {
+                int sl;
+                if (w0) {
+                    const int k = __ffs(w0) - 1;
+                    w0 &= w0 - 1u;
+                    sl = 2 * (part + parts * (c0 + k));
+                } else {
+                    const int k = __ffs(w1) - 1;
+                    w1 &= w1 - 1u;
+                    sl = 2 * (part + parts * (c0 + k)) + 1;
+                }
+                const double4 b = nbd[sl];
+                const double4 sh = shtab[nbc[sl]];
+                const double d0 = a.x - (b.x + sh.x), d1 = a.y - (b.y + sh.y), d2 = a.z - (b.z + sh.z);
+                const double r2 = fma(d2, d2, fma(d1, d1, d0 * d0));
+                if ((r2 > lo && r2 < hi) || r2 < 1e-6) {  // at the cutoff / coincident: the reference's own test
+                    md_pair_exact<LAW_LJ, 3>(a, ia, b, sh, P, fx, fy, fzz, en);
+                } else if (r2 < P.c2) {
+                    double inv = (double)__frcp_rn((float)r2);
+                    inv = fma(inv, fma(-r2, inv, 1.0), inv);
+                    inv = fma(inv, fma(-r2, inv, 1.0), inv);
+                    const double s2 = P.sig2 * inv;
+                    const double s6 = s2 * s2 * s2;
+                    const double s12 = s6 * s6;
+                    const double mag = e24 * (2.0 * s12 - s6) * inv;
+                    en = fma(e2, s12 - s6, en);
+                    fx = fma(d0, mag, fx);
+                    fy = fma(d1, mag, fy);
+                    fzz = fma(d2, mag, fzz);
+                }
+            }
+        }
+        for (int o = 1; o < parts; o <<= 1) {
+            fx += __shfl_xor_sync(0xffffffffu, fx, o);
+            fy += __shfl_xor_sync(0xffffffffu, fy, o);
+            fzz += __shfl_xor_sync(0xffffffffu, fzz, o);
+            en += __shfl_xor_sync(0xffffffffu, en, o);
+        }
+        if (act && part == 0) out[sidx[h0 + hb + hi_]] = make_double4(fx, fy, fzz, en);
+    }
+}
+
 // cell of every atom (unfused path)
 __global__ void md_assign_kernel(int n, const double4 *__restrict__ pos, const MDParams P, int use_npy,
                                  int *__restrict__ cell_of, int *__restrict__ count)
@@ -673,6 +864,7 @@ struct gc_md {
     int n = 0, ncell = 0;
     int use_npy = 0;  // reference 2-D patches use numpy floor_divide
     bool cell_path = true;  // block-per-cell kernel (false: thread-per-atom kernel)
+    bool lj_fast = MD_LJ_FAST != 0;  // 3-D LJ: md_lj3_kernel (else md_cell_kernel)
     DBuf<double4> pos, vel, spos, force;  // pos/vel/gid/cell_of: owned atoms [0, n_owned), then ghosts
     DBuf<int> cell_of, scell, sidx, count, cell_start, perm;
     DBuf<long long> gid;  // global atom id (cell order, self-pair orientation)
@@ -740,6 +932,12 @@ void md_cell_launch(gc_md *md, bool integ, double dt)
     cudaStream_t s = md->ctx->stream;
     const int blocks = md->P.slab ? (md->P.nx - 2) * md->P.ny * md->P.nz : md->ncell;  // home = owned cells
     if (blocks <= 0) return;
+    if (LAW == LAW_LJ && DIM == 3 && !integ && md->lj_fast) {
+        md_lj3_kernel<<<blocks, MDL_THREADS, 0, s>>>(md->spos.p, md->sidx.p, md->cell_start.p, md->P, band,
+                                                     md->force.p);
+        check_launch("md_lj3_kernel");
+        return;
+    }
     if (integ)
         md_cell_kernel<LAW, DIM, true><<<blocks, MDC_THREADS, 0, s>>>(md->spos.p, md->sidx.p, md->cell_start.p, md->P,
                                                                        band, inner, md->force.p, I);

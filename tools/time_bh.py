@@ -27,5 +27,7 @@ for i in range(12):
         r.append(tm[2])
 inter = nbody.interactions(tree)
 fm = statistics.median(f)
+st = np.zeros(2, np.int64)
+L.call("gc_bh_pair_stats", tree.handle, L.ptr(st, L.i64p))
 print(f"{L.LIB_PATH.split('/')[-1]} {'staged' if staged else 'fused'}: walk {statistics.median(w):.3f} ms  reorg {statistics.median(r):.3f} ms  force {fm:.3f} ms  "
-      f"{20 * inter / fm / 1e9:.2f} TFLOP/s ({inter} interactions)")
+      f"{20 * inter / fm / 1e9:.2f} TFLOP/s ({inter} interactions) issued {st[0]} eff {inter / st[0]:.3f}")
