@@ -1109,7 +1109,7 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
 // the phases' fp64 sums are added by shuffles at the end.
 // ---------------------------------------------------------------------------
 #ifndef FORCE_SUBT
-#define FORCE_SUBT 8
+#define FORCE_SUBT 32  // 32: one warp per force group (force_fused_kernel); 4 / 8 / 16: force_sub_kernel (measured slower, A/B only)
 #endif
 template <int SUBT>
 struct SubCfg {
