@@ -1093,7 +1093,7 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
 }
 
 // ---------------------------------------------------------------------------
-// SUB-GROUP force kernel (the default step): the force group's targets are
+// SUB-GROUP force kernel (A/B build knob, -DFORCE_SUBT=8): the force group's targets are
 // split into sub-groups of SUBT consecutive targets and one warp evaluates
 // one sub-group, lane = (target lane % SUBT, record phase lane / SUBT).  The
 // warp reorganises only the union entries some of ITS targets' buckets use
@@ -1106,7 +1106,11 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
 // a 32-target run, so far fewer evaluated pairs are wasted (mask efficiency
 // 0.51 -> 0.73 at SUBT = 8 on configs[2], tools/mask_stats2.py).  fp32
 // partial sums of 8 terms per half are flushed to fp64 every UNIT records;
-// the phases' fp64 sums are added by shuffles at the end.
+// the phases' fp64 sums are added by shuffles at the end.  Measured on the
+// B200 (1M clustered): 1.48 ms at SUBT = 8, 2.24 at 4, 1.21 at 16 vs 0.88 ms
+// for the 32-target kernel -- every sub-group re-gathers its records (2.8x
+// the L2 gathers at SUBT = 8) and the gather latency, not the FP32 issue,
+// bounds the kernel; so the default stays FORCE_SUBT = 32.
 // ---------------------------------------------------------------------------
 #ifndef FORCE_SUBT
 #define FORCE_SUBT 32  // 32: one warp per force group (force_fused_kernel); 4 / 8 / 16: force_sub_kernel (measured slower, A/B only)
