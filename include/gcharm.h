@@ -119,6 +119,32 @@ gc_status gc_bh_pair_stats(gc_bh *bh, int64_t out[2]);
  * the whole step as the walk.  The force kernel is a programmatic dependent launch that starts
  * when every walk block has a warp out of work. */
 gc_status gc_bh_set_overlap(gc_bh *bh, int32_t on);
+
+/* --- Distributed Barnes-Hut (paper_2008_05712_b200/bh_dist.py) ---
+ * The reference has no distributed path: it runs one process
+ * (hr/workloads/nbody.py:78-250).  These entry points let each rank build the
+ * part of the GLOBAL tree it owns and walk its own buckets over an assembled
+ * locally-essential tree, with lists bit-identical to the one-GPU tree.
+ *
+ * Octant keys of the device build (nbody.py:97-108 descent, 3 bits per level,
+ * levels 0-20 in k1, 21-41 in k2; digits of levels with half < 1e-9 are 0). */
+gc_status gc_bh_keys(gc_ctx *ctx, int64_t n, int32_t dim, const double *pos, double box, uint64_t *k1,
+                     uint64_t *k2);
+/* Cubes (level, key prefix of levels < level as (k1, k2)) that the next device
+ * build splits whatever their local particle count -- they straddle ranks and
+ * hold more than bucket_size particles globally.  n = 0 clears the list. */
+gc_status gc_bh_set_forced_splits(gc_bh *bh, int64_t n, const int32_t *level, const uint64_t *prefix /* 2n */);
+/* Upload an assembled tree in the reference's layout (level-order node ids;
+ * first_child = -1 for buckets; buckets in depth-first order; order = particle
+ * ids of the buckets' ranges into pos / pmass).  Walk groups never straddle
+ * the DFS bucket indices `cuts` (a rank's own buckets form whole groups, then
+ * gc_bh_set_range selects them). */
+gc_status gc_bh_set_tree(gc_bh *bh, int64_t n_nodes, int32_t dim, double box, int64_t bucket_size,
+                         const double *center, const double *half, const double *mass, const double *com,
+                         const int64_t *first_child, const int32_t *n_child, const int64_t *pstart,
+                         const int64_t *pcount, int64_t n_buckets, const int64_t *buckets, int64_t n_parts,
+                         const int64_t *order, const double *pos, const double *pmass, int64_t n_cuts,
+                         const int64_t *cuts);
 /* one step's walk + forces, asynchronous (= gc_bh_walk + gc_bh_forces_async) */
 gc_status gc_bh_walk_forces_async(gc_bh *bh, double theta, double g, double eps);
 gc_status gc_bh_set_build_mode(gc_bh *bh, int32_t device);

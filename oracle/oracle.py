@@ -51,6 +51,8 @@ def lib():
         L = C.CDLL(_SO)
         L.orc_build_tree.argtypes = [C.c_int64, C.c_int, f64p, f64p, C.c_double, C.c_int64, C.POINTER(_Tree)]
         L.orc_free_tree.argtypes = [C.POINTER(_Tree)]
+        L.orc_build_tree_forced.argtypes = [C.c_int64, C.c_int, f64p, f64p, C.c_double, C.c_int64, C.c_int64,
+                                            i32p, C.POINTER(C.c_uint64), C.POINTER(_Tree)]
         L.orc_build_lists.argtypes = [C.POINTER(_Tree), C.c_int, C.c_double, i64p,
                                       C.POINTER(i64p), C.POINTER(i8p), i64p, C.c_int]
         L.orc_build_lists_range.argtypes = [C.POINTER(_Tree), C.c_int, C.c_double, C.c_int64, C.c_int64, i64p,
@@ -156,13 +158,51 @@ class OracleLists:
         return self.ids[s][self.kind[s] == 1]
 
 
-def build_bucket_tree(positions, masses, bucket_size, box=1.0) -> OracleTree:
+def octant_keys(positions, box=1.0):
+    """Restatement of the device build's octant keys (bh_build.cu bb_keys =
+    the descent of hr/workloads/nbody.py:97-108): level L digit
+    q = sum_k (x_k >= c_k) << k at bits 3 (20 - L) of k1 (L < 21) or
+    3 (41 - L) of k2; levels with half < 1e-9 contribute nothing."""
+    pos = _f64(positions)
+    n, dim = pos.shape
+    nlev, h = 0, box / 2.0
+    while h >= 1e-9 and nlev <= 42:
+        nlev += 1
+        h /= 2.0
+    c = np.full((n, dim), box * 0.5)
+    h = box * 0.5
+    k1 = np.zeros(n, np.uint64)
+    k2 = np.zeros(n, np.uint64)
+    for L in range(nlev):
+        q = np.zeros(n, np.uint64)
+        for k in range(dim):
+            q |= (pos[:, k] >= c[:, k]).astype(np.uint64) << np.uint64(k)
+        if L < 21:
+            k1 |= q << np.uint64(3 * (20 - L))
+        else:
+            k2 |= q << np.uint64(3 * (41 - L))
+        ch = h * 0.5
+        for k in range(dim):
+            c[:, k] = c[:, k] + np.where((q >> np.uint64(k)) & np.uint64(1), ch, -ch)
+        h = ch
+    return k1, k2
+
+
+def build_bucket_tree(positions, masses, bucket_size, box=1.0, forced=None) -> OracleTree:
+    """forced=(levels int32 (m,), prefixes uint64 (m, 2)): cubes split whatever
+    their count (the distributed build's straddling cubes)."""
     L = lib()
     pos = _f64(positions)
     n, dim = pos.shape
     m = _f64(masses)
     t = _Tree()
-    rc = L.orc_build_tree(n, dim, _p(pos, f64p), _p(m, f64p), float(box), int(bucket_size), C.byref(t))
+    if forced is not None and len(forced[0]):
+        fl = np.ascontiguousarray(forced[0], np.int32)
+        fp = np.ascontiguousarray(forced[1], np.uint64).reshape(-1)
+        rc = L.orc_build_tree_forced(n, dim, _p(pos, f64p), _p(m, f64p), float(box), int(bucket_size), len(fl),
+                                     _p(fl, i32p), fp.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(t))
+    else:
+        rc = L.orc_build_tree(n, dim, _p(pos, f64p), _p(m, f64p), float(box), int(bucket_size), C.byref(t))
     if rc != 0:
         raise ValueError(f"orc_build_tree failed ({rc})")
     nn = t.n_nodes

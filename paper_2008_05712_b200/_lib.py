@@ -22,6 +22,7 @@ i64p = C.POINTER(C.c_int64)
 i32p = C.POINTER(C.c_int32)
 i8p = C.POINTER(C.c_int8)
 f64p = C.POINTER(C.c_double)
+u64p = C.POINTER(C.c_uint64)
 vp = C.c_void_p
 
 # name -> (argtypes); every function returns gc_status (int32) unless listed in _RESTYPE
@@ -59,6 +60,10 @@ SIGNATURES = {
     "gc_bh_set_build_mode": [vp, C.c_int32],
     "gc_bh_set_force_mode": [vp, C.c_int32],
     "gc_bh_set_overlap": [vp, C.c_int32],
+    "gc_bh_keys": [vp, C.c_int64, C.c_int32, f64p, C.c_double, u64p, u64p],
+    "gc_bh_set_forced_splits": [vp, C.c_int64, i32p, u64p],
+    "gc_bh_set_tree": [vp, C.c_int64, C.c_int32, C.c_double, C.c_int64, f64p, f64p, f64p, f64p, i64p, i32p, i64p,
+                       i64p, C.c_int64, i64p, C.c_int64, i64p, f64p, f64p, C.c_int64, i64p],
     "gc_bh_walk_forces_async": [vp, C.c_double, C.c_double, C.c_double],
     "gc_bh_pair_stats": [vp, i64p],
     "gc_debug_walk_prof": [i64p, C.c_int32],

@@ -80,27 +80,34 @@ void upload_tree(gc_bh *bh)
     }
     // walk groups: WG_BUCKETS consecutive buckets; force groups: <= 32 targets
     // of consecutive buckets inside one walk group
+    // (an assembled distributed tree may cut them at given buckets: its own
+    // buckets then form whole walk groups, gc_bh_set_tree)
     bh->h_wg.clear();
     std::vector<ForceGroup> h_fg;
-    for (int64_t b0 = 0; b0 < nb; b0 += WG_BUCKETS) {
+    size_t cut = 0;
+    for (int64_t b0 = 0; b0 < nb;) {
+        while (cut < bh->wg_cuts.size() && bh->wg_cuts[cut] <= b0) ++cut;
+        const int64_t lim = cut < bh->wg_cuts.size() ? bh->wg_cuts[cut] : nb;
         WalkGroup wg;
         wg.bfirst = (int)b0;
-        wg.nbucket = (int)std::min<int64_t>(WG_BUCKETS, nb - b0);
+        wg.nbucket = (int)std::min<int64_t>(WG_BUCKETS, lim - b0);
+        b0 += wg.nbucket;
         wg.fg_first = (int)h_fg.size();
         const int wi = (int)bh->h_wg.size();
-        for (int64_t b = b0; b < b0 + wg.nbucket;) {
+        const int64_t gb0 = wg.bfirst, gb1 = gb0 + wg.nbucket;
+        for (int64_t b = gb0; b < gb1;) {
             ForceGroup fg;
             fg.pstart = (int)t.pstart[t.buckets[b]];
             fg.wg = wi;
-            fg.boff = (int)(b - b0);
+            fg.boff = (int)(b - gb0);
             int tg = 0;
-            while (b < b0 + wg.nbucket && tg + t.pcount[t.buckets[b]] <= 32) {
+            while (b < gb1 && tg + t.pcount[t.buckets[b]] <= 32) {
                 tg += (int)t.pcount[t.buckets[b]];
                 ++b;
             }
             GC_REQUIRE(tg > 0, GC_E_VALUE, "bucket with more than 32 particles (coincident points) on the group path");
             fg.ntarget = tg;
-            fg.nb = (int)(b - b0) - fg.boff;
+            fg.nb = (int)(b - gb0) - fg.boff;
             h_fg.push_back(fg);
         }
         wg.nfg = (int)h_fg.size() - wg.fg_first;
@@ -827,6 +834,100 @@ gc_status gc_debug_walk_prof(int64_t out[6], int32_t reset)
         (void)reset;
         for (int k = 0; k < 6; ++k) out[k] = 0;
 #endif
+    });
+}
+
+// --- distributed BH (bh_dist.py) -------------------------------------------
+
+gc_status gc_bh_set_forced_splits(gc_bh *bh, int64_t n, const int32_t *level, const uint64_t *prefix)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && (n == 0 || (level && prefix)), GC_E_VALUE, "null argument");
+        std::vector<std::pair<int, std::pair<uint64_t, uint64_t>>> v((size_t)n);
+        for (int64_t i = 0; i < n; ++i) {
+            GC_REQUIRE(level[i] >= 0 && level[i] <= 42, GC_E_VALUE, "forced level out of range");
+            v[i] = {level[i], {prefix[2 * i] & 0x7fffffffffffffffull, prefix[2 * i + 1] & 0x7fffffffffffffffull}};
+        }
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+        std::vector<int> lv(v.size());
+        std::vector<ulonglong2> kv(v.size());
+        for (size_t i = 0; i < v.size(); ++i) {
+            lv[i] = v[i].first;
+            kv[i] = make_ulonglong2(v[i].second.first, v[i].second.second);
+        }
+        bh->n_forced = (int)v.size();
+        bh->d_forced_lvl.upload(lv.data(), std::max<size_t>(1, lv.size()), bh->ctx->stream);
+        bh->d_forced_key.upload(kv.data(), std::max<size_t>(1, kv.size()), bh->ctx->stream);
+        GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
+    });
+}
+
+gc_status gc_bh_keys(gc_ctx *ctx, int64_t n, int32_t dim, const double *pos, double box, uint64_t *k1, uint64_t *k2)
+{
+    return guard([&] {
+        GC_REQUIRE(ctx && pos && k1 && k2, GC_E_VALUE, "null argument");
+        GC_REQUIRE(dim >= 1 && dim <= 3 && n >= 0, GC_E_VALUE, "bad shape");
+        device_keys(ctx, n, dim, pos, box, k1, k2);
+    });
+}
+
+gc_status gc_bh_set_tree(gc_bh *bh, int64_t n_nodes, int32_t dim, double box, int64_t bucket_size,
+                         const double *center, const double *half, const double *mass, const double *com,
+                         const int64_t *first_child, const int32_t *n_child, const int64_t *pstart,
+                         const int64_t *pcount, int64_t n_buckets, const int64_t *buckets, int64_t n_parts,
+                         const int64_t *order, const double *pos, const double *pmass, int64_t n_cuts,
+                         const int64_t *cuts)
+{
+    return guard([&] {
+        GC_REQUIRE(bh && center && half && mass && com && first_child && n_child && pstart && pcount && buckets &&
+                       order && pos && pmass,
+                   GC_E_VALUE, "null argument");
+        GC_REQUIRE(n_nodes >= 1 && n_buckets >= 1 && n_parts >= 1 && dim >= 1 && dim <= 3, GC_E_VALUE, "bad sizes");
+        wait_orders(bh);
+        HostTree &t = bh->tree;
+        t.n = n_parts;
+        t.dim = dim;
+        t.box = box;
+        t.bucket_size = bucket_size;
+        t.center.assign(3 * (size_t)n_nodes, 0.0);
+        t.com.assign(3 * (size_t)n_nodes, 0.0);
+        for (int64_t i = 0; i < n_nodes; ++i)
+            for (int k = 0; k < dim; ++k) {
+                t.center[3 * i + k] = center[i * dim + k];
+                t.com[3 * i + k] = com[i * dim + k];
+            }
+        t.half.assign(half, half + n_nodes);
+        t.node_mass.assign(mass, mass + n_nodes);
+        t.first_child.assign(first_child, first_child + n_nodes);
+        t.n_child.assign(n_child, n_child + n_nodes);
+        t.pstart.assign(pstart, pstart + n_nodes);
+        t.pcount.assign(pcount, pcount + n_nodes);
+        t.buckets.assign(buckets, buckets + n_buckets);
+        t.order.assign(order, order + n_parts);
+        bh->wg_cuts.assign(cuts, cuts + n_cuts);
+        std::sort(bh->wg_cuts.begin(), bh->wg_cuts.end());
+        bh->host_tree_valid = true;
+        bh->n = n_parts;
+        bh->dim = dim;
+        bh->box = box;
+        bh->bucket_size = bucket_size;
+        bh->n_nodes = n_nodes;
+        bh->n_buckets = n_buckets;
+        upload_tree(bh);
+        upload_particles(bh, pos, pmass);
+        bh->ws.pos.upload(pos, (size_t)n_parts * dim, bh->ctx->stream);
+        bh->ws.mass.upload(pmass, (size_t)n_parts, bh->ctx->stream);
+        bh->wg_cuts.clear();
+        bh->have_tree = true;
+        bh->have_union = bh->have_member_lists = false;
+        bh->ew_mom_valid = false;
+        bh->params_valid = false;
+        bh->stats_valid = false;
+        bh->stats_dirty = false;
+        bh->orders_fresh = false;
+        bh->rg0 = 0;
+        bh->rg1 = -1;
     });
 }
 

@@ -153,7 +153,40 @@ struct LevelArgs {
     int *leaf_key, *leaf_id, *nleaf;
     int *lvl_first, *nlevels, *overflow;
     int *big, *nbig;  // this level's wide splitting nodes (warp-cooperative cuts)
+    // cubes split regardless of their count (distributed build: they straddle
+    // ranks), sorted by (level, prefix); prefix = key bits of levels < L
+    const int *forced_lvl;
+    const ulonglong2 *forced_key;
+    int n_forced;
 };
+
+__device__ __forceinline__ ulonglong2 key_prefix(unsigned long long k1, unsigned long long k2, int L)
+{
+    // digits of levels 0 .. L - 1 (level l at bits 3 (20 - l) of k1, 3 (41 - l) of k2)
+    const unsigned long long m1 = L >= 21 ? ~0ull : (L == 0 ? 0ull : ~0ull << (3 * (21 - L)));
+    const unsigned long long m2 = L <= 21 ? 0ull : (L >= 42 ? ~0ull : ~0ull << (3 * (42 - L)));
+    return make_ulonglong2(k1 & m1 & 0x7fffffffffffffffull, k2 & m2 & 0x7fffffffffffffffull);
+}
+
+// does the node of level L starting at sorted position st split?  (nbody.py:94,
+// plus the forced cubes of a distributed build)
+__device__ __forceinline__ bool node_splits(const LevelArgs &A, int ct, double half, int L, int st)
+{
+    if (!(half >= 1e-9)) return false;
+    if (ct > A.bucket) return true;
+    if (A.n_forced == 0 || ct == 0) return false;
+    const ulonglong2 k = key_prefix(A.k1[st], A.k2[st], L);
+    int lo = 0, hi = A.n_forced;  // first entry >= (L, k)
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const int ml = A.forced_lvl[mid];
+        const ulonglong2 mk = A.forced_key[mid];
+        const bool less = ml < L || (ml == L && (mk.x < k.x || (mk.x == k.x && mk.y < k.y)));
+        if (less) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo < A.n_forced && A.forced_lvl[lo] == L && A.forced_key[lo].x == k.x && A.forced_key[lo].y == k.y;
+}
 
 __device__ __forceinline__ int block_sum(int v, int *red)
 {
@@ -185,7 +218,7 @@ __global__ void __launch_bounds__(BB_TPB) bb_levels_coop(LevelArgs A)
         // 1: store this level, count the children of splitting nodes
         for (int p = tid; p < m; p += T) {
             const int st = A.start[cur][p], ct = A.count[cur][p];
-            const bool sp = ct > A.bucket && half >= 1e-9;  // nbody.py:94
+            const bool sp = node_splits(A, ct, half, L, st);  // nbody.py:94 (+ forced cubes)
             const int id = id0 + p;
             A.ncenter[id] = A.center[cur][p];
             A.pstart[id] = st;
@@ -282,7 +315,7 @@ __global__ void __launch_bounds__(BB_TPB) bb_levels_coop(LevelArgs A)
         const int nxt = cur ^ 1;
         for (int p = c0 + (int)threadIdx.x; p < c1; p += blockDim.x) {
             const int ct = A.count[cur][p];
-            if (!(ct > A.bucket && half >= 1e-9)) continue;
+            if (!node_splits(A, ct, half, L, A.start[cur][p])) continue;
             const double4 pc = A.center[cur][p];
             const double ch = pc.w * 0.5;  // == pc.w / 2 exactly
             int c = A.cbase[p];
@@ -544,6 +577,28 @@ void cubc(gc_ctx *ctx, F &&f)
     GC_CUDA(f(ctx->scratch.p, bytes));
 }
 
+void device_keys(gc_ctx *ctx, int64_t n64, int dim, const double *pos_h, double box, uint64_t *k1_h, uint64_t *k2_h)
+{
+    cudaStream_t s = ctx->stream;
+    const int n = (int)n64;
+    int nlev = 0;
+    for (double h = box / 2.0; h >= 1e-9 && nlev <= MAX_KEY_LEVELS; h /= 2.0) ++nlev;
+    GC_REQUIRE(nlev <= MAX_KEY_LEVELS, GC_E_VALUE, "box too large for the device build keys");
+    if (n == 0) return;
+    DBuf<double> pos;
+    DBuf<unsigned long long> k1, k2;
+    DBuf<int> idx;
+    pos.upload(pos_h, (size_t)n * dim, s);
+    k1.resize(n);
+    k2.resize(n);
+    idx.resize(n);
+    bb_keys<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, dim, pos.p, box, nlev, k1.p, k2.p, idx.p);
+    check_launch("bb_keys");
+    GC_CUDA(cudaMemcpyAsync(k1_h, k1.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, s));
+    GC_CUDA(cudaMemcpyAsync(k2_h, k2.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, s));
+    GC_CUDA(cudaStreamSynchronize(s));
+}
+
 void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int64_t n64, int dim, double box,
                        int64_t bucket)
 {
@@ -596,8 +651,8 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     cubc(ctx, [&](void *t, size_t &b) {
         return cub::DeviceRadixSort::SortPairs(t, b, k1.p, k1s.p, idx.p, perm.p, n, 63 - top_bits, 63, s);
     });
-    int deep = 0;
-    if (nlev > SORT_LEVELS) {
+    int deep = bh->n_forced > 0 ? 1 : 0;  // forced cubes may split below the top levels
+    if (!deep && nlev > SORT_LEVELS) {
         scratch_i.resize(1);
         scratch_i.zero(s);
         bb_long_runs<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, (int)bucket, k1s.p, 63 - top_bits, scratch_i.p);
@@ -701,6 +756,9 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     A.big = big.p;
     A.nbig = big.p + n;
     GC_CUDA(cudaMemsetAsync(big.p + n, 0, sizeof(int), s));
+    A.forced_lvl = bh->d_forced_lvl.p;
+    A.forced_key = bh->d_forced_key.p;
+    A.n_forced = bh->n_forced;
     A.lvl_first = lvlf.p;
     A.nlevels = lvlf.p + MAX_KEY_LEVELS + 2;
     A.overflow = lvlf.p + MAX_KEY_LEVELS + 3;

@@ -111,6 +111,14 @@ struct gc_bh {
     // walk begin/end, forces begin/end, reorganisation end (= force kernel begin)
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     BuildWs ws;
+    // distributed BH (bh_dist.py): cubes the device build must split whatever
+    // their local count (they straddle ranks; globally they split), as
+    // (level, left-aligned key prefix) sorted; walk-group cut points (DFS
+    // bucket indices no walk group may straddle) of an assembled tree
+    DBuf<ulonglong2> d_forced_key;
+    DBuf<int> d_forced_lvl;
+    int n_forced = 0;
+    std::vector<int64_t> wg_cuts;
     int64_t h2d = 0, d2h = 0;  // bytes moved host<->device since the last reset
     cudaStream_t side = nullptr;  // device build: mass upload overlapping the sort
     cudaEvent_t side_done = nullptr, main_ready = nullptr;
@@ -165,6 +173,8 @@ inline void wait_orders(gc_bh *bh)
         bh->order_pending = false;
     }
 }
+// octant keys of the device build (bb_keys) for host positions (gc_bh_keys)
+void device_keys(gc_ctx *ctx, int64_t n, int dim, const double *pos, double box, uint64_t *k1, uint64_t *k2);
 void device_build_tree(gc_bh *bh, const double *pos, const double *mass, int64_t n, int dim, double box,
                        int64_t bucket_size);
 void ensure_host_tree(gc_bh *bh);

@@ -69,7 +69,10 @@ class TreeNode:
 class BucketTree:
     """Device-resident bucket tree (hr/workloads/nbody.py:71-75)."""
 
-    def __init__(self, ps: ParticleSet, bucket_size: int, device_build: bool = True):
+    def __init__(self, ps: ParticleSet, bucket_size: int, device_build: bool = True, forced=None):
+        """forced=(levels (m,) int32, prefixes (m, 2) uint64): cubes the build
+        splits whatever their count (a rank's part of a distributed tree,
+        bh_dist.py)."""
         self.ps = ps
         self.bucket_size = int(bucket_size)
         self.dim = ps.positions.shape[1]
@@ -78,6 +81,10 @@ class BucketTree:
         self.handle = C.c_void_p()
         L.call("gc_bh_create", self._ctx.handle, C.byref(self.handle))
         L.call("gc_bh_set_build_mode", self.handle, int(bool(device_build)))
+        if forced is not None and len(forced[0]):
+            fl = np.ascontiguousarray(forced[0], np.int32)
+            fp = np.ascontiguousarray(forced[1], np.uint64).reshape(-1)
+            L.call("gc_bh_set_forced_splits", self.handle, len(fl), L.ptr(fl, L.i32p), L.ptr(fp, L.u64p))
         pos, m = L.f64(ps.positions), L.f64(ps.masses)
         L.call("gc_bh_set_particles", self.handle, self.n, self.dim, L.ptr(pos, L.f64p), L.ptr(m, L.f64p),
                float(ps.box), self.bucket_size)
