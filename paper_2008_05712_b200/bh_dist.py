@@ -659,12 +659,14 @@ class DistBH:
         first_child = np.where(n_child > 0, fcv, -1)
         # sealed / bucket nodes must be childless; internal nodes must have children
         assert np.all(n_child[kind != 0] == 0) and np.all(n_child[kind == 0] > 0), "assembled tree: bad node kinds"
-        # particles: own, received, one poison (sealed nodes point at it)
-        ppos = [pos] + rpos + [np.full((1, dim), np.nan)]
-        pmass = [mass] + rmass + [np.zeros(1)]
-        pgid = [gid] + rgid + [np.full(1, -1, np.int64)]
+        # particles: own, received, one poison row per sealed node (every row
+        # appears once in the bucket layout)
+        nseal = int(np.sum(kind == 2))
+        ppos = [pos] + rpos + [np.full((nseal, dim), np.nan)]
+        pmass = [mass] + rmass + [np.zeros(nseal)]
+        pgid = [gid] + rgid + [np.full(nseal, -1, np.int64)]
         ppos = np.concatenate(ppos); pmass = np.concatenate(pmass); pgid = np.concatenate(pgid)
-        poison = len(pmass) - 1
+        poison = len(pmass) - nseal
         # buckets (kinds 1, 2) in DFS order = order of their left-aligned prefixes
         leaf = np.nonzero(kind != 0)[0]
         leaf = leaf[np.lexsort((pb[leaf], pa[leaf]))]
@@ -675,6 +677,7 @@ class DistBH:
         for j, i in enumerate(leaf):
             if kind[i] == 2:
                 ids = np.array([poison], np.int64)
+                poison += 1
             elif src[i, 0] == 0:
                 b = src[i, 1]
                 ids = t["pidx"][t["pstart"][b]: t["pstart"][b] + t["pcount"][b]]
@@ -688,6 +691,7 @@ class DistBH:
             pc_out[i] = len(ids)
             off += len(ids)
         order = np.concatenate(plist)
+        assert len(order) == len(pmass) and np.array_equal(np.sort(order), np.arange(len(pmass)))
         n_own_b = int(np.sum((kind[leaf] == 1) & (src[leaf, 0] == 0)))
         assert own_lo is not None and own_hi - own_lo == n_own_b, "own buckets are not contiguous in DFS order"
         tree = dict(center=center, half=half, mass=nmass, com=com, first_child=first_child, n_child=n_child,

@@ -884,6 +884,22 @@ gc_status gc_bh_set_tree(gc_bh *bh, int64_t n_nodes, int32_t dim, double box, in
                        order && pos && pmass,
                    GC_E_VALUE, "null argument");
         GC_REQUIRE(n_nodes >= 1 && n_buckets >= 1 && n_parts >= 1 && dim >= 1 && dim <= 3, GC_E_VALUE, "bad sizes");
+        // validate the layout (the upload indexes by these values)
+        std::vector<char> seen((size_t)n_parts, 0);
+        for (int64_t b = 0; b < n_buckets; ++b) {
+            const int64_t id = buckets[b];
+            GC_REQUIRE(id >= 0 && id < n_nodes && first_child[id] < 0, GC_E_VALUE, "bucket list entry is not a leaf");
+            GC_REQUIRE(pstart[id] >= 0 && pcount[id] >= 1 && pstart[id] + pcount[id] <= n_parts, GC_E_VALUE,
+                       "bucket particle range out of bounds");
+            for (int64_t k = 0; k < pcount[id]; ++k) {
+                const int64_t p = order[pstart[id] + k];
+                GC_REQUIRE(p >= 0 && p < n_parts && !seen[p], GC_E_VALUE, "order is not a permutation of the particles");
+                seen[p] = 1;
+            }
+        }
+        for (int64_t i = 0; i < n_nodes; ++i)
+            GC_REQUIRE(first_child[i] < 0 || (n_child[i] >= 1 && first_child[i] > i && first_child[i] + n_child[i] <= n_nodes),
+                       GC_E_VALUE, "bad child range");
         wait_orders(bh);
         HostTree &t = bh->tree;
         t.n = n_parts;
