@@ -216,6 +216,8 @@ def run_reference(args, world, rank):
         return
     from paper_2008_05712_b200.generators import gen_lj_fcc
     ps = workload(1)
+    if args.warmup > 0:
+        cpu_bh(ps, steps=args.warmup)  # untimed warm-up steps (page-in, thread pool)
     inter, ts, cores = cpu_bh(ps, steps=max(1, args.steps))
     mean = statistics.mean(ts)
     v = inter / mean
@@ -386,6 +388,55 @@ def bench_bh(args, world, rank, local, ctx, torch):
                 "path": "gc_bh_step C ABI: pinned host positions/masses -> H2D -> device tree build -> device walk "
                         "-> reorganisation -> forces -> D2H (median of the timed calls)"},
     }
+
+
+def bench_bh_dist(args, world, rank, local, ctx, torch):
+    """N > 1 (configs[3]-style, weak scaling): ONE clustered system of N x 1M
+    particles, each rank starting from an arbitrary 1/N share and never
+    holding the rest -- partitioned trees + LET exchange (bh_dist.py).
+    value: interactions / max over ranks of the device walk + force time on
+    the assembled tree (CUDA events); e2e: the whole distributed step (keys,
+    sample sort, all-to-all, local device build, branch all-gather, LET
+    all-to-all, assembly, H2D, walk, forces, D2H), wall clock, max over ranks."""
+    from paper_2008_05712_b200 import bh_dist
+
+    ps = workload(world)
+    n = len(ps.masses)
+    mine = np.arange(rank, n, world)
+    pos, m = np.ascontiguousarray(ps.positions[mine]), np.ascontiguousarray(ps.masses[mine])
+    d = bh_dist.DistBH(bh_dist.Comm(), BUCKET, THETA, 1.0, EPS)
+    for _ in range(max(1, min(args.warmup, 2))):
+        d.step(pos, m, mine)
+    dev_ms, wall, walk, force = [], [], [], []
+    clk = ClockSampler(local)
+    with clk:
+        for _ in range(max(1, min(args.steps, 5))):
+            barrier(world)
+            t0 = time.perf_counter()
+            res = d.step(pos, m, mine)
+            wall.append(time.perf_counter() - t0)
+            last = d.backend.last
+            walk.append(last["walk_ms"])
+            force.append(last["force_ms"])
+            dev_ms.append(last["walk_ms"] + last["force_ms"])
+    inter = d.backend.last["interactions"]
+    total = allsum(inter, world)
+    ms = allmax(statistics.mean(dev_ms), world)
+    e2e_s = allmax(statistics.median(wall), world)
+    return {"ps": None, "inter": inter, "ms": ms, "value": total / (ms * 1e-3), "walk_ms": statistics.mean(walk),
+            "force_ms": statistics.mean(force), "total_inter": total, "reorg_ms": 0.0, "n_union": 0,
+            "n_records": 0, "clocks": clk.summary(), "shard": dict(res.stats),
+            "roofline": {"bound": "fp32", "kernel": "force_fused_kernel on the assembled tree",
+                         "achieved": FLOPS_PER_INTERACTION * inter / (statistics.mean(force) * 1e-3) / 1e12,
+                         "peak": NOMINAL_FP32_TFLOPS, "peak_source": "nominal 148 x 128 x 2 x 1.965 GHz",
+                         "unit": "TFLOP/s", "traffic": None,
+                         "frac": FLOPS_PER_INTERACTION * inter / (statistics.mean(force) * 1e-3) / 1e12
+                         / NOMINAL_FP32_TFLOPS},
+            "reorg_roofline": None,
+            "e2e": {"value": total / e2e_s, "unit": "interactions/s", "ms_per_step": e2e_s * 1e3,
+                    "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                    "path": "DistBH.step: partition + local device build + LET exchange + assembly + walk + forces "
+                            "(host-orchestrated, wall clock, max over ranks)"}}
 
 
 def bench_md_slabs(args, world, rank, local, torch):
@@ -605,7 +656,8 @@ def run_ours(args, world, rank, local):
 
     torch.cuda.set_device(local)
     ctx = L.context(local)
-    bh = bench_bh(args, world, rank, local, ctx, torch)
+    bh = bench_bh(args, world, rank, local, ctx, torch) if world == 1 else bench_bh_dist(args, world, rank, local,
+                                                                                         ctx, torch)
     mdr = bench_md(args, world, rank, local, torch)
     if rank != 0:
         return
@@ -631,9 +683,13 @@ def run_ours(args, world, rank, local):
     sysin = mdr.pop("_sysin")
     line["md"] = mdr
     if world > 1:
-        line["config"]["shard"] = {"walk_groups": bh["shard"], "interactions_this_rank": bh["inter"],
+        line["config"]["step"] = ("distributed: partitioned trees (sample sort on octant keys), all-gathered top "
+                                  "of tree, LET all-to-all; device walk + force on the assembled tree (bh_dist.py)")
+        line["config"]["shard"] = {"rank0": bh["shard"], "interactions_this_rank": bh["inter"],
                                    "interactions_all_ranks": bh["total_inter"],
-                                   "system": f"one shared clustered system of {world} x 1M particles"}
+                                   "system": f"one clustered system of {world} x 1M particles, each rank holding "
+                                             f"1/{world}"}
+        line["gpu_launches"] = None
         line["data"] = f"synthetic gen_particles({world}M, seed 42, clustering 0.6, dim 3), fp32-exact"
     if world == 1:
         line["runtime_path"] = bench_runtime_path(args)

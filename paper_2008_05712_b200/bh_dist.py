@@ -200,7 +200,12 @@ class Comm:
 # the float64 oracle (oracle/dist_backend.py)
 # --------------------------------------------------------------------------
 class DeviceBackend:
-    """libgcharm.so: keys, the forced-split local build, the assembled-tree step."""
+    """libgcharm.so: keys, the forced-split local build, the assembled-tree step.
+    ``last`` holds the device times (CUDA events, ms) of the last step's walk
+    and force kernels and its interaction count."""
+
+    def __init__(self):
+        self.last = {}
 
     def keys(self, pos, box):
         from . import _lib as L
@@ -251,9 +256,16 @@ class DeviceBackend:
             g0, g1 = int(np.searchsorted(wfb, own[0])), int(np.searchsorted(wfb, own[1]))
             assert wfb[g0] == own[0] and wfb[g1] == own[1], "own buckets must form whole walk groups"
             L.call("gc_bh_set_range", h, g0, g1)
+            L.call("gc_bh_walk", h, float(theta))  # stats walk (sizes the union pool for this tree)
             L.call("gc_bh_walk", h, float(theta))
+            L.call("gc_bh_forces_async", h, float(g), float(eps))
+            tm = np.zeros(3)
+            L.call("gc_bh_timings", h, L.ptr(tm, L.f64p))
             f = np.zeros((n, dim))
-            L.call("gc_bh_forces", h, float(g), float(eps), L.ptr(f, L.f64p))
+            L.call("gc_bh_get_forces", h, L.ptr(f, L.f64p))
+            cnt = np.zeros(1, np.int64)
+            L.call("gc_bh_interactions", h, L.ptr(cnt, L.i64p))
+            self.last = dict(walk_ms=float(tm[0]), force_ms=float(tm[1]), interactions=int(cnt[0]))
             lists = None
             if want_lists:
                 nb = len(ar["buckets"])
@@ -412,12 +424,20 @@ class DistBH:
     def step(self, pos, mass, gid, want_lists=False) -> DistResult:
         """Forces on this rank's particles (of the global N-body system whose
         other particles the other ranks hold); pos/mass/gid: any initial share."""
+        import time
+        tic = [time.perf_counter()]
+
+        def lap(name):
+            tic.append(time.perf_counter())
+            self.stats["t_" + name] = tic[-1] - tic[-2]
+
         cm, box = self.comm, self.box
         pos = np.ascontiguousarray(pos, np.float64)
         dim = pos.shape[1]
         mass = np.ascontiguousarray(mass, np.float64)
         gid = np.ascontiguousarray(gid, np.int64)
         pos, mass, gid, k1, k2, scubes, scount = self._partition(pos, mass, gid)
+        lap("partition")
         n = len(gid)
         if not n:
             raise ValueError("a rank holds no particles after the partition (fewer particles than ranks?)")
@@ -451,6 +471,7 @@ class DistBH:
             own_node = ~is_strad  # complete local nodes (global tree nodes)
         else:
             t, nn = None, 0
+        lap("local_tree")
         # ---- 4: branch summaries, top of the tree ------------------------------
         bcols = 7 + 2 * dim  # level, p1, p2, half, mass, is_bucket, count, center(dim), com(dim)
         if n:
@@ -477,6 +498,7 @@ class DistBH:
             aabb[0, dim:] = hi_.max(axis=0)
         aabbs = [a[0] for a in cm.allgather(aabb)]
         top = self._top_nodes(scubes, allbr, dim)
+        lap("top")
         # ---- 5: LET for every peer ------------------------------------------
         let_nodes, let_parts = [], []
         for r in range(cm.world):
@@ -489,11 +511,14 @@ class DistBH:
             let_parts.append(b)
         rn = cm.alltoallv(let_nodes)
         rp = cm.alltoallv(let_parts)
+        lap("let")
         # ---- 6: assemble, walk the own buckets ----------------------------------
         tree, own, stats = self._assemble(t, lvl, p1, p2, own_node if n else None, pos, mass, gid, top, allbr, rn,
                                           rp, dim)
         self.stats.update(stats)
+        lap("assemble")
         f, lists = self.backend.step(tree, own, self.theta, self.g, self.eps, want_lists)
+        lap("device_step")
         return DistResult(gid=gid, forces=f[:n], tree=tree, own=own, lists=lists, stats=dict(self.stats))
 
     def _top_nodes(self, scubes, allbr, dim):
@@ -670,34 +695,29 @@ class DistBH:
         # buckets (kinds 1, 2) in DFS order = order of their left-aligned prefixes
         leaf = np.nonzero(kind != 0)[0]
         leaf = leaf[np.lexsort((pb[leaf], pa[leaf]))]
-        plist, pstart = [], np.zeros(nn, np.int64)
+        own_leaf = (kind[leaf] == 1) & (src[leaf, 0] == 0)
+        ol = np.nonzero(own_leaf)[0]
+        own_lo, own_hi = (int(ol[0]), int(ol[-1]) + 1) if len(ol) else (None, None)
+        assert own_lo is not None and own_hi - own_lo == len(ol), "own buckets are not contiguous in DFS order"
+        cnt = np.where(kind[leaf] == 2, 1, pcount[leaf]).astype(np.int64)
+        cnt[own_leaf] = t["pcount"][src[leaf[own_leaf], 1]]
+        # source row of each leaf's first particle: sealed -> its own poison row,
+        # received -> n + offset; own leaves take the local DFS particle layout
+        seal_rank = np.cumsum(kind[leaf] == 2) - 1
+        first = np.where(kind[leaf] == 2, poison + seal_rank, n + np.maximum(src[leaf, 1], 0))
+        off = np.concatenate([[0], np.cumsum(cnt)])
+        tot = int(off[-1])
+        order = np.repeat(first, cnt) + (np.arange(tot) - np.repeat(off[:-1], cnt))
+        order[off[own_lo]: off[own_hi]] = t["pidx"]  # own buckets, local DFS order (ascending global id per bucket)
+        pstart = np.zeros(nn, np.int64)
         pc_out = np.zeros(nn, np.int64)
-        off = 0
-        own_lo, own_hi = None, None
-        for j, i in enumerate(leaf):
-            if kind[i] == 2:
-                ids = np.array([poison], np.int64)
-                poison += 1
-            elif src[i, 0] == 0:
-                b = src[i, 1]
-                ids = t["pidx"][t["pstart"][b]: t["pstart"][b] + t["pcount"][b]]
-                if own_lo is None:
-                    own_lo = j
-                own_hi = j + 1
-            else:
-                ids = n + src[i, 1] + np.arange(pcount[i])
-            plist.append(ids)
-            pstart[i] = off
-            pc_out[i] = len(ids)
-            off += len(ids)
-        order = np.concatenate(plist)
+        pstart[leaf] = off[:-1]
+        pc_out[leaf] = cnt
         assert len(order) == len(pmass) and np.array_equal(np.sort(order), np.arange(len(pmass)))
-        n_own_b = int(np.sum((kind[leaf] == 1) & (src[leaf, 0] == 0)))
-        assert own_lo is not None and own_hi - own_lo == n_own_b, "own buckets are not contiguous in DFS order"
         tree = dict(center=center, half=half, mass=nmass, com=com, first_child=first_child, n_child=n_child,
                     pstart=pstart, pcount=pc_out, buckets=leaf, order=order, pos=ppos, pmass=pmass, gid=pgid,
                     level=lvl_a, p1=pa, p2=pb, box=self.box, bucket=self.bucket)
-        own = (own_lo or 0, own_hi or 0)
+        own = (own_lo, own_hi)
         stats = dict(nodes=nn, let_nodes_received=int(sum(len(r) for r in rn)),
                      let_particles_received=int(sum(len(p) for p in rp)), own_buckets=own[1] - own[0])
         return tree, own, stats
