@@ -147,7 +147,6 @@ gc_status gc_bh_set_tree(gc_bh *bh, int64_t n_nodes, int32_t dim, double box, in
                          const int64_t *cuts);
 /* one step's walk + forces, asynchronous (= gc_bh_walk + gc_bh_forces_async) */
 gc_status gc_bh_walk_forces_async(gc_bh *bh, double theta, double g, double eps);
-gc_status gc_bh_set_build_mode(gc_bh *bh, int32_t device);
 /* Sizes: out[0..4] = n_nodes, n_buckets, per-bucket list entries, union
  * entries of the last device walk, source records they expand to (staging) */
 gc_status gc_bh_sizes(gc_bh *bh, int64_t out[5]);

@@ -69,7 +69,7 @@ def lib():
         L.orc_md2d_compute_forces.argtypes = [C.c_int64, f64p, i64p, C.c_int64, C.c_int64, C.c_double,
                                               C.c_double, C.c_double, C.c_int, f64p]
         L.orc_lj3d_compute_forces.argtypes = [C.c_int64, f64p, i64p, C.c_double, C.c_double, C.c_double,
-                                              C.c_double, C.c_int, f64p, f64p]
+                                              C.c_double, C.c_int, f64p, f64p, C.c_int]
         L.orc_lj3d_bruteforce.argtypes = [C.c_int64, f64p, f64p, C.c_double, C.c_double, C.c_double,
                                           C.c_int, f64p, f64p]
         L.orc_count_address_runs.argtypes = [i64p, C.c_int64, C.c_int64]
@@ -345,13 +345,16 @@ def md2d_step(positions, velocities, patch_of, rows, cols, patch_size, cutoff, d
     return pos, vel, r * cols + c
 
 
-def lj3d_compute_forces(positions, dims, cell_size, rc=2.5, eps=1.0, sigma=1.0, periodic=True):
+def lj3d_compute_forces(positions, dims, cell_size, rc=2.5, eps=1.0, sigma=1.0, periodic=True, nthreads=1):
+    """nthreads=1: the serial parity restatement; otherwise (0 = all) the
+    multi-core form used as the CPU baseline (same pairs, thread-private sums)."""
     pos = _f64(positions)
     d = np.ascontiguousarray(dims, np.int64)
     f = np.zeros_like(pos)
     e = np.zeros(pos.shape[0])
     lib().orc_lj3d_compute_forces(pos.shape[0], _p(pos, f64p), _p(d, i64p), float(cell_size), float(rc),
-                                  float(eps), float(sigma), int(bool(periodic)), _p(f, f64p), _p(e, f64p))
+                                  float(eps), float(sigma), int(bool(periodic)), _p(f, f64p), _p(e, f64p),
+                                  int(nthreads))
     return f, e
 
 
@@ -365,10 +368,10 @@ def lj3d_bruteforce(positions, box, rc=2.5, eps=1.0, sigma=1.0, periodic=True):
     return f, e
 
 
-def lj3d_step(positions, velocities, dims, cell_size, dt, rc=2.5, eps=1.0, sigma=1.0):
+def lj3d_step(positions, velocities, dims, cell_size, dt, rc=2.5, eps=1.0, sigma=1.0, nthreads=1):
     """LJ analogue of md_step (md.py:166-190) with periodic wrap: v += F dt
     (unit mass); x += v dt; x %= box.  Returns (pos, vel, forces, energy)."""
-    f, e = lj3d_compute_forces(positions, dims, cell_size, rc, eps, sigma, True)
+    f, e = lj3d_compute_forces(positions, dims, cell_size, rc, eps, sigma, True, nthreads)
     vel = velocities + f * dt
     pos = positions + vel * dt
     box = np.asarray(dims, np.float64) * cell_size

@@ -784,18 +784,7 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
         GC_REQUIRE(bucket_size <= 32, GC_E_VALUE, "bucket_size must be <= 32 on the B200 path");
         GC_REQUIRE(dim >= 1 && dim <= 3, GC_E_VALUE, "dim must be 1..3");
         wait_orders(bh);  // make_orders may still read the previous tree's groups
-        if (bh->device_build) {
-            device_build_tree(bh, pos, mass, n, dim, box, bucket_size);
-        } else {
-            bh->tree.build(n, dim, pos, mass, box, bucket_size);
-            bh->host_tree_valid = true;
-            bh->n = n;
-            bh->dim = dim;
-            bh->box = box;
-            bh->bucket_size = bucket_size;
-            bh->n_nodes = bh->tree.n_nodes();
-            bh->n_buckets = (int64_t)bh->tree.buckets.size();
-        }
+        device_build_tree(bh, pos, mass, n, dim, box, bucket_size);
         bh->have_tree = true;
         bh->have_union = bh->have_member_lists = false;
         bh->ew_mom_valid = false;
@@ -805,12 +794,6 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
         bh->orders_fresh = false;
         bh->rg0 = 0;
         bh->rg1 = -1;
-        if (!bh->device_build) {
-            upload_tree(bh);
-            upload_particles(bh, pos, mass);
-            bh->ws.pos.upload(pos, (size_t)n * dim, bh->ctx->stream);  // float64 copies (Ewald moments)
-            bh->ws.mass.upload(mass, (size_t)n, bh->ctx->stream);
-        }
     });
 }
 
@@ -977,14 +960,6 @@ gc_status gc_bh_set_force_mode(gc_bh *bh, int32_t fused)
     return guard([&] {
         GC_REQUIRE(bh, GC_E_VALUE, "null argument");
         bh->force_fused = fused != 0;
-    });
-}
-
-gc_status gc_bh_set_build_mode(gc_bh *bh, int32_t device)
-{
-    return guard([&] {
-        GC_REQUIRE(bh, GC_E_VALUE, "null argument");
-        bh->device_build = device != 0;
     });
 }
 

@@ -29,7 +29,6 @@ struct gc_bh {
     HostTree tree;  // host mirror (valid when host_tree_valid)
     bool have_tree = false;
     bool host_tree_valid = false;
-    bool device_build = true;  // build the tree on the GPU (gc_bh_set_build_mode)
     bool force_fused = true;
     bool overlap = false;  // walk and force kernel of a step overlap (gc_bh_set_overlap; fused mode; measured neutral)
     cudaStream_t force_stream = nullptr;

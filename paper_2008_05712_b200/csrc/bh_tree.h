@@ -1,4 +1,5 @@
-// bh_tree.h -- host-side bucket tree (product).
+// bh_tree.h -- host mirror of the device-built bucket tree (downloaded for the
+// per-bucket API and the data manager; the tree is only ever built on the GPU).
 #pragma once
 #include <stdint.h>
 
@@ -24,7 +25,6 @@ struct HostTree {
     std::vector<int64_t> order;  // particle ids; buckets' ranges laid out in DFS order
 
     int64_t n_nodes() const { return (int64_t)half.size(); }
-    void build(int64_t n, int dim, const double *pos, const double *mass, double box, int64_t bucket_size);
 };
 
 }  // namespace gc

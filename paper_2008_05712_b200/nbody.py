@@ -69,7 +69,7 @@ class TreeNode:
 class BucketTree:
     """Device-resident bucket tree (hr/workloads/nbody.py:71-75)."""
 
-    def __init__(self, ps: ParticleSet, bucket_size: int, device_build: bool = True, forced=None):
+    def __init__(self, ps: ParticleSet, bucket_size: int, forced=None):
         """forced=(levels (m,) int32, prefixes (m, 2) uint64): cubes the build
         splits whatever their count (a rank's part of a distributed tree,
         bh_dist.py)."""
@@ -80,7 +80,6 @@ class BucketTree:
         self._ctx = L.context()
         self.handle = C.c_void_p()
         L.call("gc_bh_create", self._ctx.handle, C.byref(self.handle))
-        L.call("gc_bh_set_build_mode", self.handle, int(bool(device_build)))
         if forced is not None and len(forced[0]):
             fl = np.ascontiguousarray(forced[0], np.int32)
             fp = np.ascontiguousarray(forced[1], np.uint64).reshape(-1)
@@ -153,13 +152,13 @@ class BucketTree:
         return [TreeNode(self, int(b)) for b in self.bucket_ids]
 
 
-def build_bucket_tree(ps: ParticleSet, bucket_size: int, device_build: bool = True) -> BucketTree:
+def build_bucket_tree(ps: ParticleSet, bucket_size: int) -> BucketTree:
     """hr/workloads/nbody.py:78-120: level-order ids, depth-first buckets,
     float64 mass/COM with the reference's rounding -- built on the GPU
-    (csrc/bh_build.cu) or by the host C++ builder (device_build=False)."""
+    (csrc/bh_build.cu); there is no host builder in the product."""
     if bucket_size < 1:
         raise ValueError("bucket_size must be >= 1")
-    return BucketTree(ps, bucket_size, device_build)
+    return BucketTree(ps, bucket_size)
 
 
 @dataclass

@@ -170,3 +170,15 @@ def test_potential_oracle_coincident_skip():
     ol = orc.build_interaction_lists(t, 0.5)
     phi = orc.eval_potentials(t, ol, pos, m, 1.0, 0.0)
     np.testing.assert_allclose(phi, [-1.0 * 3.0 / 0.5, -2.0 * 3.0 / 0.5, -3.0 * 3.0 / 0.5], rtol=1e-15)
+
+
+def test_lj3d_multicore_baseline_matches_serial():
+    """The multi-core LJ restatement (the CPU baseline's form) evaluates the
+    same pairs as the serial parity restatement: equal to rounding."""
+    from paper_2008_05712_b200.generators import gen_lj_fcc
+    s = gen_lj_fcc(8)
+    d = (s.cells,) * 3
+    f1, e1 = orc.lj3d_compute_forces(s.positions, d, s.cell_size, nthreads=1)
+    f2, e2 = orc.lj3d_compute_forces(s.positions, d, s.cell_size, nthreads=4)
+    np.testing.assert_allclose(f2, f1, rtol=0, atol=1e-11)
+    np.testing.assert_allclose(e2, e1, rtol=0, atol=1e-11)

@@ -4,8 +4,10 @@
 set -e
 name=$1; shift
 flags="$*"
-cd "$(dirname "$0")/../paper_2008_05712_b200/csrc"
-out=../../build/var_$name
+# SRC=<dir> builds the sources of another tree (e.g. a `git archive` of an older commit)
+root="$(cd "$(dirname "$0")/.." && pwd)"
+cd "${SRC:-$root/paper_2008_05712_b200/csrc}"
+out=$root/build/var_$name
 mkdir -p $out
 objs=""
 for f in abi.cu bh.cu bh_build.cu md.cu md_loop.cu ewald.cu dm.cu; do
@@ -14,6 +16,9 @@ for f in abi.cu bh.cu bh_build.cu md.cu md_loop.cu ewald.cu dm.cu; do
   objs="$objs $out/$f.o"
 done
 wait
-nvcc -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -ffp-contract=off -c bh_tree.cpp -o $out/bh_tree.o
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libgcharm_$name.so $objs $out/bh_tree.o -lcudart
-echo built ../libgcharm_$name.so
+if [ -f bh_tree.cpp ]; then  # older trees still had the host builder
+  nvcc -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -ffp-contract=off -c bh_tree.cpp -o $out/bh_tree.o
+  objs="$objs $out/bh_tree.o"
+fi
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $root/paper_2008_05712_b200/libgcharm_$name.so $objs -lcudart
+echo built libgcharm_$name.so
