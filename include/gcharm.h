@@ -46,6 +46,7 @@ typedef struct gc_ctx gc_ctx;
 typedef struct gc_bh gc_bh;
 typedef struct gc_dm gc_dm;
 typedef struct gc_md gc_md;
+typedef struct gc_batcher gc_batcher;
 
 const char *gc_last_error(void);
 const char *gc_version(void);
@@ -236,6 +237,45 @@ gc_status gc_dm_stage_bh(gc_dm *dm, gc_bh *bh);
 gc_status gc_bh_run_members(gc_bh *bh, gc_dm *dm, const int64_t *member_buckets, int32_t n_members,
                             const int8_t *kinds, int64_t n_positions, double g, double eps);
 gc_status gc_bh_get_forces(gc_bh *bh, double *out);
+
+/* ---- device batcher (north star subsystem (1)) ------------
+ * The aggregation trigger of hr/aggregator.py (observe_arrival / poll_combine,
+ * :41-110; size rule = exactly max_size earliest, timeout rule = strict gap >
+ * timeout_factor x running-max gap over the last `window` gaps, 0 = all) over
+ * a device ring of work requests, each emitted batch planned by the device
+ * data manager `dm` (no host round trip when every buffer id fits the slot
+ * count, else the synchronous plan), staged into its slots and evaluated by
+ * one member-kernel launch -- the launch site hr/timeline.py:300-321 executes
+ * instead of charging its cost model.  One batcher per kernel class.
+ * gc_batcher_submit: n requests in FIFO order, owners = DFS bucket indices,
+ *   arrival times (non-decreasing; GC_E_CLOCK otherwise), buffer ids as CSR
+ *   (ptr[n+1] into ids) with kinds (0 node_interaction, 1
+ *   particle_interaction); every arrival is observed and polled at its time
+ *   (Runtime.submit_work_request hr/runtime.py:151-163 + _poll_aggregation
+ *   hr/timeline.py:262-274), emitted batches are launched asynchronously.
+ * gc_batcher_poll: a poll at `now` (Timeline ticks).
+ * gc_batcher_flush: end of the phase, drain in max_size chunks
+ *   (hr/timeline.py:276-283).
+ * gc_batcher_sync: wait for every launched batch; n_batches emitted so far.
+ * gc_batcher_log: ScheduleLog rows (hr/timeline.py:63-100), 7 int64 per batch
+ *   {combined_id, first request, members, positions, buffers transferred,
+ *   transactions, synchronous plan} and 2 doubles {emit time, device ms}.
+ * gc_batcher_trigger_device: the trigger alone, evaluated on the device on
+ *   n events at the given times (or %globaltimer stamps when arrival is
+ *   NULL): an arrival (observed, then polled) or, where is_poll[i] != 0, a
+ *   poll only; emissions (first request, count, time). */
+gc_status gc_batcher_create(gc_ctx *ctx, gc_bh *bh, gc_dm *dm, int64_t max_size, double timeout_factor,
+                            int32_t window, double g, double eps, gc_batcher **out);
+gc_status gc_batcher_destroy(gc_batcher *b);
+gc_status gc_batcher_submit(gc_batcher *b, int64_t n, const int64_t *owner, const double *arrival,
+                            const int64_t *ptr, const int64_t *ids, const int8_t *kinds);
+gc_status gc_batcher_poll(gc_batcher *b, double now);
+gc_status gc_batcher_flush(gc_batcher *b, double now);
+gc_status gc_batcher_sync(gc_batcher *b, int64_t *n_batches);
+gc_status gc_batcher_log(gc_batcher *b, int64_t *rows, double *times);
+gc_status gc_batcher_trigger_device(int64_t max_size, double timeout_factor, int32_t window, int64_t n,
+                                    const double *arrival, const int8_t *is_poll, int64_t *e_first, int64_t *e_count, double *e_time,
+                                    int64_t *n_emit);
 
 /* ---- cell-pair MD (hr/workloads/md.py; 3-D Lennard-Jones extension) --------
  * law 0: soft repulsion, params = {cutoff, stiffness, -} (kernels.py:105-161);

@@ -82,6 +82,14 @@ SIGNATURES = {
     "gc_measure_fp32_peak": [vp, f64p, f64p],
     "gc_bh_step": [vp, C.c_int64, C.c_int32, f64p, f64p, C.c_double, C.c_int64, C.c_double, C.c_double,
                    C.c_double, f64p],
+    "gc_batcher_create": [vp, vp, vp, C.c_int64, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(vp)],
+    "gc_batcher_destroy": [vp],
+    "gc_batcher_submit": [vp, C.c_int64, i64p, f64p, i64p, i64p, i8p],
+    "gc_batcher_poll": [vp, C.c_double],
+    "gc_batcher_flush": [vp, C.c_double],
+    "gc_batcher_sync": [vp, i64p],
+    "gc_batcher_log": [vp, i64p, f64p],
+    "gc_batcher_trigger_device": [C.c_int64, C.c_double, C.c_int32, C.c_int64, f64p, i8p, i64p, i64p, f64p, i64p],
     "gc_dm_create": [vp, C.c_int64, C.c_int64, C.c_int32, C.POINTER(vp)],
     "gc_dm_destroy": [vp],
     "gc_dm_build_plan": [vp, i64p, i64p, C.c_int32, C.c_double, i64p, i64p],

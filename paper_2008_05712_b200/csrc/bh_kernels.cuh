@@ -875,11 +875,13 @@ force_group_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const int *_
 // round trip through HBM disappears (sources are gathered from the
 // L2-resident tree records and particles).
 // ---------------------------------------------------------------------------
+#ifndef FUSED_PREFETCH
+#define FUSED_PREFETCH 1
+#endif
 #ifndef FUSED_RING
 #define FUSED_RING 128
 #endif
 constexpr int RING = FUSED_RING;
-constexpr int ROUND = 64;  // records one production round makes (two per lane)
 __device__ __forceinline__ int ld_acquire_gpu(const int *p)
 {
     int v;
@@ -891,6 +893,7 @@ __device__ __forceinline__ int ld_list(const int *p)
 {
     return CG ? __ldcg(p) : *p;
 }
+constexpr int RING_LOW = RING / 2;  // produce while fewer records wait (RING >= RING_LOW + 33: one entry always fits)
 template <bool EPS0, bool POT, bool OVL = false>
 __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, FORCE_MINB)
 force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U, const Staging S,
@@ -942,9 +945,7 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
         const int n = ld_list<OVL>(U.gcount + gi);
         int chunk_cur = n > 0 ? ld_list<OVL>(U.gfirst + gi) : 0, cur_ci = 0;
         int chunk_nxt = (n > CHUNK) ? ld_list<OVL>(U.cnext + chunk_cur) : 0;
-        // record-level cursor: the next record to produce is record `eoff` of
-        // union entry `ebase` (entries expand to [node record] + opened particles)
-        int ebase = 0, eoff = 0, wr = 0, rd = 0;
+        int ebase = 0, wr = 0, rd = 0;
         auto load_entry = [&](int e) {
             int4 en = make_int4(0, 0, 0, 0);
             if (e < n) {
@@ -953,79 +954,73 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
             }
             return en;
         };
+#if FUSED_PREFETCH
+        int pf_base = -1;
+        int4 en_pf = make_int4(0, 0, 0, 0);
+#if FUSED_PREFETCH > 1
+        float4 h_pf = make_float4(0.f, 0.f, 0.f, 0.f), l_pf = h_pf;
+#endif
+#endif
         for (;;) {
-            // produce: load-balanced rounds of <= ROUND records, lane l makes
-            // records 2l and 2l + 1 of the round (one pair slot of the ring):
-            // the 32 entries at the cursor are scanned, every record finds its
-            // entry from a bitmap of entry starts, and the gathers of all
-            // lanes are in flight together.  Record order = the union order
-            // (the staged run's), rounds end on even records except the last.
-            while (ebase < n && RING - (wr - rd) >= 32) {
+            // produce: whole entries, in order, while the ring holds < RING_LOW records
+            while (ebase < n && wr - rd < RING_LOW) {
                 const int e = ebase + lane;
+#if FUSED_PREFETCH
+                const int4 en = pf_base == ebase ? en_pf : load_entry(e);
+#else
                 const int4 en = load_entry(e);
+#endif
                 const unsigned mx = (unsigned)en.y, my = (unsigned)en.z;
-                int cnt = e < n ? (mx ? 1 : 0) + (my ? wr_pcount(en.w) : 0) : 0;
-                if (lane == 0) cnt -= eoff;
+                const int hasnode = mx ? 1 : 0;
+                const int pc = my ? wr_pcount(en.w) : 0;
+                const int cnt = hasnode + pc;
                 int incl = cnt;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const int t = __shfl_up_sync(0xffffffffu, incl, o);
                     if (lane >= o) incl += t;
                 }
-                const int total = __shfl_sync(0xffffffffu, incl, 31);
-                const int start = incl - cnt;
-                int P = min(ROUND, min(total, RING - (wr - rd)));
-                const bool last = P == total && ebase + 32 >= n;  // the stream's final records
-                if (!last) P &= ~1;
-                const unsigned blo = __reduce_or_sync(0xffffffffu, (cnt > 0 && start < 32) ? (1u << start) : 0u);
-                const unsigned bhi =
-                    __reduce_or_sync(0xffffffffu, (cnt > 0 && start >= 32 && start < 64) ? (1u << (start - 32)) : 0u);
-                const unsigned long long starts = (unsigned long long)blo | ((unsigned long long)bhi << 32);
-                float4 rv[2];
-                unsigned mv[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int r = 2 * lane + h;
-                    const int j = max(__popcll(starts & ((2ull << r) - 1ull)) - 1, 0);  // entry of record r
-                    const int x = __shfl_sync(0xffffffffu, en.x, j);
-                    const unsigned mxj = __shfl_sync(0xffffffffu, mx, j), myj = __shfl_sync(0xffffffffu, my, j);
-                    const int wj = __shfl_sync(0xffffffffu, en.w, j);
-                    const int sj = __shfl_sync(0xffffffffu, start, j);
-                    const int k = r - sj + (j == 0 ? eoff : 0);  // record k of entry j
-                    const bool isnode = mxj != 0u && k == 0;
-                    float4 q = make_float4(0.f, 0.f, 0.f, 0.f), l = q;
-                    if (r < P) {
-                        q = isnode ? rec_hi[x] : parts[wr_pstart(wj) + k - (mxj ? 1 : 0)];
-                        if (isnode) l = rec_lo[x];
+                const bool take = e < n && incl <= RING - (wr - rd);
+                const unsigned tm = __ballot_sync(0xffffffffu, take);
+                const int ntake = __popc(tm);  // incl is nondecreasing: the taken lanes are a prefix
+                const int total = ntake ? __shfl_sync(0xffffffffu, incl, ntake - 1) : 0;
+                if (take) {
+                    const int r = wr + incl - cnt;
+                    if (mx) {
+#if FUSED_PREFETCH > 1
+                        const bool pre = pf_base == ebase;
+                        const float4 h = pre ? h_pf : rec_hi[en.x], l = pre ? l_pf : rec_lo[en.x];
+#else
+                        const float4 h = rec_hi[en.x], l = rec_lo[en.x];
+#endif
+                        put(r, (h.x - F.cx) + l.x, (h.y - F.cy) + l.y, (h.z - F.cz) + l.z, h.w, mx);
                     }
-                    rv[h] = make_float4((q.x - F.cx) + l.x, (q.y - F.cy) + l.y, (q.z - F.cz) + l.z, q.w);
-                    mv[h] = isnode ? mxj : myj;
+                    const float4 *src = parts + wr_pstart(en.w);
+                    for (int k = 0; k < pc; ++k) {
+                        const float4 q = src[k];
+                        put(r + hasnode + k, q.x - F.cx, q.y - F.cy, q.z - F.cz, q.w, my);
+                    }
                 }
-                const int q0 = (wr + 2 * lane) & (RING - 1);  // wr is even here
-                if (2 * lane + 1 < P) {
-                    r_a[warp][q0 >> 1] = make_float4(rv[0].x, rv[1].x, rv[0].y, rv[1].y);
-                    r_b[warp][q0 >> 1] = make_float4(rv[0].z, rv[1].z, rv[0].w, rv[1].w);
-                    *reinterpret_cast<uint2 *>(rm + q0) = make_uint2(mv[0], mv[1]);
-                } else if (2 * lane < P) {
-                    put(wr + 2 * lane, rv[0].x, rv[0].y, rv[0].z, rv[0].w, mv[0]);
-                }
-                wr += P;
-                // advance the cursor past the P records made
-                if (P == total) {
-                    ebase = min(n, ebase + 32);
-                    eoff = 0;
-                } else {
-                    const int jj = __popc(__ballot_sync(0xffffffffu, e < n && start <= P)) - 1;
-                    const int sjj = __shfl_sync(0xffffffffu, start, jj);
-                    eoff = P - sjj + (jj == 0 ? eoff : 0);
-                    ebase += jj;
-                }
+                wr += total;
+                ebase += ntake;
                 if (ebase / CHUNK != cur_ci && ebase < n) {  // moved into the next chunk of the chain
                     chunk_cur = chunk_nxt;
                     cur_ci = ebase / CHUNK;
                     chunk_nxt = ((cur_ci + 1) * CHUNK < n) ? ld_list<OVL>(U.cnext + chunk_cur) : 0;
                 }
             }
+#if FUSED_PREFETCH
+            if (ebase < n) {  // the next batch's entries load while this one is consumed
+                en_pf = load_entry(ebase + lane);
+                pf_base = ebase;
+#if FUSED_PREFETCH > 1
+                if (en_pf.y) {
+                    h_pf = rec_hi[en_pf.x];
+                    l_pf = rec_lo[en_pf.x];
+                }
+#endif
+            }
+#endif
             if (ebase >= n && wr - rd < PFLUSH && wr > rd) {  // end of the run: pad the last group
                 const int padded = (wr + PFLUSH - 1) & ~(PFLUSH - 1);
                 if (wr + lane < padded) put(wr + lane, 0.f, 0.f, 0.f, 0.f, 0u);

@@ -28,6 +28,7 @@
 
 #include "bh_state.h"
 #include "common.cuh"
+#include "dm_state.h"
 #include "ewald.cuh"
 
 namespace gc {
@@ -171,7 +172,7 @@ __global__ void dm_iota(int n, int *p)
 // so a node interaction reads the first two float4 and a particle
 // interaction the bucket's particles, both from the member's address map.
 // ---------------------------------------------------------------------------
-__global__ void dm_stage_bh_kernel(int nt, const int *__restrict__ transfer, int redundant,
+__global__ void dm_stage_bh_kernel(int nt, const int *__restrict__ nt_dev, const int *__restrict__ transfer, int redundant,
                                    const int *__restrict__ slot_of, int slot_f4, const float4 *__restrict__ recs,
                                    const float4 *__restrict__ rec_hi, const float4 *__restrict__ rec_lo,
                                    const int2 *__restrict__ prange,
@@ -179,7 +180,7 @@ __global__ void dm_stage_bh_kernel(int nt, const int *__restrict__ transfer, int
 {
     const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (k >= nt) return;
+    if (k >= (nt_dev ? *nt_dev : nt)) return;  // async plans: the count lives on the device
     const int b = transfer[k];
     const int slot = redundant ? k : slot_of[b];
     float4 *dst = pool + (int64_t)slot * slot_f4;
@@ -190,7 +191,7 @@ __global__ void dm_stage_bh_kernel(int nt, const int *__restrict__ transfer, int
         float4 l = rec_lo[b];
         l.w = __int_as_float(min(pc, slot_f4 - 2));
         dst[1] = l;
-        if (pc > slot_f4 - 2) atomicOr(bad, 1);
+        if (pc > slot_f4 - 2) atomicOr(bad, 2);
     }
     for (int i = lane; i < min(pc, slot_f4 - 2); i += 32) dst[2 + i] = parts[pr.x + i];
 }
@@ -303,6 +304,77 @@ ewald_slot_kernel(int nmember, const int *__restrict__ member_bucket, const int 
     }
 }
 
+// --- asynchronous plans (device batcher): counts stay on the device -------
+__global__ void dm_set_int(int *p, int v) { *p = v; }
+
+__global__ void dm_unpin_dev(int n, const int *__restrict__ cnt, const int *__restrict__ distinct, int *__restrict__ pins)
+{
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= n || d >= cnt[0]) return;
+    const int b = distinct[d];
+    pins[b] = max(pins[b] - 1, 0);
+}
+
+// cnt = [distinct D, missing K, free slots, error flags]
+__global__ void dm_lookup_pin_dev(int n, const int *__restrict__ cnt, const int *__restrict__ distinct,
+                                  const int *__restrict__ slot_of, double *__restrict__ last_use,
+                                  int *__restrict__ pins, double now, unsigned char *__restrict__ miss)
+{
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= n) return;
+    if (d >= cnt[0]) {
+        miss[d] = 0;
+        return;
+    }
+    const int b = distinct[d];
+    const bool res = slot_of[b] >= 0;
+    if (res) last_use[b] = now;
+    miss[d] = !res;
+    pins[b] += 1;  // distinct ids: no races
+}
+
+__global__ void dm_pad_tail(int n, const int *__restrict__ cnt, int *__restrict__ a)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && i >= cnt[1]) a[i] = INT_MAX;
+}
+
+__global__ void dm_alloc_dev(int n, int *__restrict__ cnt, const int *__restrict__ missing,
+                             const int *__restrict__ free_slots, int *__restrict__ slot_of,
+                             int *__restrict__ buf_of_slot, double *__restrict__ last_use, double now)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = cnt[1];
+    if (i == 0) {
+        if (k > cnt[2]) atomicOr(&cnt[3], 1);  // more missing buffers than free slots (cannot happen without eviction)
+        cnt[2] -= k;
+    }
+    if (i >= k || i >= n) return;
+    const int b = missing[i], s = free_slots[i];
+    slot_of[b] = s;
+    buf_of_slot[s] = b;
+    last_use[b] = now;
+}
+
+// row[0] += K (or P for REDUNDANT), row[1] += mult * sum of member transactions
+__global__ void dm_batch_row(const int *__restrict__ cnt, int np_redundant, const int *__restrict__ tx, int m, int mult,
+                             long long *__restrict__ row)
+{
+    __shared__ long long part[256];
+    long long t = 0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) t += tx[i];
+    part[threadIdx.x] = t;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) part[threadIdx.x] += part[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        row[0] += cnt ? cnt[1] : np_redundant;
+        row[1] += part[0] * mult;
+    }
+}
+
 void dm_kernel_spec(const char *cls, int64_t out[5])
 {
     // "ewald_member": ewald_slot_kernel; "force_slot": the member kernel
@@ -323,32 +395,6 @@ void dm_kernel_spec(const char *cls, int64_t out[5])
 
 using namespace gc;
 
-struct gc_dm {
-    gc_ctx *ctx = nullptr;
-    int64_t capacity = 0, slot_bytes = 0;
-    int mode = 2;  // 0 redundant, 1 reuse, 2 reuse_sorted (MemoryMode, memory.py:30-33)
-    int nslots = 0;
-    int64_t free_slots = 0;
-    int64_t universe = 0;
-    DBuf<int> slot_of, pins, firstpos, buf_of_slot;
-    DBuf<double> last_use;
-    // plan scratch / outputs
-    DBuf<int> ids, sorted_ids, bounds, member_of, distinct, missing, missing_sorted, cand, cand_s, cand_v,
-        free_list, addr, runflag, members_tx, iota_slots, nsel;
-    DBuf<unsigned char> flag;
-    DBuf<unsigned long long> tkeys, tkeys_s;
-    DBuf<float4> pool;  // staged payloads, slot_bytes per slot
-    // the last plan's transfer list on the device (REDUNDANT: position p -> slot p)
-    const int *last_transfer = nullptr;
-    int last_nt = 0;
-    bool last_redundant = false;
-    DBuf<int> members;  // combined request: member buckets
-    DBuf<signed char> kinds;  // per plan position: 0 node record, 1 bucket particles
-    // last plan (host copies)
-    std::vector<int64_t> h_transfer, h_addr, h_tx, h_bounds, h_evicted;
-    int64_t total_bytes = 0, indirection_bytes = 0;
-    bool indirect = true;
-};
 
 namespace {
 
@@ -495,6 +541,210 @@ void member_transactions(gc_dm *dm, int P, int M, int mult)
 
 }  // namespace
 
+namespace gc {
+
+void dm_grow_universe(gc_dm *dm, int64_t maxid) { ensure_universe(dm, std::max<int64_t>(maxid, 0)); }
+
+// Size every asynchronous-plan buffer (and the context's cub scratch) for
+// batches of up to P positions / M members up front: a plan then never
+// reallocates (cudaFree / cudaMalloc would serialise the host with the device).
+void dm_reserve(gc_dm *dm, int64_t P, int64_t M)
+{
+    const size_t p = (size_t)std::max<int64_t>(P, 1), m = (size_t)std::max<int64_t>(M, 1);
+    const size_t ns = (size_t)dm->nslots;
+    auto res = [](auto &b, size_t n) {
+        const size_t keep = b.n;
+        b.resize(std::max(n, keep));
+        b.n = keep;
+    };
+    res(dm->addr, p);
+    res(dm->kinds_s, p);
+    res(dm->flag, std::max(p, ns));
+    res(dm->distinct, p);
+    res(dm->missing, p);
+    res(dm->missing_sorted, p);
+    res(dm->sorted_ids, p);
+    res(dm->runflag, p);
+    res(dm->members_tx, m);
+    res(dm->free_list, ns);
+    res(dm->iota_slots, ns);
+    res(dm->nsel, 1);
+    if (dm->dcnt.n < 4) {
+        dm->dcnt.resize(4);
+        dm->dcnt.zero(dm->ctx->stream);
+    }
+    // cub temporary storage of the largest calls of a plan
+    gc_ctx *ctx = dm->ctx;
+    size_t need = 0, b = 0;
+    const int Pi = (int)p, Mi = (int)m;
+    GC_CUDA(cub::DeviceSelect::Flagged(nullptr, b, (const int *)nullptr, (const unsigned char *)nullptr, (int *)nullptr,
+                                       (int *)nullptr, std::max<int>(Pi, (int)ns)));
+    need = std::max(need, b);
+    GC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b, (const int *)nullptr, (int *)nullptr, Pi, 0, 32));
+    need = std::max(need, b);
+    GC_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, b, (const int *)nullptr, (int *)nullptr,
+                                                (const signed char *)nullptr, (signed char *)nullptr, Pi, Mi,
+                                                (const int *)nullptr, (const int *)nullptr));
+    need = std::max(need, b);
+    GC_CUDA(cub::DeviceSegmentedReduce::Sum(nullptr, b, (const int *)nullptr, (int *)nullptr, Mi, (const int *)nullptr,
+                                            (const int *)nullptr));
+    need = std::max(need, b);
+    if (ctx->scratch.cap < need) {
+        const size_t keep = ctx->scratch.n;
+        ctx->scratch.resize(need);
+        ctx->scratch.n = keep;
+    }
+}
+
+void dm_refresh_free(gc_dm *dm)
+{
+    if (!dm->free_stale) return;
+    int c[4];
+    dm->dcnt.download(c, 4, dm->ctx->stream);
+    GC_CUDA(cudaStreamSynchronize(dm->ctx->stream));
+    dm->free_slots = c[2];
+    dm->free_stale = false;
+}
+
+int dm_async_errors(gc_dm *dm)
+{
+    if (dm->dcnt.n < 4) return 0;
+    int c[4];
+    dm->dcnt.download(c, 4, dm->ctx->stream);
+    GC_CUDA(cudaStreamSynchronize(dm->ctx->stream));
+    if (c[3]) dm_set_int<<<1, 1, 0, dm->ctx->stream>>>(dm->dcnt.p + 3, 0);
+    return c[3];
+}
+
+bool dm_plan_async(gc_dm *dm, const int *ids, const signed char *kinds, int P, const int *bounds,
+                   const int *member_of, int M, int64_t max_id, double now, long long *row)
+{
+    gc_ctx *ctx = dm->ctx;
+    cudaStream_t s = ctx->stream;
+    if (dm->mode != 0 && max_id + 1 > dm->nslots) return false;  // an eviction may be needed: synchronous path
+    GC_REQUIRE(dm->mode != 0 || P <= dm->nslots, GC_E_CAPACITY,
+               "staging " + std::to_string(P) + " buffers exceeds " + std::to_string(dm->nslots) + " slots");
+    ensure_universe(dm, std::max<int64_t>(max_id, 0));
+    if (dm->dcnt.n < 4) {
+        dm->dcnt.resize(4);
+        dm->dcnt.zero(s);
+    }
+    if (!dm->free_stale) {  // the device takes over the free-slot count
+        dm_set_int<<<1, 1, 0, s>>>(dm->dcnt.p + 2, (int)dm->free_slots);
+        dm->free_stale = true;
+    }
+    int *cnt = dm->dcnt.p;
+    dm->addr.resize(std::max(P, 1));
+    dm->kinds_s.resize(std::max(P, 1));
+    dm->h_bounds.clear();  // the host copies describe synchronous plans only
+    const int *src = ids;
+    const signed char *ksrc = kinds;
+    if (dm->mode == 0) {  // REDUNDANT (memory.py:302-317): every position its own slot
+        dm_iota<<<grid_for(P, DM_TPB), DM_TPB, 0, s>>>(P, dm->addr.p);
+        GC_CUDA(cudaMemcpyAsync(dm->kinds_s.p, kinds, P, cudaMemcpyDeviceToDevice, s));
+        dm->last_transfer = ids;
+        dm->last_nt = P;
+        dm->last_redundant = true;
+    } else {
+        const int U = (int)std::min<int64_t>(P, max_id + 1);  // distinct ids <= the id range
+        dm->flag.resize(std::max(P, dm->nslots));
+        dm->distinct.resize(std::max(P, 1));
+        dm->missing.resize(std::max(U, 1));
+        dm_firstpos<<<grid_for(P, DM_TPB), DM_TPB, 0, s>>>(P, ids, dm->firstpos.p);
+        dm_isfirst<<<grid_for(P, DM_TPB), DM_TPB, 0, s>>>(P, ids, dm->firstpos.p, dm->flag.p);
+        dm_reset_firstpos<<<grid_for(P, DM_TPB), DM_TPB, 0, s>>>(P, ids, dm->firstpos.p);
+        cub_call(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceSelect::Flagged(t, b, ids, dm->flag.p, dm->distinct.p, cnt + 0, P, s);
+        });
+        dm_lookup_pin_dev<<<grid_for(U, DM_TPB), DM_TPB, 0, s>>>(U, cnt, dm->distinct.p, dm->slot_of.p, dm->last_use.p,
+                                                                 dm->pins.p, now, dm->flag.p);
+        cub_call(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceSelect::Flagged(t, b, dm->distinct.p, dm->flag.p, dm->missing.p, cnt + 1, U, s);
+        });
+        int *miss = dm->missing.p;
+        if (dm->mode == 2 && U > 1) {  // missing in ascending id (memory.py:329-330); the tail sorts last
+            dm_pad_tail<<<grid_for(U, DM_TPB), DM_TPB, 0, s>>>(U, cnt, dm->missing.p);
+            dm->missing_sorted.resize(U);
+            cub_call(ctx, [&](void *t, size_t &b) {
+                return cub::DeviceRadixSort::SortKeys(t, b, dm->missing.p, dm->missing_sorted.p, U, 0, 32, s);
+            });
+            miss = dm->missing_sorted.p;
+        }
+        // k-th missing buffer <- k-th smallest free slot (no eviction: every id fits)
+        dm->free_list.resize(dm->nslots);
+        dm->iota_slots.resize(dm->nslots);
+        dm->nsel.resize(1);
+        dm_iota<<<grid_for(dm->nslots, DM_TPB), DM_TPB, 0, s>>>(dm->nslots, dm->iota_slots.p);
+        dm_free_flags<<<grid_for(dm->nslots, DM_TPB), DM_TPB, 0, s>>>(dm->nslots, dm->buf_of_slot.p, dm->flag.p);
+        cub_call(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceSelect::Flagged(t, b, dm->iota_slots.p, dm->flag.p, dm->free_list.p, dm->nsel.p,
+                                              dm->nslots, s);
+        });
+        dm_alloc_dev<<<grid_for(std::max(U, 1), DM_TPB), DM_TPB, 0, s>>>(U, cnt, miss, dm->free_list.p, dm->slot_of.p,
+                                                                         dm->buf_of_slot.p, dm->last_use.p, now);
+        if (dm->mode == 2 && P) {  // per-member address maps sorted by id (memory.py:342-347), kinds alongside
+            dm->sorted_ids.resize(P);
+            cub_call(ctx, [&](void *t, size_t &b) {
+                return cub::DeviceSegmentedSort::SortPairs(t, b, ids, dm->sorted_ids.p, kinds, dm->kinds_s.p, P, M,
+                                                           bounds, bounds + 1, s);
+            });
+            src = dm->sorted_ids.p;
+            ksrc = dm->kinds_s.p;
+        } else if (P) {
+            GC_CUDA(cudaMemcpyAsync(dm->kinds_s.p, kinds, P, cudaMemcpyDeviceToDevice, s));
+        }
+        if (P) dm_addresses<<<grid_for(P, DM_TPB), DM_TPB, 0, s>>>(P, src, dm->slot_of.p, dm->addr.p);
+        dm->last_transfer = miss;
+        dm->last_nt = U;  // upper bound; the stage kernel reads K from cnt[1]
+        dm->last_redundant = false;
+    }
+    (void)ksrc;
+    // transactions (memory.py:190-225): runs per 16-lane group, x2 when indirect
+    dm->members_tx.resize(std::max(M, 1));
+    if (P) {
+        dm->runflag.resize(P);
+        dm_run_flags<<<grid_for(P, DM_TPB), DM_TPB, 0, s>>>(P, dm->addr.p, member_of, bounds, dm->runflag.p);
+        cub_call(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceSegmentedReduce::Sum(t, b, dm->runflag.p, dm->members_tx.p, M, bounds, bounds + 1, s);
+        });
+    }
+    dm_batch_row<<<1, 256, 0, s>>>(dm->mode == 0 ? nullptr : cnt, P, dm->members_tx.p, P ? M : 0,
+                                   dm->mode == 0 ? 1 : 2, row);
+    check_launch("dm_plan_async");
+    return true;
+}
+
+void dm_members_async(gc_dm *dm, gc_bh *bh, const int *members, int M, const int *bounds, int P, double g, double eps)
+{
+    cudaStream_t s = dm->ctx->stream;
+    const int slot_f4 = (int)(dm->slot_bytes / 16);
+    GC_REQUIRE(slot_f4 >= 3, GC_E_VALUE, "slot too small for a node record and a particle");
+    if (dm->pool.n == 0) {
+        dm->pool.resize((size_t)dm->nslots * slot_f4);
+        dm->pool.zero(s);
+    }
+    if (dm->last_nt > 0)
+        dm_stage_bh_kernel<<<grid_for(dm->last_nt, 8), 256, 0, s>>>(
+            dm->last_nt, dm->last_redundant ? nullptr : dm->dcnt.p + 1, dm->last_transfer, dm->last_redundant,
+            dm->slot_of.p, slot_f4, bh->d_recs.p, bh->d_rec_hi.p, bh->d_rec_lo.p, bh->d_prange.p, bh->d_parts.p,
+            dm->pool.p, dm->dcnt.p + 3);
+    bh->d_out.resize(bh->n * bh->dim);
+    const float eps2 = (float)(eps * eps);
+    if (M > 0) {
+        auto k = bh_use_cube(eps2) ? force_slot_kernel<true> : force_slot_kernel<false>;
+        k<<<grid_for(M, 8), 256, 0, s>>>(M, members, bounds, dm->addr.p, dm->kinds_s.p, bh->d_brange.p, bh->d_parts.p,
+                                        bh->d_porder.p, dm->pool.p, slot_f4, eps2, g, bh->dim, bh->d_out.p);
+    }
+    if (!dm->last_redundant) {  // release_batch (memory.py:362-369): unpin the plan's distinct buffers
+        const int U = dm->last_nt;
+        if (U > 0) dm_unpin_dev<<<grid_for(U, DM_TPB), DM_TPB, 0, s>>>(U, dm->dcnt.p, dm->distinct.p, dm->pins.p);
+    }
+    check_launch("dm_members_async");
+    (void)P;
+}
+
+}  // namespace gc
+
 extern "C" {
 
 gc_status gc_dm_create(gc_ctx *ctx, int64_t capacity_bytes, int64_t slot_bytes, int32_t mode, gc_dm **out)
@@ -555,6 +805,7 @@ gc_status gc_dm_build_plan(gc_dm *dm, const int64_t *ids, const int64_t *bounds,
             dm->indirect = false;
             member_transactions(dm, P, M, 1);
         } else {  // REUSE / REUSE_SORTED (memory.py:319-360)
+            dm_refresh_free(dm);
             const int D = dedup(dm, P);
             dm->missing.resize(std::max(D, 1));
             dm->flag.resize(std::max(D, 1));
@@ -682,6 +933,7 @@ gc_status gc_dm_evict(gc_dm *dm, int64_t needed_bytes, int64_t *evicted, int64_t
     return guard([&] {
         GC_REQUIRE(dm && n_evicted, GC_E_VALUE, "null argument");
         *n_evicted = 0;
+        dm_refresh_free(dm);
         GC_REQUIRE(needed_bytes <= dm->capacity, GC_E_CAPACITY,
                    "request of " + std::to_string(needed_bytes) + " bytes exceeds capacity " +
                        std::to_string(dm->capacity));
@@ -703,6 +955,7 @@ gc_status gc_dm_evict(gc_dm *dm, int64_t needed_bytes, int64_t *evicted, int64_t
 gc_status gc_dm_state(gc_dm *dm, int64_t out[4])
 {
     return guard([&] {
+        dm_refresh_free(dm);
         out[0] = dm->nslots;
         out[1] = dm->free_slots;
         out[2] = dm->nslots - dm->free_slots;
@@ -768,7 +1021,7 @@ gc_status gc_dm_stage_bh(gc_dm *dm, gc_bh *bh)
         GC_CUDA(cudaEventRecord(bh->ev[0], s));  // staging time -> gc_bh_timings out[0]
         if (dm->last_nt > 0)
             dm_stage_bh_kernel<<<grid_for(dm->last_nt, 8), 256, 0, s>>>(
-                dm->last_nt, dm->last_transfer, dm->last_redundant, dm->slot_of.p, slot_f4, bh->d_recs.p, bh->d_rec_hi.p,
+                dm->last_nt, nullptr, dm->last_transfer, dm->last_redundant, dm->slot_of.p, slot_f4, bh->d_recs.p, bh->d_rec_hi.p,
                 bh->d_rec_lo.p, bh->d_prange.p, bh->d_parts.p, dm->pool.p, dm->nsel.p);
         check_launch("dm_stage_bh_kernel");
         GC_CUDA(cudaEventRecord(bh->ev[1], s));

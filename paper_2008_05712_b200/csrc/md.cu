@@ -33,6 +33,9 @@ constexpr int MD_TPB = 128;
 #ifndef MD_LJ_FAST
 #define MD_LJ_FAST 1
 #endif
+#ifndef MD_LJ_COLUMN
+#define MD_LJ_COLUMN 1
+#endif
 
 enum { LAW_SOFT = 0, LAW_LJ = 1 };
 
@@ -674,6 +677,335 @@ md_lj3_kernel(const double4 *__restrict__ spos, const int *__restrict__ sidx, co
     }
 }
 
+// ---------------------------------------------------------------------------
+// 3-D Lennard-Jones COLUMN kernel (the default throughput path for grids of
+// at least 3 cells per dimension).  One block per column of KZ home cells
+// along z: the 3 x 3 x (KZ + 2) neighbour region is staged once for all
+// KZ x ~13.5 home atoms (half the staging of one block per cell); every
+// region cell starts at an even slot (a far-away pad fills odd cells), so a
+// home atom's 27 neighbour cells are 9 pair-aligned slot runs.
+//   thread = (home atom, part): PARTS = 256 / next power of two of the home
+//            count; part p takes a contiguous share of every run's slot pairs;
+//   filter:  float32 r^2 against the widened cutoff band, two candidates per
+//            step (FADD2 / FFMA2); survivors are appended straight to the
+//            thread's shared-memory list (no bit masks);
+//   pairs:   one pass over the list in float64 from the image-shifted staged
+//            positions: pairs well inside the cutoff take the force law in the
+//            home atom's orientation (reciprocal from a float seed + one Newton
+//            step); pairs at the cutoff (or coincident) take the reference's
+//            canonical orientation and cutoff test (md_pair_exact, bit for
+//            bit); parts are summed by shuffles in fixed order (deterministic:
+//            slab runs are bit-identical to the whole domain).
+// ---------------------------------------------------------------------------
+constexpr int MDK_KZ = 4;  // home cells per column block
+constexpr int MDK_THREADS = 256;
+constexpr int MDK_NR = 9 * (MDK_KZ + 2);  // region cells
+constexpr int MDK_NB = 1024;  // staged region slots incl. pads (overflow -> exact scan from global memory)
+constexpr int MDK_LIST = 48;  // survivors per thread (overflow -> the thread rescans its candidates exactly)
+constexpr int MDK_HOMES = 256;  // home atoms per pass
+constexpr int MDK_SMEM = MDK_NB * 32 + MDK_LIST * MDK_THREADS * 2 + (MDK_NB / 2) * 24 + MDK_NB + MDK_HOMES * 2;
+
+__global__ void __launch_bounds__(MDK_THREADS, 3)
+md_lj3c_kernel(const double4 *__restrict__ spos, const int *__restrict__ sidx, const int *__restrict__ cell_start,
+               const MDParams P, float band, int ncol_z, double4 *__restrict__ out)
+{
+    // dynamic shared memory (MDK_SMEM bytes)
+    extern __shared__ __align__(16) unsigned char mdk_smem[];
+    double4 *nbs = reinterpret_cast<double4 *>(mdk_smem);  // [NB] image-shifted float64 position, w = global id bits
+    unsigned short *lst = reinterpret_cast<unsigned short *>(nbs + MDK_NB);  // [LIST][THREADS] survivor slots
+    float4 *nba = reinterpret_cast<float4 *>(lst + MDK_LIST * MDK_THREADS);  // [NB/2] pairs x0 x1 y0 y1 (region frame)
+    float2 *nbz = reinterpret_cast<float2 *>(nba + MDK_NB / 2);  // [NB/2] pairs z0 z1
+    unsigned char *nbc = reinterpret_cast<unsigned char *>(nbz + MDK_NB / 2);  // [NB] region cell of the slot
+    unsigned short *hslot = reinterpret_cast<unsigned short *>(nbc + MDK_NB);  // [HOMES] home atoms' slots
+    __shared__ int pre[MDK_NR + 1], qst[MDK_NR], pop[MDK_NR];
+    __shared__ double4 shtab[MDK_NR];  // image shift of the region cell
+    __shared__ int pfx[MDK_THREADS];  // inclusive prefix of the list lengths over a home's parts
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // column: home cells (cx, cy, cz0 .. cz0 + kz - 1)
+    const int col = blockIdx.x;
+    const int czb = col % ncol_z, cxy = col / ncol_z;
+    const int cy = cxy % P.ny, cx = cxy / P.ny + (P.slab ? 1 : 0);  // slabs: owned x planes only
+    const int cz0 = czb * MDK_KZ, kz = min(MDK_KZ, P.nz - cz0);
+    constexpr int RZ = MDK_KZ + 2;
+    if (tid < MDK_NR) {
+        const int dxy = tid / RZ, dz = tid - dxy * RZ;
+        const int ox = dxy / 3 - 1, oy = dxy - 3 * (dxy / 3) - 1;
+        int qx = cx + ox, qy = cy + oy, qz = cz0 - 1 + dz;
+        bool ok = dz <= kz + 1;
+        double sy = 0.0, sz = 0.0;
+        if (qx < 0 || qx >= P.nx) {
+            ok = ok && P.periodic && !P.slab;
+            qx = qx < 0 ? qx + P.nx : qx - P.nx;
+        }
+        if (qy < 0) { ok = ok && P.periodic; qy += P.ny; sy = -P.by; }
+        else if (qy >= P.ny) { ok = ok && P.periodic; qy -= P.ny; sy = P.by; }
+        if (qz < 0) { ok = ok && P.periodic; qz += P.nz; sz = -P.bz; }
+        else if (qz >= P.nz) { ok = ok && P.periodic; qz -= P.nz; sz = P.bz; }
+        const int q = (qx * P.ny + qy) * P.nz + qz;
+        const int a0 = ok ? cell_start[q] : 0;
+        const int n = ok ? cell_start[q + 1] - a0 : 0;
+        qst[tid] = a0;
+        pop[tid] = n;
+        pre[tid + 1] = (n + 1) & ~1;  // even slot count per cell (pair-aligned runs)
+        shtab[tid] = make_double4(md_xshift(cx + ox, P), sy, sz, 0.0);
+    }
+    __syncthreads();
+    if (warp == 0) {  // inclusive scan of the padded populations (<= 64 cells: two per lane)
+        int v0 = lane < MDK_NR ? pre[lane + 1] : 0;
+        int v1 = lane + 32 < MDK_NR ? pre[lane + 33] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t0 = __shfl_up_sync(0xffffffffu, v0, o), t1 = __shfl_up_sync(0xffffffffu, v1, o);
+            if (lane >= o) {
+                v0 += t0;
+                v1 += t1;
+            }
+        }
+        v1 += __shfl_sync(0xffffffffu, v0, 31);
+        if (lane < MDK_NR) pre[lane + 1] = v0;
+        if (lane + 32 < MDK_NR) pre[lane + 33] = v1;
+        if (lane == 0) pre[0] = 0;
+    }
+    __syncthreads();
+    const int nnb = pre[MDK_NR];
+    const int hr0 = 4 * RZ + 1;  // home cells are region cells (1, 1, 1 .. kz)
+    int nh = 0;
+    for (int r = hr0; r < hr0 + kz; ++r) nh += pop[r];
+    const double orx = (cx - 1) * P.cell, ory = (cy - 1) * P.cell, orz = (cz0 - 1) * P.cell;
+    if (nnb > MDK_NB || nh > MDK_HOMES) {  // staging overflow (pathological density): exact scan from global memory
+        for (int r = hr0; r < hr0 + kz; ++r) {
+            const int hz = r - 4 * RZ;
+            for (int i = tid; i < pop[r]; i += MDK_THREADS) {
+                const int j0 = qst[r] + i;
+                const double4 a = spos[j0];
+                const long long ia = __double_as_longlong(a.w);
+                double fx = 0.0, fy = 0.0, fz = 0.0, en = 0.0;
+                for (int rr = 0; rr < MDK_NR; ++rr) {
+                    const int dxy = rr / RZ, dz = rr - dxy * RZ;
+                    if (dz < hz - 1 || dz > hz + 1) continue;
+                    const int ox = dxy / 3 - 1, oy = dxy - 3 * (dxy / 3) - 1, oz = dz - hz;
+                    const double4 sh = shtab[rr];
+                    const double4 shf =
+                        make_double4(sh.x, sh.y, sh.z, (ox | oy | oz) == 0 ? 2.0 : (md_forward(ox, oy, oz) ? 1.0 : 0.0));
+                    for (int k = 0; k < pop[rr]; ++k) {
+                        const int j = qst[rr] + k;
+                        if (j != j0) md_pair_exact<LAW_LJ, 3>(a, ia, spos[j], shf, P, fx, fy, fz, en);
+                    }
+                }
+                out[sidx[j0]] = make_double4(fx, fy, fz, en);
+            }
+        }
+        return;
+    }
+    // staging: half-warp h copies region cells h, h + 16, ... (coalesced within a cell)
+    float *fa = reinterpret_cast<float *>(nba);
+    float *fzp = reinterpret_cast<float *>(nbz);
+    for (int r = tid >> 4; r < MDK_NR; r += MDK_THREADS / 16) {
+        const int n = pop[r], s0 = pre[r], np = pre[r + 1] - s0;
+        const double4 sh = shtab[r];
+        for (int j = tid & 15; j < np; j += 16) {
+            const int s = s0 + j;
+            const int o = (s >> 1) * 4 + (s & 1);
+            if (j < n) {
+                const double4 b = spos[qst[r] + j];
+                const double4 bs = make_double4(b.x + sh.x, b.y + sh.y, b.z + sh.z, b.w);
+                nbs[s] = bs;
+                fa[o] = (float)(bs.x - orx);
+                fa[o + 2] = (float)(bs.y - ory);
+                fzp[(s >> 1) * 2 + (s & 1)] = (float)(bs.z - orz);
+                if (r >= hr0 && r < hr0 + kz) {  // home atom: its slot, in slot order
+                    int hb = 0;
+                    for (int rr = hr0; rr < r; ++rr) hb += pop[rr];
+                    hslot[hb + j] = (unsigned short)s;
+                }
+            } else {  // pad slot: far away
+                fa[o] = 1e30f;
+                fa[o + 2] = 1e30f;
+                fzp[(s >> 1) * 2 + (s & 1)] = 1e30f;
+            }
+            nbc[s] = (unsigned char)r;
+        }
+    }
+    __syncthreads();
+    const double lo = P.c2 * (1.0 - 1e-12), hi = P.c2 * (1.0 + 1e-12);
+    const double e24 = 24.0 * P.eps, e2 = 2.0 * P.eps;
+    // PARTS = 256 / (next power of two >= nh), at most 16
+    int lgh = 4;
+    while ((1 << lgh) < nh) ++lgh;
+    const int lgp = 8 - lgh;
+    const int parts = 1 << lgp;
+    const int hi_ = tid >> lgp, part = tid & (parts - 1);
+    const bool act = hi_ < nh;
+    const int si = hslot[act ? hi_ : 0];
+    const int hr = nbc[si];
+    const int hz = hr - 4 * RZ;  // region z index of the home cell (1 .. kz)
+    const float xi = fa[(si >> 1) * 4 + (si & 1)], yi = fa[(si >> 1) * 4 + (si & 1) + 2],
+                zi = fzp[(si >> 1) * 2 + (si & 1)];
+    const float2 nx2 = make_float2(-xi, -xi), ny2 = make_float2(-yi, -yi), nz2 = make_float2(-zi, -zi);
+    const double4 a = nbs[si];
+    // filter: the 9 runs (dx, dy) x region z [hz - 1, hz + 1], each part a
+    // contiguous share of the pairs; a survivor is stored at the list end and
+    // the end advances (predicated, no branch) -- a run whose share could
+    // overflow the list takes the guarded loop
+    unsigned short *lp = lst + tid;
+    int cnt = 0;
+    if (act) {
+        for (int dxy = 0; dxy < 9; ++dxy) {
+            const int p0 = pre[dxy * RZ + hz - 1] >> 1, p1 = pre[dxy * RZ + hz + 2] >> 1;
+            const int len = p1 - p0;
+            const int c0 = p0 + (len * part >> lgp), c1 = p0 + (len * (part + 1) >> lgp);
+            if (cnt + 2 * (c1 - c0) <= MDK_LIST) {
+                int wo = cnt * MDK_THREADS + tid;  // element offset of the list end
+                const float4 *pa = nba + c0;
+                const float2 *pz = nbz + c0;
+                int s2 = 2 * c0;
+#pragma unroll 4
+                for (int k = 0; k < c1 - c0; ++k) {
+                    const float4 A = pa[k];
+                    const float2 Z = pz[k];
+                    const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nx2);
+                    const float2 dy = __fadd2_rn(make_float2(A.z, A.w), ny2);
+                    const float2 dz = __fadd2_rn(Z, nz2);
+                    float2 r2 = __fmul2_rn(dz, dz);
+                    r2 = __ffma2_rn(dy, dy, r2);
+                    r2 = __ffma2_rn(dx, dx, r2);
+                    if (r2.x < band) {
+                        lst[wo] = (unsigned short)s2;
+                        wo += MDK_THREADS;
+                    }
+                    if (r2.y < band) {
+                        lst[wo] = (unsigned short)(s2 + 1);
+                        wo += MDK_THREADS;
+                    }
+                    s2 += 2;
+                }
+                cnt = (wo - tid) / MDK_THREADS;
+            } else {
+                for (int pr = c0; pr < c1; ++pr) {
+                    const float4 A = nba[pr];
+                    const float2 Z = nbz[pr];
+                    const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nx2);
+                    const float2 dy = __fadd2_rn(make_float2(A.z, A.w), ny2);
+                    const float2 dz = __fadd2_rn(Z, nz2);
+                    float2 r2 = __fmul2_rn(dz, dz);
+                    r2 = __ffma2_rn(dy, dy, r2);
+                    r2 = __ffma2_rn(dx, dx, r2);
+                    if (r2.x < band) {
+                        if (cnt < MDK_LIST) lp[cnt * MDK_THREADS] = (unsigned short)(2 * pr);
+                        ++cnt;
+                    }
+                    if (r2.y < band) {
+                        if (cnt < MDK_LIST) lp[cnt * MDK_THREADS] = (unsigned short)(2 * pr + 1);
+                        ++cnt;
+                    }
+                }
+            }
+        }
+    }
+    // the home's survivors are re-dealt evenly over its parts (lists differ in
+    // length; the float64 loop runs the longest list of the warp): combined
+    // entry e = part + parts * i lives in the list of the part q whose prefix
+    // range contains e
+    const bool over = __any_sync(0xffffffffu, cnt > MDK_LIST);
+    const int mine = min(cnt, MDK_LIST);
+    int incl = mine;  // inclusive prefix over the parts of this home (lanes part 0 .. parts - 1)
+    for (int o = 1; o < parts; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (part >= o) incl += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, (lane & ~(parts - 1)) + parts - 1);
+    const int gbase = tid - part;  // list column of part 0 of this home
+    pfx[tid] = incl;
+    __syncwarp();
+    double fx = 0.0, fy = 0.0, fzz = 0.0, en = 0.0;
+    // the reference's own test (canonical orientation, md_pair_exact) for a
+    // pair at the cutoff or coincident -- rare; deferred out of the main loop
+    auto pair_exact = [&](int sl) {
+        if (sl == si) return;
+        const int r = nbc[sl];
+        const int dxy = r / RZ, dz = r - dxy * RZ;
+        const int ox = dxy / 3 - 1, oy = dxy - 3 * (dxy / 3) - 1, oz = dz - hz;
+        const double4 sh = shtab[r];
+        const double4 shf =
+            make_double4(sh.x, sh.y, sh.z, (ox | oy | oz) == 0 ? 2.0 : (md_forward(ox, oy, oz) ? 1.0 : 0.0));
+        const double4 b = spos[qst[r] + (sl - pre[r])];  // the unshifted position
+        const double4 ah = spos[qst[hr] + (si - pre[hr])];
+        md_pair_exact<LAW_LJ, 3>(ah, __double_as_longlong(ah.w), b, shf, P, fx, fy, fzz, en);
+    };
+    if (!over) {
+        unsigned long long defer = 0ull;  // list entries (bit = combined index / parts) for pair_exact
+        int ne = 0;
+        for (int e = part; e < total; e += parts, ++ne) {
+            int q = 0, base = 0;  // the part holding combined entry e, and its prefix start
+            for (int k = 0; k < parts - 1; ++k) {
+                const int ik = pfx[gbase + k];
+                if (e >= ik) {
+                    q = k + 1;
+                    base = ik;
+                }
+            }
+            const int sl = lst[(e - base) * MDK_THREADS + gbase + q];
+            const double4 bs = nbs[sl];
+            const double d0 = a.x - bs.x, d1 = a.y - bs.y, d2 = a.z - bs.z;
+            const double r2 = fma(d2, d2, fma(d1, d1, d0 * d0));
+            const bool exact = (r2 > lo && r2 < hi) || r2 < 1e-6;
+            if (exact) defer |= 1ull << ne;
+            // certain pairs: the force law in the home atom's orientation,
+            // reciprocal from a float seed + one Newton step (2^-46 relative)
+            double inv = (double)__frcp_rn((float)r2);
+            inv = fma(inv, fma(-r2, inv, 1.0), inv);
+            const double s2 = P.sig2 * inv;
+            const double s6 = s2 * s2 * s2;
+            const double s12 = s6 * s6;
+            const bool in = !exact && r2 < P.c2;
+            const double mag = in ? e24 * fma(2.0, s12, -s6) * inv : 0.0;
+            const double ep = fma(e2, s12 - s6, en);  // (inf - inf for the home atom itself: not taken)
+            en = in ? ep : en;
+            fx = fma(d0, mag, fx);
+            fy = fma(d1, mag, fy);
+            fzz = fma(d2, mag, fzz);
+        }
+        for (ne = 0; defer; defer >>= 1, ++ne) {
+            if (!(defer & 1ull)) continue;
+            const int e = part + ne * parts;
+            int q = 0, base = 0;
+            for (int k = 0; k < parts - 1; ++k) {
+                const int ik = pfx[gbase + k];
+                if (e >= ik) {
+                    q = k + 1;
+                    base = ik;
+                }
+            }
+            pair_exact(lst[(e - base) * MDK_THREADS + gbase + q]);
+        }
+    } else if (act) {  // a list overflowed in this warp: exact rescan of every thread's own share
+        const double4 ah = spos[qst[hr] + (si - pre[hr])];
+        const long long ia = __double_as_longlong(ah.w);
+        for (int dxy = 0; dxy < 9; ++dxy) {
+            const int p0 = pre[dxy * RZ + hz - 1] >> 1, p1 = pre[dxy * RZ + hz + 2] >> 1;
+            const int len = p1 - p0;
+            const int c0 = p0 + (len * part >> lgp), c1 = p0 + (len * (part + 1) >> lgp);
+            for (int sl = 2 * c0; sl < 2 * c1; ++sl) {
+                const int r = nbc[sl], k = sl - pre[r];
+                if (k >= pop[r] || sl == si) continue;  // pad slot / the home atom itself
+                const int dxy2 = r / RZ, dz = r - dxy2 * RZ;
+                const int ox = dxy2 / 3 - 1, oy = dxy2 - 3 * (dxy2 / 3) - 1, oz = dz - hz;
+                const double4 sh = shtab[r];
+                const double4 shf =
+                    make_double4(sh.x, sh.y, sh.z, (ox | oy | oz) == 0 ? 2.0 : (md_forward(ox, oy, oz) ? 1.0 : 0.0));
+                md_pair_exact<LAW_LJ, 3>(ah, ia, spos[qst[r] + k], shf, P, fx, fy, fzz, en);
+            }
+        }
+    }
+    for (int o = 1; o < parts; o <<= 1) {
+        fx += __shfl_xor_sync(0xffffffffu, fx, o);
+        fy += __shfl_xor_sync(0xffffffffu, fy, o);
+        fzz += __shfl_xor_sync(0xffffffffu, fzz, o);
+        en += __shfl_xor_sync(0xffffffffu, en, o);
+    }
+    if (act && part == 0) out[sidx[qst[hr] + (si - pre[hr])]] = make_double4(fx, fy, fzz, en);
+}
+
 // cell of every atom (unfused path)
 __global__ void md_assign_kernel(int n, const double4 *__restrict__ pos, const MDParams P, int use_npy,
                                  int *__restrict__ cell_of, int *__restrict__ count)
@@ -865,6 +1197,7 @@ struct gc_md {
     int use_npy = 0;  // reference 2-D patches use numpy floor_divide
     bool cell_path = true;  // block-per-cell kernel (false: thread-per-atom kernel)
     bool lj_fast = MD_LJ_FAST != 0;  // 3-D LJ: md_lj3_kernel (else md_cell_kernel)
+    bool lj_column = MD_LJ_COLUMN != 0;  // 3-D LJ: column blocks (md_lj3c_kernel) where the grid allows
     DBuf<double4> pos, vel, spos, force;  // pos/vel/gid/cell_of: owned atoms [0, n_owned), then ghosts
     DBuf<int> cell_of, scell, sidx, count, cell_start, perm;
     DBuf<long long> gid;  // global atom id (cell order, self-pair orientation)
@@ -933,6 +1266,22 @@ void md_cell_launch(gc_md *md, bool integ, double dt)
     const int blocks = md->P.slab ? (md->P.nx - 2) * md->P.ny * md->P.nz : md->ncell;  // home = owned cells
     if (blocks <= 0) return;
     if (LAW == LAW_LJ && DIM == 3 && !integ && md->lj_fast) {
+        if (md->lj_column && md->P.nx >= 3 && md->P.ny >= 3 && md->P.nz >= 3) {
+            // column blocks: the float32 coordinates span (KZ + 2) cells -> widen the band accordingly
+            const double extc = (MDK_KZ + 2) * md->P.cell;
+            const float bandc = (float)(md->P.c2 + 1e-5 * extc * extc + 1e-6);
+            const int ncz = (md->P.nz + MDK_KZ - 1) / MDK_KZ;
+            const int cols = (md->P.slab ? md->P.nx - 2 : md->P.nx) * md->P.ny * ncz;
+            static bool attr = false;
+            if (!attr) {
+                GC_CUDA(cudaFuncSetAttribute(md_lj3c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MDK_SMEM));
+                attr = true;
+            }
+            md_lj3c_kernel<<<cols, MDK_THREADS, MDK_SMEM, s>>>(md->spos.p, md->sidx.p, md->cell_start.p, md->P, bandc, ncz,
+                                                        md->force.p);
+            check_launch("md_lj3c_kernel");
+            return;
+        }
         md_lj3_kernel<<<blocks, MDL_THREADS, 0, s>>>(md->spos.p, md->sidx.p, md->cell_start.p, md->P, band,
                                                      md->force.p);
         check_launch("md_lj3_kernel");

@@ -33,6 +33,7 @@ order (hr/timeline.py:262-266).
 
 from __future__ import annotations
 
+import ctypes as C
 import time
 from dataclasses import dataclass, field
 
@@ -95,13 +96,81 @@ def plan_kinds(ptr, ids, kind, buckets, sorted_members: bool) -> np.ndarray:
     return np.ascontiguousarray(kd, dtype=np.int8)
 
 
+class DeviceBatcher:
+    """The device batcher of one kernel class (gc_batcher_*, csrc/batcher.cu):
+    vectorised submission into a device ring, the trigger of
+    hr/aggregator.py:41-110 (observe + poll at every arrival, size rule and
+    strict timeout rule), and per emitted batch the device data manager's plan,
+    the slot staging and one member-kernel launch -- all asynchronous; the
+    host synchronises once in ``log``."""
+
+    def __init__(self, tree, memory: DeviceMemory, max_size: int, timeout_factor: float = 2.0, window: int = 0,
+                 g: float = 1.0, eps: float = DEFAULT_SOFTENING):
+        self.tree, self.memory = tree, memory
+        self._ctx = L.context()
+        self.handle = C.c_void_p()
+        L.call("gc_batcher_create", self._ctx.handle, tree.handle, memory.handle, int(max_size),
+               float(timeout_factor), int(window), float(g), float(eps), C.byref(self.handle))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                L.load().gc_batcher_destroy(self.handle)
+        except Exception:
+            pass
+
+    def submit(self, owners, arrivals, ptr, ids, kinds) -> None:
+        owners, ptr, ids = L.i64(owners), L.i64(ptr), L.i64(ids)
+        arrivals = L.f64(arrivals)
+        kinds = np.ascontiguousarray(kinds, np.int8)
+        L.call("gc_batcher_submit", self.handle, len(owners), L.ptr(owners, L.i64p), L.ptr(arrivals, L.f64p),
+               L.ptr(ptr, L.i64p), L.ptr(ids, L.i64p), L.ptr(kinds, L.i8p))
+
+    def poll(self, now: float) -> None:
+        L.call("gc_batcher_poll", self.handle, float(now))
+
+    def flush(self, now: float) -> None:
+        L.call("gc_batcher_flush", self.handle, float(now))
+
+    def log(self):
+        """Synchronise; ScheduleLog rows: int64 (n, 7) {combined_id, first
+        request, members, positions, transferred, transactions, synchronous
+        plan} and float64 (n, 2) {emit time, device ms}."""
+        n = np.zeros(1, np.int64)
+        L.call("gc_batcher_sync", self.handle, L.ptr(n, L.i64p))
+        rows = np.zeros((int(n[0]), 7), np.int64)
+        times = np.zeros((int(n[0]), 2))
+        L.call("gc_batcher_log", self.handle, L.ptr(rows, L.i64p), L.ptr(times, L.f64p))
+        return rows, times
+
+    @staticmethod
+    def trigger_device(max_size: int, timeout_factor: float, window: int, arrivals=None, n: int | None = None,
+                       is_poll=None):
+        """The trigger alone, evaluated on the device: emissions (first
+        request, count, time) for events at `arrivals` (is_poll[i] != 0: a
+        poll, else an arrival), or for n arrivals stamped by %globaltimer."""
+        if arrivals is not None:
+            arrivals = L.f64(arrivals)
+            n = len(arrivals)
+        ip = None if is_poll is None else np.ascontiguousarray(is_poll, np.int8)
+        cap = max(int(n), 1)
+        f, c, t = np.zeros(cap, np.int64), np.zeros(cap, np.int64), np.zeros(cap)
+        ne = np.zeros(1, np.int64)
+        L.call("gc_batcher_trigger_device", int(max_size), float(timeout_factor), int(window), int(n),
+               None if arrivals is None else L.ptr(arrivals, L.f64p), None if ip is None else L.ptr(ip, L.i8p),
+               L.ptr(f, L.i64p), L.ptr(c, L.i64p),
+               L.ptr(t, L.f64p), L.ptr(ne, L.i64p))
+        k = int(ne[0])
+        return f[:k], c[:k], t[:k]
+
+
 class GpuForceExecutor:
     """Runs one BH force phase through the runtime API on the device."""
 
     def __init__(self, tree, lists, mode: MemoryMode = MemoryMode.REUSE_SORTED, capacity_bytes: int = 8 << 20,
                  slot_bytes: int = 256, g: float = 1.0, eps: float = DEFAULT_SOFTENING,
                  timeout_factor: float = 2.0, max_size: int | None = None, ewald=None,
-                 ewald_max_size: int | None = None):
+                 ewald_max_size: int | None = None, device_batcher: bool = True):
         self.tree = tree
         self.ptr, self.ids, self.kind, self.item_count = lists.csr()
         self.mode = mode
@@ -127,7 +196,8 @@ class GpuForceExecutor:
             self.runtime.register_group(self.states[c])
         self.state = self.states["force"]
         self._next_id = 0
-        self.plan_log = None  # set to a list to record every plan
+        self.plan_log = None  # set to a list to record every plan (host-driven path)
+        self.device_batcher = device_batcher  # the force class through gc_batcher (no ewald class, no plan log)
 
     # -- one combined launch (replaces Timeline._launch_gpu's cost model) ----------
     def _member_kinds(self, buckets) -> np.ndarray:
@@ -158,6 +228,31 @@ class GpuForceExecutor:
         return BatchRecord(combined.combined_id, len(members), npos, len(plan.to_transfer), plan.total_bytes,
                            plan.indirection_bytes, int(layout.total_transactions()), now, float(tm[0] + tm[1]), cls)
 
+    # -- the force phase through the device batcher -----------------------------------
+    def _run_device_batcher(self, times) -> RunResult:
+        nb = len(self.ptr) - 1
+        st = self.state
+        res = RunResult(forces=None)
+        t0 = time.perf_counter()
+        bat = DeviceBatcher(self.tree, self.memory, st.max_size, st.timeout_factor, st.window, self.g, self.eps)
+        self.runtime.submit_to_device("force", nb)
+        bat.submit(np.arange(nb), times, self.ptr, self.ids, self.kind)
+        bat.flush(float(times[-1]) if nb else 0.0)  # end of the phase (hr/timeline.py:276-298)
+        rows, tms = bat.log()
+        res.wall_s = time.perf_counter() - t0
+        indirect = self.mode is not MemoryMode.REDUNDANT
+        for r, t in zip(rows, tms):
+            res.batches.append(BatchRecord(self._next_id, int(r[2]), int(r[3]), int(r[4]),
+                                           int(r[4]) * self.memory.slot_bytes, 4 * int(r[3]) if indirect else 0,
+                                           int(r[5]), float(t[0]), float(t[1])))
+            self._next_id += 1
+            self.runtime.complete_on_device(int(r[2]))
+        self.batcher = bat
+        out = np.zeros((self.tree.n, self.tree.dim))
+        L.call("gc_bh_get_forces", self.tree.handle, L.ptr(out, L.f64p))
+        res.forces = out
+        return res
+
     # -- the force phase ------------------------------------------------------------
     def run(self, arrival_times=None) -> RunResult:
         """One work request per bucket (DFS order) at `arrival_times` (default:
@@ -166,6 +261,8 @@ class GpuForceExecutor:
         from .aggregator import make_combined
         nb = len(self.ptr) - 1
         times = np.zeros(nb) if arrival_times is None else np.asarray(arrival_times, float)
+        if self.device_batcher and self.ewald is None and self.plan_log is None:
+            return self._run_device_batcher(times)
         res = RunResult(forces=None)
         t0 = time.perf_counter()
         for b in range(nb):

@@ -118,3 +118,41 @@ def replay_forces(records, tree, lists, **executor_kw):
         if r.item_count != int(ex.item_count[b]):
             raise ValueError(f"trace record {b}: item_count {r.item_count} != {int(ex.item_count[b])}")
     return ex.run([r.arrival_time for r in force])
+
+
+# -- large streams (SURVEY.md §8f-2 at configs[2] / configs[3] scale) ------------
+# A text trace of the 1M-particle BH force phase would hold ~10^8 buffer ids
+# (hundreds of MB of text); the same records are kept in a compact binary
+# form: arrival times, the buffer CSR (ptr, ids), kinds and item counts.
+
+def dump_stream_npz(path, times, ptr, ids, item_count, kinds) -> None:
+    """One "force" record per bucket k: arrival times[k], buffers
+    ids[ptr[k]:ptr[k+1]] with kinds (0 node, 1 particle interaction),
+    item_count[k] -- the content of the text trace lines, binary."""
+    np.savez(path, times=np.asarray(times, np.float64), ptr=np.asarray(ptr, np.int64),
+             ids=np.asarray(ids, np.int32), kinds=np.asarray(kinds, np.int8),
+             item_count=np.asarray(item_count, np.int64))
+
+
+def load_stream_npz(path) -> dict:
+    z = np.load(path)
+    s = {k: z[k] for k in ("times", "ptr", "ids", "kinds", "item_count")}
+    n = len(s["times"])
+    if len(s["ptr"]) != n + 1 or len(s["item_count"]) != n or s["ptr"][-1] != len(s["ids"]):
+        raise TraceFormatError(0, "inconsistent stream arrays")
+    if np.any(np.diff(s["times"]) < 0):
+        raise TraceFormatError(0, "arrival times decrease")
+    return s
+
+
+def replay_stream(stream: dict, tree, lists, **executor_kw):
+    """Replay a binary force stream on the device batcher (the requests must
+    be the tree's buckets in DFS order with their device-walk lists)."""
+    from .executor import GpuForceExecutor
+    ex = GpuForceExecutor(tree, lists, **executor_kw)
+    if len(stream["times"]) != len(ex.ptr) - 1:
+        raise ValueError(f"stream has {len(stream['times'])} records for {len(ex.ptr) - 1} buckets")
+    if not (np.array_equal(stream["ptr"], ex.ptr) and np.array_equal(stream["ids"], ex.ids)
+            and np.array_equal(stream["kinds"], ex.kind) and np.array_equal(stream["item_count"], ex.item_count)):
+        raise ValueError("stream records do not match the tree's interaction lists")
+    return ex.run(stream["times"])

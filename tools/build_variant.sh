@@ -10,7 +10,7 @@ cd "${SRC:-$root/paper_2008_05712_b200/csrc}"
 out=$root/build/var_$name
 mkdir -p $out
 objs=""
-for f in abi.cu bh.cu bh_build.cu md.cu md_loop.cu ewald.cu dm.cu; do
+for f in abi.cu bh.cu bh_build.cu md.cu md_loop.cu ewald.cu dm.cu $( [ -f batcher.cu ] && echo batcher.cu ); do
   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
        --expt-relaxed-constexpr $flags -c $f -o $out/$f.o &
   objs="$objs $out/$f.o"
