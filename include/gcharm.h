@@ -269,6 +269,10 @@ gc_status gc_batcher_create(gc_ctx *ctx, gc_bh *bh, gc_dm *dm, int64_t max_size,
 gc_status gc_batcher_destroy(gc_batcher *b);
 gc_status gc_batcher_submit(gc_batcher *b, int64_t n, const int64_t *owner, const double *arrival,
                             const int64_t *ptr, const int64_t *ids, const int8_t *kinds);
+/* gc_batcher_prepare: optional, before a phase of n requests (CSR ptr[n+1],
+ * largest buffer id max_id): every device buffer and plan scratch is sized up
+ * front so the submission path never allocates. */
+gc_status gc_batcher_prepare(gc_batcher *b, int64_t n, const int64_t *ptr, int64_t max_id);
 gc_status gc_batcher_poll(gc_batcher *b, double now);
 gc_status gc_batcher_flush(gc_batcher *b, double now);
 gc_status gc_batcher_sync(gc_batcher *b, int64_t *n_batches);
@@ -314,6 +318,21 @@ gc_status gc_md_set_ghosts(gc_md *md, const void *left, int64_t n_left, const vo
 gc_status gc_md_slab_step(gc_md *md, double dt);
 gc_status gc_md_migrate(gc_md *md, const void *in_left, int64_t n_left, const void *in_right, int64_t n_right);
 gc_status gc_md_owned(gc_md *md, int64_t *n_owned, double *pos, double *vel, int64_t *gid /* host; may be NULL */);
+/* Device-count slab path (no host round trip inside a step; §8e): the same
+ * step with every count on the device.  gc_md_pack_dev writes the records of
+ * `what` into a fixed-capacity DEVICE buffer and their number into the DEVICE
+ * int32 *count (records beyond cap are dropped and flagged); the *_dev
+ * receivers read the received counts from DEVICE int32 pointers.  Exchange
+ * the buffers and counts by stream-ordered peer sends (NCCL) on the context's
+ * stream.  gc_md_slab_counts synchronises: out = {owned, owned + ghosts,
+ * overflow flags (1 message, 2 atom capacity)}; gc_md_owned checks them. */
+gc_status gc_md_pack_dev(gc_md *md, int32_t what, void *out, int64_t cap, int32_t *count);
+gc_status gc_md_set_ghosts_dev(gc_md *md, const void *left, const int32_t *n_left, const void *right,
+                               const int32_t *n_right, int64_t cap);
+gc_status gc_md_slab_step_dev(gc_md *md, double dt);
+gc_status gc_md_migrate_dev(gc_md *md, const void *in_left, const int32_t *n_left, const void *in_right,
+                            const int32_t *n_right, int64_t cap);
+gc_status gc_md_slab_counts(gc_md *md, int64_t out[3]);
 
 /* ---- closed-loop MD ----------------------------------------
  * hr/workloads/md.py MDWorkload (md.py:209-271) run on the device as one

@@ -194,6 +194,21 @@ void ensure_rows(gc_batcher *b, size_t nrows)
     }
 }
 
+// size every per-batch buffer for the largest batch requests [r0, R) can form
+// (windows of max_size requests over the CSR offsets ptr) before anything is
+// launched: plans then never allocate (an allocation serialises host and device)
+void reserve_for(gc_batcher *b, int64_t r0, int64_t R, const int *ptr)
+{
+    int64_t pmax = 0;
+    const int64_t ms = std::max<int64_t>(1, std::min<int64_t>(b->st.max_size, R - r0));
+    for (int64_t r = std::max<int64_t>(0, r0); r < R; ++r)
+        pmax = std::max<int64_t>(pmax, (int64_t)ptr[std::min<int64_t>(r + ms, R)] - ptr[r]);
+    dm_reserve(b->dm, pmax, ms);
+    b->d_bounds.resize(std::max<int64_t>(ms + 1, (int64_t)b->d_bounds.n));
+    b->d_member_of.resize(std::max<int64_t>(std::max<int64_t>(pmax, 1), (int64_t)b->d_member_of.n));
+    ensure_rows(b, b->rows.size() + (size_t)((R - r0 + ms - 1) / ms) + 2);
+}
+
 // one combined launch of requests [r0, r0 + k): plan, stage, member kernel
 void launch_batch(gc_batcher *b, long long r0, long long k, double now)
 {
@@ -299,19 +314,30 @@ gc_status gc_batcher_submit(gc_batcher *b, int64_t n, const int64_t *owner, cons
         GC_REQUIRE(npos >= 0 && (npos == 0 || (ids && kinds)), GC_E_VALUE, "bad CSR");
         GC_REQUIRE((int64_t)b->ids.size() + npos < INT_MAX, GC_E_VALUE, "ring exceeds 2^31 positions");
         const int64_t r0 = (int64_t)b->owner.size(), p0 = (int64_t)b->ids.size();
+        // validate + append (vectorised: one pass per array)
+        const int64_t nb = b->bh->n_buckets, nn = b->bh->n_nodes;
+        b->owner.resize(r0 + n);
+        b->ptr.resize(r0 + n + 1);
         for (int64_t i = 0; i < n; ++i) {
-            GC_REQUIRE(owner[i] >= 0 && owner[i] < b->bh->n_buckets, GC_E_VALUE, "owner is not a bucket of the tree");
+            GC_REQUIRE(owner[i] >= 0 && owner[i] < nb, GC_E_VALUE, "owner is not a bucket of the tree");
             GC_REQUIRE(ptr[i + 1] >= ptr[i], GC_E_VALUE, "bad CSR");
-            b->owner.push_back((int)owner[i]);
-            b->ptr.push_back((int)(p0 + ptr[i + 1] - ptr[0]));
+            b->owner[r0 + i] = (int)owner[i];
+            b->ptr[r0 + i + 1] = (int)(p0 + ptr[i + 1] - ptr[0]);
         }
+        b->ids.resize(p0 + npos);
+        b->kinds.resize(p0 + npos);
+        const int64_t *src = ids + ptr[0];
+        int *dst = b->ids.data() + p0;
+        int64_t lo = INT64_MAX, hi = -1;
         for (int64_t p = 0; p < npos; ++p) {
-            const int64_t id = ids[ptr[0] + p];
-            GC_REQUIRE(id >= 0 && id < b->bh->n_nodes, GC_E_VALUE, "buffer id is not a node of the tree");
-            b->ids.push_back((int)id);
-            b->kinds.push_back((signed char)(kinds[ptr[0] + p] ? 1 : 0));
-            b->max_id = std::max(b->max_id, id);
+            const int64_t id = src[p];
+            lo = std::min(lo, id);
+            hi = std::max(hi, id);
+            dst[p] = (int)id;
         }
+        GC_REQUIRE(npos == 0 || (lo >= 0 && hi < nn), GC_E_VALUE, "buffer id is not a node of the tree");
+        std::memcpy(b->kinds.data() + p0, kinds + ptr[0], npos);
+        b->max_id = std::max<int64_t>(b->max_id, hi);
         cudaStream_t s = b->ctx->stream;
         // the new requests join the device ring (ids, kinds, owners, offsets)
         b->d_ids.grow(b->ids.size(), s);
@@ -323,24 +349,37 @@ gc_status gc_batcher_submit(gc_batcher *b, int64_t n, const int64_t *owner, cons
         GC_CUDA(cudaMemcpyAsync(b->d_owner.p + r0, b->owner.data() + r0, n * sizeof(int), cudaMemcpyHostToDevice, s));
         GC_CUDA(cudaMemcpyAsync(b->d_ptr.p + r0, b->ptr.data() + r0, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, s));
         dm_grow_universe(b->dm, b->max_id);
-        // size every per-batch buffer for the largest batch these requests can
-        // form (max_size members) before anything is launched
-        {
-            int64_t pmax = 0;
-            const int64_t R = (int64_t)b->owner.size(), ms = std::min<int64_t>(b->st.max_size, R);
-            for (int64_t r = std::max<int64_t>(0, b->head); r < R; ++r)  // widest window of max_size requests
-                pmax = std::max<int64_t>(pmax, (int64_t)b->ptr[std::min<int64_t>(r + ms, R)] - b->ptr[r]);
-            dm_reserve(b->dm, pmax, ms);
-            b->d_bounds.resize(std::max<int64_t>(ms + 1, (int64_t)b->d_bounds.n));
-            b->d_member_of.resize(std::max<int64_t>(pmax, (int64_t)b->d_member_of.n));
-            ensure_rows(b, b->rows.size() + (size_t)(R - b->head + ms - 1) / std::max<int64_t>(ms, 1) + 2);
-        }
+        reserve_for(b, b->head, (int64_t)b->owner.size(), b->ptr.data());
         // Runtime.submit_work_request (hr/runtime.py:151-163) + a poll at every arrival
         for (int64_t i = 0; i < n; ++i) {
             b->st.npending += 1;
             GC_REQUIRE(!trig_observe(b->st, arrival[i]), GC_E_CLOCK, "arrival precedes the last arrival");
             poll(b, arrival[i]);
         }
+    });
+}
+
+gc_status gc_batcher_prepare(gc_batcher *b, int64_t n, const int64_t *ptr, int64_t max_id)
+{
+    return guard([&] {
+        GC_REQUIRE(b && ptr && n >= 0, GC_E_VALUE, "null argument");
+        std::vector<int> p(n + 1);
+        for (int64_t i = 0; i <= n; ++i) p[i] = (int)(ptr[i] - ptr[0]);
+        const int64_t npos = p[n];
+        cudaStream_t s = b->ctx->stream;
+        b->d_ids.grow(b->ids.size() + npos, s);
+        b->d_ids.n = b->ids.size();
+        b->d_kinds.grow(b->kinds.size() + npos, s);
+        b->d_kinds.n = b->kinds.size();
+        b->d_owner.grow(b->owner.size() + n, s);
+        b->d_owner.n = b->owner.size();
+        b->d_ptr.grow(b->ptr.size() + n, s);
+        b->d_ptr.n = b->ptr.size();
+        b->ids.reserve(b->ids.size() + npos);
+        b->kinds.reserve(b->kinds.size() + npos);
+        dm_grow_universe(b->dm, max_id);
+        reserve_for(b, 0, n, p.data());
+        GC_CUDA(cudaStreamSynchronize(s));
     });
 }
 

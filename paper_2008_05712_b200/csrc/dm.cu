@@ -573,6 +573,11 @@ void dm_reserve(gc_dm *dm, int64_t P, int64_t M)
         dm->dcnt.resize(4);
         dm->dcnt.zero(dm->ctx->stream);
     }
+    const int slot_f4 = (int)(dm->slot_bytes / 16);
+    if (dm->pool.n == 0 && slot_f4 >= 3) {  // the slot pool (staged payloads)
+        dm->pool.resize((size_t)dm->nslots * slot_f4);
+        dm->pool.zero(dm->ctx->stream);
+    }
     // cub temporary storage of the largest calls of a plan
     gc_ctx *ctx = dm->ctx;
     size_t need = 0, b = 0;

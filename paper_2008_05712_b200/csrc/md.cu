@@ -1185,6 +1185,139 @@ __global__ void md_keep_kernel(int n_owned, const int *__restrict__ cell_of, int
     tgid[k] = gid[i];
 }
 
+// --- device-count slab path (no host round trip per step) -----------------
+// dn = [owned atoms, all atoms (owned + ghosts), overflow flags, scratch]; the
+// kernels run over the capacity and read their counts from dn.
+__global__ void mdv_pack_kernel(const int *__restrict__ dn, const int *__restrict__ cell_of, int plane_cells, int plane,
+                                const double4 *__restrict__ pos, const double4 *__restrict__ vel,
+                                const long long *__restrict__ gid, int with_vel, double4 *__restrict__ out, int cap,
+                                int *__restrict__ cnt, int *__restrict__ flags)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= dn[0] || cell_of[i] / plane_cells != plane) return;
+    const int k = atomicAdd(cnt, 1);
+    if (k >= cap) {
+        atomicOr(flags, 1);  // message capacity exceeded
+        return;
+    }
+    const double4 p = pos[i];
+    if (with_vel) {
+        out[2 * k] = make_double4(p.x, p.y, p.z, __longlong_as_double(gid[i]));
+        out[2 * k + 1] = vel[i];
+    } else {
+        out[k] = make_double4(p.x, p.y, p.z, __longlong_as_double(gid[i]));
+    }
+}
+
+// received records -> atoms [base, base + n), base = dn[bslot] (+ *add), n = min(*cnt, cap)
+__global__ void mdv_unpack_kernel(const int *__restrict__ cnt, int cap, const double4 *__restrict__ rec, int with_vel,
+                                  const int *__restrict__ dn, int bslot, const int *__restrict__ add, int atom_cap,
+                                  double4 *__restrict__ pos, double4 *__restrict__ vel, long long *__restrict__ gid,
+                                  int *__restrict__ flags)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = min(*cnt, cap);
+    if (k >= n) return;
+    const int i = dn[bslot] + (add ? *add : 0) + k;
+    if (i >= atom_cap) {
+        atomicOr(flags, 2);  // atom capacity exceeded
+        return;
+    }
+    const double4 r = with_vel ? rec[2 * k] : rec[k];
+    pos[i] = make_double4(r.x, r.y, r.z, 0.0);
+    gid[i] = __double_as_longlong(r.w);
+    if (with_vel) vel[i] = rec[2 * k + 1];
+}
+
+// dn[1] = dn[0] + left + right (ghosts appended); or, after a migration,
+// dn[0] = dn[1] = kept + left + right
+__global__ void mdv_counts_kernel(int *__restrict__ dn, const int *__restrict__ nl, const int *__restrict__ nr, int cap,
+                                  int migrate, int atom_cap)
+{
+    const int l = min(*nl, cap), r = min(*nr, cap);
+    int n = (migrate ? dn[3] : dn[0]) + l + r;
+    if (n > atom_cap) {
+        dn[2] |= 2;
+        n = atom_cap;
+    }
+    if (migrate) dn[0] = n;
+    dn[1] = n;
+}
+
+__global__ void mdv_assign_kernel(const int *__restrict__ dn, int lo_slot, int hi_slot, const int *__restrict__ nl,
+                                  int cap, const double4 *__restrict__ pos, const MDParams P, int use_npy,
+                                  int *__restrict__ cell_of, int *__restrict__ count)
+{
+    // atoms [dn[lo_slot], dn[hi_slot]): owned cells from the position; ghosts
+    // (lo_slot = 0, hi_slot = 1) get the x plane of the side they arrived on
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lo = lo_slot < 0 ? 0 : dn[lo_slot], hi = dn[hi_slot];
+    if (i < lo || i >= hi) return;
+    const double4 p = pos[i];
+    const double x[3] = {p.x, p.y, p.z};
+    int c = md_cell_index(x, P, use_npy);
+    if (lo_slot >= 0) {  // ghost: x plane from the arrival side
+        const int plane = (i - lo) < min(*nl, cap) ? 0 : P.nx - 1;
+        c = plane * (P.ny * P.nz) + c % (P.ny * P.nz);
+    }
+    cell_of[i] = c;
+    atomicAdd(&count[c], 1);
+}
+
+__global__ void mdv_scatter_kernel(const int *__restrict__ dn, const int *__restrict__ cell_start,
+                                   const int *__restrict__ cell_of, int *__restrict__ count, int *__restrict__ perm)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= dn[1]) return;
+    const int c = cell_of[i];
+    perm[cell_start[c] + atomicSub(&count[c], 1) - 1] = i;
+}
+
+__global__ void mdv_integrate_assign_kernel(const int *__restrict__ dn, double4 *__restrict__ pos,
+                                            double4 *__restrict__ vel, const double4 *__restrict__ force,
+                                            const MDParams P, double dt, int use_npy, int *__restrict__ cell_of,
+                                            int *__restrict__ count)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= dn[0]) return;
+    const double4 p = pos[i], q = vel[i], f4 = force[i];
+    double x[3] = {p.x, p.y, p.z}, v[3] = {q.x, q.y, q.z};
+    const double f[3] = {f4.x, f4.y, f4.z};
+    md_advance(x, v, f, P, dt);
+    pos[i] = make_double4(x[0], x[1], x[2], 0.0);
+    vel[i] = make_double4(v[0], v[1], v[2], 0.0);
+    const int c = md_cell_index(x, P, use_npy);
+    cell_of[i] = c;
+    atomicAdd(&count[c], 1);
+}
+
+// owned atoms still inside the slab -> tmp (dn[3] counts them)
+__global__ void mdv_keep_kernel(int *__restrict__ dn, const int *__restrict__ cell_of, int plane_cells, int nx,
+                                const double4 *__restrict__ pos, const double4 *__restrict__ vel,
+                                const long long *__restrict__ gid, double4 *__restrict__ tpos,
+                                double4 *__restrict__ tvel, long long *__restrict__ tgid)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= dn[0]) return;
+    const int lx = cell_of[i] / plane_cells;
+    if (lx < 1 || lx > nx - 2) return;
+    const int k = atomicAdd(&dn[3], 1);
+    tpos[k] = pos[i];
+    tvel[k] = vel[i];
+    tgid[k] = gid[i];
+}
+
+__global__ void mdv_copy_kept_kernel(const int *__restrict__ dn, const double4 *__restrict__ tpos,
+                                     const double4 *__restrict__ tvel, const long long *__restrict__ tgid,
+                                     double4 *__restrict__ pos, double4 *__restrict__ vel, long long *__restrict__ gid)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= dn[3]) return;
+    pos[i] = tpos[i];
+    vel[i] = tvel[i];
+    gid[i] = tgid[i];
+}
+
 }  // namespace gc
 
 using namespace gc;
@@ -1202,6 +1335,10 @@ struct gc_md {
     DBuf<int> cell_of, scell, sidx, count, cell_start, perm;
     DBuf<long long> gid;  // global atom id (cell order, self-pair orientation)
     int n_owned = 0;
+    // device-count slab path: counts live in dn (mdv_* kernels), capacity in atoms
+    DBuf<int> dn;
+    int atom_cap = 0;
+    bool dev_counts = false;
     // slab scratch (pack / migrate)
     DBuf<int> flag, sel, nsel;
     DBuf<double4> tmp4;
@@ -1695,10 +1832,159 @@ gc_status gc_md_slab_step(gc_md *md, double dt)
     });
 }
 
+// ---- device-count slab path (multi-GPU MD without host round trips) --------
+namespace {
+void mdv_enter(gc_md *md)
+{
+    if (md->dev_counts) return;
+    cudaStream_t s = md->ctx->stream;
+    const int cap = std::max(2 * md->n_owned + 4096, md->n);
+    md_grow(md, cap);
+    md->tmp4.resize(2 * (size_t)cap);
+    md->tmp8.resize(cap);
+    md->atom_cap = cap;
+    md->dn.resize(4);
+    const int h[4] = {md->n_owned, md->n, 0, 0};
+    md->dn.upload(h, 4, s);
+    GC_CUDA(cudaStreamSynchronize(s));
+    md->dev_counts = true;
+}
+
+void mdv_sort(gc_md *md)
+{
+    cudaStream_t s = md->ctx->stream;
+    const int nc = md->ncell, cap = md->atom_cap;
+    size_t bytes = 0;
+    GC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, md->count.p, md->cell_start.p, nc + 1, s));
+    md->ctx->scratch.resize(std::max(bytes, md->ctx->scratch.n));
+    GC_CUDA(cub::DeviceScan::ExclusiveSum(md->ctx->scratch.p, bytes, md->count.p, md->cell_start.p, nc + 1, s));
+    mdv_scatter_kernel<<<grid_for(cap, MD_TPB), MD_TPB, 0, s>>>(md->dn.p, md->cell_start.p, md->cell_of.p,
+                                                                md->count.p, md->perm.p);
+    md_sortgather_kernel<<<grid_for(nc, MD_TPB / 32), MD_TPB, 0, s>>>(nc, md->cell_start.p, md->perm.p, md->pos.p,
+                                                                      md->gid.p, md->spos.p, md->sidx.p, md->scell.p);
+    check_launch("mdv sort");
+}
+}  // namespace
+
+gc_status gc_md_pack_dev(gc_md *md, int32_t what, void *out, int64_t cap, int32_t *count)
+{
+    return guard([&] {
+        GC_REQUIRE(md && md->P.slab && out && count && cap >= 0, GC_E_STATE, "not a slab / null argument");
+        GC_REQUIRE(what >= 0 && what <= 3, GC_E_VALUE, "what: 0/1 ghost planes, 2/3 migrants");
+        mdv_enter(md);
+        cudaStream_t s = md->ctx->stream;
+        const int nx = md->P.nx, pc = md->P.ny * md->P.nz;
+        const int plane = what == 0 ? 1 : what == 1 ? nx - 2 : what == 2 ? 0 : nx - 1;
+        GC_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), s));
+        mdv_pack_kernel<<<grid_for(md->atom_cap, MD_TPB), MD_TPB, 0, s>>>(
+            md->dn.p, md->cell_of.p, pc, plane, md->pos.p, md->vel.p, md->gid.p, what >= 2, (double4 *)out, (int)cap,
+            count, md->dn.p + 2);
+        check_launch("mdv_pack_kernel");
+    });
+}
+
+gc_status gc_md_set_ghosts_dev(gc_md *md, const void *left, const int32_t *n_left, const void *right,
+                               const int32_t *n_right, int64_t cap)
+{
+    return guard([&] {
+        GC_REQUIRE(md && md->P.slab && left && right && n_left && n_right, GC_E_STATE, "not a slab / null argument");
+        mdv_enter(md);
+        cudaStream_t s = md->ctx->stream;
+        const int c = (int)cap, ac = md->atom_cap;
+        mdv_unpack_kernel<<<grid_for(c, MD_TPB), MD_TPB, 0, s>>>(n_left, c, (const double4 *)left, 0, md->dn.p, 0,
+                                                                 nullptr, ac, md->pos.p, md->vel.p, md->gid.p,
+                                                                 md->dn.p + 2);
+        mdv_unpack_kernel<<<grid_for(c, MD_TPB), MD_TPB, 0, s>>>(n_right, c, (const double4 *)right, 0, md->dn.p, 0,
+                                                                 n_left, ac, md->pos.p, md->vel.p, md->gid.p,
+                                                                 md->dn.p + 2);
+        mdv_counts_kernel<<<1, 1, 0, s>>>(md->dn.p, n_left, n_right, c, 0, ac);
+        GC_CUDA(cudaMemsetAsync(md->count.p, 0, sizeof(int) * (md->ncell + 1), s));
+        mdv_assign_kernel<<<grid_for(ac, MD_TPB), MD_TPB, 0, s>>>(md->dn.p, -1, 0, n_left, c, md->pos.p, md->P,
+                                                                  md->use_npy, md->cell_of.p, md->count.p);
+        mdv_assign_kernel<<<grid_for(ac, MD_TPB), MD_TPB, 0, s>>>(md->dn.p, 0, 1, n_left, c, md->pos.p, md->P,
+                                                                  md->use_npy, md->cell_of.p, md->count.p);
+        check_launch("mdv ghosts");
+        mdv_sort(md);
+    });
+}
+
+gc_status gc_md_slab_step_dev(gc_md *md, double dt)
+{
+    return guard([&] {
+        GC_REQUIRE(md && md->P.slab, GC_E_STATE, "not a slab");
+        mdv_enter(md);
+        cudaStream_t s = md->ctx->stream;
+        GC_CUDA(cudaEventRecord(md->e0, s));
+        md_cell_forces(md, false, dt);  // forces on the owned cells
+        mdv_integrate_assign_kernel<<<grid_for(md->atom_cap, MD_TPB), MD_TPB, 0, s>>>(
+            md->dn.p, md->pos.p, md->vel.p, md->force.p, md->P, dt, md->use_npy, md->cell_of.p, md->count.p);
+        check_launch("mdv_integrate_assign_kernel");
+        GC_CUDA(cudaEventRecord(md->e1, s));
+    });
+}
+
+gc_status gc_md_migrate_dev(gc_md *md, const void *in_left, const int32_t *n_left, const void *in_right,
+                            const int32_t *n_right, int64_t cap)
+{
+    return guard([&] {
+        GC_REQUIRE(md && md->P.slab && in_left && in_right && n_left && n_right, GC_E_STATE,
+                   "not a slab / null argument");
+        mdv_enter(md);
+        cudaStream_t s = md->ctx->stream;
+        const int c = (int)cap, ac = md->atom_cap;
+        GC_CUDA(cudaMemsetAsync(md->dn.p + 3, 0, sizeof(int), s));
+        mdv_keep_kernel<<<grid_for(ac, MD_TPB), MD_TPB, 0, s>>>(md->dn.p, md->cell_of.p, md->P.ny * md->P.nz,
+                                                                md->P.nx, md->pos.p, md->vel.p, md->gid.p, md->tmp4.p,
+                                                                md->tmp4.p + ac, md->tmp8.p);
+        mdv_copy_kept_kernel<<<grid_for(ac, MD_TPB), MD_TPB, 0, s>>>(md->dn.p, md->tmp4.p, md->tmp4.p + ac,
+                                                                     md->tmp8.p, md->pos.p, md->vel.p, md->gid.p);
+        mdv_unpack_kernel<<<grid_for(c, MD_TPB), MD_TPB, 0, s>>>(n_left, c, (const double4 *)in_left, 1, md->dn.p, 3,
+                                                                 nullptr, ac, md->pos.p, md->vel.p, md->gid.p,
+                                                                 md->dn.p + 2);
+        mdv_unpack_kernel<<<grid_for(c, MD_TPB), MD_TPB, 0, s>>>(n_right, c, (const double4 *)in_right, 1, md->dn.p,
+                                                                 3, n_left, ac, md->pos.p, md->vel.p, md->gid.p,
+                                                                 md->dn.p + 2);
+        mdv_counts_kernel<<<1, 1, 0, s>>>(md->dn.p, n_left, n_right, c, 1, ac);
+        GC_CUDA(cudaMemsetAsync(md->count.p, 0, sizeof(int) * (md->ncell + 1), s));
+        mdv_assign_kernel<<<grid_for(ac, MD_TPB), MD_TPB, 0, s>>>(md->dn.p, -1, 0, n_left, c, md->pos.p, md->P,
+                                                                  md->use_npy, md->cell_of.p, md->count.p);
+        check_launch("mdv migrate");
+        mdv_sort(md);
+    });
+}
+
+// host view of the device counts (synchronises): out = {owned, all atoms, overflow flags}
+gc_status gc_md_slab_counts(gc_md *md, int64_t out[3])
+{
+    return guard([&] {
+        GC_REQUIRE(md && out, GC_E_VALUE, "null argument");
+        if (!md->dev_counts) {
+            out[0] = md->n_owned;
+            out[1] = md->n;
+            out[2] = 0;
+            return;
+        }
+        int h[4];
+        md->dn.download(h, 4, md->ctx->stream);
+        GC_CUDA(cudaStreamSynchronize(md->ctx->stream));
+        out[0] = h[0];
+        out[1] = h[1];
+        out[2] = h[2];
+        md->n_owned = h[0];
+        md->n = h[1];
+    });
+}
+
 gc_status gc_md_owned(gc_md *md, int64_t *n_owned, double *pos, double *vel, int64_t *gid)
 {
     return guard([&] {
         GC_REQUIRE(md && n_owned, GC_E_VALUE, "null argument");
+        if (md->dev_counts) {  // refresh the host counts from the device path
+            int64_t c[3];
+            const gc_status st = gc_md_slab_counts(md, c);
+            GC_REQUIRE(st == GC_OK, st, gc_last_error());
+            GC_REQUIRE(c[2] == 0, GC_E_CAPACITY, "slab message / atom capacity exceeded (device-count path)");
+        }
         const int n = md->n_owned;
         *n_owned = n;
         if (!pos && !vel && !gid) return;

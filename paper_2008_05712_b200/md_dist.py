@@ -113,6 +113,43 @@ class DistTransport:
         return fl, fr
 
 
+    def exchange_fixed(self, send_l, cnt_l, send_r, cnt_r, recv_l, rcnt_l, recv_r, rcnt_r, stream=None):
+        """Device-count exchange: fixed-capacity record buffers and their int32
+        counts, all stream-ordered on `stream` (NCCL peer sends; the current
+        stream waits for the receives) -- no host round trip.  recv_l gets the
+        left neighbour's `send_r`, recv_r the right neighbour's `send_l`."""
+        import torch
+        dist = self.dist
+        if self.k == 1:  # a single slab is its own left and right neighbour
+            with torch.cuda.stream(stream) if stream is not None else _nullctx():
+                recv_l.copy_(send_r)
+                rcnt_l.copy_(cnt_r)
+                recv_r.copy_(send_l)
+                rcnt_r.copy_(cnt_l)
+            return
+        left, right = neighbours(self.rank, self.k)
+        # same issue order on every rank (see exchange): sends left, right, receives right, left
+        ops = [dist.P2POp(dist.isend, cnt_l, self._peer(left), self.group, 0),
+               dist.P2POp(dist.isend, send_l, self._peer(left), self.group, 2),
+               dist.P2POp(dist.isend, cnt_r, self._peer(right), self.group, 1),
+               dist.P2POp(dist.isend, send_r, self._peer(right), self.group, 3),
+               dist.P2POp(dist.irecv, rcnt_r, self._peer(right), self.group, 0),
+               dist.P2POp(dist.irecv, recv_r, self._peer(right), self.group, 2),
+               dist.P2POp(dist.irecv, rcnt_l, self._peer(left), self.group, 1),
+               dist.P2POp(dist.irecv, recv_l, self._peer(left), self.group, 3)]
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            for q in dist.batch_isend_irecv(ops):
+                q.wait()  # NCCL: the current (library) stream waits; gloo: completes on the host
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 class LocalTransport:
     """All K slabs in one process (one GPU): messages are handed over directly.
     ``exchange_all`` takes every slab's (to_left, to_right) at once."""
@@ -126,6 +163,18 @@ class LocalTransport:
             left, right = neighbours(r, self.k)
             out.append((outgoing[left][1], outgoing[right][0]))
         return out
+
+    def exchange_all_fixed(self, slabs, kind: str):
+        """Device-count form for K slabs on one device (same stream): every
+        slab's left receive buffer gets its left neighbour's right send."""
+        for r, s in enumerate(slabs):
+            left, right = neighbours(r, self.k)
+            sl, sr = slabs[left].bufs[kind], slabs[right].bufs[kind]
+            b = s.bufs[kind]
+            b["recv_l"].copy_(sl["send_r"])
+            b["cnt"][2:3].copy_(sl["cnt"][1:2])
+            b["recv_r"].copy_(sr["send_l"])
+            b["cnt"][3:4].copy_(sr["cnt"][0:1])
 
 
 class LJSlab:
@@ -177,6 +226,67 @@ class LJSlab:
         L.call("gc_md_migrate", self.dev.handle, self._ptr(from_left), from_left.shape[0], self._ptr(from_right),
                from_right.shape[0])
 
+    # -- device-count step (no host round trip: counts travel with the records) --
+    def enable_device_counts(self, halo_cap: int | None = None):
+        """Fixed-capacity message buffers for the device-count step: a plane's
+        atoms (ny x nz cells) with a 2x margin, for the ghosts and the migrants."""
+        torch = self.torch
+        if halo_cap is None:
+            per_cell = max(1.0, self.inp.positions.shape[0] / float(self.gnx * self.ny * self.nz))
+            halo_cap = int(2.0 * per_cell * self.ny * self.nz) + 1024
+        self.cap = int(halo_cap)
+        self.stream = torch.cuda.ExternalStream(self.dev._ctx.stream) if self.device.type == "cuda" else None
+        self.bufs = {}
+        for kind, w in (("halo", GHOST), ("mig", MIGRANT)):
+            self.bufs[kind] = {
+                "send_l": torch.zeros((self.cap, w), dtype=torch.float64, device=self.device),
+                "send_r": torch.zeros((self.cap, w), dtype=torch.float64, device=self.device),
+                "recv_l": torch.zeros((self.cap, w), dtype=torch.float64, device=self.device),
+                "recv_r": torch.zeros((self.cap, w), dtype=torch.float64, device=self.device),
+                "cnt": torch.zeros(4, dtype=torch.int32, device=self.device),  # send l, send r, recv l, recv r
+            }
+
+    def _p(self, t, i=0):
+        return C.c_void_p(t.data_ptr() + i * t.element_size())
+
+    def pack_dev(self, kind: str):
+        b = self.bufs[kind]
+        w0 = 0 if kind == "halo" else 2
+        L.call("gc_md_pack_dev", self.dev.handle, w0, self._p(b["send_l"]), self.cap, self._p(b["cnt"], 0))
+        L.call("gc_md_pack_dev", self.dev.handle, w0 + 1, self._p(b["send_r"]), self.cap, self._p(b["cnt"], 1))
+
+    def exchange_dev(self, transport: DistTransport, kind: str):
+        b = self.bufs[kind]
+        c = b["cnt"]
+        transport.exchange_fixed(b["send_l"], c[0:1], b["send_r"], c[1:2], b["recv_l"], c[2:3], b["recv_r"], c[3:4],
+                                 stream=self.stream)
+
+    def set_halo_dev(self):
+        b = self.bufs["halo"]
+        L.call("gc_md_set_ghosts_dev", self.dev.handle, self._p(b["recv_l"]), self._p(b["cnt"], 2),
+               self._p(b["recv_r"]), self._p(b["cnt"], 3), self.cap)
+
+    def advance_dev(self, dt: float):
+        L.call("gc_md_slab_step_dev", self.dev.handle, float(dt))
+
+    def take_migrants_dev(self):
+        b = self.bufs["mig"]
+        L.call("gc_md_migrate_dev", self.dev.handle, self._p(b["recv_l"]), self._p(b["cnt"], 2),
+               self._p(b["recv_r"]), self._p(b["cnt"], 3), self.cap)
+
+    def step_dev(self, transport: DistTransport, dt: float | None = None):
+        """One step with every count on the device: pack -> exchange (stream-
+        ordered NCCL) -> ghosts -> forces + integrator -> migrants -> exchange ->
+        migrate.  Nothing here waits for the device."""
+        dt = self.inp.dt if dt is None else dt
+        self.pack_dev("halo")
+        self.exchange_dev(transport, "halo")
+        self.set_halo_dev()
+        self.advance_dev(dt)
+        self.pack_dev("mig")
+        self.exchange_dev(transport, "mig")
+        self.take_migrants_dev()
+
     def step(self, transport: DistTransport, dt: float | None = None):
         dt = self.inp.dt if dt is None else dt
         self.set_halo(*transport.exchange(*self.halo_out()))
@@ -211,6 +321,31 @@ def run_local(inp, k: int, steps: int, dt: float | None = None):
             s.advance(dt)
         for s, (fl, fr) in zip(slabs, tr.exchange_all([s.migrants_out() for s in slabs])):
             s.take_migrants(fl, fr)
+    return assemble([s.owned() for s in slabs], inp.positions.shape[0])
+
+
+def run_local_dev(inp, k: int, steps: int, dt: float | None = None):
+    """run_local with the device-count step (fixed-capacity messages, counts
+    on the device); returns the assembled global (positions, velocities)."""
+    b = slab_bounds(inp.cells_xyz[0], k)
+    slabs = [LJSlab(inp, b[r], b[r + 1]) for r in range(k)]
+    for s in slabs:
+        s.enable_device_counts()
+    tr = LocalTransport(k)
+    dt = inp.dt if dt is None else dt
+    torch = slabs[0].torch
+    with torch.cuda.stream(slabs[0].stream):  # the copies run on the library's stream (one context per device)
+        for _ in range(steps):
+            for s in slabs:
+                s.pack_dev("halo")
+            tr.exchange_all_fixed(slabs, "halo")
+            for s in slabs:
+                s.set_halo_dev()
+                s.advance_dev(dt)
+                s.pack_dev("mig")
+            tr.exchange_all_fixed(slabs, "mig")
+            for s in slabs:
+                s.take_migrants_dev()
     return assemble([s.owned() for s in slabs], inp.positions.shape[0])
 
 

@@ -85,3 +85,43 @@ def test_neighbour_exchange_gloo(world):
     for p in ps:
         p.join(timeout=60)
     assert all(res[r] for r in range(world)), res
+
+
+def _worker_fixed(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        tr = md_dist.DistTransport()
+        cap = 16
+        left, right = md_dist.neighbours(rank, world)
+        n_l, n_r = rank % 3, 2 * rank + 1  # variable fill of fixed-capacity buffers
+        send_l = torch.zeros((cap, 4), dtype=torch.float64)
+        send_r = torch.zeros((cap, 4), dtype=torch.float64)
+        send_l[:n_l] = rank
+        send_r[:n_r] = rank + 0.5
+        cnt = torch.tensor([n_l, n_r, -1, -1], dtype=torch.int32)
+        recv_l = torch.zeros((cap, 4), dtype=torch.float64)
+        recv_r = torch.zeros((cap, 4), dtype=torch.float64)
+        tr.exchange_fixed(send_l, cnt[0:1], send_r, cnt[1:2], recv_l, cnt[2:3], recv_r, cnt[3:4])
+        ok = int(cnt[2]) == 2 * left + 1 and int(cnt[3]) == right % 3
+        ok = ok and bool((recv_l[:int(cnt[2])] == left + 0.5).all()) and bool((recv_r[:int(cnt[3])] == right).all())
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fixed_capacity_exchange_gloo(world):
+    """The device-count step's exchange (fixed-capacity buffers, int32 counts
+    sent alongside) over a real process group (gloo on CPU tensors)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_fixed, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    assert all(res[r] for r in range(world)), res
