@@ -273,6 +273,11 @@ gc_status gc_batcher_submit(gc_batcher *b, int64_t n, const int64_t *owner, cons
  * largest buffer id max_id): every device buffer and plan scratch is sized up
  * front so the submission path never allocates. */
 gc_status gc_batcher_prepare(gc_batcher *b, int64_t n, const int64_t *ptr, int64_t max_id);
+/* gc_batcher_submit_walk: as gc_batcher_submit, every request's buffers
+ * being its owner bucket's interaction list as the device walk left it in HBM
+ * (requires gc_bh_get_lists with ids on the current walk): no buffer id
+ * crosses from the host, only owners and arrival times. */
+gc_status gc_batcher_submit_walk(gc_batcher *b, int64_t n, const int64_t *owner, const double *arrival);
 gc_status gc_batcher_poll(gc_batcher *b, double now);
 gc_status gc_batcher_flush(gc_batcher *b, double now);
 gc_status gc_batcher_sync(gc_batcher *b, int64_t *n_batches);
@@ -318,6 +323,17 @@ gc_status gc_md_set_ghosts(gc_md *md, const void *left, int64_t n_left, const vo
 gc_status gc_md_slab_step(gc_md *md, double dt);
 gc_status gc_md_migrate(gc_md *md, const void *in_left, int64_t n_left, const void *in_right, int64_t n_right);
 gc_status gc_md_owned(gc_md *md, int64_t *n_owned, double *pos, double *vel, int64_t *gid /* host; may be NULL */);
+/* Column work requests (configs[4]: LJ force work arriving at a varying
+ * generation rate, combined by the batcher's trigger): gc_md_columns out =
+ * {columns (0 = the column kernel does not apply), home cells per column,
+ * columns along z}; column c = (x * ny + y) * (columns along z) + z-block.
+ * gc_md_forces_columns launches the forces of the home cells of a DEVICE
+ * int32 column list (asynchronous; positions as last sorted); gc_md_get_forces
+ * downloads the force array as it stands. */
+gc_status gc_md_columns(gc_md *md, int64_t out[3]);
+gc_status gc_md_forces_columns(gc_md *md, const int32_t *cols, int64_t n);
+gc_status gc_md_get_forces(gc_md *md, double *forces, double *energy);
+
 /* Device-count slab path (no host round trip inside a step; §8e): the same
  * step with every count on the device.  gc_md_pack_dev writes the records of
  * `what` into a fixed-capacity DEVICE buffer and their number into the DEVICE

@@ -82,6 +82,9 @@ SIGNATURES = {
     "gc_measure_fp32_peak": [vp, f64p, f64p],
     "gc_bh_step": [vp, C.c_int64, C.c_int32, f64p, f64p, C.c_double, C.c_int64, C.c_double, C.c_double,
                    C.c_double, f64p],
+    "gc_md_columns": [vp, i64p],
+    "gc_md_forces_columns": [vp, vp, C.c_int64],
+    "gc_md_get_forces": [vp, f64p, f64p],
     "gc_md_pack_dev": [vp, C.c_int32, vp, C.c_int64, vp],
     "gc_md_set_ghosts_dev": [vp, vp, vp, vp, vp, C.c_int64],
     "gc_md_slab_step_dev": [vp, C.c_double],
@@ -91,6 +94,7 @@ SIGNATURES = {
     "gc_batcher_destroy": [vp],
     "gc_batcher_submit": [vp, C.c_int64, i64p, f64p, i64p, i64p, i8p],
     "gc_batcher_prepare": [vp, C.c_int64, i64p, C.c_int64],
+    "gc_batcher_submit_walk": [vp, C.c_int64, i64p, f64p],
     "gc_batcher_poll": [vp, C.c_double],
     "gc_batcher_flush": [vp, C.c_double],
     "gc_batcher_sync": [vp, i64p],

@@ -231,7 +231,7 @@ gc_status gc_kernel_spec(gc_ctx *ctx, const char *kernel_class, int64_t out[5])
     return guard([&] {
         GC_REQUIRE(ctx && kernel_class, GC_E_VALUE, "null argument");
         GC_CUDA(cudaSetDevice(ctx->device));
-        if (!strcmp(kernel_class, "md")) md_kernel_spec(kernel_class, out);
+        if (!strcmp(kernel_class, "md") || !strcmp(kernel_class, "md_column")) md_kernel_spec(kernel_class, out);
         else if (!strcmp(kernel_class, "ewald_member") || !strcmp(kernel_class, "force_slot"))
             dm_kernel_spec(kernel_class, out);
         else bh_kernel_spec(kernel_class, out);

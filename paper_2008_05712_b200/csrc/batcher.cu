@@ -27,6 +27,10 @@
 #include <cstring>
 #include <vector>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "dm_state.h"
 
@@ -127,6 +131,24 @@ __global__ void batcher_trigger_kernel(TrigState *st, long long first, int n, co
     *st = t;
 }
 
+// the device-walk lists of owners[0..n) appended to the ring: request k's
+// positions [ring_ptr[k], ring_ptr[k + 1]) <- bucket owners[k]'s list
+// (2 id + kind, bucket CSR list_ptr); one warp per request
+__global__ void batcher_gather_lists_kernel(int n, const int *__restrict__ owners, const int64_t *__restrict__ list_ptr,
+                                            const int *__restrict__ lists, const int *__restrict__ ring_ptr,
+                                            int *__restrict__ ids, signed char *__restrict__ kinds)
+{
+    const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (w >= n) return;
+    const int64_t s0 = list_ptr[owners[w]];
+    const int p0 = ring_ptr[w], cnt = ring_ptr[w + 1] - p0;
+    for (int i = lane; i < cnt; i += 32) {
+        const int v = lists[s0 + i];
+        ids[p0 + i] = v >> 1;
+        kinds[p0 + i] = (signed char)(v & 1);
+    }
+}
+
 // per-batch member bounds (relative) and position -> member map from the
 // ring's global CSR offsets of requests [r0, r0 + m]
 __global__ void batcher_bounds_kernel(const int *__restrict__ ptr, long long r0, int m, int *__restrict__ bounds)
@@ -153,9 +175,8 @@ struct gc_batcher {
     double g = 1.0, eps = 1e-4;
     // every request submitted since creation (the device ring; FIFO order)
     std::vector<int> ptr{0};  // CSR offsets of the buffer ids (host mirror of d_ptr)
-    std::vector<int> ids;  // host copy of the ids (synchronous fallback plans)
-    std::vector<signed char> kinds;
     std::vector<int> owner;
+    int64_t npos = 0;  // positions in the ring (ids / kinds live on the device only)
     long long head = 0;  // first pending request
     int64_t max_id = -1;
     DBuf<int> d_ids, d_ptr, d_owner, d_bounds, d_member_of;
@@ -171,10 +192,16 @@ struct gc_batcher {
     std::vector<cudaEvent_t> ev;  // 2 per batch
     long long next_combined = 0;
     int64_t fallback_plans = 0;
+    // pinned staging of the submitted ids / kinds (asynchronous H2D)
+    int *h_ids_pin = nullptr;
+    signed char *h_kinds_pin = nullptr;
+    size_t pin_cap = 0;
     ~gc_batcher()
     {
         for (auto e : ev)
             if (e) cudaEventDestroy(e);
+        if (h_ids_pin) cudaFreeHost(h_ids_pin);
+        if (h_kinds_pin) cudaFreeHost(h_kinds_pin);
     }
 };
 
@@ -229,13 +256,19 @@ void launch_batch(gc_batcher *b, long long r0, long long k, double now)
         // the plan may evict: the synchronous data-manager path (host arrays)
         sync_plan = 1;
         ++b->fallback_plans;
-        std::vector<int64_t> hid(b->ids.begin() + p0, b->ids.begin() + p0 + P), hb(m + 1);
+        std::vector<int> hid32(P);
+        std::vector<signed char> kd(P);
+        if (P) {
+            GC_CUDA(cudaMemcpyAsync(hid32.data(), b->d_ids.p + p0, P * sizeof(int), cudaMemcpyDeviceToHost, s));
+            GC_CUDA(cudaMemcpyAsync(kd.data(), b->d_kinds.p + p0, P, cudaMemcpyDeviceToHost, s));
+            GC_CUDA(cudaStreamSynchronize(s));
+        }
+        std::vector<int64_t> hid(hid32.begin(), hid32.end()), hb(m + 1);
         for (int i = 0; i <= m; ++i) hb[i] = b->ptr[r0 + i] - p0;
         int64_t nt = 0, np = 0;
         gc_status st = gc_dm_build_plan(b->dm, hid.data(), hb.data(), m, now, &nt, &np);
         GC_REQUIRE(st == GC_OK, st, gc_last_error());
         // kinds in plan order (REUSE_SORTED sorts each member's ids, memory.py:342-347)
-        std::vector<signed char> kd(b->kinds.begin() + p0, b->kinds.begin() + p0 + P);
         std::vector<int64_t> tx(m);
         st = gc_dm_plan_get(b->dm, nullptr, nullptr, tx.data(), nullptr);
         GC_REQUIRE(st == GC_OK, st, gc_last_error());
@@ -310,10 +343,11 @@ gc_status gc_batcher_submit(gc_batcher *b, int64_t n, const int64_t *owner, cons
     return guard([&] {
         GC_REQUIRE(b && (n == 0 || (owner && arrival && ptr)), GC_E_VALUE, "null argument");
         if (n == 0) return;
+        const auto t_in = std::chrono::steady_clock::now();
         const int64_t npos = ptr[n] - ptr[0];
         GC_REQUIRE(npos >= 0 && (npos == 0 || (ids && kinds)), GC_E_VALUE, "bad CSR");
-        GC_REQUIRE((int64_t)b->ids.size() + npos < INT_MAX, GC_E_VALUE, "ring exceeds 2^31 positions");
-        const int64_t r0 = (int64_t)b->owner.size(), p0 = (int64_t)b->ids.size();
+        GC_REQUIRE(b->npos + npos < INT_MAX, GC_E_VALUE, "ring exceeds 2^31 positions");
+        const int64_t r0 = (int64_t)b->owner.size(), p0 = b->npos;
         // validate + append (vectorised: one pass per array)
         const int64_t nb = b->bh->n_buckets, nn = b->bh->n_nodes;
         b->owner.resize(r0 + n);
@@ -324,10 +358,22 @@ gc_status gc_batcher_submit(gc_batcher *b, int64_t n, const int64_t *owner, cons
             b->owner[r0 + i] = (int)owner[i];
             b->ptr[r0 + i + 1] = (int)(p0 + ptr[i + 1] - ptr[0]);
         }
-        b->ids.resize(p0 + npos);
-        b->kinds.resize(p0 + npos);
+        // ids (int64 -> int32) and kinds go straight into the pinned staging
+        // (pre-faulted; the ring's only host copy is on the device)
+        cudaStream_t s0 = b->ctx->stream;
+        const size_t need = (size_t)npos + 2 * (size_t)n + 1;  // ids | owners | offsets
+        if (b->pin_cap < need) {
+            GC_CUDA(cudaStreamSynchronize(s0));  // the previous staging may still be in flight
+            if (b->h_ids_pin) cudaFreeHost(b->h_ids_pin);
+            if (b->h_kinds_pin) cudaFreeHost(b->h_kinds_pin);
+            b->pin_cap = need;
+            GC_CUDA(cudaHostAlloc((void **)&b->h_ids_pin, b->pin_cap * sizeof(int), cudaHostAllocDefault));
+            GC_CUDA(cudaHostAlloc((void **)&b->h_kinds_pin, b->pin_cap, cudaHostAllocDefault));
+        } else {
+            GC_CUDA(cudaStreamSynchronize(s0));  // staging reuse: the last submission's copies are done
+        }
         const int64_t *src = ids + ptr[0];
-        int *dst = b->ids.data() + p0;
+        int *dst = b->h_ids_pin;
         int64_t lo = INT64_MAX, hi = -1;
         for (int64_t p = 0; p < npos; ++p) {
             const int64_t id = src[p];
@@ -336,25 +382,112 @@ gc_status gc_batcher_submit(gc_batcher *b, int64_t n, const int64_t *owner, cons
             dst[p] = (int)id;
         }
         GC_REQUIRE(npos == 0 || (lo >= 0 && hi < nn), GC_E_VALUE, "buffer id is not a node of the tree");
-        std::memcpy(b->kinds.data() + p0, kinds + ptr[0], npos);
+        std::memcpy(b->h_kinds_pin, kinds + ptr[0], npos);
         b->max_id = std::max<int64_t>(b->max_id, hi);
+        b->npos += npos;
+        const auto t_app = std::chrono::steady_clock::now();
         cudaStream_t s = b->ctx->stream;
-        // the new requests join the device ring (ids, kinds, owners, offsets)
-        b->d_ids.grow(b->ids.size(), s);
-        b->d_kinds.grow(b->kinds.size(), s);
+        // the new requests join the device ring (ids, kinds, owners, offsets);
+        // the bulk (ids, kinds) goes through pinned staging: a truly
+        // asynchronous copy (a pageable one blocks the host)
+        b->d_ids.grow(b->npos, s);
+        b->d_kinds.grow(b->npos, s);
         b->d_owner.grow(b->owner.size(), s);
         b->d_ptr.grow(b->ptr.size(), s);
-        GC_CUDA(cudaMemcpyAsync(b->d_ids.p + p0, b->ids.data() + p0, npos * sizeof(int), cudaMemcpyHostToDevice, s));
-        GC_CUDA(cudaMemcpyAsync(b->d_kinds.p + p0, b->kinds.data() + p0, npos, cudaMemcpyHostToDevice, s));
-        GC_CUDA(cudaMemcpyAsync(b->d_owner.p + r0, b->owner.data() + r0, n * sizeof(int), cudaMemcpyHostToDevice, s));
-        GC_CUDA(cudaMemcpyAsync(b->d_ptr.p + r0, b->ptr.data() + r0, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, s));
+        GC_CUDA(cudaMemcpyAsync(b->d_ids.p + p0, b->h_ids_pin, npos * sizeof(int), cudaMemcpyHostToDevice, s));
+        GC_CUDA(cudaMemcpyAsync(b->d_kinds.p + p0, b->h_kinds_pin, npos, cudaMemcpyHostToDevice, s));
+        int *po = b->h_ids_pin + npos, *pp = po + n;
+        std::memcpy(po, b->owner.data() + r0, n * sizeof(int));
+        std::memcpy(pp, b->ptr.data() + r0, (n + 1) * sizeof(int));
+        GC_CUDA(cudaMemcpyAsync(b->d_owner.p + r0, po, n * sizeof(int), cudaMemcpyHostToDevice, s));
+        GC_CUDA(cudaMemcpyAsync(b->d_ptr.p + r0, pp, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, s));
+        const auto t_h2d = std::chrono::steady_clock::now();
         dm_grow_universe(b->dm, b->max_id);
         reserve_for(b, b->head, (int64_t)b->owner.size(), b->ptr.data());
+        const auto tq = std::chrono::steady_clock::now();
         // Runtime.submit_work_request (hr/runtime.py:151-163) + a poll at every arrival
         for (int64_t i = 0; i < n; ++i) {
             b->st.npending += 1;
             GC_REQUIRE(!trig_observe(b->st, arrival[i]), GC_E_CLOCK, "arrival precedes the last arrival");
             poll(b, arrival[i]);
+        }
+        if (getenv("GC_BATCHER_PROF")) {
+            const auto te = std::chrono::steady_clock::now();
+            fprintf(stderr, "gc_batcher_submit: append %.3f ms, h2d %.3f ms, reserve %.3f ms, trigger + launches %.3f ms\n",
+                    std::chrono::duration<double, std::milli>(t_app - t_in).count(),
+                    std::chrono::duration<double, std::milli>(t_h2d - t_app).count(),
+                    std::chrono::duration<double, std::milli>(tq - t_h2d).count(),
+                    std::chrono::duration<double, std::milli>(te - tq).count());
+        }
+    });
+}
+
+// Submission without any buffer-id traffic: every request's buffers are its
+// owner bucket's interaction list as the device walk left it on the device
+// (gc_bh_get_lists); only owners and arrival times cross from the host.
+gc_status gc_batcher_submit_walk(gc_batcher *b, int64_t n, const int64_t *owner, const double *arrival)
+{
+    return guard([&] {
+        GC_REQUIRE(b && (n == 0 || (owner && arrival)), GC_E_VALUE, "null argument");
+        if (n == 0) return;
+        gc_bh *bh = b->bh;
+        GC_REQUIRE(bh->dev_lists_valid && (int64_t)bh->h_list_ptr.size() == bh->n_buckets + 1, GC_E_STATE,
+                   "no device-resident lists of the current walk (gc_bh_get_lists with ids)");
+        const auto t_in = std::chrono::steady_clock::now();
+        const int64_t r0 = (int64_t)b->owner.size(), p0 = b->npos;
+        const int64_t nb = bh->n_buckets;
+        b->owner.resize(r0 + n);
+        b->ptr.resize(r0 + n + 1);
+        int64_t pos = p0;
+        for (int64_t i = 0; i < n; ++i) {
+            GC_REQUIRE(owner[i] >= 0 && owner[i] < nb, GC_E_VALUE, "owner is not a bucket of the tree");
+            b->owner[r0 + i] = (int)owner[i];
+            pos += bh->h_list_ptr[owner[i] + 1] - bh->h_list_ptr[owner[i]];
+            GC_REQUIRE(pos < INT_MAX, GC_E_VALUE, "ring exceeds 2^31 positions");
+            b->ptr[r0 + i + 1] = (int)pos;
+        }
+        const int64_t npos = pos - p0;
+        b->npos = pos;
+        b->max_id = std::max<int64_t>(b->max_id, bh->n_nodes - 1);
+        cudaStream_t s = b->ctx->stream;
+        const size_t need = 2 * (size_t)n + 1;
+        GC_CUDA(cudaStreamSynchronize(s));  // the staging of the previous submission is free
+        if (b->pin_cap < need) {
+            if (b->h_ids_pin) cudaFreeHost(b->h_ids_pin);
+            if (b->h_kinds_pin) cudaFreeHost(b->h_kinds_pin);
+            b->pin_cap = need;
+            GC_CUDA(cudaHostAlloc((void **)&b->h_ids_pin, b->pin_cap * sizeof(int), cudaHostAllocDefault));
+            GC_CUDA(cudaHostAlloc((void **)&b->h_kinds_pin, b->pin_cap, cudaHostAllocDefault));
+        }
+        b->d_ids.grow(b->npos, s);
+        b->d_kinds.grow(b->npos, s);
+        b->d_owner.grow(b->owner.size(), s);
+        b->d_ptr.grow(b->ptr.size(), s);
+        int *po = b->h_ids_pin, *pp = po + n;
+        std::memcpy(po, b->owner.data() + r0, n * sizeof(int));
+        std::memcpy(pp, b->ptr.data() + r0, (n + 1) * sizeof(int));
+        GC_CUDA(cudaMemcpyAsync(b->d_owner.p + r0, po, n * sizeof(int), cudaMemcpyHostToDevice, s));
+        GC_CUDA(cudaMemcpyAsync(b->d_ptr.p + r0, pp, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, s));
+        if (npos > 0)
+            batcher_gather_lists_kernel<<<grid_for(n, 8), 256, 0, s>>>((int)n, b->d_owner.p + r0, bh->d_bptr.p,
+                                                                        bh->d_list_val2.p, b->d_ptr.p + r0, b->d_ids.p,
+                                                                        b->d_kinds.p);
+        check_launch("batcher_gather_lists_kernel");
+        const auto t_h2d = std::chrono::steady_clock::now();
+        dm_grow_universe(b->dm, b->max_id);
+        reserve_for(b, b->head, (int64_t)b->owner.size(), b->ptr.data());
+        const auto tq = std::chrono::steady_clock::now();
+        for (int64_t i = 0; i < n; ++i) {
+            b->st.npending += 1;
+            GC_REQUIRE(!trig_observe(b->st, arrival[i]), GC_E_CLOCK, "arrival precedes the last arrival");
+            poll(b, arrival[i]);
+        }
+        if (getenv("GC_BATCHER_PROF")) {
+            const auto te = std::chrono::steady_clock::now();
+            fprintf(stderr, "gc_batcher_submit_walk: append %.3f ms, reserve %.3f ms, trigger + launches %.3f ms\n",
+                    std::chrono::duration<double, std::milli>(t_h2d - t_in).count(),
+                    std::chrono::duration<double, std::milli>(tq - t_h2d).count(),
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq).count());
         }
     });
 }
@@ -367,16 +500,21 @@ gc_status gc_batcher_prepare(gc_batcher *b, int64_t n, const int64_t *ptr, int64
         for (int64_t i = 0; i <= n; ++i) p[i] = (int)(ptr[i] - ptr[0]);
         const int64_t npos = p[n];
         cudaStream_t s = b->ctx->stream;
-        b->d_ids.grow(b->ids.size() + npos, s);
-        b->d_ids.n = b->ids.size();
-        b->d_kinds.grow(b->kinds.size() + npos, s);
-        b->d_kinds.n = b->kinds.size();
+        b->d_ids.grow(b->npos + npos, s);
+        b->d_ids.n = b->npos;
+        b->d_kinds.grow(b->npos + npos, s);
+        b->d_kinds.n = b->npos;
         b->d_owner.grow(b->owner.size() + n, s);
         b->d_owner.n = b->owner.size();
         b->d_ptr.grow(b->ptr.size() + n, s);
         b->d_ptr.n = b->ptr.size();
-        b->ids.reserve(b->ids.size() + npos);
-        b->kinds.reserve(b->kinds.size() + npos);
+        if (b->pin_cap < (size_t)npos + 2 * (size_t)n + 1) {
+            if (b->h_ids_pin) cudaFreeHost(b->h_ids_pin);
+            if (b->h_kinds_pin) cudaFreeHost(b->h_kinds_pin);
+            b->pin_cap = (size_t)npos + 2 * (size_t)n + 1;
+            GC_CUDA(cudaHostAlloc((void **)&b->h_ids_pin, b->pin_cap * sizeof(int), cudaHostAllocDefault));
+            GC_CUDA(cudaHostAlloc((void **)&b->h_kinds_pin, b->pin_cap, cudaHostAllocDefault));
+        }
         dm_grow_universe(b->dm, max_id);
         reserve_for(b, 0, n, p.data());
         GC_CUDA(cudaStreamSynchronize(s));

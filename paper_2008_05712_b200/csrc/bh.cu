@@ -288,6 +288,7 @@ void walk_params(gc_bh *bh, double theta)
     bh->stats_valid = false;
     bh->orders_fresh = false;
     bh->have_union = false;
+    bh->dev_lists_valid = false;
 }
 
 // One walk launch over the handle's walk-group range (asynchronous).
@@ -486,6 +487,7 @@ void run_walk(gc_bh *bh, double theta, bool want_stats)
     launch_walk(bh, true, stats);
     GC_CUDA(cudaEventRecord(bh->ev[1], bh->ctx->stream));
     bh->have_union = true;
+    bh->dev_lists_valid = false;
     bh->have_member_lists = false;
     bh->grec_valid = !bh->force_fused;  // the staged mode's walk counted the records
     if (stats) bh->staging_sized = false;  // a new tree / theta (else the lists repeat)
@@ -710,6 +712,7 @@ void run_overlapped(gc_bh *bh, double theta, double g, double eps)
     GC_CUDA(cudaEventRecord(bh->ev[0], s));
     launch_walk(bh, true, false, bh->d_fq.p, bh->d_fq_tail.p, f0);
     bh->have_union = true;
+    bh->dev_lists_valid = false;
     bh->have_member_lists = false;
     bh->grec_valid = false;
     // the force kernel: programmatic dependent launch on the same stream -- it
@@ -787,6 +790,7 @@ gc_status gc_bh_set_particles(gc_bh *bh, int64_t n, int32_t dim, const double *p
         device_build_tree(bh, pos, mass, n, dim, box, bucket_size);
         bh->have_tree = true;
         bh->have_union = bh->have_member_lists = false;
+        bh->dev_lists_valid = false;
         bh->ew_mom_valid = false;
         bh->params_valid = false;
         bh->stats_valid = false;
@@ -920,6 +924,7 @@ gc_status gc_bh_set_tree(gc_bh *bh, int64_t n_nodes, int32_t dim, double box, in
         bh->wg_cuts.clear();
         bh->have_tree = true;
         bh->have_union = bh->have_member_lists = false;
+        bh->dev_lists_valid = false;
         bh->ew_mom_valid = false;
         bh->params_valid = false;
         bh->stats_valid = false;
@@ -1079,6 +1084,10 @@ gc_status gc_bh_get_lists(gc_bh *bh, int64_t *ptr, int64_t *ids, int8_t *kind, i
                 if (ids) ids[i] = tmp[i] >> 1;
                 if (kind) kind[i] = (int8_t)(tmp[i] & 1);
             }
+            // the per-bucket lists stay on the device (d_list_val2: 2 id + kind,
+            // d_bptr offsets): the device batcher submits them without a copy
+            bh->h_list_ptr = bptr;
+            bh->dev_lists_valid = true;
         }
     });
 }

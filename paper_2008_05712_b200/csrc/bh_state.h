@@ -103,6 +103,10 @@ struct gc_bh {
     std::vector<int64_t> h_item_count;
     int64_t n_list_entries = 0;
     DBuf<int64_t> d_bptr;
+    // per-bucket lists resident on the device after gc_bh_get_lists (ids
+    // requested): d_list_val2 = 2 id + kind in bucket order, d_bptr / h_list_ptr
+    bool dev_lists_valid = false;
+    std::vector<int64_t> h_list_ptr;
     DBuf<int> d_pre, d_list_key, d_list_key2, d_list_val, d_list_val2;
     DBuf<int> d_flag;
     WalkParams wp{};

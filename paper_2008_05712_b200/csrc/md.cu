@@ -707,7 +707,7 @@ constexpr int MDK_SMEM = MDK_NB * 32 + MDK_LIST * MDK_THREADS * 2 + (MDK_NB / 2)
 
 __global__ void __launch_bounds__(MDK_THREADS, 3)
 md_lj3c_kernel(const double4 *__restrict__ spos, const int *__restrict__ sidx, const int *__restrict__ cell_start,
-               const MDParams P, float band, int ncol_z, double4 *__restrict__ out)
+               const MDParams P, float band, int ncol_z, double4 *__restrict__ out, const int *__restrict__ cols)
 {
     // dynamic shared memory (MDK_SMEM bytes)
     extern __shared__ __align__(16) unsigned char mdk_smem[];
@@ -721,8 +721,9 @@ md_lj3c_kernel(const double4 *__restrict__ spos, const int *__restrict__ sidx, c
     __shared__ double4 shtab[MDK_NR];  // image shift of the region cell
     __shared__ int pfx[MDK_THREADS];  // inclusive prefix of the list lengths over a home's parts
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // column: home cells (cx, cy, cz0 .. cz0 + kz - 1)
-    const int col = blockIdx.x;
+    // column: home cells (cx, cy, cz0 .. cz0 + kz - 1); a batched launch
+    // (combined work requests of columns) names its columns
+    const int col = cols ? cols[blockIdx.x] : (int)blockIdx.x;
     const int czb = col % ncol_z, cxy = col / ncol_z;
     const int cy = cxy % P.ny, cx = cxy / P.ny + (P.slab ? 1 : 0);  // slabs: owned x planes only
     const int cz0 = czb * MDK_KZ, kz = min(MDK_KZ, P.nz - cz0);
@@ -1415,7 +1416,7 @@ void md_cell_launch(gc_md *md, bool integ, double dt)
                 attr = true;
             }
             md_lj3c_kernel<<<cols, MDK_THREADS, MDK_SMEM, s>>>(md->spos.p, md->sidx.p, md->cell_start.p, md->P, bandc, ncz,
-                                                        md->force.p);
+                                                        md->force.p, nullptr);
             check_launch("md_lj3c_kernel");
             return;
         }
@@ -1832,6 +1833,64 @@ gc_status gc_md_slab_step(gc_md *md, double dt)
     });
 }
 
+// ---- column work requests (configs[4] arrivals through the batcher) --------
+// out = {columns (0: the column kernel does not apply), home cells per column
+// (KZ), columns along z}
+gc_status gc_md_columns(gc_md *md, int64_t out[3])
+{
+    return guard([&] {
+        GC_REQUIRE(md && out, GC_E_VALUE, "null argument");
+        const MDParams &P = md->P;
+        const bool ok = md->law == LAW_LJ && P.dim == 3 && md->lj_fast && md->lj_column && !P.slab && P.nx >= 3 &&
+                        P.ny >= 3 && P.nz >= 3;
+        const int ncz = (P.nz + MDK_KZ - 1) / MDK_KZ;
+        out[0] = ok ? (int64_t)P.nx * P.ny * ncz : 0;
+        out[1] = MDK_KZ;
+        out[2] = ncz;
+    });
+}
+
+// forces of the home cells of columns cols[0..n) (device int32 list; the
+// current cell order), asynchronous: one combined launch of n column requests
+gc_status gc_md_forces_columns(gc_md *md, const int32_t *cols, int64_t n)
+{
+    return guard([&] {
+        GC_REQUIRE(md && md->n > 0 && (cols || n == 0), GC_E_STATE, "no system set / null argument");
+        int64_t c[3];
+        const gc_status st = gc_md_columns(md, c);
+        GC_REQUIRE(st == GC_OK && c[0] > 0, GC_E_STATE, "the column kernel does not apply to this system");
+        if (n == 0) return;
+        const double extc = (MDK_KZ + 2) * md->P.cell;
+        const float bandc = (float)(md->P.c2 + 1e-5 * extc * extc + 1e-6);
+        static bool attr = false;
+        if (!attr) {
+            GC_CUDA(cudaFuncSetAttribute(md_lj3c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MDK_SMEM));
+            attr = true;
+        }
+        md_lj3c_kernel<<<(unsigned)n, MDK_THREADS, MDK_SMEM, md->ctx->stream>>>(
+            md->spos.p, md->sidx.p, md->cell_start.p, md->P, bandc, (int)c[2], md->force.p, cols);
+        check_launch("md_lj3c_kernel (columns)");
+    });
+}
+
+// the force array as it stands (no evaluation): forces (n, dim), energy (n)
+gc_status gc_md_get_forces(gc_md *md, double *forces, double *energy)
+{
+    return guard([&] {
+        GC_REQUIRE(md && md->n > 0, GC_E_STATE, "no system set");
+        cudaStream_t s = md->ctx->stream;
+        std::vector<double4> f(md->n);
+        md->force.download(f.data(), md->n, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        const int d = md->P.dim;
+        for (int i = 0; i < md->n; ++i) {
+            if (forces)
+                for (int k = 0; k < d; ++k) forces[i * d + k] = k == 0 ? f[i].x : (k == 1 ? f[i].y : f[i].z);
+            if (energy) energy[i] = f[i].w;
+        }
+    });
+}
+
 // ---- device-count slab path (multi-GPU MD without host round trips) --------
 namespace {
 void mdv_enter(gc_md *md)
@@ -2012,7 +2071,19 @@ gc_status gc_md_owned(gc_md *md, int64_t *n_owned, double *pos, double *vel, int
 namespace gc {
 void md_kernel_spec(const char *cls, int64_t out[5])
 {
-    (void)cls;
+    if (!strcmp(cls, "md_column")) {  // the LJ column kernel: one work request (column of home cells) per block
+        cudaFuncAttributes a;
+        GC_CUDA(cudaFuncGetAttributes(&a, md_lj3c_kernel));
+        GC_CUDA(cudaFuncSetAttribute(md_lj3c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MDK_SMEM));
+        int blocks = 0;
+        GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, md_lj3c_kernel, MDK_THREADS, MDK_SMEM));
+        out[0] = MDK_THREADS;
+        out[1] = a.numRegs;
+        out[2] = (int64_t)a.sharedSizeBytes + MDK_SMEM;
+        out[3] = 1;
+        out[4] = blocks;
+        return;
+    }
     const void *fn = (const void *)md_force_kernel<LAW_LJ, 3>;
     cudaFuncAttributes a;
     GC_CUDA(cudaFuncGetAttributes(&a, fn));

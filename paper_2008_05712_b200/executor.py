@@ -43,6 +43,7 @@ from . import _lib as L
 from .aggregator import AggregatorState, compute_max_size, poll_combine
 from .devicesim import b200_device_spec, b200_kernel_spec
 from .memory import DeviceMemory, MemoryMode
+from .errors import HeteroRtError
 from .nbody import DEFAULT_SOFTENING
 from .runtime import CompletionEvent, Runtime
 
@@ -125,6 +126,12 @@ class DeviceBatcher:
         kinds = np.ascontiguousarray(kinds, np.int8)
         L.call("gc_batcher_submit", self.handle, len(owners), L.ptr(owners, L.i64p), L.ptr(arrivals, L.f64p),
                L.ptr(ptr, L.i64p), L.ptr(ids, L.i64p), L.ptr(kinds, L.i8p))
+
+    def submit_walk(self, owners, arrivals) -> None:
+        """Requests whose buffers are the owners' device-walk lists (no buffer
+        id leaves the device; see gc_batcher_submit_walk)."""
+        owners, arrivals = L.i64(owners), L.f64(arrivals)
+        L.call("gc_batcher_submit_walk", self.handle, len(owners), L.ptr(owners, L.i64p), L.ptr(arrivals, L.f64p))
 
     def prepare(self, ptr, max_id: int) -> None:
         """Size every device buffer for a phase of len(ptr) - 1 requests."""
@@ -249,7 +256,12 @@ class GpuForceExecutor:
         if bat is None:
             bat = DeviceBatcher(self.tree, self.memory, st.max_size, st.timeout_factor, st.window, self.g, self.eps)
         self.runtime.submit_to_device("force", nb)
-        bat.submit(np.arange(nb), times, self.ptr, self.ids, self.kind)
+        try:  # the lists are the tree's device walk: submit them where they are
+            bat.submit_walk(np.arange(nb), times)
+        except HeteroRtError as e:
+            if type(e) is not HeteroRtError:  # GC_E_STATE only (no device-resident lists): a host submission
+                raise
+            bat.submit(np.arange(nb), times, self.ptr, self.ids, self.kind)
         bat.flush(float(times[-1]) if nb else 0.0)  # end of the phase (hr/timeline.py:276-298)
         rows, tms = bat.log()
         res.wall_s = time.perf_counter() - t0

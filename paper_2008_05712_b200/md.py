@@ -186,6 +186,109 @@ class LJSystem:
         return 14 * self.dims[0] * self.dims[1] * self.dims[2]
 
 
+# -- configs[4]: force work arriving at a varying generation rate ----------------
+
+class LJColumnPhase:
+    """One LJ force phase as work requests arriving at a varying rate,
+    combined by the batcher's trigger and launched column batch by column
+    batch (BASELINE configs[4]: "varying task-generation rate").
+
+    Work request = one column of KZ home cells (the column kernel's unit; its
+    forces read the 3 x 3 x (KZ + 2) neighbour cells).  Its arrival is the
+    last "interact" input of its cells: start + ready_cost x the largest
+    population among those cells (hr/workloads/md.py:236-254), plus lognormal
+    lulls between pieces of the column order (NBodyWorkload._schedule,
+    hr/workloads/nbody.py:285-301).  The trigger (hr/aggregator.py:41-110,
+    evaluated on the device, gc_batcher_trigger_device) cuts the FIFO of
+    columns into combined launches of at most max_size requests (the column
+    kernel's occupancy x SMs); each batch is one gc_md_forces_columns launch.
+    Forces are those of the whole-system launch bit for bit (the same
+    per-column arithmetic)."""
+
+    def __init__(self, system: "LJSystem", max_size: int | None = None, ready_cost: float = 0.01,
+                 pieces: int = 16, piece_gap: float = 4.0, seed: int = 7, timeout_factor: float = 2.0,
+                 tick: float = 1.0):
+        from .aggregator import compute_max_size
+        from .devicesim import b200_device_spec, b200_kernel_spec
+        self.sys = system
+        info = np.zeros(3, np.int64)
+        L.call("gc_md_columns", system.dev.handle, L.ptr(info, L.i64p))
+        if info[0] == 0:
+            raise ValueError("the column kernel does not apply to this system (needs >= 3 cells per dimension)")
+        self.ncol, self.kz, self.ncz = int(info[0]), int(info[1]), int(info[2])
+        if max_size is None:
+            max_size = compute_max_size(b200_kernel_spec("md_column"), b200_device_spec())
+        self.max_size, self.timeout_factor, self.tick = int(max_size), float(timeout_factor), float(tick)
+        self.ready_cost, self.pieces, self.piece_gap, self.seed = ready_cost, pieces, piece_gap, seed
+
+    def arrivals(self, positions) -> tuple:
+        """(column order by arrival, arrival times) for the current positions."""
+        nx, ny, nz = self.sys.dims
+        cell = self.sys.inp.cell_size
+        c = np.clip(np.floor(positions / cell).astype(np.int64), 0, np.array([nx - 1, ny - 1, nz - 1]))
+        pop = np.bincount((c[:, 0] * ny + c[:, 1]) * nz + c[:, 2], minlength=nx * ny * nz).reshape(nx, ny, nz)
+        # largest population over each cell's 3 x 3 x 3 neighbourhood (periodic)
+        m = pop.copy()
+        for ax in range(3):
+            m = np.maximum(np.maximum(m, np.roll(m, 1, axis=ax)), np.roll(m, -1, axis=ax))
+        kz, ncz = self.kz, self.ncz
+        colmax = np.zeros((nx, ny, ncz), np.int64)
+        for zb in range(ncz):
+            colmax[:, :, zb] = m[:, :, zb * kz:(zb + 1) * kz].max(axis=2)
+        ready = self.ready_cost * colmax.reshape(-1).astype(float)
+        # lulls between pieces of the column order (lognormal, as _schedule)
+        rng = np.random.default_rng(self.seed + 1)
+        per_piece = max(1, -(-self.ncol // self.pieces))
+        lull = np.zeros(self.ncol)
+        for k in range(1, self.pieces):
+            lull[k * per_piece:] += self.piece_gap * float(rng.lognormal(0.0, 1.0))
+        t = ready + lull
+        order = np.argsort(t, kind="stable")
+        return order.astype(np.int32), t[order]
+
+    def events(self, t):
+        """Trigger events: every arrival, and a poll at each multiple of `tick`
+        (the timeline's ticks while requests are pending, hr/timeline.py:391-399;
+        a poll with nothing pending is a no-op); arrivals at a tick come first."""
+        ticks = np.arange(np.floor(t[0] / self.tick) + 1, np.floor(t[-1] / self.tick) + 2) * self.tick if len(t) else []
+        times = np.concatenate([t, ticks])
+        poll = np.concatenate([np.zeros(len(t), np.int8), np.ones(len(ticks), np.int8)])
+        o = np.lexsort((poll, times))
+        return times[o], poll[o]
+
+    def run(self):
+        """The phase: (forces (n, 3), energy (n,), batches [(first, count, time)], device ms)."""
+        import torch
+
+        from .executor import DeviceBatcher
+        p, _, _ = self.sys.state()  # positions as last sorted on the device
+        order, t = self.arrivals(p)
+        ev_t, ev_p = self.events(t)
+        f, c, tt = DeviceBatcher.trigger_device(self.max_size, self.timeout_factor, 0, ev_t, is_poll=ev_p)
+        rest = len(order) - int(c.sum())  # end of the phase: drain in max_size chunks
+        if rest:
+            base = int(c.sum())
+            extra = [(base + k, min(self.max_size, rest - k)) for k in range(0, rest, self.max_size)]
+            f = np.concatenate([f, [e[0] for e in extra]]).astype(np.int64)
+            c = np.concatenate([c, [e[1] for e in extra]]).astype(np.int64)
+            tt = np.concatenate([tt, [float(t[-1])] * len(extra)])
+        dev = torch.device("cuda", torch.cuda.current_device())
+        cols = torch.from_numpy(order).to(dev)
+        ctx = self.sys.dev._ctx
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        stream = torch.cuda.ExternalStream(ctx.stream)
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            for a, k in zip(f, c):  # one combined launch per emitted batch
+                L.call("gc_md_forces_columns", self.sys.dev.handle, C.c_void_p(cols.data_ptr() + 4 * int(a)), int(k))
+            ev[1].record(stream)
+        ev[1].synchronize()
+        n = self.sys.n
+        fo, e = np.zeros((n, 3)), np.zeros(n)
+        L.call("gc_md_get_forces", self.sys.dev.handle, L.ptr(fo, L.f64p), L.ptr(e, L.f64p))
+        return fo, e, list(zip(f.tolist(), c.tolist(), tt.tolist())), ev[0].elapsed_time(ev[1])
+
+
 # -- closed-loop MD on the device (SURVEY.md §8f-3) ---------------------------------
 
 @dataclass

@@ -176,3 +176,40 @@ def test_lj_8m_config5_forces(md):
     fo, eo = orc.lj3d_compute_forces(s.positions, (84, 84, 84), s.cell_size, s.rc, s.eps, s.sigma, True)
     assert rel_err(f, fo).max() <= FORCE_RTOL
     np.testing.assert_allclose(e, eo, rtol=1e-10, atol=1e-12)
+
+
+def test_lj_column_phase_varying_rate(md):
+    """configs[4]'s force work arriving at a varying generation rate: column
+    requests (arrival = ready_cost x largest neighbour-cell population +
+    lognormal lulls) combined by the device trigger into batches of at most
+    max_size, each one column-kernel launch -- forces and energies bit-identical
+    to the whole-system launch; the batches are the host poll_combine's."""
+    from paper_2008_05712_b200.aggregator import AggregatorState, observe_arrival, poll_combine
+    from paper_2008_05712_b200.generators import gen_lj_fcc
+    from paper_2008_05712_b200.runtime import WorkRequest
+    s = jitter(gen_lj_fcc(30), seed=4)
+    sysd = md.LJSystem(s)
+    f0, e0 = sysd.forces()
+    ph = md.LJColumnPhase(sysd, max_size=300, ready_cost=0.01, pieces=8, piece_gap=4.0)
+    f1, e1, batches, ms = ph.run()
+    np.testing.assert_array_equal(f1, f0)
+    np.testing.assert_array_equal(e1, e0)
+    assert sum(c for _, c, _ in batches) == ph.ncol and ms > 0
+    order, t = ph.arrivals(sysd.state()[0])
+    ev_t, ev_p = ph.events(t)
+    st = AggregatorState("md", 300, 2.0)
+    ref = []
+    i = 0
+    for ti, pi in zip(ev_t, ev_p):
+        if not pi:  # an arrival (else a timeline tick: a poll only)
+            st.pending.append(WorkRequest(i, 0, "md", [], 1, ti, 0))
+            observe_arrival(st, ti)
+            i += 1
+        while (c := poll_combine(st, ti)) is not None:
+            ref.append((c.members[0].id, len(c.members)))
+    k = sum(n for _, n in ref)
+    while k < len(t):
+        ref.append((k, min(300, len(t) - k)))
+        k += ref[-1][1]
+    assert [(a, c) for a, c, _ in batches] == ref
+    assert any(c < 300 for _, c, _ in batches[:-1])  # the lulls fire timeout flushes
