@@ -213,6 +213,46 @@ def md_task_bytes(cell_of, ncell_dim):
     return total
 
 
+def md_candidates(cell_of, ncell_dim):
+    """Candidate pairs the full-shell cell kernel filters per step (every
+    atom against the atoms of its 27 neighbour cells, itself excluded)."""
+    n = ncell_dim
+    pops = np.bincount(cell_of, minlength=n ** 3).reshape(n, n, n).astype(np.float64)
+    shell = np.zeros_like(pops)
+    for dx in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dz in (-1, 0, 1):
+                shell += np.roll(pops, shift=(dx, dy, dz), axis=(0, 1, 2))
+    return float((pops * shell).sum() - pops.sum())
+
+
+def md_roofline_8m(ms, cells, ncell, natoms, sysin, hbm):
+    """configs[4] LJ against both rooflines: the DRAM bytes
+    ncu measured for one step's kernels (profiles/ncu_traffic.json) vs the
+    measured HBM peak, and the flops convention 9 x candidate + 23 x in-cutoff
+    pair vs the FP32 peak (in-cutoff pairs from the FCC density: each atom
+    sees n (4/3) pi rc^3 neighbours; the full-shell kernel evaluates both
+    orientations)."""
+    tr = {}
+    try:
+        tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")))
+    except OSError:
+        pass
+    step_bytes = tr.get("md8m_step_kernels")
+    cand = md_candidates(cells, ncell)
+    rho = natoms / float(np.prod(sysin.box_lengths if hasattr(sysin, "box_lengths") else [ncell * sysin.cell_size] * 3))
+    inc = natoms * rho * 4.0 / 3.0 * np.pi * sysin.rc ** 3
+    flops = 9.0 * cand + 23.0 * inc
+    return {"kernel": "md_lj3c_kernel (+ cell sort, integrator)", "ms_per_step": ms,
+            "dram_bytes_per_step_ncu": step_bytes,
+            "dram_gbs": step_bytes / (ms * 1e-3) / 1e9 if step_bytes else None,
+            "dram_frac": step_bytes / (ms * 1e-3) / 1e9 / hbm if step_bytes else None,
+            "candidate_pairs": cand, "in_cutoff_pairs_est": inc, "flops_convention": flops,
+            "tflops": flops / (ms * 1e-3) / 1e12, "fp32_frac": flops / (ms * 1e-3) / 74.44992e12,
+            "note": "issue-bound irregular kernel (ncu: profiles/r02_md_ncu_summary.txt): float32 filter of the "
+                    "27-cell shell + float64 pair math with the reference's cutoff decisions"}
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
@@ -606,10 +646,20 @@ def bench_md8m(args):
     _, _, cells = sysd.state()
     task_bytes = md_task_bytes(cells, sysin.cells)
     hbm, src = measured_hbm()
-    return {"workload": "configs[4] system on 1 GPU: LJ FCC 8,001,504 atoms, 84^3 cells, rc 2.5, periodic",
-            "ms_per_step": ms, "unit": "ms/step",
-            "task_model_gbs": task_bytes / (ms * 1e-3) / 1e9, "task_model_frac": task_bytes / (ms * 1e-3) / 1e9 / hbm,
-            "algorithmic_bytes_per_step": task_bytes}
+    out = {"workload": "configs[4] system on 1 GPU: LJ FCC 8,001,504 atoms, 84^3 cells, rc 2.5, periodic",
+           "ms_per_step": ms, "unit": "ms/step",
+           "task_model_gbs": task_bytes / (ms * 1e-3) / 1e9, "task_model_frac": task_bytes / (ms * 1e-3) / 1e9 / hbm,
+           "algorithmic_bytes_per_step": task_bytes,
+           "roofline": md_roofline_8m(ms, cells, sysin.cells, sysin.positions.shape[0], sysin, hbm)}
+    # configs[4]'s varying task-generation rate: the force phase as column
+    # requests through the device trigger, one column-kernel launch per batch
+    ph = md.LJColumnPhase(sysd)
+    f1, _, batches, bms = ph.run()
+    out["generation_rate_phase"] = {
+        "requests": ph.ncol, "batches": len(batches), "max_size": ph.max_size, "device_ms": bms,
+        "path": "md.LJColumnPhase: arrivals = ready_cost x neighbour population + lognormal lulls + ticks, "
+                "gc_batcher_trigger_device, gc_md_forces_columns per batch (forces bit-identical to one launch)"}
+    return out
 
 
 def bench_md_closed_loop(args):

@@ -190,7 +190,7 @@ def test_lj_column_phase_varying_rate(md):
     s = jitter(gen_lj_fcc(30), seed=4)
     sysd = md.LJSystem(s)
     f0, e0 = sysd.forces()
-    ph = md.LJColumnPhase(sysd, max_size=300, ready_cost=0.01, pieces=8, piece_gap=4.0)
+    ph = md.LJColumnPhase(sysd, max_size=300, ready_cost=0.01, pieces=8, piece_gap=4.0, tick=0.25)
     f1, e1, batches, ms = ph.run()
     np.testing.assert_array_equal(f1, f0)
     np.testing.assert_array_equal(e1, e0)
