@@ -697,15 +697,27 @@ md_lj3_kernel(const double4 *__restrict__ spos, const int *__restrict__ sidx, co
 //            bit); parts are summed by shuffles in fixed order (deterministic:
 //            slab runs are bit-identical to the whole domain).
 // ---------------------------------------------------------------------------
-constexpr int MDK_KZ = 4;  // home cells per column block
+#ifndef MDK_KZ_SET
+#define MDK_KZ_SET 4
+#endif
+#ifndef MDK_NB_SET
+#define MDK_NB_SET 1024
+#endif
+#ifndef MDK_LIST_SET
+#define MDK_LIST_SET 48
+#endif
+#ifndef MDK_MINB
+#define MDK_MINB 3
+#endif
+constexpr int MDK_KZ = MDK_KZ_SET;  // home cells per column block
 constexpr int MDK_THREADS = 256;
 constexpr int MDK_NR = 9 * (MDK_KZ + 2);  // region cells
-constexpr int MDK_NB = 1024;  // staged region slots incl. pads (overflow -> exact scan from global memory)
-constexpr int MDK_LIST = 48;  // survivors per thread (overflow -> the thread rescans its candidates exactly)
+constexpr int MDK_NB = MDK_NB_SET;  // staged region slots incl. pads (overflow -> exact scan from global memory)
+constexpr int MDK_LIST = MDK_LIST_SET;  // survivors per thread (overflow -> the thread rescans its candidates exactly)
 constexpr int MDK_HOMES = 256;  // home atoms per pass
 constexpr int MDK_SMEM = MDK_NB * 32 + MDK_LIST * MDK_THREADS * 2 + (MDK_NB / 2) * 24 + MDK_NB + MDK_HOMES * 2;
 
-__global__ void __launch_bounds__(MDK_THREADS, 3)
+__global__ void __launch_bounds__(MDK_THREADS, MDK_MINB)
 md_lj3c_kernel(const double4 *__restrict__ spos, const int *__restrict__ sidx, const int *__restrict__ cell_start,
                const MDParams P, float band, int ncol_z, double4 *__restrict__ out, const int *__restrict__ cols)
 {
@@ -751,20 +763,19 @@ md_lj3c_kernel(const double4 *__restrict__ spos, const int *__restrict__ sidx, c
         shtab[tid] = make_double4(md_xshift(cx + ox, P), sy, sz, 0.0);
     }
     __syncthreads();
-    if (warp == 0) {  // inclusive scan of the padded populations (<= 64 cells: two per lane)
-        int v0 = lane < MDK_NR ? pre[lane + 1] : 0;
-        int v1 = lane + 32 < MDK_NR ? pre[lane + 33] : 0;
+    if (warp == 0) {  // inclusive scan of the padded populations, 32 cells per round with a carry
+        int carry = 0;
+        for (int c0 = 0; c0 < MDK_NR; c0 += 32) {
+            int v = c0 + lane < MDK_NR ? pre[c0 + lane + 1] : 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t0 = __shfl_up_sync(0xffffffffu, v0, o), t1 = __shfl_up_sync(0xffffffffu, v1, o);
-            if (lane >= o) {
-                v0 += t0;
-                v1 += t1;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += t;
             }
+            v += carry;
+            if (c0 + lane < MDK_NR) pre[c0 + lane + 1] = v;
+            carry = __shfl_sync(0xffffffffu, v, 31);
         }
-        v1 += __shfl_sync(0xffffffffu, v0, 31);
-        if (lane < MDK_NR) pre[lane + 1] = v0;
-        if (lane + 32 < MDK_NR) pre[lane + 33] = v1;
         if (lane == 0) pre[0] = 0;
     }
     __syncthreads();
