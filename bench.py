@@ -684,6 +684,33 @@ def bench_md_closed_loop(args):
             "cpu_oracle_ms_per_md_step": cpu_ms, "parity": "bit-identical to the reference MDWorkload (goldens)"}
 
 
+def bench_periodic(args):
+    """periodic Barnes-Hut on configs[2]'s 1M clustered set
+    (27 images of the unit box, theta 0.7): device walk + force times."""
+    from paper_2008_05712_b200 import _lib as L
+    from paper_2008_05712_b200 import generators as gen
+    from paper_2008_05712_b200 import nbody
+
+    ps = gen.fp32_exact(gen.gen_particles(1_000_000, 42, clustering=0.6, dim=3))
+    tree = nbody.build_bucket_tree(ps, BUCKET)
+    L.call("gc_bh_set_periodic", tree.handle, 1, 1.0)
+    tm = np.zeros(3)
+    w, f = [], []
+    for i in range(4):
+        L.call("gc_bh_walk", tree.handle, THETA)
+        L.call("gc_bh_forces_async", tree.handle, 1.0, EPS)
+        L.call("gc_bh_timings", tree.handle, L.ptr(tm, L.f64p))
+        if i:
+            w.append(tm[0])
+            f.append(tm[1] + tm[2])
+    inter = nbody.interactions(tree)
+    ms = statistics.median(w) + statistics.median(f)
+    return {"workload": "configs[2] set, periodic: 27 images of the unit box, theta 0.7, bucket 8",
+            "interactions": inter, "walk_ms": statistics.median(w), "force_ms": statistics.median(f),
+            "ms_per_step": ms, "value": inter / (ms * 1e-3), "unit": "interactions/s",
+            "force_tflops": FLOPS_PER_INTERACTION * inter / (statistics.median(f) * 1e-3) / 1e12}
+
+
 def bench_ewald(args):
     """Ewald correction of 1M points from a root multipole
     (float64; 343 real-space replicas + 80 Fourier vectors per point)."""
@@ -751,6 +778,7 @@ def run_ours(args, world, rank, local):
         line["md8m"] = bench_md8m(args)
         line["md_closed_loop"] = bench_md_closed_loop(args)
         line["ewald"] = bench_ewald(args)
+        line["periodic"] = bench_periodic(args)
     if world == 1 and not args.no_cpu_baseline:
         c_inter, c_ts, cores = cpu_bh(bh["ps"], 1)
         line["cpu_baseline"] = {"value": c_inter / c_ts[0], "unit": "interactions/s", "cores": cores,

@@ -150,6 +150,16 @@ gc_status gc_bh_set_tree(gc_bh *bh, int64_t n_nodes, int32_t dim, double box, in
 gc_status gc_bh_walk_forces_async(gc_bh *bh, double theta, double g, double eps);
 /* Sizes: out[0..4] = n_nodes, n_buckets, per-bucket list entries, union
  * entries of the last device walk, source records they expand to (staging) */
+/* Periodic Barnes-Hut (no reference implementation, the
+ * float64 restatement is oracle/gcharm_oracle.c orc_periodic_forces): with
+ * nrep > 0 every bucket walks the tree once per image of the box (side L =
+ * the tree's box, (2 nrep + 1)^3 images, node centres of mass shifted in the
+ * opening test; nrep <= 1: ChaNGa's nReplicas) and the fused force kernel
+ * evaluates the shifted sources.
+ * Per-bucket counts (gc_bh_get_lists ptr / item_count) cover all images; the
+ * per-bucket id lists, potentials, the staged mode and the overlap are
+ * unavailable.  nrep = 0 restores the open-boundary walk. */
+gc_status gc_bh_set_periodic(gc_bh *bh, int32_t nrep, double L);
 gc_status gc_bh_sizes(gc_bh *bh, int64_t out[5]);
 /* Tree arrays (host, caller-allocated by gc_bh_sizes): any pointer may be NULL */
 gc_status gc_bh_get_tree(gc_bh *bh, double *center, double *half, double *mass, double *com,

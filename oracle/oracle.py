@@ -60,6 +60,8 @@ def lib():
         L.orc_eval_forces.argtypes = [C.POINTER(_Tree), C.c_int, f64p, f64p, i64p, i64p, i8p,
                                       C.c_int64, C.c_int64, C.c_double, C.c_double, f64p, C.c_int]
         L.orc_eval_potentials.argtypes = L.orc_eval_forces.argtypes
+        L.orc_periodic_forces.argtypes = [C.POINTER(_Tree), C.c_int, C.c_double, C.c_double, C.c_int, f64p, f64p,
+                                          C.c_int64, C.c_int64, C.c_double, C.c_double, f64p, i64p, i64p, C.c_int]
         L.orc_forces_from_points.argtypes = [C.c_int64, C.c_int64, C.c_int, f64p, f64p, f64p, f64p,
                                              C.c_double, C.c_double, f64p]
         L.orc_direct_forces.argtypes = [C.c_int64, C.c_int, f64p, f64p, C.c_double, C.c_double, f64p, C.c_int]
@@ -258,6 +260,29 @@ def eval_forces(tree: OracleTree, lists: OracleLists, positions, masses, g=1.0, 
     L.orc_eval_forces(C.byref(ct), tree.dim, _p(pos, f64p), _p(m, f64p), _p(ptr, i64p), _p(ids, i64p),
                       _p(kind, i8p), int(b0), int(b1), float(g), float(eps), _p(out, f64p), int(nthreads))
     return out
+
+
+def periodic_forces(tree: OracleTree, positions, masses, theta, L=1.0, nrep=1, g=1.0, eps=1e-4,
+                    bucket_range=None, nthreads=0):
+    """Periodic BH restatement (no reference implementation: parity
+    unpinned): every bucket walks the tree once per image shift of the box
+    (side L, (2 nrep + 1)^3 images) with shifted centres of mass in the
+    opening test; returns (forces, entries per bucket, items per bucket)."""
+    lb = lib()
+    ct = tree._ctree()
+    pos, m = _f64(positions), _f64(masses)
+    n = pos.shape[0]
+    out = np.zeros((n, 3))
+    nb = len(tree.buckets)
+    b0, b1 = (0, nb) if bucket_range is None else bucket_range
+    ent = np.zeros(nb, np.int64)
+    itm = np.zeros(nb, np.int64)
+    rc = lb.orc_periodic_forces(C.byref(ct), tree.dim, float(theta), float(L), int(nrep), _p(pos, f64p), _p(m, f64p),
+                                int(b0), int(b1), float(g), float(eps), _p(out, f64p), _p(ent, i64p), _p(itm, i64p),
+                                int(nthreads))
+    if rc != 0:
+        raise ValueError("orc_periodic_forces: bad arguments (3-D, 0 <= nrep <= 2)")
+    return out, ent, itm
 
 
 def eval_potentials(tree: OracleTree, lists: OracleLists, positions, masses, g=1.0, eps=1e-4,

@@ -57,6 +57,7 @@ SIGNATURES = {
     "gc_bh_destroy": [vp],
     "gc_bh_set_particles": [vp, C.c_int64, C.c_int32, f64p, f64p, C.c_double, C.c_int64],
     "gc_bh_sizes": [vp, i64p],
+    "gc_bh_set_periodic": [vp, C.c_int32, C.c_double],
     "gc_bh_set_force_mode": [vp, C.c_int32],
     "gc_bh_set_overlap": [vp, C.c_int32],
     "gc_bh_keys": [vp, C.c_int64, C.c_int32, f64p, C.c_double, u64p, u64p],

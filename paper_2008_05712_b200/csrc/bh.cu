@@ -243,6 +243,8 @@ void size_pool(gc_bh *bh, int64_t chunks)
 void walk_params(gc_bh *bh, double theta)
 {
     if (bh->params_valid && bh->cap_theta == theta) return;
+    GC_REQUIRE(bh->per_nrep == 0 || (bh->dim == 3 && bh->per_L == bh->box), GC_E_VALUE,
+               "the periodic walk needs a 3-D tree whose box is the periodic box");
     const double th2 = theta * theta;
     const double root = bh->box;
     // Per-level float32 thresholds on the float32 s ~ d^2 (walk_group_kernel).
@@ -253,7 +255,21 @@ void walk_params(gc_bh *bh, double theta)
     // so s > A certainly accepts when A - E(A) >= ta and s < R certainly rejects
     // when R + E(R) <= tr (both sides monotone in s there); A and R solve the
     // quadratics in sqrt(s), widened by 1e-6 and rounded outwards.
-    const double dd2 = bh->walk_dd2, dd3 = bh->walk_dd3, c = 4.8e-7, k = dd2 * std::sqrt(3.000001);
+    double dd2 = bh->walk_dd2, dd3 = bh->walk_dd3;
+    if (bh->per_nrep > 0) {
+        // periodic images: coordinates up to cmax + nrep L, one more float32
+        // rounding (com + shift) in every component
+        const double cp = bh->cmax + bh->per_nrep * bh->per_L;
+        const double delta = 1.25 * 8.0 * std::ldexp(1.0, -24) * cp;
+        dd2 = (float)(2.0 * delta * (1.0 + 1e-6));
+        dd3 = (float)(3.0 * delta * delta * (1.0 + 1e-6));
+        int e = 0;
+        std::frexp(cp, &e);
+        bh->cgrid_per = (float)std::ldexp(1.0, e - 24);
+        GC_REQUIRE(std::fmod(bh->per_L, (double)bh->cgrid_per) == 0.0, GC_E_VALUE,
+                   "periodic box side must be a multiple of the float32 coordinate grid");
+    }
+    const double c = 4.8e-7, k = dd2 * std::sqrt(3.000001);
     std::vector<float2> tt(MAX_LEVELS);
     for (int l = 0; l < MAX_LEVELS; ++l) {
         const double size = std::ldexp(root, -l);
@@ -280,8 +296,10 @@ void walk_params(gc_bh *bh, double theta)
     bh->wp.theta = theta;
     bh->wp.theta2 = th2;
     bh->wp.root_size = root;
-    bh->wp.dd2 = bh->walk_dd2;
-    bh->wp.dd3 = bh->walk_dd3;
+    bh->wp.dd2 = (float)dd2;
+    bh->wp.dd3 = (float)dd3;
+    bh->wp.nrep = bh->per_nrep;
+    bh->wp.per_L = bh->per_L;
     bh->wp.tt = bh->d_tt.p;
     bh->params_valid = true;
     bh->cap_theta = theta;
@@ -308,8 +326,9 @@ void launch_walk(gc_bh *bh, bool write, bool stats, int *fq = nullptr, int *fq_t
         bh->d_bstat.zero(s);
     }
     if (write) {
-        // first guess ~128 entries per bucket; an overflow grows it to the walk's demand
-        const int64_t guess = 2 * bh->n_buckets + 2 * (int64_t)nf + 64;
+        // first guess ~128 entries per bucket (and image); an overflow grows it to the walk's demand
+        const int64_t nimg = bh->per_nrep > 0 ? (int64_t)(2 * bh->per_nrep + 1) * (2 * bh->per_nrep + 1) * (2 * bh->per_nrep + 1) : 1;
+        const int64_t guess = (2 * bh->n_buckets + 2 * (int64_t)nf) * (nimg > 1 ? 4 : 1) + 64;
         if (bh->pool_chunks < guess) size_pool(bh, guess);
         bh->d_gfirst.resize(nf);
         bh->d_gcount.resize(nf);
@@ -328,6 +347,11 @@ void launch_walk(gc_bh *bh, bool write, bool stats, int *fq = nullptr, int *fq_t
     auto k = write ? (stats ? (nrec ? walk_group_kernel<true, true, true> : walk_group_kernel<true, true, false>)
                             : (nrec ? walk_group_kernel<true, false, true> : walk_group_kernel<true, false, false>))
                    : walk_group_kernel<false, true>;
+    if (bh->per_nrep > 0) {  // periodic walk: the image loop instances (fused force path only)
+        GC_REQUIRE(bh->force_fused, GC_E_STATE, "the periodic walk feeds the fused force path only");
+        k = write ? (stats ? walk_group_kernel<true, true, false, true> : walk_group_kernel<true, false, false, true>)
+                  : walk_group_kernel<false, true, false, true>;
+    }
     int per_sm = 0;
     GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * WARPS_PER_BLOCK, 0));
     const unsigned pgrid = (unsigned)std::max<int64_t>(
@@ -541,23 +565,17 @@ void ensure_union_complete(gc_bh *bh)
     while (walk_overflowed(bh)) launch_walk(bh, true, false);
 }
 
-// The default (fused) force kernel: sub-groups of FORCE_SUBT targets per warp
-// (force_sub_kernel), or FORCE_SUBT = 32: one warp per force group
-// (force_fused_kernel, the round-1 kernel; kept for A/B).
+// The default force kernel: the reorganisation into shared memory fused in
+// (PER: the periodic walk's image-tagged entries).
 using FusedFn = void (*)(int, const ForceGroup *, const UnionPool, const Staging, const float4 *, const float4 *,
                          const float4 *, const int *, const int *, const WalkGroup *, float, float, double, int,
-                         double *, double *);
-constexpr int kFusedItems = FORCE_SUBT >= 32 ? 1 : 32 / FORCE_SUBT;  // warp work items per force group
+                         double *, double *, int, double);
 template <bool OVL>
-FusedFn fused_kernel(bool eps0, bool pot)
+FusedFn fused_kernel(bool eps0, bool pot, bool per = false)
 {
-#if FORCE_SUBT >= 32
+    if (per) return eps0 ? force_fused_kernel<true, false, OVL, true> : force_fused_kernel<false, false, OVL, true>;
     return eps0 ? (pot ? force_fused_kernel<true, true, OVL> : force_fused_kernel<true, false, OVL>)
                 : (pot ? force_fused_kernel<false, true, OVL> : force_fused_kernel<false, false, OVL>);
-#else
-    return eps0 ? (pot ? force_sub_kernel<true, true, OVL, FORCE_SUBT> : force_sub_kernel<true, false, OVL, FORCE_SUBT>)
-                : (pot ? force_sub_kernel<false, true, OVL, FORCE_SUBT> : force_sub_kernel<false, false, OVL, FORCE_SUBT>);
-#endif
 }
 
 void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
@@ -592,22 +610,25 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
             S.order = lpt ? bh->d_fg_lpt.p : bh->d_fg_order.p;
             S.next = bh->d_next.p;
             GC_CUDA(cudaEventRecord(bh->ev[4], s));
-            auto k = fused_kernel<false>(eps0, pot);
+            const bool per = bh->per_nrep > 0;
+            GC_REQUIRE(!(per && pot), GC_E_STATE, "potentials are not evaluated by the periodic walk");
+            auto k = fused_kernel<false>(eps0, pot, per);
             if (nfg > 0) {
                 int per_sm = 0;
                 GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * WARPS_PER_BLOCK, 0));
                 const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(
-                    (int64_t)per_sm * ctx->prop.multiProcessorCount, grid_for(nfg * kFusedItems, WARPS_PER_BLOCK)));
+                    (int64_t)per_sm * ctx->prop.multiProcessorCount, grid_for(nfg, WARPS_PER_BLOCK)));
                 k<<<pgrid, 32 * WARPS_PER_BLOCK, 0, s>>>(nfg, bh->d_fg.p + f0, U, S, bh->d_parts.p, bh->d_rec_hi.p,
                                                          bh->d_rec_lo.p, bh->d_part_bucket.p, bh->d_porder.p,
-                                                         bh->d_wg.p, bh->cgrid, eps2, g, bh->dim, bh->d_out.p,
-                                                         bh->d_pot.p);
+                                                         bh->d_wg.p, per ? bh->cgrid_per : bh->cgrid, eps2, g, bh->dim,
+                                                         bh->d_out.p, bh->d_pot.p, bh->per_nrep, bh->per_L);
                 check_launch("force_fused_kernel");
             }
             if (!bh->orders_fresh) make_orders(bh);
             GC_CUDA(cudaEventRecord(bh->ev[3], s));
             return;
         }
+        GC_REQUIRE(bh->per_nrep == 0, GC_E_STATE, "the periodic walk feeds the fused force path only");
         // staging runs: exclusive scan of the rounded record counts
         ensure_grec(bh);
         bh->d_rbase.resize(nfg + 1);
@@ -732,7 +753,7 @@ void run_overlapped(gc_bh *bh, double theta, double g, double eps)
         int per_sm = 0;
         GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * WARPS_PER_BLOCK, 0));
         const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(
-            (int64_t)per_sm * ctx->prop.multiProcessorCount, grid_for(nfg * kFusedItems, WARPS_PER_BLOCK)));
+            (int64_t)per_sm * ctx->prop.multiProcessorCount, grid_for(nfg, WARPS_PER_BLOCK)));
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(pgrid);
         cfg.blockDim = dim3(32 * WARPS_PER_BLOCK);
@@ -748,7 +769,7 @@ void run_overlapped(gc_bh *bh, double theta, double g, double eps)
                                    (const float4 *)bh->d_rec_hi.p, (const float4 *)bh->d_rec_lo.p,
                                    (const int *)bh->d_part_bucket.p, (const int *)bh->d_porder.p,
                                    (const WalkGroup *)bh->d_wg.p, bh->cgrid, eps2, g, bh->dim, bh->d_out.p,
-                                   bh->d_pot.p));
+                                   bh->d_pot.p, 0, 0.0));
         check_launch("force_fused_kernel (overlap)");
     }
     // timings in this mode: walk = the whole overlapped step, force = 0
@@ -951,7 +972,8 @@ gc_status gc_bh_walk_forces_async(gc_bh *bh, double theta, double g, double eps)
         GC_REQUIRE(bh && bh->have_tree, GC_E_STATE, "no particles set");
         // the overlapped walk has no overflow re-walk: only for a (tree, theta)
         // whose pool was sized by a completed stats walk
-        if (bh->overlap && bh->force_fused && bh->stats_valid && bh->params_valid && bh->cap_theta == theta) {
+        if (bh->overlap && bh->force_fused && bh->per_nrep == 0 && bh->stats_valid && bh->params_valid &&
+            bh->cap_theta == theta) {
             run_overlapped(bh, theta, g, eps);
         } else {
             run_walk(bh, theta, true);
@@ -965,6 +987,25 @@ gc_status gc_bh_set_force_mode(gc_bh *bh, int32_t fused)
     return guard([&] {
         GC_REQUIRE(bh, GC_E_VALUE, "null argument");
         bh->force_fused = fused != 0;
+    });
+}
+
+gc_status gc_bh_set_periodic(gc_bh *bh, int32_t nrep, double L)
+{
+    return guard([&] {
+        GC_REQUIRE(bh, GC_E_VALUE, "null argument");
+        GC_REQUIRE(nrep == 0 || nrep == 1, GC_E_VALUE, "nrep must be 0 or 1 (27 images: the image index fits the entry tag)");
+        GC_REQUIRE(nrep == 0 || (L > 0.0 && (!bh->have_tree || (bh->dim == 3 && L == bh->box))), GC_E_VALUE,
+                   "the periodic box is the tree's 3-D box (L = box)");
+        if (bh->per_nrep != nrep || bh->per_L != L) {
+            bh->per_nrep = nrep;
+            bh->per_L = nrep ? L : 0.0;
+            bh->params_valid = false;  // thresholds and coordinate bounds change
+            bh->stats_valid = false;
+            bh->have_union = false;
+            bh->dev_lists_valid = false;
+            bh->orders_fresh = false;
+        }
     });
 }
 
@@ -1047,6 +1088,8 @@ gc_status gc_bh_get_lists(gc_bh *bh, int64_t *ptr, int64_t *ids, int8_t *kind, i
         if (item_count)
             for (int64_t b = 0; b < nb; ++b) item_count[b] = st[2 * b + 1];
         if (ids || kind) {
+            GC_REQUIRE(bh->per_nrep == 0, GC_E_STATE,
+                       "periodic lists carry image shifts: only per-bucket counts (ptr, item_count) are available");
             GC_REQUIRE(tot < (1ll << 31), GC_E_VALUE, "more than 2^31 list entries");
             const int f0 = wg_fg_first(bh, bh->rg0), nf = wg_fg_first(bh, bh->rg1 < 0 ? bh->n_wg : bh->rg1) - f0;
             UnionPool U = pool_view(bh);
@@ -1193,25 +1236,6 @@ gc_status gc_bh_pair_stats(gc_bh *bh, int64_t out[2])
         GC_REQUIRE(bh && bh->have_union && out, GC_E_STATE, "no device walk has run");
         cudaStream_t s = bh->ctx->stream;
         const int nf = bh->n_fg;
-#if FORCE_SUBT < 32
-        if (bh->force_fused) {  // the sub-group kernel's own accounting
-            ensure_union_complete(bh);
-            DBuf<unsigned long long> acc;
-            acc.resize(2);
-            acc.zero(s);
-            const int ni = nf * kFusedItems;
-            if (ni > 0)
-                sub_stats_kernel<FORCE_SUBT><<<grid_for(ni, WARPS_PER_BLOCK), 32 * WARPS_PER_BLOCK, 0, s>>>(
-                    nf, bh->d_fg.p, pool_view(bh), bh->d_part_bucket.p, bh->d_wg.p, acc.p);
-            check_launch("sub_stats_kernel");
-            unsigned long long h[2];
-            acc.download(h, 2, s);
-            GC_CUDA(cudaStreamSynchronize(s));
-            out[0] = (int64_t)h[0];
-            out[1] = (int64_t)h[1];
-            return;
-        }
-#endif
         std::vector<int> rec(nf);
         std::vector<ForceGroup> fg(nf);
         ensure_grec(bh);
@@ -1299,7 +1323,7 @@ gc_status gc_bh_step(gc_bh *bh, int64_t n, int32_t dim, const double *pos, const
     if (bh) bh->h2d = bh->d2h = 0;
     gc_status st = gc_bh_set_particles(bh, n, dim, pos, mass, box, bucket_size);
     if (st) return st;
-    if (bh->overlap && bh->force_fused) {
+    if (bh->overlap && bh->force_fused && bh->per_nrep == 0) {
         st = guard([&] {
             run_overlapped(bh, theta, g, eps);
             // a walk that overflowed the union pool is re-run (pool grown) before its forces count

@@ -76,7 +76,20 @@ struct WalkParams {
     double theta, theta2, root_size;
     float dd2, dd3;  // 2*delta and 3*delta^2: float32 coordinate error bound
     const float2 *tt;  // per level: s > x certainly accepts, s < y certainly rejects (error band folded in)
+    int nrep;  // periodic walk (PER instances): images {-nrep..nrep}^3 of the box ...
+    double per_L;  // ... of side per_L
 };
+
+// periodic images: index i = ((ix + nrep) s + iy + nrep) s + iz + nrep, s = 2 nrep + 1;
+// a union entry of image i carries node | i << IMG_SHIFT (node ids < 2^26)
+constexpr int IMG_SHIFT = 26;
+__host__ __device__ __forceinline__ void image_shift(int img, int nrep, double L, double sh[3])
+{
+    const int side = 2 * nrep + 1;
+    sh[0] = (img / (side * side) - nrep) * L;
+    sh[1] = ((img / side) % side - nrep) * L;
+    sh[2] = (img % side - nrep) * L;
+}
 
 // Walk record per node: float32 centre of mass and a packed word
 //   internal: (first_child << 3) | (n_child - 1)                   (>= 8)
@@ -156,7 +169,7 @@ struct UnionPool {
 #define WALK_UNROLL 2
 #endif
 constexpr int kWalkUnroll = WALK_UNROLL;  // sibling-loop unroll
-template <bool WRITE, bool STATS, bool NREC = false>
+template <bool WRITE, bool STATS, bool NREC = false, bool PER = false>
 __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, WALK_MINB)
 walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const ForceGroup *__restrict__ fgroups,
                   const float4 *__restrict__ recs, const double4 *__restrict__ com64,
@@ -264,6 +277,23 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
 #if WALK_PROF
     unsigned long long pv = 0, pa = 0, ph = 0, pe = 0;
 #endif
+    // periodic walk (PER): the same walk once per image of the box, node
+    // centres of mass shifted by the image vector; one chain per force group
+    const int nimg = PER ? (2 * P.nrep + 1) * (2 * P.nrep + 1) * (2 * P.nrep + 1) : 1;
+    for (int img = 0; img < nimg; ++img) {
+    if (sp < 0) break;  // stack overflow in an earlier image (flagged)
+    sp = 0;
+    float sx = 0.f, sy = 0.f, sz = 0.f;
+    double4 sh64 = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (PER) {
+        double sh[3];
+        image_shift(img, P.nrep, P.per_L, sh);
+        sx = (float)sh[0];
+        sy = (float)sh[1];
+        sz = (float)sh[2];
+        sh64 = make_double4(sh[0], sh[1], sh[2], 0.0);
+    }
+    const int img_tag = PER ? img << IMG_SHIFT : 0;
     // the root is a sibling group of one, tested by every bucket
     int first = 0, nc = 1, lvl = 0;
     u64 act = full;
@@ -287,9 +317,9 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
                 // 2 max(u, 0) = u + |u| exactly: an FADD (FMA pipe) instead of an
                 // FMNMX (ALU pipe, the walk's bottleneck); sv = 4 s exactly, and
                 // the level thresholds are stored x4 (tt_s)
-                const float u0 = fabsf(nd.x - bf[k].x) - bf[k].w;
-                const float u1 = fabsf(nd.y - bf[k].y) - bf[k].w;
-                const float u2 = fabsf(nd.z - bf[k].z) - bf[k].w;
+                const float u0 = fabsf((PER ? nd.x + sx : nd.x) - bf[k].x) - bf[k].w;
+                const float u1 = fabsf((PER ? nd.y + sy : nd.y) - bf[k].y) - bf[k].w;
+                const float u2 = fabsf((PER ? nd.z + sz : nd.z) - bf[k].z) - bf[k].w;
                 const float v0 = u0 + fabsf(u0), v1 = u1 + fabsf(u1), v2 = u2 + fabsf(u2);
 #else
                 const float v0 = fmaxf(fabsf(nd.x - bf[k].x) - bf[k].w, 0.f);
@@ -311,9 +341,16 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
 #pragma unroll
                 for (int k = 0; k < BPL; ++k) {
                     bool a = false;
-                    if ((unsure >> (lane + 32 * k)) & 1ull)
-                        a = mac_accept64(com64[node], ldexp(P.root_size, -lvl), bgeo[gd.bfirst + lane + 32 * k],
+                    if ((unsure >> (lane + 32 * k)) & 1ull) {
+                        double4 c64 = com64[node];
+                        if (PER) {  // float64 com + s (the periodic restatement, orc_periodic_forces)
+                            c64.x += sh64.x;
+                            c64.y += sh64.y;
+                            c64.z += sh64.z;
+                        }
+                        a = mac_accept64(c64, ldexp(P.root_size, -lvl), bgeo[gd.bfirst + lane + 32 * k],
                                          P.theta, P.theta2);
+                    }
                     acc |= (u64)__ballot_sync(0xffffffffu, a) << (32 * k);
                 }
             }
@@ -331,7 +368,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
 #endif
                 const unsigned ma = (unsigned)((acc & fgm) >> boff), mp = (unsigned)((part & fgm) >> boff);
                 const bool hit = (ma | mp) != 0u;
-                if (emits) *wp = make_int4(node, (int)ma, (int)mp, wd);
+                if (emits) *wp = make_int4(node | img_tag, (int)ma, (int)mp, wd);
                 w += hit ? 1 : 0;
                 wp += hit ? 1 : 0;
                 if (NREC) nrec += (ma ? 1 : 0) + (mp ? wr_pcount(wd) : 0);
@@ -379,6 +416,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
         lvl = slvl[sp];
         __syncwarp();
     }
+    }  // images
 #if WALK_PROF
     if (lane == 0) {
         atomicAdd(&g_walk_prof[0], pv);
@@ -894,13 +932,14 @@ __device__ __forceinline__ int ld_list(const int *p)
     return CG ? __ldcg(p) : *p;
 }
 constexpr int RING_LOW = RING / 2;  // produce while fewer records wait (RING >= RING_LOW + 33: one entry always fits)
-template <bool EPS0, bool POT, bool OVL = false>
+template <bool EPS0, bool POT, bool OVL = false, bool PER = false>
 __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, FORCE_MINB)
 force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U, const Staging S,
                    const float4 *__restrict__ parts, const float4 *__restrict__ rec_hi,
                    const float4 *__restrict__ rec_lo, const int *__restrict__ part_bucket,
                    const int *__restrict__ porder, const WalkGroup *__restrict__ wgroups, float cgrid, float eps2,
-                   double g, int dim, double *__restrict__ out, double *__restrict__ pot_out)
+                   double g, int dim, double *__restrict__ out, double *__restrict__ pot_out, int per_nrep = 0,
+                   double per_L = 0.0)
 {
     __shared__ __align__(16) float4 r_a[WARPS_PER_BLOCK][RING / 2];  // pairs: x0 x1 y0 y1
     __shared__ __align__(16) float4 r_b[WARPS_PER_BLOCK][RING / 2];  // pairs: z0 z1 m0 m1
@@ -986,19 +1025,31 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
                 const int total = ntake ? __shfl_sync(0xffffffffu, incl, ntake - 1) : 0;
                 if (take) {
                     const int r = wr + incl - cnt;
+                    // the frame origin of this entry's sources: F, or (periodic) F minus
+                    // the image shift -- exact: F and the shift are multiples of cgrid
+                    float ox = F.cx, oy = F.cy, oz = F.cz;
+                    int nid = en.x;
+                    if (PER) {
+                        double sh[3];
+                        image_shift(en.x >> IMG_SHIFT, per_nrep, per_L, sh);
+                        ox = F.cx - (float)sh[0];
+                        oy = F.cy - (float)sh[1];
+                        oz = F.cz - (float)sh[2];
+                        nid = en.x & ((1 << IMG_SHIFT) - 1);
+                    }
                     if (mx) {
 #if FUSED_PREFETCH > 1
-                        const bool pre = pf_base == ebase;
-                        const float4 h = pre ? h_pf : rec_hi[en.x], l = pre ? l_pf : rec_lo[en.x];
+                        const bool pre = !PER && pf_base == ebase;
+                        const float4 h = pre ? h_pf : rec_hi[nid], l = pre ? l_pf : rec_lo[nid];
 #else
-                        const float4 h = rec_hi[en.x], l = rec_lo[en.x];
+                        const float4 h = rec_hi[nid], l = rec_lo[nid];
 #endif
-                        put(r, (h.x - F.cx) + l.x, (h.y - F.cy) + l.y, (h.z - F.cz) + l.z, h.w, mx);
+                        put(r, (h.x - ox) + l.x, (h.y - oy) + l.y, (h.z - oz) + l.z, h.w, mx);
                     }
                     const float4 *src = parts + wr_pstart(en.w);
                     for (int k = 0; k < pc; ++k) {
                         const float4 q = src[k];
-                        put(r + hasnode + k, q.x - F.cx, q.y - F.cy, q.z - F.cz, q.w, my);
+                        put(r + hasnode + k, q.x - ox, q.y - oy, q.z - oz, q.w, my);
                     }
                 }
                 wr += total;
@@ -1015,8 +1066,8 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
                 pf_base = ebase;
 #if FUSED_PREFETCH > 1
                 if (en_pf.y) {
-                    h_pf = rec_hi[en_pf.x];
-                    l_pf = rec_lo[en_pf.x];
+                    h_pf = rec_hi[en_pf.x & ((1 << IMG_SHIFT) - 1)];
+                    l_pf = rec_lo[en_pf.x & ((1 << IMG_SHIFT) - 1)];
                 }
 #endif
             }
@@ -1092,272 +1143,6 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
     }
 }
 
-// ---------------------------------------------------------------------------
-// SUB-GROUP force kernel (A/B build knob, -DFORCE_SUBT=8): the force group's targets are
-// split into sub-groups of SUBT consecutive targets and one warp evaluates
-// one sub-group, lane = (target lane % SUBT, record phase lane / SUBT).  The
-// warp reorganises only the union entries some of ITS targets' buckets use
-// (node record and / or the opened bucket's particles) into its shared-memory
-// ring -- the paper's gather into a contiguous staging layout -- and the PH =
-// 32 / SUBT phases split that run: per step each phase takes one record pair
-// (FADD2/FFMA2/FMUL2 over the pair, one MUFU.RSQ per interaction).  A record
-// still reaches every lane of its phase (bucket mask -> mass 0 for the lanes
-// whose bucket does not use it), but fewer buckets share a sub-group run than
-// a 32-target run, so far fewer evaluated pairs are wasted (mask efficiency
-// 0.51 -> 0.73 at SUBT = 8 on configs[2], tools/mask_stats2.py).  fp32
-// partial sums of 8 terms per half are flushed to fp64 every UNIT records;
-// the phases' fp64 sums are added by shuffles at the end.  Measured on the
-// B200 (1M clustered): 1.48 ms at SUBT = 8, 2.24 at 4, 1.21 at 16 vs 0.88 ms
-// for the 32-target kernel -- every sub-group re-gathers its records (2.8x
-// the L2 gathers at SUBT = 8) and the gather latency, not the FP32 issue,
-// bounds the kernel; so the default stays FORCE_SUBT = 32.
-// ---------------------------------------------------------------------------
-#ifndef FORCE_SUBT
-#define FORCE_SUBT 32  // 32: one warp per force group (force_fused_kernel); 4 / 8 / 16: force_sub_kernel (measured slower, A/B only)
-#endif
-template <int SUBT>
-struct SubCfg {
-    static constexpr int PH = 32 / SUBT;  // record phases
-    static constexpr int NSUB = 32 / SUBT;  // sub-groups per force group (<= 32 targets)
-    static constexpr int STEP = 2 * PH;  // records per consumer step
-    static constexpr int UNIT = 8 * STEP;  // records per fp64 flush (8 per packed half per lane)
-    static constexpr int RING = UNIT + 64 <= 128 ? 128 : (UNIT + 64 <= 256 ? 256 : 512);  // >= UNIT + 33
-};
-template <bool EPS0, bool POT, bool OVL, int SUBT>
-__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, FORCE_MINB)
-force_sub_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U, const Staging S,
-                 const float4 *__restrict__ parts, const float4 *__restrict__ rec_hi, const float4 *__restrict__ rec_lo,
-                 const int *__restrict__ part_bucket, const int *__restrict__ porder,
-                 const WalkGroup *__restrict__ wgroups, float cgrid, float eps2, double g, int dim,
-                 double *__restrict__ out, double *__restrict__ pot_out)
-{
-    using C = SubCfg<SUBT>;
-    constexpr int RING_ = C::RING, UNIT = C::UNIT, PH = C::PH, NSUB = C::NSUB;
-    __shared__ __align__(16) float4 r_a[WARPS_PER_BLOCK][RING_ / 2];  // pairs: x0 x1 y0 y1
-    __shared__ __align__(16) float4 r_b[WARPS_PER_BLOCK][RING_ / 2];  // pairs: z0 z1 m0 m1
-    __shared__ __align__(16) unsigned r_m[WARPS_PER_BLOCK][RING_];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tl = lane % SUBT, ph = lane / SUBT;
-    float *ra = reinterpret_cast<float *>(r_a[warp]);
-    float *rb = reinterpret_cast<float *>(r_b[warp]);
-    unsigned *rm = r_m[warp];
-    const float2 e2 = f2(eps2, eps2);
-    auto put = [&](int pos, float x, float y, float z, float m, unsigned msk) {
-        const int q = pos & (RING_ - 1), o = (q >> 1) * 4 + (q & 1);
-        ra[o] = x;
-        ra[o + 2] = y;
-        rb[o] = z;
-        rb[o + 2] = m;
-        rm[q] = msk;
-    };
-    const int nitem = nfg * NSUB;
-    for (int slot = lane == 0 ? atomicAdd(S.next, 1) : 0;;) {
-        slot = __shfl_sync(0xffffffffu, slot, 0);
-        if (slot >= nitem) break;
-        const int fslot = slot / NSUB, sub = slot % NSUB;
-        int gi;
-        if (OVL) {  // overlap mode: wait until the walk published this force group (acquire)
-            if (lane == 0)
-                while ((gi = ld_acquire_gpu(S.fq + fslot)) < 0) __nanosleep(64);
-            gi = __shfl_sync(0xffffffffu, gi, 0);
-        } else {
-            gi = S.order[fslot];
-        }
-        const ForceGroup fg = fgroups[gi];
-        if (sub * SUBT >= fg.ntarget) {  // no targets in this sub-group
-            if (lane == 0) slot = atomicAdd(S.next, 1);
-            continue;
-        }
-        const int ti = sub * SUBT + tl;
-        const bool tgt = ti < fg.ntarget;
-        const int p = fg.pstart + (tgt ? ti : sub * SUBT);
-        const float4 xp = parts[p];
-        const unsigned mybit = tgt ? (1u << (part_bucket[p] - wgroups[fg.wg].bfirst - fg.boff)) : 0u;
-        const unsigned submask = __reduce_or_sync(0xffffffffu, mybit);  // the sub-group's buckets
-        const GroupFrame F = group_frame(xp, cgrid);
-        const float2 nx = f2(F.cx - xp.x, F.cx - xp.x), ny = f2(F.cy - xp.y, F.cy - xp.y),
-                     nz = f2(F.cz - xp.z, F.cz - xp.z);
-        double ax = 0.0, ay = 0.0, az = 0.0, ap = 0.0;
-        const int n = ld_list<OVL>(U.gcount + gi);
-        int chunk_cur = n > 0 ? ld_list<OVL>(U.gfirst + gi) : 0, cur_ci = 0;
-        int chunk_nxt = (n > CHUNK) ? ld_list<OVL>(U.cnext + chunk_cur) : 0;
-        int ebase = 0, wr = 0, rd = 0;
-        auto load_entry = [&](int e) {
-            int4 en = make_int4(0, 0, 0, 0);
-            if (e < n) {
-                const int c = (e / CHUNK == cur_ci) ? chunk_cur : chunk_nxt;
-                const int4 *ep = U.ent + (int64_t)c * CHUNK + (e & (CHUNK - 1));
-                en = OVL ? __ldcg(ep) : *ep;
-            }
-            return en;
-        };
-        int pf_base = -1;
-        int4 en_pf = make_int4(0, 0, 0, 0);
-        for (;;) {
-            // produce: the sub-group's entries, in order, while less than a unit waits
-            while (ebase < n && wr - rd < UNIT) {
-                const int e = ebase + lane;
-                const int4 en = pf_base == ebase ? en_pf : load_entry(e);
-                const unsigned mx = (unsigned)en.y, my = (unsigned)en.z;
-                const int hasnode = (mx & submask) ? 1 : 0;
-                const int pc = (my & submask) ? wr_pcount(en.w) : 0;
-                const int cnt = hasnode + pc;
-                int incl = cnt;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += t;
-                }
-                // RING - STEP: room for the end padding (one entry always fits: RING >= UNIT + 64)
-                const bool take = e < n && incl <= RING_ - C::STEP - (wr - rd);
-                const unsigned tm = __ballot_sync(0xffffffffu, take);
-                const int ntake = __popc(tm);  // incl is nondecreasing: the taken lanes are a prefix
-                const int total = ntake ? __shfl_sync(0xffffffffu, incl, ntake - 1) : 0;
-                if (take && cnt) {
-                    const int r = wr + incl - cnt;
-                    if (hasnode) {
-                        const float4 h = rec_hi[en.x], l = rec_lo[en.x];
-                        put(r, (h.x - F.cx) + l.x, (h.y - F.cy) + l.y, (h.z - F.cz) + l.z, h.w, mx);
-                    }
-                    const float4 *src = parts + wr_pstart(en.w);
-                    for (int k = 0; k < pc; ++k) {
-                        const float4 q = src[k];
-                        put(r + hasnode + k, q.x - F.cx, q.y - F.cy, q.z - F.cz, q.w, my);
-                    }
-                }
-                wr += total;
-                ebase += ntake;
-                if (ebase / CHUNK != cur_ci && ebase < n) {  // moved into the next chunk of the chain
-                    chunk_cur = chunk_nxt;
-                    cur_ci = ebase / CHUNK;
-                    chunk_nxt = ((cur_ci + 1) * CHUNK < n) ? ld_list<OVL>(U.cnext + chunk_cur) : 0;
-                }
-            }
-            if (ebase < n) {  // the next batch's entries load while this unit is consumed
-                en_pf = load_entry(ebase + lane);
-                pf_base = ebase;
-            }
-            int avail = wr - rd;
-            if (ebase >= n) {  // end of the run: pad to whole steps
-                const int padded = (wr + C::STEP - 1) & ~(C::STEP - 1);
-                if (wr + lane < padded) put(wr + lane, 0.f, 0.f, 0.f, 0.f, 0u);
-                wr = padded;
-                avail = wr - rd;
-                if (avail == 0) break;
-            } else if (avail < UNIT) {
-                continue;  // (unreachable: production stops only with a full unit)
-            }
-            const int take_rec = avail < UNIT ? avail : UNIT;
-            __syncwarp();
-            {
-                float2 sx = f2(0.f, 0.f), sy = f2(0.f, 0.f), sz = f2(0.f, 0.f), sp = f2(0.f, 0.f);
-                const int nstep = take_rec / C::STEP;
-#pragma unroll 2
-                for (int st = 0; st < nstep; ++st) {
-                    const int q = (rd + st * C::STEP + 2 * ph) & (RING_ - 1);  // this phase's record pair
-                    const float4 A = r_a[warp][q >> 1];
-                    const float4 B = r_b[warp][q >> 1];
-                    const uint2 km = *reinterpret_cast<const uint2 *>(rm + q);
-                    const float2 dx = __fadd2_rn(f2(A.x, A.y), nx);
-                    const float2 dy = __fadd2_rn(f2(A.z, A.w), ny);
-                    const float2 dz = __fadd2_rn(f2(B.x, B.y), nz);
-                    float2 r2 = __ffma2_rn(dz, dz, e2);
-                    r2 = __ffma2_rn(dy, dy, r2);
-                    r2 = __ffma2_rn(dx, dx, r2);
-                    float i0, i1;
-                    if (EPS0) {  // no softening floor: cube 1/r (r^6 may leave the float range)
-                        const float j0 = rsqrt_approx(r2.x), j1 = rsqrt_approx(r2.y);
-                        i0 = r2.x > kCubeFloor ? j0 * j0 * j0 : 0.f;  // coincident source (kernels.py:83-84)
-                        i1 = r2.y > kCubeFloor ? j1 * j1 * j1 : 0.f;
-                    } else {
-                        const float2 r6 = __fmul2_rn(__fmul2_rn(r2, r2), r2);
-                        i0 = rsqrt_approx(r6.x);
-                        i1 = rsqrt_approx(r6.y);
-                    }
-                    const float2 me = f2((km.x & mybit) ? B.z : 0.f, (km.y & mybit) ? B.w : 0.f);
-                    const float2 w = __fmul2_rn(me, f2(i0, i1));
-                    sx = __ffma2_rn(dx, w, sx);
-                    sy = __ffma2_rn(dy, w, sy);
-                    sz = __ffma2_rn(dz, w, sz);
-                    if (POT) {  // m / sqrt(r^2 + eps^2); coincident skipped (kernels.py:78-84: all dx == 0)
-                        const float2 wp = f2((dx.x != 0.f || dy.x != 0.f || dz.x != 0.f) ? w.x : 0.f,
-                                             (dx.y != 0.f || dy.y != 0.f || dz.y != 0.f) ? w.y : 0.f);
-                        sp = __ffma2_rn(wp, r2, sp);
-                    }
-                }
-                ax += (double)(sx.x + sx.y);
-                ay += (double)(sy.x + sy.y);
-                az += (double)(sz.x + sz.y);
-                if (POT) ap += (double)(sp.x + sp.y);
-            }
-            rd += take_rec;
-            __syncwarp();  // consumed slots are rewritten by the next production
-            if (ebase >= n && rd == wr) break;
-        }
-        // the phases' sums (fp64, fixed order)
-#pragma unroll
-        for (int o = SUBT; o < 32; o <<= 1) {
-            ax += __shfl_xor_sync(0xffffffffu, ax, o);
-            ay += __shfl_xor_sync(0xffffffffu, ay, o);
-            az += __shfl_xor_sync(0xffffffffu, az, o);
-            if (POT) ap += __shfl_xor_sync(0xffffffffu, ap, o);
-        }
-        if (tgt && ph == 0) {
-            const int orig = porder[p];
-            const double gm = g * (double)xp.w;
-            out[(int64_t)orig * dim + 0] = gm * ax;
-            if (dim > 1) out[(int64_t)orig * dim + 1] = gm * ay;
-            if (dim > 2) out[(int64_t)orig * dim + 2] = gm * az;
-            if (POT) pot_out[orig] = -gm * ap;
-        }
-        __syncwarp();
-        if (lane == 0) slot = atomicAdd(S.next, 1);
-    }
-}
-
-// Pair statistics of the sub-group kernel (gc_bh_pair_stats): per work item
-// its filtered run length R (records the sub-group's buckets use), padded to
-// whole steps; issued lane-pairs = 32 * padded / PH, target lane-pairs =
-// targets * padded.  One warp per (force group, sub-group).
-template <int SUBT>
-__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK)
-sub_stats_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U,
-                 const int *__restrict__ part_bucket, const WalkGroup *__restrict__ wgroups,
-                 unsigned long long *__restrict__ acc)
-{
-    using C = SubCfg<SUBT>;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int item = blockIdx.x * WARPS_PER_BLOCK + warp;
-    if (item >= nfg * C::NSUB) return;
-    const int gi = item / C::NSUB, sub = item % C::NSUB;
-    const ForceGroup fg = fgroups[gi];
-    if (sub * SUBT >= fg.ntarget) return;
-    const int ti = sub * SUBT + (lane % SUBT);
-    const bool tgt = ti < fg.ntarget;
-    const unsigned mybit = tgt ? (1u << (part_bucket[fg.pstart + ti] - wgroups[fg.wg].bfirst - fg.boff)) : 0u;
-    const unsigned submask = __reduce_or_sync(0xffffffffu, mybit);
-    const int ntg = min(SUBT, fg.ntarget - sub * SUBT);
-    const int n = U.gcount[gi];
-    int chunk = n > 0 ? U.gfirst[gi] : 0, r = 0;
-    for (int e0 = 0; e0 < n; e0 += CHUNK) {
-        if (e0 > 0) chunk = U.cnext[chunk];
-        for (int e = e0 + lane; e < min(n, e0 + CHUNK); e += 32) {
-            const int4 en = U.ent[(int64_t)chunk * CHUNK + (e & (CHUNK - 1))];
-            r += (((unsigned)en.y & submask) ? 1 : 0) + (((unsigned)en.z & submask) ? wr_pcount(en.w) : 0);
-        }
-    }
-    r = __reduce_add_sync(0xffffffffu, r);
-    if (lane == 0) {
-        const unsigned long long padded = (unsigned long long)((r + C::STEP - 1) / C::STEP * C::STEP);
-        atomicAdd(acc, 32ull * padded / C::PH);
-        atomicAdd(acc + 1, (unsigned long long)ntg * padded);
-    }
-}
-
-// Member kernel: one warp per work request (bucket), lanes split its list.
-// naddr/paddr are node ids (direct) or data-manager slots (staged pool);
-// node terms come from rec_hi/rec_lo[addr], particle terms from
-// src_parts[prange[addr].x + k].
 template <bool EPS0>
 __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK)
 force_member_kernel(int nmember, const int *__restrict__ member_bucket, const int2 *__restrict__ brange,

@@ -90,6 +90,11 @@ struct gc_bh {
     DBuf<int64_t> d_bstat;
     int64_t n_union = 0;
     float cgrid = 0.f;  // float32 ulp bound of every tree coordinate (force-group origins)
+    double cmax = 0.0;  // coordinate bound of the tree (set_tree_bounds)
+    // periodic walk (gc_bh_set_periodic): images {-nrep..nrep}^3 of the box of side per_L
+    int per_nrep = 0;
+    double per_L = 0.0;
+    float cgrid_per = 0.f;
     // per-bucket CSR (host-supplied lists)
     bool have_member_lists = false;
     DBuf<int64_t> d_nptr, d_pptr;
@@ -159,6 +164,7 @@ namespace gc {
 inline void set_tree_bounds(gc_bh *bh, double cmax)
 {
     cmax = std::max(cmax, 1e-30);
+    bh->cmax = cmax;
     // |v32 - v64| <= delta for every opening-test component (walk_group_kernel):
     // com rounding + two float32 subtractions, each <= 2^-24 * |operand|
     const double delta = 1.25 * 6.0 * std::ldexp(1.0, -24) * cmax;

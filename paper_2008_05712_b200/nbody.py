@@ -297,6 +297,27 @@ def interactions(tree: BucketTree) -> int:
     return int(out[0])
 
 
+def periodic_forces(tree: BucketTree, theta: float, nrep: int = 1, g: float = 1.0,
+                    eps: float = DEFAULT_SOFTENING):
+    """Periodic Barnes-Hut forces: every bucket walks the
+    tree once per image of the box ((2 nrep + 1)^3 images, the box of the
+    tree; nrep <= 1), the sources of image s at their position + s.  The long-range
+    remainder beyond the images is the ewald kernel class (ewald.py).
+    Returns (forces (n, 3), per-bucket entries, per-bucket items)."""
+    L.call("gc_bh_set_periodic", tree.handle, int(nrep), float(tree.ps.box))
+    try:
+        L.call("gc_bh_walk", tree.handle, float(theta))
+        out = np.zeros((tree.n, tree.dim))
+        L.call("gc_bh_forces", tree.handle, float(g), float(eps), L.ptr(out, L.f64p))
+        nb = int(tree.sizes()[1])
+        ptr, ic = np.zeros(nb + 1, np.int64), np.zeros(nb, np.int64)
+        L.call("gc_bh_get_lists", tree.handle, L.ptr(ptr, L.i64p), None, None, L.ptr(ic, L.i64p))
+    finally:
+        L.call("gc_bh_set_periodic", tree.handle, 0, 0.0)
+        tree._gen += 1
+    return out, np.diff(ptr), ic
+
+
 def direct_force_oracle(ps: ParticleSet, g: float = 1.0, eps: float = DEFAULT_SOFTENING) -> np.ndarray:
     """hr/workloads/nbody.py:202-213 on the GPU (exact float64 pair sums)."""
     from . import kernels

@@ -453,3 +453,29 @@ def test_plummer16m_config4_sampled_parity(nb):
         ntot += len(sel)
     L.call("gc_bh_set_range", tree.handle, 0, int(ngr[0]))
     assert ntot > 3 * 4096
+
+
+@pytest.mark.parametrize("n,seed,cl,nrep", [(20_000, 5, 0.6, 1), (4096, 9, None, 1), (3000, 2, 0.0, 1), (3000, 2, 0.0, 0)])
+def test_periodic_walk_matches_oracle(nb, n, seed, cl, nrep):
+    """Periodic BH (no reference implementation -- the float64
+    restatement oracle/gcharm_oracle.c orc_periodic_forces): per-bucket entry
+    and item counts over all (2 nrep + 1)^3 images bit-exact (every opening
+    decision, shifted centres of mass), forces within 1e-5 per particle; the
+    open-boundary path is untouched afterwards."""
+    from oracle import oracle as orc
+    from paper_2008_05712_b200 import generators as gen
+    ps = gen.fp32_exact(gen.gen_plummer(n, seed) if cl is None else gen.gen_particles(n, seed, cl, 3))
+    tree = nb.build_bucket_tree(ps, 8)
+    f, ent, itm = nb.periodic_forces(tree, 0.7, nrep=nrep)
+    ot = orc.build_bucket_tree(ps.positions, ps.masses, 8)
+    fo, eo, io = orc.periodic_forces(ot, ps.positions, ps.masses, 0.7, 1.0, nrep)
+    np.testing.assert_array_equal(ent, eo)
+    np.testing.assert_array_equal(itm, io)
+    assert rel_err(f, fo).max() <= FORCE_RTOL
+    lists = nb.build_interaction_lists(tree, 0.7, ps)
+    ol = orc.build_interaction_lists(ot, 0.7)
+    ptr, ids, kind, ic = lists.csr()
+    np.testing.assert_array_equal(ids, ol.ids)
+    assert rel_err(nb.eval_forces(tree, lists, ps), orc.eval_forces(ot, ol, ps.positions, ps.masses)).max() <= FORCE_RTOL
+    with pytest.raises(ValueError):
+        nb.periodic_forces(tree, 0.7, nrep=2)  # 125 images exceed the entry's image tag

@@ -182,3 +182,29 @@ def test_lj3d_multicore_baseline_matches_serial():
     f2, e2 = orc.lj3d_compute_forces(s.positions, d, s.cell_size, nthreads=4)
     np.testing.assert_allclose(f2, f1, rtol=0, atol=1e-11)
     np.testing.assert_allclose(e2, e1, rtol=0, atol=1e-11)
+
+
+def test_periodic_oracle_pinned():
+    """The periodic BH restatement (no reference implementation): nrep = 0 is
+    the open-boundary eval_forces bit for bit, and at theta = 0 (every node
+    opened) it equals an independent numpy direct sum over the 27 images."""
+    from paper_2008_05712_b200 import generators as gen
+    ps = gen.fp32_exact(gen.gen_particles(600, 4, clustering=0.5, dim=3))
+    t = orc.build_bucket_tree(ps.positions, ps.masses, 8)
+    f0, _, i0 = orc.periodic_forces(t, ps.positions, ps.masses, 0.7, 1.0, 0)
+    lists = orc.build_interaction_lists(t, 0.7)
+    np.testing.assert_array_equal(f0, orc.eval_forces(t, lists, ps.positions, ps.masses))
+    np.testing.assert_array_equal(i0, lists.item_count)
+    f, _, _ = orc.periodic_forces(t, ps.positions, ps.masses, 0.0, 1.0, 1)
+    p, m, eps = ps.positions, ps.masses, 1e-4
+    ref = np.zeros_like(p)
+    for ix in (-1, 0, 1):
+        for iy in (-1, 0, 1):
+            for iz in (-1, 0, 1):
+                q = p + np.array([ix, iy, iz], float)
+                d = q[None, :, :] - p[:, None, :]
+                r2 = eps * eps + (d * d).sum(axis=2)
+                same = np.all(d == 0.0, axis=2)
+                w = np.where(same, 0.0, m[None, :] / (r2 * np.sqrt(r2)))
+                ref += m[:, None] * (d * w[:, :, None]).sum(axis=1)
+    np.testing.assert_allclose(f, ref, rtol=1e-9, atol=1e-9 * np.abs(ref).max())
