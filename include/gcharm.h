@@ -229,6 +229,14 @@ gc_status gc_dm_evict(gc_dm *dm, int64_t needed_bytes, int64_t *evicted, int64_t
 /* lookup_residency (memory.py:78-93): resident[i] = 1 if ids[i] has a slot
  * (and its last_use_time becomes now) */
 gc_status gc_dm_lookup(gc_dm *dm, const int64_t *ids, int64_t n, double now, int8_t *resident);
+/* observe_indices (memory.py:252-256) into the SortedIndexArray
+ * (memory.py:125-179) held on the device: gc_dm_observe appends ids in order
+ * (every call = one insert per id, the reference's binary-insertion
+ * comparison count computed exactly from each insertion's set size and rank);
+ * gc_dm_sorted_index: out = {size, comparisons, inserts}, indices ascending
+ * (may be NULL). */
+gc_status gc_dm_observe(gc_dm *dm, const int64_t *ids, int64_t n);
+gc_status gc_dm_sorted_index(gc_dm *dm, int64_t out[3], int64_t *indices);
 /* out = {slot_count, free_slots, resident_buffers, id_universe} */
 gc_status gc_dm_state(gc_dm *dm, int64_t out[4]);
 /* resident table sorted by buffer id (ChareTable, memory.py:50-75) */

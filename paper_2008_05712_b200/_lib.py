@@ -110,6 +110,8 @@ SIGNATURES = {
     "gc_dm_evict": [vp, C.c_int64, i64p, i64p],
     "gc_dm_lookup": [vp, i64p, C.c_int64, C.c_double, i8p],
     "gc_dm_state": [vp, i64p],
+    "gc_dm_observe": [vp, i64p, C.c_int64],
+    "gc_dm_sorted_index": [vp, i64p, i64p],
     "gc_dm_table": [vp, i64p, i64p, f64p, i64p],
     "gc_md_create": [vp, C.POINTER(vp)],
     "gc_md_destroy": [vp],

@@ -375,6 +375,86 @@ __global__ void dm_batch_row(const int *__restrict__ cnt, int np_redundant, cons
     }
 }
 
+// --- SortedIndexArray on the device (hr/memory.py:125-179) ------------------
+// insert(idx) runs bisect over the current sorted distinct set (size m): the
+// loop's path depends only on (m, p), p = #elements < idx, so the comparison
+// count of every insertion follows from (m_k, p_k): m_k = distinct values seen
+// before element k, p_k = those smaller than its value -- a prefix rank query
+// answered by a merge-sort tree over the distinct values in first-seen order.
+__device__ __forceinline__ unsigned long long bisect_comparisons(int m, int p)
+{
+    int lo = 0, hi = m;
+    unsigned long long c = 0;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        ++c;
+        if (mid < p) lo = mid + 1;
+        else hi = mid;
+    }
+    return c + (p < m ? 1ull : 0ull);  // the equality probe (memory.py:171-174)
+}
+
+__global__ void obs_first_kernel(int n, const int *__restrict__ ids, const int *__restrict__ in_set,
+                                 int *__restrict__ firstpos)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n && !in_set[ids[k]]) atomicMin(&firstpos[ids[k]], k);
+}
+
+__global__ void obs_isnew_kernel(int n, const int *__restrict__ ids, const int *__restrict__ in_set,
+                                 const int *__restrict__ firstpos, unsigned char *__restrict__ flag,
+                                 int *__restrict__ cnt)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int v = ids[k];
+    flag[k] = !in_set[v] && firstpos[v] == k;
+    cnt[k] = flag[k];
+}
+
+// rank of v in the prefix T[0, m) through the merge-sort tree (level l =
+// sorted runs of 2^l, stride D between levels)
+__global__ void obs_query_kernel(int n, const int *__restrict__ ids, const int *__restrict__ mprefix, int D0, int D,
+                                 int levels, const int *__restrict__ tree, unsigned long long *__restrict__ cmp)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long c = 0;
+    if (k < n) {
+        const int v = ids[k];
+        const int m = D0 + mprefix[k];
+        int off = 0, p = 0;
+        for (int l = levels; l >= 0; --l) {
+            const int len = 1 << l;
+            if (m - off >= len) {
+                const int *run = tree + (int64_t)l * D + off;
+                int lo = 0, hi = len;  // lower_bound(v) in the run
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (run[mid] < v) lo = mid + 1;
+                    else hi = mid;
+                }
+                p += lo;
+                off += len;
+            }
+        }
+        c = bisect_comparisons(m, p);
+    }
+    // warp reduce + one atomic per warp
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(cmp, c);
+}
+
+__global__ void obs_mark_kernel(int n, const int *__restrict__ vals, int *__restrict__ in_set)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) in_set[vals[i]] = 1;
+}
+
+struct ObsSeg {  // segment offsets of a level: r * len, clamped to D
+    int len, D;
+    __host__ __device__ int operator()(int r) const { return min(r * len, D); }
+};
+
 void dm_kernel_spec(const char *cls, int64_t out[5])
 {
     // "ewald_member": ewald_slot_kernel; "force_slot": the member kernel
@@ -886,6 +966,94 @@ gc_status gc_dm_build_plan(gc_dm *dm, const int64_t *ids, const int64_t *bounds,
         }
         *n_transfer = (int64_t)dm->h_transfer.size();
         *n_positions = P;
+    });
+}
+
+/* observe_indices (hr/memory.py:252-256) feeding the SortedIndexArray
+ * (memory.py:125-179) on the device: ids appended in order; counters of the
+ * reference's binary insertion (comparisons, inserts) and the sorted set. */
+gc_status gc_dm_observe(gc_dm *dm, const int64_t *ids, int64_t n)
+{
+    return guard([&] {
+        GC_REQUIRE(dm && (ids || n == 0), GC_E_VALUE, "null argument");
+        if (n == 0) return;
+        gc_ctx *ctx = dm->ctx;
+        cudaStream_t s = ctx->stream;
+        const int N = upload_ids(dm, ids, n, dm->obs_ids);
+        if ((int64_t)dm->obs_in.n < dm->universe) {  // membership flags over the id universe
+            const size_t old = dm->obs_in.n;
+            dm->obs_in.grow(dm->universe, s);
+            GC_CUDA(cudaMemsetAsync(dm->obs_in.p + old, 0, (dm->obs_in.n - old) * sizeof(int), s));
+        }
+        if (dm->obs_cmp.n == 0) {
+            dm->obs_cmp.resize(1);
+            dm->obs_cmp.zero(s);
+        }
+        const int D0 = (int)dm->obs_n;
+        dm->obs_flag.resize(N);
+        dm->obs_m.resize(N + 1);
+        dm->obs_first.resize(N);
+        obs_first_kernel<<<grid_for(N, DM_TPB), DM_TPB, 0, s>>>(N, dm->obs_ids.p, dm->obs_in.p, dm->firstpos.p);
+        obs_isnew_kernel<<<grid_for(N, DM_TPB), DM_TPB, 0, s>>>(N, dm->obs_ids.p, dm->obs_in.p, dm->firstpos.p,
+                                                                dm->obs_flag.p, dm->obs_first.p);
+        dm_reset_firstpos<<<grid_for(N, DM_TPB), DM_TPB, 0, s>>>(N, dm->obs_ids.p, dm->firstpos.p);
+        cub_call(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceScan::ExclusiveSum(t, b, dm->obs_first.p, dm->obs_m.p, N, s);
+        });
+        // T = the current set (sorted) ++ this chunk's new values in first-seen order
+        dm->obs_new.resize(N);
+        dm->nsel.resize(1);
+        cub_call(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceSelect::Flagged(t, b, dm->obs_ids.p, dm->obs_flag.p, dm->obs_new.p, dm->nsel.p, N, s);
+        });
+        int Dn = 0;
+        GC_CUDA(cudaMemcpyAsync(&Dn, dm->nsel.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        GC_CUDA(cudaStreamSynchronize(s));
+        const int D = D0 + Dn;
+        int levels = 0;
+        while ((1 << levels) < D) ++levels;
+        dm->obs_tree.resize((size_t)(levels + 1) * std::max(D, 1));
+        if (D0) GC_CUDA(cudaMemcpyAsync(dm->obs_tree.p, dm->obs_set.p, D0 * sizeof(int), cudaMemcpyDeviceToDevice, s));
+        if (Dn) GC_CUDA(cudaMemcpyAsync(dm->obs_tree.p + D0, dm->obs_new.p, Dn * sizeof(int), cudaMemcpyDeviceToDevice, s));
+        for (int l = 1; l <= levels; ++l) {  // level l: runs of 2^l sorted
+            const int len = 1 << l, nseg = (D + len - 1) / len;
+            auto off = cub::TransformInputIterator<int, ObsSeg, cub::CountingInputIterator<int>>(
+                cub::CountingInputIterator<int>(0), ObsSeg{len, D});
+            cub_call(ctx, [&](void *t, size_t &b) {
+                return cub::DeviceSegmentedSort::SortKeys(t, b, dm->obs_tree.p, dm->obs_tree.p + (int64_t)l * D, D, nseg,
+                                                          off, off + 1, s);
+            });
+        }
+        obs_query_kernel<<<grid_for(N, DM_TPB), DM_TPB, 0, s>>>(N, dm->obs_ids.p, dm->obs_m.p, D0, D, levels,
+                                                                dm->obs_tree.p, dm->obs_cmp.p);
+        // the new set: the last level (fully sorted), membership of the new values
+        dm->obs_set.grow(std::max(D, 1), s);
+        GC_CUDA(cudaMemcpyAsync(dm->obs_set.p, dm->obs_tree.p + (int64_t)levels * D, D * sizeof(int),
+                                cudaMemcpyDeviceToDevice, s));
+        if (Dn) obs_mark_kernel<<<grid_for(Dn, DM_TPB), DM_TPB, 0, s>>>(Dn, dm->obs_new.p, dm->obs_in.p);
+        check_launch("gc_dm_observe");
+        dm->obs_n = D;
+        dm->obs_inserts += n;
+    });
+}
+
+/* The SortedIndexArray state: out = {size, comparisons, inserts}; indices
+ * (ascending, may be NULL) */
+gc_status gc_dm_sorted_index(gc_dm *dm, int64_t out[3], int64_t *indices)
+{
+    return guard([&] {
+        GC_REQUIRE(dm && out, GC_E_VALUE, "null argument");
+        cudaStream_t s = dm->ctx->stream;
+        unsigned long long c = 0;
+        if (dm->obs_cmp.n) dm->obs_cmp.download(&c, 1, s);
+        std::vector<int> v(dm->obs_n);
+        if (indices && dm->obs_n) dm->obs_set.download(v.data(), dm->obs_n, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        out[0] = dm->obs_n;
+        out[1] = (int64_t)c;
+        out[2] = dm->obs_inserts;
+        if (indices)
+            for (int64_t i = 0; i < dm->obs_n; ++i) indices[i] = v[i];
     });
 }
 

@@ -38,6 +38,12 @@ struct gc_dm {
     DBuf<int> dcnt;
     DBuf<signed char> kinds_s;
     bool free_stale = false;  // free_slots changed on the device (async plans)
+    // SortedIndexArray of the observed indices (hr/memory.py:125-179, 252-256):
+    // the sorted distinct set on the device, membership flags, counters
+    DBuf<int> obs_set, obs_in, obs_ids, obs_first, obs_m, obs_T, obs_tree, obs_new;
+    DBuf<unsigned char> obs_flag;
+    DBuf<unsigned long long> obs_cmp;
+    int64_t obs_n = 0, obs_inserts = 0;
 };
 
 namespace gc {

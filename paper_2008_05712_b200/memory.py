@@ -151,6 +151,44 @@ def insert_sorted_index(arr: SortedIndexArray, idx: int) -> int:
     return arr.insert(idx)
 
 
+class DeviceSortedIndex:
+    """The SortedIndexArray a DeviceMemory observes, held on the device
+    (gc_dm_observe / gc_dm_sorted_index): same indices, comparisons and
+    inserts as the reference's binary insertion (memory.py:125-179)."""
+
+    def __init__(self, mem: "DeviceMemory"):
+        self._mem = mem
+
+    def _state(self, with_indices: bool):
+        out = np.zeros(3, np.int64)
+        L.call("gc_dm_sorted_index", self._mem.handle, L.ptr(out, L.i64p), None)
+        idx = None
+        if with_indices:
+            idx = np.zeros(int(out[0]), np.int64)
+            L.call("gc_dm_sorted_index", self._mem.handle, L.ptr(out, L.i64p), L.ptr(idx, L.i64p))
+        return out, idx
+
+    def __len__(self):
+        return int(self._state(False)[0][0])
+
+    @property
+    def indices(self):
+        return self._state(True)[1].tolist()
+
+    @property
+    def comparisons(self) -> int:
+        return int(self._state(False)[0][1])
+
+    @property
+    def inserts(self) -> int:
+        return int(self._state(False)[0][2])
+
+    def position(self, idx: int):
+        a = self._state(True)[1]
+        k = int(np.searchsorted(a, idx))
+        return k if k < len(a) and a[k] == idx else None
+
+
 @dataclass
 class TransferPlan:
     to_transfer: list  # (buffer index, bytes)
@@ -210,7 +248,7 @@ class DeviceMemory:
                C.byref(self.handle))
         self.heap = DeviceHeap(self)
         self.table = ChareTable(self)
-        self.sorted_index = SortedIndexArray()
+        self.sorted_index = DeviceSortedIndex(self)
 
     def __del__(self):
         try:
@@ -245,9 +283,12 @@ class DeviceMemory:
             L.call("gc_dm_pin", self.handle, L.ptr(ids, L.i64p), len(ids), -1)
 
     def observe_indices(self, buffer_indices) -> None:
+        """Feed request indices into the per-class sorted array in REUSE_SORTED
+        mode (hr/memory.py:252-256) -- on the device (gc_dm_observe)."""
         if self.mode is MemoryMode.REUSE_SORTED:
-            for b in buffer_indices:
-                self.sorted_index.insert(int(b))
+            ids = L.i64(np.asarray(buffer_indices, np.int64).reshape(-1))
+            if len(ids):
+                L.call("gc_dm_observe", self.handle, L.ptr(ids, L.i64p), len(ids))
 
     # -- eviction ----------------------------------------------------------------
     def evict_slots(self, needed_bytes: int) -> list:
