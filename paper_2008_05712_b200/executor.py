@@ -246,8 +246,9 @@ class GpuForceExecutor:
                            plan.indirection_bytes, int(layout.total_transactions()), now, float(tm[0] + tm[1]), cls)
 
     # -- the force phase through the device batcher -----------------------------------
-    def _run_device_batcher(self, times) -> RunResult:
-        nb = len(self.ptr) - 1
+    def _run_device_batcher(self, times, buckets=None) -> RunResult:
+        owners = np.arange(len(self.ptr) - 1) if buckets is None else np.asarray(buckets, np.int64)
+        nb = len(owners)
         st = self.state
         res = RunResult(forces=None)
         t0 = time.perf_counter()
@@ -257,11 +258,18 @@ class GpuForceExecutor:
             bat = DeviceBatcher(self.tree, self.memory, st.max_size, st.timeout_factor, st.window, self.g, self.eps)
         self.runtime.submit_to_device("force", nb)
         try:  # the lists are the tree's device walk: submit them where they are
-            bat.submit_walk(np.arange(nb), times)
+            bat.submit_walk(owners, times)
         except HeteroRtError as e:
             if type(e) is not HeteroRtError:  # GC_E_STATE only (no device-resident lists): a host submission
                 raise
-            bat.submit(np.arange(nb), times, self.ptr, self.ids, self.kind)
+            if buckets is not None:  # the CSR of the listed buckets
+                lens = self.ptr[owners + 1] - self.ptr[owners]
+                sub = np.concatenate([[0], np.cumsum(lens)])
+                pos = np.concatenate([np.arange(self.ptr[b], self.ptr[b + 1]) for b in owners]) if len(owners) \
+                    else np.zeros(0, np.int64)
+                bat.submit(owners, times, sub, self.ids[pos], self.kind[pos])
+            else:
+                bat.submit(owners, times, self.ptr, self.ids, self.kind)
         bat.flush(float(times[-1]) if nb else 0.0)  # end of the phase (hr/timeline.py:276-298)
         rows, tms = bat.log()
         res.wall_s = time.perf_counter() - t0
@@ -279,15 +287,18 @@ class GpuForceExecutor:
         return res
 
     # -- the force phase ------------------------------------------------------------
-    def run(self, arrival_times=None) -> RunResult:
+    def run(self, arrival_times=None, buckets=None) -> RunResult:
         """One work request per bucket (DFS order) at `arrival_times` (default:
         back to back) -- plus its ewald request when enabled; returns the
-        forces and the per-batch log."""
+        forces and the per-batch log.  `buckets` (device batcher only): the
+        requests of these buckets alone (arrival_times per listed bucket)."""
         from .aggregator import make_combined
-        nb = len(self.ptr) - 1
+        nb = len(self.ptr) - 1 if buckets is None else len(buckets)
         times = np.zeros(nb) if arrival_times is None else np.asarray(arrival_times, float)
         if self.device_batcher and self.ewald is None and self.plan_log is None:
-            return self._run_device_batcher(times)
+            return self._run_device_batcher(times, buckets)
+        if buckets is not None:
+            raise ValueError("a bucket subset runs through the device batcher only")
         res = RunResult(forces=None)
         t0 = time.perf_counter()
         for b in range(nb):

@@ -125,18 +125,21 @@ def replay_forces(records, tree, lists, **executor_kw):
 # (hundreds of MB of text); the same records are kept in a compact binary
 # form: arrival times, the buffer CSR (ptr, ids), kinds and item counts.
 
-def dump_stream_npz(path, times, ptr, ids, item_count, kinds) -> None:
-    """One "force" record per bucket k: arrival times[k], buffers
-    ids[ptr[k]:ptr[k+1]] with kinds (0 node, 1 particle interaction),
-    item_count[k] -- the content of the text trace lines, binary."""
+def dump_stream_npz(path, times, ptr, ids, item_count, kinds, buckets=None) -> None:
+    """One "force" record per bucket k (or per bucket buckets[k]): arrival
+    times[k], buffers ids[ptr[k]:ptr[k+1]] with kinds (0 node, 1 particle
+    interaction), item_count[k] -- the content of the text trace lines, binary."""
+    extra = {} if buckets is None else {"buckets": np.asarray(buckets, np.int64)}
     np.savez(path, times=np.asarray(times, np.float64), ptr=np.asarray(ptr, np.int64),
              ids=np.asarray(ids, np.int32), kinds=np.asarray(kinds, np.int8),
-             item_count=np.asarray(item_count, np.int64))
+             item_count=np.asarray(item_count, np.int64), **extra)
 
 
 def load_stream_npz(path) -> dict:
     z = np.load(path)
     s = {k: z[k] for k in ("times", "ptr", "ids", "kinds", "item_count")}
+    if "buckets" in z:
+        s["buckets"] = z["buckets"]
     n = len(s["times"])
     if len(s["ptr"]) != n + 1 or len(s["item_count"]) != n or s["ptr"][-1] != len(s["ids"]):
         raise TraceFormatError(0, "inconsistent stream arrays")
@@ -150,9 +153,19 @@ def replay_stream(stream: dict, tree, lists, **executor_kw):
     be the tree's buckets in DFS order with their device-walk lists)."""
     from .executor import GpuForceExecutor
     ex = GpuForceExecutor(tree, lists, **executor_kw)
-    if len(stream["times"]) != len(ex.ptr) - 1:
-        raise ValueError(f"stream has {len(stream['times'])} records for {len(ex.ptr) - 1} buckets")
-    if not (np.array_equal(stream["ptr"], ex.ptr) and np.array_equal(stream["ids"], ex.ids)
-            and np.array_equal(stream["kinds"], ex.kind) and np.array_equal(stream["item_count"], ex.item_count)):
+    b = stream.get("buckets")
+    if b is None:
+        if len(stream["times"]) != len(ex.ptr) - 1:
+            raise ValueError(f"stream has {len(stream['times'])} records for {len(ex.ptr) - 1} buckets")
+        if not (np.array_equal(stream["ptr"], ex.ptr) and np.array_equal(stream["ids"], ex.ids)
+                and np.array_equal(stream["kinds"], ex.kind) and np.array_equal(stream["item_count"], ex.item_count)):
+            raise ValueError("stream records do not match the tree's interaction lists")
+        return ex.run(stream["times"])
+    # a sampled stream: the records of buckets b (configs[3] scale)
+    lens = ex.ptr[b + 1] - ex.ptr[b]
+    if not (np.array_equal(np.diff(stream["ptr"]), lens) and np.array_equal(stream["item_count"], ex.item_count[b])):
         raise ValueError("stream records do not match the tree's interaction lists")
-    return ex.run(stream["times"])
+    pos = np.concatenate([np.arange(ex.ptr[x], ex.ptr[x + 1]) for x in b]) if len(b) else np.zeros(0, np.int64)
+    if not (np.array_equal(stream["ids"], ex.ids[pos]) and np.array_equal(stream["kinds"], ex.kind[pos])):
+        raise ValueError("stream records do not match the tree's interaction lists")
+    return ex.run(stream["times"], buckets=b)
