@@ -310,7 +310,8 @@ void walk_params(gc_bh *bh, double theta)
 }
 
 // One walk launch over the handle's walk-group range (asynchronous).
-void launch_walk(gc_bh *bh, bool write, bool stats, int *fq = nullptr, int *fq_tail = nullptr, int fq_base = 0)
+void launch_walk(gc_bh *bh, bool write, bool stats, int *fq = nullptr, int *fq_tail = nullptr, int fq_base = 0,
+                 bool setup_only = false)
 {
     wait_orders(bh);
     cudaStream_t s = bh->ctx->stream;
@@ -360,6 +361,7 @@ void launch_walk(gc_bh *bh, bool write, bool stats, int *fq = nullptr, int *fq_t
     bh->d_wnext.zero(s);
     const bool ordered = WALK_LPT && bh->order_ng == ng && bh->order_rg0 == g0;
     if (WALK_COST_LPT) GC_CUDA(cudaMemsetAsync(bh->d_wcost.p + g0, 0, sizeof(int) * ng, s));
+    if (setup_only) return;  // the caller launches a kernel with the walk inside (walk_force_kernel)
     // with hints: 2 ng work items (heavy groups split in two, -1 padding)
     k<<<pgrid, 32 * WARPS_PER_BLOCK, 0, s>>>(ordered ? 2 * ng : ng, wg, bh->d_fg.p, bh->d_recs.p, bh->d_com64.p,
                                              bh->d_bgeo.p, bh->d_bgeo32.p, bh->wp, U, bh->d_bstat.p, bh->d_flag.p,
@@ -708,6 +710,18 @@ void launch_forces(gc_bh *bh, double g, double eps, bool pot = false)
 // each finished walk group's force groups to a device queue and the force
 // kernel, launched concurrently on a second stream, consumes them in that
 // order -- its blocks take the SM slots the walk's tail frees.
+// warps per block of walk_force_kernel that start on force groups
+// (GC_WF_FORCE_FIRST, 0 .. WARPS_PER_BLOCK - 1)
+static int wf_force_first()
+{
+    static const int v = [] {
+        const char *e = getenv("GC_WF_FORCE_FIRST");
+        const int x = e ? atoi(e) : 0;
+        return std::max(0, std::min(WARPS_PER_BLOCK - 1, x));
+    }();
+    return v;
+}
+
 void run_overlapped(gc_bh *bh, double theta, double g, double eps)
 {
     GC_REQUIRE(theta >= 0.0, GC_E_VALUE, "theta must be >= 0");
@@ -731,6 +745,36 @@ void run_overlapped(gc_bh *bh, double theta, double g, double eps)
     bh->d_next.resize(1);
     bh->d_next.zero(s);
     GC_CUDA(cudaEventRecord(bh->ev[0], s));
+    if (bh->overlap == 2 && nfg > 0 && f0 == 0) {  // one persistent kernel: walk items, then force groups (whole range)
+        const int g0w = bh->rg0, ng = (bh->rg1 < 0 ? bh->n_wg : bh->rg1) - g0w;
+        launch_walk(bh, true, false, nullptr, nullptr, 0, /*setup_only=*/true);
+        const float eps2 = (float)(eps * eps);
+        auto k = bh_use_cube(eps2) ? walk_force_kernel<true> : walk_force_kernel<false>;
+        int per_sm = 0;
+        GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * WARPS_PER_BLOCK, 0));
+        const unsigned pgrid = (unsigned)std::max(1, per_sm * ctx->prop.multiProcessorCount);
+        const bool ordered = WALK_LPT && bh->order_ng == ng && bh->order_rg0 == g0w;
+        UnionPool U = pool_view(bh);
+        Staging S{};
+        S.next = bh->d_next.p;
+        S.fq = bh->d_fq.p;
+        k<<<pgrid, 32 * WARPS_PER_BLOCK, 0, s>>>(
+            ordered ? 2 * ng : ng, bh->d_wg.p + g0w, bh->d_fg.p, bh->d_recs.p, bh->d_com64.p, bh->d_bgeo.p,
+            bh->d_bgeo32.p, bh->wp, U, bh->d_bstat.p, bh->d_flag.p, ordered ? bh->d_wg_order.p : nullptr,
+            bh->d_wnext.p, WALK_COST_LPT ? bh->d_wcost.p + g0w : nullptr, bh->d_fq.p, bh->d_fq_tail.p, f0, nfg, S,
+            bh->d_parts.p, bh->d_rec_hi.p, bh->d_rec_lo.p, bh->d_part_bucket.p, bh->d_porder.p, bh->cgrid, eps2, g,
+            bh->dim, bh->d_out.p, wf_force_first());
+        check_launch("walk_force_kernel");
+        bh->have_union = true;
+        bh->dev_lists_valid = false;
+        bh->have_member_lists = false;
+        GC_CUDA(cudaEventRecord(bh->ev[1], s));
+        GC_CUDA(cudaEventRecord(bh->ev[2], s));
+        GC_CUDA(cudaEventRecord(bh->ev[4], s));
+        GC_CUDA(cudaEventRecord(bh->ev[3], s));
+        if (!bh->orders_fresh) make_orders(bh);
+        return;
+    }
     launch_walk(bh, true, false, bh->d_fq.p, bh->d_fq_tail.p, f0);
     bh->have_union = true;
     bh->dev_lists_valid = false;
@@ -960,7 +1004,8 @@ gc_status gc_bh_set_overlap(gc_bh *bh, int32_t on)
 {
     return guard([&] {
         GC_REQUIRE(bh, GC_E_VALUE, "null argument");
-        bh->overlap = on != 0;
+        GC_REQUIRE(on >= 0 && on <= 2, GC_E_VALUE, "overlap mode 0, 1 or 2");
+        bh->overlap = on;
     });
 }
 

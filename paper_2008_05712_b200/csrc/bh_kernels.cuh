@@ -169,23 +169,31 @@ struct UnionPool {
 #define WALK_UNROLL 2
 #endif
 constexpr int kWalkUnroll = WALK_UNROLL;  // sibling-loop unroll
-template <bool WRITE, bool STATS, bool NREC = false, bool PER = false>
-__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, WALK_MINB)
-walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const ForceGroup *__restrict__ fgroups,
-                  const float4 *__restrict__ recs, const double4 *__restrict__ com64,
-                  const double4 *__restrict__ bgeo, const float4 *__restrict__ bgeo32, const WalkParams P,
-                  UnionPool U, int64_t *__restrict__ bstat, int *__restrict__ flag, const int *__restrict__ order,
-                  int *__restrict__ next, int *__restrict__ wcost, int *__restrict__ fq = nullptr,
-                  int *__restrict__ fq_tail = nullptr, int fq_base = 0)
+#define WALK_ARGS_DECL                                                                                         \
+    int ngroups, const WalkGroup *__restrict__ groups, const ForceGroup *__restrict__ fgroups,                  \
+        const float4 *__restrict__ recs, const double4 *__restrict__ com64, const double4 *__restrict__ bgeo,   \
+        const float4 *__restrict__ bgeo32, const WalkParams P, UnionPool U, int64_t *__restrict__ bstat,        \
+        int *__restrict__ flag, const int *__restrict__ order, int *__restrict__ next, int *__restrict__ wcost,  \
+        int *__restrict__ fq, int *__restrict__ fq_tail, int fq_base
+#define WALK_ARGS ngroups, groups, fgroups, recs, com64, bgeo, bgeo32, P, U, bstat, flag, order, next, wcost, fq, fq_tail, fq_base
+// per-warp walk stack: pending sibling groups (first | (nc - 1) << NODE_BITS,
+// active buckets 0-31), active buckets 32-63, level
+struct WalkSmem {
+    int2 stack[STACK_CAP];
+    unsigned act_hi[STACK_CAP];
+    unsigned char lvl[STACK_CAP];
+};
+// level thresholds into shared memory (block-wide, before any warp walks)
+__device__ __forceinline__ void load_thresholds(const WalkParams &P, float2 *tt_s)
 {
-    using u64 = unsigned long long;
-    __shared__ int2 stack_s[WARPS_PER_BLOCK][STACK_CAP];  // (first | (nc - 1) << NODE_BITS, active buckets 0-31)
-    __shared__ unsigned act_hi_s[WARPS_PER_BLOCK][STACK_CAP];  // active buckets 32-63
-    __shared__ unsigned char lvl_s[WARPS_PER_BLOCK][STACK_CAP];
-    __shared__ float2 tt_s[MAX_LEVELS];
     for (int i = threadIdx.x; i < MAX_LEVELS; i += blockDim.x)
         tt_s[i] = WALK_RELU_ADD ? make_float2(4.f * P.tt[i].x, 4.f * P.tt[i].y) : P.tt[i];
     __syncthreads();
+}
+template <bool WRITE, bool STATS, bool NREC, bool PER>
+__device__ __forceinline__ void walk_group_body(WALK_ARGS_DECL, WalkSmem &ws, float2 *tt_s)
+{
+    using u64 = unsigned long long;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // persistent warps: walk groups handed out dynamically, in `order` (heaviest
     // first, from the previous walk of this tree) when known
@@ -247,9 +255,9 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
         full &= (bhi >= 64 ? ~0ull : ((1ull << bhi) - 1ull)) & ~((1ull << blo) - 1ull);
     }
     const u64 exact = ~inexact;
-    int2 *stack = stack_s[warp];
-    unsigned *sact = act_hi_s[warp];
-    unsigned char *slvl = lvl_s[warp];
+    int2 *stack = ws.stack;
+    unsigned *sact = ws.act_hi;
+    unsigned char *slvl = ws.lvl;
     int sp = 0;
     // lane f < nfg emits the list of force group fg_first + f (masks shifted to
     // its own buckets); its current chunk always has room for slot w % CHUNK
@@ -449,6 +457,21 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
         }
     }
     }  // persistent loop
+}
+
+template <bool WRITE, bool STATS, bool NREC = false, bool PER = false>
+__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, WALK_MINB)
+walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const ForceGroup *__restrict__ fgroups,
+                  const float4 *__restrict__ recs, const double4 *__restrict__ com64,
+                  const double4 *__restrict__ bgeo, const float4 *__restrict__ bgeo32, const WalkParams P,
+                  UnionPool U, int64_t *__restrict__ bstat, int *__restrict__ flag, const int *__restrict__ order,
+                  int *__restrict__ next, int *__restrict__ wcost, int *__restrict__ fq = nullptr,
+                  int *__restrict__ fq_tail = nullptr, int fq_base = 0)
+{
+    __shared__ WalkSmem ws_s[WARPS_PER_BLOCK];
+    __shared__ float2 tt_s[MAX_LEVELS];
+    load_thresholds(P, tt_s);
+    walk_group_body<WRITE, STATS, NREC, PER>(WALK_ARGS, ws_s[threadIdx.x >> 5], tt_s);
 }
 
 // Per-bucket walk_order / kind CSR from the union lists (parity + drop-in API):
@@ -932,22 +955,26 @@ __device__ __forceinline__ int ld_list(const int *p)
     return CG ? __ldcg(p) : *p;
 }
 constexpr int RING_LOW = RING / 2;  // produce while fewer records wait (RING >= RING_LOW + 33: one entry always fits)
-template <bool EPS0, bool POT, bool OVL = false, bool PER = false>
-__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, FORCE_MINB)
-force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U, const Staging S,
-                   const float4 *__restrict__ parts, const float4 *__restrict__ rec_hi,
-                   const float4 *__restrict__ rec_lo, const int *__restrict__ part_bucket,
-                   const int *__restrict__ porder, const WalkGroup *__restrict__ wgroups, float cgrid, float eps2,
-                   double g, int dim, double *__restrict__ out, double *__restrict__ pot_out, int per_nrep = 0,
-                   double per_L = 0.0)
+#define FORCE_ARGS_DECL                                                                                        \
+    int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U, const Staging S,                        \
+        const float4 *__restrict__ parts, const float4 *__restrict__ rec_hi, const float4 *__restrict__ rec_lo,  \
+        const int *__restrict__ part_bucket, const int *__restrict__ porder, const WalkGroup *__restrict__ wgroups, \
+        float cgrid, float eps2, double g, int dim, double *__restrict__ out, double *__restrict__ pot_out,     \
+        int per_nrep, double per_L
+#define FORCE_ARGS nfg, fgroups, U, S, parts, rec_hi, rec_lo, part_bucket, porder, wgroups, cgrid, eps2, g, dim, out, pot_out, per_nrep, per_L
+// per-warp ring of the fused force kernel: record pairs (x0 x1 y0 y1 | z0 z1 m0 m1) + masks
+struct RingSmem {
+    float4 a[RING / 2];
+    float4 b[RING / 2];
+    unsigned m[RING];
+};
+template <bool EPS0, bool POT, bool OVL, bool PER>
+__device__ __forceinline__ void force_fused_body(FORCE_ARGS_DECL, RingSmem &rs)
 {
-    __shared__ __align__(16) float4 r_a[WARPS_PER_BLOCK][RING / 2];  // pairs: x0 x1 y0 y1
-    __shared__ __align__(16) float4 r_b[WARPS_PER_BLOCK][RING / 2];  // pairs: z0 z1 m0 m1
-    __shared__ __align__(16) unsigned r_m[WARPS_PER_BLOCK][RING];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float *ra = reinterpret_cast<float *>(r_a[warp]);
-    float *rb = reinterpret_cast<float *>(r_b[warp]);
-    unsigned *rm = r_m[warp];
+    float *ra = reinterpret_cast<float *>(rs.a);
+    float *rb = reinterpret_cast<float *>(rs.b);
+    unsigned *rm = rs.m;
     const float2 e2 = f2(eps2, eps2);
     // record pos -> ring: pair (pos % RING) / 2, half pos & 1
     auto put = [&](int pos, float x, float y, float z, float m, unsigned msk) {
@@ -1082,8 +1109,8 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
             // consume every complete PFLUSH group
             for (; wr - rd >= PFLUSH; rd += PFLUSH) {
                 const int q0 = rd & (RING - 1);
-                const float4 *qa = r_a[warp] + q0 / 2;
-                const float4 *qb = r_b[warp] + q0 / 2;
+                const float4 *qa = rs.a + q0 / 2;
+                const float4 *qb = rs.b + q0 / 2;
                 const unsigned *qm = rm + q0;
                 float2 sx = f2(0.f, 0.f), sy = f2(0.f, 0.f), sz = f2(0.f, 0.f), sp = f2(0.f, 0.f);
 #pragma unroll
@@ -1141,6 +1168,56 @@ force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionP
         __syncwarp();
         if (lane == 0) slot = atomicAdd(S.next, 1);
     }
+}
+
+template <bool EPS0, bool POT, bool OVL = false, bool PER = false>
+__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, FORCE_MINB)
+force_fused_kernel(int nfg, const ForceGroup *__restrict__ fgroups, const UnionPool U, const Staging S,
+                   const float4 *__restrict__ parts, const float4 *__restrict__ rec_hi,
+                   const float4 *__restrict__ rec_lo, const int *__restrict__ part_bucket,
+                   const int *__restrict__ porder, const WalkGroup *__restrict__ wgroups, float cgrid, float eps2,
+                   double g, int dim, double *__restrict__ out, double *__restrict__ pot_out, int per_nrep = 0,
+                   double per_L = 0.0)
+{
+    __shared__ __align__(16) RingSmem rs_s[WARPS_PER_BLOCK];
+    force_fused_body<EPS0, POT, OVL, PER>(FORCE_ARGS, rs_s[threadIdx.x >> 5]);
+}
+
+// WALK + FORCE in one persistent kernel (gc_bh_set_overlap(2)): every warp
+// first takes walk items (publishing each walk group's force groups to the
+// readiness queue), then, with the walk's items exhausted, force groups in
+// publication order -- the ALU-bound walk and the FP-bound force loop share
+// the SMs instead of running back to back.  No deadlock: a force warp only
+// waits for force groups of walk items that resident warps of this same
+// grid have claimed.
+#ifndef WF_MINB
+#define WF_MINB 3
+#endif
+template <bool EPS0>
+__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, WF_MINB)
+walk_force_kernel(WALK_ARGS_DECL, int nfg, const Staging S, const float4 *__restrict__ parts,
+                  const float4 *__restrict__ rec_hi, const float4 *__restrict__ rec_lo,
+                  const int *__restrict__ part_bucket, const int *__restrict__ porder, float cgrid, float eps2,
+                  double g, int dim, double *__restrict__ out, int force_first)
+{
+    // a warp is in its walk phase or in its force phase: one private region
+    // per warp holds either view
+    union __align__(16) WarpSmem {
+        WalkSmem w;
+        RingSmem r;
+    };
+    __shared__ WarpSmem u_s[WARPS_PER_BLOCK];
+    __shared__ float2 tt_s[MAX_LEVELS];
+    WarpSmem &u = u_s[threadIdx.x >> 5];
+    load_thresholds(P, tt_s);
+    // warps (threadIdx.x >> 5) < force_first consume force groups from the
+    // readiness queue from the start (co-resident with the walking warps on
+    // every SM), then help with any walk items left; the others walk first
+    const bool ff = (int)(threadIdx.x >> 5) < force_first;
+    if (!ff) walk_group_body<true, false, false, false>(WALK_ARGS, u.w, tt_s);
+    __syncwarp();
+    force_fused_body<EPS0, false, true, false>(nfg, fgroups, U, S, parts, rec_hi, rec_lo, part_bucket, porder, groups,
+                                               cgrid, eps2, g, dim, out, nullptr, 0, 0.0, u.r);
 }
 
 template <bool EPS0>

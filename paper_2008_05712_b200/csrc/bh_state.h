@@ -30,7 +30,7 @@ struct gc_bh {
     bool have_tree = false;
     bool host_tree_valid = false;
     bool force_fused = true;
-    bool overlap = false;  // walk and force kernel of a step overlap (gc_bh_set_overlap; fused mode; measured neutral)
+    int overlap = 0;  // 1: the force kernel a PDL dependent of the walk (measured neutral); 2: one walk + force kernel (gc_bh_set_overlap)
     cudaStream_t force_stream = nullptr;
     cudaEvent_t ov_pre = nullptr, ov_done = nullptr;
     DBuf<int> d_fq, d_fq_tail;

@@ -303,7 +303,8 @@ def test_pair_stats_bounds():
 def test_overlapped_step_bit_identical():
     """gc_bh_walk_forces_async with the walk/force overlap (programmatic
     dependent launch + readiness queue) gives exactly the forces of the
-    back-to-back kernels; so does gc_bh_step."""
+    back-to-back kernels; so does the one persistent walk+force kernel
+    (overlap mode 2) and gc_bh_step."""
     from paper_2008_05712_b200 import _lib as L
     from paper_2008_05712_b200 import generators as gen
     from paper_2008_05712_b200 import nbody
@@ -312,7 +313,7 @@ def test_overlapped_step_bit_identical():
     tree = nbody.build_bucket_tree(ps, 8)
     L.call("gc_bh_walk", tree.handle, 0.7)  # stats walk: the overlapped path needs known lists
     out = {}
-    for ov in (0, 1, 1):
+    for ov in (0, 1, 1, 2, 2):
         L.call("gc_bh_set_overlap", tree.handle, ov)
         L.call("gc_bh_walk_forces_async", tree.handle, 0.7, 1.0, 1e-4)
         f = np.zeros((n, 3))
@@ -321,9 +322,10 @@ def test_overlapped_step_bit_identical():
             np.testing.assert_array_equal(f, out[ov])
         out[ov] = f
     np.testing.assert_array_equal(out[0], out[1])
+    np.testing.assert_array_equal(out[0], out[2])
     st = nbody.BHStep(8, 0.7, 1.0, 1e-4)
     g = np.zeros((n, 3))
-    for ov in (1, 0):
+    for ov in (1, 2, 0):
         L.call("gc_bh_set_overlap", st.handle, ov)
         st(ps.positions, ps.masses, 1.0, g)
         np.testing.assert_array_equal(g, out[0])
