@@ -68,6 +68,46 @@ __global__ void bb_keys(int n, int dim, const double *__restrict__ pos, double b
     idx[i] = i;
 }
 
+// power-of-two box: every centre of the descent is an exact dyadic multiple of
+// the box (no rounding in c +- half/2), so x >= c at level L is bit L of the
+// fixed-point t = x / box (exact scaling) -- integer digits, same keys
+__device__ __forceinline__ unsigned long long spread3(unsigned long long x)  // bit j -> bit 3j (21 bits)
+{
+    x &= 0x1fffffull;
+    x = (x | x << 32) & 0x1f00000000ffffull;
+    x = (x | x << 16) & 0x1f0000ff0000ffull;
+    x = (x | x << 8) & 0x100f00f00f00f00full;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+    x = (x | x << 2) & 0x1249249249249249ull;
+    return x;
+}
+
+__global__ void bb_keys_dyadic(int n, int dim, const double *__restrict__ pos, double inv_box, int nlev,
+                               unsigned long long *__restrict__ k1, unsigned long long *__restrict__ k2,
+                               int *__restrict__ idx)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double scale = ldexp(1.0, nlev);
+    const unsigned long long top = (1ull << nlev) - 1ull;
+    unsigned long long a = 0, b = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (k >= dim) break;
+        const double t = pos[(int64_t)i * dim + k] * inv_box;
+        // m: the nlev digits of this coordinate, level 0 in bit nlev - 1
+        const unsigned long long m = t >= 1.0 ? top : (t >= 0.0 ? (unsigned long long)(t * scale) : 0ull);  // NaN: 0
+        // levels 0..20 -> k1 (level L at bit 3 (20 - L) + k), levels 21..41 -> k2
+        const unsigned long long hi = nlev >= 21 ? m >> (nlev - 21) : m << (21 - nlev);
+        const unsigned long long lo = nlev > 21 ? m << (42 - nlev) : 0ull;
+        a |= spread3(hi) << k;
+        b |= spread3(lo) << k;
+    }
+    k1[i] = a;
+    k2[i] = b;
+    idx[i] = i;
+}
+
 // a run of more than `bucket` equal sorted keys (above bit `shift`): some node
 // at the deepest sorted level still splits
 __global__ void bb_long_runs(int n, int bucket, const unsigned long long *__restrict__ ks, int shift,
@@ -352,6 +392,146 @@ __global__ void __launch_bounds__(BB_TPB) bb_levels_coop(LevelArgs A)
 
 
 
+// ---------------------------------------------------------------------------
+// Bottom-up enumeration of the same tree (no forced cubes): no level loop, no
+// grid-wide barrier.  With d_i = common prefix (levels) of sorted keys i-1, i
+// and e_i = common prefix of keys i, i+bucket:
+//   * particle i starts a level-L run iff L > d_i;
+//   * a run is longer than `bucket` (its node splits, below level nlev) iff it
+//     holds a window [j, j + bucket] with e_j >= its level -- so the level-d_i
+//     run around i splits iff max(e_j, j in [i - bucket, i]) >= d_i, and the
+//     run starting at i at level L >= d_i + 1 splits iff e_i >= L;
+//   * a splitting run's ancestors are longer still: they split too.
+// Hence particle i starts the nodes of levels a_i = d_i + 1 .. c_i =
+// max(a_i, min(e_i + 1, nlev)) when its parent run splits (none otherwise),
+// and the node of level c_i is a bucket.  Level-order ids (the reference's
+// breadth-first numbering, nbody.py:110-123) are ONE exclusive scan over
+// per-level bitmaps of run starts, level-major; an extra row numbers the
+// buckets in start order (= depth-first order).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int key_lcp(unsigned long long a1, unsigned long long a2, unsigned long long b1,
+                                       unsigned long long b2, int cap)
+{
+    const unsigned long long x1 = a1 ^ b1, x2 = a2 ^ b2;
+    const int l = x1 ? (__clzll(x1) - 1) / 3 : (x2 ? 21 + (__clzll(x2) - 1) / 3 : 42);  // bit 63 unused
+    return min(l, cap);
+}
+
+__global__ void bb_lcp(int n, int bucket, int cap, const unsigned long long *__restrict__ k1,
+                       const unsigned long long *__restrict__ k2, signed char *__restrict__ d,
+                       signed char *__restrict__ e)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long a1 = k1[i], a2 = k2[i];
+    d[i] = (signed char)(i == 0 ? -1 : key_lcp(k1[i - 1], k2[i - 1], a1, a2, cap));
+    e[i] = (signed char)(i + bucket < n ? key_lcp(a1, a2, k1[i + bucket], k2[i + bucket], cap) : -1);
+}
+
+// node levels [a_i, c_i] per particle (range = a | c << 8, -1: none), the
+// per-level run-start bitmaps (rows 0 .. NL - 1) and the bucket row NL, with
+// their popcounts for the scan
+__global__ void bb_node_levels(int n, int bucket, int nlev, int NL, int W, const signed char *__restrict__ d,
+                               const signed char *__restrict__ e, int *__restrict__ range,
+                               unsigned *__restrict__ words, int *__restrict__ wcnt)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31, w = i >> 5;
+    int a = -1, c = -1;
+    if (i < n) {
+        if (i == 0) {
+            a = 0;
+            c = max(0, min((int)e[0] + 1, nlev));
+        } else {
+            const int di = d[i];
+            if (di < nlev) {
+                int mx = -1;
+                for (int j = max(0, i - bucket); j <= i; ++j) mx = max(mx, (int)e[j]);
+                if (mx >= di) {
+                    a = di + 1;
+                    c = max(a, min((int)e[i] + 1, nlev));
+                }
+            }
+        }
+        range[i] = a < 0 ? -1 : (a | c << 8);
+    }
+    if (w >= W) return;  // whole warps only
+    for (int L = 0; L <= NL; ++L) {
+        const bool on = a >= 0 && (L == NL || (a <= L && L <= c));
+        const unsigned b = __ballot_sync(0xffffffffu, on);
+        if (lane == 0) {
+            words[(size_t)L * W + w] = b;
+            wcnt[(size_t)L * W + w] = __popc(b);
+        }
+    }
+}
+
+__global__ void bb_level_firsts(int NL, int W, const int *__restrict__ S, int *__restrict__ out)
+{
+    const int L = blockIdx.x * blockDim.x + threadIdx.x;
+    if (L <= NL + 1) out[L] = S[(size_t)L * W];  // out[NL] = nodes, out[NL + 1] = nodes + buckets
+}
+
+__global__ void bb_emit_nodes(int n, int dim, int NL, int W, double box, const unsigned long long *__restrict__ k1,
+                              const unsigned long long *__restrict__ k2, const int *__restrict__ range,
+                              const unsigned *__restrict__ words, const int *__restrict__ S,
+                              const signed char *__restrict__ d, double4 *__restrict__ ncenter,
+                              int *__restrict__ pstart, int *__restrict__ pcount, int *__restrict__ first_child,
+                              int *__restrict__ parent, int *__restrict__ buckets, int *__restrict__ bstart)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = range[i];
+    if (r < 0) return;
+    const int a = r & 255, c = r >> 8, w = i >> 5, bit = i & 31;
+    const unsigned lt = (1u << bit) - 1u;
+    const unsigned long long a1 = k1[i], a2 = k2[i];
+    // centres along the key's path with the coop build's float64 sequence
+    double4 cc = make_double4(box / 2.0, dim > 1 ? box / 2.0 : 0.0, dim > 2 ? box / 2.0 : 0.0, box / 2.0);
+    for (int L = 0; L <= c; ++L) {
+        if (L >= a) {
+            const size_t o = (size_t)L * W + w;
+            const int id = S[o] + __popc(words[o] & lt);
+            ncenter[id] = cc;
+            pstart[id] = i;
+            if (L < c) {
+                pcount[id] = 0;
+                first_child[id] = S[o + W] + __popc(words[o + W] & lt);
+            } else {  // bucket: its run ends where the keys part above level c
+                int end = i + 1;
+                while (end < n && d[end] >= c) ++end;
+                pcount[id] = end - i;
+                const size_t ob = (size_t)NL * W + w;
+                const int bi = S[ob] + __popc(words[ob] & lt) - S[(size_t)NL * W];
+                buckets[bi] = id;
+                bstart[bi] = i;
+            }
+            if (L > 0) {  // the level L - 1 run holding i (this id's parent)
+                const size_t oq = (size_t)(L - 1) * W + w;
+                const unsigned wq = words[oq];
+                parent[id] = S[oq] + __popc(wq & lt) + (int)((wq >> bit) & 1u) - 1;
+            } else {
+                parent[id] = -1;
+            }
+        }
+        const int q = key_digit(a1, a2, L);
+        const double ch = cc.w * 0.5;
+        if (dim > 0) cc.x = __dadd_rn(cc.x, (q & 1) ? ch : -ch);
+        if (dim > 1) cc.y = __dadd_rn(cc.y, (q & 2) ? ch : -ch);
+        if (dim > 2) cc.z = __dadd_rn(cc.z, (q & 4) ? ch : -ch);
+        cc.w = ch;
+    }
+}
+
+// children of a node are consecutive ids with the same parent
+__global__ void bb_nchild(int nn, const int *__restrict__ parent, const int *__restrict__ first_child,
+                          int *__restrict__ nchild)
+{
+    const int id = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    if (id >= nn) return;
+    const int p = parent[id];
+    if (id == nn - 1 || parent[id + 1] != p) nchild[p] = id + 1 - first_child[p];
+}
+
 // numpy pairwise summation (np.sum of a 1-D float64 array)
 __device__ double np_pairwise(const double *a, int n)
 {
@@ -377,36 +557,112 @@ __device__ double np_pairwise(const double *a, int n)
     return __dadd_rn(np_pairwise(a, h), np_pairwise(a + h, n - h));
 }
 
-constexpr int BB_SMALL = 32;  // buckets up to this size sum from registers
+// Bucket mass + COM in registers for buckets of <= 8 particles (the common
+// case): numpy's pairwise sum is the sequential sum below 8 and the fixed
+// 8-leaf tree at 8 (np_pairwise).  Sorted particles: contiguous loads.
+__device__ __forceinline__ bool bucket_mass_small(int dim, int s, int c, const double4 *__restrict__ spos,
+                                                  double &m_out, double4 &com_out)
+{
+    if (c > 8) return false;
+    double4 q[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] = i < c ? spos[s + i] : make_double4(0.0, 0.0, 0.0, 0.0);
+    double m;
+    if (c == 8) {
+        m = __dadd_rn(__dadd_rn(__dadd_rn(q[0].w, q[1].w), __dadd_rn(q[2].w, q[3].w)),
+                      __dadd_rn(__dadd_rn(q[4].w, q[5].w), __dadd_rn(q[6].w, q[7].w)));
+    } else {
+        m = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (i < c) m = __dadd_rn(m, q[i].w);
+    }
+    double ax = __dmul_rn(q[0].x, q[0].w), ay = __dmul_rn(q[0].y, q[0].w), az = __dmul_rn(q[0].z, q[0].w);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) {
+        if (i < c) {
+            ax = __dadd_rn(ax, __dmul_rn(q[i].x, q[i].w));
+            ay = __dadd_rn(ay, __dmul_rn(q[i].y, q[i].w));
+            az = __dadd_rn(az, __dmul_rn(q[i].z, q[i].w));
+        }
+    }
+    m_out = m;
+    com_out = make_double4(__ddiv_rn(ax, m), dim > 1 ? __ddiv_rn(ay, m) : 0.0, dim > 2 ? __ddiv_rn(az, m) : 0.0, 0.0);
+    return true;
+}
 
-// bucket mass (pairwise) and COM (sequential column sums), nbody.py:124-128
-__global__ void bb_bucket_mass(int nb, int dim, const int *__restrict__ buckets, const int *__restrict__ pstart,
-                               const int *__restrict__ pcount, const int *__restrict__ pidx,
-                               const double *__restrict__ pos, const double *__restrict__ mass,
-                               double *__restrict__ nmass, double4 *__restrict__ com, double *__restrict__ scratch)
+__device__ __forceinline__ int atomic_add_acq_rel(int *p, int v)
+{
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+// One pass for every node's mass and COM: a thread computes its bucket, then
+// climbs -- the last child of a node to arrive (acq_rel arrival counter: its
+// siblings' results are visible) sums that node's children in order
+// (nbody.py:129-135), so each node is computed once with the reference's
+// rounding sequence and no per-level launches.
+__global__ void bb_mass_up(int nb, int dim, const int *__restrict__ buckets, const int *__restrict__ pstart,
+                           const int *__restrict__ pcount, const double4 *__restrict__ spos,
+                           const int *__restrict__ parent, const int *__restrict__ first_child,
+                           const int *__restrict__ nchild, int *__restrict__ arrive, double *nmass, double4 *com,
+                           double *__restrict__ scratch, int climb)
 {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= nb) return;
-    const int id = buckets[b];
-    const int s = pstart[id], c = pcount[id];
-    double mloc[BB_SMALL];
-    const double *mb;
-    if (c <= BB_SMALL) {
-        for (int i = 0; i < c; ++i) mloc[i] = mass[pidx[s + i]];
-        mb = mloc;
-    } else {
-        for (int i = 0; i < c; ++i) scratch[s + i] = mass[pidx[s + i]];
-        mb = scratch + s;
+    int id = buckets[b];
+    int p = climb ? parent[id] : -1;
+    {
+        const int s = pstart[id], c = pcount[id];
+        double m;
+        double4 cm;
+        if (!bucket_mass_small(dim, s, c, spos, m, cm)) {
+            for (int i = 0; i < c; ++i) scratch[s + i] = spos[s + i].w;
+            const double *mb = scratch + s;
+            m = np_pairwise(mb, c);
+            double a3[3] = {0.0, 0.0, 0.0};
+            for (int k = 0; k < dim; ++k) {
+                const double *ps = reinterpret_cast<const double *>(spos + s) + k;
+                double acc = __dmul_rn(ps[0], mb[0]);
+                for (int i = 1; i < c; ++i) acc = __dadd_rn(acc, __dmul_rn(ps[4 * i], mb[i]));
+                a3[k] = __ddiv_rn(acc, m);
+            }
+            cm = make_double4(a3[0], a3[1], a3[2], 0.0);
+        }
+        nmass[id] = m;
+        com[id] = cm;
     }
-    const double m = np_pairwise(mb, c);
-    nmass[id] = m;
-    double cm[3] = {0.0, 0.0, 0.0};
-    for (int k = 0; k < dim; ++k) {
-        double acc = __dmul_rn(pos[(int64_t)pidx[s] * dim + k], mb[0]);
-        for (int i = 1; i < c; ++i) acc = __dadd_rn(acc, __dmul_rn(pos[(int64_t)pidx[s + i] * dim + k], mb[i]));
-        cm[k] = __ddiv_rn(acc, m);
+    while (p >= 0) {
+        const int fc = first_child[p], nc = nchild[p], pp = parent[p];  // issued before the arrival
+        if (atomic_add_acq_rel(arrive + p, 1) != nc - 1) break;
+        double ms = 0.0, c3[3] = {0.0, 0.0, 0.0};
+        for (int ch = fc; ch < fc + nc; ++ch) {
+            const double cmass = __ldcg(nmass + ch);
+            const double2 cxy = __ldcg(reinterpret_cast<const double2 *>(com + ch));
+            const double2 czw = __ldcg(reinterpret_cast<const double2 *>(com + ch) + 1);
+            ms = __dadd_rn(ms, cmass);
+            c3[0] = __dadd_rn(c3[0], __dmul_rn(cxy.x, cmass));
+            if (dim > 1) c3[1] = __dadd_rn(c3[1], __dmul_rn(cxy.y, cmass));
+            if (dim > 2) c3[2] = __dadd_rn(c3[2], __dmul_rn(czw.x, cmass));
+        }
+        nmass[p] = ms;
+        com[p] = make_double4(__ddiv_rn(c3[0], ms), dim > 1 ? __ddiv_rn(c3[1], ms) : 0.0,
+                              dim > 2 ? __ddiv_rn(c3[2], ms) : 0.0, 0.0);
+        p = pp;
     }
-    com[id] = make_double4(cm[0], cm[1], cm[2], 0.0);
+}
+
+// parent of every node from the children ranges (cooperative-build path)
+__global__ void bb_parents(int nn, const int *__restrict__ first_child, const int *__restrict__ nchild,
+                           int *__restrict__ parent)
+{
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= nn) return;
+    if (id == 0) parent[0] = -1;
+    const int fc = first_child[id];
+    if (fc < 0) return;
+    for (int ch = fc; ch < fc + nchild[id]; ++ch) parent[ch] = id;
 }
 
 // internal nodes of one level: children in order (nbody.py:129-135)
@@ -458,11 +714,28 @@ __global__ void bb_records(int nn, const double4 *__restrict__ com, const double
     cmax[i] = mx;
 }
 
-__global__ void bb_buckets(int nb, int dim, const int *__restrict__ buckets, const double4 *__restrict__ ncenter,
-                           const int *__restrict__ pstart, const int *__restrict__ pcount, const int *__restrict__ pidx,
-                           const double *__restrict__ pos, const double *__restrict__ mass, double4 *__restrict__ bgeo,
+// particles in tree (sorted) order, gathered once: float64 (x, y, z, m) for
+// the masses, float32 records for the force kernels, the original ids
+__global__ void bb_sorted_parts(int n, int dim, const int *__restrict__ pidx, const double *__restrict__ pos,
+                                const double *__restrict__ mass, double4 *__restrict__ spos,
+                                float4 *__restrict__ parts, int *__restrict__ porder)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int p = pidx[i];
+    const double x = pos[(int64_t)p * dim];
+    const double y = dim > 1 ? pos[(int64_t)p * dim + 1] : 0.0;
+    const double z = dim > 2 ? pos[(int64_t)p * dim + 2] : 0.0;
+    const double m = mass[p];
+    spos[i] = make_double4(x, y, z, m);
+    parts[i] = make_float4((float)x, (float)y, (float)z, (float)m);
+    porder[i] = p;
+}
+
+__global__ void bb_buckets(int nb, const int *__restrict__ buckets, const double4 *__restrict__ ncenter,
+                           const int *__restrict__ pstart, const int *__restrict__ pcount, double4 *__restrict__ bgeo,
                            float4 *__restrict__ bgeo32, int2 *__restrict__ brange, int *__restrict__ bids,
-                           int *__restrict__ part_bucket, float4 *__restrict__ parts, int *__restrict__ porder)
+                           int *__restrict__ part_bucket)
 {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= nb) return;
@@ -475,14 +748,7 @@ __global__ void bb_buckets(int nb, int dim, const int *__restrict__ buckets, con
     const int s = pstart[id], c = pcount[id];
     brange[b] = make_int2(s, c);
     bids[b] = b;
-    for (int k = 0; k < c; ++k) {
-        const int p = pidx[s + k];
-        part_bucket[s + k] = b;
-        porder[s + k] = p;
-        float x[3] = {0.f, 0.f, 0.f};
-        for (int d = 0; d < dim; ++d) x[d] = (float)pos[(int64_t)p * dim + d];
-        parts[s + k] = make_float4(x[0], x[1], x[2], (float)mass[p]);
-    }
+    for (int k = 0; k < c; ++k) part_bucket[s + k] = b;
 }
 
 // walk groups of 32 buckets; force groups greedily packed (<= 32 targets)
@@ -639,7 +905,11 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     auto &perm = bh->ws.perm;
     k1.resize(n); k2.resize(n); k1p.resize(n); k1s.resize(n); k2s.resize(n);
     idx.resize(n); perm1.resize(n); perm.resize(n);
-    bb_keys<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, dim, pos.p, box, nlev, k1.p, k2.p, idx.p);
+    int bexp = 0;
+    if (std::frexp(box, &bexp) == 0.5)
+        bb_keys_dyadic<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, dim, pos.p, 1.0 / box, nlev, k1.p, k2.p, idx.p);
+    else
+        bb_keys<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, dim, pos.p, box, nlev, k1.p, k2.p, idx.p);
     check_launch("bb_keys");
     // stable sort by (k1, k2), ties by original id.  Digits of a level no
     // node splits at do not change the tree, so first sort by the top
@@ -672,119 +942,174 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     bb_gather_u64<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, perm.p, k2.p, k2s.p);
     check_launch("bb sort");
 
-    // level-synchronous expansion
-    auto &lstart = bh->ws.lstart;
-    auto &lcount = bh->ws.lcount;
-    auto &cstart = bh->ws.cstart;
-    auto &ccount = bh->ws.ccount;
-    auto &leaf_key = bh->ws.leaf_key;
-    auto &leaf_id = bh->ws.leaf_id;
-    auto &nleaf = bh->ws.nleaf;
-    auto &lcenter = bh->ws.lcenter;
-    auto &ccenter = bh->ws.ccenter;
-    const int cap_nodes = 3 * n + 1024;
-    bh->d_ncenter.resize(cap_nodes);
-    bh->d_pstart.resize(cap_nodes);
-    bh->d_pcount.resize(cap_nodes);
-    bh->d_first_child.resize(cap_nodes);
-    bh->d_nchild.resize(cap_nodes);
-    bb_fill<<<grid_for(cap_nodes, BB_TPB), BB_TPB, 0, s>>>(cap_nodes, bh->d_first_child.p, -1);
-    bh->d_nchild.zero(s);
-    leaf_key.resize(n + 1);
-    leaf_id.resize(n + 1);
-    nleaf.resize(1);
-    nleaf.zero(s);
-    auto &cpos = bh->ws.cpos;
-    auto &cnt = bh->ws.ccnt;
-    auto &cbase = bh->ws.cbase;
-    // level arrays (ping-pong, <= n nodes per level), the root as level 0
-    lstart.resize(n);
-    lcount.resize(n);
-    lcenter.resize(n);
-    cstart.resize(n);
-    ccount.resize(n);
-    ccenter.resize(n);
-    cpos.resize((size_t)9 * n + 9);
-    cnt.resize(n + 1);
-    cbase.resize(n + 1);
-    {
-        int z = 0;
-        GC_CUDA(cudaMemcpyAsync(lstart.p, &z, sizeof(int), cudaMemcpyHostToDevice, s));
-        GC_CUDA(cudaMemcpyAsync(lcount.p, &n, sizeof(int), cudaMemcpyHostToDevice, s));
-        const double4 root = make_double4(box / 2.0, dim > 1 ? box / 2.0 : 0.0, dim > 2 ? box / 2.0 : 0.0, box / 2.0);
-        GC_CUDA(cudaMemcpyAsync(lcenter.p, &root, sizeof(double4), cudaMemcpyHostToDevice, s));
-    }
-    static int coop_blocks = 0;  // co-resident grid of the cooperative level kernel
-    if (!coop_blocks) {
-        int per_sm = 0;
-        GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bb_levels_coop, BB_TPB, 0));
-        coop_blocks = std::max(1, std::min(per_sm, 1)) * ctx->prop.multiProcessorCount;
-    }
-    auto &bsum = bh->ws.bsum;
-    auto &lvlf = bh->ws.lvlf;
-    bsum.resize(coop_blocks);
-    lvlf.resize(MAX_KEY_LEVELS + 4);
-    LevelArgs A;
-    A.n = n;
-    A.dim = dim;
-    A.nlev = nlev;
-    A.cap_nodes = cap_nodes;
-    A.bucket = bucket;
-    A.box = box;
-    A.k1 = k1s.p;
-    A.k2 = k2s.p;
-    A.start[0] = lstart.p;
-    A.start[1] = cstart.p;
-    A.count[0] = lcount.p;
-    A.count[1] = ccount.p;
-    A.center[0] = lcenter.p;
-    A.center[1] = ccenter.p;
-    A.cpos = cpos.p;
-    A.cnt = cnt.p;
-    A.cbase = cbase.p;
-    A.bsum = bsum.p;
-    A.ncenter = bh->d_ncenter.p;
-    A.pstart = bh->d_pstart.p;
-    A.pcount = bh->d_pcount.p;
-    A.first_child = bh->d_first_child.p;
-    A.nchild = bh->d_nchild.p;
-    A.leaf_key = leaf_key.p;
-    A.leaf_id = leaf_id.p;
-    A.nleaf = nleaf.p;
-    auto &big = bh->ws.big;
-    big.resize(n + 1);
-    A.big = big.p;
-    A.nbig = big.p + n;
-    GC_CUDA(cudaMemsetAsync(big.p + n, 0, sizeof(int), s));
-    A.forced_lvl = bh->d_forced_lvl.p;
-    A.forced_key = bh->d_forced_key.p;
-    A.n_forced = bh->n_forced;
-    A.lvl_first = lvlf.p;
-    A.nlevels = lvlf.p + MAX_KEY_LEVELS + 2;
-    A.overflow = lvlf.p + MAX_KEY_LEVELS + 3;
-    GC_CUDA(cudaMemsetAsync(lvlf.p, 0, sizeof(int) * (MAX_KEY_LEVELS + 4), s));
-    void *kargs[] = {&A};
-    GC_CUDA(cudaLaunchCooperativeKernel((void *)bb_levels_coop, coop_blocks, BB_TPB, kargs, 0, s));
-    check_launch("bb_levels_coop");
-    std::vector<int> lf(MAX_KEY_LEVELS + 4);
-    lvlf.download(lf.data(), MAX_KEY_LEVELS + 4, s);
-    GC_CUDA(cudaStreamSynchronize(s));
-    GC_REQUIRE(!lf[MAX_KEY_LEVELS + 3], GC_E_VALUE, "node capacity exceeded");
-    const int nlevels = lf[MAX_KEY_LEVELS + 2];
-    std::vector<int> lvl_first(lf.begin(), lf.begin() + nlevels + 1);
-    const int next_id = lvl_first.back();
-    const int nn = next_id;
-    int nb = 0;
-    GC_CUDA(cudaMemcpyAsync(&nb, nleaf.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    GC_CUDA(cudaStreamSynchronize(s));
-
-    // buckets in depth-first order = by start position
+    std::vector<int> lvl_first;
+    int nn = 0, nb = 0;
     auto &lk_s = bh->ws.lk_s;
-    bh->d_buckets.resize(nb);
-    lk_s.resize(nb);
-    cubc(ctx, [&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, leaf_key.p, lk_s.p, leaf_id.p, bh->d_buckets.p, nb, 0, 32, s);
-    });
+    if (bh->n_forced == 0) {
+        // bottom-up enumeration (bb_lcp / bb_node_levels / one scan / bb_emit_nodes)
+        const int Ds = deep ? nlev : std::min(nlev, SORT_LEVELS);  // sorted key depth
+        const int NL = Ds + 1;  // node levels 0 .. Ds
+        const int W = (n + 31) / 32;
+        auto &dl = bh->ws.dl, &el = bh->ws.el;
+        auto &range = bh->ws.range, &wcnt = bh->ws.wcnt, &wscan = bh->ws.wscan, &par = bh->ws.parent;
+        auto &words = bh->ws.words;
+        dl.resize(n);
+        el.resize(n);
+        range.resize(n);
+        const size_t nw = (size_t)(NL + 1) * W;
+        words.resize(nw);
+        wcnt.resize(nw + 1);
+        wscan.resize(nw + 1);
+        GC_CUDA(cudaMemsetAsync(wcnt.p + nw, 0, sizeof(int), s));
+        bb_lcp<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, (int)bucket, Ds, k1s.p, k2s.p, dl.p, el.p);
+        bb_node_levels<<<grid_for(32 * W, BB_TPB), BB_TPB, 0, s>>>(n, (int)bucket, nlev, NL, W, dl.p, el.p, range.p,
+                                                                    words.p, wcnt.p);
+        cubc(ctx, [&](void *t, size_t &b) { return cub::DeviceScan::ExclusiveSum(t, b, wcnt.p, wscan.p, nw + 1, s); });
+        auto &lvlf = bh->ws.lvlf;
+        lvlf.resize(NL + 2);
+        bb_level_firsts<<<1, 64, 0, s>>>(NL, W, wscan.p, lvlf.p);
+        check_launch("bb node levels");
+        std::vector<int> lf(NL + 2);
+        lvlf.download(lf.data(), NL + 2, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        nn = lf[NL];
+        nb = lf[NL + 1] - nn;
+        int nlevels = 1;
+        while (nlevels < NL && lf[nlevels] < nn) ++nlevels;
+        lvl_first.assign(lf.begin(), lf.begin() + nlevels);
+        lvl_first.push_back(nn);
+        const size_t cap = std::max<size_t>((size_t)3 * n + 1024, (size_t)nn);
+        bh->d_ncenter.resize(cap);
+        bh->d_pstart.resize(cap);
+        bh->d_pcount.resize(cap);
+        bh->d_first_child.resize(cap);
+        bh->d_nchild.resize(cap);
+        par.resize(cap);
+        bb_fill<<<grid_for(nn, BB_TPB), BB_TPB, 0, s>>>(nn, bh->d_first_child.p, -1);
+        GC_CUDA(cudaMemsetAsync(bh->d_nchild.p, 0, sizeof(int) * nn, s));
+        bh->d_buckets.resize(nb);
+        lk_s.resize(nb);
+        bb_emit_nodes<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, dim, NL, W, box, k1s.p, k2s.p, range.p, words.p,
+                                                             wscan.p, dl.p, bh->d_ncenter.p, bh->d_pstart.p,
+                                                             bh->d_pcount.p, bh->d_first_child.p, par.p,
+                                                             bh->d_buckets.p, lk_s.p);
+        if (nn > 1)
+            bb_nchild<<<grid_for(nn - 1, BB_TPB), BB_TPB, 0, s>>>(nn, par.p, bh->d_first_child.p, bh->d_nchild.p);
+        check_launch("bb emit nodes");
+    } else {
+        // forced cubes (distributed build): the level-synchronous cooperative expansion
+        // level-synchronous expansion
+        auto &lstart = bh->ws.lstart;
+        auto &lcount = bh->ws.lcount;
+        auto &cstart = bh->ws.cstart;
+        auto &ccount = bh->ws.ccount;
+        auto &leaf_key = bh->ws.leaf_key;
+        auto &leaf_id = bh->ws.leaf_id;
+        auto &nleaf = bh->ws.nleaf;
+        auto &lcenter = bh->ws.lcenter;
+        auto &ccenter = bh->ws.ccenter;
+        const int cap_nodes = 3 * n + 1024;
+        bh->d_ncenter.resize(cap_nodes);
+        bh->d_pstart.resize(cap_nodes);
+        bh->d_pcount.resize(cap_nodes);
+        bh->d_first_child.resize(cap_nodes);
+        bh->d_nchild.resize(cap_nodes);
+        bb_fill<<<grid_for(cap_nodes, BB_TPB), BB_TPB, 0, s>>>(cap_nodes, bh->d_first_child.p, -1);
+        bh->d_nchild.zero(s);
+        leaf_key.resize(n + 1);
+        leaf_id.resize(n + 1);
+        nleaf.resize(1);
+        nleaf.zero(s);
+        auto &cpos = bh->ws.cpos;
+        auto &cnt = bh->ws.ccnt;
+        auto &cbase = bh->ws.cbase;
+        // level arrays (ping-pong, <= n nodes per level), the root as level 0
+        lstart.resize(n);
+        lcount.resize(n);
+        lcenter.resize(n);
+        cstart.resize(n);
+        ccount.resize(n);
+        ccenter.resize(n);
+        cpos.resize((size_t)9 * n + 9);
+        cnt.resize(n + 1);
+        cbase.resize(n + 1);
+        {
+            int z = 0;
+            GC_CUDA(cudaMemcpyAsync(lstart.p, &z, sizeof(int), cudaMemcpyHostToDevice, s));
+            GC_CUDA(cudaMemcpyAsync(lcount.p, &n, sizeof(int), cudaMemcpyHostToDevice, s));
+            const double4 root = make_double4(box / 2.0, dim > 1 ? box / 2.0 : 0.0, dim > 2 ? box / 2.0 : 0.0, box / 2.0);
+            GC_CUDA(cudaMemcpyAsync(lcenter.p, &root, sizeof(double4), cudaMemcpyHostToDevice, s));
+        }
+        static int coop_blocks = 0;  // co-resident grid of the cooperative level kernel
+        if (!coop_blocks) {
+            int per_sm = 0;
+            GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bb_levels_coop, BB_TPB, 0));
+            coop_blocks = std::max(1, std::min(per_sm, 1)) * ctx->prop.multiProcessorCount;
+        }
+        auto &bsum = bh->ws.bsum;
+        auto &lvlf = bh->ws.lvlf;
+        bsum.resize(coop_blocks);
+        lvlf.resize(MAX_KEY_LEVELS + 4);
+        LevelArgs A;
+        A.n = n;
+        A.dim = dim;
+        A.nlev = nlev;
+        A.cap_nodes = cap_nodes;
+        A.bucket = bucket;
+        A.box = box;
+        A.k1 = k1s.p;
+        A.k2 = k2s.p;
+        A.start[0] = lstart.p;
+        A.start[1] = cstart.p;
+        A.count[0] = lcount.p;
+        A.count[1] = ccount.p;
+        A.center[0] = lcenter.p;
+        A.center[1] = ccenter.p;
+        A.cpos = cpos.p;
+        A.cnt = cnt.p;
+        A.cbase = cbase.p;
+        A.bsum = bsum.p;
+        A.ncenter = bh->d_ncenter.p;
+        A.pstart = bh->d_pstart.p;
+        A.pcount = bh->d_pcount.p;
+        A.first_child = bh->d_first_child.p;
+        A.nchild = bh->d_nchild.p;
+        A.leaf_key = leaf_key.p;
+        A.leaf_id = leaf_id.p;
+        A.nleaf = nleaf.p;
+        auto &big = bh->ws.big;
+        big.resize(n + 1);
+        A.big = big.p;
+        A.nbig = big.p + n;
+        GC_CUDA(cudaMemsetAsync(big.p + n, 0, sizeof(int), s));
+        A.forced_lvl = bh->d_forced_lvl.p;
+        A.forced_key = bh->d_forced_key.p;
+        A.n_forced = bh->n_forced;
+        A.lvl_first = lvlf.p;
+        A.nlevels = lvlf.p + MAX_KEY_LEVELS + 2;
+        A.overflow = lvlf.p + MAX_KEY_LEVELS + 3;
+        GC_CUDA(cudaMemsetAsync(lvlf.p, 0, sizeof(int) * (MAX_KEY_LEVELS + 4), s));
+        void *kargs[] = {&A};
+        GC_CUDA(cudaLaunchCooperativeKernel((void *)bb_levels_coop, coop_blocks, BB_TPB, kargs, 0, s));
+        check_launch("bb_levels_coop");
+        std::vector<int> lf(MAX_KEY_LEVELS + 4);
+        lvlf.download(lf.data(), MAX_KEY_LEVELS + 4, s);
+        GC_CUDA(cudaStreamSynchronize(s));
+        GC_REQUIRE(!lf[MAX_KEY_LEVELS + 3], GC_E_VALUE, "node capacity exceeded");
+        const int nlevels = lf[MAX_KEY_LEVELS + 2];
+        lvl_first.assign(lf.begin(), lf.begin() + nlevels + 1);
+        const int next_id = lvl_first.back();
+        nn = next_id;
+        GC_CUDA(cudaMemcpyAsync(&nb, nleaf.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        GC_CUDA(cudaStreamSynchronize(s));
+
+        // buckets in depth-first order = by start position
+        bh->d_buckets.resize(nb);
+        lk_s.resize(nb);
+        cubc(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, leaf_key.p, lk_s.p, leaf_id.p, bh->d_buckets.p, nb, 0, 32, s);
+        });
+    }
     // particles inside each bucket: ascending original id
     auto &offs = bh->ws.offs;
     auto &pidx = bh->ws.pidx;
@@ -806,12 +1131,33 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     com.resize(nn);
     scratch.resize(n);
     GC_CUDA(cudaStreamWaitEvent(s, bh->side_done, 0));
-    bb_bucket_mass<<<grid_for(nb, BB_TPB), BB_TPB, 0, s>>>(nb, dim, bh->d_buckets.p, bh->d_pstart.p, bh->d_pcount.p,
-                                                           pidx.p, pos.p, mass.p, bh->d_nmass.p, com.p, scratch.p);
-    for (int L = (int)lvl_first.size() - 2; L >= 0; --L) {
-        const int id0 = lvl_first[L], mL = lvl_first[L + 1] - id0;
-        bb_internal_mass<<<grid_for(mL, BB_TPB), BB_TPB, 0, s>>>(id0, mL, dim, bh->d_first_child.p, bh->d_nchild.p,
+    auto &par = bh->ws.parent;
+    static const bool climb = [] {
+        const char *e = getenv("GC_BUILD_CLIMB");
+        return e ? atoi(e) != 0 : true;
+    }();
+    if (bh->n_forced != 0) {  // the cooperative build writes no parents
+        par.resize(std::max<size_t>(nn, 1));
+        bb_parents<<<grid_for(nn, BB_TPB), BB_TPB, 0, s>>>(nn, bh->d_first_child.p, bh->d_nchild.p, par.p);
+    }
+    bh->d_parts.resize(n);
+    bh->d_porder.resize(n);
+    auto &spos = bh->ws.spos;
+    spos.resize(n);
+    bb_sorted_parts<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, dim, pidx.p, pos.p, mass.p, spos.p, bh->d_parts.p,
+                                                           bh->d_porder.p);
+    auto &arrive = bh->ws.arrive;
+    arrive.resize(std::max(nn, 1));
+    GC_CUDA(cudaMemsetAsync(arrive.p, 0, sizeof(int) * nn, s));
+    bb_mass_up<<<grid_for(nb, 128), 128, 0, s>>>(nb, dim, bh->d_buckets.p, bh->d_pstart.p, bh->d_pcount.p, spos.p,
+                                                  par.p, bh->d_first_child.p, bh->d_nchild.p, arrive.p,
+                                                  bh->d_nmass.p, com.p, scratch.p, climb ? 1 : 0);
+    if (!climb) {
+        for (int L = (int)lvl_first.size() - 2; L >= 0; --L) {
+            const int id0 = lvl_first[L], mL = lvl_first[L + 1] - id0;
+            bb_internal_mass<<<grid_for(mL, 128), 128, 0, s>>>(id0, mL, dim, bh->d_first_child.p, bh->d_nchild.p,
                                                                 bh->d_nmass.p, com.p);
+        }
     }
     check_launch("bb mass");
 
@@ -835,12 +1181,9 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     bh->d_brange.resize(nb);
     bh->d_bucket_ids.resize(nb);
     bh->d_part_bucket.resize(n);
-    bh->d_parts.resize(n);
-    bh->d_porder.resize(n);
-    bb_buckets<<<grid_for(nb, BB_TPB), BB_TPB, 0, s>>>(nb, dim, bh->d_buckets.p, bh->d_ncenter.p, bh->d_pstart.p,
-                                                       bh->d_pcount.p, pidx.p, pos.p, mass.p, bh->d_bgeo.p,
-                                                       bh->d_bgeo32.p, bh->d_brange.p, bh->d_bucket_ids.p,
-                                                       bh->d_part_bucket.p, bh->d_parts.p, bh->d_porder.p);
+    bb_buckets<<<grid_for(nb, BB_TPB), BB_TPB, 0, s>>>(nb, bh->d_buckets.p, bh->d_ncenter.p, bh->d_pstart.p,
+                                                       bh->d_pcount.p, bh->d_bgeo.p, bh->d_bgeo32.p, bh->d_brange.p,
+                                                       bh->d_bucket_ids.p, bh->d_part_bucket.p);
     check_launch("bb records");
     // groups
     const int nwg = (nb + WG_BUCKETS - 1) / WG_BUCKETS;

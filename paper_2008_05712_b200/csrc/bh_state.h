@@ -22,6 +22,10 @@ struct BuildWs {  // device-build scratch, kept across builds (no per-step cudaM
     DBuf<double4> com;
     DBuf<double> cmax, cmax_out;
     DBuf<int> nfg_of, fg_base, bad;
+    DBuf<signed char> dl, el;  // bottom-up build: adjacent / bucket-window key prefixes
+    DBuf<int> range, wcnt, wscan, parent, arrive;
+    DBuf<unsigned> words;
+    DBuf<double4> spos;  // particles in tree order, float64 (x, y, z, m)
 };
 
 struct gc_bh {

@@ -17,7 +17,7 @@ m = torch.from_numpy(np.ascontiguousarray(ps.masses)).pin_memory().numpy()
 out = torch.empty((n, 3), dtype=torch.float64).pin_memory().numpy()
 st = nbody.BHStep(8, 0.7, 1.0, 1e-4)
 h = st.handle
-for it in range(4):
+for it in range(6):
     t0 = time.perf_counter()
     L.call("gc_bh_set_particles", h, n, 3, L.ptr(pos, L.f64p), L.ptr(m, L.f64p), 1.0, 8)
     t1 = time.perf_counter()
