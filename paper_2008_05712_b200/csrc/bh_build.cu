@@ -4,25 +4,30 @@
 //  1. Octant keys.  Every particle descends the reference's cells in float64:
 //     digit q_L = sum_k (x_k >= c_k) << k, child centre c + (+-1)*half/2
 //     (nbody.py:97-108), for every level at which a node may still split
-//     (half >= 1e-9, nbody.py:94).  3 bits per level, two 64-bit words.
+//     (half >= 1e-9, nbody.py:94).  3 bits per level, two 64-bit words.  For a
+//     power-of-two box every centre is an exact dyadic fraction of the box, so
+//     the digits are the bits of x / box in fixed point (bb_keys_dyadic).
 //  2. One stable radix sort by (key, original id): every node of the
 //     reference is a contiguous range of this order, its children are the
 //     sub-ranges of equal next digit in ascending digit (= octant) order.
-//  3. Level-synchronous expansion in ONE cooperative launch: at each level a
-//     splitting node (count > bucket_size and half >= 1e-9) is cut by 8 binary
-//     searches of its sorted level digit; a grid-wide scan numbers the
-//     children in position order, which is the reference's breadth-first id
-//     order.  Non-splitting nodes are buckets.
-//  4. Buckets sorted by position = depth-first order; each bucket's particles
-//     re-sorted by original id (the reference keeps ascending particle_idx).
+//  3. Nodes bottom-up from the sorted keys (bb_lcp / bb_node_levels /
+//     bb_emit_nodes): a particle starts the nodes of levels (d_i, c_i] where
+//     d_i is its common prefix with its predecessor; one scan over per-level
+//     run-start bitmaps gives the reference's breadth-first ids and the
+//     depth-first bucket order.  (The level-synchronous cooperative expansion
+//     remains for distributed builds with forced cubes.)
+//  4. Each bucket's particles re-sorted by original id (the reference keeps
+//     ascending particle_idx), particles gathered once in tree order.
 //  5. Masses/centres of mass with the reference's float64 rounding sequence:
 //     bucket mass = numpy pairwise sum, COM = sequential column sum / mass;
-//     internal nodes add children in order, deepest level first.
+//     internal nodes add children in order -- one bottom-up pass, the last
+//     child to finish computes its parent (bb_mass_up).
 //  6. Force/walk records, bucket geometry and walk/force groups in HBM.
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 
@@ -81,6 +86,7 @@ __device__ __forceinline__ unsigned long long spread3(unsigned long long x)  // 
     x = (x | x << 2) & 0x1249249249249249ull;
     return x;
 }
+
 
 __global__ void bb_keys_dyadic(int n, int dim, const double *__restrict__ pos, double inv_box, int nlev,
                                unsigned long long *__restrict__ k1, unsigned long long *__restrict__ k2,
@@ -591,16 +597,9 @@ __device__ __forceinline__ bool bucket_mass_small(int dim, int s, int c, const d
     return true;
 }
 
-__device__ __forceinline__ int atomic_add_acq_rel(int *p, int v)
-{
-    int old;
-    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-    return old;
-}
-
 // One pass for every node's mass and COM: a thread computes its bucket, then
-// climbs -- the last child of a node to arrive (acq_rel arrival counter: its
-// siblings' results are visible) sums that node's children in order
+// climbs -- the last child of a node to arrive (fence + arrival counter: its
+// siblings' results are visible in L2) sums that node's children in order
 // (nbody.py:129-135), so each node is computed once with the reference's
 // rounding sequence and no per-level launches.
 __global__ void bb_mass_up(int nb, int dim, const int *__restrict__ buckets, const int *__restrict__ pstart,
@@ -635,16 +634,30 @@ __global__ void bb_mass_up(int nb, int dim, const int *__restrict__ buckets, con
     }
     while (p >= 0) {
         const int fc = first_child[p], nc = nchild[p], pp = parent[p];  // issued before the arrival
-        if (atomic_add_acq_rel(arrive + p, 1) != nc - 1) break;
+        int old;  // release: this thread's node results are visible before its arrival
+        asm volatile("atom.release.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(arrive + p) : "memory");
+        if (old != nc - 1) break;
+        // the last arrival: every sibling fenced before arriving; read them from
+        // L2 (.cg, no stale L1 lines), all loads issued before the in-order sums
+        double cm[8];
+        double2 cxy[8], czw[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (k < nc) {
+                cm[k] = __ldcg(nmass + fc + k);
+                cxy[k] = __ldcg(reinterpret_cast<const double2 *>(com + fc + k));
+                czw[k] = __ldcg(reinterpret_cast<const double2 *>(com + fc + k) + 1);
+            }
+        }
         double ms = 0.0, c3[3] = {0.0, 0.0, 0.0};
-        for (int ch = fc; ch < fc + nc; ++ch) {
-            const double cmass = __ldcg(nmass + ch);
-            const double2 cxy = __ldcg(reinterpret_cast<const double2 *>(com + ch));
-            const double2 czw = __ldcg(reinterpret_cast<const double2 *>(com + ch) + 1);
-            ms = __dadd_rn(ms, cmass);
-            c3[0] = __dadd_rn(c3[0], __dmul_rn(cxy.x, cmass));
-            if (dim > 1) c3[1] = __dadd_rn(c3[1], __dmul_rn(cxy.y, cmass));
-            if (dim > 2) c3[2] = __dadd_rn(c3[2], __dmul_rn(czw.x, cmass));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (k < nc) {
+                ms = __dadd_rn(ms, cm[k]);
+                c3[0] = __dadd_rn(c3[0], __dmul_rn(cxy[k].x, cm[k]));
+                if (dim > 1) c3[1] = __dadd_rn(c3[1], __dmul_rn(cxy[k].y, cm[k]));
+                if (dim > 2) c3[2] = __dadd_rn(c3[2], __dmul_rn(czw[k].x, cm[k]));
+            }
         }
         nmass[p] = ms;
         com[p] = make_double4(__ddiv_rn(c3[0], ms), dim > 1 ? __ddiv_rn(c3[1], ms) : 0.0,
@@ -865,9 +878,51 @@ void device_keys(gc_ctx *ctx, int64_t n64, int dim, const double *pos_h, double 
     GC_CUDA(cudaStreamSynchronize(s));
 }
 
+// GC_BUILD_PROF=1: live per-phase device times of the build (CUDA events)
+struct BuildProf {
+    bool on = false;
+    cudaStream_t s = nullptr;
+    std::vector<std::pair<const char *, cudaEvent_t>> ev;
+    std::vector<std::chrono::steady_clock::time_point> ht;
+    BuildProf(cudaStream_t st) : s(st)
+    {
+        static const bool env = getenv("GC_BUILD_PROF") != nullptr;
+        on = env;
+        mark("start");
+    }
+    void mark(const char *name)
+    {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        ev.emplace_back(name, e);
+        ht.push_back(std::chrono::steady_clock::now());
+    }
+    ~BuildProf()
+    {
+        if (!on) return;
+        cudaEventSynchronize(ev.back().second);
+        fprintf(stderr, "device_build_tree:");
+        for (size_t i = 1; i < ev.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+            fprintf(stderr, " %s %.3f", ev[i].first, ms);
+        }
+        float tot = 0.f;
+        cudaEventElapsedTime(&tot, ev.front().second, ev.back().second);
+        fprintf(stderr, " | total %.3f ms\n  host:", tot);
+        for (size_t i = 1; i < ht.size(); ++i)
+            fprintf(stderr, " %s %.3f", ev[i].first, std::chrono::duration<double, std::milli>(ht[i] - ht[i - 1]).count());
+        fprintf(stderr, "\n");
+        for (auto &p : ev) cudaEventDestroy(p.second);
+    }
+};
+
 void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int64_t n64, int dim, double box,
                        int64_t bucket)
 {
+    BuildProf prof(bh->ctx->stream);
     gc_ctx *ctx = bh->ctx;
     cudaStream_t s = ctx->stream;
     GC_REQUIRE(n64 < (1 << PSTART_BITS), GC_E_VALUE, "too many particles for one tree (packed bucket words)");
@@ -881,6 +936,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     auto &mass = bh->ws.mass;
     auto &scratch = bh->ws.scratch;
     pos.upload(pos_h, (size_t)n * dim, s);
+    prof.mark("h2d");
     // masses are first needed by the bucket masses: copy them on a side stream
     // while the keys, the sort and the level expansion run
     if (!bh->side) {
@@ -891,7 +947,8 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     mass.resize(n);
     GC_CUDA(cudaEventRecord(bh->main_ready, s));  // earlier work on `mass` (previous build) is done
     GC_CUDA(cudaStreamWaitEvent(bh->side, bh->main_ready, 0));
-    GC_CUDA(cudaMemcpyAsync(mass.p, mass_h, sizeof(double) * n, cudaMemcpyHostToDevice, bh->side));
+    static const bool mass_main = getenv("GC_MASS_MAIN") != nullptr;  // A/B knob
+    GC_CUDA(cudaMemcpyAsync(mass.p, mass_h, sizeof(double) * n, cudaMemcpyHostToDevice, mass_main ? s : bh->side));
     GC_CUDA(cudaEventRecord(bh->side_done, bh->side));
     bh->h2d += (int64_t)n * (dim + 1) * (int64_t)sizeof(double);
     auto &k1 = bh->ws.k1;
@@ -905,31 +962,28 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     auto &perm = bh->ws.perm;
     k1.resize(n); k2.resize(n); k1p.resize(n); k1s.resize(n); k2s.resize(n);
     idx.resize(n); perm1.resize(n); perm.resize(n);
+    // stable sort by (k1, k2), ties by original id.  Digits of a level no
+    // node splits at do not change the tree, so first sort by the top
+    // SORT_LEVELS levels only; if some run of equal top keys is longer than a
+    // bucket (a node of that level would split), redo it with all levels
+    // (LSD on k2, then k1).  (Measured: splitting the 48-bit sort into 32-bit
+    // + 16-bit key passes is not faster at 1M.)
+    constexpr int SORT_LEVELS = 16;  // 48 bits: six 8-bit radix passes
+    const int top_bits = 3 * std::min(nlev, SORT_LEVELS);
     int bexp = 0;
     if (std::frexp(box, &bexp) == 0.5)
         bb_keys_dyadic<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, dim, pos.p, 1.0 / box, nlev, k1.p, k2.p, idx.p);
     else
         bb_keys<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, dim, pos.p, box, nlev, k1.p, k2.p, idx.p);
     check_launch("bb_keys");
-    // stable sort by (k1, k2), ties by original id.  Digits of a level no
-    // node splits at do not change the tree, so first sort by the top
-    // SORT_LEVELS levels only; if some run of equal top keys is longer than a
-    // bucket (a node of that level would split), redo it with all levels
-    // (LSD on k2, then k1).
-    constexpr int SORT_LEVELS = 14;
-    const int top_bits = 3 * std::min(nlev, SORT_LEVELS);
+    prof.mark("keys");
     cubc(ctx, [&](void *t, size_t &b) {
         return cub::DeviceRadixSort::SortPairs(t, b, k1.p, k1s.p, idx.p, perm.p, n, 63 - top_bits, 63, s);
     });
-    int deep = bh->n_forced > 0 ? 1 : 0;  // forced cubes may split below the top levels
-    if (!deep && nlev > SORT_LEVELS) {
-        scratch_i.resize(1);
-        scratch_i.zero(s);
-        bb_long_runs<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, (int)bucket, k1s.p, 63 - top_bits, scratch_i.p);
-        GC_CUDA(cudaMemcpyAsync(&deep, scratch_i.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-        GC_CUDA(cudaStreamSynchronize(s));
-    }
-    if (deep) {
+    // k1s holds the full keys in the sorted order; k2 follows the permutation
+    bb_gather_u64<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, perm.p, k2.p, k2s.p);
+    prof.mark("radix");
+    auto sort_deep = [&] {
         cubc(ctx, [&](void *t, size_t &b) {
             return cub::DeviceRadixSort::SortPairs(t, b, k2.p, k2s.p, idx.p, perm1.p, n, 0, 64, s);
         });
@@ -937,15 +991,25 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
         cubc(ctx, [&](void *t, size_t &b) {
             return cub::DeviceRadixSort::SortPairs(t, b, k1p.p, k1s.p, perm1.p, perm.p, n, 0, 64, s);
         });
-    }
-    bb_gather_u64<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, perm.p, k1.p, k1s.p);
-    bb_gather_u64<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, perm.p, k2.p, k2s.p);
+        bb_gather_u64<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, perm.p, k2.p, k2s.p);
+    };
+    int deep = bh->n_forced > 0 ? 1 : 0;  // forced cubes may split below the top levels
+    // a run of equal top keys longer than a bucket: checked on the device, read
+    // back at the level-count sync below (the rare deep case re-sorts there)
+    bool check_deep = !deep && nlev > SORT_LEVELS;
+    scratch_i.resize(1);
+    scratch_i.zero(s);
+    if (check_deep)
+        bb_long_runs<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, (int)bucket, k1s.p, 63 - top_bits, scratch_i.p);
+    if (deep) sort_deep();
     check_launch("bb sort");
+    prof.mark("sort");
 
     std::vector<int> lvl_first;
     int nn = 0, nb = 0;
     auto &lk_s = bh->ws.lk_s;
     if (bh->n_forced == 0) {
+      for (;;) {  // once, or twice when the top-level sort was not deep enough
         // bottom-up enumeration (bb_lcp / bb_node_levels / one scan / bb_emit_nodes)
         const int Ds = deep ? nlev : std::min(nlev, SORT_LEVELS);  // sorted key depth
         const int NL = Ds + 1;  // node levels 0 .. Ds
@@ -966,12 +1030,20 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
                                                                     words.p, wcnt.p);
         cubc(ctx, [&](void *t, size_t &b) { return cub::DeviceScan::ExclusiveSum(t, b, wcnt.p, wscan.p, nw + 1, s); });
         auto &lvlf = bh->ws.lvlf;
-        lvlf.resize(NL + 2);
+        lvlf.resize(NL + 3);
         bb_level_firsts<<<1, 64, 0, s>>>(NL, W, wscan.p, lvlf.p);
+        GC_CUDA(cudaMemcpyAsync(lvlf.p + NL + 2, scratch_i.p, sizeof(int), cudaMemcpyDeviceToDevice, s));
         check_launch("bb node levels");
-        std::vector<int> lf(NL + 2);
-        lvlf.download(lf.data(), NL + 2, s);
+        prof.mark("levels");
+        std::vector<int> lf(NL + 3);
+        lvlf.download(lf.data(), NL + 3, s);
         GC_CUDA(cudaStreamSynchronize(s));
+        if (check_deep && lf[NL + 2]) {
+            deep = 1;
+            check_deep = false;
+            sort_deep();
+            continue;
+        }
         nn = lf[NL];
         nb = lf[NL + 1] - nn;
         int nlevels = 1;
@@ -996,6 +1068,9 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
         if (nn > 1)
             bb_nchild<<<grid_for(nn - 1, BB_TPB), BB_TPB, 0, s>>>(nn, par.p, bh->d_first_child.p, bh->d_nchild.p);
         check_launch("bb emit nodes");
+        break;
+      }
+        prof.mark("emit");
     } else {
         // forced cubes (distributed build): the level-synchronous cooperative expansion
         // level-synchronous expansion
@@ -1124,6 +1199,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
         return cub::DeviceSegmentedSort::SortKeys(t, b, perm.p, pidx.p, n, nb, offs.p, offs.p + 1, s);
     });
     check_launch("bb buckets");
+    prof.mark("segsort");
 
     // masses and centres of mass
     bh->d_nmass.resize(nn);
@@ -1160,6 +1236,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
         }
     }
     check_launch("bb mass");
+    prof.mark("mass");
 
     // records
     auto &cmax = bh->ws.cmax;
@@ -1185,6 +1262,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
                                                        bh->d_pcount.p, bh->d_bgeo.p, bh->d_bgeo32.p, bh->d_brange.p,
                                                        bh->d_bucket_ids.p, bh->d_part_bucket.p);
     check_launch("bb records");
+    prof.mark("records");
     // groups
     const int nwg = (nb + WG_BUCKETS - 1) / WG_BUCKETS;
     auto &nfg_of = bh->ws.nfg_of;
@@ -1200,6 +1278,14 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     cubc(ctx, [&](void *t, size_t &b) {
         return cub::DeviceScan::ExclusiveSum(t, b, nfg_of.p, fg_base.p, nwg + 1, s);
     });
+    // every force group holds >= 1 bucket: nb bounds the group count, so the
+    // second pass needs no host round trip; counts and checks come back at the end
+    bh->d_wg.resize(nwg);
+    bh->d_fg.resize(std::max(nb, 1));
+    bb_groups<1><<<grid_for(nwg, BB_TPB / 32), BB_TPB, 0, s>>>(nwg, nb, bh->d_brange.p, nullptr, fg_base.p, bh->d_wg.p,
+                                                          bh->d_fg.p, bad.p, bh->d_bgeo.p);
+    check_launch("bb groups");
+    prof.mark("groups");
     int nfg = 0, badh = 0;
     GC_CUDA(cudaMemcpyAsync(&nfg, fg_base.p + nwg, sizeof(int), cudaMemcpyDeviceToHost, s));
     GC_CUDA(cudaMemcpyAsync(&badh, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1208,15 +1294,10 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     GC_CUDA(cudaStreamSynchronize(s));
     GC_REQUIRE(!(badh & 1), GC_E_VALUE, "bucket with more than 32 particles (coincident points) on the group path");
     GC_REQUIRE(!(badh & 2), GC_E_VALUE, "walk group with more than 32 force groups");
-    bh->d_wg.resize(nwg);
-    bh->d_fg.resize(nfg);
-    bb_groups<1><<<grid_for(nwg, BB_TPB / 32), BB_TPB, 0, s>>>(nwg, nb, bh->d_brange.p, nullptr, fg_base.p, bh->d_wg.p,
-                                                          bh->d_fg.p, bad.p, bh->d_bgeo.p);
-    check_launch("bb groups");
+    bh->d_fg.n = nfg;
     bh->n_wg = nwg;
     bh->h_wg_valid = false;  // fetched on demand (sub-range launches, gc_bh_groups)
     bh->n_fg = nfg;
-    GC_CUDA(cudaStreamSynchronize(s));
     set_tree_bounds(bh, cm);
     GC_CUDA(cudaEventSynchronize(bh->side_done));  // long done: the caller may reuse its mass buffer
     bh->n = n;
