@@ -210,6 +210,52 @@ def test_device_build_equals_oracle_tree(nb, name, n, seed, cl, dim):
         np.testing.assert_array_equal(a.particle_idx(int(b)), o.particle_idx(int(b)))
 
 
+def _edge_set(case):
+    from paper_2008_05712_b200 import generators as gen
+    rng = np.random.default_rng(7)
+    box, dim = 1.0, 3
+    if case in ("n1", "n8", "n9"):
+        pos = rng.uniform(0.0, 1.0, size=(int(case[1:]), 3))
+    elif case == "coincident":  # 20 identical points: a level-nlev bucket, the deep sort path
+        pos = np.concatenate([rng.uniform(0.0, 1.0, size=(3000, 3)), np.full((20, 3), 0.3141592)])
+    elif case == "tight_pairs":  # pairs 1e-7 apart: single-child chains ~23 levels deep
+        a = rng.uniform(0.0, 1.0, size=(2000, 3))
+        pos = np.concatenate([a, a + 1e-7])
+    elif case in ("dim1", "dim2"):
+        dim = int(case[-1])
+        pos = rng.uniform(0.0, 1.0, size=(5000, dim))
+    elif case == "box3.7":  # non-dyadic box: the float64 key descent
+        box = 3.7
+        pos = gen.gen_particles(20_000, 3, clustering=0.7, dim=3, box=box).positions
+    elif case == "box0.25":  # dyadic, not 1
+        box = 0.25
+        pos = gen.gen_particles(20_000, 4, clustering=0.7, dim=3, box=box).positions
+    pos = pos.astype(np.float32).astype(np.float64)
+    m = rng.uniform(0.5, 1.5, size=len(pos)).astype(np.float32).astype(np.float64)
+    return gen.ParticleSet(pos, m, np.zeros_like(pos), box)
+
+
+@pytest.mark.parametrize("case,bucket", [("n1", 8), ("n8", 8), ("n9", 8), ("coincident", 8), ("tight_pairs", 8),
+                                         ("tight_pairs", 1), ("dim1", 8), ("dim2", 8), ("box3.7", 8),
+                                         ("box0.25", 32)])
+def test_device_build_edge_cases(nb, case, bucket):
+    """The bottom-up device build (bb_node_levels / bb_emit_nodes / bb_mass_up)
+    on the shapes it special-cases: a root that is a bucket, one particle more
+    than a bucket, runs longer than a bucket below the sorted top levels (the
+    deep re-sort), deep single-child chains, 1-D / 2-D keys, non-dyadic and
+    non-unit dyadic boxes -- equal to the float64 oracle's tree bit for bit."""
+    from oracle import oracle as orc
+    ps = _edge_set(case)
+    a = nb.build_bucket_tree(ps, bucket)
+    o = orc.build_bucket_tree(ps.positions, ps.masses, bucket, box=ps.box)
+    for k in ("center", "half", "mass", "com", "first_child", "n_child", "pcount"):
+        np.testing.assert_array_equal(np.asarray(getattr(a, k)).reshape(np.shape(getattr(o, k))), getattr(o, k),
+                                      err_msg=k)
+    np.testing.assert_array_equal(a.bucket_ids, o.buckets)
+    for b in o.buckets:
+        np.testing.assert_array_equal(a.particle_idx(int(b)), o.particle_idx(int(b)))
+
+
 @pytest.mark.parametrize("bucket,eps,n", [(32, 0.0, 20_000), (1, 1e-4, 5_000), (8, 0.0, 3)])
 def test_fused_ring_edge_cases(bucket, eps, n):
     """Opened buckets of 32 particles (33 records from one union entry: the
