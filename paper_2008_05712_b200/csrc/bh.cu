@@ -319,7 +319,7 @@ void launch_walk(gc_bh *bh, bool write, bool stats, int *fq = nullptr, int *fq_t
     const int g0 = bh->rg0, g1 = bh->rg1 < 0 ? bh->n_wg : bh->rg1;
     const int ng = g1 - g0;
     const WalkGroup *wg = bh->d_wg.p + g0;
-    const unsigned grid = grid_for(std::max(ng, 1), WARPS_PER_BLOCK);
+    const unsigned grid = grid_for(std::max(ng, 1), WALK_WPB);
     bh->d_flag.resize(1);
     bh->d_flag.zero(s);
     if (stats) {
@@ -354,7 +354,7 @@ void launch_walk(gc_bh *bh, bool write, bool stats, int *fq = nullptr, int *fq_t
                   : walk_group_kernel<false, true, false, true>;
     }
     int per_sm = 0;
-    GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * WARPS_PER_BLOCK, 0));
+    GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * WALK_WPB, 0));
     const unsigned pgrid = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>((int64_t)per_sm * bh->ctx->prop.multiProcessorCount, grid));
     bh->d_wnext.resize(1);
@@ -363,7 +363,7 @@ void launch_walk(gc_bh *bh, bool write, bool stats, int *fq = nullptr, int *fq_t
     if (WALK_COST_LPT) GC_CUDA(cudaMemsetAsync(bh->d_wcost.p + g0, 0, sizeof(int) * ng, s));
     if (setup_only) return;  // the caller launches a kernel with the walk inside (walk_force_kernel)
     // with hints: 2 ng work items (heavy groups split in two, -1 padding)
-    k<<<pgrid, 32 * WARPS_PER_BLOCK, 0, s>>>(ordered ? 2 * ng : ng, wg, bh->d_fg.p, bh->d_recs.p, bh->d_com64.p,
+    k<<<pgrid, 32 * WALK_WPB, 0, s>>>(ordered ? 2 * ng : ng, wg, bh->d_fg.p, bh->d_recs.p, bh->d_com64.p,
                                              bh->d_bgeo.p, bh->d_bgeo32.p, bh->wp, U, bh->d_bstat.p, bh->d_flag.p,
                                              ordered ? bh->d_wg_order.p : nullptr, bh->d_wnext.p,
                                              WALK_COST_LPT ? bh->d_wcost.p + g0 : nullptr, fq, fq_tail, fq_base);
@@ -1403,11 +1403,12 @@ void bh_kernel_spec(const char *cls, int64_t out[5])
     cudaFuncAttributes a;
     GC_CUDA(cudaFuncGetAttributes(&a, fn));
     int blocks = 0;
-    GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, 32 * WARPS_PER_BLOCK, 0));
-    out[0] = 32 * WARPS_PER_BLOCK;
+    const int wpb = !strcmp(cls, "walk") ? WALK_WPB : WARPS_PER_BLOCK;
+    GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, 32 * wpb, 0));
+    out[0] = 32 * wpb;
     out[1] = a.numRegs;
     out[2] = (int64_t)a.sharedSizeBytes;
-    out[3] = WARPS_PER_BLOCK;
+    out[3] = wpb;
     out[4] = blocks;
 }
 }  // namespace gc

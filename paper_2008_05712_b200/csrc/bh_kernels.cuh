@@ -165,6 +165,10 @@ struct UnionPool {
 #ifndef WALK_MINB
 #define WALK_MINB 3
 #endif
+#ifndef GC_WALK_WPB
+#define GC_WALK_WPB 8
+#endif
+constexpr int WALK_WPB = GC_WALK_WPB;  // warps per walk block (occupancy granularity)
 #ifndef WALK_UNROLL
 #define WALK_UNROLL 2
 #endif
@@ -460,7 +464,7 @@ __device__ __forceinline__ void walk_group_body(WALK_ARGS_DECL, WalkSmem &ws, fl
 }
 
 template <bool WRITE, bool STATS, bool NREC = false, bool PER = false>
-__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, WALK_MINB)
+__global__ void __launch_bounds__(32 * WALK_WPB, WALK_MINB)
 walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const ForceGroup *__restrict__ fgroups,
                   const float4 *__restrict__ recs, const double4 *__restrict__ com64,
                   const double4 *__restrict__ bgeo, const float4 *__restrict__ bgeo32, const WalkParams P,
@@ -468,7 +472,7 @@ walk_group_kernel(int ngroups, const WalkGroup *__restrict__ groups, const Force
                   int *__restrict__ next, int *__restrict__ wcost, int *__restrict__ fq = nullptr,
                   int *__restrict__ fq_tail = nullptr, int fq_base = 0)
 {
-    __shared__ WalkSmem ws_s[WARPS_PER_BLOCK];
+    __shared__ WalkSmem ws_s[WALK_WPB];
     __shared__ float2 tt_s[MAX_LEVELS];
     load_thresholds(P, tt_s);
     walk_group_body<WRITE, STATS, NREC, PER>(WALK_ARGS, ws_s[threadIdx.x >> 5], tt_s);
