@@ -116,9 +116,12 @@ gc_status gc_debug_walk_prof(int64_t out[6], int32_t reset);
 gc_status gc_bh_pair_stats(gc_bh *bh, int64_t out[2]);
 /* 1: gc_bh_walk_forces_async / gc_bh_step run the walk and the fused force
  * kernel concurrently (force groups consumed as their walk groups finish);
- * results are identical.  Default 0 (measured neutral); timings then report
- * the whole step as the walk.  The force kernel is a programmatic dependent launch that starts
- * when every walk block has a warp out of work. */
+ * the force kernel is a programmatic dependent launch that starts when every
+ * walk block has a warp out of work.  2: one persistent kernel does both
+ * (walk_force_kernel: a warp drains walk items, then force groups from the
+ * readiness queue; its shared memory holds either the walk stack or the
+ * force ring).  Results are identical in all modes.  Default 0 (1 and 2
+ * measured neutral / slower); timings then report the whole step as the walk. */
 gc_status gc_bh_set_overlap(gc_bh *bh, int32_t on);
 
 /* --- Distributed Barnes-Hut (paper_2008_05712_b200/bh_dist.py) ---
