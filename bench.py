@@ -555,7 +555,9 @@ def bench_md(args, world, rank, local, torch):
         "config": {"workload": "configs[1] LJ FCC 30^3x4 = 108,000 atoms, rho 0.8442, T 1.44, rc 2.5, 20^3 "
                                "cells, dt 0.005, periodic", "tasks_per_step": sysd.task_count(),
                    "timed": "CUDA-graph of 100 full steps (fused force+integrator+cell count kernel, cell sort), "
-                            "events"},
+                            "events",
+                   "parity": "tests/test_md_gpu.py::test_lj_108k_config2_forces / test_lj_steps_vs_oracle (float64 "
+                             "oracle, <= 1e-10); 3-D LJ parity is UNPINNED (no LJ in the reference)"},
         "roofline": {"bound": "hbm", "kernel": "md step (task model)", "achieved": achieved, "peak": hbm,
                      "peak_source": src, "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic("md_cell_kernel"),
                      "algorithmic_bytes_per_step": task_bytes,
@@ -627,7 +629,10 @@ def bench_plummer16m(args):
     out = {"workload": "configs[3] system on 1 GPU: Plummer 16,777,216 particles, theta 0.7, bucket 8",
            "interactions": inter, "ms_per_step": ms, "value": inter / (ms * 1e-3), "unit": "interactions/s",
            "walk_ms": statistics.median(w), "reorg_ms": statistics.median(r), "force_ms": statistics.median(f),
-           "force_tflops": fp, "device_gib": (torch.cuda.mem_get_info()[1] - torch.cuda.mem_get_info()[0]) / 2**30}
+           "force_tflops": fp, "device_gib": (torch.cuda.mem_get_info()[1] - torch.cuda.mem_get_info()[0]) / 2**30,
+           "parity": "tests/test_bh_gpu.py::test_plummer16m_config4_sampled_parity: device tree bit-identical to the "
+                     "oracle's, lists bit-exact and forces <= 1e-5 on sampled walk groups (Plummer has no reference "
+                     "generator: inputs unpinned, algorithm pinned)"}
     del tree
     return out
 
@@ -650,7 +655,10 @@ def bench_md8m(args):
            "ms_per_step": ms, "unit": "ms/step",
            "task_model_gbs": task_bytes / (ms * 1e-3) / 1e9, "task_model_frac": task_bytes / (ms * 1e-3) / 1e9 / hbm,
            "algorithmic_bytes_per_step": task_bytes,
-           "roofline": md_roofline_8m(ms, cells, sysin.cells, sysin.positions.shape[0], sysin, hbm)}
+           "roofline": md_roofline_8m(ms, cells, sysin.cells, sysin.positions.shape[0], sysin, hbm),
+           "parity": "tests/test_md_gpu.py::test_lj_8m_config5_forces (full size vs the float64 oracle, <= 1e-10); "
+                     "3-D LJ parity is UNPINNED: the reference has no LJ workload, the oracle restates md.py's "
+                     "cell-pair algorithm with the LJ law (DESIGN.md section 2)"}
     # configs[4]'s varying task-generation rate: the force phase as column
     # requests through the device trigger, one column-kernel launch per batch
     ph = md.LJColumnPhase(sysd)
@@ -708,7 +716,10 @@ def bench_periodic(args):
     return {"workload": "configs[2] set, periodic: 27 images of the unit box, theta 0.7, bucket 8",
             "interactions": inter, "walk_ms": statistics.median(w), "force_ms": statistics.median(f),
             "ms_per_step": ms, "value": inter / (ms * 1e-3), "unit": "interactions/s",
-            "force_tflops": FLOPS_PER_INTERACTION * inter / (statistics.median(f) * 1e-3) / 1e12}
+            "force_tflops": FLOPS_PER_INTERACTION * inter / (statistics.median(f) * 1e-3) / 1e12,
+            "parity": "tests/test_bh_gpu.py::test_periodic_walk_matches_oracle (per-bucket counts over all images "
+                      "bit-exact, forces <= 1e-5 vs orc_periodic_forces); UNPINNED: the reference only models the "
+                      "periodic class, the restatement is pinned by known answers (test_periodic_oracle_pinned)"}
 
 
 def bench_ewald(args):
