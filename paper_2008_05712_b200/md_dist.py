@@ -128,6 +128,10 @@ class DistTransport:
                 rcnt_r.copy_(cnt_l)
             return
         left, right = neighbours(self.rank, self.k)
+        if send_l.is_cuda and dist.get_backend(self.group) == "gloo":
+            self._exchange_fixed_gloo(left, right, (cnt_l, send_l, cnt_r, send_r), (rcnt_r, recv_r, rcnt_l, recv_l),
+                                      stream)
+            return
         # same issue order on every rank (see exchange): sends left, right, receives right, left
         ops = [dist.P2POp(dist.isend, cnt_l, self._peer(left), self.group, 0),
                dist.P2POp(dist.isend, send_l, self._peer(left), self.group, 2),
@@ -140,6 +144,29 @@ class DistTransport:
         with torch.cuda.stream(stream) if stream is not None else _nullctx():
             for q in dist.batch_isend_irecv(ops):
                 q.wait()  # NCCL: the current (library) stream waits; gloo: completes on the host
+
+
+    def _exchange_fixed_gloo(self, left, right, sends, recvs, stream):
+        """exchange_fixed for the GCHARM_DIST_BACKEND=gloo dry run: gloo moves
+        host memory only, so the device buffers are staged through the host
+        (synchronous; the NCCL path above has no host round trip)."""
+        import torch
+        dist = self.dist
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            hs = [t.cpu() for t in sends]
+            hr = [torch.empty(t.shape, dtype=t.dtype) for t in recvs]
+            ops = [dist.P2POp(dist.isend, hs[0], self._peer(left), self.group, 0),
+                   dist.P2POp(dist.isend, hs[1], self._peer(left), self.group, 2),
+                   dist.P2POp(dist.isend, hs[2], self._peer(right), self.group, 1),
+                   dist.P2POp(dist.isend, hs[3], self._peer(right), self.group, 3),
+                   dist.P2POp(dist.irecv, hr[0], self._peer(right), self.group, 0),
+                   dist.P2POp(dist.irecv, hr[1], self._peer(right), self.group, 2),
+                   dist.P2POp(dist.irecv, hr[2], self._peer(left), self.group, 1),
+                   dist.P2POp(dist.irecv, hr[3], self._peer(left), self.group, 3)]
+            for q in dist.batch_isend_irecv(ops):
+                q.wait()
+            for dst, src in zip(recvs, hr):
+                dst.copy_(src)
 
 
 class _nullctx:
