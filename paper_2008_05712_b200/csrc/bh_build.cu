@@ -606,12 +606,12 @@ __global__ void bb_mass_up(int nb, int dim, const int *__restrict__ buckets, con
                            const int *__restrict__ pcount, const double4 *__restrict__ spos,
                            const int *__restrict__ parent, const int *__restrict__ first_child,
                            const int *__restrict__ nchild, int *__restrict__ arrive, double *nmass, double4 *com,
-                           double *__restrict__ scratch, int climb)
+                           double *__restrict__ scratch)
 {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= nb) return;
     int id = buckets[b];
-    int p = climb ? parent[id] : -1;
+    int p = parent[id];
     {
         const int s = pstart[id], c = pcount[id];
         double m;
@@ -676,29 +676,6 @@ __global__ void bb_parents(int nn, const int *__restrict__ first_child, const in
     const int fc = first_child[id];
     if (fc < 0) return;
     for (int ch = fc; ch < fc + nchild[id]; ++ch) parent[ch] = id;
-}
-
-// internal nodes of one level: children in order (nbody.py:129-135)
-__global__ void bb_internal_mass(int id0, int m, int dim, const int *__restrict__ first_child,
-                                 const int *__restrict__ nchild, double *__restrict__ nmass, double4 *__restrict__ com)
-{
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= m) return;
-    const int id = id0 + p;
-    const int fc = first_child[id];
-    if (fc < 0) return;
-    double ms = 0.0, c3[3] = {0.0, 0.0, 0.0};
-    for (int ch = fc; ch < fc + nchild[id]; ++ch) {
-        const double cmass = nmass[ch];
-        const double4 cc = com[ch];
-        ms = __dadd_rn(ms, cmass);
-        c3[0] = __dadd_rn(c3[0], __dmul_rn(cc.x, cmass));
-        if (dim > 1) c3[1] = __dadd_rn(c3[1], __dmul_rn(cc.y, cmass));
-        if (dim > 2) c3[2] = __dadd_rn(c3[2], __dmul_rn(cc.z, cmass));
-    }
-    nmass[id] = ms;
-    com[id] = make_double4(__ddiv_rn(c3[0], ms), dim > 1 ? __ddiv_rn(c3[1], ms) : 0.0,
-                           dim > 2 ? __ddiv_rn(c3[2], ms) : 0.0, 0.0);
 }
 
 // walk/force records of every node (same encoding as the host upload path)
@@ -947,8 +924,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     mass.resize(n);
     GC_CUDA(cudaEventRecord(bh->main_ready, s));  // earlier work on `mass` (previous build) is done
     GC_CUDA(cudaStreamWaitEvent(bh->side, bh->main_ready, 0));
-    static const bool mass_main = getenv("GC_MASS_MAIN") != nullptr;  // A/B knob
-    GC_CUDA(cudaMemcpyAsync(mass.p, mass_h, sizeof(double) * n, cudaMemcpyHostToDevice, mass_main ? s : bh->side));
+    GC_CUDA(cudaMemcpyAsync(mass.p, mass_h, sizeof(double) * n, cudaMemcpyHostToDevice, bh->side));
     GC_CUDA(cudaEventRecord(bh->side_done, bh->side));
     bh->h2d += (int64_t)n * (dim + 1) * (int64_t)sizeof(double);
     auto &k1 = bh->ws.k1;
@@ -1005,7 +981,6 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     check_launch("bb sort");
     prof.mark("sort");
 
-    std::vector<int> lvl_first;
     int nn = 0, nb = 0;
     auto &lk_s = bh->ws.lk_s;
     if (bh->n_forced == 0) {
@@ -1046,10 +1021,6 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
         }
         nn = lf[NL];
         nb = lf[NL + 1] - nn;
-        int nlevels = 1;
-        while (nlevels < NL && lf[nlevels] < nn) ++nlevels;
-        lvl_first.assign(lf.begin(), lf.begin() + nlevels);
-        lvl_first.push_back(nn);
         const size_t cap = std::max<size_t>((size_t)3 * n + 1024, (size_t)nn);
         bh->d_ncenter.resize(cap);
         bh->d_pstart.resize(cap);
@@ -1172,9 +1143,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
         GC_CUDA(cudaStreamSynchronize(s));
         GC_REQUIRE(!lf[MAX_KEY_LEVELS + 3], GC_E_VALUE, "node capacity exceeded");
         const int nlevels = lf[MAX_KEY_LEVELS + 2];
-        lvl_first.assign(lf.begin(), lf.begin() + nlevels + 1);
-        const int next_id = lvl_first.back();
-        nn = next_id;
+        nn = lf[nlevels];  // level firsts lf[0 .. nlevels]: the last is the node count
         GC_CUDA(cudaMemcpyAsync(&nb, nleaf.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         GC_CUDA(cudaStreamSynchronize(s));
 
@@ -1208,10 +1177,6 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     scratch.resize(n);
     GC_CUDA(cudaStreamWaitEvent(s, bh->side_done, 0));
     auto &par = bh->ws.parent;
-    static const bool climb = [] {
-        const char *e = getenv("GC_BUILD_CLIMB");
-        return e ? atoi(e) != 0 : true;
-    }();
     if (bh->n_forced != 0) {  // the cooperative build writes no parents
         par.resize(std::max<size_t>(nn, 1));
         bb_parents<<<grid_for(nn, BB_TPB), BB_TPB, 0, s>>>(nn, bh->d_first_child.p, bh->d_nchild.p, par.p);
@@ -1227,14 +1192,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     GC_CUDA(cudaMemsetAsync(arrive.p, 0, sizeof(int) * nn, s));
     bb_mass_up<<<grid_for(nb, 128), 128, 0, s>>>(nb, dim, bh->d_buckets.p, bh->d_pstart.p, bh->d_pcount.p, spos.p,
                                                   par.p, bh->d_first_child.p, bh->d_nchild.p, arrive.p,
-                                                  bh->d_nmass.p, com.p, scratch.p, climb ? 1 : 0);
-    if (!climb) {
-        for (int L = (int)lvl_first.size() - 2; L >= 0; --L) {
-            const int id0 = lvl_first[L], mL = lvl_first[L + 1] - id0;
-            bb_internal_mass<<<grid_for(mL, 128), 128, 0, s>>>(id0, mL, dim, bh->d_first_child.p, bh->d_nchild.p,
-                                                                bh->d_nmass.p, com.p);
-        }
-    }
+                                                  bh->d_nmass.p, com.p, scratch.p);
     check_launch("bb mass");
     prof.mark("mass");
 
