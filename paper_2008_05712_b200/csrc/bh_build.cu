@@ -704,6 +704,64 @@ __global__ void bb_records(int nn, const double4 *__restrict__ com, const double
     cmax[i] = mx;
 }
 
+// Particles inside each bucket in ascending original id (nbody.py:110 keeps
+// particle_idx ascending): one thread per bucket, a bitonic network in
+// registers for <= 8 / <= 32 particles (ids are distinct), an insertion sort
+// otherwise (such buckets are rejected by bb_groups anyway).
+template <int N>
+__device__ __forceinline__ void bitonic_sort_regs(int (&v)[N])
+{
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const int a = v[i], b = v[l];
+                    const bool up = (i & k) == 0;
+                    v[i] = up ? min(a, b) : max(a, b);
+                    v[l] = up ? max(a, b) : min(a, b);
+                }
+            }
+}
+
+template <int N>
+__device__ __forceinline__ void bucket_sort_net(int s, int c, const int *__restrict__ perm, int *__restrict__ pidx)
+{
+    int v[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = i < c ? perm[s + i] : INT_MAX;
+    bitonic_sort_regs<N>(v);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        if (i < c) pidx[s + i] = v[i];
+}
+
+__global__ void bb_bucket_sort(int nb, int n, const int *__restrict__ bstart, const int *__restrict__ perm,
+                               int *__restrict__ pidx)
+{
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    const int s = bstart[b], c = (b + 1 < nb ? bstart[b + 1] : n) - s;
+    if (c <= 8) {
+        bucket_sort_net<8>(s, c, perm, pidx);
+    } else if (c <= 32) {
+        bucket_sort_net<32>(s, c, perm, pidx);
+    } else {
+        for (int i = 0; i < c; ++i) {
+            const int v = perm[s + i];
+            int j = i - 1;
+            while (j >= 0 && pidx[s + j] > v) {
+                pidx[s + j + 1] = pidx[s + j];
+                --j;
+            }
+            pidx[s + j + 1] = v;
+        }
+    }
+}
+
 // particles in tree (sorted) order, gathered once: float64 (x, y, z, m) for
 // the masses, float32 records for the force kernels, the original ids
 __global__ void bb_sorted_parts(int n, int dim, const int *__restrict__ pidx, const double *__restrict__ pos,
@@ -1154,19 +1212,11 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
             return cub::DeviceRadixSort::SortPairs(t, b, leaf_key.p, lk_s.p, leaf_id.p, bh->d_buckets.p, nb, 0, 32, s);
         });
     }
-    // particles inside each bucket: ascending original id
-    auto &offs = bh->ws.offs;
+    // particles inside each bucket: ascending original id (buckets tile the
+    // sorted particles in start order)
     auto &pidx = bh->ws.pidx;
-    offs.resize(nb + 1);
-    {
-        // offsets = sorted bucket starts, plus n
-        GC_CUDA(cudaMemcpyAsync(offs.p, lk_s.p, sizeof(int) * nb, cudaMemcpyDeviceToDevice, s));
-        GC_CUDA(cudaMemcpyAsync(offs.p + nb, &n, sizeof(int), cudaMemcpyHostToDevice, s));
-    }
     pidx.resize(n);
-    cubc(ctx, [&](void *t, size_t &b) {
-        return cub::DeviceSegmentedSort::SortKeys(t, b, perm.p, pidx.p, n, nb, offs.p, offs.p + 1, s);
-    });
+    bb_bucket_sort<<<grid_for(nb, 128), 128, 0, s>>>(nb, n, lk_s.p, perm.p, pidx.p);
     check_launch("bb buckets");
     prof.mark("segsort");
 

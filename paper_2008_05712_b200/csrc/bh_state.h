@@ -18,7 +18,7 @@ struct BuildWs {  // device-build scratch, kept across builds (no per-step cudaM
     DBuf<int> lstart, lcount, cstart, ccount, leaf_key, leaf_id, nleaf;
     DBuf<double4> lcenter, ccenter;
     DBuf<int> lk_s;
-    DBuf<int> offs, pidx;
+    DBuf<int> pidx;
     DBuf<double4> com;
     DBuf<double> cmax, cmax_out;
     DBuf<int> nfg_of, fg_base, bad;
