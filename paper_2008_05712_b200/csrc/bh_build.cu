@@ -997,13 +997,14 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     k1.resize(n); k2.resize(n); k1p.resize(n); k1s.resize(n); k2s.resize(n);
     idx.resize(n); perm1.resize(n); perm.resize(n);
     // stable sort by (k1, k2), ties by original id.  Digits of a level no
-    // node splits at do not change the tree, so first sort by the top
-    // SORT_LEVELS levels only; if some run of equal top keys is longer than a
-    // bucket (a node of that level would split), redo it with all levels
-    // (LSD on k2, then k1).  (Measured: splitting the 48-bit sort into 32-bit
-    // + 16-bit key passes is not faster at 1M.)
-    constexpr int SORT_LEVELS = 16;  // 48 bits: six 8-bit radix passes
-    const int top_bits = 3 * std::min(nlev, SORT_LEVELS);
+    // node splits at do not change the tree, so first sort by the top Ls
+    // levels only; if some run of equal top keys is longer than a bucket (a
+    // node of that level would split), redo it with SORT_LEVELS_MAX levels,
+    // then with all levels (LSD on k2, then k1).  Ls starts at 10 (30 bits,
+    // four 8-bit radix passes: enough for clustered 1M) and sticks per handle
+    // at the depth the last build needed (Plummer: 16).  (Measured: splitting
+    // the 48-bit sort into 32-bit + 16-bit key passes is not faster at 1M.)
+    constexpr int SORT_LEVELS_MAX = 16;  // 48 bits: six passes
     int bexp = 0;
     if (std::frexp(box, &bexp) == 0.5)
         bb_keys_dyadic<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, dim, pos.p, 1.0 / box, nlev, k1.p, k2.p, idx.p);
@@ -1011,12 +1012,24 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
         bb_keys<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, dim, pos.p, box, nlev, k1.p, k2.p, idx.p);
     check_launch("bb_keys");
     prof.mark("keys");
-    cubc(ctx, [&](void *t, size_t &b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, k1.p, k1s.p, idx.p, perm.p, n, 63 - top_bits, 63, s);
-    });
-    // k1s holds the full keys in the sorted order; k2 follows the permutation
-    bb_gather_u64<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, perm.p, k2.p, k2s.p);
-    prof.mark("radix");
+    scratch_i.resize(1);
+    int deep = bh->n_forced > 0 ? 1 : 0;  // forced cubes may split below the top levels
+    int Ls = std::min(bh->sort_levels, SORT_LEVELS_MAX);
+    // a run of equal top keys longer than a bucket: checked on the device, read
+    // back at the level-count sync below (a deeper sort redoes the levels there)
+    bool check_deep = false;
+    auto sort_top = [&](int levels) {
+        const int top_bits = 3 * std::min(nlev, levels);
+        cubc(ctx, [&](void *t, size_t &b) {
+            return cub::DeviceRadixSort::SortPairs(t, b, k1.p, k1s.p, idx.p, perm.p, n, 63 - top_bits, 63, s);
+        });
+        // k1s holds the full keys in the sorted order; k2 follows the permutation
+        bb_gather_u64<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, perm.p, k2.p, k2s.p);
+        check_deep = nlev > levels;
+        scratch_i.zero(s);
+        if (check_deep)
+            bb_long_runs<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, (int)bucket, k1s.p, 63 - top_bits, scratch_i.p);
+    };
     auto sort_deep = [&] {
         cubc(ctx, [&](void *t, size_t &b) {
             return cub::DeviceRadixSort::SortPairs(t, b, k2.p, k2s.p, idx.p, perm1.p, n, 0, 64, s);
@@ -1026,16 +1039,12 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
             return cub::DeviceRadixSort::SortPairs(t, b, k1p.p, k1s.p, perm1.p, perm.p, n, 0, 64, s);
         });
         bb_gather_u64<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, perm.p, k2.p, k2s.p);
+        check_deep = false;
+        scratch_i.zero(s);
     };
-    int deep = bh->n_forced > 0 ? 1 : 0;  // forced cubes may split below the top levels
-    // a run of equal top keys longer than a bucket: checked on the device, read
-    // back at the level-count sync below (the rare deep case re-sorts there)
-    bool check_deep = !deep && nlev > SORT_LEVELS;
-    scratch_i.resize(1);
-    scratch_i.zero(s);
-    if (check_deep)
-        bb_long_runs<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, (int)bucket, k1s.p, 63 - top_bits, scratch_i.p);
     if (deep) sort_deep();
+    else sort_top(Ls);
+    prof.mark("radix");
     check_launch("bb sort");
     prof.mark("sort");
 
@@ -1044,7 +1053,7 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
     if (bh->n_forced == 0) {
       for (;;) {  // once, or twice when the top-level sort was not deep enough
         // bottom-up enumeration (bb_lcp / bb_node_levels / one scan / bb_emit_nodes)
-        const int Ds = deep ? nlev : std::min(nlev, SORT_LEVELS);  // sorted key depth
+        const int Ds = deep ? nlev : std::min(nlev, Ls);  // sorted key depth
         const int NL = Ds + 1;  // node levels 0 .. Ds
         const int W = (n + 31) / 32;
         auto &dl = bh->ws.dl, &el = bh->ws.el;
@@ -1071,10 +1080,15 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
         std::vector<int> lf(NL + 3);
         lvlf.download(lf.data(), NL + 3, s);
         GC_CUDA(cudaStreamSynchronize(s));
-        if (check_deep && lf[NL + 2]) {
-            deep = 1;
-            check_deep = false;
-            sort_deep();
+        if (check_deep && lf[NL + 2]) {  // a run longer than a bucket below the sorted levels
+            if (Ls < SORT_LEVELS_MAX && nlev > Ls) {
+                Ls = SORT_LEVELS_MAX;
+                bh->sort_levels = Ls;  // sticks for the next builds of this handle
+                sort_top(Ls);
+            } else {
+                deep = 1;
+                sort_deep();
+            }
             continue;
         }
         nn = lf[NL];

@@ -123,6 +123,7 @@ struct gc_bh {
     // walk begin/end, forces begin/end, reorganisation end (= force kernel begin)
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     BuildWs ws;
+    int sort_levels = 10;  // key levels the device build sorts first (grows to 16 when a run exceeds a bucket)
     // distributed BH (bh_dist.py): cubes the device build must split whatever
     // their local count (they straddle ranks; globally they split), as
     // (level, left-aligned key prefix) sorted; walk-group cut points (DFS
