@@ -21,7 +21,7 @@
 //  5. Masses/centres of mass with the reference's float64 rounding sequence:
 //     bucket mass = numpy pairwise sum, COM = sequential column sum / mass;
 //     internal nodes add children in order -- one bottom-up pass, the last
-//     child to finish computes its parent (bb_mass_up).
+//     child to finish computes its parent (bb_bucket_pass).
 //  6. Force/walk records, bucket geometry and walk/force groups in HBM.
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
@@ -563,81 +563,51 @@ __device__ double np_pairwise(const double *a, int n)
     return __dadd_rn(np_pairwise(a, h), np_pairwise(a + h, n - h));
 }
 
-// Bucket mass + COM in registers for buckets of <= 8 particles (the common
-// case): numpy's pairwise sum is the sequential sum below 8 and the fixed
-// 8-leaf tree at 8 (np_pairwise).  Sorted particles: contiguous loads.
-__device__ __forceinline__ bool bucket_mass_small(int dim, int s, int c, const double4 *__restrict__ spos,
-                                                  double &m_out, double4 &com_out)
+// particle ids of a bucket in ascending order (nbody.py:110 keeps
+// particle_idx ascending): a bitonic network in registers (ids are distinct)
+template <int N>
+__device__ __forceinline__ void bitonic_sort_regs(int (&v)[N])
 {
-    if (c > 8) return false;
-    double4 q[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) q[i] = i < c ? spos[s + i] : make_double4(0.0, 0.0, 0.0, 0.0);
-    double m;
-    if (c == 8) {
-        m = __dadd_rn(__dadd_rn(__dadd_rn(q[0].w, q[1].w), __dadd_rn(q[2].w, q[3].w)),
-                      __dadd_rn(__dadd_rn(q[4].w, q[5].w), __dadd_rn(q[6].w, q[7].w)));
-    } else {
-        m = 0.0;
+    for (int k = 2; k <= N; k <<= 1)
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (i < c) m = __dadd_rn(m, q[i].w);
-    }
-    double ax = __dmul_rn(q[0].x, q[0].w), ay = __dmul_rn(q[0].y, q[0].w), az = __dmul_rn(q[0].z, q[0].w);
+        for (int j = k >> 1; j > 0; j >>= 1)
 #pragma unroll
-    for (int i = 1; i < 8; ++i) {
-        if (i < c) {
-            ax = __dadd_rn(ax, __dmul_rn(q[i].x, q[i].w));
-            ay = __dadd_rn(ay, __dmul_rn(q[i].y, q[i].w));
-            az = __dadd_rn(az, __dmul_rn(q[i].z, q[i].w));
-        }
-    }
-    m_out = m;
-    com_out = make_double4(__ddiv_rn(ax, m), dim > 1 ? __ddiv_rn(ay, m) : 0.0, dim > 2 ? __ddiv_rn(az, m) : 0.0, 0.0);
-    return true;
+            for (int i = 0; i < N; ++i) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const int a = v[i], b = v[l];
+                    const bool up = (i & k) == 0;
+                    v[i] = up ? min(a, b) : max(a, b);
+                    v[l] = up ? max(a, b) : min(a, b);
+                }
+            }
 }
 
-// One pass for every node's mass and COM: a thread computes its bucket, then
-// climbs -- the last child of a node to arrive (fence + arrival counter: its
-// siblings' results are visible in L2) sums that node's children in order
-// (nbody.py:129-135), so each node is computed once with the reference's
-// rounding sequence and no per-level launches.
-__global__ void bb_mass_up(int nb, int dim, const int *__restrict__ buckets, const int *__restrict__ pstart,
-                           const int *__restrict__ pcount, const double4 *__restrict__ spos,
-                           const int *__restrict__ parent, const int *__restrict__ first_child,
-                           const int *__restrict__ nchild, int *__restrict__ arrive, double *nmass, double4 *com,
-                           double *__restrict__ scratch)
+template <int N>
+__device__ __forceinline__ void bucket_sort_net(int s, int c, const int *__restrict__ perm, int *__restrict__ pidx)
 {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nb) return;
-    int id = buckets[b];
-    int p = parent[id];
-    {
-        const int s = pstart[id], c = pcount[id];
-        double m;
-        double4 cm;
-        if (!bucket_mass_small(dim, s, c, spos, m, cm)) {
-            for (int i = 0; i < c; ++i) scratch[s + i] = spos[s + i].w;
-            const double *mb = scratch + s;
-            m = np_pairwise(mb, c);
-            double a3[3] = {0.0, 0.0, 0.0};
-            for (int k = 0; k < dim; ++k) {
-                const double *ps = reinterpret_cast<const double *>(spos + s) + k;
-                double acc = __dmul_rn(ps[0], mb[0]);
-                for (int i = 1; i < c; ++i) acc = __dadd_rn(acc, __dmul_rn(ps[4 * i], mb[i]));
-                a3[k] = __ddiv_rn(acc, m);
-            }
-            cm = make_double4(a3[0], a3[1], a3[2], 0.0);
-        }
-        nmass[id] = m;
-        com[id] = cm;
-    }
+    int v[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = i < c ? perm[s + i] : INT_MAX;
+    bitonic_sort_regs<N>(v);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        if (i < c) pidx[s + i] = v[i];
+}
+
+// climb from a finished node: the last child of a node to arrive sums that
+// node's children in order (nbody.py:129-135)
+__device__ __forceinline__ void mass_climb(int p, int dim, const int *__restrict__ parent,
+                                           const int *__restrict__ first_child, const int *__restrict__ nchild,
+                                           int *__restrict__ arrive, double *nmass, double4 *com)
+{
     while (p >= 0) {
         const int fc = first_child[p], nc = nchild[p], pp = parent[p];  // issued before the arrival
         int old;  // release: this thread's node results are visible before its arrival
         asm volatile("atom.release.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(arrive + p) : "memory");
-        if (old != nc - 1) break;
-        // the last arrival: every sibling fenced before arriving; read them from
+        if (old != nc - 1) return;
+        // the last arrival: every sibling released before arriving; read them from
         // L2 (.cg, no stale L1 lines), all loads issued before the in-order sums
         double cm[8];
         double2 cxy[8], czw[8];
@@ -664,6 +634,119 @@ __global__ void bb_mass_up(int nb, int dim, const int *__restrict__ buckets, con
                               dim > 2 ? __ddiv_rn(c3[2], ms) : 0.0, 0.0);
         p = pp;
     }
+}
+
+// Every bucket in one pass (thread = bucket): its particle ids in ascending
+// original id (nbody.py:110), the particles gathered into tree order (float32
+// records, original ids, bucket of each particle), the bucket's mass (numpy
+// pairwise order) and COM (sequential) from registers, its geometry, then the
+// climb to the root.  Buckets of more than 8 particles take the general path
+// through global scratch (sorted ids in pidx, float64 particles in spos).
+__global__ void bb_bucket_pass(int nb, int dim, const int *__restrict__ buckets, const int *__restrict__ pstart,
+                               const int *__restrict__ pcount, const int *__restrict__ perm,
+                               const double *__restrict__ pos, const double *__restrict__ mass,
+                               const double4 *__restrict__ ncenter, const int *__restrict__ parent,
+                               const int *__restrict__ first_child, const int *__restrict__ nchild,
+                               int *__restrict__ arrive, double *nmass, double4 *com, float4 *__restrict__ parts,
+                               int *__restrict__ porder, int *__restrict__ part_bucket, double4 *__restrict__ bgeo,
+                               float4 *__restrict__ bgeo32, int2 *__restrict__ brange, int *__restrict__ bids,
+                               int *__restrict__ pidx, double4 *__restrict__ spos, double *__restrict__ scratch)
+{
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    const int id = buckets[b];
+    const int s = pstart[id], c = pcount[id];
+    double m;
+    double4 cm;
+    if (c <= 8) {
+        int v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = i < c ? perm[s + i] : INT_MAX;
+        bitonic_sort_regs<8>(v);
+        double4 q[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (i < c) {
+                const int p = v[i];
+                q[i] = make_double4(pos[(int64_t)p * dim], dim > 1 ? pos[(int64_t)p * dim + 1] : 0.0,
+                                    dim > 2 ? pos[(int64_t)p * dim + 2] : 0.0, mass[p]);
+            } else {
+                q[i] = make_double4(0.0, 0.0, 0.0, 0.0);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (i < c) {
+                parts[s + i] = make_float4((float)q[i].x, (float)q[i].y, (float)q[i].z, (float)q[i].w);
+                porder[s + i] = v[i];
+                part_bucket[s + i] = b;
+            }
+        }
+        // numpy pairwise: sequential below 8, the fixed 8-leaf tree at 8
+        if (c == 8) {
+            m = __dadd_rn(__dadd_rn(__dadd_rn(q[0].w, q[1].w), __dadd_rn(q[2].w, q[3].w)),
+                          __dadd_rn(__dadd_rn(q[4].w, q[5].w), __dadd_rn(q[6].w, q[7].w)));
+        } else {
+            m = 0.0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (i < c) m = __dadd_rn(m, q[i].w);
+        }
+        double ax = __dmul_rn(q[0].x, q[0].w), ay = __dmul_rn(q[0].y, q[0].w), az = __dmul_rn(q[0].z, q[0].w);
+#pragma unroll
+        for (int i = 1; i < 8; ++i) {
+            if (i < c) {
+                ax = __dadd_rn(ax, __dmul_rn(q[i].x, q[i].w));
+                ay = __dadd_rn(ay, __dmul_rn(q[i].y, q[i].w));
+                az = __dadd_rn(az, __dmul_rn(q[i].z, q[i].w));
+            }
+        }
+        cm = make_double4(__ddiv_rn(ax, m), dim > 1 ? __ddiv_rn(ay, m) : 0.0, dim > 2 ? __ddiv_rn(az, m) : 0.0, 0.0);
+    } else {
+        if (c <= 32) {
+            bucket_sort_net<32>(s, c, perm, pidx);
+        } else {
+            for (int i = 0; i < c; ++i) {
+                const int v = perm[s + i];
+                int j = i - 1;
+                while (j >= 0 && pidx[s + j] > v) {
+                    pidx[s + j + 1] = pidx[s + j];
+                    --j;
+                }
+                pidx[s + j + 1] = v;
+            }
+        }
+        for (int i = 0; i < c; ++i) {
+            const int p = pidx[s + i];
+            const double4 q = make_double4(pos[(int64_t)p * dim], dim > 1 ? pos[(int64_t)p * dim + 1] : 0.0,
+                                           dim > 2 ? pos[(int64_t)p * dim + 2] : 0.0, mass[p]);
+            spos[s + i] = q;
+            scratch[s + i] = q.w;
+            parts[s + i] = make_float4((float)q.x, (float)q.y, (float)q.z, (float)q.w);
+            porder[s + i] = p;
+            part_bucket[s + i] = b;
+        }
+        m = np_pairwise(scratch + s, c);
+        double a3[3] = {0.0, 0.0, 0.0};
+        for (int k = 0; k < dim; ++k) {
+            const double *ps = reinterpret_cast<const double *>(spos + s) + k;
+            double acc = __dmul_rn(ps[0], scratch[s]);
+            for (int i = 1; i < c; ++i) acc = __dadd_rn(acc, __dmul_rn(ps[4 * i], scratch[s + i]));
+            a3[k] = __ddiv_rn(acc, m);
+        }
+        cm = make_double4(a3[0], a3[1], a3[2], 0.0);
+    }
+    nmass[id] = m;
+    com[id] = cm;
+    // bucket geometry (walk tests: float32 copy when exact, else flagged)
+    const double4 g = ncenter[id];
+    bgeo[b] = g;
+    const float f0 = (float)g.x, f1 = (float)g.y, f2 = (float)g.z, fh = (float)g.w;
+    const bool ex = f0 == g.x && f1 == g.y && f2 == g.z && fh == g.w;
+    bgeo32[b] = make_float4(f0, f1, f2, ex ? fh : -1.f);
+    brange[b] = make_int2(s, c);
+    bids[b] = b;
+    mass_climb(parent[id], dim, parent, first_child, nchild, arrive, nmass, com);
 }
 
 // parent of every node from the children ranges (cooperative-build path)
@@ -704,100 +787,7 @@ __global__ void bb_records(int nn, const double4 *__restrict__ com, const double
     cmax[i] = mx;
 }
 
-// Particles inside each bucket in ascending original id (nbody.py:110 keeps
-// particle_idx ascending): one thread per bucket, a bitonic network in
-// registers for <= 8 / <= 32 particles (ids are distinct), an insertion sort
-// otherwise (such buckets are rejected by bb_groups anyway).
-template <int N>
-__device__ __forceinline__ void bitonic_sort_regs(int (&v)[N])
-{
-#pragma unroll
-    for (int k = 2; k <= N; k <<= 1)
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1)
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                const int l = i ^ j;
-                if (l > i) {
-                    const int a = v[i], b = v[l];
-                    const bool up = (i & k) == 0;
-                    v[i] = up ? min(a, b) : max(a, b);
-                    v[l] = up ? max(a, b) : min(a, b);
-                }
-            }
-}
 
-template <int N>
-__device__ __forceinline__ void bucket_sort_net(int s, int c, const int *__restrict__ perm, int *__restrict__ pidx)
-{
-    int v[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) v[i] = i < c ? perm[s + i] : INT_MAX;
-    bitonic_sort_regs<N>(v);
-#pragma unroll
-    for (int i = 0; i < N; ++i)
-        if (i < c) pidx[s + i] = v[i];
-}
-
-__global__ void bb_bucket_sort(int nb, int n, const int *__restrict__ bstart, const int *__restrict__ perm,
-                               int *__restrict__ pidx)
-{
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nb) return;
-    const int s = bstart[b], c = (b + 1 < nb ? bstart[b + 1] : n) - s;
-    if (c <= 8) {
-        bucket_sort_net<8>(s, c, perm, pidx);
-    } else if (c <= 32) {
-        bucket_sort_net<32>(s, c, perm, pidx);
-    } else {
-        for (int i = 0; i < c; ++i) {
-            const int v = perm[s + i];
-            int j = i - 1;
-            while (j >= 0 && pidx[s + j] > v) {
-                pidx[s + j + 1] = pidx[s + j];
-                --j;
-            }
-            pidx[s + j + 1] = v;
-        }
-    }
-}
-
-// particles in tree (sorted) order, gathered once: float64 (x, y, z, m) for
-// the masses, float32 records for the force kernels, the original ids
-__global__ void bb_sorted_parts(int n, int dim, const int *__restrict__ pidx, const double *__restrict__ pos,
-                                const double *__restrict__ mass, double4 *__restrict__ spos,
-                                float4 *__restrict__ parts, int *__restrict__ porder)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int p = pidx[i];
-    const double x = pos[(int64_t)p * dim];
-    const double y = dim > 1 ? pos[(int64_t)p * dim + 1] : 0.0;
-    const double z = dim > 2 ? pos[(int64_t)p * dim + 2] : 0.0;
-    const double m = mass[p];
-    spos[i] = make_double4(x, y, z, m);
-    parts[i] = make_float4((float)x, (float)y, (float)z, (float)m);
-    porder[i] = p;
-}
-
-__global__ void bb_buckets(int nb, const int *__restrict__ buckets, const double4 *__restrict__ ncenter,
-                           const int *__restrict__ pstart, const int *__restrict__ pcount, double4 *__restrict__ bgeo,
-                           float4 *__restrict__ bgeo32, int2 *__restrict__ brange, int *__restrict__ bids,
-                           int *__restrict__ part_bucket)
-{
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nb) return;
-    const int id = buckets[b];
-    const double4 g = ncenter[id];
-    bgeo[b] = g;
-    const float f0 = (float)g.x, f1 = (float)g.y, f2 = (float)g.z, fh = (float)g.w;
-    const bool ex = f0 == g.x && f1 == g.y && f2 == g.z && fh == g.w;
-    bgeo32[b] = make_float4(f0, f1, f2, ex ? fh : -1.f);
-    const int s = pstart[id], c = pcount[id];
-    brange[b] = make_int2(s, c);
-    bids[b] = b;
-    for (int k = 0; k < c; ++k) part_bucket[s + k] = b;
-}
 
 // walk groups of 32 buckets; force groups greedily packed (<= 32 targets)
 // inside each walk group, as the host path: pass 0 counts, pass 1 writes
@@ -1226,39 +1216,39 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
             return cub::DeviceRadixSort::SortPairs(t, b, leaf_key.p, lk_s.p, leaf_id.p, bh->d_buckets.p, nb, 0, 32, s);
         });
     }
-    // particles inside each bucket: ascending original id (buckets tile the
-    // sorted particles in start order)
-    auto &pidx = bh->ws.pidx;
-    pidx.resize(n);
-    bb_bucket_sort<<<grid_for(nb, 128), 128, 0, s>>>(nb, n, lk_s.p, perm.p, pidx.p);
-    check_launch("bb buckets");
-    prof.mark("segsort");
-
-    // masses and centres of mass
+    // every bucket in one pass: particle order, tree-ordered particles, bucket
+    // mass / COM and geometry, the climb to the root
+    GC_CUDA(cudaStreamWaitEvent(s, bh->side_done, 0));
     bh->d_nmass.resize(nn);
     auto &com = bh->ws.com;
     com.resize(nn);
     scratch.resize(n);
-    GC_CUDA(cudaStreamWaitEvent(s, bh->side_done, 0));
     auto &par = bh->ws.parent;
     if (bh->n_forced != 0) {  // the cooperative build writes no parents
         par.resize(std::max<size_t>(nn, 1));
         bb_parents<<<grid_for(nn, BB_TPB), BB_TPB, 0, s>>>(nn, bh->d_first_child.p, bh->d_nchild.p, par.p);
     }
+    auto &pidx = bh->ws.pidx;
+    auto &spos = bh->ws.spos;
+    pidx.resize(n);
+    spos.resize(n);
     bh->d_parts.resize(n);
     bh->d_porder.resize(n);
-    auto &spos = bh->ws.spos;
-    spos.resize(n);
-    bb_sorted_parts<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, dim, pidx.p, pos.p, mass.p, spos.p, bh->d_parts.p,
-                                                           bh->d_porder.p);
+    bh->d_part_bucket.resize(n);
+    bh->d_bgeo.resize(nb);
+    bh->d_bgeo32.resize(nb);
+    bh->d_brange.resize(nb);
+    bh->d_bucket_ids.resize(nb);
     auto &arrive = bh->ws.arrive;
     arrive.resize(std::max(nn, 1));
     GC_CUDA(cudaMemsetAsync(arrive.p, 0, sizeof(int) * nn, s));
-    bb_mass_up<<<grid_for(nb, 128), 128, 0, s>>>(nb, dim, bh->d_buckets.p, bh->d_pstart.p, bh->d_pcount.p, spos.p,
-                                                  par.p, bh->d_first_child.p, bh->d_nchild.p, arrive.p,
-                                                  bh->d_nmass.p, com.p, scratch.p);
-    check_launch("bb mass");
-    prof.mark("mass");
+    bb_bucket_pass<<<grid_for(nb, 128), 128, 0, s>>>(
+        nb, dim, bh->d_buckets.p, bh->d_pstart.p, bh->d_pcount.p, perm.p, pos.p, mass.p, bh->d_ncenter.p, par.p,
+        bh->d_first_child.p, bh->d_nchild.p, arrive.p, bh->d_nmass.p, com.p, bh->d_parts.p, bh->d_porder.p,
+        bh->d_part_bucket.p, bh->d_bgeo.p, bh->d_bgeo32.p, bh->d_brange.p, bh->d_bucket_ids.p, pidx.p, spos.p,
+        scratch.p);
+    check_launch("bb bucket pass");
+    prof.mark("buckets+mass");
 
     // records
     auto &cmax = bh->ws.cmax;
@@ -1275,14 +1265,6 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
                                                        bh->d_com64.p, bh->d_rec_hi.p, bh->d_rec_lo.p, bh->d_prange.p,
                                                        cmax.p);
     cubc(ctx, [&](void *t, size_t &b) { return cub::DeviceReduce::Max(t, b, cmax.p, cmax_out.p, nn, s); });
-    bh->d_bgeo.resize(nb);
-    bh->d_bgeo32.resize(nb);
-    bh->d_brange.resize(nb);
-    bh->d_bucket_ids.resize(nb);
-    bh->d_part_bucket.resize(n);
-    bb_buckets<<<grid_for(nb, BB_TPB), BB_TPB, 0, s>>>(nb, bh->d_buckets.p, bh->d_ncenter.p, bh->d_pstart.p,
-                                                       bh->d_pcount.p, bh->d_bgeo.p, bh->d_bgeo32.p, bh->d_brange.p,
-                                                       bh->d_bucket_ids.p, bh->d_part_bucket.p);
     check_launch("bb records");
     prof.mark("records");
     // groups
