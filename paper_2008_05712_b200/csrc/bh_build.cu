@@ -482,7 +482,8 @@ __global__ void bb_emit_nodes(int n, int dim, int NL, int W, double box, const u
                               const unsigned *__restrict__ words, const int *__restrict__ S,
                               const signed char *__restrict__ d, double4 *__restrict__ ncenter,
                               int *__restrict__ pstart, int *__restrict__ pcount, int *__restrict__ first_child,
-                              int *__restrict__ parent, int *__restrict__ buckets, int *__restrict__ bstart)
+                              int *__restrict__ nchild, int *__restrict__ parent, int *__restrict__ buckets,
+                              int *__restrict__ bstart)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -506,6 +507,8 @@ __global__ void bb_emit_nodes(int n, int dim, int NL, int W, double box, const u
                 int end = i + 1;
                 while (end < n && d[end] >= c) ++end;
                 pcount[id] = end - i;
+                first_child[id] = -1;
+                nchild[id] = 0;
                 const size_t ob = (size_t)NL * W + w;
                 const int bi = S[ob] + __popc(words[ob] & lt) - S[(size_t)NL * W];
                 buckets[bi] = id;
@@ -1090,14 +1093,12 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
         bh->d_first_child.resize(cap);
         bh->d_nchild.resize(cap);
         par.resize(cap);
-        bb_fill<<<grid_for(nn, BB_TPB), BB_TPB, 0, s>>>(nn, bh->d_first_child.p, -1);
-        GC_CUDA(cudaMemsetAsync(bh->d_nchild.p, 0, sizeof(int) * nn, s));
         bh->d_buckets.resize(nb);
         lk_s.resize(nb);
         bb_emit_nodes<<<grid_for(n, BB_TPB), BB_TPB, 0, s>>>(n, dim, NL, W, box, k1s.p, k2s.p, range.p, words.p,
                                                              wscan.p, dl.p, bh->d_ncenter.p, bh->d_pstart.p,
-                                                             bh->d_pcount.p, bh->d_first_child.p, par.p,
-                                                             bh->d_buckets.p, lk_s.p);
+                                                             bh->d_pcount.p, bh->d_first_child.p, bh->d_nchild.p,
+                                                             par.p, bh->d_buckets.p, lk_s.p);
         if (nn > 1)
             bb_nchild<<<grid_for(nn - 1, BB_TPB), BB_TPB, 0, s>>>(nn, par.p, bh->d_first_child.p, bh->d_nchild.p);
         check_launch("bb emit nodes");
