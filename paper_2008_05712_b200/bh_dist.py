@@ -110,6 +110,67 @@ def cube_range(k1, k2, level: int, P: int):
     return lo, hi
 
 
+# --------------------------------------------------------------------------
+# host-orchestration helpers: the protocol's million-row sorts and gathers run
+# on the GPU when one is present (numpy costs ~0.5 s per 1M-row lexsort);
+# small arrays and CPU-only runs keep numpy
+# --------------------------------------------------------------------------
+_DEV_ROWS = 1 << 16
+
+
+def _on_gpu(n: int) -> bool:
+    if n < _DEV_ROWS:
+        return False
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except ImportError:  # pragma: no cover
+        return False
+
+
+def _as_i64(k: np.ndarray):
+    """A sort key as int64 with the same order, or None (uint64 with the top bit set)."""
+    k = np.ascontiguousarray(k)
+    if k.dtype == np.uint64:
+        return None if np.any(k >> np.uint64(63)) else k.view(np.int64)
+    if k.dtype == np.bool_:
+        return k.astype(np.int64)
+    return k.astype(np.int64, copy=False)
+
+
+def _lexsort(keys) -> np.ndarray:
+    """np.lexsort(keys) (the last key is the primary one): stable LSD passes of
+    torch.argsort on the GPU for large inputs."""
+    n = len(keys[0])
+    if not _on_gpu(n):
+        return np.lexsort(keys)
+    ks = [_as_i64(k) for k in keys]
+    if any(k is None for k in ks):
+        return np.lexsort(keys)
+    import torch
+    o = None
+    for k in ks:
+        t = torch.from_numpy(k).cuda()
+        o = torch.argsort(t, stable=True) if o is None else o[torch.argsort(t[o], stable=True)]
+    return o.cpu().numpy()
+
+
+def _take(o: np.ndarray, *arrays):
+    """Row gathers a[o] for each array (GPU for large inputs)."""
+    if not _on_gpu(len(o)):
+        return tuple(a[o] for a in arrays)
+    import torch
+    ot = torch.from_numpy(np.ascontiguousarray(o, np.int64)).cuda()
+    out = []
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        raw = a.dtype == np.uint64
+        t = torch.from_numpy(a.view(np.int64) if raw else a).cuda()
+        r = t[ot].cpu().numpy()
+        out.append(r.view(np.uint64) if raw else r)
+    return tuple(out)
+
+
 def _key16(lvl, p1, p2) -> np.ndarray:
     """Sortable bytes of (level, prefix) for vectorised searches (big endian)."""
     a = np.empty(len(lvl), dtype=[("l", ">u2"), ("a", ">u8"), ("b", ">u8")])
@@ -206,6 +267,16 @@ class DeviceBackend:
 
     def __init__(self):
         self.last = {}
+        self._local = None  # BucketTree reused across steps (its device buffers stay allocated)
+        self._h = None  # handle of the assembled tree, reused across steps
+
+    def __del__(self):
+        try:
+            if self._h is not None:
+                from . import _lib as L
+                L.load().gc_bh_destroy(self._h)
+        except Exception:
+            pass
 
     def keys(self, pos, box):
         from . import _lib as L
@@ -221,10 +292,13 @@ class DeviceBackend:
         from . import nbody
         from .generators import ParticleSet
         ps = ParticleSet(pos, mass, np.zeros_like(pos), box)
-        t = nbody.BucketTree(ps, bucket, forced=forced)
+        t = self._local
+        if t is None or t.bucket_size != int(bucket):
+            t = self._local = nbody.BucketTree(ps, bucket, forced=forced)
+        else:
+            t.reset(ps, forced)
         a = dict(t._load())
         a["buckets"] = np.asarray(t.bucket_ids)
-        self._keep_local = t
         return a
 
     def step(self, tree: dict, own: tuple, theta: float, g: float, eps: float, want_lists: bool):
@@ -232,52 +306,52 @@ class DeviceBackend:
         tree; returns (forces of every particle row, lists CSR or None)."""
         from . import _lib as L
         ctx = L.context()
-        h = C.c_void_p()
-        L.call("gc_bh_create", ctx.handle, C.byref(h))
-        try:
-            n = len(tree["pmass"])
-            nn = len(tree["half"])
-            dim = tree["center"].shape[1]
-            cuts = np.array(own, np.int64)
-            ar = {k: np.ascontiguousarray(v) for k, v in tree.items()}
-            L.call("gc_bh_set_tree", h, nn, dim, float(tree["box"]), int(tree["bucket"]),
-                   L.ptr(L.f64(ar["center"]), L.f64p), L.ptr(L.f64(ar["half"]), L.f64p),
-                   L.ptr(L.f64(ar["mass"]), L.f64p), L.ptr(L.f64(ar["com"]), L.f64p),
-                   L.ptr(L.i64(ar["first_child"]), L.i64p), L.ptr(np.ascontiguousarray(ar["n_child"], np.int32),
-                                                                   L.i32p),
-                   L.ptr(L.i64(ar["pstart"]), L.i64p), L.ptr(L.i64(ar["pcount"]), L.i64p),
-                   len(ar["buckets"]), L.ptr(L.i64(ar["buckets"]), L.i64p), n, L.ptr(L.i64(ar["order"]), L.i64p),
-                   L.ptr(L.f64(ar["pos"]), L.f64p), L.ptr(L.f64(ar["pmass"]), L.f64p), len(cuts),
-                   L.ptr(cuts, L.i64p))
-            ng = np.zeros(1, np.int64)
-            L.call("gc_bh_groups", h, L.ptr(ng, L.i64p), None)
-            wfb = np.zeros(int(ng[0]) + 1, np.int64)
-            L.call("gc_bh_groups", h, L.ptr(ng, L.i64p), L.ptr(wfb, L.i64p))
-            g0, g1 = int(np.searchsorted(wfb, own[0])), int(np.searchsorted(wfb, own[1]))
-            assert wfb[g0] == own[0] and wfb[g1] == own[1], "own buckets must form whole walk groups"
-            L.call("gc_bh_set_range", h, g0, g1)
-            L.call("gc_bh_walk", h, float(theta))  # stats walk (sizes the union pool for this tree)
-            L.call("gc_bh_walk", h, float(theta))
-            L.call("gc_bh_forces_async", h, float(g), float(eps))
-            tm = np.zeros(3)
-            L.call("gc_bh_timings", h, L.ptr(tm, L.f64p))
-            f = np.zeros((n, dim))
-            L.call("gc_bh_get_forces", h, L.ptr(f, L.f64p))
-            cnt = np.zeros(1, np.int64)
-            L.call("gc_bh_interactions", h, L.ptr(cnt, L.i64p))
-            self.last = dict(walk_ms=float(tm[0]), force_ms=float(tm[1]), interactions=int(cnt[0]))
-            lists = None
-            if want_lists:
-                nb = len(ar["buckets"])
-                ptr, ic = np.zeros(nb + 1, np.int64), np.zeros(nb, np.int64)
-                L.call("gc_bh_get_lists", h, L.ptr(ptr, L.i64p), None, None, L.ptr(ic, L.i64p))
-                ids, kind = np.zeros(int(ptr[-1]), np.int64), np.zeros(int(ptr[-1]), np.int8)
-                L.call("gc_bh_get_lists", h, L.ptr(ptr, L.i64p), L.ptr(ids, L.i64p), L.ptr(kind, L.i8p),
-                       L.ptr(ic, L.i64p))
-                lists = (ptr, ids, kind, ic)
-            return f, lists
-        finally:
-            L.load().gc_bh_destroy(h)
+        if self._h is None:
+            self._h = C.c_void_p()
+            L.call("gc_bh_create", ctx.handle, C.byref(self._h))
+        h = self._h
+        # the handle is kept across steps: gc_bh_set_tree resets every per-tree state
+        n = len(tree["pmass"])
+        nn = len(tree["half"])
+        dim = tree["center"].shape[1]
+        cuts = np.array(own, np.int64)
+        ar = {k: np.ascontiguousarray(v) for k, v in tree.items()}
+        L.call("gc_bh_set_tree", h, nn, dim, float(tree["box"]), int(tree["bucket"]),
+               L.ptr(L.f64(ar["center"]), L.f64p), L.ptr(L.f64(ar["half"]), L.f64p),
+               L.ptr(L.f64(ar["mass"]), L.f64p), L.ptr(L.f64(ar["com"]), L.f64p),
+               L.ptr(L.i64(ar["first_child"]), L.i64p), L.ptr(np.ascontiguousarray(ar["n_child"], np.int32),
+                                                               L.i32p),
+               L.ptr(L.i64(ar["pstart"]), L.i64p), L.ptr(L.i64(ar["pcount"]), L.i64p),
+               len(ar["buckets"]), L.ptr(L.i64(ar["buckets"]), L.i64p), n, L.ptr(L.i64(ar["order"]), L.i64p),
+               L.ptr(L.f64(ar["pos"]), L.f64p), L.ptr(L.f64(ar["pmass"]), L.f64p), len(cuts),
+               L.ptr(cuts, L.i64p))
+        ng = np.zeros(1, np.int64)
+        L.call("gc_bh_groups", h, L.ptr(ng, L.i64p), None)
+        wfb = np.zeros(int(ng[0]) + 1, np.int64)
+        L.call("gc_bh_groups", h, L.ptr(ng, L.i64p), L.ptr(wfb, L.i64p))
+        g0, g1 = int(np.searchsorted(wfb, own[0])), int(np.searchsorted(wfb, own[1]))
+        assert wfb[g0] == own[0] and wfb[g1] == own[1], "own buckets must form whole walk groups"
+        L.call("gc_bh_set_range", h, g0, g1)
+        L.call("gc_bh_walk", h, float(theta))  # stats walk (sizes the union pool for this tree)
+        L.call("gc_bh_walk", h, float(theta))
+        L.call("gc_bh_forces_async", h, float(g), float(eps))
+        tm = np.zeros(3)
+        L.call("gc_bh_timings", h, L.ptr(tm, L.f64p))
+        f = np.zeros((n, dim))
+        L.call("gc_bh_get_forces", h, L.ptr(f, L.f64p))
+        cnt = np.zeros(1, np.int64)
+        L.call("gc_bh_interactions", h, L.ptr(cnt, L.i64p))
+        self.last = dict(walk_ms=float(tm[0]), force_ms=float(tm[1]), interactions=int(cnt[0]))
+        lists = None
+        if want_lists:
+            nb = len(ar["buckets"])
+            ptr, ic = np.zeros(nb + 1, np.int64), np.zeros(nb, np.int64)
+            L.call("gc_bh_get_lists", h, L.ptr(ptr, L.i64p), None, None, L.ptr(ic, L.i64p))
+            ids, kind = np.zeros(int(ptr[-1]), np.int64), np.zeros(int(ptr[-1]), np.int8)
+            L.call("gc_bh_get_lists", h, L.ptr(ptr, L.i64p), L.ptr(ids, L.i64p), L.ptr(kind, L.i8p),
+                   L.ptr(ic, L.i64p))
+            lists = (ptr, ids, kind, ic)
+        return f, lists
 
 
 # --------------------------------------------------------------------------
@@ -357,8 +431,8 @@ class DistBH:
         cm, box = self.comm, self.box
         nlev = n_levels(box)
         k1, k2 = self.backend.keys(pos, box)
-        o = np.lexsort((gid, k2, k1))
-        pos, mass, gid, k1, k2 = pos[o], mass[o], gid[o], k1[o], k2[o]
+        o = _lexsort((gid, k2, k1))
+        pos, mass, gid, k1, k2 = _take(o, pos, mass, gid, k1, k2)
         # splitters: world - 1 quantiles of an all-gathered sample of (key, gid)
         n = len(gid)
         take = np.unique(np.linspace(0, max(n - 1, 0), min(n, self.sample)).astype(np.int64)) if n else np.zeros(0, int)
@@ -383,8 +457,8 @@ class DistBH:
             recv_k2 = cm.alltoallv([k2[cut[r]:cut[r + 1]] for r in range(cm.world)])
             pos, mass, gid = np.concatenate(recv_pos), np.concatenate(recv_m), np.concatenate(recv_g)
             k1, k2 = np.concatenate(recv_k1), np.concatenate(recv_k2)
-            o = np.lexsort((gid, k2, k1))
-            pos, mass, gid, k1, k2 = pos[o], mass[o], gid[o], k1[o], k2[o]
+            o = _lexsort((gid, k2, k1))
+            pos, mass, gid, k1, k2 = _take(o, pos, mass, gid, k1, k2)
             # boundaries between consecutive non-empty ranks
             ends = np.array([[len(gid), _join(k1[0], k2[0]) >> 63 if len(gid) else 0,
                               _join(k1[0], k2[0]) & _M63 if len(gid) else 0,
@@ -444,8 +518,8 @@ class DistBH:
         # local ids in ascending global id: buckets keep ascending particle_idx
         # (nbody.py:110), so sums over a bucket's particles run in the
         # single-process order
-        o = np.argsort(gid, kind="stable")
-        pos, mass, gid = pos[o], mass[o], gid[o]
+        o = _lexsort((gid,))
+        pos, mass, gid = _take(o, pos, mass, gid)
         forced = (np.array([L for L, _ in scubes], np.int32),
                   np.array([[P >> 63, P & _M63] for _, P in scubes], np.uint64).reshape(-1, 2))
         # ---- 3: own subtrees ------------------------------------------------
@@ -587,8 +661,11 @@ class DistBH:
         rows[:, 8:8 + dim] = t["center"][idx]
         rows[:, 8 + dim:] = t["com"][idx]
         bsel = idx[kind == 2]
-        if len(bsel):
-            pid = np.concatenate([t["pidx"][t["pstart"][b]: t["pstart"][b] + t["pcount"][b]] for b in bsel])
+        if len(bsel):  # the opened buckets' particle ranges, concatenated in bucket order
+            st = t["pstart"][bsel].astype(np.int64)
+            cnt = t["pcount"][bsel].astype(np.int64)
+            rel = np.arange(int(cnt.sum())) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+            pid = t["pidx"][np.repeat(st, cnt) + rel]
         else:
             pid = np.zeros(0, np.int64)
         parts = np.zeros((len(pid), dim + 2))
@@ -657,14 +734,14 @@ class DistBH:
         center = np.concatenate(C_).reshape(-1, dim); com = np.concatenate(O_).reshape(-1, dim)
         pcount = np.concatenate(PC_); src = np.concatenate(SRC_)
         # dedupe (level, prefix): a received node overrides a branch summary (kind 3)
-        o = np.lexsort((kind == 3, pb, pa, lvl_a))
+        o = _lexsort((kind == 3, pb, pa, lvl_a))
         key = _key16(lvl_a[o], pa[o], pb[o])
         first = np.ones(len(o), bool)
         first[1:] = key[1:] != key[:-1]
         o = o[first]
         key = key[first]
-        lvl_a, pa, pb, kind, half, nmass = lvl_a[o], pa[o], pb[o], kind[o], half[o], nmass[o]
-        center, com, pcount, src = center[o], com[o], pcount[o], src[o]
+        lvl_a, pa, pb, kind, half, nmass, center, com, pcount, src = _take(
+            o, lvl_a, pa, pb, kind, half, nmass, center, com, pcount, src)
         kind[kind == 3] = 2
         nn = len(o)
         # children: nodes of level L + 1 grouped by parent prefix (contiguous, octant order)
@@ -678,10 +755,13 @@ class DistBH:
         pk = _key16(pl, pa[ci] & m1[pl], pb[ci] & m2[pl])
         par = np.searchsorted(key, pk)
         assert np.all(key[np.minimum(par, nn - 1)] == pk), "assembled tree: a node without its parent"
-        fcv = np.full(nn, np.iinfo(np.int64).max, np.int64)
-        np.minimum.at(fcv, par, ci)
-        np.add.at(n_child, par, 1)
-        first_child = np.where(n_child > 0, fcv, -1)
+        # children of one parent are contiguous in this order (level, prefix), ci ascending
+        n_child = np.bincount(par, minlength=nn).astype(np.int32)
+        first_child = np.full(nn, -1, np.int64)
+        if len(ci):
+            head = np.ones(len(ci), bool)
+            head[1:] = par[1:] != par[:-1]
+            first_child[par[head]] = ci[head]
         # sealed / bucket nodes must be childless; internal nodes must have children
         assert np.all(n_child[kind != 0] == 0) and np.all(n_child[kind == 0] > 0), "assembled tree: bad node kinds"
         # particles: own, received, one poison row per sealed node (every row
@@ -694,7 +774,7 @@ class DistBH:
         poison = len(pmass) - nseal
         # buckets (kinds 1, 2) in DFS order = order of their left-aligned prefixes
         leaf = np.nonzero(kind != 0)[0]
-        leaf = leaf[np.lexsort((pb[leaf], pa[leaf]))]
+        leaf = leaf[_lexsort((pb[leaf], pa[leaf]))]
         own_leaf = (kind[leaf] == 1) & (src[leaf, 0] == 0)
         ol = np.nonzero(own_leaf)[0]
         own_lo, own_hi = (int(ol[0]), int(ol[-1]) + 1) if len(ol) else (None, None)

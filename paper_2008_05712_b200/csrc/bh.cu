@@ -909,8 +909,13 @@ gc_status gc_bh_set_forced_splits(gc_bh *bh, int64_t n, const int32_t *level, co
             kv[i] = make_ulonglong2(v[i].second.first, v[i].second.second);
         }
         bh->n_forced = (int)v.size();
-        bh->d_forced_lvl.upload(lv.data(), std::max<size_t>(1, lv.size()), bh->ctx->stream);
-        bh->d_forced_key.upload(kv.data(), std::max<size_t>(1, kv.size()), bh->ctx->stream);
+        if (v.empty()) {  // cleared: the build takes the bottom-up path again
+            bh->d_forced_lvl.resize(1);
+            bh->d_forced_key.resize(1);
+            return;
+        }
+        bh->d_forced_lvl.upload(lv.data(), lv.size(), bh->ctx->stream);
+        bh->d_forced_key.upload(kv.data(), kv.size(), bh->ctx->stream);
         GC_CUDA(cudaStreamSynchronize(bh->ctx->stream));
     });
 }

@@ -80,15 +80,29 @@ class BucketTree:
         self._ctx = L.context()
         self.handle = C.c_void_p()
         L.call("gc_bh_create", self._ctx.handle, C.byref(self.handle))
+        self._gen = 0  # bumps when the handle's list state changes
+        self._set(ps, forced, clear_forced=False)
+
+    def _set(self, ps: ParticleSet, forced, clear_forced: bool):
         if forced is not None and len(forced[0]):
             fl = np.ascontiguousarray(forced[0], np.int32)
             fp = np.ascontiguousarray(forced[1], np.uint64).reshape(-1)
             L.call("gc_bh_set_forced_splits", self.handle, len(fl), L.ptr(fl, L.i32p), L.ptr(fp, L.u64p))
+        elif clear_forced:
+            L.call("gc_bh_set_forced_splits", self.handle, 0, None, None)
         pos, m = L.f64(ps.positions), L.f64(ps.masses)
         L.call("gc_bh_set_particles", self.handle, self.n, self.dim, L.ptr(pos, L.f64p), L.ptr(m, L.f64p),
                float(ps.box), self.bucket_size)
-        self._gen = 0  # bumps when the handle's list state changes
         self._arrays = None
+
+    def reset(self, ps: ParticleSet, forced=None):
+        """Rebuild the tree of a new particle set on the same device handle
+        (buffers kept: no per-step allocation)."""
+        self.ps = ps
+        self.dim = ps.positions.shape[1]
+        self.n = ps.positions.shape[0]
+        self._gen += 1
+        self._set(ps, forced, clear_forced=True)
 
     def __del__(self):
         try:

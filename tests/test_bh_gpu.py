@@ -256,6 +256,22 @@ def test_device_build_edge_cases(nb, case, bucket):
         np.testing.assert_array_equal(a.particle_idx(int(b)), o.particle_idx(int(b)))
 
 
+def test_bucket_tree_reset_equals_fresh_build(nb):
+    """BucketTree.reset (the distributed backend's per-step rebuild on one
+    handle) gives the fresh build's tree for a new set, also after a build
+    with forced splits (they are cleared)."""
+    from paper_2008_05712_b200 import generators as gen
+    a = gen.fp32_exact(gen.gen_particles(60_000, 1, clustering=0.6, dim=3))
+    b = gen.fp32_exact(gen.gen_particles(45_000, 2, clustering=0.3, dim=3))
+    forced = (np.array([1, 2], np.int32), np.array([[0, 0], [0, 0]], np.uint64))
+    t = nb.BucketTree(a, 8, forced=forced)
+    t.reset(b)
+    f = nb.build_bucket_tree(b, 8)
+    for k in ("center", "half", "mass", "com", "first_child", "n_child", "pcount", "pidx"):
+        np.testing.assert_array_equal(getattr(t, k), getattr(f, k), err_msg=k)
+    np.testing.assert_array_equal(t.bucket_ids, f.bucket_ids)
+
+
 @pytest.mark.parametrize("bucket,eps,n", [(32, 0.0, 20_000), (1, 1e-4, 5_000), (8, 0.0, 3)])
 def test_fused_ring_edge_cases(bucket, eps, n):
     """Opened buckets of 32 particles (33 records from one union entry: the
