@@ -1044,16 +1044,14 @@ __global__ void md_scatter_kernel(int n, const int *__restrict__ cell_start, con
     perm[cell_start[c] + atomicSub(&count[c], 1) - 1] = i;  // counts end at zero
 }
 
-// warp per cell: rank sort of the cell's atoms by global id (deterministic
-// order for any atomic scatter order, the same order on every slab) fused
-// with the gather: spos = (x, y, z, global id bits), sidx = local index
-__global__ void md_sortgather_kernel(int ncell, const int *__restrict__ cell_start, int *__restrict__ perm,
-                                     const double4 *__restrict__ pos, const long long *__restrict__ gid,
-                                     double4 *__restrict__ spos, int *__restrict__ sidx, int *__restrict__ scell)
+// Rank sort of a cell's atoms by global id (deterministic order for any
+// atomic scatter order, the same order on every slab) fused with the gather:
+// spos = (x, y, z, global id bits), sidx = local index.  Whole warp per cell.
+__device__ __forceinline__ void md_sortgather_cell(int c, int lane, const int *__restrict__ cell_start,
+                                                   int *__restrict__ perm, const double4 *__restrict__ pos,
+                                                   const long long *__restrict__ gid, double4 *__restrict__ spos,
+                                                   int *__restrict__ sidx, int *__restrict__ scell)
 {
-    const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (c >= ncell) return;
     const int s = cell_start[c], n = cell_start[c + 1] - s;
     if (n > 32) {  // rare: serial insertion sort by global id, then gather
         if (lane == 0)
@@ -1076,6 +1074,7 @@ __global__ void md_sortgather_kernel(int ncell, const int *__restrict__ cell_sta
             sidx[s + k] = i;
             scell[s + k] = c;
         }
+        __syncwarp();
         return;
     }
     const int v = lane < n ? perm[s + lane] : -1;
@@ -1085,6 +1084,44 @@ __global__ void md_sortgather_kernel(int ncell, const int *__restrict__ cell_sta
     for (int k = 0; k < n; ++k) rank += __shfl_sync(0xffffffffu, g32, k) < g32;
     __syncwarp();
     if (lane < n) {
+        perm[s + rank] = v;
+        double4 p = pos[v];
+        p.w = __longlong_as_double(g);
+        spos[s + rank] = p;
+        sidx[s + rank] = v;
+        scell[s + rank] = c;
+    }
+    __syncwarp();
+}
+
+// two cells per warp: half-warp rank sorts when both hold <= 16 atoms (the
+// common case at ~13.5 atoms per cell), else the whole warp per cell
+__global__ void md_sortgather_kernel(int ncell, const int *__restrict__ cell_start, int *__restrict__ perm,
+                                     const double4 *__restrict__ pos, const long long *__restrict__ gid,
+                                     double4 *__restrict__ spos, int *__restrict__ sidx, int *__restrict__ scell)
+{
+    const int c0 = 2 * (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+    const int lane = threadIdx.x & 31;
+    if (c0 >= ncell) return;
+    const bool two = c0 + 1 < ncell;
+    const int s0 = cell_start[c0], n0 = cell_start[c0 + 1] - s0;
+    const int s1 = two ? cell_start[c0 + 1] : 0, n1 = two ? cell_start[c0 + 2] - s1 : 0;
+    if (n0 > 16 || n1 > 16) {
+        md_sortgather_cell(c0, lane, cell_start, perm, pos, gid, spos, sidx, scell);
+        if (two) md_sortgather_cell(c0 + 1, lane, cell_start, perm, pos, gid, spos, sidx, scell);
+        return;
+    }
+    const int h = lane >> 4, l = lane & 15;
+    const int c = c0 + h, s = h ? s1 : s0, n = h ? n1 : n0;
+    const bool on = l < n;
+    const int v = on ? perm[s + l] : -1;
+    const long long g = on ? gid[v] : LLONG_MAX;
+    const int g32 = on ? (int)g : INT_MAX;
+    const int nm = max(n0, n1);
+    int rank = 0;
+    for (int k = 0; k < nm; ++k) rank += __shfl_sync(0xffffffffu, g32, k, 16) < g32;  // own half's lane k
+    __syncwarp();
+    if (on) {
         perm[s + rank] = v;
         double4 p = pos[v];
         p.w = __longlong_as_double(g);
@@ -1380,7 +1417,7 @@ void md_sort_counted(gc_md *md)
     GC_CUDA(cub::DeviceScan::ExclusiveSum(md->ctx->scratch.p, bytes, md->count.p, md->cell_start.p, nc + 1, s));
     md_scatter_kernel<<<grid_for(n, MD_TPB), MD_TPB, 0, s>>>(n, md->cell_start.p, md->cell_of.p, md->count.p,
                                                              md->perm.p);
-    md_sortgather_kernel<<<grid_for(nc, MD_TPB / 32), MD_TPB, 0, s>>>(nc, md->cell_start.p, md->perm.p, md->pos.p,
+    md_sortgather_kernel<<<grid_for((nc + 1) / 2, MD_TPB / 32), MD_TPB, 0, s>>>(nc, md->cell_start.p, md->perm.p, md->pos.p,
                                                                       md->gid.p, md->spos.p, md->sidx.p, md->scell.p);
     check_launch("md sort");
 }
@@ -1928,7 +1965,7 @@ void mdv_sort(gc_md *md)
     GC_CUDA(cub::DeviceScan::ExclusiveSum(md->ctx->scratch.p, bytes, md->count.p, md->cell_start.p, nc + 1, s));
     mdv_scatter_kernel<<<grid_for(cap, MD_TPB), MD_TPB, 0, s>>>(md->dn.p, md->cell_start.p, md->cell_of.p,
                                                                 md->count.p, md->perm.p);
-    md_sortgather_kernel<<<grid_for(nc, MD_TPB / 32), MD_TPB, 0, s>>>(nc, md->cell_start.p, md->perm.p, md->pos.p,
+    md_sortgather_kernel<<<grid_for((nc + 1) / 2, MD_TPB / 32), MD_TPB, 0, s>>>(nc, md->cell_start.p, md->perm.p, md->pos.p,
                                                                       md->gid.p, md->spos.p, md->sidx.p, md->scell.p);
     check_launch("mdv sort");
 }
