@@ -717,8 +717,9 @@ def bench_periodic(args):
             "interactions": inter, "walk_ms": statistics.median(w), "force_ms": statistics.median(f),
             "ms_per_step": ms, "value": inter / (ms * 1e-3), "unit": "interactions/s",
             "force_tflops": FLOPS_PER_INTERACTION * inter / (statistics.median(f) * 1e-3) / 1e12,
-            "parity": "tests/test_bh_gpu.py::test_periodic_walk_matches_oracle (per-bucket counts over all images "
-                      "bit-exact, forces <= 1e-5 vs orc_periodic_forces); UNPINNED: the reference only models the "
+            "parity": "tests/test_bh_gpu.py::test_periodic_1m_bench_workload_sampled_parity (this workload, 3 x 600 "
+                      "buckets: per-bucket counts over all images bit-exact, forces <= 1e-5 vs orc_periodic_forces) "
+                      "and test_periodic_walk_matches_oracle (whole systems); UNPINNED: the reference only models the "
                       "periodic class, the restatement is pinned by known answers (test_periodic_oracle_pinned)"}
 
 

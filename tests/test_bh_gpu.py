@@ -541,6 +541,27 @@ def test_plummer16m_config4_sampled_parity(nb):
     assert ntot > 3 * 4096
 
 
+def test_periodic_1m_bench_workload_sampled_parity(nb):
+    """The bench's periodic workload at full size (configs[2] clustered 1M, 27
+    images, theta 0.7): on three 600-bucket ranges the per-bucket entry / item
+    counts over all images equal the float64 restatement bit for bit and the
+    forces of their particles are within 1e-5."""
+    from oracle import oracle as orc
+    from paper_2008_05712_b200 import generators as gen
+    ps = gen.fp32_exact(gen.gen_particles(1_000_000, 42, clustering=0.6, dim=3))
+    tree = nb.build_bucket_tree(ps, 8)
+    f, ent, itm = nb.periodic_forces(tree, 0.7, nrep=1)
+    ot = orc.build_bucket_tree(ps.positions, ps.masses, 8)
+    nbk = len(ot.buckets)
+    for b0 in (0, nbk // 2, nbk - 600):
+        b1 = b0 + 600
+        fo, eo, io = orc.periodic_forces(ot, ps.positions, ps.masses, 0.7, 1.0, 1, bucket_range=(b0, b1))
+        np.testing.assert_array_equal(ent[b0:b1], eo[b0:b1])
+        np.testing.assert_array_equal(itm[b0:b1], io[b0:b1])
+        pidx = np.concatenate([ot.particle_idx(int(b)) for b in ot.buckets[b0:b1]])
+        assert rel_err(f[pidx], fo[pidx]).max() <= FORCE_RTOL
+
+
 @pytest.mark.parametrize("n,seed,cl,nrep", [(20_000, 5, 0.6, 1), (4096, 9, None, 1), (3000, 2, 0.0, 1), (3000, 2, 0.0, 0)])
 def test_periodic_walk_matches_oracle(nb, n, seed, cl, nrep):
     """Periodic BH (no reference implementation -- the float64
