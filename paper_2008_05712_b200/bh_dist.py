@@ -128,6 +128,13 @@ def _on_gpu(n: int) -> bool:
         return False
 
 
+def _gpu():
+    """The library context's device (the rank's GPU), as a torch device."""
+    import torch
+    from . import _lib as L
+    return torch.device("cuda", L.context().device % torch.cuda.device_count())
+
+
 def _as_i64(k: np.ndarray):
     """A sort key as int64 with the same order, or None (uint64 with the top bit set)."""
     k = np.ascontiguousarray(k)
@@ -148,9 +155,10 @@ def _lexsort(keys) -> np.ndarray:
     if any(k is None for k in ks):
         return np.lexsort(keys)
     import torch
+    dev = _gpu()
     o = None
     for k in ks:
-        t = torch.from_numpy(k).cuda()
+        t = torch.from_numpy(k).to(dev)
         o = torch.argsort(t, stable=True) if o is None else o[torch.argsort(t[o], stable=True)]
     return o.cpu().numpy()
 
@@ -160,12 +168,13 @@ def _take(o: np.ndarray, *arrays):
     if not _on_gpu(len(o)):
         return tuple(a[o] for a in arrays)
     import torch
-    ot = torch.from_numpy(np.ascontiguousarray(o, np.int64)).cuda()
+    dev = _gpu()
+    ot = torch.from_numpy(np.ascontiguousarray(o, np.int64)).to(dev)
     out = []
     for a in arrays:
         a = np.ascontiguousarray(a)
         raw = a.dtype == np.uint64
-        t = torch.from_numpy(a.view(np.int64) if raw else a).cuda()
+        t = torch.from_numpy(a.view(np.int64) if raw else a).to(dev)
         r = t[ot].cpu().numpy()
         out.append(r.view(np.uint64) if raw else r)
     return tuple(out)

@@ -1149,12 +1149,10 @@ void device_build_tree(gc_bh *bh, const double *pos_h, const double *mass_h, int
             const double4 root = make_double4(box / 2.0, dim > 1 ? box / 2.0 : 0.0, dim > 2 ? box / 2.0 : 0.0, box / 2.0);
             GC_CUDA(cudaMemcpyAsync(lcenter.p, &root, sizeof(double4), cudaMemcpyHostToDevice, s));
         }
-        static int coop_blocks = 0;  // co-resident grid of the cooperative level kernel
-        if (!coop_blocks) {
-            int per_sm = 0;
-            GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bb_levels_coop, BB_TPB, 0));
-            coop_blocks = std::max(1, std::min(per_sm, 1)) * ctx->prop.multiProcessorCount;
-        }
+        // co-resident grid of the cooperative level kernel (this context's device)
+        int per_sm = 0;
+        GC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bb_levels_coop, BB_TPB, 0));
+        const int coop_blocks = std::max(1, std::min(per_sm, 1)) * ctx->prop.multiProcessorCount;
         auto &bsum = bh->ws.bsum;
         auto &lvlf = bh->ws.lvlf;
         bsum.resize(coop_blocks);

@@ -1456,11 +1456,8 @@ void md_cell_launch(gc_md *md, bool integ, double dt)
             const float bandc = (float)(md->P.c2 + 1e-5 * extc * extc + 1e-6);
             const int ncz = (md->P.nz + MDK_KZ - 1) / MDK_KZ;
             const int cols = (md->P.slab ? md->P.nx - 2 : md->P.nx) * md->P.ny * ncz;
-            static bool attr = false;
-            if (!attr) {
-                GC_CUDA(cudaFuncSetAttribute(md_lj3c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MDK_SMEM));
-                attr = true;
-            }
+            // per device (cheap): a process may drive several GPUs
+            GC_CUDA(cudaFuncSetAttribute(md_lj3c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MDK_SMEM));
             md_lj3c_kernel<<<cols, MDK_THREADS, MDK_SMEM, s>>>(md->spos.p, md->sidx.p, md->cell_start.p, md->P, bandc, ncz,
                                                         md->force.p, nullptr);
             check_launch("md_lj3c_kernel");
@@ -1908,11 +1905,7 @@ gc_status gc_md_forces_columns(gc_md *md, const int32_t *cols, int64_t n)
         if (n == 0) return;
         const double extc = (MDK_KZ + 2) * md->P.cell;
         const float bandc = (float)(md->P.c2 + 1e-5 * extc * extc + 1e-6);
-        static bool attr = false;
-        if (!attr) {
-            GC_CUDA(cudaFuncSetAttribute(md_lj3c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MDK_SMEM));
-            attr = true;
-        }
+        GC_CUDA(cudaFuncSetAttribute(md_lj3c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MDK_SMEM));
         md_lj3c_kernel<<<(unsigned)n, MDK_THREADS, MDK_SMEM, md->ctx->stream>>>(
             md->spos.p, md->sidx.p, md->cell_start.p, md->P, bandc, (int)c[2], md->force.p, cols);
         check_launch("md_lj3c_kernel (columns)");
