@@ -427,13 +427,36 @@ class DistBH:
     ``comm`` (configs[3]); the reference API's parameters (bucket_size,
     theta, g, eps: hr/workloads/nbody.py:23, 216)."""
 
-    def __init__(self, comm, bucket_size=8, theta=0.7, g=1.0, eps=1e-4, box=1.0, backend=None, sample=256):
+    def __init__(self, comm, bucket_size=8, theta=0.7, g=1.0, eps=1e-4, box=1.0, backend=None, sample=256,
+                 shares=None, balance=True):
+        """shares: fixed particle shares per rank (default: equal, then --
+        with balance -- the measured speeds of the previous steps).  The
+        reference's adaptive CPU/GPU split (hr/scheduler.py, scheduler.KWayEstimate)
+        over the ranks: each step's device walk + force time per own particle
+        is all-gathered, and the next partition cuts the key order at the
+        speed-proportional cumulative shares.  Lists and forces do not depend
+        on where the boundaries fall."""
+        from . import scheduler as sch
         self.comm = comm
         self.bucket = int(bucket_size)
         self.theta, self.g, self.eps, self.box = float(theta), float(g), float(eps), float(box)
         self.backend = backend or DeviceBackend()
         self.sample = sample
         self.stats = {}
+        self.fixed_shares = None if shares is None else [float(x) for x in shares]
+        if self.fixed_shares is not None and (len(self.fixed_shares) != comm.world or
+                                              abs(sum(self.fixed_shares) - 1.0) > 1e-9 or
+                                              min(self.fixed_shares) <= 0.0):
+            raise ValueError("shares: one positive share per rank, summing to 1")
+        self.balance = sch.KWayEstimate(comm.world) if balance else None
+
+    def shares(self):
+        """Particle shares of the next partition."""
+        if self.fixed_shares is not None:
+            return list(self.fixed_shares)
+        if self.balance is not None:
+            return self.balance.shares()
+        return [1.0 / self.comm.world] * self.comm.world
 
     # ---- 1 + 2: keys, sample sort, straddling cubes ----------------------------
     def _partition(self, pos, mass, gid):
@@ -449,8 +472,12 @@ class DistBH:
         allsmp = np.concatenate(cm.allgather(smp))
         allsmp = allsmp[np.lexsort((allsmp[:, 2], allsmp[:, 1].view(np.uint64), allsmp[:, 0].view(np.uint64)))]
         splitters = []
+        shares = self.shares()
+        equal = all(abs(x - 1.0 / cm.world) < 1e-12 for x in shares)
+        cum = np.cumsum(shares)
         for r in range(1, cm.world):
-            j = (r * len(allsmp)) // cm.world
+            # the sample quantile at the cumulative share of ranks < r
+            j = (r * len(allsmp)) // cm.world if equal else int(cum[r - 1] * len(allsmp))
             s = allsmp[min(j, len(allsmp) - 1)]
             splitters.append((_join(np.uint64(s[0]), np.uint64(s[1])), int(s[2])))
         for it in range(64):
@@ -602,7 +629,21 @@ class DistBH:
         lap("assemble")
         f, lists = self.backend.step(tree, own, self.theta, self.g, self.eps, want_lists)
         lap("device_step")
+        self._record_speed(n)
         return DistResult(gid=gid, forces=f[:n], tree=tree, own=own, lists=lists, stats=dict(self.stats))
+
+    def _record_speed(self, n_own: int):
+        """All-gather this step's device walk + force time per own particle
+        into the balancer (every rank records the same samples)."""
+        last = getattr(self.backend, "last", None) or {}
+        if self.balance is None or "walk_ms" not in last:
+            return
+        ms = float(last["walk_ms"]) + float(last["force_ms"])
+        rows = self.comm.allgather(np.array([[ms, float(n_own)]]))
+        for r, row in enumerate(rows):
+            if len(row) and row[0, 0] > 0.0 and row[0, 1] >= 1.0:
+                self.balance.record(r, int(row[0, 1]), float(row[0, 0]))
+        self.stats["shares_next"] = [round(x, 4) for x in self.balance.shares()]
 
     def _top_nodes(self, scubes, allbr, dim):
         """Straddling nodes with the reference's mass / COM sums over children in octant order."""

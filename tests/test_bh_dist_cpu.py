@@ -27,7 +27,7 @@ def _problem(n, seed, cl):
     return gen.fp32_exact(gen.gen_particles(n, seed, clustering=cl, dim=3))
 
 
-def _worker(rank, world, port, q, n, seed, cl, theta):
+def _worker(rank, world, port, q, n, seed, cl, theta, shares=None):
     import torch.distributed as dist
     from oracle import oracle as orc
     from oracle.dist_backend import OracleBackend
@@ -37,7 +37,7 @@ def _worker(rank, world, port, q, n, seed, cl, theta):
     try:
         ps = _problem(n, seed, cl)
         mine = np.arange(rank, n, world)  # an arbitrary initial share
-        d = bh_dist.DistBH(bh_dist.Comm(), bucket_size=8, theta=theta, backend=OracleBackend())
+        d = bh_dist.DistBH(bh_dist.Comm(), bucket_size=8, theta=theta, backend=OracleBackend(), shares=shares)
         res = d.step(ps.positions[mine], ps.masses[mine], mine, want_lists=True)
         # the single-process reference tree and lists
         gt = orc.build_bucket_tree(ps.positions, ps.masses, 8)
@@ -83,6 +83,40 @@ def test_dist_bh_lists_and_forces_match_single_process(world, n, seed, cl, theta
         assert lists_eq, f"rank {rank}: lists differ from the single-process tree"
         assert forces_eq, f"rank {rank}: forces differ"
         assert stats["let_nodes_received"] > 0
+
+
+def test_dist_bh_uneven_shares_move_the_boundary_not_the_results():
+    """The balancer's shares (hr/scheduler.py's adaptive split over the
+    ranks, scheduler.KWayEstimate) only move the partition: with shares
+    0.3 / 0.7 rank 0 owns ~30 % of the particles and every list and float64
+    force still equals the single-process reference."""
+    world, n = 2, 6000
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q, n, 3, 0.6, 0.7, [0.3, 0.7])) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert sum(o[4] for o in out) == n
+    assert 0.2 * n < out[0][4] < 0.4 * n, [o[4] for o in out]
+    for rank, contig, lists_eq, forces_eq, nloc, stats in out:
+        assert contig and lists_eq and forces_eq, rank
+
+
+def test_balancer_shares_follow_speed():
+    """KWayEstimate as the distributed step feeds it: equal shares until every
+    rank reported, then shares proportional to particles per millisecond."""
+    from paper_2008_05712_b200 import scheduler as sch
+    b = sch.KWayEstimate(2)
+    assert b.shares() == [0.5, 0.5]
+    b.record(0, 1000, 2.0)  # 500 particles / ms
+    assert b.shares() == [0.5, 0.5]
+    b.record(1, 1000, 1.0)  # 1000 particles / ms
+    assert np.allclose(b.shares(), [1 / 3, 2 / 3])
 
 
 def test_key_restatement_orders_like_the_tree():

@@ -1,4 +1,4 @@
 #!/bin/bash
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-nproc > gpurun_out/prof_dist.log
-for i in 1 2; do timeout 900 python tools/prof_dist.py 2000000 2>&1 | head -1 >> gpurun_out/prof_dist.log; done
+timeout 900 python -m pytest tests/test_bh_dist_gpu.py -q -p no:cacheprovider -m gpu > gpurun_out/r2o_tests.log 2>&1; echo "rc=$?" >> gpurun_out/r2o_tests.log
+GCHARM_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 3 --warmup 3 > gpurun_out/bench2.log 2>&1; echo "bench2 rc=$?" >> gpurun_out/bench2.log
