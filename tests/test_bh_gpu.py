@@ -260,14 +260,14 @@ def test_step_handle_reuse_across_systems(nb):
     """gc_bh_step on ONE handle over systems of different size, clustering and
     box (grow-only device buffers, the sticky sorted key depth, the walk's
     scheduling hints of the previous tree): forces bit-identical to a fresh
-    handle's for every system, in both overlap modes."""
+    handle's for every system, in every overlap mode."""
     from paper_2008_05712_b200 import _lib as L
     from paper_2008_05712_b200 import generators as gen
     systems = [gen.fp32_exact(gen.gen_plummer(40_000, 3)),  # deep core: the sort depth grows
                gen.fp32_exact(gen.gen_particles(120_000, 4, clustering=0.6, dim=3)),
                gen.fp32_exact(gen.gen_particles(7_000, 5, clustering=0.0, dim=3)),
                gen.fp32_exact(gen.gen_particles(90_000, 6, clustering=0.8, dim=3, box=2.0))]
-    for ov in (0, 1):
+    for ov in (0, 1, 2):
         st = nb.BHStep(8, 0.7, 1.0, 1e-4)
         L.call("gc_bh_set_overlap", st.handle, ov)
         for rep in range(2):
